@@ -1,0 +1,202 @@
+/*
+ * zinpaint_b200.h -- the drop-in C ABI of the B200-native SFC multi-index hot path.
+ *
+ * The reference (`zinpaint`, /root/reference/proj) has no C ABI: its hot path sits behind
+ * C++ free functions and value types (proj/include/zinpaint/{zcurve,builder,engine}.hpp) and
+ * a pybind11 module (proj/python/bindings.cpp).  Every entry point below names the reference
+ * interface it replaces (file:line).  Plain pointers and sizes only; all buffers are HOST
+ * buffers owned by the caller; device memory is owned by the opaque handles.  No exception
+ * crosses this boundary: every call returns a zi_status and zi_last_error() explains it.
+ * The C++ mirror of the reference API (include/zinpaint_b200.hpp) rethrows the reference's
+ * exception types from these codes.
+ */
+#ifndef ZINPAINT_B200_H
+#define ZINPAINT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes; the C++ mirror maps them back to the reference's exceptions ---- */
+typedef enum {
+    ZI_OK = 0,
+    ZI_E_INVALID = 1,    /* std::invalid_argument   (proj/src/builder.cpp:38-53, zcurve.cpp:111-114) */
+    ZI_E_EMPTY_DICT = 2, /* empty_dictionary_error  (proj/include/zinpaint/builder.hpp:19-22) */
+    ZI_E_RUNTIME = 3,    /* std::runtime_error      (proj/src/engine.cpp:387-388) */
+    ZI_E_RANGE = 4,      /* std::out_of_range       (proj/src/image.cpp:12-13) */
+    ZI_E_CUDA = 5,       /* CUDA runtime failure (no reference counterpart) */
+    ZI_E_OOM = 6         /* device allocation failure */
+} zi_status;
+
+typedef enum { ZI_NORM_L2 = 0, ZI_NORM_L1 = 1 } zi_norm; /* norm_kind (types.hpp:7) */
+
+/* index_config (proj/include/zinpaint/builder.hpp:24-34); defaults 9/0.6/10/80/256/2048/L2 */
+typedef struct {
+    int32_t patch_size;
+    double coverage;
+    int32_t dims;
+    int32_t knn;
+    uint32_t mu; /* accepted and validated; the GPU search does not traverse by leaves */
+    uint32_t nu; /* accepted and validated; no CPU thread pool on the GPU path */
+    int32_t norm;
+} zi_index_config;
+
+/* inpaint_config (proj/include/zinpaint/engine.hpp:25-31) minus the index part */
+typedef struct {
+    int32_t workers; /* accepted; the GPU path has no CPU worker pool */
+    int32_t oracle;  /* run the exhaustive scan beside the index every oracle_stride iterations */
+    uint64_t oracle_stride;
+    int32_t brute_force; /* replace the index query with the exhaustive scan */
+} zi_inpaint_config;
+
+/* best_patch (proj/include/zinpaint/engine.hpp:52-58) */
+typedef struct {
+    uint32_t key; /* packed y<<16 | x (types.hpp:15-17) */
+    uint32_t cost;
+    double error;
+    uint32_t layout_id;
+    uint64_t candidates;
+} zi_best_patch;
+
+/* iteration_record (proj/include/zinpaint/engine.hpp:14-23); bf_error is NaN when absent */
+typedef struct {
+    uint64_t iteration;
+    int32_t target_x, target_y;
+    uint32_t layout_id;
+    uint32_t source_key;
+    uint32_t cost;
+    uint32_t pad_;
+    double z_error;
+    double bf_error;
+    uint64_t candidates;
+    double elapsed_seconds;
+} zi_iteration_record;
+
+/* run_stats (proj/include/zinpaint/engine.hpp:33-44); mean_ae is NaN when absent */
+typedef struct {
+    uint64_t dictionary_size;
+    double sort_seconds;
+    double build_wall_seconds;
+    double inpaint_seconds;
+    uint64_t iterations;
+    double mean_ae;
+    uint64_t ae_excluded;
+    double confidence_low;
+    double confidence_high;
+} zi_run_stats;
+
+typedef struct {
+    uint64_t n;       /* dictionary size */
+    int32_t dims;     /* effective D = min(cfg.dims, m*C, n)  (proj/src/builder.cpp:137) */
+    int32_t m;        /* pixels per layout = subset_pixel_count(K, c) */
+    int32_t channels;
+    int32_t patch_size;
+    int32_t width, height;
+    double build_seconds;      /* device time of the last build (events) */
+    double eigen_seconds;      /* host eigen-solve part of it */
+} zi_multi_index_info;
+
+typedef struct zi_ctx zi_ctx;                 /* one device + one stream + scratch */
+typedef struct zi_index zi_index;             /* zcurve_index (proj/include/zinpaint/zcurve.hpp:117-145) */
+typedef struct zi_multi_index zi_multi_index; /* multi_index (proj/include/zinpaint/builder.hpp:84-92) */
+
+const char* zi_last_error(void);
+const char* zi_version(void);
+
+/* ---- context ---- */
+zi_status zi_ctx_create(int device, zi_ctx** out);
+zi_status zi_ctx_destroy(zi_ctx* ctx);
+zi_status zi_ctx_synchronize(zi_ctx* ctx);
+/* device-side timing on the ctx stream (CUDA events), for bench.py */
+zi_status zi_timer_start(zi_ctx* ctx);
+zi_status zi_timer_stop(zi_ctx* ctx, double* ms);
+/* number of kernels this ctx has launched so far (gpu_launches evidence) */
+uint64_t zi_ctx_kernel_launches(const zi_ctx* ctx);
+/* per-kernel device time accumulated while profiling is on (name-indexed, see api.cu) */
+zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on);
+zi_status zi_ctx_profile(const zi_ctx* ctx, int slot, double* ms, uint64_t* launches,
+                         const char** name);
+
+/* ---- host utilities with reference counterparts ---- */
+int zi_less_most_significant_bit(int a, int b);                          /* morton.hpp:10-12 */
+int zi_morton_less(const uint8_t* a, const uint8_t* b, uint32_t dims);   /* morton.hpp:18-29 */
+int zi_subset_pixel_count(int patch_size, double coverage);             /* layouts.cpp:9-11 */
+/* build_subset_layouts (layouts.cpp:13-60); rc_out holds 8*m*2 int32 (row, col) */
+zi_status zi_subset_layouts(int patch_size, double coverage, int32_t* rc_out, int32_t* m_out);
+zi_status zi_index_config_validate(const zi_index_config* cfg, int channels); /* builder.cpp:38-53 */
+void zi_index_config_default(zi_index_config* cfg);
+
+/* ---- z-curve index ---- */
+/* zcurve_index::from_descriptors (zcurve.hpp:121-123, zcurve.cpp:108-138): coords n*dims
+ * row-major, keys packed y<<16|x; sorted on the device by an LSD radix sort of the Morton key */
+zi_status zi_index_from_descriptors(zi_ctx* ctx, const uint8_t* coords, const uint32_t* keys,
+                                    uint64_t n, uint32_t dims, uint32_t layout_id, zi_index** out);
+zi_status zi_index_destroy(zi_index* idx);
+zi_status zi_index_size(const zi_index* idx, uint64_t* n, uint32_t* dims);
+/* zcurve_index::coords()/keys() (zcurve.hpp:130-133): sorted coords n*dims + keys n */
+zi_status zi_index_export(zi_index* idx, uint8_t* coords_out, uint32_t* keys_out);
+/* knn_search (zcurve.hpp:158-162, zcurve.cpp:429-452): exact k-NN in (distance, key) order;
+ * packed_out receives min(k, n) packed (dist<<32 | key) ascending. mu is validated only. */
+zi_status zi_knn_search(zi_index* idx, const uint8_t* query, uint32_t k, uint32_t mu, int32_t norm,
+                        uint64_t* packed_out, uint32_t* count_out);
+/* batched form for the cfg-5 sweep: queries nq*dims, packed_out nq*k, counts_out nq */
+zi_status zi_knn_search_batch(zi_index* idx, const uint8_t* queries, uint64_t nq, uint32_t k,
+                              int32_t norm, uint64_t* packed_out, uint32_t* counts_out);
+
+/* ---- dictionary: collect_dictionary (builder.hpp:52-55, builder.cpp:74-108) ---- */
+zi_status zi_dictionary_collect(zi_ctx* ctx, const uint8_t* known, int32_t width, int32_t height,
+                                int32_t patch_size, uint32_t* keys_out, uint64_t cap, uint64_t* n_out);
+
+/* ---- multi_index::build (builder.hpp:90-91, builder.cpp:202-224) ----
+ * image: height*width*channels u8 (row-major, channel-interleaved); known: height*width
+ * (nonzero = KNOWN).  All 8 layout indices are built on the device. */
+zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t* known,
+                               int32_t width, int32_t height, int32_t channels,
+                               const zi_index_config* cfg, zi_multi_index** out);
+/* rebuild from the device-resident image/mask (bench: inputs already in HBM) */
+zi_status zi_multi_index_rebuild(zi_multi_index* mi);
+zi_status zi_multi_index_destroy(zi_multi_index* mi);
+zi_status zi_multi_index_get_info(const zi_multi_index* mi, zi_multi_index_info* info);
+zi_status zi_multi_index_dictionary(zi_multi_index* mi, uint32_t* keys_out);
+/* patch_index fields (builder.hpp:60-75): layout rc m*2, pca mean (m*C), components
+ * (dims rows of m*C), eigenvalues (dims), quantizer lo/hi (dims).  NULL pointers are skipped. */
+zi_status zi_multi_index_layout(zi_multi_index* mi, int32_t layout, int32_t* rc, double* mean,
+                                double* components, double* eigenvalues, double* lo, double* hi);
+zi_status zi_multi_index_layout_index(zi_multi_index* mi, int32_t layout, uint8_t* coords_out,
+                                      uint32_t* keys_out);
+/* borrowed view of one layout's zcurve_index (valid until mi is destroyed or rebuilt) */
+zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index** out);
+/* exact int64 moments of the full K*K*C patch vector (s[F], S[F*F]) behind the PCA fit */
+zi_status zi_multi_index_moments(zi_multi_index* mi, int64_t* s_out, int64_t* S_out);
+
+/* ---- query ---- */
+/* query_best_patch (engine.hpp:93-96, engine.cpp:178-213): select_index + make_query + exact
+ * knn + masked-cost refine; target_values K*K*C, target_known K*K.  knn_out (optional)
+ * receives the sorted candidate list (best->candidates entries). */
+zi_status zi_query_best_patch(zi_multi_index* mi, const uint8_t* target_values,
+                              const uint8_t* target_known, uint32_t k, int32_t norm,
+                              zi_best_patch* out, uint64_t* knn_out);
+/* brute_force_best (engine.hpp:98-99, engine.cpp:220-236) over the whole dictionary */
+zi_status zi_brute_force_best(zi_multi_index* mi, const uint8_t* target_values,
+                              const uint8_t* target_known, int32_t norm, zi_best_patch* out);
+
+/* ---- inpaint (engine.hpp:112-118, engine.cpp:442-506) ----
+ * records: capacity `cap` (the iteration count never exceeds the unknown pixel count). */
+zi_status zi_inpaint(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t width,
+                     int32_t height, int32_t channels, const zi_index_config* cfg,
+                     const zi_inpaint_config* icfg, uint8_t* image_out,
+                     zi_iteration_record* records, uint64_t cap, uint64_t* n_records,
+                     zi_run_stats* stats);
+/* variant with prebuilt indices (engine.hpp:115-118): query-side knobs from cfg */
+zi_status zi_inpaint_with_index(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
+                                const zi_index_config* cfg, const zi_inpaint_config* icfg,
+                                uint8_t* image_out, zi_iteration_record* records, uint64_t cap,
+                                uint64_t* n_records, zi_run_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZINPAINT_B200_H */

@@ -1,0 +1,548 @@
+// api.cu -- the extern "C" boundary (include/zinpaint_b200.h).  Every entry point catches
+// internal exceptions and returns a zi_status; zi_last_error() holds the message.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+thread_local std::string g_err;
+
+zi_status fail(zi_status s, const std::string& m) {
+    g_err = m;
+    return s;
+}
+
+template <typename F>
+zi_status guard(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return ZI_OK;
+    } catch (const zi::error& e) {
+        return fail(e.code, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(ZI_E_OOM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(ZI_E_RUNTIME, e.what());
+    }
+}
+
+void require(bool ok, const char* msg) {
+    if (!ok) throw zi::error(ZI_E_INVALID, msg);
+}
+}  // namespace
+
+namespace zi {
+
+void launch_begin(zi_ctx* ctx, const char* name) {
+    ++ctx->launches;
+    if (!ctx->profiling) return;
+    prof_slot* s = nullptr;
+    for (auto& p : ctx->prof)
+        if (std::strcmp(p.name, name) == 0) s = &p;
+    if (!s) {
+        ctx->prof.emplace_back();
+        s = &ctx->prof.back();
+        s->name = name;
+    }
+    if (s->used == s->events.size()) {
+        cudaEvent_t a, b;
+        ZI_CUDA(cudaEventCreate(&a));
+        ZI_CUDA(cudaEventCreate(&b));
+        s->events.emplace_back(a, b);
+    }
+    ZI_CUDA(cudaEventRecord(s->events[s->used].first, ctx->stream));
+}
+
+void launch_end(zi_ctx* ctx, const char* name) {
+    if (!ctx->profiling) return;
+    for (auto& p : ctx->prof)
+        if (std::strcmp(p.name, name) == 0) {
+            ZI_CUDA(cudaEventRecord(p.events[p.used].second, ctx->stream));
+            ++p.used;
+            ++p.launches;
+            return;
+        }
+}
+
+}  // namespace zi
+
+static void upload_layouts(zi_multi_index* mi) {
+    std::vector<int32_t> rc;
+    mi->m = zi::subset_layouts(mi->K, mi->cfg.coverage, rc);
+    mi->mc = mi->m * mi->C;
+    std::vector<int32_t> off(static_cast<size_t>(8) * mi->m), loc(static_cast<size_t>(8) * mi->m);
+    for (int l = 0; l < 8; ++l) {
+        mi->L[l].rc.assign(rc.begin() + static_cast<size_t>(l) * mi->m * 2, rc.begin() + static_cast<size_t>(l + 1) * mi->m * 2);
+        for (int p = 0; p < mi->m; ++p) {
+            const int r = mi->L[l].rc[2 * p], c = mi->L[l].rc[2 * p + 1];
+            off[static_cast<size_t>(l) * mi->m + p] = (r * mi->w + c) * mi->C;
+            loc[static_cast<size_t>(l) * mi->m + p] = r * mi->K + c;
+        }
+    }
+    mi->layout_off.ensure(off.size());
+    mi->layout_local.ensure(loc.size());
+    ZI_CUDA(cudaMemcpyAsync(mi->layout_off.p, off.data(), off.size() * sizeof(int32_t), cudaMemcpyHostToDevice, mi->ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(mi->layout_local.p, loc.data(), loc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, mi->ctx->stream));
+}
+
+static void upload_image(zi_multi_index* mi, const uint8_t* image, const uint8_t* known) {
+    const size_t npx = static_cast<size_t>(mi->w) * mi->h;
+    mi->image.ensure(npx * mi->C);
+    mi->known.ensure(npx);
+    ZI_CUDA(cudaMemcpyAsync(mi->image.p, image, npx * mi->C, cudaMemcpyHostToDevice, mi->ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(mi->known.p, known, npx, cudaMemcpyHostToDevice, mi->ctx->stream));
+}
+
+static zi_multi_index* new_multi_index(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h,
+                                       int32_t C, const zi_index_config* cfg) {
+    require(ctx && image && known && cfg, "null argument");
+    require(w > 0 && h > 0 && (C == 1 || C == 3), "raster_image: bad dimensions");
+    require(w <= 65535 && h <= 65535, "image side above the 16-bit patch_key range");
+    require(static_cast<uint64_t>(w) * h * C < (1ull << 31), "image above 2^31 bytes");
+    zi::validate_config(*cfg, C);
+    auto* mi = new zi_multi_index();
+    mi->ctx = ctx;
+    mi->cfg = *cfg;
+    mi->w = w;
+    mi->h = h;
+    mi->C = C;
+    mi->K = cfg->patch_size;
+    try {
+        upload_layouts(mi);
+        upload_image(mi, image, known);
+    } catch (...) {
+        delete mi;
+        throw;
+    }
+    return mi;
+}
+
+extern "C" {
+
+const char* zi_last_error(void) { return g_err.c_str(); }
+const char* zi_version(void) { return "zinpaint_b200 0.1 (sm_100a)"; }
+
+zi_status zi_ctx_create(int device, zi_ctx** out) {
+    return guard([&] {
+        require(out != nullptr, "null argument");
+        ZI_CUDA(cudaSetDevice(device));
+        auto* c = new zi_ctx();
+        c->device = device;
+        cudaDeviceProp prop;
+        ZI_CUDA(cudaGetDeviceProperties(&prop, device));
+        c->num_sms = prop.multiProcessorCount;
+        ZI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        ZI_CUDA(cudaEventCreate(&c->t0));
+        ZI_CUDA(cudaEventCreate(&c->t1));
+        *out = c;
+    });
+}
+
+zi_status zi_ctx_destroy(zi_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& p : ctx->prof)
+            for (auto& e : p.events) {
+                cudaEventDestroy(e.first);
+                cudaEventDestroy(e.second);
+            }
+        cudaEventDestroy(ctx->t0);
+        cudaEventDestroy(ctx->t1);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+zi_status zi_ctx_synchronize(zi_ctx* ctx) {
+    return guard([&] { ZI_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+zi_status zi_timer_start(zi_ctx* ctx) {
+    return guard([&] { ZI_CUDA(cudaEventRecord(ctx->t0, ctx->stream)); });
+}
+
+zi_status zi_timer_stop(zi_ctx* ctx, double* ms) {
+    return guard([&] {
+        ZI_CUDA(cudaEventRecord(ctx->t1, ctx->stream));
+        ZI_CUDA(cudaEventSynchronize(ctx->t1));
+        float f = 0.f;
+        ZI_CUDA(cudaEventElapsedTime(&f, ctx->t0, ctx->t1));
+        *ms = f;
+    });
+}
+
+uint64_t zi_ctx_kernel_launches(const zi_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on) {
+    return guard([&] {
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->profiling = on != 0;
+        for (auto& p : ctx->prof) {
+            p.used = 0;
+            p.launches = 0;
+        }
+    });
+}
+
+zi_status zi_ctx_profile(const zi_ctx* ctx, int slot, double* ms, uint64_t* launches, const char** name) {
+    return guard([&] {
+        require(slot >= 0 && static_cast<size_t>(slot) < ctx->prof.size(), "profile slot out of range");
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        const auto& p = ctx->prof[slot];
+        double total = 0.0;
+        for (size_t i = 0; i < p.used; ++i) {
+            float f = 0.f;
+            ZI_CUDA(cudaEventElapsedTime(&f, p.events[i].first, p.events[i].second));
+            total += f;
+        }
+        if (ms) *ms = total;
+        if (launches) *launches = p.launches;
+        if (name) *name = p.name;
+    });
+}
+
+int zi_less_most_significant_bit(int a, int b) {
+    const uint8_t ua = static_cast<uint8_t>(a), ub = static_cast<uint8_t>(b);
+    return (ua < ub) && (ua < (ua ^ ub));
+}
+
+int zi_morton_less(const uint8_t* a, const uint8_t* b, uint32_t dims) {
+    uint8_t best_diff = 0;
+    uint32_t best_dim = 0;
+    for (uint32_t d = 0; d < dims; ++d) {
+        const uint8_t diff = static_cast<uint8_t>(a[d] ^ b[d]);
+        if (zi_less_most_significant_bit(best_diff, diff)) {
+            best_diff = diff;
+            best_dim = d;
+        }
+    }
+    return dims ? a[best_dim] < b[best_dim] : 0;
+}
+
+int zi_subset_pixel_count(int patch_size, double coverage) { return zi::subset_pixel_count(patch_size, coverage); }
+
+zi_status zi_subset_layouts(int patch_size, double coverage, int32_t* rc_out, int32_t* m_out) {
+    return guard([&] {
+        std::vector<int32_t> rc;
+        const int m = zi::subset_layouts(patch_size, coverage, rc);
+        if (rc_out) std::memcpy(rc_out, rc.data(), rc.size() * sizeof(int32_t));
+        if (m_out) *m_out = m;
+    });
+}
+
+void zi_index_config_default(zi_index_config* c) {
+    c->patch_size = 9;
+    c->coverage = 0.6;
+    c->dims = 10;
+    c->knn = 80;
+    c->mu = 256;
+    c->nu = 2048;
+    c->norm = ZI_NORM_L2;
+}
+
+zi_status zi_index_config_validate(const zi_index_config* cfg, int channels) {
+    return guard([&] { zi::validate_config(*cfg, channels); });
+}
+
+// ---------------------------------------------------------------- z-curve index
+zi_status zi_index_from_descriptors(zi_ctx* ctx, const uint8_t* coords, const uint32_t* keys, uint64_t n, uint32_t dims,
+                                    uint32_t layout_id, zi_index** out) {
+    return guard([&] {
+        require(ctx && out, "null argument");
+        if (dims == 0 || dims > 32) throw zi::error(ZI_E_INVALID, "zcurve_index: dims must be in [1, 32]");
+        require(n == 0 || (coords && keys), "null argument");
+        auto* idx = new zi_index();
+        idx->ctx = ctx;
+        idx->layout_id = layout_id;
+        try {
+            const int W = static_cast<int>((dims + 3) / 4);
+            zi::dbuf<uint8_t> dc;
+            zi::dbuf<uint32_t> recs;
+            if (n) {
+                dc.ensure(n * dims);
+                recs.ensure(static_cast<size_t>(W + 1) * n + n);
+                uint32_t* keys_in = recs.p + static_cast<size_t>(W + 1) * n;
+                ZI_CUDA(cudaMemcpyAsync(dc.p, coords, n * dims, cudaMemcpyHostToDevice, ctx->stream));
+                ZI_CUDA(cudaMemcpyAsync(keys_in, keys, n * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+                bool ascending = true;
+                for (uint64_t i = 1; i < n && ascending; ++i) ascending = keys[i - 1] < keys[i];
+                uint32_t* keyw = recs.p;
+                uint32_t* val = recs.p + static_cast<size_t>(W) * n;
+                zi::interleave_coords(ctx, dc.p, keys_in, n, static_cast<int>(dims), keyw, val);
+                zi::morton_sort(ctx, keyw, val, n, static_cast<int>(dims), !ascending);
+                zi::finalize_index(ctx, keyw, val, n, static_cast<int>(dims), idx);
+                ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+            } else {
+                zi::finalize_index(ctx, nullptr, nullptr, 0, static_cast<int>(dims), idx);
+            }
+        } catch (...) {
+            delete idx;
+            throw;
+        }
+        *out = idx;
+    });
+}
+
+zi_status zi_index_destroy(zi_index* idx) {
+    return guard([&] { delete idx; });
+}
+
+zi_status zi_index_size(const zi_index* idx, uint64_t* n, uint32_t* dims) {
+    return guard([&] {
+        if (n) *n = idx->n;
+        if (dims) *dims = idx->dims;
+    });
+}
+
+static void export_index(zi_index* idx, uint8_t* coords_out, uint32_t* keys_out) {
+    zi_ctx* ctx = idx->ctx;
+    const uint64_t n = idx->n;
+    if (n == 0) return;
+    if (keys_out) ZI_CUDA(cudaMemcpyAsync(keys_out, idx->keys.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    if (coords_out) {
+        std::vector<uint32_t> planes(static_cast<size_t>(idx->planes_n) * n);
+        ZI_CUDA(cudaMemcpyAsync(planes.data(), idx->planes.p, planes.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        const uint32_t D = idx->dims;
+        for (uint64_t i = 0; i < n; ++i)
+            for (uint32_t d = 0; d < D; ++d)
+                coords_out[i * D + d] = static_cast<uint8_t>((planes[static_cast<size_t>(d >> 2) * n + i] >> ((d & 3) * 8)) & 0xff);
+    }
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+zi_status zi_index_export(zi_index* idx, uint8_t* coords_out, uint32_t* keys_out) {
+    return guard([&] { export_index(idx, coords_out, keys_out); });
+}
+
+zi_status zi_knn_search(zi_index* idx, const uint8_t* query, uint32_t k, uint32_t mu, int32_t norm, uint64_t* packed_out,
+                        uint32_t* count_out) {
+    return guard([&] {
+        require(idx && query && packed_out && count_out, "null argument");
+        require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
+        (void)mu;  // leaf threshold of the CPU traversal; the GPU scan has no leaves
+        *count_out = zi::knn_search(idx, query, k, norm, packed_out);
+    });
+}
+
+zi_status zi_knn_search_batch(zi_index* idx, const uint8_t* queries, uint64_t nq, uint32_t k, int32_t norm,
+                              uint64_t* packed_out, uint32_t* counts_out) {
+    return guard([&] {
+        require(idx && (nq == 0 || (queries && packed_out && counts_out)), "null argument");
+        require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
+        zi::knn_search_batch(idx, queries, nq, k, norm, packed_out, counts_out);
+    });
+}
+
+// ---------------------------------------------------------------- dictionary
+zi_status zi_dictionary_collect(zi_ctx* ctx, const uint8_t* known, int32_t w, int32_t h, int32_t K, uint32_t* keys_out,
+                                uint64_t cap, uint64_t* n_out) {
+    return guard([&] {
+        require(ctx && known && n_out, "null argument");
+        require(w > 0 && h > 0 && w <= 65535 && h <= 65535, "mask_image: bad dimensions");
+        require(K >= 1, "patch size must be positive");
+        zi::dbuf<uint8_t> dk;
+        zi::dbuf<uint32_t> keys;
+        dk.ensure(static_cast<size_t>(w) * h);
+        ZI_CUDA(cudaMemcpyAsync(dk.p, known, static_cast<size_t>(w) * h, cudaMemcpyHostToDevice, ctx->stream));
+        const uint64_t n = zi::collect_dictionary(ctx, dk.p, w, h, K, keys);
+        *n_out = n;
+        if (n == 0) throw zi::error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
+        if (keys_out) {
+            require(cap >= n, "keys_out capacity below the dictionary size");
+            ZI_CUDA(cudaMemcpyAsync(keys_out, keys.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ---------------------------------------------------------------- multi-index
+zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h,
+                               int32_t C, const zi_index_config* cfg, zi_multi_index** out) {
+    return guard([&] {
+        require(out != nullptr, "null argument");
+        zi_multi_index* mi = new_multi_index(ctx, image, known, w, h, C, cfg);
+        try {
+            zi::build_multi_index(mi);
+        } catch (...) {
+            delete mi;
+            throw;
+        }
+        *out = mi;
+    });
+}
+
+zi_status zi_multi_index_rebuild(zi_multi_index* mi) {
+    return guard([&] { zi::build_multi_index(mi); });
+}
+
+zi_status zi_multi_index_destroy(zi_multi_index* mi) {
+    return guard([&] {
+        if (mi) cudaStreamSynchronize(mi->ctx->stream);
+        delete mi;
+    });
+}
+
+zi_status zi_multi_index_get_info(const zi_multi_index* mi, zi_multi_index_info* info) {
+    return guard([&] {
+        info->n = mi->n;
+        info->dims = mi->dims;
+        info->m = mi->m;
+        info->channels = mi->C;
+        info->patch_size = mi->K;
+        info->width = mi->w;
+        info->height = mi->h;
+        info->build_seconds = mi->build_ms * 1e-3;
+        info->eigen_seconds = mi->eigen_s;
+    });
+}
+
+zi_status zi_multi_index_dictionary(zi_multi_index* mi, uint32_t* keys_out) {
+    return guard([&] {
+        ZI_CUDA(cudaMemcpyAsync(keys_out, mi->dict.p, mi->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, mi->ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(mi->ctx->stream));
+    });
+}
+
+zi_status zi_multi_index_layout(zi_multi_index* mi, int32_t layout, int32_t* rc, double* mean, double* components,
+                                double* eigenvalues, double* lo, double* hi) {
+    return guard([&] {
+        require(layout >= 0 && layout < 8, "layout id must be in [0, 8)");
+        const auto& L = mi->L[layout];
+        if (rc) std::memcpy(rc, L.rc.data(), L.rc.size() * sizeof(int32_t));
+        if (mean) std::memcpy(mean, L.mean.data(), L.mean.size() * sizeof(double));
+        if (components) std::memcpy(components, L.comp.data(), L.comp.size() * sizeof(double));
+        if (eigenvalues) std::memcpy(eigenvalues, L.eig.data(), L.eig.size() * sizeof(double));
+        if (lo) std::memcpy(lo, L.lo.data(), L.lo.size() * sizeof(double));
+        if (hi) std::memcpy(hi, L.hi.data(), L.hi.size() * sizeof(double));
+    });
+}
+
+zi_status zi_multi_index_layout_index(zi_multi_index* mi, int32_t layout, uint8_t* coords_out, uint32_t* keys_out) {
+    return guard([&] {
+        require(layout >= 0 && layout < 8, "layout id must be in [0, 8)");
+        export_index(&mi->L[layout].index, coords_out, keys_out);
+    });
+}
+
+zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index** out) {
+    return guard([&] {
+        require(layout >= 0 && layout < 8, "layout id must be in [0, 8)");
+        *out = &mi->L[layout].index;
+    });
+}
+
+zi_status zi_multi_index_moments(zi_multi_index* mi, int64_t* s_out, int64_t* S_out) {
+    return guard([&] {
+        if (s_out) std::memcpy(s_out, mi->s.data(), mi->s.size() * sizeof(int64_t));
+        if (S_out) std::memcpy(S_out, mi->S.data(), mi->S.size() * sizeof(int64_t));
+    });
+}
+
+// ---------------------------------------------------------------- query
+zi_status zi_query_best_patch(zi_multi_index* mi, const uint8_t* tv, const uint8_t* tk, uint32_t k, int32_t norm,
+                              zi_best_patch* out, uint64_t* knn_out) {
+    return guard([&] {
+        require(mi && tv && tk && out, "null argument");
+        require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
+        const zi::query_result r = zi::query_best_patch(mi, tv, tk, k, norm, knn_out);
+        out->key = static_cast<uint32_t>(r.best & 0xffffffffu);
+        out->cost = static_cast<uint32_t>(r.best >> 32);
+        out->error = norm == ZI_NORM_L2 ? std::sqrt(static_cast<double>(out->cost)) : static_cast<double>(out->cost);
+        out->layout_id = r.lid;
+        out->candidates = r.count;
+    });
+}
+
+zi_status zi_brute_force_best(zi_multi_index* mi, const uint8_t* tv, const uint8_t* tk, int32_t norm, zi_best_patch* out) {
+    return guard([&] {
+        require(mi && tv && tk && out, "null argument");
+        require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
+        const uint64_t b = zi::brute_force_best(mi, tv, tk, norm);
+        out->key = static_cast<uint32_t>(b & 0xffffffffu);
+        out->cost = static_cast<uint32_t>(b >> 32);
+        out->error = norm == ZI_NORM_L2 ? std::sqrt(static_cast<double>(out->cost)) : static_cast<double>(out->cost);
+        out->layout_id = 0;
+        out->candidates = mi->n;
+    });
+}
+
+// ---------------------------------------------------------------- inpaint
+static void fill_stats_defaults(zi_run_stats* st) {
+    std::memset(st, 0, sizeof(*st));
+    st->mean_ae = std::numeric_limits<double>::quiet_NaN();
+    st->confidence_low = 1.0;
+}
+
+zi_status zi_inpaint(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h, int32_t C,
+                     const zi_index_config* cfg, const zi_inpaint_config* icfg, uint8_t* image_out,
+                     zi_iteration_record* records, uint64_t cap, uint64_t* n_records, zi_run_stats* stats) {
+    return guard([&] {
+        require(ctx && image && known && cfg && icfg && image_out && n_records && stats, "null argument");
+        require(w > 0 && h > 0 && (C == 1 || C == 3), "raster_image: bad dimensions");
+        zi::validate_config(*cfg, C);
+        fill_stats_defaults(stats);
+        *n_records = 0;
+        uint64_t unknown = 0;
+        for (size_t i = 0; i < static_cast<size_t>(w) * h; ++i) unknown += known[i] == 0;
+        if (unknown == 0) {  // engine.cpp:449-453
+            std::memcpy(image_out, image, static_cast<size_t>(w) * h * C);
+            return;
+        }
+        zi_multi_index* mi = new_multi_index(ctx, image, known, w, h, C, cfg);
+        try {
+            const auto t0 = std::chrono::steady_clock::now();
+            if (icfg->brute_force) {  // dictionary only (engine.cpp:466-473)
+                mi->n = zi::collect_dictionary(ctx, mi->known.p, w, h, mi->K, mi->dict);
+                if (mi->n == 0) throw zi::error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
+            } else {
+                zi::build_multi_index(mi);
+            }
+            stats->build_wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            stats->dictionary_size = mi->n;
+            zi::run_inpaint(mi, image, known, *cfg, *icfg, image_out, records, cap, n_records, stats);
+            stats->dictionary_size = mi->n;
+        } catch (...) {
+            delete mi;
+            throw;
+        }
+        delete mi;
+    });
+}
+
+zi_status zi_inpaint_with_index(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
+                                const zi_index_config* cfg, const zi_inpaint_config* icfg, uint8_t* image_out,
+                                zi_iteration_record* records, uint64_t cap, uint64_t* n_records, zi_run_stats* stats) {
+    return guard([&] {
+        require(mi && image && known && cfg && icfg && image_out && n_records && stats, "null argument");
+        fill_stats_defaults(stats);
+        *n_records = 0;
+        uint64_t unknown = 0;
+        for (size_t i = 0; i < static_cast<size_t>(mi->w) * mi->h; ++i) unknown += known[i] == 0;
+        if (unknown == 0) {
+            std::memcpy(image_out, image, static_cast<size_t>(mi->w) * mi->h * mi->C);
+            return;
+        }
+        // query-side knobs from cfg; build-side parameters pinned by the index (engine.cpp:498-505)
+        zi_index_config eff = *cfg;
+        eff.patch_size = mi->cfg.patch_size;
+        eff.coverage = mi->cfg.coverage;
+        eff.dims = mi->cfg.dims;
+        require(eff.norm == ZI_NORM_L2 || eff.norm == ZI_NORM_L1, "norm must be l2 or l1");
+        ZI_CUDA(cudaMemcpyAsync(mi->image.p, image, static_cast<size_t>(mi->w) * mi->h * mi->C, cudaMemcpyHostToDevice,
+                                mi->ctx->stream));
+        stats->dictionary_size = mi->n;
+        zi::run_inpaint(mi, image, known, eff, *icfg, image_out, records, cap, n_records, stats);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// build.cu -- multi_index::build on the device (proj/src/builder.cpp:129-224).
+//
+// Pipeline (one stream, everything device resident except the tiny eigen-solves):
+//   K1 collect_dictionary -> n keys (row-major)                       builder.cpp:74-108
+//   K2 exact int64 moments of the full K*K*C vector (one Gram serves
+//      all 8 layouts: each layout's covariance is a sub-block)        pca.cpp:20-37
+//   host: 8 eigen-solves in parallel threads (host_pca.cpp)            pca.cpp:39-67
+//   per layout: K3 project (fp64 canonical) -> min/max -> quantise +
+//      Morton interleave -> K4 onesweep radix sort -> K5 finalize      builder.cpp:159-195
+#include <algorithm>
+#include <chrono>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace zi {
+
+void build_multi_index(zi_multi_index* mi) {
+    zi_ctx* ctx = mi->ctx;
+    const auto wall0 = std::chrono::steady_clock::now();
+    cudaEvent_t e0, e1;
+    ZI_CUDA(cudaEventCreate(&e0));
+    ZI_CUDA(cudaEventCreate(&e1));
+    ZI_CUDA(cudaEventRecord(e0, ctx->stream));
+    const int K = mi->K, C = mi->C, w = mi->w, h = mi->h;
+
+    // K1
+    mi->n = collect_dictionary(ctx, mi->known.p, w, h, K, mi->dict);
+    if (mi->n == 0) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        throw error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
+    }
+    const uint64_t n = mi->n;
+    mi->dims = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(mi->cfg.dims),
+                                                   std::min<uint64_t>(static_cast<uint64_t>(mi->mc), n)));
+    const int D = mi->dims, mc = mi->mc, m = mi->m;
+
+    // K2
+    const int F = K * K * C;
+    mi->F = F;
+    const size_t nmom = static_cast<size_t>(F) + static_cast<size_t>(F) * F;
+    mi->moments.ensure(nmom);
+    patch_moments(ctx, mi->image.p, w, C, K, mi->dict.p, n, mi->moments.p);
+    unsigned long long* hm = mi->hmom.ensure(nmom);
+    ZI_CUDA(cudaMemcpyAsync(hm, mi->moments.p, nmom * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    mi->s.assign(F, 0);
+    mi->S.assign(static_cast<size_t>(F) * F, 0);
+    for (int i = 0; i < F; ++i) mi->s[i] = static_cast<int64_t>(hm[i]);
+    constexpr int kTile = 64;  // k_moments computes tile pairs ti <= tj only
+    for (int i = 0; i < F; ++i)
+        for (int j = 0; j < F; ++j) {
+            const int a = (i / kTile <= j / kTile) ? i : j, b = (i / kTile <= j / kTile) ? j : i;
+            mi->S[static_cast<size_t>(i) * F + j] = static_cast<int64_t>(hm[F + static_cast<size_t>(a) * F + b]);
+        }
+
+    // host eigen-solves, one thread per layout
+    const auto te0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int l = 0; l < 8; ++l) {
+        th.emplace_back([mi, l, F, n, D, C, K, m] {
+            auto& L = mi->L[l];
+            std::vector<int32_t> cols;
+            for (int p = 0; p < m; ++p)
+                for (int ch = 0; ch < C; ++ch) cols.push_back((L.rc[2 * p] * K + L.rc[2 * p + 1]) * C + ch);
+            pca_fit_layout(mi->s, mi->S, F, n, cols, D, L.mean, L.comp, L.eig);
+        });
+    }
+    for (auto& t : th) t.join();
+    mi->eigen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - te0).count();
+
+    // upload the 8 models: mean [l][j], comp [l][j][d]
+    std::vector<double> hmean(static_cast<size_t>(8) * mc), hcomp(static_cast<size_t>(8) * mc * D);
+    for (int l = 0; l < 8; ++l) {
+        std::copy(mi->L[l].mean.begin(), mi->L[l].mean.end(), hmean.begin() + static_cast<size_t>(l) * mc);
+        for (int j = 0; j < mc; ++j)
+            for (int d = 0; d < D; ++d)
+                hcomp[(static_cast<size_t>(l) * mc + j) * D + d] = mi->L[l].comp[static_cast<size_t>(d) * mc + j];
+    }
+    mi->pca_mean.ensure(hmean.size());
+    mi->pca_comp.ensure(hcomp.size());
+    ZI_CUDA(cudaMemcpyAsync(mi->pca_mean.p, hmean.data(), hmean.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(mi->pca_comp.p, hcomp.data(), hcomp.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    mi->minmax.ensure(static_cast<size_t>(8) * 2 * D);
+
+    // per layout: project, lo/hi, quantise + interleave, sort, finalize
+    const int W = (D + 3) / 4;
+    mi->proj.ensure(static_cast<size_t>(D) * n);
+    zi::dbuf<uint32_t>& recs = mi->recs;
+    recs.ensure(static_cast<size_t>(W + 1) * n);
+    for (int l = 0; l < 8; ++l) {
+        unsigned long long* mm = mi->minmax.p + static_cast<size_t>(l) * 2 * D;
+        project(ctx, mi->image.p, w, C, mi->dict.p, n, mi->layout_off.p + static_cast<size_t>(l) * m, m,
+                mi->pca_mean.p + static_cast<size_t>(l) * mc, mi->pca_comp.p + static_cast<size_t>(l) * mc * D, D,
+                mi->proj.p, mm);
+        uint32_t* keyw = recs.p;
+        uint32_t* val = recs.p + static_cast<size_t>(W) * n;
+        quantize_interleave(ctx, mi->proj.p, mm, mi->dict.p, n, D, keyw, val);
+        morton_sort(ctx, keyw, val, n, D, /*payload_first=*/false);
+        mi->L[l].index.ctx = ctx;
+        mi->L[l].index.layout_id = static_cast<uint32_t>(l);
+        finalize_index(ctx, keyw, val, n, D, &mi->L[l].index);
+    }
+    std::vector<unsigned long long> hmm(static_cast<size_t>(8) * 2 * D);
+    ZI_CUDA(cudaMemcpyAsync(hmm.data(), mi->minmax.p, hmm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    ZI_CUDA(cudaEventRecord(e1, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int l = 0; l < 8; ++l) {
+        mi->L[l].lo.resize(D);
+        mi->L[l].hi.resize(D);
+        for (int d = 0; d < D; ++d) {
+            mi->L[l].lo[d] = ordered_to_double(hmm[static_cast<size_t>(l) * 2 * D + d]);
+            mi->L[l].hi[d] = ordered_to_double(hmm[static_cast<size_t>(l) * 2 * D + D + d]);
+        }
+    }
+    float ms = 0.f;
+    ZI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    mi->build_ms = ms;
+    mi->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
+}  // namespace zi

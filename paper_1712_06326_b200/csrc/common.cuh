@@ -1,0 +1,86 @@
+// common.cuh -- device helpers shared by the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "zi_internal.h"
+
+#define ZI_LAUNCH(ctx, name, kernel, grid, block, smem, ...)                    \
+    do {                                                                        \
+        ::zi::launch_begin((ctx), (name));                                      \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);        \
+        ::zi::check_launch(name);                                               \
+        ::zi::launch_end((ctx), (name));                                        \
+    } while (0)
+
+namespace zi {
+
+constexpr uint64_t kU64Max = ~0ull;
+
+// Order-preserving map of a finite double onto uint64 (used for atomic min/max of lo/hi).
+__host__ __device__ inline unsigned long long double_to_ordered(double x) {
+    unsigned long long b;
+#ifdef __CUDA_ARCH__
+    b = static_cast<unsigned long long>(__double_as_longlong(x));
+#else
+    std::memcpy(&b, &x, sizeof(b));
+#endif
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__host__ __device__ inline double ordered_to_double_hd(unsigned long long u) {
+    const unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(static_cast<long long>(b));
+#else
+    double x;
+    std::memcpy(&x, &b, sizeof(x));
+    return x;
+#endif
+}
+
+// quantizer::quantize (proj/src/builder.cpp:55-61): IEEE ops spelled out so nothing is fused.
+__device__ inline uint8_t quantize_rn(double l, double h, double y) {
+    if (!(h > l)) return 0;
+    const double c = y < l ? l : (h < y ? h : y);
+    const double v = __ddiv_rn(__dmul_rn(255.0, __dsub_rn(c, l)), __dsub_rn(h, l));
+    return static_cast<uint8_t>(llround(v));
+}
+
+// less_most_significant_bit / morton_less (proj/include/zinpaint/morton.hpp:10-29)
+__device__ inline bool less_msb(uint32_t a, uint32_t b) { return (a < b) && (a < (a ^ b)); }
+
+__device__ inline uint32_t plane_byte(uint32_t w, int d) { return (w >> ((d & 3) * 8)) & 0xffu; }
+
+// Morton bit position (from the LSB) of bit L of dim d in a D-dim, 8-bit interleave:
+// level 7 first, dim 0 first within a level  ->  u = L*D + (D-1-d).
+__host__ __device__ inline int morton_bit(int L, int d, int D) { return L * D + (D - 1 - d); }
+
+__device__ inline uint64_t pack_candidate(uint32_t dist, uint32_t key) {
+    return (static_cast<uint64_t>(dist) << 32) | key;
+}
+
+// distance of 4 packed bytes (L2 squared / L1)
+__device__ inline uint32_t dist4(uint32_t a, uint32_t b, int norm, uint32_t acc) {
+    const uint32_t d = __vabsdiffu4(a, b);
+    return norm == 0 ? __dp4a(d, d, acc) : __dp4a(d, 0x01010101u, acc);
+}
+
+// lower bound of the distance from q to the byte box [mn, mx] over 4 packed dims
+__device__ inline uint32_t gap4(uint32_t q, uint32_t mn, uint32_t mx, int norm, uint32_t acc) {
+    const uint32_t g = __vsubus4(mn, q) | __vsubus4(q, mx);
+    return norm == 0 ? __dp4a(g, g, acc) : __dp4a(g, 0x01010101u, acc);
+}
+
+template <typename T>
+__device__ inline T warp_min(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+
+}  // namespace zi

@@ -1,0 +1,304 @@
+// host_engine.cpp -- the sequential fill loop (host) around the device query.
+//
+// Restates proj/src/engine.cpp:83-146 (confidence / priority), :238-257 (paste),
+// :283-369 (fill_driver), :371-438 (run_loop), :259-276 (acceleration_error).  The loop is
+// inherently sequential (each paste changes the next target), so it stays on the host; each
+// iteration's patch search runs on the GPU (zi::query_best_patch / zi::brute_force_best).
+// Sources are dictionary windows, which are fully known and never overwritten, so the
+// device copy of the input image stays valid for every cost evaluation.
+//
+// Built with -ffp-contract=off: priorities are compared exactly (std::set order, `!=`
+// refresh), so no expression may be silently fused.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <set>
+#include <utility>
+#include <vector>
+
+#include "zi_internal.h"
+
+namespace zi {
+namespace {
+
+constexpr double kPriorityEpsilon = 1e-3;
+
+struct raster {
+    int w, h, C;
+    std::vector<uint8_t> px;
+    const uint8_t* at(int x, int y) const { return px.data() + (static_cast<size_t>(y) * w + x) * C; }
+    uint8_t* at(int x, int y) { return px.data() + (static_cast<size_t>(y) * w + x) * C; }
+};
+
+struct mask {
+    int w, h;
+    std::vector<uint8_t> known;
+    bool is_known(int x, int y) const { return known[static_cast<size_t>(y) * w + x] != 0; }
+    bool in_bounds(int x, int y) const { return x >= 0 && x < w && y >= 0 && y < h; }
+    size_t idx(int x, int y) const { return static_cast<size_t>(y) * w + x; }
+};
+
+// proj/src/image.cpp:49-55
+bool is_fillfront_pixel(const mask& m, int x, int y) {
+    if (!m.is_known(x, y)) return false;
+    return (x > 0 && !m.is_known(x - 1, y)) || (x + 1 < m.w && !m.is_known(x + 1, y)) ||
+           (y > 0 && !m.is_known(x, y - 1)) || (y + 1 < m.h && !m.is_known(x, y + 1));
+}
+
+double channel_mean(const uint8_t* p, int C) {
+    int sum = 0;
+    for (int c = 0; c < C; ++c) sum += p[c];
+    return static_cast<double>(sum) / C;
+}
+
+// proj/src/engine.cpp:83-94
+double confidence_term(const mask& m, const std::vector<double>& conf, int cx, int cy, int K) {
+    const int r = (K - 1) / 2;
+    double sum = 0.0;
+    for (int y = cy - r; y <= cy + r; ++y)
+        for (int x = cx - r; x <= cx + r; ++x) {
+            if (!m.in_bounds(x, y) || !m.is_known(x, y)) continue;
+            sum += conf[m.idx(x, y)];
+        }
+    return sum / (static_cast<double>(K) * K);
+}
+
+// proj/src/engine.cpp:96-146
+double compute_priority(const raster& img, const mask& m, const std::vector<double>& conf, int cx, int cy, int K) {
+    const int r = (K - 1) / 2;
+    const double cterm = confidence_term(m, conf, cx, cy, K);
+    double best_sq = -1.0, bgx = 0.0, bgy = 0.0;
+    for (int y = cy - r; y <= cy + r; ++y)
+        for (int x = cx - r; x <= cx + r; ++x) {
+            if (x < 1 || y < 1 || x + 1 >= img.w || y + 1 >= img.h) continue;
+            if (!m.is_known(x, y) || !m.is_known(x - 1, y) || !m.is_known(x + 1, y) || !m.is_known(x, y - 1) ||
+                !m.is_known(x, y + 1))
+                continue;
+            const double gx = (channel_mean(img.at(x + 1, y), img.C) - channel_mean(img.at(x - 1, y), img.C)) / 2.0;
+            const double gy = (channel_mean(img.at(x, y + 1), img.C) - channel_mean(img.at(x, y - 1), img.C)) / 2.0;
+            const double sq = gx * gx + gy * gy;
+            if (sq > best_sq) {
+                best_sq = sq;
+                bgx = gx;
+                bgy = gy;
+            }
+        }
+    auto unknown_at = [&](int x, int y) {
+        x = std::clamp(x, 0, m.w - 1);
+        y = std::clamp(y, 0, m.h - 1);
+        return m.is_known(x, y) ? 0.0 : 1.0;
+    };
+    const double nx = (unknown_at(cx + 1, cy) - unknown_at(cx - 1, cy)) / 2.0;
+    const double ny = (unknown_at(cx, cy + 1) - unknown_at(cx, cy - 1)) / 2.0;
+    const double nlen = std::hypot(nx, ny);
+    double data = kPriorityEpsilon;
+    if (best_sq > 0.0 && nlen > 0.0) {
+        const double iso_x = -bgy, iso_y = bgx;
+        data = std::abs(iso_x * nx / nlen + iso_y * ny / nlen) / 255.0 + kPriorityEpsilon;
+    }
+    return cterm * data;
+}
+
+struct by_priority {
+    bool operator()(const std::pair<double, uint32_t>& a, const std::pair<double, uint32_t>& b) const {
+        if (a.first != b.first) return a.first > b.first;
+        return a.second < b.second;
+    }
+};
+
+// proj/src/engine.cpp:283-369 -- fill front ordered by (priority desc, row-major asc),
+// priorities cached and refreshed only where a paste could change them.
+class fill_driver {
+public:
+    fill_driver(raster& img, mask& m, int K)
+        : img_(img), m_(m), K_(K), conf_(static_cast<size_t>(m.w) * m.h, 0.0),
+          cached_(static_cast<size_t>(m.w) * m.h, 0.0), in_front_(static_cast<size_t>(m.w) * m.h, 0) {
+        for (size_t i = 0; i < conf_.size(); ++i) conf_[i] = m.known[i] ? 1.0 : 0.0;
+        for (int y = 0; y < m.h; ++y)
+            for (int x = 0; x < m.w; ++x)
+                if (is_fillfront_pixel(m_, x, y)) add(x, y);
+    }
+    bool empty() const { return queue_.empty(); }
+    void next_target(int& x, int& y) const {
+        const uint32_t pos = queue_.begin()->second;
+        x = static_cast<int>(pos % m_.w);
+        y = static_cast<int>(pos / m_.w);
+    }
+    // paste (engine.cpp:238-257) + membership / priority refresh (engine.cpp:307-330)
+    int apply_paste(int cx, int cy, uint32_t src, double* center_conf) {
+        const int r = (K_ - 1) / 2;
+        const double cc = confidence_term(m_, conf_, cx, cy, K_);
+        const int sx = static_cast<int>(src & 0xffffu), sy = static_cast<int>(src >> 16);
+        int filled = 0;
+        for (int dy = 0; dy < K_; ++dy) {
+            const int y = cy - r + dy;
+            for (int dx = 0; dx < K_; ++dx) {
+                const int x = cx - r + dx;
+                if (!m_.in_bounds(x, y) || m_.is_known(x, y)) continue;
+                const uint8_t* s = img_.at(sx + dx, sy + dy);
+                uint8_t* d = img_.at(x, y);
+                for (int c = 0; c < img_.C; ++c) d[c] = s[c];
+                m_.known[m_.idx(x, y)] = 1;
+                conf_[m_.idx(x, y)] = cc;
+                ++filled;
+            }
+        }
+        const int refresh = K_ - 1;
+        for (int y = cy - refresh; y <= cy + refresh; ++y) {
+            if (y < 0 || y >= m_.h) continue;
+            for (int x = cx - refresh; x <= cx + refresh; ++x) {
+                if (x < 0 || x >= m_.w) continue;
+                const size_t i = m_.idx(x, y);
+                const bool zone = std::abs(x - cx) <= r + 1 && std::abs(y - cy) <= r + 1;
+                const bool now = zone ? is_fillfront_pixel(m_, x, y) : in_front_[i] != 0;
+                if (in_front_[i] && !now) remove(x, y);
+                else if (!in_front_[i] && now) add(x, y);
+                else if (in_front_[i] && now) refresh_one(x, y);
+            }
+        }
+        *center_conf = cc;
+        return filled;
+    }
+
+private:
+    void add(int x, int y) {
+        const size_t i = m_.idx(x, y);
+        cached_[i] = compute_priority(img_, m_, conf_, x, y, K_);
+        in_front_[i] = 1;
+        queue_.emplace(cached_[i], static_cast<uint32_t>(i));
+    }
+    void remove(int x, int y) {
+        const size_t i = m_.idx(x, y);
+        queue_.erase({cached_[i], static_cast<uint32_t>(i)});
+        in_front_[i] = 0;
+    }
+    void refresh_one(int x, int y) {
+        const size_t i = m_.idx(x, y);
+        const double fresh = compute_priority(img_, m_, conf_, x, y, K_);
+        if (fresh != cached_[i]) {
+            queue_.erase({cached_[i], static_cast<uint32_t>(i)});
+            cached_[i] = fresh;
+            queue_.emplace(fresh, static_cast<uint32_t>(i));
+        }
+    }
+    raster& img_;
+    mask& m_;
+    int K_;
+    std::vector<double> conf_, cached_;
+    std::vector<uint8_t> in_front_;
+    std::set<std::pair<double, uint32_t>, by_priority> queue_;
+};
+
+// extract_patch_clamped (proj/src/image.cpp:7-47)
+void extract_clamped(const raster& img, const mask& m, int cx, int cy, int K, std::vector<uint8_t>& tv,
+                     std::vector<uint8_t>& tk) {
+    const int r = (K - 1) / 2;
+    std::fill(tv.begin(), tv.end(), 0);
+    std::fill(tk.begin(), tk.end(), 0);
+    for (int dy = 0; dy < K; ++dy) {
+        const int y = cy - r + dy;
+        for (int dx = 0; dx < K; ++dx) {
+            const int x = cx - r + dx;
+            if (!m.in_bounds(x, y) || !m.is_known(x, y)) continue;
+            const int local = dy * K + dx;
+            tk[local] = 1;
+            const uint8_t* s = img.at(x, y);
+            for (int c = 0; c < img.C; ++c) tv[static_cast<size_t>(local) * img.C + c] = s[c];
+        }
+    }
+}
+
+double cost_to_error(uint32_t cost, int norm) {
+    return norm == ZI_NORM_L2 ? std::sqrt(static_cast<double>(cost)) : static_cast<double>(cost);
+}
+
+}  // namespace
+
+// run_loop (proj/src/engine.cpp:371-438)
+void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known, const zi_index_config& cfg,
+                 const zi_inpaint_config& icfg, uint8_t* image_out, zi_iteration_record* records, uint64_t cap,
+                 uint64_t* n_records, zi_run_stats* stats) {
+    raster img{mi->w, mi->h, mi->C, std::vector<uint8_t>(image, image + static_cast<size_t>(mi->w) * mi->h * mi->C)};
+    mask m{mi->w, mi->h, std::vector<uint8_t>(static_cast<size_t>(mi->w) * mi->h)};
+    for (size_t i = 0; i < m.known.size(); ++i) m.known[i] = known[i] ? 1 : 0;
+    uint64_t unknown_left = 0;
+    for (auto v : m.known) unknown_left += v == 0;
+    uint64_t it = 0;
+    double ae_sum = 0.0;
+    uint64_t ae_contrib = 0, ae_excl = 0;
+    stats->iterations = 0;
+    stats->mean_ae = std::numeric_limits<double>::quiet_NaN();
+    stats->ae_excluded = 0;
+    stats->confidence_low = 1.0;
+    stats->confidence_high = 0.0;
+    if (unknown_left == 0) {
+        std::copy(img.px.begin(), img.px.end(), image_out);
+        *n_records = 0;
+        stats->inpaint_seconds = 0.0;
+        return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const int K = mi->K;
+    fill_driver drv(img, m, K);
+    std::vector<uint8_t> tv(static_cast<size_t>(K) * K * mi->C), tk(static_cast<size_t>(K) * K);
+    const uint32_t k = static_cast<uint32_t>(std::max(cfg.knn, 1));
+    while (unknown_left > 0) {
+        if (drv.empty()) throw error(ZI_E_RUNTIME, "inpaint: unknown pixels unreachable from the fillfront");
+        const auto t_it = std::chrono::steady_clock::now();
+        int tx, ty;
+        drv.next_target(tx, ty);
+        extract_clamped(img, m, tx, ty, K, tv, tk);
+        zi_iteration_record rec{};
+        rec.iteration = it;
+        rec.target_x = tx;
+        rec.target_y = ty;
+        uint64_t best;
+        if (icfg.brute_force) {
+            best = brute_force_best(mi, tv.data(), tk.data(), cfg.norm);
+            rec.layout_id = 0;
+            rec.candidates = mi->n;
+        } else {
+            const query_result q = query_best_patch(mi, tv.data(), tk.data(), k, cfg.norm, nullptr);
+            best = q.best;
+            rec.layout_id = q.lid;
+            rec.candidates = q.count;
+        }
+        rec.cost = static_cast<uint32_t>(best >> 32);
+        rec.source_key = static_cast<uint32_t>(best & 0xffffffffu);
+        rec.z_error = cost_to_error(rec.cost, cfg.norm);
+        rec.bf_error = std::numeric_limits<double>::quiet_NaN();
+        if (icfg.oracle && !icfg.brute_force && it % std::max<uint64_t>(1, icfg.oracle_stride) == 0) {
+            const uint64_t o = brute_force_best(mi, tv.data(), tk.data(), cfg.norm);
+            rec.bf_error = cost_to_error(static_cast<uint32_t>(o >> 32), cfg.norm);
+        } else if (icfg.brute_force) {
+            rec.bf_error = rec.z_error;
+        }
+        // acceleration_error (engine.cpp:259-276)
+        if (!std::isnan(rec.bf_error)) {
+            if (rec.bf_error > 0.0) {
+                ae_sum += rec.z_error / rec.bf_error - 1.0;
+                ++ae_contrib;
+            } else if (rec.z_error == 0.0) {
+                ++ae_contrib;
+            } else {
+                ++ae_excl;
+            }
+        }
+        double cc;
+        unknown_left -= static_cast<uint64_t>(drv.apply_paste(tx, ty, rec.source_key, &cc));
+        stats->confidence_low = std::min(stats->confidence_low, cc);
+        stats->confidence_high = std::max(stats->confidence_high, cc);
+        rec.elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_it).count();
+        if (records && it < cap) records[it] = rec;
+        ++it;
+    }
+    std::copy(img.px.begin(), img.px.end(), image_out);
+    *n_records = it;
+    stats->iterations = it;
+    stats->inpaint_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (ae_contrib > 0) stats->mean_ae = ae_sum / static_cast<double>(ae_contrib);
+    stats->ae_excluded = ae_excl;
+}
+
+}  // namespace zi

@@ -1,0 +1,512 @@
+// k_build.cu -- index-construction kernels (sm_100a):
+//   K1 collect_dictionary   proj/src/builder.cpp:74-108
+//   K2 patch_moments        proj/src/pca.cpp:20-37 (exact integer restatement)
+//   K3 project / quantize   proj/src/builder.cpp:159-187, :55-61
+//   K5 finalize_index       proj/src/zcurve.cpp:127-137 (+ per-block bounding boxes)
+#include <algorithm>
+#include <climits>
+
+#include "common.cuh"
+
+namespace zi {
+
+// ============================================================== K1: dictionary collection
+// colflag[y][x] = 1 iff any unknown pixel in column x, rows y..y+K-1
+__global__ void k_colflag(const uint8_t* __restrict__ known, int w, int h, int K,
+                          uint8_t* __restrict__ colflag) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= w) return;
+    uint8_t any = 0;
+    for (int r = 0; r < K; ++r) any |= known[static_cast<size_t>(y + r) * w + x] == 0;
+    colflag[static_cast<size_t>(y) * w + x] = any;
+}
+
+// valid[y][x] (x < w-K+1) = no flagged column among x..x+K-1
+__global__ void k_validflag(const uint8_t* __restrict__ colflag, int w, int K, int wo,
+                            uint8_t* __restrict__ valid) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= wo) return;
+    uint8_t any = 0;
+    const uint8_t* row = colflag + static_cast<size_t>(y) * w + x;
+    for (int c = 0; c < K; ++c) any |= row[c];
+    valid[static_cast<size_t>(y) * wo + x] = any ? 0 : 1;
+}
+
+constexpr int kCompactThreads = 256;
+constexpr int kCompactPer = 16;
+constexpr int kCompactTile = kCompactThreads * kCompactPer;  // 4096 flags per block
+
+__device__ inline uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        uint32_t t = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < nw) s_warp[lane] = t;  // inclusive per-warp totals
+    }
+    __syncthreads();
+    const uint32_t warp_prefix = warp ? s_warp[warp - 1] : 0;
+    if (total) *total = s_warp[(blockDim.x >> 5) - 1];
+    const uint32_t r = warp_prefix + x - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_count_flags(const uint8_t* __restrict__ flags, uint64_t n,
+                                                                 uint32_t* __restrict__ counts) {
+    __shared__ uint32_t s_warp[32];
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kCompactTile + threadIdx.x * kCompactPer;
+    uint32_t c = 0;
+    for (int i = 0; i < kCompactPer; ++i) c += (base + i < n) ? flags[base + i] : 0;
+    uint32_t total;
+    block_exclusive_scan(c, s_warp, &total);
+    if (threadIdx.x == 0) counts[blockIdx.x] = total;
+}
+
+// single-CTA exclusive scan of nb block counts (in place); total -> counts[nb]
+__global__ void __launch_bounds__(1024) k_scan_counts(uint32_t* counts, uint64_t nb) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (uint64_t b = 0; b < nb; b += 1024) {
+        const uint64_t i = b + threadIdx.x;
+        const uint32_t v = i < nb ? counts[i] : 0;
+        uint32_t total;
+        const uint32_t ex = block_exclusive_scan(v, s_warp, &total);
+        if (i < nb) counts[i] = s_carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) counts[nb] = s_carry;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_write_keys(const uint8_t* __restrict__ flags, uint64_t n,
+                                                                int wo, const uint32_t* __restrict__ offsets,
+                                                                uint32_t* __restrict__ keys) {
+    __shared__ uint32_t s_warp[32];
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kCompactTile + threadIdx.x * kCompactPer;
+    uint8_t f[kCompactPer];
+    uint32_t c = 0;
+    for (int i = 0; i < kCompactPer; ++i) {
+        f[i] = (base + i < n) ? flags[base + i] : 0;
+        c += f[i];
+    }
+    uint32_t pos = offsets[blockIdx.x] + block_exclusive_scan(c, s_warp, nullptr);
+    for (int i = 0; i < kCompactPer; ++i)
+        if (f[i]) {
+            const uint64_t o = base + i;
+            const uint32_t y = static_cast<uint32_t>(o / wo), x = static_cast<uint32_t>(o % wo);
+            keys[pos++] = (y << 16) | x;
+        }
+}
+
+uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, int K,
+                            dbuf<uint32_t>& keys_out) {
+    if (w < K || h < K) return 0;
+    const int ho = h - K + 1, wo = w - K + 1;
+    const uint64_t n_orig = static_cast<uint64_t>(ho) * wo;
+    const uint64_t nb = (n_orig + kCompactTile - 1) / kCompactTile;
+    // scratch: colflag (ho*w) + valid (n_orig) + counts (nb+1)
+    const size_t sz_col = static_cast<size_t>(ho) * w, sz_valid = n_orig;
+    uint8_t* base = ctx->scratch.ensure(sz_col + sz_valid + 16 + (nb + 1) * sizeof(uint32_t) + 16);
+    uint8_t* colflag = base;
+    uint8_t* valid = base + sz_col;
+    uint32_t* counts = reinterpret_cast<uint32_t*>(base + ((sz_col + sz_valid + 15) & ~size_t(15)));
+    ZI_LAUNCH(ctx, "collect_colflag", k_colflag, dim3((w + 255) / 256, ho), 256, 0, d_known, w, h, K, colflag);
+    ZI_LAUNCH(ctx, "collect_validflag", k_validflag, dim3((wo + 255) / 256, ho), 256, 0, colflag, w, K, wo, valid);
+    ZI_LAUNCH(ctx, "collect_count", k_count_flags, dim3(static_cast<unsigned>(nb)), kCompactThreads, 0, valid,
+              n_orig, counts);
+    ZI_LAUNCH(ctx, "collect_scan", k_scan_counts, 1, 1024, 0, counts, nb);
+    uint32_t total = 0;
+    ZI_CUDA(cudaMemcpyAsync(&total, counts + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    keys_out.ensure(total ? total : 1);
+    if (total)
+        ZI_LAUNCH(ctx, "collect_write", k_write_keys, dim3(static_cast<unsigned>(nb)), kCompactThreads, 0, valid,
+                  n_orig, wo, counts, keys_out.p);
+    return total;
+}
+
+// ============================================================== K2: exact patch moments
+// S = sum_p x_p x_p^T and s = sum_p x_p over the full K*K*C patch vectors (u8), on the
+// integer dot-product path (__dp4a, exact).  One CTA = one 64x64 feature tile pair (ti<=tj) x
+// one chunk of <= 32768 patches (32768 * 255^2 < 2^31 keeps the int32 accumulators exact);
+// chunk partials are added into int64 with atomics (order-free => deterministic).
+constexpr int kMomTile = 64;
+constexpr int kMomBatch = 64;
+constexpr int kMomChunk = 32768;
+constexpr int kMomPitch = kMomBatch + 4;  // bytes per smem row: 17 words -> conflict-free columns
+
+__global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ img, int w, int C, int K, int F,
+                                                 const uint32_t* __restrict__ keys, uint64_t n, int ntile,
+                                                 unsigned long long* __restrict__ out) {
+    __shared__ int s_offi[kMomTile], s_offj[kMomTile];
+    __shared__ __align__(16) uint8_t s_xi[kMomTile * kMomPitch];
+    __shared__ __align__(16) uint8_t s_xj[kMomTile * kMomPitch];
+    __shared__ int s_base[kMomBatch];
+
+    int p = blockIdx.x, ti = 0;
+    while (p >= ntile - ti) {
+        p -= ntile - ti;
+        ++ti;
+    }
+    const int tj = ti + p;
+    const bool diag = ti == tj;
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    if (tid < kMomTile) {
+        const int f = ti * kMomTile + tid;
+        s_offi[tid] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : -1;
+    } else if (tid < 2 * kMomTile) {
+        const int f = tj * kMomTile + tid - kMomTile;
+        s_offj[tid - kMomTile] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : -1;
+    }
+    const uint64_t c0 = static_cast<uint64_t>(blockIdx.y) * kMomChunk;
+    const uint64_t c1 = c0 + kMomChunk < n ? c0 + kMomChunk : n;
+
+    uint32_t acc[4][4] = {};
+    uint32_t rs[4] = {};
+    for (uint64_t b = c0; b < c1; b += kMomBatch) {
+        __syncthreads();
+        if (tid < kMomBatch) {
+            const uint64_t idx = b + tid;
+            if (idx < c1) {
+                const uint32_t key = keys[idx];
+                s_base[tid] = static_cast<int>(((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C);
+            } else {
+                s_base[tid] = -1;
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < kMomTile * kMomBatch; e += 256) {
+            const int f = e / kMomBatch, pp = e % kMomBatch;
+            const int bs = s_base[pp];
+            const int oi = s_offi[f], oj = s_offj[f];
+            s_xi[f * kMomPitch + pp] = (bs >= 0 && oi >= 0) ? __ldg(img + bs + oi) : 0;
+            s_xj[f * kMomPitch + pp] = (bs >= 0 && oj >= 0) ? __ldg(img + bs + oj) : 0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int pp = 0; pp < kMomBatch; pp += 4) {
+            uint32_t a[4], bb[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const uint32_t*>(s_xi + (ty * 4 + r) * kMomPitch + pp);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) bb[c] = *reinterpret_cast<const uint32_t*>(s_xj + (tx * 4 + c) * kMomPitch + pp);
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] = __dp4a(a[r], bb[c], acc[r][c]);
+            if (diag && tx == 0) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) rs[r] = __dp4a(a[r], 0x01010101u, rs[r]);
+            }
+        }
+    }
+    for (int r = 0; r < 4; ++r) {
+        const int fi = ti * kMomTile + ty * 4 + r;
+        if (fi >= F) continue;
+        for (int c = 0; c < 4; ++c) {
+            const int fj = tj * kMomTile + tx * 4 + c;
+            if (fj < F && acc[r][c]) atomicAdd(out + F + static_cast<size_t>(fi) * F + fj, static_cast<unsigned long long>(acc[r][c]));
+        }
+        if (diag && tx == 0 && rs[r]) atomicAdd(out + fi, static_cast<unsigned long long>(rs[r]));
+    }
+}
+
+void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const uint32_t* d_keys,
+                   uint64_t n, unsigned long long* d_out) {
+    const int F = K * K * C;
+    ZI_CUDA(cudaMemsetAsync(d_out, 0, (static_cast<size_t>(F) + static_cast<size_t>(F) * F) * sizeof(unsigned long long),
+                            ctx->stream));
+    if (n == 0) return;
+    const int ntile = (F + kMomTile - 1) / kMomTile;
+    const int npairs = ntile * (ntile + 1) / 2;
+    const uint64_t nchunk = (n + kMomChunk - 1) / kMomChunk;
+    ZI_LAUNCH(ctx, "patch_moments", k_moments, dim3(npairs, static_cast<unsigned>(nchunk)), 256, 0, d_img, w, C, K, F,
+              d_keys, n, ntile, d_out);
+}
+
+// ============================================================== K3: projection
+// Y[d*n + i] = sum_j fma(comp[j][d], x_ij - mean_j) in the canonical order (j ascending,
+// starting from +0.0) -- bit-identical to the oracle's restatement of
+// proj/src/builder.cpp:166-167/180-181 (fill_chunk gather order :20-34).
+template <int D>
+__global__ void __launch_bounds__(256) k_project(const uint8_t* __restrict__ img, int w, int C,
+                                                 const uint32_t* __restrict__ keys, uint64_t n,
+                                                 const int32_t* __restrict__ off, int m,
+                                                 const double* __restrict__ mean,
+                                                 const double* __restrict__ comp, double* __restrict__ Y) {
+    extern __shared__ double sm[];
+    const int mc = m * C;
+    double* s_comp = sm;                 // mc*D  ([j][d])
+    double* s_mean = sm + mc * D;        // mc
+    int* s_off = reinterpret_cast<int*>(s_mean + mc);  // m
+    for (int i = threadIdx.x; i < mc * D; i += blockDim.x) s_comp[i] = comp[i];
+    for (int i = threadIdx.x; i < mc; i += blockDim.x) s_mean[i] = mean[i];
+    for (int i = threadIdx.x; i < m; i += blockDim.x) s_off[i] = off[i];
+    __syncthreads();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t key = keys[i];
+        const uint8_t* base = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
+        double y[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) y[d] = 0.0;
+        int j = 0;
+        for (int p = 0; p < m; ++p) {
+            const uint8_t* px = base + s_off[p];
+            for (int ch = 0; ch < C; ++ch, ++j) {
+                const double xc = __dsub_rn(static_cast<double>(__ldg(px + ch)), s_mean[j]);
+                const double* cj = s_comp + j * D;
+#pragma unroll
+                for (int d = 0; d < D; ++d) y[d] = __fma_rn(cj[d], xc, y[d]);
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) Y[static_cast<size_t>(d) * n + i] = y[d];
+    }
+}
+
+// per-dimension min/max of Y -> ordered-u64 atomics (lo: atomicMin, hi: atomicMax)
+__global__ void __launch_bounds__(256) k_minmax(const double* __restrict__ Y, uint64_t n,
+                                                unsigned long long* __restrict__ minmax, int D) {
+    const int d = blockIdx.y;
+    const double* y = Y + static_cast<size_t>(d) * n;
+    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double v = y[i];
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    __shared__ double s_lo[8], s_hi[8];
+    if ((threadIdx.x & 31) == 0) {
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) {
+            lo = s_lo[k] < lo ? s_lo[k] : lo;
+            hi = s_hi[k] > hi ? s_hi[k] : hi;
+        }
+        atomicMin(minmax + d, double_to_ordered(lo));
+        atomicMax(minmax + D + d, double_to_ordered(hi));
+    }
+}
+
+// quantise (proj/src/builder.cpp:55-61) and interleave to the 8*D-bit Morton key
+// (proj/include/zinpaint/morton.hpp:14-29): bit L of dim d -> key bit L*D + D-1-d.
+template <int D>
+__global__ void __launch_bounds__(256) k_quantize(const double* __restrict__ Y,
+                                                  const unsigned long long* __restrict__ minmax,
+                                                  const uint32_t* __restrict__ dict, uint64_t n,
+                                                  uint32_t* __restrict__ keyw, uint32_t* __restrict__ val) {
+    constexpr int W = (D + 3) / 4;
+    __shared__ double s_lo[D], s_hi[D];
+    if (threadIdx.x < D) {
+        s_lo[threadIdx.x] = ordered_to_double_hd(minmax[threadIdx.x]);
+        s_hi[threadIdx.x] = ordered_to_double_hd(minmax[D + threadIdx.x]);
+    }
+    __syncthreads();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        uint32_t kw[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) kw[k] = 0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const uint32_t q = quantize_rn(s_lo[d], s_hi[d], Y[static_cast<size_t>(d) * n + i]);
+#pragma unroll
+            for (int L = 0; L < 8; ++L) {
+                const int u = morton_bit(L, d, D);
+                kw[u >> 5] |= ((q >> L) & 1u) << (u & 31);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < W; ++k) keyw[static_cast<size_t>(k) * n + i] = kw[k];
+        val[i] = dict[i];
+    }
+}
+
+// row-major coords (zcurve_index::from_descriptors input) -> Morton key words
+__global__ void __launch_bounds__(256) k_interleave(const uint8_t* __restrict__ coords,
+                                                    const uint32_t* __restrict__ keys_in, uint64_t n, int D,
+                                                    uint32_t* __restrict__ keyw, uint32_t* __restrict__ val) {
+    const int W = (D + 3) / 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        uint32_t kw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int d = 0; d < D; ++d) {
+            const uint32_t q = coords[i * D + d];
+            for (int L = 0; L < 8; ++L) {
+                const int u = morton_bit(L, d, D);
+                kw[u >> 5] |= ((q >> L) & 1u) << (u & 31);
+            }
+        }
+        for (int k = 0; k < W; ++k) keyw[static_cast<size_t>(k) * n + i] = kw[k];
+        val[i] = keys_in[i];
+    }
+}
+
+// ============================================================== K5: finalize
+// Sorted Morton words -> dim planes (4 dims per u32), keys, and per-256-entry bboxes.
+__global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
+                                                  uint64_t n, int D, uint32_t* __restrict__ planes,
+                                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
+                                                  uint32_t* __restrict__ bmax, uint64_t nblk) {
+    const int W = (D + 3) / 4, P = W;
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
+    const bool ok = i < n;
+    uint32_t kw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (ok) {
+        for (int k = 0; k < W; ++k) kw[k] = keyw[static_cast<size_t>(k) * n + i];
+        keys[i] = val[i];
+    }
+    __shared__ uint32_t s_mn[8][8], s_mx[8][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int p = 0; p < P; ++p) {
+        uint32_t word = 0;
+        for (int b = 0; b < 4; ++b) {
+            const int d = p * 4 + b;
+            if (d >= D) break;
+            uint32_t c = 0;
+            for (int L = 0; L < 8; ++L) {
+                const int u = morton_bit(L, d, D);
+                c |= ((kw[u >> 5] >> (u & 31)) & 1u) << L;
+            }
+            word |= c << (8 * b);
+        }
+        if (ok) planes[static_cast<size_t>(p) * n + i] = word;
+        uint32_t mn = ok ? word : 0xffffffffu, mx = ok ? word : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = __vminu4(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = __vmaxu4(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            s_mn[p][warp] = mn;
+            s_mx[p][warp] = mx;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < P) {
+        const int p = threadIdx.x;
+        uint32_t mn = 0xffffffffu, mx = 0;
+        for (int k = 0; k < 8; ++k) {
+            mn = __vminu4(mn, s_mn[p][k]);
+            mx = __vmaxu4(mx, s_mx[p][k]);
+        }
+        // padding bytes (dims >= D) are zero in both coords and queries
+        bmin[static_cast<size_t>(p) * nblk + blockIdx.x] = mn;
+        bmax[static_cast<size_t>(p) * nblk + blockIdx.x] = mx;
+    }
+}
+
+// ============================================================== host launchers
+template <int D>
+static void launch_project_t(zi_ctx* ctx, const uint8_t* img, int w, int C, const uint32_t* keys, uint64_t n,
+                             const int32_t* off, int m, const double* mean, const double* comp, double* Y) {
+    const size_t smem = static_cast<size_t>(m) * C * D * sizeof(double) + static_cast<size_t>(m) * C * sizeof(double) +
+                        static_cast<size_t>(m) * sizeof(int);
+    static bool attr_set = false;
+    if (!attr_set) {
+        ZI_CUDA(cudaFuncSetAttribute(k_project<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
+    ZI_LAUNCH(ctx, "project", k_project<D>, grid, 256, smem, img, w, C, keys, n, off, m, mean, comp, Y);
+}
+
+template <int D>
+static void launch_quantize_t(zi_ctx* ctx, const double* Y, const unsigned long long* mm, const uint32_t* dict,
+                              uint64_t n, uint32_t* keyw, uint32_t* val) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 16));
+    ZI_LAUNCH(ctx, "quantize_interleave", k_quantize<D>, grid, 256, 0, Y, mm, dict, n, keyw, val);
+}
+
+#define ZI_DIMS_SWITCH(D, FN, ...)                                                        \
+    switch (D) {                                                                          \
+        case 1: FN<1>(__VA_ARGS__); break;   case 2: FN<2>(__VA_ARGS__); break;          \
+        case 3: FN<3>(__VA_ARGS__); break;   case 4: FN<4>(__VA_ARGS__); break;          \
+        case 5: FN<5>(__VA_ARGS__); break;   case 6: FN<6>(__VA_ARGS__); break;          \
+        case 7: FN<7>(__VA_ARGS__); break;   case 8: FN<8>(__VA_ARGS__); break;          \
+        case 9: FN<9>(__VA_ARGS__); break;   case 10: FN<10>(__VA_ARGS__); break;        \
+        case 11: FN<11>(__VA_ARGS__); break; case 12: FN<12>(__VA_ARGS__); break;        \
+        case 13: FN<13>(__VA_ARGS__); break; case 14: FN<14>(__VA_ARGS__); break;        \
+        case 15: FN<15>(__VA_ARGS__); break; case 16: FN<16>(__VA_ARGS__); break;        \
+        case 17: FN<17>(__VA_ARGS__); break; case 18: FN<18>(__VA_ARGS__); break;        \
+        case 19: FN<19>(__VA_ARGS__); break; case 20: FN<20>(__VA_ARGS__); break;        \
+        case 21: FN<21>(__VA_ARGS__); break; case 22: FN<22>(__VA_ARGS__); break;        \
+        case 23: FN<23>(__VA_ARGS__); break; case 24: FN<24>(__VA_ARGS__); break;        \
+        case 25: FN<25>(__VA_ARGS__); break; case 26: FN<26>(__VA_ARGS__); break;        \
+        case 27: FN<27>(__VA_ARGS__); break; case 28: FN<28>(__VA_ARGS__); break;        \
+        case 29: FN<29>(__VA_ARGS__); break; case 30: FN<30>(__VA_ARGS__); break;        \
+        case 31: FN<31>(__VA_ARGS__); break; case 32: FN<32>(__VA_ARGS__); break;        \
+        default: throw error(ZI_E_INVALID, "dims must be in [1, 32]");                   \
+    }
+
+void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_keys, uint64_t n,
+             const int32_t* d_off, int m, const double* d_mean, const double* d_comp, int D, double* d_Y,
+             unsigned long long* d_minmax) {
+    if (n == 0) return;
+    ZI_DIMS_SWITCH(D, launch_project_t, ctx, d_img, w, C, d_keys, n, d_off, m, d_mean, d_comp, d_Y);
+    // lo slots start at the ordered max, hi slots at the ordered min
+    ZI_CUDA(cudaMemsetAsync(d_minmax, 0xff, D * sizeof(unsigned long long), ctx->stream));
+    ZI_CUDA(cudaMemsetAsync(d_minmax + D, 0x00, D * sizeof(unsigned long long), ctx->stream));
+    const unsigned gx = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, std::max(1, ctx->num_sms * 4 / D)));
+    ZI_LAUNCH(ctx, "proj_minmax", k_minmax, dim3(gx, D), 256, 0, d_Y, n, d_minmax, D);
+}
+
+void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax, const uint32_t* d_dict,
+                         uint64_t n, int D, uint32_t* d_keyw, uint32_t* d_val) {
+    if (n == 0) return;
+    ZI_DIMS_SWITCH(D, launch_quantize_t, ctx, d_Y, d_minmax, d_dict, n, d_keyw, d_val);
+}
+
+void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_keys_in, uint64_t n, int D,
+                       uint32_t* d_keyw, uint32_t* d_val) {
+    if (n == 0) return;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 16));
+    ZI_LAUNCH(ctx, "interleave_coords", k_interleave, grid, 256, 0, d_coords, d_keys_in, n, D, d_keyw, d_val);
+}
+
+void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t n, int D, zi_index* idx) {
+    idx->n = n;
+    idx->dims = static_cast<uint32_t>(D);
+    idx->planes_n = static_cast<uint32_t>((D + 3) / 4);
+    idx->nblk = (n + 255) / 256;
+    idx->planes.ensure(static_cast<size_t>(idx->planes_n) * (n ? n : 1));
+    idx->keys.ensure(n ? n : 1);
+    idx->bbox_min.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
+    idx->bbox_max.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
+    if (n == 0) return;
+    ZI_LAUNCH(ctx, "finalize_index", k_finalize, static_cast<unsigned>(idx->nblk), 256, 0, d_keyw, d_val, n, D,
+              idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk);
+}
+
+double ordered_to_double(unsigned long long u) { return ordered_to_double_hd(u); }
+
+}  // namespace zi

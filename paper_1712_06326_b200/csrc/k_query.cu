@@ -1,0 +1,702 @@
+// k_query.cu -- per-iteration query kernels (sm_100a):
+//   K6 query_prep   select_index + make_query   proj/src/engine.cpp:162-176; builder.cpp:110-127
+//   K7 seed         lower_bound in Morton order + window scoring (subinterval analogue,
+//                   proj/src/zcurve.cpp:140-179) -> first k-th bound
+//   K8 knn_scan     bbox-pruned exact scan; prune iff (lb<<32) > bound, the reference's
+//                   prunable() predicate (proj/src/zcurve.cpp:290-292) on packed values
+//   K8b knn_merge   exact top-k in (distance, key) order (knn_list::sorted, zcurve.cpp:51-62)
+//   K9 refine       masked_cost_at over the candidates, min (cost, key)  engine.cpp:197-210, 48-76
+//   K10 brute_force masked cost over the whole dictionary             engine.cpp:220-236
+//
+// Exactness argument: every bound used is the packed (dist,key) value of the k-th element of
+// some SUBSET of the index, so it is >= the true k-th value; an entry is dropped only if it is
+// above such a bound, or if k smaller entries exist in the same CTA buffer.  Packed values are
+// unique (keys are), so the final k smallest are exactly the reference's knn_search result.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace zi {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanCap = 4096;     // CTA candidate buffer (u64)
+constexpr int kMergeThreads = 1024;
+constexpr int kMergeCap = 4096;
+constexpr uint32_t kMaxScanK = 2048;  // above: exhaustive sort path
+
+// device workspace of one query
+struct qws {
+    unsigned long long bound;
+    unsigned long long best;
+    uint32_t q4[8];
+    uint8_t q[32];
+    uint32_t lid;
+    uint32_t count;
+    uint32_t pad[6];
+};
+
+struct index_view {
+    const uint32_t* planes;
+    const uint32_t* keys;
+    const uint32_t* bmin;
+    const uint32_t* bmax;
+    uint64_t n, nblk;
+    int P, D;
+};
+
+// the 8 layout views; kernels after the prep pick views.v[ws->lid] on the device, so the
+// query needs no host round trip between select_index and the scan
+struct views8 {
+    index_view v[8];
+};
+
+__device__ inline void block_bitonic_sort(unsigned long long* a, int n) {
+    for (int size = 2; size <= n; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+                const int i = 2 * stride * (t / stride) + (t % stride);
+                const int j = i + stride;
+                const bool up = (i & size) == 0;
+                const unsigned long long x = a[i], y = a[j];
+                if ((x > y) == up) {
+                    a[i] = y;
+                    a[j] = x;
+                }
+            }
+            __syncthreads();
+        }
+}
+
+__device__ inline int pow2ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+__device__ inline uint32_t entry_byte(const index_view& v, uint64_t i, int d) {
+    return plane_byte(v.planes[static_cast<size_t>(d >> 2) * v.n + i], d);
+}
+
+// morton_less(entry_i, q)  (proj/include/zinpaint/morton.hpp:18-29)
+__device__ inline bool entry_less_query(const index_view& v, uint64_t i, const uint8_t* q) {
+    uint32_t best_diff = 0;
+    int best_dim = 0;
+    for (int d = 0; d < v.D; ++d) {
+        const uint32_t diff = entry_byte(v, i, d) ^ q[d];
+        if (less_msb(best_diff, diff)) {
+            best_diff = diff;
+            best_dim = d;
+        }
+    }
+    return entry_byte(v, i, best_dim) < q[best_dim];
+}
+
+__device__ inline uint32_t entry_dist(const index_view& v, uint64_t i, const uint32_t* q4, int norm) {
+    uint32_t acc = 0;
+    for (int p = 0; p < v.P; ++p) acc = dist4(v.planes[static_cast<size_t>(p) * v.n + i], q4[p], norm, acc);
+    return acc;
+}
+
+// K7: lower_bound of q in Morton order (256-ary search), then score a window of `win`
+// entries around it and take the k-th smallest packed value as the starting bound.
+__device__ void seed_bound(const index_view& v, const uint8_t* s_q, const uint32_t* s_q4, uint32_t k, int norm,
+                           int win, unsigned long long* s_buf, qws* ws) {
+    __shared__ uint64_t s_lo, s_hi;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_lo = 0;
+        s_hi = v.n;
+    }
+    __syncthreads();
+    while (true) {
+        const uint64_t lo = s_lo, hi = s_hi;
+        const uint64_t len = hi - lo;
+        if (len <= static_cast<uint64_t>(blockDim.x)) {
+            const bool less = tid < static_cast<int>(len) && entry_less_query(v, lo + tid, s_q);
+            const int c = __syncthreads_count(less);
+            if (tid == 0) s_lo = lo + c;
+            __syncthreads();
+            break;
+        }
+        const int np = blockDim.x;
+        const uint64_t piv = lo + (static_cast<uint64_t>(tid) + 1) * len / (np + 1);
+        const bool less = entry_less_query(v, piv, s_q);
+        const int c = __syncthreads_count(less);
+        if (tid == 0) {
+            const uint64_t nlo = c > 0 ? lo + static_cast<uint64_t>(c) * len / (np + 1) + 1 : lo;
+            const uint64_t nhi = c < np ? lo + (static_cast<uint64_t>(c) + 1) * len / (np + 1) : hi;
+            s_lo = nlo;
+            s_hi = nhi;
+        }
+        __syncthreads();
+    }
+    const uint64_t pos = s_lo;
+    const uint64_t wn = v.n < static_cast<uint64_t>(win) ? v.n : static_cast<uint64_t>(win);
+    uint64_t start = pos > wn / 2 ? pos - wn / 2 : 0;
+    if (start + wn > v.n) start = v.n - wn;
+    for (int t = tid; t < win; t += blockDim.x) {
+        unsigned long long c = kU64Max;
+        if (static_cast<uint64_t>(t) < wn) {
+            const uint64_t i = start + t;
+            c = pack_candidate(entry_dist(v, i, s_q4, norm), v.keys[i]);
+        }
+        s_buf[t] = c;
+    }
+    __syncthreads();
+    block_bitonic_sort(s_buf, win);
+    if (tid == 0) {
+        ws->bound = (wn >= k && k <= static_cast<uint32_t>(win)) ? s_buf[k - 1] : kU64Max;
+        ws->best = kU64Max;
+        ws->count = 0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_seed_query(index_view v, const uint8_t* __restrict__ query, qws* ws,
+                                                    uint32_t k, int norm, int win) {
+    extern __shared__ unsigned long long s_buf[];
+    __shared__ uint8_t s_q[32];
+    __shared__ uint32_t s_q4[8];
+    if (threadIdx.x < 32) s_q[threadIdx.x] = threadIdx.x < v.D ? query[threadIdx.x] : 0;
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        uint32_t w = 0;
+        for (int b = 0; b < 4; ++b) w |= static_cast<uint32_t>(s_q[threadIdx.x * 4 + b]) << (8 * b);
+        s_q4[threadIdx.x] = w;
+        ws->q4[threadIdx.x] = w;
+    }
+    if (threadIdx.x < 32) ws->q[threadIdx.x] = s_q[threadIdx.x];
+    if (threadIdx.x == 0) ws->lid = 0;
+    __syncthreads();
+    seed_bound(v, s_q, s_q4, k, norm, win, s_buf, ws);
+}
+
+// multi-index: select_index + make_query on the device, then the seed on the chosen layout
+struct mi_view {
+    index_view idx[8];
+    const int32_t* local;  // 8*m  (r*K + c)
+    const double* mean;    // 8*mc
+    const double* comp;    // 8*mc*D  ([layout][j][d])
+    const unsigned long long* minmax;  // 8*2D
+    int m, C, K, D;
+};
+
+__global__ void __launch_bounds__(256) k_query_prep(mi_view mv, const uint8_t* __restrict__ target, qws* ws,
+                                                    uint32_t k, int norm, int win) {
+    extern __shared__ unsigned long long s_buf[];
+    __shared__ int s_ov[8];
+    __shared__ int s_lid;
+    __shared__ uint8_t s_q[32];
+    __shared__ uint32_t s_q4[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int KK = mv.K * mv.K, mc = mv.m * mv.C;
+    const uint8_t* tv = target;
+    const uint8_t* tk = target + static_cast<size_t>(KK) * mv.C;
+    // select_index (proj/src/engine.cpp:162-176): strict '>' from 0, ties -> lowest id
+    if (warp < 8) {
+        int ov = 0;
+        for (int p = lane; p < mv.m; p += 32) ov += tk[mv.local[warp * mv.m + p]] != 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ov += __shfl_xor_sync(0xffffffffu, ov, o);
+        if (lane == 0) s_ov[warp] = ov;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int best = 0, bid = 0;
+        for (int l = 0; l < 8; ++l)
+            if (s_ov[l] > best) {
+                best = s_ov[l];
+                bid = l;
+            }
+        s_lid = bid;
+        ws->lid = static_cast<uint32_t>(bid);
+    }
+    if (tid < 32) s_q[tid] = 0;
+    __syncthreads();
+    const int lid = s_lid;
+    // make_query (proj/src/builder.cpp:110-127) in the build's canonical fp64 order
+    if (tid < mv.D) {
+        const int d = tid;
+        const double* mean = mv.mean + static_cast<size_t>(lid) * mc;
+        const double* comp = mv.comp + static_cast<size_t>(lid) * mc * mv.D;
+        const int32_t* loc = mv.local + lid * mv.m;
+        double y = 0.0;
+        int j = 0;
+        for (int p = 0; p < mv.m; ++p) {
+            const int l = loc[p];
+            const bool known = tk[l] != 0;
+            for (int ch = 0; ch < mv.C; ++ch, ++j) {
+                const double x = known ? static_cast<double>(tv[l * mv.C + ch]) : mean[j];
+                const double xc = __dsub_rn(x, mean[j]);
+                y = __fma_rn(comp[static_cast<size_t>(j) * mv.D + d], xc, y);
+            }
+        }
+        const unsigned long long* mm = mv.minmax + static_cast<size_t>(lid) * 2 * mv.D;
+        s_q[d] = quantize_rn(ordered_to_double_hd(mm[d]), ordered_to_double_hd(mm[mv.D + d]), y);
+    }
+    __syncthreads();
+    if (tid < 8) {
+        uint32_t w = 0;
+        for (int b = 0; b < 4; ++b) w |= static_cast<uint32_t>(s_q[tid * 4 + b]) << (8 * b);
+        s_q4[tid] = w;
+        ws->q4[tid] = w;
+    }
+    if (tid < 32) ws->q[tid] = s_q[tid];
+    __syncthreads();
+    seed_bound(mv.idx[lid], s_q, s_q4, k, norm, win, s_buf, ws);
+}
+
+// keep the <= k smallest of buf[0..cnt) (sorted), tighten the bounds
+__device__ void compact_buffer(unsigned long long* buf, int* s_cnt, unsigned long long* s_bound, uint32_t k,
+                               qws* ws, bool publish) {
+    const int cnt = *s_cnt;
+    if (cnt == 0) return;
+    const int sz = pow2ceil(cnt < 2 ? 2 : cnt);
+    for (int t = cnt + threadIdx.x; t < sz; t += blockDim.x) buf[t] = kU64Max;
+    __syncthreads();
+    block_bitonic_sort(buf, sz);
+    if (threadIdx.x == 0) {
+        int keep = cnt < static_cast<int>(k) ? cnt : static_cast<int>(k);
+        if (cnt >= static_cast<int>(k)) {
+            const unsigned long long kth = buf[k - 1];
+            if (kth < *s_bound) *s_bound = kth;
+            if (publish) atomicMin(&ws->bound, kth);
+        }
+        // entries above the bound can never be in the answer
+        while (keep > 0 && buf[keep - 1] > *s_bound) --keep;
+        *s_cnt = keep;
+    }
+    __syncthreads();
+}
+
+// K8: one CTA = interleaved 256-entry blocks; 8 warps score one block each per round.
+__global__ void __launch_bounds__(kScanThreads) k_knn_scan(views8 V, qws* ws, uint32_t k, int norm,
+                                                           uint32_t* __restrict__ cand_cnt,
+                                                           unsigned long long* __restrict__ cand) {
+    __shared__ unsigned long long s_buf[kScanCap];
+    __shared__ int s_cnt;
+    __shared__ unsigned long long s_bound;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const index_view v = V.v[ws->lid & 7];
+    uint32_t q4[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) q4[p] = ws->q4[p];
+    if (tid == 0) {
+        s_cnt = 0;
+        s_bound = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+    }
+    __syncthreads();
+    const uint64_t G = gridDim.x;
+    const uint64_t rounds = (v.nblk + 8 * G - 1) / (8 * G);
+    for (uint64_t r = 0; r < rounds; ++r) {
+        const uint64_t b = blockIdx.x + (r * 8 + warp) * G;
+        const unsigned long long bound = s_bound;
+        if (b < v.nblk) {
+            uint32_t lb = 0;
+            for (int p = 0; p < v.P; ++p)
+                lb = gap4(q4[p], v.bmin[static_cast<size_t>(p) * v.nblk + b], v.bmax[static_cast<size_t>(p) * v.nblk + b],
+                          norm, lb);
+            if ((static_cast<unsigned long long>(lb) << 32) <= bound) {
+#pragma unroll 2
+                for (int e = 0; e < 8; ++e) {
+                    const uint64_t i = b * 256 + e * 32 + lane;
+                    if (i < v.n) {
+                        uint32_t dist = 0;
+                        for (int p = 0; p < v.P; ++p) dist = dist4(v.planes[static_cast<size_t>(p) * v.n + i], q4[p], norm, dist);
+                        const unsigned long long c = pack_candidate(dist, v.keys[i]);
+                        if (c <= bound) s_buf[atomicAdd(&s_cnt, 1)] = c;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (s_cnt > kScanCap - 8 * 256) {
+            compact_buffer(s_buf, &s_cnt, &s_bound, k, ws, true);
+        } else if (tid == 0) {
+            const unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+            if (g < s_bound) s_bound = g;
+        }
+        __syncthreads();
+    }
+    compact_buffer(s_buf, &s_cnt, &s_bound, k, ws, true);
+    const int cnt = s_cnt;
+    for (int t = tid; t < cnt; t += blockDim.x) cand[static_cast<size_t>(blockIdx.x) * k + t] = s_buf[t];
+    if (tid == 0) cand_cnt[blockIdx.x] = static_cast<uint32_t>(cnt);
+}
+
+// K8b: merge the per-CTA lists into the exact top-k (sorted); out[0..count)
+__global__ void __launch_bounds__(kMergeThreads) k_knn_merge(qws* ws, uint32_t k, int G,
+                                                             const uint32_t* __restrict__ cand_cnt,
+                                                             const unsigned long long* __restrict__ cand,
+                                                             unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long s_buf[kMergeCap];
+    __shared__ uint32_t s_pref[1025];  // G <= 1024 CTA lists
+    __shared__ int s_cnt;
+    __shared__ unsigned long long s_bound;
+    __shared__ uint32_t s_warp[32];
+    const int tid = threadIdx.x;
+    // prefix over the CTA list lengths (G <= 1024)
+    uint32_t carry = 0;
+    for (int base = 0; base < G; base += kMergeThreads) {
+        const int i = base + tid;
+        const uint32_t c = i < G ? cand_cnt[i] : 0;
+        uint32_t x = c;
+        const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t t = s_warp[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            s_warp[lane] = t;
+        }
+        __syncthreads();
+        const uint32_t ex = carry + (warp ? s_warp[warp - 1] : 0) + x - c;
+        if (i < G) s_pref[i] = ex;
+        carry += s_warp[31];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        s_pref[G] = carry;
+        s_cnt = 0;
+        s_bound = ws->bound;
+    }
+    __syncthreads();
+    const uint32_t total = s_pref[G];
+    const int chunk = kMergeCap - static_cast<int>(k);
+    for (uint32_t f0 = 0; f0 < total; f0 += chunk) {
+        const unsigned long long bound = s_bound;
+        for (uint32_t f = f0 + tid; f < f0 + chunk && f < total; f += kMergeThreads) {
+            // owner list of flat index f
+            int lo = 0, hi = G;  // s_pref[lo] <= f < s_pref[hi]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pref[mid] <= f) lo = mid;
+                else hi = mid;
+            }
+            const unsigned long long c = cand[static_cast<size_t>(lo) * k + (f - s_pref[lo])];
+            if (c <= bound) s_buf[atomicAdd(&s_cnt, 1)] = c;
+        }
+        __syncthreads();
+        compact_buffer(s_buf, &s_cnt, &s_bound, k, ws, false);
+    }
+    const int cnt = s_cnt;
+    for (int t = tid; t < cnt; t += kMergeThreads) out[t] = s_buf[t];
+    if (tid == 0) ws->count = static_cast<uint32_t>(cnt);
+}
+
+// K9: refine -- masked_cost_at (proj/src/engine.cpp:48-76) per candidate, warp per candidate,
+// min over packed (cost, key) (engine.cpp:202-209).
+__global__ void __launch_bounds__(1024) k_refine(const uint8_t* __restrict__ img, int w, int C, int K,
+                                                 const uint8_t* __restrict__ target, qws* ws,
+                                                 const unsigned long long* __restrict__ list, int norm) {
+    extern __shared__ uint8_t s_t[];  // tv (K*K*C) then locals (u16)
+    __shared__ int s_nloc;
+    __shared__ unsigned long long s_best;
+    const int KK = K * K;
+    uint16_t* s_loc = reinterpret_cast<uint16_t*>(s_t + ((KK * C + 1) & ~1));
+    for (int i = threadIdx.x; i < KK * C; i += blockDim.x) s_t[i] = target[i];
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int l = 0; l < KK; ++l)
+            if (target[KK * C + l]) s_loc[c++] = static_cast<uint16_t>(l);
+        s_nloc = c;
+        s_best = kU64Max;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const int cnt = static_cast<int>(ws->count);
+    const int nloc = s_nloc;
+    for (int e = warp; e < cnt; e += nwarp) {
+        const uint32_t key = static_cast<uint32_t>(list[e] & 0xffffffffu);
+        const int sx = key & 0xffff, sy = key >> 16;
+        uint32_t acc = 0;
+        for (int li = lane; li < nloc; li += 32) {
+            const int l = s_loc[li];
+            const int ly = l / K, lx = l % K;
+            const uint8_t* s = img + (static_cast<size_t>(sy + ly) * w + sx + lx) * C;
+            const uint8_t* t = s_t + l * C;
+            for (int c = 0; c < C; ++c) {
+                const int d = static_cast<int>(t[c]) - static_cast<int>(__ldg(s + c));
+                acc += norm == 0 ? static_cast<uint32_t>(d * d) : static_cast<uint32_t>(d < 0 ? -d : d);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) atomicMin(&s_best, pack_candidate(acc, key));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) ws->best = s_best;
+}
+
+// K10: exhaustive masked-cost scan over the dictionary (brute_force_best)
+__global__ void __launch_bounds__(256) k_brute(const uint8_t* __restrict__ img, int w, int C, int K,
+                                               const uint32_t* __restrict__ dict, uint64_t n,
+                                               const uint8_t* __restrict__ target, int norm,
+                                               unsigned long long* __restrict__ best) {
+    extern __shared__ uint8_t s_t[];
+    __shared__ int s_nloc;
+    __shared__ unsigned long long s_best;
+    const int KK = K * K;
+    uint16_t* s_loc = reinterpret_cast<uint16_t*>(s_t + ((KK * C + 1) & ~1));
+    for (int i = threadIdx.x; i < KK * C; i += blockDim.x) s_t[i] = target[i];
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int l = 0; l < KK; ++l)
+            if (target[KK * C + l]) s_loc[c++] = static_cast<uint16_t>(l);
+        s_nloc = c;
+        s_best = kU64Max;
+    }
+    __syncthreads();
+    const int nloc = s_nloc;
+    unsigned long long mine = kU64Max;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t key = dict[i];
+        const int sx = key & 0xffff, sy = key >> 16;
+        const uint8_t* base = img + (static_cast<size_t>(sy) * w + sx) * C;
+        uint32_t acc = 0;
+        for (int li = 0; li < nloc; ++li) {
+            const int l = s_loc[li];
+            const int ly = l / K, lx = l % K;
+            const uint8_t* s = base + (static_cast<size_t>(ly) * w + lx) * C;
+            const uint8_t* t = s_t + l * C;
+            for (int c = 0; c < C; ++c) {
+                const int d = static_cast<int>(t[c]) - static_cast<int>(__ldg(s + c));
+                acc += norm == 0 ? static_cast<uint32_t>(d * d) : static_cast<uint32_t>(d < 0 ? -d : d);
+            }
+        }
+        const unsigned long long c = pack_candidate(acc, key);
+        mine = c < mine ? c : mine;
+    }
+    mine = warp_min(mine);
+    if ((threadIdx.x & 31) == 0) atomicMin(&s_best, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMin(best, s_best);
+}
+
+// exhaustive path for k > kMaxScanK: pack every entry, radix-sort the u64 packed values
+__global__ void __launch_bounds__(256) k_pack_all(views8 V, const qws* ws, int norm, uint32_t* __restrict__ lo,
+                                                  uint32_t* __restrict__ hi) {
+    const index_view v = V.v[ws->lid & 7];
+    uint32_t q4[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) q4[p] = ws->q4[p];
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < v.n; i += stride) {
+        lo[i] = v.keys[i];
+        hi[i] = entry_dist(v, i, q4, norm);
+    }
+}
+
+__global__ void k_gather_topk(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, uint32_t cnt,
+                              qws* ws, unsigned long long* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cnt) out[i] = (static_cast<unsigned long long>(hi[i]) << 32) | lo[i];
+    if (i == 0) ws->count = cnt;
+}
+
+// ===================================================================== host side
+void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes);
+
+static index_view view_of(const zi_index* idx) {
+    index_view v;
+    v.planes = idx->planes.p;
+    v.keys = idx->keys.p;
+    v.bmin = idx->bbox_min.p;
+    v.bmax = idx->bbox_max.p;
+    v.n = idx->n;
+    v.nblk = idx->nblk;
+    v.P = static_cast<int>(idx->planes_n);
+    v.D = static_cast<int>(idx->dims);
+    return v;
+}
+
+static int seed_window(uint32_t k) {
+    int w = 256;
+    while (w < static_cast<int>(2 * k) && w < 4096) w <<= 1;
+    return w;
+}
+
+struct query_scratch {
+    qws* ws;
+    uint32_t* cand_cnt;
+    unsigned long long* cand;
+    unsigned long long* out;
+    uint8_t* target;
+    int G;
+};
+
+static query_scratch carve(dbuf<uint8_t>& buf, const zi_ctx* ctx, uint64_t nblk, uint32_t k, size_t target_bytes) {
+    query_scratch s;
+    s.G = static_cast<int>(std::min<uint64_t>(std::min<uint64_t>(std::max<uint64_t>(nblk, 1), static_cast<uint64_t>(ctx->num_sms) * 2), 1024));
+    const size_t kk = std::max<uint32_t>(k, 1);
+    const size_t kscan = std::min<size_t>(kk, kMaxScanK);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = (off + bytes + 255) & ~size_t(255);
+        return o;
+    };
+    const size_t o_ws = take(sizeof(qws));
+    const size_t o_cc = take(s.G * sizeof(uint32_t));
+    const size_t o_c = take(static_cast<size_t>(s.G) * kscan * sizeof(unsigned long long));
+    const size_t o_out = take(kk * sizeof(unsigned long long));
+    const size_t o_t = take(target_bytes + 64);
+    uint8_t* b = buf.ensure(off);
+    s.ws = reinterpret_cast<qws*>(b + o_ws);
+    s.cand_cnt = reinterpret_cast<uint32_t*>(b + o_cc);
+    s.cand = reinterpret_cast<unsigned long long*>(b + o_c);
+    s.out = reinterpret_cast<unsigned long long*>(b + o_out);
+    s.target = b + o_t;
+    return s;
+}
+
+// scan + merge, or the exhaustive sort for very large k; result sorted in s.out, count in ws.
+// The layout actually searched is ws->lid (set by the prep kernel).
+static void run_knn(zi_ctx* ctx, const views8& V, uint64_t n, uint64_t nblk, const query_scratch& s, uint32_t k,
+                    int norm) {
+    (void)nblk;
+    if (k <= kMaxScanK) {
+        ZI_LAUNCH(ctx, "knn_scan", k_knn_scan, s.G, kScanThreads, 0, V, s.ws, k, norm, s.cand_cnt, s.cand);
+        ZI_LAUNCH(ctx, "knn_merge", k_knn_merge, 1, kMergeThreads, 0, s.ws, k, s.G, s.cand_cnt, s.cand, s.out);
+        return;
+    }
+    // exhaustive: sort all n packed values (two-word LSD radix), take the first min(k, n)
+    uint32_t* lohi = ctx->counter.ensure(2 * n + 64);
+    uint32_t* lo = lohi;
+    uint32_t* hi = lohi + n;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
+    ZI_LAUNCH(ctx, "knn_pack_all", k_pack_all, grid, 256, 0, V, s.ws, norm, lo, hi);
+    uint32_t* words[2] = {lo, hi};
+    std::vector<int2> passes;
+    for (int b = 0; b < 4; ++b) passes.push_back(make_int2(0, 8 * b));
+    for (int b = 0; b < 4; ++b) passes.push_back(make_int2(1, 8 * b));
+    radix_sort_words(ctx, words, 2, n, passes);
+    const uint32_t cnt = static_cast<uint32_t>(std::min<uint64_t>(k, n));
+    ZI_LAUNCH(ctx, "knn_gather_topk", k_gather_topk, (cnt + 255) / 256, 256, 0, lo, hi, cnt, s.ws, s.out);
+}
+
+static void ensure_smem_attr() {
+    static bool done = false;
+    if (done) return;
+    ZI_CUDA(cudaFuncSetAttribute(k_seed_query, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8));
+    ZI_CUDA(cudaFuncSetAttribute(k_query_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8));
+    done = true;
+}
+
+uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm, uint64_t* out) {
+    zi_ctx* ctx = idx->ctx;
+    k = std::max<uint32_t>(k, 1);  // knn_list capacity = max(k, 1) (proj/src/zcurve.cpp:25-31)
+    if (idx->n == 0) return 0;
+    ensure_smem_attr();
+    views8 V;
+    for (int l = 0; l < 8; ++l) V.v[l] = view_of(idx);
+    const query_scratch s = carve(idx->qscratch, ctx, idx->nblk, k, 32);
+    uint8_t* stage = idx->hstage.ensure(256);
+    std::memset(stage, 0, 32);
+    std::memcpy(stage, h_query, idx->dims);
+    ZI_CUDA(cudaMemcpyAsync(s.target, stage, 32, cudaMemcpyHostToDevice, ctx->stream));
+    const int win = seed_window(k);
+    ZI_LAUNCH(ctx, "knn_seed", k_seed_query, 1, 256, win * sizeof(unsigned long long), V.v[0], s.target, s.ws, k, norm,
+              win);
+    run_knn(ctx, V, idx->n, idx->nblk, s, k, norm);
+    qws* hq = reinterpret_cast<qws*>(stage + 64);
+    ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint32_t cnt = hq->count;
+    if (cnt) {
+        ZI_CUDA(cudaMemcpyAsync(out, s.out, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return cnt;
+}
+
+void knn_search_batch(zi_index* idx, const uint8_t* h_queries, uint64_t nq, uint32_t k, int norm, uint64_t* out,
+                      uint32_t* counts) {
+    const uint32_t kk = std::max<uint32_t>(k, 1);
+    for (uint64_t q = 0; q < nq; ++q)
+        counts[q] = knn_search(idx, h_queries + q * idx->dims, kk, norm, out + q * kk);
+}
+
+static mi_view mi_view_of(zi_multi_index* mi) {
+    mi_view mv;
+    for (int l = 0; l < 8; ++l) mv.idx[l] = view_of(&mi->L[l].index);
+    mv.local = mi->layout_local.p;
+    mv.mean = mi->pca_mean.p;
+    mv.comp = mi->pca_comp.p;
+    mv.minmax = mi->minmax.p;
+    mv.m = mi->m;
+    mv.C = mi->C;
+    mv.K = mi->K;
+    mv.D = mi->dims;
+    return mv;
+}
+
+query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, uint32_t k, int norm,
+                              uint64_t* knn_out) {
+    zi_ctx* ctx = mi->ctx;
+    k = std::max<uint32_t>(k, 1);
+    ensure_smem_attr();
+    const size_t KK = static_cast<size_t>(mi->K) * mi->K;
+    const size_t tbytes = KK * mi->C + KK;
+    const uint64_t nblk = mi->L[0].index.nblk;
+    const query_scratch s = carve(mi->qscratch, ctx, nblk, k, tbytes);
+    const size_t res_off = (tbytes + 255) & ~size_t(255);
+    uint8_t* stage = mi->hstage.ensure(res_off + sizeof(qws));
+    std::memcpy(stage, h_tv, KK * mi->C);
+    std::memcpy(stage + KK * mi->C, h_tk, KK);
+    ZI_CUDA(cudaMemcpyAsync(s.target, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
+    const mi_view mv = mi_view_of(mi);
+    const int win = seed_window(k);
+    ZI_LAUNCH(ctx, "query_prep", k_query_prep, 1, 256, win * sizeof(unsigned long long), mv, s.target, s.ws, k, norm,
+              win);
+    views8 V;
+    for (int l = 0; l < 8; ++l) V.v[l] = mv.idx[l];
+    run_knn(ctx, V, mi->n, nblk, s, k, norm);
+    const size_t rsmem = ((KK * mi->C + 1) & ~size_t(1)) + KK * sizeof(uint16_t) + 16;
+    ZI_LAUNCH(ctx, "refine", k_refine, 1, 1024, rsmem, mi->image.p, mi->w, mi->C, mi->K, s.target, s.ws, s.out, norm);
+    qws* hq = reinterpret_cast<qws*>(stage + res_off);
+    ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    query_result r;
+    r.best = hq->best;
+    r.lid = hq->lid;
+    r.count = hq->count;
+    if (knn_out && r.count) {
+        ZI_CUDA(cudaMemcpyAsync(knn_out, s.out, r.count * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return r;
+}
+
+uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, int norm) {
+    zi_ctx* ctx = mi->ctx;
+    const size_t KK = static_cast<size_t>(mi->K) * mi->K;
+    const size_t tbytes = KK * mi->C + KK;
+    const query_scratch s = carve(mi->qscratch, ctx, 1, 1, tbytes);
+    const size_t res_off = (tbytes + 255) & ~size_t(255);
+    uint8_t* stage = mi->hstage.ensure(res_off + sizeof(qws));
+    std::memcpy(stage, h_tv, KK * mi->C);
+    std::memcpy(stage + KK * mi->C, h_tk, KK);
+    ZI_CUDA(cudaMemcpyAsync(s.target, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
+    ZI_CUDA(cudaMemsetAsync(&s.ws->best, 0xff, sizeof(unsigned long long), ctx->stream));
+    const size_t smem = ((KK * mi->C + 1) & ~size_t(1)) + KK * sizeof(uint16_t) + 16;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((mi->n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
+    ZI_LAUNCH(ctx, "brute_force", k_brute, grid, 256, smem, mi->image.p, mi->w, mi->C, mi->K, mi->dict.p, mi->n, s.target,
+              norm, &s.ws->best);
+    unsigned long long* hb = reinterpret_cast<unsigned long long*>(stage + res_off);
+    ZI_CUDA(cudaMemcpyAsync(hb, &s.ws->best, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    return *hb;
+}
+
+}  // namespace zi

@@ -1,0 +1,219 @@
+// zi_internal.h -- internal types shared by the host runtime (C++) and the sm_100a kernels.
+// Nothing here crosses the C ABI (include/zinpaint_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "zinpaint_b200.h"
+
+namespace zi {
+
+// Internal exception; converted to a zi_status at the ABI boundary (api.cu).
+struct error : std::runtime_error {
+    zi_status code;
+    error(zi_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define ZI_CUDA(x)                                                                              \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            throw ::zi::error(e_ == cudaErrorMemoryAllocation ? ZI_E_OOM : ZI_E_CUDA,           \
+                              std::string(#x) + ": " + cudaGetErrorString(e_));                 \
+    } while (0)
+
+inline void check_launch(const char* name) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw error(ZI_E_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+}
+
+// Growable device buffer (cudaMalloc'd, never shrinks).
+template <typename T>
+struct dbuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    dbuf() = default;
+    dbuf(const dbuf&) = delete;
+    dbuf& operator=(const dbuf&) = delete;
+    ~dbuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    T* ensure(size_t n) {
+        if (n <= cap && p) return p;
+        release();
+        const size_t bytes = (n ? n : 1) * sizeof(T);
+        ZI_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), bytes));
+        cap = n ? n : 1;
+        return p;
+    }
+};
+
+// Pinned host staging buffer.
+template <typename T>
+struct hbuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    hbuf() = default;
+    hbuf(const hbuf&) = delete;
+    hbuf& operator=(const hbuf&) = delete;
+    ~hbuf() {
+        if (p) cudaFreeHost(p);
+    }
+    T* ensure(size_t n) {
+        if (n <= cap && p) return p;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        ZI_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), (n ? n : 1) * sizeof(T)));
+        cap = n ? n : 1;
+        return p;
+    }
+};
+
+// Per-kernel device timing (CUDA events on the ctx stream), used by bench.py for the
+// roofline's "average launch duration measured live".
+struct prof_slot {
+    const char* name = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+    size_t used = 0;
+    uint64_t launches = 0;
+};
+
+}  // namespace zi
+
+struct zi_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    uint64_t launches = 0;
+    bool profiling = false;
+    std::vector<zi::prof_slot> prof;
+    int num_sms = 148;
+    // shared scratch for sorts / collection
+    zi::dbuf<uint8_t> scratch;
+    zi::dbuf<uint32_t> counter;  // small integer scratch (tile counters etc.)
+};
+
+// One z-curve-sorted index, device resident.
+//   planes : P = ceil(dims/4) uint32 planes of n words; plane p holds dims 4p..4p+3 (dim 4p in
+//            the low byte) of every entry, in Morton order -> coalesced 4-dim loads.
+//   keys   : packed patch keys (y<<16|x), Morton order.
+//   bbox   : per 256-entry block, per-dim min and max bytes, packed the same way as planes.
+struct zi_index {
+    zi_ctx* ctx = nullptr;
+    uint64_t n = 0;
+    uint32_t dims = 0, planes_n = 0, layout_id = 0;
+    uint64_t nblk = 0;
+    zi::dbuf<uint32_t> planes, keys, bbox_min, bbox_max;
+    // query scratch
+    zi::dbuf<uint8_t> qscratch;
+    zi::hbuf<uint8_t> hstage;
+};
+
+struct zi_layout_state {
+    std::vector<int32_t> rc;  // m*2
+    std::vector<double> mean, comp, eig, lo, hi;
+    zi_index index;
+};
+
+struct zi_multi_index {
+    zi_ctx* ctx = nullptr;
+    zi_index_config cfg{};
+    int32_t w = 0, h = 0, C = 1, K = 9, m = 0, mc = 0, F = 0, dims = 0;
+    uint64_t n = 0;
+    double build_ms = 0.0, eigen_s = 0.0, wall_s = 0.0;
+    zi::dbuf<uint8_t> image, known;
+    zi::dbuf<uint32_t> dict;
+    zi::dbuf<int32_t> layout_off;        // 8*m pixel offsets (r*w + c)*C
+    zi::dbuf<int32_t> layout_local;      // 8*m local indices r*K + c
+    zi::dbuf<double> pca_mean, pca_comp; // 8*mc, 8*mc*D ([layout][j][d])
+    zi::dbuf<unsigned long long> minmax; // 8 * 2*D ordered-u64 lo / hi
+    zi::dbuf<unsigned long long> moments;  // F + F*F (s, S)
+    zi::dbuf<double> proj;               // D*n fp64 projections (reused across layouts)
+    zi::dbuf<uint32_t> recs;             // (W+1)*n sort records (Morton words + payload)
+    zi::dbuf<uint8_t> qscratch;          // query scratch
+    zi::hbuf<uint8_t> hstage;            // pinned staging for targets/results
+    zi::hbuf<unsigned long long> hmom;
+    std::vector<int64_t> s, S;           // host copy of the moments
+    zi_layout_state L[8];
+};
+
+namespace zi {
+
+// ---- kernel entry points (implemented in the .cu files) ----
+void launch_begin(zi_ctx* ctx, const char* name);  // counts launches; profiling events
+void launch_end(zi_ctx* ctx, const char* name);
+
+// collect_dictionary on the device: known (w*h) -> keys (row-major); returns n (syncs)
+uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, int K,
+                            dbuf<uint32_t>& keys_out);
+
+// exact moments s (F) and S (F*F, full symmetric) of the K*K*C patch vectors
+void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const uint32_t* d_keys,
+                   uint64_t n, unsigned long long* d_out /* F + F*F */);
+
+// projection pass: Y[d*n + i] fp64 and ordered-u64 lo/hi in minmax (2*D)
+void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_keys, uint64_t n,
+             const int32_t* d_off, int m, const double* d_mean, const double* d_comp, int D,
+             double* d_Y, unsigned long long* d_minmax);
+
+// quantise + Morton interleave -> key words (SoA, W words) + payload = dictionary key
+void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax,
+                         const uint32_t* d_dict, uint64_t n, int D, uint32_t* d_keyw,
+                         uint32_t* d_val);
+// row-major coords (n*D) -> Morton key words + payload copy
+void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_keys_in, uint64_t n,
+                       int D, uint32_t* d_keyw, uint32_t* d_val);
+
+// stable LSD radix sort of (key words, payload) by the D-byte Morton key; when
+// payload_first, 4 leading passes order by the payload (ties of the Morton key -> key order).
+// d_keyw: W*n words (SoA), d_val: n.  Result in place.
+void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first);
+
+// sorted key words + payload -> index planes, keys, bbox
+void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t n, int D,
+                    zi_index* idx);
+
+// decode the ordered-u64 min/max pair of layout `l` into host lo/hi
+double ordered_to_double(unsigned long long u);
+
+// ---- query side ----
+struct query_result {
+    uint64_t best;   // packed (cost<<32 | key)
+    uint32_t lid;
+    uint32_t count;  // number of knn candidates
+};
+// full query_best_patch on the device for the target staged at d_target (K*K*C values then K*K
+// flags); knn list optionally copied out.
+query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk,
+                              uint32_t k, int norm, uint64_t* knn_out);
+uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, int norm);
+// knn over a bare index (zcurve_index + query bytes)
+uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm, uint64_t* out);
+void knn_search_batch(zi_index* idx, const uint8_t* h_queries, uint64_t nq, uint32_t k, int norm,
+                      uint64_t* out, uint32_t* counts);
+
+// ---- host pieces ----
+int subset_pixel_count(int K, double c);
+int subset_layouts(int K, double c, std::vector<int32_t>& rc);  // returns m
+void validate_config(const zi_index_config& cfg, int channels);
+// covariance + eigen-solve + sign rule for one layout (host, deterministic)
+void pca_fit_layout(const std::vector<int64_t>& s, const std::vector<int64_t>& S, int F, uint64_t n,
+                    const std::vector<int32_t>& cols, int dims, std::vector<double>& mean,
+                    std::vector<double>& comp /* dims*mc, row d */, std::vector<double>& eig);
+void build_multi_index(zi_multi_index* mi);
+
+// fill loop (host_engine.cpp): run_loop / inpaint (proj/src/engine.cpp:283-506)
+void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known, const zi_index_config& cfg,
+                 const zi_inpaint_config& icfg, uint8_t* image_out, zi_iteration_record* records, uint64_t cap,
+                 uint64_t* n_records, zi_run_stats* stats);
+
+}  // namespace zi

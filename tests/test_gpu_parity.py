@@ -1,0 +1,418 @@
+"""GPU parity: every sm_100a kernel, through the C ABI, against the CPU oracle / the reference's
+own vectors.  Bit-exact for all integer, byte and index work; the PCA eigen-solve (fp64, the one
+floating-point product whose order is not pinned) is checked by tolerance."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from tests.helpers import fillfront, is_morton_sorted, pca_of
+
+pytestmark = pytest.mark.gpu
+
+L2, L1 = 0, 1
+
+
+# ------------------------------------------------------------------ z-curve index vs the reference
+@pytest.mark.parametrize("kind", ["uniform", "clustered"])
+@pytest.mark.parametrize("D", [4, 8, 10, 16])
+def test_from_descriptors_matches_reference_vectors(zb, golden, kind, D):
+    tag = f"{kind}_D{D}"
+    coords = golden[tag + "__coords"]
+    keys = np.arange(coords.shape[0], dtype=np.uint32)
+    idx = zb.ZCurveIndex.from_descriptors(coords, keys, D)
+    c, k = idx.export()
+    assert np.array_equal(c, golden[tag + "__sorted_coords"])
+    assert np.array_equal(k, golden[tag + "__sorted_keys"])
+
+
+@pytest.mark.parametrize("kind", ["uniform", "clustered"])
+@pytest.mark.parametrize("D", [4, 8, 10, 16])
+def test_knn_matches_reference_vectors(zb, golden, kind, D):
+    tag = f"{kind}_D{D}"
+    coords = golden[tag + "__coords"]
+    idx = zb.ZCurveIndex.from_descriptors(coords, np.arange(coords.shape[0], dtype=np.uint32), D)
+    for norm, nname in ((L2, "l2"), (L1, "l1")):
+        for k in (1, 10, 80):
+            ref = golden[f"{tag}__knn_{nname}_k{k}"]
+            for qi, q in enumerate(golden[tag + "__queries"]):
+                got = idx.knn(q, k, norm=norm)
+                assert np.array_equal(got, ref[qi]), (norm, k, qi)
+
+
+def test_from_descriptors_unsorted_keys(zb):
+    rng = np.random.default_rng(3)
+    n, D = 50000, 6
+    coords = (rng.integers(0, 256, (n, D)) // 16 * 16).astype(np.uint8)  # many ties
+    keys = rng.permutation(np.arange(n, dtype=np.uint32) * 7 + 3).astype(np.uint32)
+    idx = zb.ZCurveIndex.from_descriptors(coords, keys, D)
+    c, k = idx.export()
+    rc, rk = oracle.from_descriptors(coords, keys)
+    assert np.array_equal(c, rc) and np.array_equal(k, rk)
+
+
+@pytest.mark.parametrize("D", [1, 3, 4, 7, 8, 12, 16, 20, 32])
+def test_from_descriptors_all_widths(zb, D):
+    rng = np.random.default_rng(D)
+    n = 9000 + 37 * D
+    coords = rng.integers(0, 256, (n, D)).astype(np.uint8)
+    coords[::3] = coords[::3] // 64 * 64
+    keys = np.arange(n, dtype=np.uint32)
+    c, k = zb.ZCurveIndex.from_descriptors(coords, keys, D).export()
+    rc, rk = oracle.from_descriptors(coords, keys)
+    assert np.array_equal(c, rc) and np.array_equal(k, rk)
+
+
+@pytest.mark.parametrize("D,kind", [(4, "clustered"), (8, "clustered"), (8, "uniform"), (12, "clustered"),
+                                    (16, "uniform")])
+@pytest.mark.parametrize("k", [1, 80, 160, 1000, 3000])
+def test_knn_random_vs_linear_oracle(zb, D, kind, k):
+    rng = np.random.default_rng(100 + D + k)
+    n = 120000
+    if kind == "uniform":
+        coords = rng.integers(0, 256, (n, D)).astype(np.uint8)
+    else:
+        centers = rng.integers(0, 256, (12, D))
+        lab = rng.integers(0, 12, n)
+        coords = np.clip(np.rint(centers[lab] + rng.normal(0, 6, (n, D))), 0, 255).astype(np.uint8)
+    keys = np.arange(n, dtype=np.uint32)
+    idx = zb.ZCurveIndex.from_descriptors(coords, keys, D)
+    sc, sk = idx.export()
+    for t in range(4):
+        q = coords[rng.integers(0, n)] if t % 2 == 0 else rng.integers(0, 256, D).astype(np.uint8)
+        for norm in (L2, L1):
+            got = idx.knn(q, k, norm=norm)
+            ref = oracle.knn_linear(sc, sk, q, k, norm)
+            assert np.array_equal(got, ref), (t, norm)
+
+
+def test_knn_edge_cases(zb):
+    rng = np.random.default_rng(9)
+    coords = rng.integers(0, 256, (37, 5)).astype(np.uint8)
+    keys = np.arange(37, dtype=np.uint32)
+    idx = zb.ZCurveIndex.from_descriptors(coords, keys, 5)
+    q = rng.integers(0, 256, 5).astype(np.uint8)
+    for k in (0, 1, 36, 37, 38, 500):
+        got = idx.knn(q, k)
+        ref = oracle.knn_linear(coords, keys, q, k, L2)
+        assert np.array_equal(got, ref), k
+    # all-identical coordinates: pure key order
+    same = np.full((1000, 4), 77, dtype=np.uint8)
+    idx2 = zb.ZCurveIndex.from_descriptors(same, np.arange(1000, dtype=np.uint32), 4)
+    got = idx2.knn(same[0], 80)
+    assert np.array_equal(got & np.uint64(0xFFFFFFFF), np.arange(80, dtype=np.uint64))
+    # single entry
+    one = zb.ZCurveIndex.from_descriptors(coords[:1], keys[:1], 5)
+    assert np.array_equal(one.knn(q, 10), oracle.knn_linear(coords[:1], keys[:1], q, 10, L2))
+
+
+def test_knn_batch(zb):
+    rng = np.random.default_rng(11)
+    coords = rng.integers(0, 256, (20000, 8)).astype(np.uint8)
+    keys = np.arange(20000, dtype=np.uint32)
+    idx = zb.ZCurveIndex.from_descriptors(coords, keys, 8)
+    sc, sk = idx.export()
+    qs = rng.integers(0, 256, (16, 8)).astype(np.uint8)
+    out, cnt = idx.knn_batch(qs, 40)
+    for i in range(16):
+        assert cnt[i] == 40
+        assert np.array_equal(out[i], oracle.knn_linear(sc, sk, qs[i], 40, L2))
+
+
+def test_binding_knn_search_matches_numpy(zb):
+    """proj/tests/python/test_smoke.py:37-48 protocol against the mirror binding."""
+    rng = np.random.default_rng(0)
+    points = rng.integers(0, 256, size=(5000, 8)).astype(np.uint8)
+    for norm in ("l2", "l1"):
+        for k in (1, 15):
+            query = rng.integers(0, 256, size=8).astype(np.uint8)
+            dist, idx = zb.knn_search(points, query, k=k, norm=norm)
+            diff = points.astype(np.int64) - query.astype(np.int64)
+            ref = (diff ** 2).sum(axis=1) if norm == "l2" else np.abs(diff).sum(axis=1)
+            order = np.lexsort((np.arange(len(points)), ref))[:k]
+            assert np.array_equal(idx, order)
+            assert np.array_equal(dist, ref[order])
+
+
+# ------------------------------------------------------------------ index build
+def _images(golden):
+    out = []
+    for tag, frac_tag in (("eval_64x64_g_s90_m91", True), ("eval_48x40_c_s101_m102", True),
+                          ("eval_60x50_c_s7_m8", True), ("eval_96x80_g_s11_m12", True)):
+        out.append((tag, golden[tag + "__image"].squeeze(-1) if golden[tag + "__image"].shape[-1] == 1
+                    else golden[tag + "__image"], golden[tag + "__known"]))
+    img, kn = workloads.small_image(70, 90, 3, seed=21, hole_frac=0.08)
+    out.append(("small_rgb", img, kn))
+    img, kn = workloads.small_image(64, 64, 1, seed=22, hole_frac=0.12)
+    out.append(("small_gray", img, kn))
+    return out
+
+
+def test_dictionary_collect(zb, golden):
+    for tag, img, kn in _images(golden):
+        for K in (3, 5, 9, 11):
+            mi_dict = oracle.collect_dictionary(kn, K)
+            if mi_dict.size == 0:
+                continue
+            cfg = zb.index_config(patch_size=K, dims=4)
+            mi = zb.MultiIndex(img, kn, cfg)
+            assert np.array_equal(mi.dictionary, mi_dict), (tag, K)
+
+
+def test_empty_dictionary_raises(zb):
+    img = np.zeros((20, 20), np.uint8)
+    with pytest.raises(zb.EmptyDictionaryError):
+        zb.MultiIndex(img, np.zeros((20, 20), np.uint8), zb.index_config(dims=4))
+
+
+def test_moments_exact(zb, golden):
+    for tag, img, kn in _images(golden)[:3]:
+        mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=6))
+        s, S = mi.moments()
+        rs, rS = oracle.patch_moments(img, 9, mi.dictionary)
+        assert np.array_equal(s, rs) and np.array_equal(S, rS), tag
+
+
+def test_pca_matches_oracle_fit(zb, golden):
+    for tag, img, kn in _images(golden)[:4]:
+        mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8))
+        s, S = mi.moments()
+        ch = 1 if img.ndim == 2 else img.shape[2]
+        for l in range(8):
+            lay = mi.layout(l)
+            cols = oracle.layout_columns(lay["pixels"], 9, ch)
+            mean, cov = oracle.layout_covariance(s, S, mi.n, cols)
+            assert np.array_equal(lay["mean"], mean)
+            comp, eig = oracle.pca_from_cov(cov, mi.dims)
+            np.testing.assert_allclose(lay["eigenvalues"], eig, rtol=1e-9, atol=1e-9 * eig[0])
+            # orthonormal, eigen-residual small, and equal to the oracle's where the spectrum is simple
+            C = lay["components"]
+            np.testing.assert_allclose(C @ C.T, np.eye(mi.dims), atol=1e-10)
+            res = cov @ C.T - C.T * lay["eigenvalues"]
+            assert np.abs(res).max() <= 1e-9 * max(1.0, eig[0])
+            gaps = np.abs(np.diff(eig))
+            for d in range(mi.dims):
+                g = min(gaps[d - 1] if d > 0 else np.inf, gaps[d] if d < len(gaps) else np.inf)
+                if g > 1e-6 * eig[0]:
+                    np.testing.assert_allclose(C[d], comp[d], atol=1e-7)
+
+
+def test_build_bitexact_against_oracle(zb, golden):
+    for tag, img, kn in _images(golden):
+        for dims in (4, 8):
+            mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=dims))
+            pm, pc = pca_of(mi)
+            om = oracle.MultiIndex(img, kn, 9, 0.6, dims, pca_mean=pm, pca_comp=pc)
+            for l in range(8):
+                c, k = mi.index_arrays(l)
+                ref = om.index(l)
+                lay = mi.layout(l)
+                assert np.array_equal(lay["lo"], ref.lo) and np.array_equal(lay["hi"], ref.hi), (tag, l)
+                assert np.array_equal(c, ref.coords) and np.array_equal(k, ref.keys), (tag, l)
+
+
+def test_build_tiny_dictionary_shrinks_dims(zb, golden):
+    """A1: D = min(cfg.dims, m*C, n) -- one-patch dictionary gives D = 1 (test_builder.cpp:41-50)."""
+    img = golden["eval_20x20_g_s1__image"][:9, :9, 0].copy()
+    mi = zb.MultiIndex(img, np.ones((9, 9), np.uint8), zb.index_config(patch_size=9, dims=4))
+    assert mi.n == 1 and mi.dims == 1
+
+
+def test_constant_image_ties_in_key_order(zb):
+    """test_builder.cpp:52-63: identical content -> row-major key order."""
+    img = np.full((12, 24), 120, np.uint8)
+    mi = zb.MultiIndex(img, np.ones((12, 24), np.uint8), zb.index_config(patch_size=9, dims=2))
+    for l in range(8):
+        _, k = mi.index_arrays(l)
+        assert (np.diff(k.astype(np.int64)) > 0).all()
+
+
+def test_rebuild_bit_identical(zb, golden):
+    img = golden["eval_32x24_c_s4__image"]
+    kn = np.ones(img.shape[:2], np.uint8)
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9))
+    a = [mi.index_arrays(l) for l in range(8)]
+    la = [mi.layout(l) for l in range(8)]
+    mi.rebuild()
+    for l in range(8):
+        c, k = mi.index_arrays(l)
+        assert np.array_equal(c, a[l][0]) and np.array_equal(k, a[l][1])
+        for f in ("mean", "components", "lo", "hi"):
+            assert np.array_equal(mi.layout(l)[f], la[l][f])
+
+
+# ------------------------------------------------------------------ queries
+def _query_cases(img, kn, stride=3):
+    out = []
+    for i, (x, y) in enumerate(fillfront(kn)):
+        if i % stride == 0:
+            out.append(oracle.extract_patch_clamped(img, kn, x, y, 9))
+    return out
+
+
+@pytest.mark.parametrize("k", [1, 8, 80, 300])
+@pytest.mark.parametrize("norm", [L2, L1])
+def test_query_best_patch_matches_oracle(zb, golden, k, norm):
+    for tag, img, kn in _images(golden)[:4]:
+        mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8, norm=norm))
+        pm, pc = pca_of(mi)
+        om = oracle.MultiIndex(img, kn, 9, 0.6, 8, pca_mean=pm, pca_comp=pc)
+        for tv, tk in _query_cases(img, kn, 5):
+            (key, cost, err, lid, ncand), cands = mi.query_best_patch(tv, tk, k, norm, return_candidates=True)
+            best, rlid, rn, rknn = om.query_best_patch(img, tv, tk, k, norm)
+            assert lid == rlid and ncand == rn, tag
+            assert np.array_equal(cands, rknn), tag
+            assert (cost << 32 | key) == best, tag
+
+
+def test_query_with_k_equal_n_is_brute_force(zb, golden):
+    """test_engine.cpp:210-231: k = dictionary size -> filter+refine == brute force."""
+    img = golden["eval_40x32_g_s84__image"][:, :, 0]
+    kn = np.ones(img.shape, np.uint8)
+    kn[10:18, 22:30] = 0
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8))
+    n = mi.n
+    for tv, tk in _query_cases(img, kn, 3):
+        key, cost, *_ = mi.query_best_patch(tv, tk, n)
+        bkey, bcost, _ = mi.brute_force_best(tv, tk)
+        assert key == bkey and cost == bcost
+
+
+@pytest.mark.parametrize("norm", [L2, L1])
+def test_brute_force_matches_oracle(zb, golden, norm):
+    for tag, img, kn in _images(golden):
+        mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=4))
+        d = mi.dictionary
+        for tv, tk in _query_cases(img, kn, 9):
+            key, cost, _ = mi.brute_force_best(tv, tk, norm)
+            assert (cost << 32 | key) == oracle.brute_force_best(img, tv, tk, 9, d, norm), tag
+
+
+def test_brute_force_exact_match_cost_zero(zb, golden):
+    """test_engine.cpp:258-270"""
+    img = golden["eval_30x30_g_s91__image"][:, :, 0]
+    kn = np.ones((30, 30), np.uint8)
+    kn[20:29, 20:29] = 0
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=4))
+    full = np.ones((30, 30), np.uint8)
+    tv, tk = oracle.extract_patch_clamped(img, full, 6, 6, 9)
+    key, cost, _ = mi.brute_force_best(tv, tk)
+    assert cost == 0 and key == (2 << 16 | 2)
+
+
+# ------------------------------------------------------------------ fill loop end to end
+def _compare_runs(out, recs, rout, rrecs):
+    assert len(recs) == len(rrecs)
+    assert np.array_equal(recs["target_x"], rrecs["tx"]) and np.array_equal(recs["target_y"], rrecs["ty"])
+    assert np.array_equal(recs["source_key"], (rrecs["sy"].astype(np.uint32) << 16) | rrecs["sx"].astype(np.uint32))
+    assert np.array_equal(recs["cost"], rrecs["cost"])
+    assert np.array_equal(out, rout)
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_inpaint_bitexact_against_oracle(zb, golden, case):
+    tag, img, kn = _images(golden)[case]
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8, knn=12))
+    pm, pc = pca_of(mi)
+    out, recs, stats = mi.inpaint(oracle=True, oracle_stride=2)
+    rout, rrecs = oracle.inpaint(img, kn, 9, 0.6, 8, knn=12, oracle=True, oracle_stride=2, pca_mean=pm, pca_comp=pc)
+    _compare_runs(out, recs, rout, rrecs)
+    assert np.array_equal(recs["layout_id"], rrecs["layout_id"])
+    bf = recs["bf_error"]
+    rbf = rrecs["bf_error"]
+    assert np.array_equal(np.isnan(bf), np.isnan(rbf))
+    assert np.array_equal(bf[~np.isnan(bf)], rbf[~np.isnan(rbf)])
+    known = kn != 0
+    assert np.array_equal(out[known], img[known])  # conservation
+
+
+def test_inpaint_brute_force_mode(zb, golden):
+    tag, img, kn = _images(golden)[1]
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8))
+    out, recs, _ = mi.inpaint(brute_force=True)
+    rout, rrecs = oracle.inpaint(img, kn, 9, 0.6, 8, brute_force=True)
+    _compare_runs(out, recs, rout, rrecs)
+
+
+def test_binding_inpaint_roundtrip(zb):
+    """proj/tests/python/test_smoke.py:51-63 + 65-75 protocols on the mirror binding."""
+    rng = np.random.default_rng(3)
+    yy, xx = np.mgrid[0:60, 0:80]
+    base = 120 + 60 * np.sin(0.21 * xx + 0.13 * yy) + 0.2 * xx
+    img = np.stack([base + 10 * c for c in range(3)], axis=-1) + rng.integers(-6, 7, size=(60, 80, 3))
+    img = np.clip(img, 0, 255).astype(np.uint8)
+    mask = np.full((60, 80), 255, dtype=np.uint8)
+    mask[20:24, 10:70] = 0
+    mask[40:43, 5:60] = 0
+    out = zb.inpaint(img, mask, dims=6, knn=8, workers=2)
+    assert out["image"].shape == img.shape
+    known = mask >= 128
+    assert np.array_equal(out["image"][known], img[known])
+    assert out["stats"]["iterations"] == len(out["records"]) > 0
+    g = img[:40, :50, 0].copy()
+    m2 = np.full((40, 50), 255, dtype=np.uint8)
+    m2[15:18, 8:40] = 0
+    o2 = zb.inpaint(g, m2, dims=6, knn=6, workers=1, oracle=True)
+    assert o2["stats"]["mean_ae"] is not None and o2["stats"]["mean_ae"] >= 0.0
+    for rec in o2["records"]:
+        assert rec["bf_error"] is not None and rec["z_error"] >= rec["bf_error"] - 1e-12
+    with pytest.raises(Exception):
+        zb.inpaint(img, np.zeros((10, 10), dtype=np.uint8))
+    with pytest.raises(Exception):
+        zb.inpaint(img, np.zeros((60, 80), dtype=np.uint8))
+
+
+def test_inpaint_degenerate_masks(zb, golden):
+    """test_engine.cpp:337-353"""
+    img = golden["eval_20x20_g_s1__image"][:, :, 0]
+    cfg = zb.index_config(patch_size=9, dims=4)
+    out, recs, _ = zb.inpaint_raw(img, np.ones((20, 20), np.uint8), cfg)
+    assert len(recs) == 0 and np.array_equal(out, img)
+    one = np.ones((20, 20), np.uint8)
+    one[10, 10] = 0
+    out, recs, st = zb.inpaint_raw(img, one, cfg)
+    assert len(recs) == 1 and st.iterations == 1
+
+
+@pytest.mark.slow
+def test_cfg1_end_to_end_bitexact(zb):
+    img, kn, p = workloads.cfg1()
+    cfg = zb.index_config(patch_size=9, dims=8, knn=80)
+    mi = zb.MultiIndex(img, kn, cfg)
+    assert mi.n == int(oracle.collect_dictionary(kn, 9).size) == 58368
+    pm, pc = pca_of(mi)
+    om = oracle.MultiIndex(img, kn, 9, 0.6, 8, pca_mean=pm, pca_comp=pc)
+    for l in range(8):
+        c, k = mi.index_arrays(l)
+        r = om.index(l)
+        assert np.array_equal(c, r.coords) and np.array_equal(k, r.keys)
+    out, recs, _ = mi.inpaint()
+    rout, rrecs = oracle.inpaint(img, kn, 9, 0.6, 8, knn=80, mi=om)
+    _compare_runs(out, recs, rout, rrecs)
+
+
+@pytest.mark.slow
+def test_cfg2_build_properties(zb):
+    """Full-size cfg2 build: permutation, Morton sortedness, lo/hi, and spot knn vs the oracle."""
+    img, kn, p = workloads.cfg2()
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=11, dims=12))
+    d = mi.dictionary
+    assert np.array_equal(d, oracle.collect_dictionary(kn, 11))
+    rng = np.random.default_rng(0)
+    for l in (0, 5):
+        c, k = mi.index_arrays(l)
+        assert np.array_equal(np.sort(k), d)
+        assert is_morton_sorted(c, k)
+        lay = mi.layout(l)
+        sub = rng.choice(len(d), 2000, replace=False)
+        lo, hi, coords, y = oracle.project_build(img, d[sub], lay["pixels"], lay["mean"], lay["components"])
+        assert (y.min(0) >= lay["lo"]).all() and (y.max(0) <= lay["hi"]).all()
+        pos = np.searchsorted(d, d[sub])
+        # quantised bytes of the sampled patches equal the oracle quantiser with the global lo/hi
+        order = np.argsort(k)
+        q = np.array([[oracle.quantize(lay["lo"][j], lay["hi"][j], y[i, j]) for j in range(mi.dims)] for i in range(200)])
+        assert np.array_equal(c[order[pos[:200]]], q)
+        idx = mi.index(l)
+        for t in range(3):
+            qv = c[rng.integers(0, len(k))]
+            assert np.array_equal(idx.knn(qv, 80), oracle.knn_linear(c, k, qv, 80))
