@@ -113,6 +113,8 @@ zi_status zi_ctx_synchronize(zi_ctx* ctx);
 /* device-side timing on the ctx stream (CUDA events), for bench.py */
 zi_status zi_timer_start(zi_ctx* ctx);
 zi_status zi_timer_stop(zi_ctx* ctx, double* ms);
+/* write a 256 MiB scratch buffer on the ctx stream so the next step starts with a cold L2 */
+zi_status zi_ctx_flush_l2(zi_ctx* ctx);
 /* number of kernels this ctx has launched so far (gpu_launches evidence) */
 uint64_t zi_ctx_kernel_launches(const zi_ctx* ctx);
 /* per-kernel device time accumulated while profiling is on (name-indexed, see api.cu) */

@@ -100,6 +100,9 @@ class Context:
         check(lib().zi_timer_stop(self.h, C.byref(ms)))
         return ms.value
 
+    def flush_l2(self):
+        check(lib().zi_ctx_flush_l2(self.h))
+
     @property
     def kernel_launches(self) -> int:
         return int(lib().zi_ctx_kernel_launches(self.h))

@@ -67,6 +67,7 @@ SIGNATURES = {
     "zi_timer_start": (C.c_int, [vp]),
     "zi_timer_stop": (C.c_int, [vp, f64p]),
     "zi_ctx_kernel_launches": (C.c_uint64, [vp]),
+    "zi_ctx_flush_l2": (C.c_int, [vp]),
     "zi_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
     "zi_ctx_profile": (C.c_int, [vp, C.c_int, f64p, u64p, C.POINTER(C.c_char_p)]),
     "zi_less_most_significant_bit": (C.c_int, [C.c_int, C.c_int]),

@@ -181,6 +181,14 @@ zi_status zi_timer_stop(zi_ctx* ctx, double* ms) {
 
 uint64_t zi_ctx_kernel_launches(const zi_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+zi_status zi_ctx_flush_l2(zi_ctx* ctx) {
+    return guard([&] {
+        const size_t bytes = size_t(256) << 20;
+        uint8_t* p = ctx->flush.ensure(bytes);
+        ZI_CUDA(cudaMemsetAsync(p, ctx->flush_toggle++ & 0xff, bytes, ctx->stream));
+    });
+}
+
 zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on) {
     return guard([&] {
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -100,6 +100,8 @@ struct zi_ctx {
     // shared scratch for sorts / collection
     zi::dbuf<uint8_t> scratch;
     zi::dbuf<uint32_t> counter;  // small integer scratch (tile counters etc.)
+    zi::dbuf<uint8_t> flush;     // L2 flush buffer (bench hygiene)
+    int flush_toggle = 1;
 };
 
 // One z-curve-sorted index, device resident.
