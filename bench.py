@@ -180,11 +180,13 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- roofline model
 def algorithmic_bytes(kernel: str, n: int, D: int, mc: int) -> float | None:
-    """Algorithmic HBM bytes per launch; gathered pixels are L1/L2 served."""
+    """Algorithmic HBM bytes per launch; gathered pixels are L1/L2 served.
+    The radix sort runs once over the records of all 8 layouts (N = 8n)."""
     W = (D + 3) // 4
+    N = 8 * n
     return {
-        "radix_onesweep": 2 * 4 * (W + 1) * n,          # read + write of (W key words + payload)
-        "radix_hist": 4 * (W + 1) * n,
+        "radix_onesweep": 2 * 4 * (W + 1) * N,          # read + write of (W key words + payload)
+        "radix_hist": 4 * (W + 1) * N,
         "project": (4 + 8 * D) * n,                     # dictionary key in, fp64 projections out
         "proj_minmax": 8 * D * n,
         "quantize_interleave": (8 * D + 4 + 4 * (W + 1)) * n,

@@ -286,10 +286,10 @@ zi_status zi_index_from_descriptors(zi_ctx* ctx, const uint8_t* coords, const ui
                 uint32_t* val = recs.p + static_cast<size_t>(W) * n;
                 zi::interleave_coords(ctx, dc.p, keys_in, n, static_cast<int>(dims), keyw, val);
                 zi::morton_sort(ctx, keyw, val, n, static_cast<int>(dims), !ascending);
-                zi::finalize_index(ctx, keyw, val, n, static_cast<int>(dims), idx);
+                zi::finalize_index(ctx, keyw, val, n, 0, n, static_cast<int>(dims), nullptr, idx);
                 ZI_CUDA(cudaStreamSynchronize(ctx->stream));
             } else {
-                zi::finalize_index(ctx, nullptr, nullptr, 0, static_cast<int>(dims), idx);
+                zi::finalize_index(ctx, nullptr, nullptr, 0, 0, 0, static_cast<int>(dims), nullptr, idx);
             }
         } catch (...) {
             delete idx;

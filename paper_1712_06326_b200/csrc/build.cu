@@ -85,23 +85,28 @@ void build_multi_index(zi_multi_index* mi) {
     ZI_CUDA(cudaMemcpyAsync(mi->pca_comp.p, hcomp.data(), hcomp.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     mi->minmax.ensure(static_cast<size_t>(8) * 2 * D);
 
-    // per layout: project, lo/hi, quantise + interleave, sort, finalize
+    // per layout: project, lo/hi, quantise + interleave into one 8n-record array; then ONE
+    // radix sort over all layouts (better occupancy than 8 small sorts) and per-layout finalize
     const int W = (D + 3) / 4;
+    const uint64_t N = 8 * n;
+    if (N > (1ull << 30)) throw error(ZI_E_INVALID, "dictionary above 2^27 patches");
     mi->proj.ensure(static_cast<size_t>(D) * n);
     zi::dbuf<uint32_t>& recs = mi->recs;
-    recs.ensure(static_cast<size_t>(W + 1) * n);
+    recs.ensure(static_cast<size_t>(W + 1) * N);
+    uint32_t* keyw = recs.p;
+    uint32_t* val = recs.p + static_cast<size_t>(W) * N;
     for (int l = 0; l < 8; ++l) {
         unsigned long long* mm = mi->minmax.p + static_cast<size_t>(l) * 2 * D;
         project(ctx, mi->image.p, w, C, mi->dict.p, n, mi->layout_off.p + static_cast<size_t>(l) * m, m,
                 mi->pca_mean.p + static_cast<size_t>(l) * mc, mi->pca_comp.p + static_cast<size_t>(l) * mc * D, D,
                 mi->proj.p, mm);
-        uint32_t* keyw = recs.p;
-        uint32_t* val = recs.p + static_cast<size_t>(W) * n;
-        quantize_interleave(ctx, mi->proj.p, mm, mi->dict.p, n, D, keyw, val);
-        morton_sort(ctx, keyw, val, n, D, /*payload_first=*/false);
+        quantize_interleave(ctx, mi->proj.p, mm, n, N, static_cast<uint32_t>(l), D, keyw, val);
+    }
+    morton_sort_layouts(ctx, keyw, val, N, D);
+    for (int l = 0; l < 8; ++l) {
         mi->L[l].index.ctx = ctx;
         mi->L[l].index.layout_id = static_cast<uint32_t>(l);
-        finalize_index(ctx, keyw, val, n, D, &mi->L[l].index);
+        finalize_index(ctx, keyw, val, N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p, &mi->L[l].index);
     }
     std::vector<unsigned long long> hmm(static_cast<size_t>(8) * 2 * D);
     ZI_CUDA(cudaMemcpyAsync(hmm.data(), mi->minmax.p, hmm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,

@@ -70,7 +70,18 @@ void validate_config(const zi_index_config& cfg, int channels) {
 
 namespace {
 
-// Householder reduction A = Q T Q^T (full storage, row-major n x n, destroyed).
+// Dot product with 8 independent partial sums (a fixed, deterministic association that lets
+// the compiler use AVX lanes despite -ffp-contract=off and strict IEEE semantics).
+inline double dot8(const double* a, const double* b, int m) {
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int j = 0;
+    for (; j + 8 <= m; j += 8)
+        for (int t = 0; t < 8; ++t) acc[t] += a[j + t] * b[j + t];
+    for (; j < m; ++j) acc[j & 7] += a[j] * b[j];
+    return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
+// Householder reduction A = Q T Q^T (row-major n x n, lower triangle used, destroyed).
 // Reflector k acts on rows/cols k+1..n-1: H_k = I - tau_k v_k v_k^T.
 struct tridiag {
     int n;
@@ -102,8 +113,7 @@ tridiag householder(std::vector<double>& A, int n) {
         const double alpha = x0 >= 0 ? -std::sqrt(norm2) : std::sqrt(norm2);
         for (int i = 0; i < m; ++i) v[i] = A[static_cast<size_t>(k + 1 + i) * n + k];
         v[0] -= alpha;
-        double vtv = 0.0;
-        for (int i = 0; i < m; ++i) vtv += v[i] * v[i];
+        const double vtv = dot8(v.data(), v.data(), m);
         if (vtv == 0.0) {
             t.e[k] = x0;
             t.tau[k] = 0.0;
@@ -112,41 +122,28 @@ tridiag householder(std::vector<double>& A, int n) {
         const double tau = 2.0 / vtv;
         t.tau[k] = tau;
         t.e[k] = alpha;
-        // p = tau * A22 v
+        // p = tau * A22 v from the lower triangle only: row i contributes its prefix dot
+        // product to p[i] and, transposed, an axpy into p[0..i-1]
         for (int i = 0; i < m; ++i) {
             const double* row = &A[static_cast<size_t>(k + 1 + i) * n + k + 1];
-            double s = 0.0;
-            for (int j = 0; j < m; ++j) s += row[j] * v[j];
-            p[i] = tau * s;
+            p[i] = dot8(row, v.data(), i + 1);
+            const double vi = v[i];
+            for (int j = 0; j < i; ++j) p[j] += row[j] * vi;
         }
-        double vp = 0.0;
-        for (int i = 0; i < m; ++i) vp += v[i] * p[i];
+        for (int i = 0; i < m; ++i) p[i] *= tau;
+        const double vp = dot8(v.data(), p.data(), m);
         const double K2 = 0.5 * tau * vp;
         for (int i = 0; i < m; ++i) w[i] = p[i] - K2 * v[i];
-        // A22 -= v w^T + w v^T
+        // A22 -= v w^T + w v^T  (lower triangle)
         for (int i = 0; i < m; ++i) {
             double* row = &A[static_cast<size_t>(k + 1 + i) * n + k + 1];
             const double vi = v[i], wi = w[i];
-            for (int j = 0; j < m; ++j) row[j] -= vi * w[j] + wi * v[j];
+            for (int j = 0; j <= i; ++j) row[j] -= vi * w[j] + wi * v[j];
         }
     }
     for (int i = 0; i < n; ++i) t.d[i] = A[static_cast<size_t>(i) * n + i];
     if (n >= 2) t.e[n - 2] = A[static_cast<size_t>(n - 1) * n + n - 2];
     return t;
-}
-
-// number of eigenvalues of T strictly below x (Sturm sequence)
-int sturm_count(const tridiag& t, double x, double pivmin) {
-    int cnt = 0;
-    double q = t.d[0] - x;
-    if (std::fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0;
-    for (int i = 1; i < t.n; ++i) {
-        q = t.d[i] - x - t.e[i - 1] * t.e[i - 1] / q;
-        if (std::fabs(q) < pivmin) q = -pivmin;
-        cnt += q < 0;
-    }
-    return cnt;
 }
 
 // solve (T - sigma I) x = b in place (tridiagonal LU with partial pivoting)
@@ -237,20 +234,48 @@ void pca_fit_layout(const std::vector<int64_t>& s, const std::vector<int64_t>& S
     }
     gl -= 2 * eps * safe + pivmin;
     gu += 2 * eps * safe + pivmin;
-    // top-D eigenvalues, descending (index mc-1-j among ascending)
-    std::vector<double> lam(dims);
-    for (int j = 0; j < dims; ++j) {
-        const int target = mc - 1 - j;
-        double lo = gl, hi = gu;
-        for (int it = 0; it < 256; ++it) {
-            const double mid = 0.5 * (lo + hi);
-            if (mid <= lo || mid >= hi) break;
-            if (hi - lo <= 2 * eps * std::max(std::fabs(lo), std::fabs(hi)) + pivmin) break;
-            if (sturm_count(t, mid, pivmin) > target) hi = mid;
-            else lo = mid;
+    // top-D eigenvalues, descending (index mc-1-j among ascending): D independent Sturm
+    // bisections advanced together so the divide chains overlap (identical arithmetic per chain)
+    std::vector<double> lam(dims), blo(dims, gl), bhi(dims, gu), mid(dims), q(dims);
+    std::vector<int> cnt(dims);
+    std::vector<char> active(dims, 1);
+    std::vector<double> e2(mc > 1 ? mc - 1 : 1);
+    for (int i = 0; i + 1 < mc; ++i) e2[i] = t.e[i] * t.e[i];
+    for (int it = 0; it < 256; ++it) {
+        int nact = 0;
+        for (int j = 0; j < dims; ++j) {
+            if (!active[j]) continue;
+            const double lo = blo[j], hi = bhi[j];
+            const double md = 0.5 * (lo + hi);
+            if (md <= lo || md >= hi || hi - lo <= 2 * eps * std::max(std::fabs(lo), std::fabs(hi)) + pivmin) {
+                active[j] = 0;
+                continue;
+            }
+            mid[j] = md;
+            ++nact;
         }
-        lam[j] = 0.5 * (lo + hi);
+        if (nact == 0) break;
+        for (int j = 0; j < dims; ++j) {
+            q[j] = t.d[0] - mid[j];
+            if (std::fabs(q[j]) < pivmin) q[j] = -pivmin;
+            cnt[j] = q[j] < 0;
+        }
+        for (int i = 1; i < mc; ++i) {
+            const double di = t.d[i], ei = e2[i - 1];
+            for (int j = 0; j < dims; ++j) {
+                double v = di - mid[j] - ei / q[j];
+                if (std::fabs(v) < pivmin) v = -pivmin;
+                q[j] = v;
+                cnt[j] += v < 0;
+            }
+        }
+        for (int j = 0; j < dims; ++j) {
+            if (!active[j]) continue;
+            if (cnt[j] > mc - 1 - j) bhi[j] = mid[j];
+            else blo[j] = mid[j];
+        }
     }
+    for (int j = 0; j < dims; ++j) lam[j] = 0.5 * (blo[j] + bhi[j]);
     // inverse iteration, re-orthogonalised inside clusters of close eigenvalues
     const double tiny = eps * safe;
     const double cluster = 1e-3 * safe;
@@ -287,9 +312,7 @@ void pca_fit_layout(const std::vector<int64_t>& s, const std::vector<int64_t>& S
             if (t.tau[k] == 0.0) continue;
             const auto& v = t.v[k];
             const int m = mc - k - 1;
-            double dot = 0.0;
-            for (int i = 0; i < m; ++i) dot += v[i] * x[k + 1 + i];
-            const double f = t.tau[k] * dot;
+            const double f = t.tau[k] * dot8(v.data(), &x[k + 1], m);
             for (int i = 0; i < m; ++i) x[k + 1 + i] -= f * v[i];
         }
         int arg = 0;

@@ -319,11 +319,13 @@ __global__ void __launch_bounds__(256) k_minmax(const double* __restrict__ Y, ui
 
 // quantise (proj/src/builder.cpp:55-61) and interleave to the 8*D-bit Morton key
 // (proj/include/zinpaint/morton.hpp:14-29): bit L of dim d -> key bit L*D + D-1-d.
+// Records of all 8 layouts share one array of N = 8n entries (layout-major); word k of entry
+// e lives at keyw[k*N + e]; the payload is (layout << 29) | dictionary row.
 template <int D>
 __global__ void __launch_bounds__(256) k_quantize(const double* __restrict__ Y,
-                                                  const unsigned long long* __restrict__ minmax,
-                                                  const uint32_t* __restrict__ dict, uint64_t n,
-                                                  uint32_t* __restrict__ keyw, uint32_t* __restrict__ val) {
+                                                  const unsigned long long* __restrict__ minmax, uint64_t n,
+                                                  uint64_t N, uint32_t layout, uint32_t* __restrict__ keyw,
+                                                  uint32_t* __restrict__ val) {
     constexpr int W = (D + 3) / 4;
     __shared__ double s_lo[D], s_hi[D];
     if (threadIdx.x < D) {
@@ -345,9 +347,10 @@ __global__ void __launch_bounds__(256) k_quantize(const double* __restrict__ Y,
                 kw[u >> 5] |= ((q >> L) & 1u) << (u & 31);
             }
         }
+        const uint64_t e = static_cast<uint64_t>(layout) * n + i;
 #pragma unroll
-        for (int k = 0; k < W; ++k) keyw[static_cast<size_t>(k) * n + i] = kw[k];
-        val[i] = dict[i];
+        for (int k = 0; k < W; ++k) keyw[static_cast<size_t>(k) * N + e] = kw[k];
+        val[e] = (layout << 29) | static_cast<uint32_t>(i);
     }
 }
 
@@ -373,8 +376,11 @@ __global__ void __launch_bounds__(256) k_interleave(const uint8_t* __restrict__ 
 
 // ============================================================== K5: finalize
 // Sorted Morton words -> dim planes (4 dims per u32), keys, and per-256-entry bboxes.
+// Entries [off, off+n) of a record array with word stride N; when dict != nullptr the payload
+// is a dictionary row (low 29 bits) and the key is gathered from dict.
 __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
-                                                  uint64_t n, int D, uint32_t* __restrict__ planes,
+                                                  uint64_t N, uint64_t off, uint64_t n, int D,
+                                                  const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
                                                   uint32_t* __restrict__ bmax, uint64_t nblk) {
     const int W = (D + 3) / 4, P = W;
@@ -382,8 +388,9 @@ __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ k
     const bool ok = i < n;
     uint32_t kw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (ok) {
-        for (int k = 0; k < W; ++k) kw[k] = keyw[static_cast<size_t>(k) * n + i];
-        keys[i] = val[i];
+        for (int k = 0; k < W; ++k) kw[k] = keyw[static_cast<size_t>(k) * N + off + i];
+        const uint32_t v = val[off + i];
+        keys[i] = dict ? dict[v & ((1u << 29) - 1u)] : v;
     }
     __shared__ uint32_t s_mn[8][8], s_mx[8][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -441,10 +448,10 @@ static void launch_project_t(zi_ctx* ctx, const uint8_t* img, int w, int C, cons
 }
 
 template <int D>
-static void launch_quantize_t(zi_ctx* ctx, const double* Y, const unsigned long long* mm, const uint32_t* dict,
-                              uint64_t n, uint32_t* keyw, uint32_t* val) {
+static void launch_quantize_t(zi_ctx* ctx, const double* Y, const unsigned long long* mm, uint64_t n, uint64_t N,
+                              uint32_t layout, uint32_t* keyw, uint32_t* val) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 16));
-    ZI_LAUNCH(ctx, "quantize_interleave", k_quantize<D>, grid, 256, 0, Y, mm, dict, n, keyw, val);
+    ZI_LAUNCH(ctx, "quantize_interleave", k_quantize<D>, grid, 256, 0, Y, mm, n, N, layout, keyw, val);
 }
 
 #define ZI_DIMS_SWITCH(D, FN, ...)                                                        \
@@ -480,10 +487,10 @@ void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_
     ZI_LAUNCH(ctx, "proj_minmax", k_minmax, dim3(gx, D), 256, 0, d_Y, n, d_minmax, D);
 }
 
-void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax, const uint32_t* d_dict,
-                         uint64_t n, int D, uint32_t* d_keyw, uint32_t* d_val) {
+void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax, uint64_t n, uint64_t N,
+                         uint32_t layout, int D, uint32_t* d_keyw, uint32_t* d_val) {
     if (n == 0) return;
-    ZI_DIMS_SWITCH(D, launch_quantize_t, ctx, d_Y, d_minmax, d_dict, n, d_keyw, d_val);
+    ZI_DIMS_SWITCH(D, launch_quantize_t, ctx, d_Y, d_minmax, n, N, layout, d_keyw, d_val);
 }
 
 void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_keys_in, uint64_t n, int D,
@@ -493,7 +500,8 @@ void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_k
     ZI_LAUNCH(ctx, "interleave_coords", k_interleave, grid, 256, 0, d_coords, d_keys_in, n, D, d_keyw, d_val);
 }
 
-void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t n, int D, zi_index* idx) {
+void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t off, uint64_t n,
+                    int D, const uint32_t* d_dict, zi_index* idx) {
     idx->n = n;
     idx->dims = static_cast<uint32_t>(D);
     idx->planes_n = static_cast<uint32_t>((D + 3) / 4);
@@ -503,8 +511,8 @@ void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, 
     idx->bbox_min.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
     idx->bbox_max.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
     if (n == 0) return;
-    ZI_LAUNCH(ctx, "finalize_index", k_finalize, static_cast<unsigned>(idx->nblk), 256, 0, d_keyw, d_val, n, D,
-              idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk);
+    ZI_LAUNCH(ctx, "finalize_index", k_finalize, static_cast<unsigned>(idx->nblk), 256, 0, d_keyw, d_val, N, off, n, D,
+              d_dict, idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk);
 }
 
 double ordered_to_double(unsigned long long u) { return ordered_to_double_hd(u); }

@@ -262,4 +262,15 @@ void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int
     radix_sort_words(ctx, words, W + 1, n, passes);
 }
 
+void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D) {
+    const int W = (D + 3) / 4;
+    uint32_t* words[kMaxWords];
+    for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * N;
+    words[W] = d_val;
+    std::vector<int2> passes;
+    for (int p = 0; p < D; ++p) passes.push_back(make_int2(p >> 2, (p & 3) * 8));
+    passes.push_back(make_int2(W, 29));  // layout id (3 bits)
+    radix_sort_words(ctx, words, W + 1, N, passes);
+}
+
 }  // namespace zi

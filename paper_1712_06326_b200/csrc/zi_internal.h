@@ -168,9 +168,9 @@ void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_
              double* d_Y, unsigned long long* d_minmax);
 
 // quantise + Morton interleave -> key words (SoA, W words) + payload = dictionary key
-void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax,
-                         const uint32_t* d_dict, uint64_t n, int D, uint32_t* d_keyw,
-                         uint32_t* d_val);
+// (records of all layouts in one array of N entries; this layout's entries start at layout*n)
+void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax, uint64_t n,
+                         uint64_t N, uint32_t layout, int D, uint32_t* d_keyw, uint32_t* d_val);
 // row-major coords (n*D) -> Morton key words + payload copy
 void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_keys_in, uint64_t n,
                        int D, uint32_t* d_keyw, uint32_t* d_val);
@@ -179,10 +179,13 @@ void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_k
 // payload_first, 4 leading passes order by the payload (ties of the Morton key -> key order).
 // d_keyw: W*n words (SoA), d_val: n.  Result in place.
 void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first);
+// all 8 layouts at once: N = 8n records, Morton passes then one pass on the layout bits of the
+// payload ((layout << 29) | row) -- stable, so each layout segment ends in reference order
+void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D);
 
 // sorted key words + payload -> index planes, keys, bbox
-void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t n, int D,
-                    zi_index* idx);
+void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t off,
+                    uint64_t n, int D, const uint32_t* d_dict, zi_index* idx);
 
 // decode the ordered-u64 min/max pair of layout `l` into host lo/hi
 double ordered_to_double(unsigned long long u);
