@@ -49,7 +49,7 @@ void build_multi_index(zi_multi_index* mi) {
     mi->s.assign(F, 0);
     mi->S.assign(static_cast<size_t>(F) * F, 0);
     for (int i = 0; i < F; ++i) mi->s[i] = static_cast<int64_t>(hm[i]);
-    constexpr int kTile = 64;  // k_moments computes tile pairs ti <= tj only
+    constexpr int kTile = 128;  // k_moments computes tile pairs ti <= tj only
     for (int i = 0; i < F; ++i)
         for (int j = 0; j < F; ++j) {
             const int a = (i / kTile <= j / kTile) ? i : j, b = (i / kTile <= j / kTile) ? j : i;

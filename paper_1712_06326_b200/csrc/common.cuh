@@ -48,6 +48,20 @@ __device__ inline uint8_t quantize_rn(double l, double h, double y) {
     return static_cast<uint8_t>(llround(v));
 }
 
+// Same result as quantize_rn with the IEEE division replaced by a multiply with the rounded
+// reciprocal whenever that provably cannot change llround(): |t*r - t/(h-l)| < 2^-44.5 for
+// quotients below 256, so unless the approximate quotient lies within 8 ulp (2^-41) of a
+// half-integer the rounded integer is the same; otherwise the exact __ddiv_rn is taken.
+__device__ inline uint8_t quantize_fast(double l, double h, double rcp, double y) {
+    if (!(h > l)) return 0;
+    const double c = y < l ? l : (h < y ? h : y);
+    const double t = __dmul_rn(255.0, __dsub_rn(c, l));
+    double v = __dmul_rn(t, rcp);
+    const double f = v - floor(v);
+    if (fabs(f - 0.5) <= 4.547473508864641e-13 /* 2^-41 */) v = __ddiv_rn(t, __dsub_rn(h, l));
+    return static_cast<uint8_t>(llround(v));
+}
+
 // less_most_significant_bit / morton_less (proj/include/zinpaint/morton.hpp:10-29)
 __device__ inline bool less_msb(uint32_t a, uint32_t b) { return (a < b) && (a < (a ^ b)); }
 

@@ -5,6 +5,7 @@
 //   K5 finalize_index       proj/src/zcurve.cpp:127-137 (+ per-block bounding boxes)
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -144,14 +145,24 @@ uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, i
 }
 
 // ============================================================== K2: exact patch moments
-// S = sum_p x_p x_p^T and s = sum_p x_p over the full K*K*C patch vectors (u8), on the
-// integer dot-product path (__dp4a, exact).  One CTA = one 64x64 feature tile pair (ti<=tj) x
-// one chunk of <= 32768 patches (32768 * 255^2 < 2^31 keeps the int32 accumulators exact);
-// chunk partials are added into int64 with atomics (order-free => deterministic).
-constexpr int kMomTile = 64;
-constexpr int kMomBatch = 64;
-constexpr int kMomChunk = 32768;
-constexpr int kMomPitch = kMomBatch + 4;  // bytes per smem row: 17 words -> conflict-free columns
+// S = sum_p x_p x_p^T and s = sum_p x_p over the full K*K*C patch vectors (u8), exact.
+// Tensor cores (mma.sync m16n8k32 u8 x u8 -> s32): the Gram is X^T X with X (patches x F), so
+// both operands are the feature-major gather XT[f][p] staged in shared memory.  One CTA = one
+// 128x128 feature tile pair (ti <= tj) x one chunk of <= 8192 patches (int32 accumulators stay
+// exact: 8192 * 255^2 < 2^31); chunk partials are added into int64 with atomics (order-free =>
+// deterministic).
+constexpr int kMomTile = 128;
+constexpr int kMomBatch = 64;               // patches per smem stage (two k32 MMA steps)
+constexpr int kMomChunk = 8192;
+constexpr int kMomPitch = kMomBatch + 16;   // 80 B rows: 20 words -> conflict-free fragment loads
+
+__device__ inline void mma_u8_16832(int (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
 
 __global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ img, int w, int C, int K, int F,
                                                  const uint32_t* __restrict__ keys, uint64_t n, int ntile,
@@ -161,30 +172,38 @@ __global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ img
     __shared__ __align__(16) uint8_t s_xj[kMomTile * kMomPitch];
     __shared__ int s_base[kMomBatch];
 
-    int p = blockIdx.x, ti = 0;
-    while (p >= ntile - ti) {
-        p -= ntile - ti;
+    int pr = blockIdx.x, ti = 0;
+    while (pr >= ntile - ti) {
+        pr -= ntile - ti;
         ++ti;
     }
-    const int tj = ti + p;
+    const int tj = ti + pr;
     const bool diag = ti == tj;
-    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp >> 2, wn = warp & 3;  // warp tile: rows wm*64..+64, cols wn*32..+32
     if (tid < kMomTile) {
         const int f = ti * kMomTile + tid;
         s_offi[tid] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : -1;
-    } else if (tid < 2 * kMomTile) {
-        const int f = tj * kMomTile + tid - kMomTile;
-        s_offj[tid - kMomTile] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : -1;
+        const int f2 = tj * kMomTile + tid;
+        s_offj[tid] = f2 < F ? (((f2 / C) / K) * w + (f2 / C) % K) * C + f2 % C : -1;
     }
     const uint64_t c0 = static_cast<uint64_t>(blockIdx.y) * kMomChunk;
     const uint64_t c1 = c0 + kMomChunk < n ? c0 + kMomChunk : n;
 
-    uint32_t acc[4][4] = {};
-    uint32_t rs[4] = {};
-    for (uint64_t b = c0; b < c1; b += kMomBatch) {
+    int acc[4][4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[a][b][c] = 0;
+    uint32_t rs = 0;  // row sum of row `tid` (diagonal CTAs, tid < 128)
+
+    for (uint64_t b0 = c0; b0 < c1; b0 += kMomBatch) {
         __syncthreads();
         if (tid < kMomBatch) {
-            const uint64_t idx = b + tid;
+            const uint64_t idx = b0 + tid;
             if (idx < c1) {
                 const uint32_t key = keys[idx];
                 s_base[tid] = static_cast<int>(((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C);
@@ -193,39 +212,67 @@ __global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ img
             }
         }
         __syncthreads();
-        for (int e = tid; e < kMomTile * kMomBatch; e += 256) {
-            const int f = e / kMomBatch, pp = e % kMomBatch;
-            const int bs = s_base[pp];
+        // gather: 2 x 128 rows x 16 groups of 4 patches, packed into u32 smem stores
+        for (int e = tid; e < kMomTile * (kMomBatch / 4); e += 256) {
+            const int f = e >> 4, p4 = (e & 15) * 4;
             const int oi = s_offi[f], oj = s_offj[f];
-            s_xi[f * kMomPitch + pp] = (bs >= 0 && oi >= 0) ? __ldg(img + bs + oi) : 0;
-            s_xj[f * kMomPitch + pp] = (bs >= 0 && oj >= 0) ? __ldg(img + bs + oj) : 0;
+            uint32_t vi = 0, vj = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int bs = s_base[p4 + q];
+                if (bs >= 0) {
+                    if (oi >= 0) vi |= static_cast<uint32_t>(__ldg(img + bs + oi)) << (8 * q);
+                    if (oj >= 0) vj |= static_cast<uint32_t>(__ldg(img + bs + oj)) << (8 * q);
+                }
+            }
+            *reinterpret_cast<uint32_t*>(s_xi + f * kMomPitch + p4) = vi;
+            *reinterpret_cast<uint32_t*>(s_xj + f * kMomPitch + p4) = vj;
         }
         __syncthreads();
-#pragma unroll 4
-        for (int pp = 0; pp < kMomBatch; pp += 4) {
-            uint32_t a[4], bb[4];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const uint32_t*>(s_xi + (ty * 4 + r) * kMomPitch + pp);
+        for (int kk = 0; kk < kMomBatch; kk += 32) {
+            uint32_t af[4][4], bf[4][2];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) bb[c] = *reinterpret_cast<const uint32_t*>(s_xj + (tx * 4 + c) * kMomPitch + pp);
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = __dp4a(a[r], bb[c], acc[r][c]);
-            if (diag && tx == 0) {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) rs[r] = __dp4a(a[r], 0x01010101u, rs[r]);
+            for (int mt = 0; mt < 4; ++mt) {
+                const uint8_t* r0 = s_xi + (wm * 64 + mt * 16 + g) * kMomPitch + kk + 4 * t;
+                const uint8_t* r1 = r0 + 8 * kMomPitch;
+                af[mt][0] = *reinterpret_cast<const uint32_t*>(r0);
+                af[mt][1] = *reinterpret_cast<const uint32_t*>(r1);
+                af[mt][2] = *reinterpret_cast<const uint32_t*>(r0 + 16);
+                af[mt][3] = *reinterpret_cast<const uint32_t*>(r1 + 16);
             }
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const uint8_t* c = s_xj + (wn * 32 + nt * 8 + g) * kMomPitch + kk + 4 * t;
+                bf[nt][0] = *reinterpret_cast<const uint32_t*>(c);
+                bf[nt][1] = *reinterpret_cast<const uint32_t*>(c + 16);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) mma_u8_16832(acc[mt][nt], af[mt], bf[nt]);
+        }
+        if (diag && tid < kMomTile) {
+            const uint8_t* row = s_xi + tid * kMomPitch;
+#pragma unroll
+            for (int q = 0; q < kMomBatch; q += 4) rs = __dp4a(*reinterpret_cast<const uint32_t*>(row + q), 0x01010101u, rs);
         }
     }
-    for (int r = 0; r < 4; ++r) {
-        const int fi = ti * kMomTile + ty * 4 + r;
-        if (fi >= F) continue;
-        for (int c = 0; c < 4; ++c) {
-            const int fj = tj * kMomTile + tx * 4 + c;
-            if (fj < F && acc[r][c]) atomicAdd(out + F + static_cast<size_t>(fi) * F + fj, static_cast<unsigned long long>(acc[r][c]));
-        }
-        if (diag && tx == 0 && rs[r]) atomicAdd(out + fi, static_cast<unsigned long long>(rs[r]));
+    // flush: D fragment (row g / g+8, cols 2t, 2t+1) of every 16x8 tile
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int fi = ti * kMomTile + wm * 64 + mt * 16 + g + (c >> 1) * 8;
+                const int fj = tj * kMomTile + wn * 32 + nt * 8 + 2 * t + (c & 1);
+                const int v = acc[mt][nt][c];
+                if (fi < F && fj < F && v) atomicAdd(out + F + static_cast<size_t>(fi) * F + fj, static_cast<unsigned long long>(static_cast<unsigned>(v)));
+            }
+    if (diag && tid < kMomTile && rs) {
+        const int fi = ti * kMomTile + tid;
+        if (fi < F) atomicAdd(out + fi, static_cast<unsigned long long>(rs));
     }
 }
 
@@ -246,8 +293,25 @@ void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const
 // Y[d*n + i] = sum_j fma(comp[j][d], x_ij - mean_j) in the canonical order (j ascending,
 // starting from +0.0) -- bit-identical to the oracle's restatement of
 // proj/src/builder.cpp:166-167/180-181 (fill_chunk gather order :20-34).
-template <int D>
-__global__ void __launch_bounds__(256) k_project(const uint8_t* __restrict__ img, int w, int C,
+__host__ __device__ constexpr int project_ppt(int D) { return D <= 12 ? 4 : (D <= 24 ? 2 : 1); }
+
+// patches per thread: ZI_PROJECT_PPT overrides the default (1, 2 or 4) for tuning runs
+static int project_ppt_runtime(int D) {
+    static int env = [] {
+        const char* e = std::getenv("ZI_PROJECT_PPT");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (env >= 1 && env <= 4) return env;
+    return project_ppt(D);
+}
+
+// One thread projects PPT patches (i, i+T, ..., T = total threads) so every component row loaded
+// from shared memory feeds PPT*D independent fp64 FMA chains (the LDS pipe, not the FP64 pipe,
+// bounded the one-patch-per-thread version).
+constexpr int kProjThreads = 128;
+
+template <int D, int PPT>
+__global__ void __launch_bounds__(kProjThreads, PPT >= 4 ? 3 : (PPT == 3 ? 4 : 5)) k_project(const uint8_t* __restrict__ img, int w, int C,
                                                  const uint32_t* __restrict__ keys, uint64_t n,
                                                  const int32_t* __restrict__ off, int m,
                                                  const double* __restrict__ mean,
@@ -256,30 +320,62 @@ __global__ void __launch_bounds__(256) k_project(const uint8_t* __restrict__ img
     const int mc = m * C;
     double* s_comp = sm;                 // mc*D  ([j][d])
     double* s_mean = sm + mc * D;        // mc
-    int* s_off = reinterpret_cast<int*>(s_mean + mc);  // m
+    int* s_joff = reinterpret_cast<int*>(s_mean + mc);  // mc: image byte offset of column j
     for (int i = threadIdx.x; i < mc * D; i += blockDim.x) s_comp[i] = comp[i];
-    for (int i = threadIdx.x; i < mc; i += blockDim.x) s_mean[i] = mean[i];
-    for (int i = threadIdx.x; i < m; i += blockDim.x) s_off[i] = off[i];
+    for (int i = threadIdx.x; i < mc; i += blockDim.x) {
+        s_mean[i] = mean[i];
+        s_joff[i] = off[i / C] + i % C;
+    }
     __syncthreads();
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t key = keys[i];
-        const uint8_t* base = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
-        double y[D];
+    const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += T * PPT) {
+        const uint8_t* base[PPT];
+        bool ok[PPT];
 #pragma unroll
-        for (int d = 0; d < D; ++d) y[d] = 0.0;
-        int j = 0;
-        for (int p = 0; p < m; ++p) {
-            const uint8_t* px = base + s_off[p];
-            for (int ch = 0; ch < C; ++ch, ++j) {
-                const double xc = __dsub_rn(static_cast<double>(__ldg(px + ch)), s_mean[j]);
-                const double* cj = s_comp + j * D;
+        for (int k = 0; k < PPT; ++k) {
+            const uint64_t i = i0 + k * T;
+            ok[k] = i < n;
+            const uint32_t key = ok[k] ? keys[i] : 0u;
+            base[k] = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
+        }
+        double y[PPT][D];
 #pragma unroll
-                for (int d = 0; d < D; ++d) y[d] = __fma_rn(cj[d], xc, y[d]);
+        for (int k = 0; k < PPT; ++k)
+#pragma unroll
+            for (int d = 0; d < D; ++d) y[k][d] = 0.0;
+        // software-pipelined gather: the bytes of column j+1 are in flight while column j's
+        // PPT*D FMAs issue
+        uint32_t xn[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) xn[k] = __ldg(base[k] + s_joff[0]);
+        for (int j = 0; j < mc; ++j) {
+            uint32_t xcur[PPT];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) xcur[k] = xn[k];
+            if (j + 1 < mc) {
+                const int o = s_joff[j + 1];
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) xn[k] = __ldg(base[k] + o);
+            }
+            const double mj = s_mean[j];
+            double xc[PPT];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) xc[k] = __dsub_rn(static_cast<double>(xcur[k]), mj);
+            const double* cj = s_comp + j * D;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const double c = cj[d];
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) y[k][d] = __fma_rn(c, xc[k], y[k][d]);
             }
         }
 #pragma unroll
-        for (int d = 0; d < D; ++d) Y[static_cast<size_t>(d) * n + i] = y[d];
+        for (int k = 0; k < PPT; ++k)
+            if (ok[k]) {
+                const uint64_t i = i0 + k * T;
+#pragma unroll
+                for (int d = 0; d < D; ++d) Y[static_cast<size_t>(d) * n + i] = y[k][d];
+            }
     }
 }
 
@@ -327,20 +423,26 @@ __global__ void __launch_bounds__(256) k_quantize(const double* __restrict__ Y,
                                                   uint64_t N, uint32_t layout, uint32_t* __restrict__ keyw,
                                                   uint32_t* __restrict__ val) {
     constexpr int W = (D + 3) / 4;
-    __shared__ double s_lo[D], s_hi[D];
+    __shared__ double s_lo[D], s_hi[D], s_rcp[D];
     if (threadIdx.x < D) {
-        s_lo[threadIdx.x] = ordered_to_double_hd(minmax[threadIdx.x]);
-        s_hi[threadIdx.x] = ordered_to_double_hd(minmax[D + threadIdx.x]);
+        const double l = ordered_to_double_hd(minmax[threadIdx.x]);
+        const double h = ordered_to_double_hd(minmax[D + threadIdx.x]);
+        s_lo[threadIdx.x] = l;
+        s_hi[threadIdx.x] = h;
+        s_rcp[threadIdx.x] = h > l ? __ddiv_rn(1.0, __dsub_rn(h, l)) : 0.0;
     }
     __syncthreads();
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double y[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) y[d] = Y[static_cast<size_t>(d) * n + i];
         uint32_t kw[W];
 #pragma unroll
         for (int k = 0; k < W; ++k) kw[k] = 0;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-            const uint32_t q = quantize_rn(s_lo[d], s_hi[d], Y[static_cast<size_t>(d) * n + i]);
+            const uint32_t q = quantize_fast(s_lo[d], s_hi[d], s_rcp[d], y[d]);
 #pragma unroll
             for (int L = 0; L < 8; ++L) {
                 const int u = morton_bit(L, d, D);
@@ -378,33 +480,39 @@ __global__ void __launch_bounds__(256) k_interleave(const uint8_t* __restrict__ 
 // Sorted Morton words -> dim planes (4 dims per u32), keys, and per-256-entry bboxes.
 // Entries [off, off+n) of a record array with word stride N; when dict != nullptr the payload
 // is a dictionary row (low 29 bits) and the key is gathered from dict.
+template <int D>
 __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
-                                                  uint64_t N, uint64_t off, uint64_t n, int D,
+                                                  uint64_t N, uint64_t off, uint64_t n,
                                                   const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
                                                   uint32_t* __restrict__ bmax, uint64_t nblk) {
-    const int W = (D + 3) / 4, P = W;
+    constexpr int W = (D + 3) / 4, P = W;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
     const bool ok = i < n;
-    uint32_t kw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t kw[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) kw[k] = ok ? keyw[static_cast<size_t>(k) * N + off + i] : 0u;
     if (ok) {
-        for (int k = 0; k < W; ++k) kw[k] = keyw[static_cast<size_t>(k) * N + off + i];
         const uint32_t v = val[off + i];
         keys[i] = dict ? dict[v & ((1u << 29) - 1u)] : v;
     }
-    __shared__ uint32_t s_mn[8][8], s_mx[8][8];
+    __shared__ uint32_t s_mn[P][8], s_mx[P][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
     for (int p = 0; p < P; ++p) {
         uint32_t word = 0;
+#pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int d = p * 4 + b;
-            if (d >= D) break;
-            uint32_t c = 0;
-            for (int L = 0; L < 8; ++L) {
-                const int u = morton_bit(L, d, D);
-                c |= ((kw[u >> 5] >> (u & 31)) & 1u) << L;
+            if (d < D) {
+                uint32_t c = 0;
+#pragma unroll
+                for (int L = 0; L < 8; ++L) {
+                    const int u = morton_bit(L, d, D);
+                    c |= ((kw[u >> 5] >> (u & 31)) & 1u) << L;
+                }
+                word |= c << (8 * b);
             }
-            word |= c << (8 * b);
         }
         if (ok) planes[static_cast<size_t>(p) * n + i] = word;
         uint32_t mn = ok ? word : 0xffffffffu, mx = ok ? word : 0u;
@@ -433,18 +541,31 @@ __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ k
 }
 
 // ============================================================== host launchers
+template <int D, int PPT>
+static void launch_project_ppt(zi_ctx* ctx, const uint8_t* img, int w, int C, const uint32_t* keys, uint64_t n,
+                               const int32_t* off, int m, const double* mean, const double* comp, double* Y) {
+    const size_t smem = static_cast<size_t>(m) * C * D * sizeof(double) + static_cast<size_t>(m) * C * sizeof(double) +
+                        static_cast<size_t>(m) * C * sizeof(int);
+    static bool attr_set = false;
+    if (!attr_set) {
+        ZI_CUDA(cudaFuncSetAttribute(k_project<D, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    const uint64_t threads = (n + PPT - 1) / PPT;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((threads + kProjThreads - 1) / kProjThreads,
+                                                                   static_cast<uint64_t>(ctx->num_sms) * 16));
+    ZI_LAUNCH(ctx, "project", (k_project<D, PPT>), grid, kProjThreads, smem, img, w, C, keys, n, off, m, mean, comp, Y);
+}
+
 template <int D>
 static void launch_project_t(zi_ctx* ctx, const uint8_t* img, int w, int C, const uint32_t* keys, uint64_t n,
                              const int32_t* off, int m, const double* mean, const double* comp, double* Y) {
-    const size_t smem = static_cast<size_t>(m) * C * D * sizeof(double) + static_cast<size_t>(m) * C * sizeof(double) +
-                        static_cast<size_t>(m) * sizeof(int);
-    static bool attr_set = false;
-    if (!attr_set) {
-        ZI_CUDA(cudaFuncSetAttribute(k_project<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
+    switch (project_ppt_runtime(D)) {
+        case 4: launch_project_ppt<D, 4>(ctx, img, w, C, keys, n, off, m, mean, comp, Y); break;
+        case 3: launch_project_ppt<D, 3>(ctx, img, w, C, keys, n, off, m, mean, comp, Y); break;
+        case 2: launch_project_ppt<D, 2>(ctx, img, w, C, keys, n, off, m, mean, comp, Y); break;
+        default: launch_project_ppt<D, 1>(ctx, img, w, C, keys, n, off, m, mean, comp, Y); break;
     }
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
-    ZI_LAUNCH(ctx, "project", k_project<D>, grid, 256, smem, img, w, C, keys, n, off, m, mean, comp, Y);
 }
 
 template <int D>
@@ -475,6 +596,13 @@ static void launch_quantize_t(zi_ctx* ctx, const double* Y, const unsigned long 
         default: throw error(ZI_E_INVALID, "dims must be in [1, 32]");                   \
     }
 
+template <int D>
+static void launch_finalize_t(zi_ctx* ctx, const uint32_t* keyw, const uint32_t* val, uint64_t N, uint64_t off,
+                              uint64_t n, const uint32_t* dict, zi_index* idx) {
+    ZI_LAUNCH(ctx, "finalize_index", k_finalize<D>, static_cast<unsigned>(idx->nblk), 256, 0, keyw, val, N, off, n,
+              dict, idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk);
+}
+
 void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_keys, uint64_t n,
              const int32_t* d_off, int m, const double* d_mean, const double* d_comp, int D, double* d_Y,
              unsigned long long* d_minmax) {
@@ -483,7 +611,7 @@ void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_
     // lo slots start at the ordered max, hi slots at the ordered min
     ZI_CUDA(cudaMemsetAsync(d_minmax, 0xff, D * sizeof(unsigned long long), ctx->stream));
     ZI_CUDA(cudaMemsetAsync(d_minmax + D, 0x00, D * sizeof(unsigned long long), ctx->stream));
-    const unsigned gx = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, std::max(1, ctx->num_sms * 4 / D)));
+    const unsigned gx = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, std::max(1, ctx->num_sms * 16 / D)));
     ZI_LAUNCH(ctx, "proj_minmax", k_minmax, dim3(gx, D), 256, 0, d_Y, n, d_minmax, D);
 }
 
@@ -511,8 +639,7 @@ void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, 
     idx->bbox_min.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
     idx->bbox_max.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
     if (n == 0) return;
-    ZI_LAUNCH(ctx, "finalize_index", k_finalize, static_cast<unsigned>(idx->nblk), 256, 0, d_keyw, d_val, N, off, n, D,
-              d_dict, idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk);
+    ZI_DIMS_SWITCH(D, launch_finalize_t, ctx, d_keyw, d_val, N, off, n, d_dict, idx);
 }
 
 double ordered_to_double(unsigned long long u) { return ordered_to_double_hd(u); }

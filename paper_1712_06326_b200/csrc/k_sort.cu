@@ -66,12 +66,19 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(sort_words io, int dw
     const uint64_t tbase = static_cast<uint64_t>(tile) * kSortTile;
     const uint64_t wbase = tbase + warp * (kSortItems * 32);
 
+    // every word of the tile's records is loaded up front (maximum loads in flight)
+    uint32_t rec[kSortItems][NW];
     uint32_t dig[kSortItems];
     uint32_t rank[kSortItems];
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
         const uint64_t idx = wbase + i * 32 + lane;
-        dig[i] = idx < n ? (io.in[dw][idx] >> ds) & 0xffu : 0x100u;
+        const bool ok = idx < n;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) rec[i][k] = ok ? io.in[k][idx] : 0u;
+        // (a second, L1-hitting load of the digit word: selecting it from rec[] by the runtime
+        // dw makes the compiler spill rec[] to local memory)
+        dig[i] = ok ? (__ldg(io.in[dw] + idx) >> ds) & 0xffu : 0x100u;
     }
     const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
@@ -136,11 +143,10 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(sort_words io, int dw
     // stage records in tile-sorted order
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
-        const uint64_t idx = wbase + i * 32 + lane;
         if (dig[i] < 256u) {
             const uint32_t pos = s_start[dig[i]] + s_hist[warp][dig[i]] + rank[i];
 #pragma unroll
-            for (int k = 0; k < NW; ++k) s_stage[k * kSortTile + pos] = io.in[k][idx];
+            for (int k = 0; k < NW; ++k) s_stage[k * kSortTile + pos] = rec[i][k];
         }
     }
     __syncthreads();
