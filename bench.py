@@ -45,6 +45,10 @@ def parse():
     p.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-inpaint", action="store_true")
+    p.add_argument("--no-knn", action="store_true")
+    p.add_argument("--knn-n", type=int, default=1 << 22, help="cfg5-like dictionary size for the k-NN line")
+    p.add_argument("--knn-dims", type=int, default=16)
+    p.add_argument("--knn-queries", type=int, default=1 << 14)
     return p.parse_args()
 
 
@@ -194,6 +198,49 @@ def algorithmic_bytes(kernel: str, n: int, D: int, mc: int) -> float | None:
     }.get(kernel)
 
 
+def candidate_scoring(zb, ctx, args, hbm_peak):
+    """cfg5-style batched k-NN (the reference's Python knn_search path over u8 descriptors):
+    dictionary sorted on the device, then nq queries answered by the warp-per-query kernel."""
+    import oracle
+    n, D, nq, k = args.knn_n, args.knn_dims, args.knn_queries, 80
+    coords, queries = workloads.cfg5_descriptors(n, D, nq)
+    keys = np.arange(n, dtype=np.uint32)
+    ctx.synchronize()
+    ctx.timer_start()
+    idx = zb.ZCurveIndex.from_descriptors(coords, keys, D, ctx=ctx)
+    sort_ms = ctx.timer_stop()
+    ms, stats, _ = idx.knn_batch_bench(queries, k, reps=3)
+    P = (D + 3) // 4
+    blocks, scored, results = (int(x) for x in stats)
+    alg = scored * (4 * P + 4) + blocks * 8 * P
+    full = n * (4 * P + 4) + (n // 256) * 8 * P
+    line = {"workload": f"cfg5-like: n={n} u8 descriptors D={D} (top-D PCA coords of 0.9^k-decay Gaussians), "
+                        f"{nq} queries with 40% of 125 coords unknown, k={k}, L2",
+            "queries_per_s": nq / (ms * 1e-3), "ms_per_batch": ms,
+            "algorithmic_bytes_per_query": alg / nq, "full_scan_bytes_per_query": full,
+            "touched_fraction": scored / (nq * n),
+            "achieved_GBps": alg / (ms * 1e-3) / 1e9, "frac_of_hbm": alg / (ms * 1e-3) / 1e9 / hbm_peak,
+            "index_bytes": n * (4 * P + 4), "from_descriptors_ms_incl_h2d": sort_ms,
+            "note": "index bytes vs the 126 MB L2 decide whether this is an HBM or an L2 roofline"}
+    # CPU: the reference's own knn_search (compiled zcurve.cpp), sequential, on a query sample
+    if oracle.ref_available():
+        import ctypes as C
+        R = oracle.ref()
+        sc, sk = idx.export()
+        h = R.zr_index_create(sc.ctypes.data_as(C.POINTER(C.c_uint8)), sk.ctypes.data_as(C.POINTER(C.c_uint32)), n, D)
+        ns = 32
+        out = np.zeros(ns * k, dtype=np.uint64)
+        qs = np.ascontiguousarray(queries[:ns])
+        t0 = time.perf_counter()
+        R.zr_index_knn_batch(h, qs.ctypes.data_as(C.POINTER(C.c_uint8)), ns, k, 256, 2048, 0, 1,
+                             out.ctypes.data_as(C.POINTER(C.c_uint64)))
+        dt = time.perf_counter() - t0
+        R.zr_index_free(h)
+        line["cpu_baseline"] = {"value": ns / dt, "unit": "queries/s", "cores": 1, "kind": "reference",
+                                "sample": f"first {ns} queries, sequential knn_search (mu=256)"}
+    return line
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -340,6 +387,13 @@ def main():
         inpaint = {"iterations": int(st.iterations), "seconds": dt, "iterations_per_s": st.iterations / dt,
                    "unit": "iterations/s", "mean_query_us": 1e6 * float(np.mean(recs["elapsed_seconds"]))}
 
+    knn = None
+    if rank == 0 and not args.no_knn:
+        try:
+            knn = candidate_scoring(zb, ctx, args, hbm_peak)
+        except Exception as ex:  # noqa: BLE001
+            knn = {"error": repr(ex)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -360,7 +414,7 @@ def main():
                        "global_batch": n_total, "parallelism": f"replicas x{world} (independent images)",
                        "l2": "flushed (256 MiB write) before every timed step"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk, "inpaint": inpaint,
+            "clocks": clk, "inpaint": inpaint, "candidate_scoring": knn,
             "breakdown": {"host_eigen_s_per_step": float(np.mean(host_eigen)), "kernels": breakdown},
         }
         print(json.dumps(line), flush=True)

@@ -148,6 +148,14 @@ zi_status zi_knn_search(zi_index* idx, const uint8_t* query, uint32_t k, uint32_
 zi_status zi_knn_search_batch(zi_index* idx, const uint8_t* queries, uint64_t nq, uint32_t k,
                               int32_t norm, uint64_t* packed_out, uint32_t* counts_out);
 
+/* timed device-resident batch (bench helper): queries uploaded once, `reps` launches timed with
+ * CUDA events; ms_per_batch = mean device time of one launch over nq queries; stats3 (optional)
+ * = {bbox tests, entries scored, results} of one launch.  Results of the last launch are copied
+ * to packed_out / counts_out when non-NULL. */
+zi_status zi_knn_batch_bench(zi_index* idx, const uint8_t* queries, uint64_t nq, uint32_t k, int32_t norm,
+                             int32_t reps, double* ms_per_batch, uint64_t* stats3, uint64_t* packed_out,
+                             uint32_t* counts_out);
+
 /* ---- dictionary: collect_dictionary (builder.hpp:52-55, builder.cpp:74-108) ---- */
 zi_status zi_dictionary_collect(zi_ctx* ctx, const uint8_t* known, int32_t width, int32_t height,
                                 int32_t patch_size, uint32_t* keys_out, uint64_t cap, uint64_t* n_out);

@@ -189,6 +189,19 @@ class ZCurveIndex:
         check(lib().zi_knn_search_batch(self.h, ptr(q, u8p), nq, k, _norm(norm), ptr(out, u64p), ptr(cnt, u32p)))
         return out, cnt
 
+    def knn_batch_bench(self, queries, k: int, norm="l2", reps: int = 5, return_results: bool = False):
+        """Device-resident batched k-NN timed with CUDA events -> (ms per batch, stats[3], results)."""
+        q = _u8(queries)
+        nq = q.shape[0]
+        ms = C.c_double()
+        stats = np.zeros(3, dtype=np.uint64)
+        out = np.zeros((nq, k), dtype=np.uint64) if return_results else None
+        cnt = np.zeros(nq, dtype=np.uint32) if return_results else None
+        check(lib().zi_knn_batch_bench(self.h, ptr(q, u8p), nq, k, _norm(norm), reps, C.byref(ms), ptr(stats, u64p),
+                                       ptr(out, u64p) if out is not None else None,
+                                       ptr(cnt, u32p) if cnt is not None else None))
+        return ms.value, stats, (out, cnt)
+
     def __del__(self):
         h = getattr(self, "h", None)
         if h and self._owner is None:

@@ -82,6 +82,8 @@ SIGNATURES = {
     "zi_index_export": (C.c_int, [vp, u8p, u32p]),
     "zi_knn_search": (C.c_int, [vp, u8p, C.c_uint32, C.c_uint32, C.c_int32, u64p, C.POINTER(C.c_uint32)]),
     "zi_knn_search_batch": (C.c_int, [vp, u8p, C.c_uint64, C.c_uint32, C.c_int32, u64p, C.POINTER(C.c_uint32)]),
+    "zi_knn_batch_bench": (C.c_int, [vp, u8p, C.c_uint64, C.c_uint32, C.c_int32, C.c_int32, f64p, u64p, u64p,
+                                     C.POINTER(C.c_uint32)]),
     "zi_dictionary_collect": (C.c_int, [vp, u8p, C.c_int32, C.c_int32, C.c_int32, u32p, C.c_uint64, u64p]),
     "zi_multi_index_build": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig),
                                        C.POINTER(vp)]),

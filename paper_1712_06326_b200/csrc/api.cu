@@ -351,6 +351,45 @@ zi_status zi_knn_search_batch(zi_index* idx, const uint8_t* queries, uint64_t nq
     });
 }
 
+zi_status zi_knn_batch_bench(zi_index* idx, const uint8_t* queries, uint64_t nq, uint32_t k, int32_t norm, int32_t reps,
+                             double* ms_per_batch, uint64_t* stats3, uint64_t* packed_out, uint32_t* counts_out) {
+    return guard([&] {
+        require(idx && queries && ms_per_batch && nq > 0 && reps > 0, "bad argument");
+        require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
+        require(k >= 1 && k <= 256, "batch bench supports 1 <= k <= 256");
+        zi_ctx* ctx = idx->ctx;
+        zi::dbuf<uint8_t> dq;
+        zi::dbuf<unsigned long long> dout, dstats;
+        zi::dbuf<uint32_t> dcnt;
+        dq.ensure(nq * idx->dims);
+        dout.ensure(nq * k);
+        dcnt.ensure(nq);
+        dstats.ensure(4);
+        ZI_CUDA(cudaMemcpyAsync(dq.p, queries, nq * idx->dims, cudaMemcpyHostToDevice, ctx->stream));
+        zi::knn_batch_device(ctx, idx, dq.p, nq, k, norm, dout.p, dcnt.p, nullptr);  // warm-up
+        ZI_CUDA(cudaMemsetAsync(dstats.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
+        cudaEvent_t e0, e1;
+        ZI_CUDA(cudaEventCreate(&e0));
+        ZI_CUDA(cudaEventCreate(&e1));
+        float total = 0.f;
+        for (int r = 0; r < reps; ++r) {
+            ZI_CUDA(cudaEventRecord(e0, ctx->stream));
+            zi::knn_batch_device(ctx, idx, dq.p, nq, k, norm, dout.p, dcnt.p, r == 0 ? dstats.p : nullptr);
+            ZI_CUDA(cudaEventRecord(e1, ctx->stream));
+            ZI_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            ZI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            total += ms;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_per_batch = total / reps;
+        if (stats3) ZI_CUDA(cudaMemcpy(stats3, dstats.p, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        if (packed_out) ZI_CUDA(cudaMemcpy(packed_out, dout.p, nq * k * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        if (counts_out) ZI_CUDA(cudaMemcpy(counts_out, dcnt.p, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    });
+}
+
 // ---------------------------------------------------------------- dictionary
 zi_status zi_dictionary_collect(zi_ctx* ctx, const uint8_t* known, int32_t w, int32_t h, int32_t K, uint32_t* keys_out,
                                 uint64_t cap, uint64_t* n_out) {

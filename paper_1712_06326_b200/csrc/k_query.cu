@@ -98,6 +98,31 @@ __device__ inline uint32_t entry_dist(const index_view& v, uint64_t i, const uin
     return acc;
 }
 
+// Packed (dist<<32 | key) of the 8 entries lane, lane+32, ..., lane+224 of 256-entry block b;
+// all 8*(P+1) loads are issued before any arithmetic (P = dim planes, a compile-time constant).
+template <int P>
+__device__ inline void score_block(const index_view& v, uint64_t b, const uint32_t (&q4)[8], int norm,
+                                   unsigned long long (&c)[8]) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t base = b * 256 + lane;
+    uint32_t w[8][P], kk[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const uint64_t i = base + e * 32;
+        const bool ok = i < v.n;
+#pragma unroll
+        for (int p = 0; p < P; ++p) w[e][p] = ok ? __ldg(v.planes + static_cast<size_t>(p) * v.n + i) : 0u;
+        kk[e] = ok ? __ldg(v.keys + i) : 0u;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        uint32_t dist = 0;
+#pragma unroll
+        for (int p = 0; p < P; ++p) dist = dist4(w[e][p], q4[p], norm, dist);
+        c[e] = base + e * 32 < v.n ? pack_candidate(dist, kk[e]) : kU64Max;
+    }
+}
+
 // K7: lower_bound of q in Morton order (256-ary search), then score a window of `win`
 // entries around it and take the k-th smallest packed value as the starting bound.
 __device__ void seed_bound(const index_view& v, const uint8_t* s_q, const uint32_t* s_q4, uint32_t k, int norm,
@@ -270,6 +295,7 @@ __device__ void compact_buffer(unsigned long long* buf, int* s_cnt, unsigned lon
 }
 
 // K8: one CTA = interleaved 256-entry blocks; 8 warps score one block each per round.
+template <int P>
 __global__ void __launch_bounds__(kScanThreads) k_knn_scan(views8 V, qws* ws, uint32_t k, int norm,
                                                            uint32_t* __restrict__ cand_cnt,
                                                            unsigned long long* __restrict__ cand) {
@@ -293,21 +319,18 @@ __global__ void __launch_bounds__(kScanThreads) k_knn_scan(views8 V, qws* ws, ui
         const unsigned long long bound = s_bound;
         if (b < v.nblk) {
             uint32_t lb = 0;
-            for (int p = 0; p < v.P; ++p)
+#pragma unroll
+            for (int p = 0; p < P; ++p)
                 lb = gap4(q4[p], v.bmin[static_cast<size_t>(p) * v.nblk + b], v.bmax[static_cast<size_t>(p) * v.nblk + b],
                           norm, lb);
             if ((static_cast<unsigned long long>(lb) << 32) <= bound) {
-#pragma unroll 2
-                for (int e = 0; e < 8; ++e) {
-                    const uint64_t i = b * 256 + e * 32 + lane;
-                    if (i < v.n) {
-                        uint32_t dist = 0;
-                        for (int p = 0; p < v.P; ++p) dist = dist4(v.planes[static_cast<size_t>(p) * v.n + i], q4[p], norm, dist);
-                        const unsigned long long c = pack_candidate(dist, v.keys[i]);
-                        if (c <= bound) s_buf[atomicAdd(&s_cnt, 1)] = c;
-                    }
-                }
+                unsigned long long c[8];
+                score_block<P>(v, b, q4, norm, c);
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (c[e] != kU64Max && c[e] <= bound) s_buf[atomicAdd(&s_cnt, 1)] = c[e];
             }
+            (void)lane;
         }
         __syncthreads();
         if (s_cnt > kScanCap - 8 * 256) {
@@ -504,6 +527,160 @@ __global__ void k_gather_topk(const uint32_t* __restrict__ lo, const uint32_t* _
     if (i == 0) ws->count = cnt;
 }
 
+// ===================================================================== batched k-NN (warp per query)
+// cfg-5 style throughput path: one warp answers one query end to end -- 32-ary Morton
+// lower_bound, a seed window for the first k-th bound, then every 256-entry block visited in
+// outward order from the seed block (32 bboxes per warp step, pruned iff (lb<<32) > bound),
+// candidates <= bound appended to a private shared-memory buffer that is sorted and cut to k
+// when it fills.  Same exactness argument as the multi-CTA scan.
+constexpr int kWarpBuf = 1024;     // u64 candidates per warp
+constexpr uint32_t kWarpMaxK = 256;
+constexpr int kBatchWarps = 4;
+
+__device__ inline void warp_bitonic_sort(unsigned long long* a, int n) {
+    const int lane = threadIdx.x & 31;
+    for (int size = 2; size <= n; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = lane; t < (n >> 1); t += 32) {
+                const int i = 2 * stride * (t / stride) + (t % stride);
+                const int j = i + stride;
+                const bool up = (i & size) == 0;
+                const unsigned long long x = a[i], y = a[j];
+                if ((x > y) == up) {
+                    a[i] = y;
+                    a[j] = x;
+                }
+            }
+            __syncwarp();
+        }
+}
+
+// sort buf[0..cnt), keep the k smallest that are <= bound; returns the new count and tightens bound
+__device__ inline int warp_compact(unsigned long long* buf, int cnt, uint32_t k, unsigned long long& bound) {
+    const int lane = threadIdx.x & 31;
+    if (cnt == 0) return 0;
+    int sz = 32;
+    while (sz < cnt) sz <<= 1;
+    for (int t = cnt + lane; t < sz; t += 32) buf[t] = kU64Max;
+    __syncwarp();
+    warp_bitonic_sort(buf, sz);
+    if (cnt >= static_cast<int>(k)) {
+        const unsigned long long kth = buf[k - 1];
+        if (kth < bound) bound = kth;
+        cnt = static_cast<int>(k);
+    }
+    while (cnt > 0 && buf[cnt - 1] > bound) --cnt;  // warp-uniform
+    return cnt;
+}
+
+__device__ inline int64_t outward_block(int64_t b0, int64_t v, int64_t nblk) {
+    const int64_t b = (v & 1) ? b0 - (v + 1) / 2 : b0 + v / 2;
+    return (b >= 0 && b < nblk) ? b : -1;
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * kBatchWarps) k_knn_batch(index_view v, const uint8_t* __restrict__ queries,
+                                                               uint64_t nq, uint32_t k, int norm, int win,
+                                                               unsigned long long* __restrict__ out,
+                                                               uint32_t* __restrict__ counts,
+                                                               unsigned long long* __restrict__ stats) {
+    __shared__ unsigned long long s_buf[kBatchWarps][kWarpBuf];
+    __shared__ uint8_t s_q[kBatchWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long* buf = s_buf[warp];
+    uint8_t* q = s_q[warp];
+    unsigned long long st_blocks = 0, st_scored = 0, st_cand = 0;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (uint64_t qi = static_cast<uint64_t>(blockIdx.x) * kBatchWarps + warp; qi < nq;
+         qi += static_cast<uint64_t>(gridDim.x) * kBatchWarps) {
+        q[lane] = lane < v.D ? queries[qi * v.D + lane] : 0;
+        __syncwarp();
+        uint32_t q4[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+            q4[p] = static_cast<uint32_t>(q[4 * p]) | (static_cast<uint32_t>(q[4 * p + 1]) << 8) |
+                    (static_cast<uint32_t>(q[4 * p + 2]) << 16) | (static_cast<uint32_t>(q[4 * p + 3]) << 24);
+        // 32-ary lower_bound in Morton order; invariant: position in [lo, hi]
+        uint64_t lo = 0, hi = v.n;
+        while (hi - lo > 32) {
+            const uint64_t len = hi - lo;
+            const uint64_t piv = lo + (static_cast<uint64_t>(lane) + 1) * len / 33;
+            const int c = __popc(__ballot_sync(0xffffffffu, entry_less_query(v, piv, q)));
+            const uint64_t nlo = c > 0 ? lo + static_cast<uint64_t>(c) * len / 33 + 1 : lo;
+            const uint64_t nhi = c < 32 ? lo + (static_cast<uint64_t>(c) + 1) * len / 33 : hi;
+            lo = nlo;
+            hi = nhi;
+        }
+        {
+            const bool less = lo + lane < hi && entry_less_query(v, lo + lane, q);
+            lo += __popc(__ballot_sync(0xffffffffu, less));
+        }
+        const uint64_t pos = lo;
+        // seed window -> first bound
+        unsigned long long bound = kU64Max;
+        {
+            const uint64_t wn = v.n < static_cast<uint64_t>(win) ? v.n : static_cast<uint64_t>(win);
+            uint64_t start = pos > wn / 2 ? pos - wn / 2 : 0;
+            if (start + wn > v.n) start = v.n - wn;
+            for (int t = lane; t < win; t += 32)
+                buf[t] = static_cast<uint64_t>(t) < wn
+                             ? pack_candidate(entry_dist(v, start + t, q4, norm), v.keys[start + t])
+                             : kU64Max;
+            __syncwarp();
+            warp_bitonic_sort(buf, win);
+            if (wn >= k) bound = buf[k - 1];
+            __syncwarp();
+        }
+        // outward scan over all blocks
+        int cnt = 0;
+        const int64_t nblk = static_cast<int64_t>(v.nblk);
+        const int64_t b0 = static_cast<int64_t>(pos / 256 < v.nblk ? pos / 256 : v.nblk - 1);
+        const int64_t span = 2 * (b0 + 1 > nblk - b0 ? b0 + 1 : nblk - b0);
+        for (int64_t vb = 0; vb < span; vb += 32) {
+            const int64_t b = outward_block(b0, vb + lane, nblk);
+            uint32_t lb = 0xffffffffu;
+            if (b >= 0) {
+                lb = 0;
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    lb = gap4(q4[p], v.bmin[static_cast<size_t>(p) * v.nblk + b], v.bmax[static_cast<size_t>(p) * v.nblk + b],
+                              norm, lb);
+                ++st_blocks;
+            }
+            unsigned live = __ballot_sync(0xffffffffu, b >= 0 && (static_cast<unsigned long long>(lb) << 32) <= bound);
+            while (live) {
+                const int src = __ffs(live) - 1;
+                live &= live - 1;
+                const int64_t bb = __shfl_sync(0xffffffffu, b, src);
+                const uint32_t blb = __shfl_sync(0xffffffffu, lb, src);
+                if ((static_cast<unsigned long long>(blb) << 32) > bound) continue;  // bound tightened meanwhile
+                if (cnt > kWarpBuf - 256) cnt = warp_compact(buf, cnt, k, bound);
+                unsigned long long c[8];
+                score_block<P>(v, static_cast<uint64_t>(bb), q4, norm, c);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const bool take = c[e] != kU64Max && c[e] <= bound;
+                    st_scored += c[e] != kU64Max;
+                    const unsigned m = __ballot_sync(0xffffffffu, take);
+                    if (take) buf[cnt + __popc(m & lt_mask)] = c[e];
+                    cnt += __popc(m);
+                }
+                __syncwarp();
+            }
+        }
+        cnt = warp_compact(buf, cnt, k, bound);
+        for (int t = lane; t < cnt; t += 32) out[qi * k + t] = buf[t];
+        if (lane == 0) counts[qi] = static_cast<uint32_t>(cnt);
+        st_cand += static_cast<unsigned long long>(cnt);
+        __syncwarp();
+    }
+    if (stats) {
+        atomicAdd(stats + 0, st_blocks);
+        atomicAdd(stats + 1, st_scored);
+        if (lane == 0) atomicAdd(stats + 2, st_cand);
+    }
+}
+
 // ===================================================================== host side
 void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes);
 
@@ -566,7 +743,14 @@ static void run_knn(zi_ctx* ctx, const views8& V, uint64_t n, uint64_t nblk, con
                     int norm) {
     (void)nblk;
     if (k <= kMaxScanK) {
-        ZI_LAUNCH(ctx, "knn_scan", k_knn_scan, s.G, kScanThreads, 0, V, s.ws, k, norm, s.cand_cnt, s.cand);
+        switch (V.v[0].P) {
+#define ZI_SCAN_CASE(PP) \
+    case PP: ZI_LAUNCH(ctx, "knn_scan", k_knn_scan<PP>, s.G, kScanThreads, 0, V, s.ws, k, norm, s.cand_cnt, s.cand); break;
+            ZI_SCAN_CASE(1) ZI_SCAN_CASE(2) ZI_SCAN_CASE(3) ZI_SCAN_CASE(4)
+            ZI_SCAN_CASE(5) ZI_SCAN_CASE(6) ZI_SCAN_CASE(7) ZI_SCAN_CASE(8)
+#undef ZI_SCAN_CASE
+            default: throw error(ZI_E_INVALID, "dims above 32");
+        }
         ZI_LAUNCH(ctx, "knn_merge", k_knn_merge, 1, kMergeThreads, 0, s.ws, k, s.G, s.cand_cnt, s.cand, s.out);
         return;
     }
@@ -612,7 +796,7 @@ uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm,
     qws* hq = reinterpret_cast<qws*>(stage + 64);
     ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
-    const uint32_t cnt = hq->count;
+    const uint32_t cnt = static_cast<uint32_t>(std::min<uint64_t>(hq->count, std::min<uint64_t>(k, idx->n)));
     if (cnt) {
         ZI_CUDA(cudaMemcpyAsync(out, s.out, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -623,8 +807,47 @@ uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm,
 void knn_search_batch(zi_index* idx, const uint8_t* h_queries, uint64_t nq, uint32_t k, int norm, uint64_t* out,
                       uint32_t* counts) {
     const uint32_t kk = std::max<uint32_t>(k, 1);
-    for (uint64_t q = 0; q < nq; ++q)
-        counts[q] = knn_search(idx, h_queries + q * idx->dims, kk, norm, out + q * kk);
+    if (nq == 0) return;
+    if (idx->n == 0) {
+        std::memset(counts, 0, nq * sizeof(uint32_t));
+        return;
+    }
+    if (kk > kWarpMaxK) {  // large k: one multi-CTA query at a time
+        for (uint64_t q = 0; q < nq; ++q) counts[q] = knn_search(idx, h_queries + q * idx->dims, kk, norm, out + q * kk);
+        return;
+    }
+    zi_ctx* ctx = idx->ctx;
+    const size_t qbytes = nq * idx->dims;
+    const size_t obytes = nq * kk * sizeof(uint64_t);
+    uint8_t* b = idx->qscratch.ensure(qbytes + obytes + nq * sizeof(uint32_t) + 1024);
+    uint8_t* d_q = b;
+    unsigned long long* d_out = reinterpret_cast<unsigned long long*>(b + ((qbytes + 255) & ~size_t(255)));
+    uint32_t* d_cnt = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(d_out) + obytes);
+    ZI_CUDA(cudaMemcpyAsync(d_q, h_queries, qbytes, cudaMemcpyHostToDevice, ctx->stream));
+    knn_batch_device(ctx, idx, d_q, nq, kk, norm, d_out, d_cnt, nullptr);
+    ZI_CUDA(cudaMemcpyAsync(out, d_out, obytes, cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(counts, d_cnt, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void knn_batch_device(zi_ctx* ctx, zi_index* idx, const uint8_t* d_queries, uint64_t nq, uint32_t k, int norm,
+                      unsigned long long* d_out, uint32_t* d_counts, unsigned long long* d_stats) {
+    const index_view v = view_of(idx);
+    int win = 64;
+    while (win < static_cast<int>(2 * k)) win <<= 1;  // window >= 2k (<= 512)
+    const uint64_t per_cta = kBatchWarps;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((nq + per_cta - 1) / per_cta, 1u << 20));
+    switch (v.P) {
+#define ZI_BATCH_CASE(PP)                                                                                     \
+    case PP:                                                                                                  \
+        ZI_LAUNCH(ctx, "knn_batch", k_knn_batch<PP>, grid, 32 * kBatchWarps, 0, v, d_queries, nq, k, norm, win, \
+                  d_out, d_counts, d_stats);                                                                  \
+        break;
+        ZI_BATCH_CASE(1) ZI_BATCH_CASE(2) ZI_BATCH_CASE(3) ZI_BATCH_CASE(4)
+        ZI_BATCH_CASE(5) ZI_BATCH_CASE(6) ZI_BATCH_CASE(7) ZI_BATCH_CASE(8)
+#undef ZI_BATCH_CASE
+        default: throw error(ZI_E_INVALID, "dims above 32");
+    }
 }
 
 static mi_view mi_view_of(zi_multi_index* mi) {
@@ -670,7 +893,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
     query_result r;
     r.best = hq->best;
     r.lid = hq->lid;
-    r.count = hq->count;
+    r.count = static_cast<uint32_t>(std::min<uint64_t>(hq->count, std::min<uint64_t>(k, mi->n)));
     if (knn_out && r.count) {
         ZI_CUDA(cudaMemcpyAsync(knn_out, s.out, r.count * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -205,6 +205,10 @@ uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t
 uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm, uint64_t* out);
 void knn_search_batch(zi_index* idx, const uint8_t* h_queries, uint64_t nq, uint32_t k, int norm,
                       uint64_t* out, uint32_t* counts);
+// device-resident batch (k <= 256): warp per query; stats (optional) = {blocks bbox-tested,
+// entries scored, results}
+void knn_batch_device(zi_ctx* ctx, zi_index* idx, const uint8_t* d_queries, uint64_t nq, uint32_t k, int norm,
+                      unsigned long long* d_out, uint32_t* d_counts, unsigned long long* d_stats);
 
 // ---- host pieces ----
 int subset_pixel_count(int K, double c);

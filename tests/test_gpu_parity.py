@@ -416,3 +416,18 @@ def test_cfg2_build_properties(zb):
         for t in range(3):
             qv = c[rng.integers(0, len(k))]
             assert np.array_equal(idx.knn(qv, 80), oracle.knn_linear(c, k, qv, 80))
+
+
+@pytest.mark.parametrize("D", [4, 8, 16])
+def test_knn_batch_cfg5_like_vs_oracle(zb, D):
+    coords, queries = workloads.cfg5_descriptors(60000, D, 64, seed=D)
+    keys = np.arange(coords.shape[0], dtype=np.uint32)
+    idx = zb.ZCurveIndex.from_descriptors(coords, keys, D)
+    sc, sk = idx.export()
+    for k in (1, 80, 256):
+        out, cnt = idx.knn_batch(queries, k)
+        ms, stats, (o2, c2) = idx.knn_batch_bench(queries, k, reps=1, return_results=True)
+        assert np.array_equal(out, o2) and np.array_equal(cnt, c2)
+        for i in range(0, 64, 7):
+            ref = oracle.knn_linear(sc, sk, queries[i], k)
+            assert cnt[i] == ref.size and np.array_equal(out[i, :cnt[i]], ref), (k, i)

@@ -112,6 +112,31 @@ def cfg5_points(n: int, dims_in: int = 125, seed: int = 5):
     return (z * scale.astype(np.float32)) @ q.T.astype(np.float32)
 
 
+def cfg5_descriptors(n: int, D: int, nq: int, seed: int = 5, dims_in: int = 125, miss: float = 0.4):
+    """cfg5 stand-in for the k-NN sweep: the quantised top-D principal coordinates of
+    x = Q diag(0.9^(k/2)) z (their PCA basis is Q's first D columns, eigenvalues 0.9^k), and
+    nq held-out queries with 40% of their 125 coordinates unknown -> mean (make_query semantics,
+    proj/src/builder.cpp:110-127), projected and quantised with the dictionary's lo/hi."""
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.normal(size=(dims_in, dims_in)))
+    scale = 0.9 ** (np.arange(dims_in) / 2.0)
+    y = rng.standard_normal((n, D), dtype=np.float32) * scale[:D].astype(np.float32)
+    lo, hi = y.min(0).astype(np.float64), y.max(0).astype(np.float64)
+
+    def quant(v):
+        c = np.clip(v, lo, hi)
+        return np.floor(255.0 * (c - lo) / (hi - lo) + 0.5).astype(np.uint8)
+
+    coords = np.empty((n, D), dtype=np.uint8)
+    for b in range(0, n, 1 << 20):
+        coords[b:b + (1 << 20)] = quant(y[b:b + (1 << 20)].astype(np.float64))
+    zq = rng.standard_normal((nq, dims_in))
+    xq = (zq * scale) @ Q.T
+    xq[rng.random((nq, dims_in)) < miss] = 0.0  # unknown -> mean (the distribution mean is 0)
+    queries = quant(xq @ Q[:, :D])
+    return coords, queries
+
+
 def small_image(h: int, w: int, channels: int, seed: int, hole_frac: float = 0.1):
     """Small textured image + random rectangular holes, for parity tests."""
     rng = np.random.default_rng(seed)
