@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -61,6 +62,11 @@ void launch_begin(zi_ctx* ctx, const char* name) {
 }
 
 void launch_end(zi_ctx* ctx, const char* name) {
+    static const bool sync_check = std::getenv("ZI_SYNC_CHECK") != nullptr;
+    if (sync_check) {  // debug: attribute asynchronous faults to the kernel that caused them
+        const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) throw error(ZI_E_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
+    }
     if (!ctx->profiling) return;
     for (auto& p : ctx->prof)
         if (std::strcmp(p.name, name) == 0) {

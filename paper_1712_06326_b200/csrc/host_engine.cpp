@@ -11,6 +11,8 @@
 // refresh), so no expression may be silently fused.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <set>
@@ -243,6 +245,7 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
     fill_driver drv(img, m, K);
     std::vector<uint8_t> tv(static_cast<size_t>(K) * K * mi->C), tk(static_cast<size_t>(K) * K);
     const uint32_t k = static_cast<uint32_t>(std::max(cfg.knn, 1));
+    double t_query = 0.0, t_paste = 0.0;
     while (unknown_left > 0) {
         if (drv.empty()) throw error(ZI_E_RUNTIME, "inpaint: unknown pixels unreachable from the fillfront");
         const auto t_it = std::chrono::steady_clock::now();
@@ -254,6 +257,7 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
         rec.target_x = tx;
         rec.target_y = ty;
         uint64_t best;
+        const auto tq0 = std::chrono::steady_clock::now();
         if (icfg.brute_force) {
             best = brute_force_best(mi, tv.data(), tk.data(), cfg.norm);
             rec.layout_id = 0;
@@ -285,8 +289,11 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
                 ++ae_excl;
             }
         }
+        const auto tp0 = std::chrono::steady_clock::now();
+        t_query += std::chrono::duration<double>(tp0 - tq0).count();
         double cc;
         unknown_left -= static_cast<uint64_t>(drv.apply_paste(tx, ty, rec.source_key, &cc));
+        t_paste += std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count();
         stats->confidence_low = std::min(stats->confidence_low, cc);
         stats->confidence_high = std::max(stats->confidence_high, cc);
         rec.elapsed_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_it).count();
@@ -298,6 +305,9 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
     stats->iterations = it;
     stats->inpaint_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (ae_contrib > 0) stats->mean_ae = ae_sum / static_cast<double>(ae_contrib);
+    if (std::getenv("ZI_DEBUG_QUERY"))
+        std::fprintf(stderr, "fill loop: %llu iterations, query %.1f us/it, paste+priorities %.1f us/it\n",
+                     static_cast<unsigned long long>(it), 1e6 * t_query / it, 1e6 * t_paste / it);
     stats->ae_excluded = ae_excl;
 }
 

@@ -14,6 +14,8 @@
 // unique (keys are), so the final k smallest are exactly the reference's knn_search result.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -33,7 +35,12 @@ struct qws {
     uint8_t q[32];
     uint32_t lid;
     uint32_t count;
-    uint32_t pad[6];
+    uint32_t overflow;  // fused single-CTA query gave up (too many candidates): host falls back
+    uint32_t dbg_total, dbg_m;  // merge: candidates in all CTA lists / candidates <= the final bound
+    uint32_t done;              // k_query_one: CTAs finished (the last one merges)
+    uint32_t gcount;            // k_query_one: candidates appended to the compact global list
+    unsigned long long final_bound;
+    unsigned long long tphase[10];  // debug: %globaltimer at phase boundaries (CTA 0 / last CTA)
 };
 
 struct index_view {
@@ -123,6 +130,47 @@ __device__ inline void score_block(const index_view& v, uint64_t b, const uint32
     }
 }
 
+// K7': seed from the bbox table -- each warp finds the block with the smallest lower bound among
+// its share of all blocks, scores it, and the k-th smallest packed value of those 2048 entries
+// (any k real entries give a valid bound) becomes the starting bound.  Needs 2048 u64 of s_buf
+// and blockDim.x == 256.
+template <int P>
+__device__ void seed_bound_bbox(const index_view& v, const uint32_t (&q4)[8], uint32_t k, int norm,
+                                unsigned long long* s_buf, qws* ws) {
+    __shared__ unsigned long long s_wmin[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long mine = kU64Max;
+    for (uint64_t b = static_cast<uint64_t>(warp) * 32 + lane; b < v.nblk; b += 256) {
+        uint32_t lb = 0;
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            lb = gap4(q4[p], v.bmin[static_cast<size_t>(p) * v.nblk + b], v.bmax[static_cast<size_t>(p) * v.nblk + b], norm, lb);
+        const unsigned long long c = (static_cast<unsigned long long>(lb) << 32) | b;
+        mine = c < mine ? c : mine;
+    }
+    mine = warp_min(mine);
+    if (lane == 0) s_wmin[warp] = mine;
+    __syncthreads();
+    const unsigned long long sb = s_wmin[warp];
+    unsigned long long c[8];
+    if (sb != kU64Max) {
+        score_block<P>(v, sb & 0xffffffffull, q4, norm, c);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) c[e] = kU64Max;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s_buf[warp * 256 + e * 32 + lane] = c[e];
+    __syncthreads();
+    block_bitonic_sort(s_buf, 2048);
+    if (tid == 0) {
+        ws->bound = k <= 2048 ? s_buf[k - 1] : kU64Max;
+        ws->best = kU64Max;
+        ws->count = 0;
+        ws->overflow = 0;
+    }
+}
+
 // K7: lower_bound of q in Morton order (256-ary search), then score a window of `win`
 // entries around it and take the k-th smallest packed value as the starting bound.
 __device__ void seed_bound(const index_view& v, const uint8_t* s_q, const uint32_t* s_q4, uint32_t k, int norm,
@@ -177,6 +225,7 @@ __device__ void seed_bound(const index_view& v, const uint8_t* s_q, const uint32
     }
 }
 
+template <int P>
 __global__ void __launch_bounds__(256) k_seed_query(index_view v, const uint8_t* __restrict__ query, qws* ws,
                                                     uint32_t k, int norm, int win) {
     extern __shared__ unsigned long long s_buf[];
@@ -193,7 +242,11 @@ __global__ void __launch_bounds__(256) k_seed_query(index_view v, const uint8_t*
     if (threadIdx.x < 32) ws->q[threadIdx.x] = s_q[threadIdx.x];
     if (threadIdx.x == 0) ws->lid = 0;
     __syncthreads();
-    seed_bound(v, s_q, s_q4, k, norm, win, s_buf, ws);
+    uint32_t q4[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) q4[p] = s_q4[p];
+    (void)win;
+    seed_bound_bbox<P>(v, q4, k, norm, s_buf, ws);
 }
 
 // multi-index: select_index + make_query on the device, then the seed on the chosen layout
@@ -206,6 +259,9 @@ struct mi_view {
     int m, C, K, D;
 };
 
+// Dynamic smem: the seed window (win u64) | x row of the chosen layout (mc doubles) |
+// components of the chosen layout ([j][d], mc*D doubles) | target (K*K*C + K*K bytes).
+template <int P>
 __global__ void __launch_bounds__(256) k_query_prep(mi_view mv, const uint8_t* __restrict__ target, qws* ws,
                                                     uint32_t k, int norm, int win) {
     extern __shared__ unsigned long long s_buf[];
@@ -215,8 +271,14 @@ __global__ void __launch_bounds__(256) k_query_prep(mi_view mv, const uint8_t* _
     __shared__ uint32_t s_q4[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int KK = mv.K * mv.K, mc = mv.m * mv.C;
-    const uint8_t* tv = target;
-    const uint8_t* tk = target + static_cast<size_t>(KK) * mv.C;
+    double* s_xc = reinterpret_cast<double*>(s_buf + win);     // mc
+    double* s_comp = s_xc + mc;                                  // mc * D
+    uint8_t* s_t = reinterpret_cast<uint8_t*>(s_comp + static_cast<size_t>(mc) * mv.D);
+    const int tbytes = KK * mv.C + KK;
+    for (int i = tid; i < tbytes; i += blockDim.x) s_t[i] = target[i];
+    __syncthreads();
+    const uint8_t* tv = s_t;
+    const uint8_t* tk = s_t + KK * mv.C;
     // select_index (proj/src/engine.cpp:162-176): strict '>' from 0, ties -> lowest id
     if (warp < 8) {
         int ov = 0;
@@ -239,23 +301,25 @@ __global__ void __launch_bounds__(256) k_query_prep(mi_view mv, const uint8_t* _
     if (tid < 32) s_q[tid] = 0;
     __syncthreads();
     const int lid = s_lid;
-    // make_query (proj/src/builder.cpp:110-127) in the build's canonical fp64 order
+    // make_query (proj/src/builder.cpp:110-127): xc_j = x_j - mean_j with unknown pixels at the
+    // mean (xc = +0.0 exactly), staged in parallel; then the canonical fp64 chain per dim
+    {
+        const double* mean = mv.mean + static_cast<size_t>(lid) * mc;
+        const int32_t* loc = mv.local + lid * mv.m;
+        for (int j = tid; j < mc; j += blockDim.x) {
+            const int l = loc[j / mv.C];
+            const double mj = mean[j];
+            const double x = tk[l] ? static_cast<double>(tv[l * mv.C + j % mv.C]) : mj;
+            s_xc[j] = __dsub_rn(x, mj);
+        }
+        const double* comp = mv.comp + static_cast<size_t>(lid) * mc * mv.D;
+        for (int i = tid; i < mc * mv.D; i += blockDim.x) s_comp[i] = comp[i];
+    }
+    __syncthreads();
     if (tid < mv.D) {
         const int d = tid;
-        const double* mean = mv.mean + static_cast<size_t>(lid) * mc;
-        const double* comp = mv.comp + static_cast<size_t>(lid) * mc * mv.D;
-        const int32_t* loc = mv.local + lid * mv.m;
         double y = 0.0;
-        int j = 0;
-        for (int p = 0; p < mv.m; ++p) {
-            const int l = loc[p];
-            const bool known = tk[l] != 0;
-            for (int ch = 0; ch < mv.C; ++ch, ++j) {
-                const double x = known ? static_cast<double>(tv[l * mv.C + ch]) : mean[j];
-                const double xc = __dsub_rn(x, mean[j]);
-                y = __fma_rn(comp[static_cast<size_t>(j) * mv.D + d], xc, y);
-            }
-        }
+        for (int j = 0; j < mc; ++j) y = __fma_rn(s_comp[j * mv.D + d], s_xc[j], y);
         const unsigned long long* mm = mv.minmax + static_cast<size_t>(lid) * 2 * mv.D;
         s_q[d] = quantize_rn(ordered_to_double_hd(mm[d]), ordered_to_double_hd(mm[mv.D + d]), y);
     }
@@ -268,7 +332,10 @@ __global__ void __launch_bounds__(256) k_query_prep(mi_view mv, const uint8_t* _
     }
     if (tid < 32) ws->q[tid] = s_q[tid];
     __syncthreads();
-    seed_bound(mv.idx[lid], s_q, s_q4, k, norm, win, s_buf, ws);
+    uint32_t q4[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) q4[p] = s_q4[p];
+    seed_bound_bbox<P>(mv.idx[lid], q4, k, norm, s_buf, ws);
 }
 
 // keep the <= k smallest of buf[0..cnt) (sorted), tighten the bounds
@@ -394,6 +461,42 @@ __global__ void __launch_bounds__(kMergeThreads) k_knn_merge(qws* ws, uint32_t k
     }
     __syncthreads();
     const uint32_t total = s_pref[G];
+    // fast path: everything <= the final bound fits -> exact ranks by counting (values are unique)
+    {
+        const unsigned long long bound = s_bound;
+        for (uint32_t f = tid; f < total; f += kMergeThreads) {
+            int lo = 0, hi = G;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pref[mid] <= f) lo = mid;
+                else hi = mid;
+            }
+            const unsigned long long c = cand[static_cast<size_t>(lo) * k + (f - s_pref[lo])];
+            if (c <= bound) {
+                const int slot = atomicAdd(&s_cnt, 1);
+                if (slot < kMergeCap) s_buf[slot] = c;
+            }
+        }
+        __syncthreads();
+        const int m = s_cnt;
+        if (tid == 0) {
+            ws->dbg_total = total;
+            ws->dbg_m = static_cast<uint32_t>(m);
+        }
+        if (m <= kMergeThreads) {
+            if (tid < m) {
+                const unsigned long long c = s_buf[tid];
+                int r = 0;
+                for (int u = 0; u < m; ++u) r += s_buf[u] < c;
+                if (r < static_cast<int>(k)) out[r] = c;
+            }
+            if (tid == 0) ws->count = static_cast<uint32_t>(m < static_cast<int>(k) ? m : static_cast<int>(k));
+            return;
+        }
+        __syncthreads();
+        if (tid == 0) s_cnt = 0;
+        __syncthreads();
+    }
     const int chunk = kMergeCap - static_cast<int>(k);
     for (uint32_t f0 = 0; f0 < total; f0 += chunk) {
         const unsigned long long bound = s_bound;
@@ -418,46 +521,324 @@ __global__ void __launch_bounds__(kMergeThreads) k_knn_merge(qws* ws, uint32_t k
 
 // K9: refine -- masked_cost_at (proj/src/engine.cpp:48-76) per candidate, warp per candidate,
 // min over packed (cost, key) (engine.cpp:202-209).
-__global__ void __launch_bounds__(1024) k_refine(const uint8_t* __restrict__ img, int w, int C, int K,
-                                                 const uint8_t* __restrict__ target, qws* ws,
-                                                 const unsigned long long* __restrict__ list, int norm) {
-    extern __shared__ uint8_t s_t[];  // tv (K*K*C) then locals (u16)
+// cnt candidates of `list` (global or shared); s_t: >= K*K*C + 2*K*K + 2 bytes of shared memory
+__device__ void refine_list(const uint8_t* __restrict__ img, int w, int C, int K, const uint8_t* __restrict__ target,
+                            const unsigned long long* list, int cnt, int norm, uint8_t* s_t, qws* ws,
+                            int cost_slots = 1 << 30) {
     __shared__ int s_nloc;
     __shared__ unsigned long long s_best;
     const int KK = K * K;
     uint16_t* s_loc = reinterpret_cast<uint16_t*>(s_t + ((KK * C + 1) & ~1));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     for (int i = threadIdx.x; i < KK * C; i += blockDim.x) s_t[i] = target[i];
-    if (threadIdx.x == 0) {
+    if (warp == 0) {  // known locals, ascending (known_locals_of, engine.cpp:16-22), via ballots
         int c = 0;
-        for (int l = 0; l < KK; ++l)
-            if (target[KK * C + l]) s_loc[c++] = static_cast<uint16_t>(l);
-        s_nloc = c;
-        s_best = kU64Max;
+        for (int base = 0; base < KK; base += 32) {
+            const bool kn = base + lane < KK && target[KK * C + base + lane] != 0;
+            const unsigned m = __ballot_sync(0xffffffffu, kn);
+            if (kn) s_loc[c + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(base + lane);
+            c += __popc(m);
+        }
+        if (lane == 0) {
+            s_nloc = c;
+            s_best = kU64Max;
+        }
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    const int cnt = static_cast<int>(ws->count);
     const int nloc = s_nloc;
-    for (int e = warp; e < cnt; e += nwarp) {
-        const uint32_t key = static_cast<uint32_t>(list[e] & 0xffffffffu);
-        const int sx = key & 0xffff, sy = key >> 16;
-        uint32_t acc = 0;
-        for (int li = lane; li < nloc; li += 32) {
-            const int l = s_loc[li];
-            const int ly = l / K, lx = l % K;
-            const uint8_t* s = img + (static_cast<size_t>(sy + ly) * w + sx + lx) * C;
-            const uint8_t* t = s_t + l * C;
-            for (int c = 0; c < C; ++c) {
-                const int d = static_cast<int>(t[c]) - static_cast<int>(__ldg(s + c));
-                acc += norm == 0 ? static_cast<uint32_t>(d * d) : static_cast<uint32_t>(d < 0 ? -d : d);
+    if (cnt > cost_slots) {  // very large k: one warp per candidate
+        for (int e = warp; e < cnt; e += nwarp) {
+            const uint32_t key = static_cast<uint32_t>(list[e] & 0xffffffffu);
+            uint32_t acc = 0;
+            for (int li = lane; li < nloc; li += 32) {
+                const int l = s_loc[li];
+                const uint8_t* s = img + (static_cast<size_t>((key >> 16) + l / K) * w + (key & 0xffff) + l % K) * C;
+                for (int c = 0; c < C; ++c) {
+                    const int d = static_cast<int>(s_t[l * C + c]) - static_cast<int>(__ldg(s + c));
+                    acc += norm == 0 ? static_cast<uint32_t>(d * d) : static_cast<uint32_t>(d < 0 ? -d : d);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) atomicMin(&s_best, pack_candidate(acc, key));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) ws->best = s_best;
+        return;
+    }
+    // all (candidate, known pixel) pairs in parallel; per-candidate sums in shared memory
+    uint32_t* s_cost = reinterpret_cast<uint32_t*>(
+        s_t + ((((KK * C + 1) & ~1) + 2 * KK + 15) & ~15));  // cnt words, 16-byte aligned
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) s_cost[e] = 0;
+    __syncthreads();
+    const int pairs = cnt * nloc;
+    const int stride = blockDim.x;
+    // 4 independent pairs per step so their image loads are in flight together
+    for (int p0 = threadIdx.x; p0 < pairs; p0 += 4 * stride) {
+        uint8_t sv[4][3];
+        int pe[4], pl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int pi = p0 + u * stride;
+            pe[u] = -1;
+            if (pi < pairs) {
+                const int e = pi / nloc, li = pi - e * nloc;
+                const uint32_t key = static_cast<uint32_t>(list[e] & 0xffffffffu);
+                const int l = s_loc[li];
+                const uint8_t* s = img + (static_cast<size_t>((key >> 16) + l / K) * w + (key & 0xffff) + l % K) * C;
+                pe[u] = e;
+                pl[u] = l;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) sv[u][c] = c < C ? __ldg(s + c) : 0;
             }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) atomicMin(&s_best, pack_candidate(acc, key));
+        for (int u = 0; u < 4; ++u) {
+            if (pe[u] < 0) continue;
+            const uint8_t* t = s_t + pl[u] * C;
+            uint32_t acc = 0;
+            for (int c = 0; c < C; ++c) {
+                const int d = static_cast<int>(t[c]) - static_cast<int>(sv[u][c]);
+                acc += norm == 0 ? static_cast<uint32_t>(d * d) : static_cast<uint32_t>(d < 0 ? -d : d);
+            }
+            atomicAdd(&s_cost[pe[u]], acc);
+        }
     }
     __syncthreads();
+    unsigned long long mine = kU64Max;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const unsigned long long c = pack_candidate(s_cost[e], static_cast<uint32_t>(list[e] & 0xffffffffu));
+        mine = c < mine ? c : mine;
+    }
+    mine = warp_min(mine);
+    if (lane == 0) atomicMin(&s_best, mine);
+    (void)warp;
+    (void)nwarp;
+    __syncthreads();
     if (threadIdx.x == 0) ws->best = s_best;
+}
+
+constexpr int kRefineSlots = 4096;
+
+__global__ void __launch_bounds__(1024) k_refine(const uint8_t* __restrict__ img, int w, int C, int K,
+                                                 const uint8_t* __restrict__ target, qws* ws,
+                                                 const unsigned long long* __restrict__ list, int norm) {
+    extern __shared__ uint8_t s_t[];
+    refine_list(img, w, C, K, target, list, static_cast<int>(ws->count), norm, s_t, ws, kRefineSlots);
+}
+
+__device__ inline void warp_bitonic_sort(unsigned long long* a, int n);
+
+__device__ inline unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define ZI_TPHASE(i) \
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || (i) >= 6)) ws->tphase[i] = gtimer();
+
+// Exact top-k selection in shared memory (any blockDim): buf[0..m) holds unique packed values;
+// a histogram of their distances finds the bin holding the k-th, the boundary bin is ranked
+// exactly, and the k winners are sorted into sel[0..min(k,m)).  Returns that count, or -1 when
+// the boundary bin holds more than tmp_cap values (caller falls back).  hist: nbins+1 words.
+__device__ int select_topk(const unsigned long long* buf, int m, uint32_t k, unsigned long long* sel,
+                           unsigned long long* tmp, int tmp_cap, uint32_t* hist, int nbins, uint32_t maxd,
+                           bool sort_result) {
+    __shared__ int s_nsel, s_ntmp, s_B, s_cumB;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+    if (m > static_cast<int>(k)) {
+        for (int i = tid; i <= nbins; i += nt) hist[i] = 0;
+        if (tid == 0) {
+            s_nsel = 0;
+            s_ntmp = 0;
+            s_B = -1;
+        }
+        __syncthreads();
+        // bin = floor(dist * nbins / (maxd + 1)) as a multiply-shift: monotone in dist, < nbins
+        const uint64_t scale = (static_cast<uint64_t>(nbins) << 32) / (static_cast<uint64_t>(maxd) + 1);
+        for (int i = tid; i < m; i += nt) {
+            const uint32_t bin = static_cast<uint32_t>(((buf[i] >> 32) * scale) >> 32);
+            atomicAdd(&hist[bin < static_cast<uint32_t>(nbins) ? bin : nbins - 1], 1u);
+        }
+        __syncthreads();
+        if (warp == 0) {  // first bin where the running count reaches k
+            uint32_t run = 0;
+            for (int base = 0; base < nbins; base += 32) {
+                uint32_t x = base + lane < nbins ? hist[base + lane] : 0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, run + x >= k);
+                if (hit) {
+                    const int src = __ffs(hit) - 1;
+                    const uint32_t incl = __shfl_sync(0xffffffffu, x, src);
+                    if (lane == 0) {
+                        s_B = base + src;
+                        s_cumB = static_cast<int>(run + incl - hist[base + src]);
+                    }
+                    break;
+                }
+                run += __shfl_sync(0xffffffffu, x, 31);
+            }
+        }
+        __syncthreads();
+        const int B = s_B, cumB = s_cumB;
+        if (B < 0 || B >= nbins) {
+            if (tid == 0) printf("select_topk: no boundary bin (m=%d k=%u maxd=%u)\n", m, k, maxd);
+            return -1;
+        }
+        if (static_cast<int>(hist[B]) > tmp_cap) return -1;
+        for (int i = tid; i < m; i += nt) {
+            const unsigned long long c = buf[i];
+            const int bin = static_cast<int>(((c >> 32) * scale) >> 32);
+            if (bin < B) sel[atomicAdd(&s_nsel, 1)] = c;
+            else if (bin == B) tmp[atomicAdd(&s_ntmp, 1)] = c;
+        }
+        __syncthreads();
+        const int ntmp = s_ntmp, need = static_cast<int>(k) - cumB;
+        for (int i = tid; i < ntmp; i += nt) {
+            const unsigned long long c = tmp[i];
+            int r = 0;
+            for (int u = 0; u < ntmp; ++u) r += tmp[u] < c;
+            if (r < need) sel[cumB + r] = c;
+        }
+        __syncthreads();
+    } else {
+        for (int i = tid; i < m; i += nt) sel[i] = buf[i];
+        __syncthreads();
+    }
+    const int cnt = m < static_cast<int>(k) ? m : static_cast<int>(k);
+    if (!sort_result) return cnt;
+    int sz = 32;
+    while (sz < cnt) sz <<= 1;
+    for (int i = cnt + tid; i < sz; i += nt) sel[i] = kU64Max;
+    __syncthreads();
+    if (sz <= 256) {  // one warp, no block barriers
+        if (warp == 0) warp_bitonic_sort(sel, sz);
+        __syncthreads();
+    } else {
+        block_bitonic_sort(sel, sz);
+    }
+    return cnt;
+}
+
+__device__ inline int select_sorted_topk(const unsigned long long* buf, int m, uint32_t k, unsigned long long* sel,
+                                         unsigned long long* tmp, int tmp_cap, uint32_t* hist, int nbins,
+                                         uint32_t maxd) {
+    return select_topk(buf, m, k, sel, tmp, tmp_cap, hist, nbins, maxd, true);
+}
+
+// K8c: exact top-k of the CTA lists (multi-CTA scan) in one CTA, optionally fused with the
+// refine (K9).  ws->overflow = 2 when the candidates do not fit: the host then runs k_knn_merge
+// + k_refine instead (identical result).
+constexpr int kSelThreads = 1024;
+constexpr int kSelCap = 16384;
+constexpr int kSelBins = 2048;
+constexpr int kSelBinCap = 1024;
+
+struct gather_result {
+    int m;
+    uint32_t maxd, total;
+};
+
+__device__ gather_result gather_lists(qws* ws, uint32_t k, int G, const uint32_t* __restrict__ cand_cnt,
+                                      const unsigned long long* __restrict__ cand, unsigned long long* buf, int cap,
+                                      uint32_t* s_pref) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ int s_cnt;
+    __shared__ uint32_t s_maxd;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x, nw = nt >> 5;
+    uint32_t carry = 0;
+    for (int base = 0; base < G; base += nt) {
+        const int i = base + tid;
+        const uint32_t c = i < G ? cand_cnt[i] : 0;
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t t = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            s_warp[lane] = t;
+        }
+        __syncthreads();
+        if (i < G) s_pref[i] = carry + (warp ? s_warp[warp - 1] : 0) + x - c;
+        carry += s_warp[nw - 1];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        s_pref[G] = carry;
+        s_cnt = 0;
+        s_maxd = 0;
+    }
+    __syncthreads();
+    const uint32_t total = s_pref[G];
+    const unsigned long long bound = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+    for (uint32_t f = tid; f < total; f += nt) {
+        int lo = 0, hi = G;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_pref[mid] <= f) lo = mid;
+            else hi = mid;
+        }
+        if (f - s_pref[lo] >= k) continue;  // defensive: a list never exceeds k entries
+        const unsigned long long c = cand[static_cast<size_t>(lo) * k + (f - s_pref[lo])];
+        if (c <= bound) {
+            const int slot = atomicAdd(&s_cnt, 1);
+            if (slot < cap) buf[slot] = c;
+            atomicMax(&s_maxd, static_cast<uint32_t>(c >> 32));
+        }
+    }
+    __syncthreads();
+    gather_result r;
+    r.m = s_cnt;
+    r.maxd = s_maxd;
+    r.total = total;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_knn_select(qws* ws, uint32_t k, int G,
+                                                            const uint32_t* __restrict__ cand_cnt,
+                                                            const unsigned long long* __restrict__ cand,
+                                                            unsigned long long* __restrict__ out,
+                                                            const uint8_t* __restrict__ img, int w, int C, int K,
+                                                            const uint8_t* __restrict__ target, int norm) {
+    extern __shared__ unsigned long long s_dyn[];
+    unsigned long long* buf = s_dyn;                         // kSelCap
+    unsigned long long* sel = buf + kSelCap;                 // 2048 (k <= 2048)
+    unsigned long long* tmp = sel + 2048;                    // kSelBinCap
+    uint32_t* hist = reinterpret_cast<uint32_t*>(tmp + kSelBinCap);  // kSelBins (+1)
+    __shared__ uint32_t s_pref[1025];
+    const gather_result gr = gather_lists(ws, k, G, cand_cnt, cand, buf, kSelCap, s_pref);
+    const int m = gr.m;
+    const uint32_t maxd = gr.maxd, total = gr.total;
+    int cnt = m > kSelCap ? -1 : select_sorted_topk(buf, m, k, sel, tmp, kSelBinCap, hist, kSelBins, maxd);
+    if (cnt < 0) {
+        if (threadIdx.x == 0) ws->overflow = 2;
+        return;
+    }
+    for (int i = threadIdx.x; i < cnt; i += kSelThreads) out[i] = sel[i];
+    if (threadIdx.x == 0) {
+        ws->count = static_cast<uint32_t>(cnt);
+        ws->dbg_total = total;
+        ws->dbg_m = static_cast<uint32_t>(m);
+        ws->overflow = 0;
+    }
+    if (target != nullptr) {
+        __syncthreads();
+        refine_list(img, w, C, K, target, sel, cnt, norm, reinterpret_cast<uint8_t*>(buf), ws);
+    }
 }
 
 // K10: exhaustive masked-cost scan over the dictionary (brute_force_best)
@@ -525,6 +906,492 @@ __global__ void k_gather_topk(const uint32_t* __restrict__ lo, const uint32_t* _
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cnt) out[i] = (static_cast<unsigned long long>(hi[i]) << 32) | lo[i];
     if (i == 0) ws->count = cnt;
+}
+
+// ===================================================================== one-launch query (fill loop)
+// query_best_patch in ONE launch over G CTAs: every CTA stages the target and recomputes
+// select_index + make_query (a few microseconds, no host round trip); each CTA owns a contiguous
+// Morton range of blocks, seeds a local bound from its best block by bbox lower bound, shares it
+// through atomicMin on ws->bound, and keeps its exact local top-k; the last CTA to finish
+// (threadfence + ticket) selects the global top-k, refines it and resets the ticket/bound.
+constexpr int kOneThreads = 256;
+constexpr int kOneCap = 4096;
+constexpr uint32_t kOneMaxK = 1024;
+constexpr int kOneBins = 2048;
+constexpr int kOneBinCap = 1024;
+
+template <int P>
+__global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uint8_t* __restrict__ img, int w,
+                                                          const uint8_t* __restrict__ target, qws* ws, uint32_t k,
+                                                          int norm, uint32_t* __restrict__ cand_cnt,
+                                                          unsigned long long* __restrict__ cand,
+                                                          unsigned long long* __restrict__ out) {
+    extern __shared__ unsigned long long s_buf[];  // kOneCap | sel (kOneMaxK) | tmp | hist | xc | comp | target
+    unsigned long long* sel = s_buf + kOneCap;
+    unsigned long long* tmp = sel + kOneMaxK;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(tmp + kOneBinCap);
+    const int KK = mv.K * mv.K, mc = mv.m * mv.C, C = mv.C, D = mv.D;
+    double* s_xc = reinterpret_cast<double*>(hist + kOneBins + 2);
+    double* s_comp = s_xc + mc;
+    uint8_t* s_t = reinterpret_cast<uint8_t*>(s_comp + static_cast<size_t>(mc) * D);
+    __shared__ int s_ov[8];
+    __shared__ int s_lid, s_cnt, s_last;
+    __shared__ uint8_t s_q[32];
+    __shared__ unsigned long long s_bound, s_wmin[8];
+    __shared__ uint32_t s_pref[1025];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tbytes = KK * C + KK;
+    ZI_TPHASE(0)
+    for (int i = tid; i < tbytes; i += kOneThreads) s_t[i] = target[i];
+    if (tid < 32) s_q[tid] = 0;
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    const uint8_t* tv = s_t;
+    const uint8_t* tk = s_t + KK * C;
+    {  // select_index (engine.cpp:162-176)
+        int ov = 0;
+        for (int p = lane; p < mv.m; p += 32) ov += tk[mv.local[warp * mv.m + p]] != 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ov += __shfl_xor_sync(0xffffffffu, ov, o);
+        if (lane == 0) s_ov[warp] = ov;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int best = 0, bid = 0;
+        for (int l = 0; l < 8; ++l)
+            if (s_ov[l] > best) {
+                best = s_ov[l];
+                bid = l;
+            }
+        s_lid = bid;
+    }
+    __syncthreads();
+    const int lid = s_lid;
+    {  // make_query (builder.cpp:110-127), canonical fp64 order
+        const double* mean = mv.mean + static_cast<size_t>(lid) * mc;
+        const int32_t* loc = mv.local + lid * mv.m;
+        for (int j = tid; j < mc; j += kOneThreads) {
+            const int l = loc[j / C];
+            const double mj = mean[j];
+            const double x = tk[l] ? static_cast<double>(tv[l * C + j % C]) : mj;
+            s_xc[j] = __dsub_rn(x, mj);
+        }
+        const double* comp = mv.comp + static_cast<size_t>(lid) * mc * D;
+        for (int i = tid; i < mc * D; i += kOneThreads) s_comp[i] = comp[i];
+    }
+    __syncthreads();
+    if (tid < D) {
+        double y = 0.0;
+        for (int j = 0; j < mc; ++j) y = __fma_rn(s_comp[j * D + tid], s_xc[j], y);
+        const unsigned long long* mm = mv.minmax + static_cast<size_t>(lid) * 2 * D;
+        s_q[tid] = quantize_rn(ordered_to_double_hd(mm[tid]), ordered_to_double_hd(mm[D + tid]), y);
+    }
+    __syncthreads();
+    uint32_t q4[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+        q4[p] = static_cast<uint32_t>(s_q[4 * p]) | (static_cast<uint32_t>(s_q[4 * p + 1]) << 8) |
+                (static_cast<uint32_t>(s_q[4 * p + 2]) << 16) | (static_cast<uint32_t>(s_q[4 * p + 3]) << 24);
+    ZI_TPHASE(1)
+    const index_view v = mv.idx[lid];
+    const uint64_t nblk = v.nblk, G = gridDim.x;
+    const uint64_t per = (nblk + G - 1) / G;
+    const uint64_t bb0 = blockIdx.x * per < nblk ? blockIdx.x * per : nblk;
+    const uint64_t bb1 = bb0 + per < nblk ? bb0 + per : nblk;
+    // local seed: the range's block with the smallest bbox lower bound
+    {
+        unsigned long long mine = kU64Max;
+        for (uint64_t b = bb0 + tid; b < bb1; b += kOneThreads) {
+            uint32_t lb = 0;
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                lb = gap4(q4[p], v.bmin[static_cast<size_t>(p) * nblk + b], v.bmax[static_cast<size_t>(p) * nblk + b], norm, lb);
+            const unsigned long long c = (static_cast<unsigned long long>(lb) << 32) | b;
+            mine = c < mine ? c : mine;
+        }
+        mine = warp_min(mine);
+        if (lane == 0) s_wmin[warp] = mine;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long bm = lane < 8 ? s_wmin[lane] : kU64Max;
+        bm = warp_min(bm);
+        unsigned long long c[8];
+        if (bm != kU64Max) {
+            score_block<P>(v, bm & 0xffffffffull, q4, norm, c);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c[e] = kU64Max;
+        }
+        // k-th smallest distance of these 256 entries by radix descent (no sort): at least k
+        // entries have dist <= T, so (T<<32 | 0xffffffff) is a valid bound
+        int valid = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) valid += c[e] != kU64Max;
+        valid = __reduce_add_sync(0xffffffffu, valid);
+        unsigned long long lbound = kU64Max;
+        if (k <= 256 && valid >= static_cast<int>(k)) {
+            uint32_t T = 0;
+            int need = static_cast<int>(k);
+            for (int bit = 31; bit >= 0; --bit) {
+                int cnt = 0;
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    cnt += c[e] != kU64Max && (static_cast<uint32_t>(c[e] >> 32) >> bit) == (T >> bit);
+                cnt = __reduce_add_sync(0xffffffffu, cnt);
+                if (cnt < need) {
+                    need -= cnt;
+                    T |= 1u << bit;
+                }
+            }
+            lbound = (static_cast<unsigned long long>(T) << 32) | 0xffffffffull;
+        }
+        if (lane == 0) {
+            s_bound = lbound;
+            if (lbound != kU64Max) atomicMin(&ws->bound, lbound);
+        }
+    }
+    __syncthreads();
+    ZI_TPHASE(2)
+    // scan the range: 8 blocks per round, one per warp
+    const uint64_t rounds = (bb1 - bb0 + 7) / 8;
+    for (uint64_t r = 0; r < rounds; ++r) {
+        const uint64_t b = bb0 + r * 8 + warp;
+        unsigned long long bound = s_bound;
+        const unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+        bound = g < bound ? g : bound;
+        if (b < bb1) {
+            uint32_t lb = 0;
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                lb = gap4(q4[p], v.bmin[static_cast<size_t>(p) * nblk + b], v.bmax[static_cast<size_t>(p) * nblk + b], norm, lb);
+            if ((static_cast<unsigned long long>(lb) << 32) <= bound) {
+                unsigned long long c[8];
+                score_block<P>(v, b, q4, norm, c);
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (c[e] != kU64Max && c[e] <= bound) s_buf[atomicAdd(&s_cnt, 1)] = c[e];
+            }
+        }
+        __syncthreads();
+        if (s_cnt > kOneCap - 8 * 256) compact_buffer(s_buf, &s_cnt, &s_bound, k, ws, true);
+        __syncthreads();
+    }
+    ZI_TPHASE(3)
+    {  // exact local top-k (unsorted) by histogram selection, straight into the CTA's slot
+        const int m0 = s_cnt;
+        uint32_t mx = 0;
+        for (int t = tid; t < m0; t += kOneThreads) mx = max(mx, static_cast<uint32_t>(s_buf[t] >> 32));
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        __shared__ uint32_t s_mx;
+        if (tid == 0) s_mx = 0;
+        __syncthreads();
+        if (lane == 0) atomicMax(&s_mx, mx);
+        __syncthreads();
+        int cnt = select_topk(s_buf, m0, k, sel, tmp, kOneBinCap, hist, 256, s_mx, false);
+        if (cnt < 0) {  // degenerate boundary bin: exact sort-based compaction instead
+            compact_buffer(s_buf, &s_cnt, &s_bound, k, ws, true);
+            cnt = s_cnt;
+            for (int t = tid; t < cnt; t += kOneThreads) sel[t] = s_buf[t];
+            __syncthreads();
+        }
+        __shared__ unsigned long long s_kth;
+        if (tid == 0) s_kth = 0;
+        __syncthreads();
+        __shared__ uint32_t s_gbase;
+        if (tid == 0) s_gbase = atomicAdd(&ws->gcount, static_cast<uint32_t>(cnt));
+        __syncthreads();
+        unsigned long long kth = 0;
+        for (int t = tid; t < cnt; t += kOneThreads) {
+            cand[s_gbase + t] = sel[t];
+            kth = sel[t] > kth ? sel[t] : kth;
+        }
+        if (cnt >= static_cast<int>(k)) {  // this CTA's k-th is a valid global bound
+            atomicMax(&s_kth, kth);
+            __syncthreads();
+            if (tid == 0) atomicMin(&ws->bound, s_kth);
+        }
+    }
+    ZI_TPHASE(4)
+    // the last CTA merges
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&ws->done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    ZI_TPHASE(6)
+    int m;
+    uint32_t maxd, total;
+    {  // compact global list -> candidates <= the final bound
+        __shared__ int s_m;
+        __shared__ uint32_t s_maxd;
+        if (tid == 0) {
+            s_m = 0;
+            s_maxd = 0;
+        }
+        __syncthreads();
+        total = *reinterpret_cast<volatile uint32_t*>(&ws->gcount);
+        const unsigned long long bound = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+        for (uint32_t f = tid; f < total; f += kOneThreads) {
+            const unsigned long long c = cand[f];
+            if (c <= bound) {
+                const int slot = atomicAdd(&s_m, 1);
+                if (slot < kOneCap) s_buf[slot] = c;
+                atomicMax(&s_maxd, static_cast<uint32_t>(c >> 32));
+            }
+        }
+        __syncthreads();
+        m = s_m;
+        maxd = s_maxd;
+        (void)s_pref;
+    }
+    ZI_TPHASE(7)
+    int cnt = m > kOneCap ? -1 : select_sorted_topk(s_buf, m, k, sel, tmp, kOneBinCap, hist, 256, maxd);
+    ZI_TPHASE(8)
+    if (tid == 0) {
+        ws->lid = static_cast<uint32_t>(lid);
+        ws->dbg_total = total;
+        ws->dbg_m = static_cast<uint32_t>(m);
+        ws->final_bound = ws->bound;
+        ws->done = 0;
+        ws->gcount = 0;
+    }
+    if (cnt < 0) {
+        if (tid == 0) {
+            ws->overflow = 2;
+            cand_cnt[0] = total;  // the compact list as ONE list for k_knn_merge
+        }
+        return;  // host: k_knn_merge + k_refine over the same list
+    }
+    for (int i = tid; i < cnt; i += kOneThreads) out[i] = sel[i];
+    refine_list(img, w, C, KK > 0 ? mv.K : 1, target, sel, cnt, norm, reinterpret_cast<uint8_t*>(s_buf), ws);
+    ZI_TPHASE(9)
+    if (tid == 0) {
+        ws->count = static_cast<uint32_t>(cnt);
+        ws->overflow = 0;
+        ws->bound = kU64Max;
+    }
+}
+
+// ===================================================================== fused single-CTA query
+// The fill loop's per-iteration query in ONE launch (1024 threads): stage the target,
+// select_index, make_query, seed the bound from the 8 blocks with the smallest bbox lower bound,
+// bbox-pruned pass over every block appending candidates <= bound, exact top-k by sort, refine.
+// If more than kFusedCap candidates survive it sets ws->overflow and the host re-runs the
+// multi-CTA path (k_query_prep / k_knn_scan / k_knn_merge / k_refine) -- results identical.
+constexpr int kFusedThreads = 512;
+constexpr int kFusedCap = 8192;
+constexpr uint32_t kFusedMaxK = 1024;
+
+template <int P>
+__global__ void __launch_bounds__(kFusedThreads) k_query_fused(mi_view mv, const uint8_t* __restrict__ img, int w,
+                                                              const uint8_t* __restrict__ target, qws* ws, uint32_t k,
+                                                              int norm, unsigned long long* __restrict__ out_list) {
+    extern __shared__ unsigned long long s_buf[];  // kFusedCap candidates | xc | comp | target | locals
+    __shared__ int s_ov[8];
+    __shared__ int s_lid, s_cnt, s_nloc, s_overflow;
+    __shared__ uint8_t s_q[32];
+    __shared__ unsigned long long s_seed[32];
+    __shared__ unsigned long long s_best;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int KK = mv.K * mv.K, mc = mv.m * mv.C, C = mv.C, D = mv.D;
+    double* s_xc = reinterpret_cast<double*>(s_buf + kFusedCap);
+    double* s_comp = s_xc + mc;
+    uint8_t* s_t = reinterpret_cast<uint8_t*>(s_comp + static_cast<size_t>(mc) * D);
+    uint16_t* s_loc = reinterpret_cast<uint16_t*>(s_t + ((KK * C + KK + 1) & ~1));
+    const int tbytes = KK * C + KK;
+    for (int i = tid; i < tbytes; i += kFusedThreads) s_t[i] = target[i];
+    if (tid == 0) {
+        s_cnt = 0;
+        s_overflow = 0;
+        s_best = kU64Max;
+    }
+    if (tid < 32) s_q[tid] = 0;
+    __syncthreads();
+    const uint8_t* tv = s_t;
+    const uint8_t* tk = s_t + KK * C;
+    // select_index (engine.cpp:162-176) + known locals (engine.cpp:16-22)
+    if (warp < 8) {
+        int ov = 0;
+        for (int p = lane; p < mv.m; p += 32) ov += tk[mv.local[warp * mv.m + p]] != 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ov += __shfl_xor_sync(0xffffffffu, ov, o);
+        if (lane == 0) s_ov[warp] = ov;
+    } else if (warp == 8) {
+        int c = 0;
+        for (int base = 0; base < KK; base += 32) {
+            const bool kn = base + lane < KK && tk[base + lane] != 0;
+            const unsigned m = __ballot_sync(0xffffffffu, kn);
+            if (kn) s_loc[c + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(base + lane);
+            c += __popc(m);
+        }
+        if (lane == 0) s_nloc = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int best = 0, bid = 0;
+        for (int l = 0; l < 8; ++l)
+            if (s_ov[l] > best) {
+                best = s_ov[l];
+                bid = l;
+            }
+        s_lid = bid;
+    }
+    __syncthreads();
+    const int lid = s_lid;
+    // make_query (builder.cpp:110-127), canonical fp64 order
+    {
+        const double* mean = mv.mean + static_cast<size_t>(lid) * mc;
+        const int32_t* loc = mv.local + lid * mv.m;
+        for (int j = tid; j < mc; j += kFusedThreads) {
+            const int l = loc[j / C];
+            const double mj = mean[j];
+            const double x = tk[l] ? static_cast<double>(tv[l * C + j % C]) : mj;
+            s_xc[j] = __dsub_rn(x, mj);
+        }
+        const double* comp = mv.comp + static_cast<size_t>(lid) * mc * D;
+        for (int i = tid; i < mc * D; i += kFusedThreads) s_comp[i] = comp[i];
+    }
+    __syncthreads();
+    if (tid < D) {
+        double y = 0.0;
+        for (int j = 0; j < mc; ++j) y = __fma_rn(s_comp[j * D + tid], s_xc[j], y);
+        const unsigned long long* mm = mv.minmax + static_cast<size_t>(lid) * 2 * D;
+        s_q[tid] = quantize_rn(ordered_to_double_hd(mm[tid]), ordered_to_double_hd(mm[D + tid]), y);
+    }
+    __syncthreads();
+    uint32_t q4[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+        q4[p] = static_cast<uint32_t>(s_q[4 * p]) | (static_cast<uint32_t>(s_q[4 * p + 1]) << 8) |
+                (static_cast<uint32_t>(s_q[4 * p + 2]) << 16) | (static_cast<uint32_t>(s_q[4 * p + 3]) << 24);
+    const index_view v = mv.idx[lid];
+    const uint64_t nblk = v.nblk;
+    // seed: every warp's best block by bbox lower bound; score the 8 best of those
+    {
+        unsigned long long mine = kU64Max;
+        for (uint64_t b = static_cast<uint64_t>(warp) * 32 + lane; b < nblk; b += kFusedThreads) {
+            uint32_t lb = 0;
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                lb = gap4(q4[p], v.bmin[static_cast<size_t>(p) * nblk + b], v.bmax[static_cast<size_t>(p) * nblk + b], norm, lb);
+            const unsigned long long c = (static_cast<unsigned long long>(lb) << 32) | b;
+            mine = c < mine ? c : mine;
+        }
+        mine = warp_min(mine);
+        if (lane == 0) s_seed[warp] = mine;
+    }
+    __syncthreads();
+    if (warp == 0) {  // sort the warp minima (bitonic in registers)
+        unsigned long long x = lane < kFusedThreads / 32 ? s_seed[lane] : kU64Max;
+        for (int size = 2; size <= 32; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, stride);
+                const bool up = (lane & size) == 0;
+                const bool lower = (lane & stride) == 0;
+                x = (lower == up) ? (x < y ? x : y) : (x < y ? y : x);
+            }
+        s_seed[lane] = x;
+    }
+    __syncthreads();
+    if (warp < 8) {
+        const unsigned long long sb = s_seed[warp];
+        unsigned long long c[8];
+        if (sb != kU64Max) {
+            score_block<P>(v, sb & 0xffffffffull, q4, norm, c);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c[e] = kU64Max;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s_buf[warp * 256 + e * 32 + lane] = c[e];
+    }
+    __syncthreads();
+    block_bitonic_sort(s_buf, 2048);
+    const unsigned long long seed_bound_v = (k <= 2048) ? s_buf[k - 1] : kU64Max;  // MAX if fewer than k
+    __syncthreads();
+    // pass over every block
+    {
+        const unsigned long long bound = seed_bound_v;
+        for (uint64_t b0 = static_cast<uint64_t>(warp) * 32; b0 < nblk; b0 += kFusedThreads) {
+            const uint64_t b = b0 + lane;
+            uint32_t lb = 0xffffffffu;
+            if (b < nblk) {
+                lb = 0;
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    lb = gap4(q4[p], v.bmin[static_cast<size_t>(p) * nblk + b], v.bmax[static_cast<size_t>(p) * nblk + b], norm,
+                              lb);
+            }
+            unsigned live = __ballot_sync(0xffffffffu, b < nblk && (static_cast<unsigned long long>(lb) << 32) <= bound);
+            while (live) {
+                const int src = __ffs(live) - 1;
+                live &= live - 1;
+                unsigned long long c[8];
+                score_block<P>(v, b0 + src, q4, norm, c);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const bool take = c[e] != kU64Max && c[e] <= bound;
+                    const unsigned m = __ballot_sync(0xffffffffu, take);
+                    int base = 0;
+                    if (lane == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (take) {
+                        const int slot = base + __popc(m & ((1u << lane) - 1u));
+                        if (slot < kFusedCap) s_buf[slot] = c[e];
+                        else s_overflow = 1;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (s_overflow) {
+        if (tid == 0) {
+            ws->overflow = 1;
+            ws->lid = static_cast<uint32_t>(lid);
+        }
+        return;
+    }
+    const int m = s_cnt;
+    {
+        int sz = 2;
+        while (sz < m) sz <<= 1;
+        for (int t = m + tid; t < sz; t += kFusedThreads) s_buf[t] = kU64Max;
+        __syncthreads();
+        block_bitonic_sort(s_buf, sz);
+    }
+    const int cnt = m < static_cast<int>(k) ? m : static_cast<int>(k);
+    // refine (engine.cpp:197-210): warp per candidate, min packed (cost, key)
+    const int nloc = s_nloc;
+    for (int e = warp; e < cnt; e += kFusedThreads / 32) {
+        const uint32_t key = static_cast<uint32_t>(s_buf[e] & 0xffffffffu);
+        const int sx = key & 0xffff, sy = key >> 16;
+        uint32_t acc = 0;
+        for (int li = lane; li < nloc; li += 32) {
+            const int l = s_loc[li];
+            const int ly = l / mv.K, lx = l % mv.K;
+            const uint8_t* sp = img + (static_cast<size_t>(sy + ly) * w + sx + lx) * C;
+            const uint8_t* tp = tv + l * C;
+            for (int ch = 0; ch < C; ++ch) {
+                const int d = static_cast<int>(tp[ch]) - static_cast<int>(__ldg(sp + ch));
+                acc += norm == 0 ? static_cast<uint32_t>(d * d) : static_cast<uint32_t>(d < 0 ? -d : d);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) atomicMin(&s_best, pack_candidate(acc, key));
+    }
+    if (out_list)
+        for (int t = tid; t < cnt; t += kFusedThreads) out_list[t] = s_buf[t];
+    __syncthreads();
+    if (tid == 0) {
+        ws->best = s_best;
+        ws->count = static_cast<uint32_t>(cnt);
+        ws->lid = static_cast<uint32_t>(lid);
+        ws->overflow = 0;
+    }
 }
 
 // ===================================================================== batched k-NN (warp per query)
@@ -739,8 +1606,14 @@ static query_scratch carve(dbuf<uint8_t>& buf, const zi_ctx* ctx, uint64_t nblk,
 
 // scan + merge, or the exhaustive sort for very large k; result sorted in s.out, count in ws.
 // The layout actually searched is ws->lid (set by the prep kernel).
-static void run_knn(zi_ctx* ctx, const views8& V, uint64_t n, uint64_t nblk, const query_scratch& s, uint32_t k,
-                    int norm) {
+struct refine_args {
+    const uint8_t* img;
+    int w, C, K;
+};
+
+// Returns true when the refine (if requested) already ran inside the selection kernel.
+static bool run_knn(zi_ctx* ctx, const views8& V, uint64_t n, uint64_t nblk, const query_scratch& s, uint32_t k,
+                    int norm, const refine_args* ra = nullptr) {
     (void)nblk;
     if (k <= kMaxScanK) {
         switch (V.v[0].P) {
@@ -751,8 +1624,15 @@ static void run_knn(zi_ctx* ctx, const views8& V, uint64_t n, uint64_t nblk, con
 #undef ZI_SCAN_CASE
             default: throw error(ZI_E_INVALID, "dims above 32");
         }
-        ZI_LAUNCH(ctx, "knn_merge", k_knn_merge, 1, kMergeThreads, 0, s.ws, k, s.G, s.cand_cnt, s.cand, s.out);
-        return;
+        static bool attr = false;
+        if (!attr) {
+            ZI_CUDA(cudaFuncSetAttribute(k_knn_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        const size_t smem = (kSelCap + 2048 + kSelBinCap) * sizeof(unsigned long long) + (kSelBins + 1) * sizeof(uint32_t);
+        ZI_LAUNCH(ctx, "knn_select", k_knn_select, 1, kSelThreads, smem, s.ws, k, s.G, s.cand_cnt, s.cand, s.out,
+                  ra ? ra->img : nullptr, ra ? ra->w : 0, ra ? ra->C : 1, ra ? ra->K : 1, ra ? s.target : nullptr, norm);
+        return ra != nullptr;
     }
     // exhaustive: sort all n packed values (two-word LSD radix), take the first min(k, n)
     uint32_t* lohi = ctx->counter.ensure(2 * n + 64);
@@ -767,15 +1647,28 @@ static void run_knn(zi_ctx* ctx, const views8& V, uint64_t n, uint64_t nblk, con
     radix_sort_words(ctx, words, 2, n, passes);
     const uint32_t cnt = static_cast<uint32_t>(std::min<uint64_t>(k, n));
     ZI_LAUNCH(ctx, "knn_gather_topk", k_gather_topk, (cnt + 255) / 256, 256, 0, lo, hi, cnt, s.ws, s.out);
+    return false;
+}
+
+// rare: the selection kernel gave up (ws->overflow == 2) -> chunked merge (+ refine)
+static void knn_fallback(zi_ctx* ctx, const query_scratch& s, uint32_t k, int norm, const refine_args* ra,
+                         size_t rsmem) {
+    ZI_LAUNCH(ctx, "knn_merge", k_knn_merge, 1, kMergeThreads, 0, s.ws, k, s.G, s.cand_cnt, s.cand, s.out);
+    if (ra) ZI_LAUNCH(ctx, "refine", k_refine, 1, 1024, rsmem, ra->img, ra->w, ra->C, ra->K, s.target, s.ws, s.out, norm);
 }
 
 static void ensure_smem_attr() {
     static bool done = false;
     if (done) return;
-    ZI_CUDA(cudaFuncSetAttribute(k_seed_query, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8));
-    ZI_CUDA(cudaFuncSetAttribute(k_query_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8));
+#define ZI_ATTR(PP)                                                                                            \
+    ZI_CUDA(cudaFuncSetAttribute(k_seed_query<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8));     \
+    ZI_CUDA(cudaFuncSetAttribute(k_query_prep<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    ZI_ATTR(1) ZI_ATTR(2) ZI_ATTR(3) ZI_ATTR(4) ZI_ATTR(5) ZI_ATTR(6) ZI_ATTR(7) ZI_ATTR(8)
+#undef ZI_ATTR
     done = true;
 }
+
+static int seed_smem_words(uint32_t k) { return std::max(seed_window(k), 2048); }
 
 uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm, uint64_t* out) {
     zi_ctx* ctx = idx->ctx;
@@ -785,17 +1678,29 @@ uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm,
     views8 V;
     for (int l = 0; l < 8; ++l) V.v[l] = view_of(idx);
     const query_scratch s = carve(idx->qscratch, ctx, idx->nblk, k, 32);
-    uint8_t* stage = idx->hstage.ensure(256);
+    uint8_t* stage = idx->hstage.ensure(64 + ((sizeof(qws) + 63) & ~size_t(63)));
     std::memset(stage, 0, 32);
     std::memcpy(stage, h_query, idx->dims);
     ZI_CUDA(cudaMemcpyAsync(s.target, stage, 32, cudaMemcpyHostToDevice, ctx->stream));
     const int win = seed_window(k);
-    ZI_LAUNCH(ctx, "knn_seed", k_seed_query, 1, 256, win * sizeof(unsigned long long), V.v[0], s.target, s.ws, k, norm,
-              win);
+    const size_t seed_smem = seed_smem_words(k) * sizeof(unsigned long long);
+    switch (V.v[0].P) {
+#define ZI_SEED_CASE(PP) \
+    case PP: ZI_LAUNCH(ctx, "knn_seed", k_seed_query<PP>, 1, 256, seed_smem, V.v[0], s.target, s.ws, k, norm, win); break;
+        ZI_SEED_CASE(1) ZI_SEED_CASE(2) ZI_SEED_CASE(3) ZI_SEED_CASE(4)
+        ZI_SEED_CASE(5) ZI_SEED_CASE(6) ZI_SEED_CASE(7) ZI_SEED_CASE(8)
+#undef ZI_SEED_CASE
+        default: throw error(ZI_E_INVALID, "dims above 32");
+    }
     run_knn(ctx, V, idx->n, idx->nblk, s, k, norm);
     qws* hq = reinterpret_cast<qws*>(stage + 64);
     ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (k <= kMaxScanK && hq->overflow == 2) {
+        knn_fallback(ctx, s, k, norm, nullptr, 0);
+        ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     const uint32_t cnt = static_cast<uint32_t>(std::min<uint64_t>(hq->count, std::min<uint64_t>(k, idx->n)));
     if (cnt) {
         ZI_CUDA(cudaMemcpyAsync(out, s.out, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -864,6 +1769,36 @@ static mi_view mi_view_of(zi_multi_index* mi) {
     return mv;
 }
 
+static bool fused_query(zi_multi_index* mi, const query_scratch& s, const mi_view& mv, uint32_t k, int norm, qws* hq,
+                        bool want_list) {
+    zi_ctx* ctx = mi->ctx;
+    const size_t KK = static_cast<size_t>(mi->K) * mi->K;
+    const size_t smem = kFusedCap * sizeof(unsigned long long) + static_cast<size_t>(mi->mc) * (mi->dims + 1) * sizeof(double) +
+                        KK * mi->C + 3 * KK + 64;
+    static const bool enabled = std::getenv("ZI_QUERY_FUSED") != nullptr;
+    if (!enabled || smem > 220 * 1024 || k > kFusedMaxK) return false;
+    switch (mv.idx[0].P) {
+#define ZI_FUSED_CASE(PP)                                                                                          \
+    case PP: {                                                                                                     \
+        static bool attr = false;                                                                                  \
+        if (!attr) {                                                                                               \
+            ZI_CUDA(cudaFuncSetAttribute(k_query_fused<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)); \
+            attr = true;                                                                                           \
+        }                                                                                                          \
+        ZI_LAUNCH(ctx, "query_fused", k_query_fused<PP>, 1, kFusedThreads, smem, mv, mi->image.p, mi->w, s.target, s.ws, \
+                  k, norm, want_list ? s.out : nullptr);                                                           \
+        break;                                                                                                     \
+    }
+        ZI_FUSED_CASE(1) ZI_FUSED_CASE(2) ZI_FUSED_CASE(3) ZI_FUSED_CASE(4)
+        ZI_FUSED_CASE(5) ZI_FUSED_CASE(6) ZI_FUSED_CASE(7) ZI_FUSED_CASE(8)
+#undef ZI_FUSED_CASE
+        default: return false;
+    }
+    ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    return hq->overflow == 0;
+}
+
 query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, uint32_t k, int norm,
                               uint64_t* knn_out) {
     zi_ctx* ctx = mi->ctx;
@@ -879,17 +1814,79 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
     std::memcpy(stage + KK * mi->C, h_tk, KK);
     ZI_CUDA(cudaMemcpyAsync(s.target, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
     const mi_view mv = mi_view_of(mi);
-    const int win = seed_window(k);
-    ZI_LAUNCH(ctx, "query_prep", k_query_prep, 1, 256, win * sizeof(unsigned long long), mv, s.target, s.ws, k, norm,
-              win);
-    views8 V;
-    for (int l = 0; l < 8; ++l) V.v[l] = mv.idx[l];
-    run_knn(ctx, V, mi->n, nblk, s, k, norm);
-    const size_t rsmem = ((KK * mi->C + 1) & ~size_t(1)) + KK * sizeof(uint16_t) + 16;
-    ZI_LAUNCH(ctx, "refine", k_refine, 1, 1024, rsmem, mi->image.p, mi->w, mi->C, mi->K, s.target, s.ws, s.out, norm);
     qws* hq = reinterpret_cast<qws*>(stage + res_off);
-    ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
-    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    const size_t rsmem = ((KK * mi->C + 1) & ~size_t(1)) + (KK + 16) * sizeof(uint16_t) + kRefineSlots * sizeof(uint32_t) + 32;
+    const refine_args ra{mi->image.p, mi->w, mi->C, mi->K};
+    const size_t one_smem = (kOneCap + kOneMaxK + kOneBinCap) * sizeof(unsigned long long) + (kOneBins + 2) * sizeof(uint32_t) +
+                            static_cast<size_t>(mi->mc) * (mi->dims + 1) * sizeof(double) + tbytes + 16;
+    bool done = false;
+    if (k <= kOneMaxK && one_smem <= 220 * 1024 && !std::getenv("ZI_QUERY_MULTI")) {
+        const int G1 = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(nblk, 1),
+                                                           std::min<uint64_t>(static_cast<uint64_t>(s.G), 2ull * ctx->num_sms)));
+        ZI_CUDA(cudaMemsetAsync(&s.ws->bound, 0xff, sizeof(unsigned long long), ctx->stream));
+        ZI_CUDA(cudaMemsetAsync(&s.ws->done, 0, 2 * sizeof(uint32_t), ctx->stream));  // done + gcount
+        switch (mv.idx[0].P) {
+#define ZI_ONE_CASE(PP)                                                                                              \
+    case PP: {                                                                                                       \
+        static bool attr = false;                                                                                    \
+        if (!attr) {                                                                                                 \
+            ZI_CUDA(cudaFuncSetAttribute(k_query_one<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));  \
+            attr = true;                                                                                             \
+        }                                                                                                            \
+        ZI_LAUNCH(ctx, "query_one", k_query_one<PP>, G1, kOneThreads, one_smem, mv, mi->image.p, mi->w, s.target, s.ws, \
+                  k, norm, s.cand_cnt, s.cand, s.out);                                                               \
+        break;                                                                                                       \
+    }
+            ZI_ONE_CASE(1) ZI_ONE_CASE(2) ZI_ONE_CASE(3) ZI_ONE_CASE(4)
+            ZI_ONE_CASE(5) ZI_ONE_CASE(6) ZI_ONE_CASE(7) ZI_ONE_CASE(8)
+#undef ZI_ONE_CASE
+            default: throw error(ZI_E_INVALID, "dims above 32");
+        }
+        ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (hq->overflow == 2) {  // rare: the merge did not fit -> chunked merge over the same CTA lists
+            query_scratch s1 = s;
+            s1.G = 1;
+            knn_fallback(ctx, s1, k, norm, &ra, rsmem);
+            ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        done = true;
+    }
+    if (!done && !fused_query(mi, s, mv, k, norm, hq, knn_out != nullptr)) {
+        const int win = seed_window(k);
+        const size_t prep_smem = seed_smem_words(k) * sizeof(unsigned long long) +
+                                 static_cast<size_t>(mi->mc) * (mi->dims + 1) * sizeof(double) + tbytes + 16;
+        switch (mv.idx[0].P) {
+#define ZI_PREP_CASE(PP) \
+    case PP: ZI_LAUNCH(ctx, "query_prep", k_query_prep<PP>, 1, 256, prep_smem, mv, s.target, s.ws, k, norm, \
+                       seed_smem_words(k)); break;
+            ZI_PREP_CASE(1) ZI_PREP_CASE(2) ZI_PREP_CASE(3) ZI_PREP_CASE(4)
+            ZI_PREP_CASE(5) ZI_PREP_CASE(6) ZI_PREP_CASE(7) ZI_PREP_CASE(8)
+#undef ZI_PREP_CASE
+            default: throw error(ZI_E_INVALID, "dims above 32");
+        }
+        (void)win;
+        views8 V;
+        for (int l = 0; l < 8; ++l) V.v[l] = mv.idx[l];
+        const bool refined = run_knn(ctx, V, mi->n, nblk, s, k, norm, &ra);
+        if (!refined)
+            ZI_LAUNCH(ctx, "refine", k_refine, 1, 1024, rsmem, mi->image.p, mi->w, mi->C, mi->K, s.target, s.ws, s.out, norm);
+        ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (refined && hq->overflow == 2) {
+            knn_fallback(ctx, s, k, norm, &ra, rsmem);
+            ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+    }
+    if (std::getenv("ZI_DEBUG_QUERY")) {
+        std::fprintf(stderr, "query lid=%u bound_dist=%u total=%u m=%u count=%u overflow=%u phases_us:", hq->lid,
+                     static_cast<unsigned>(hq->final_bound >> 32), hq->dbg_total, hq->dbg_m, hq->count, hq->overflow);
+        for (int i = 1; i < 10; ++i)
+            std::fprintf(stderr, " %.1f", (static_cast<double>(hq->tphase[i]) - static_cast<double>(hq->tphase[0])) * 1e-3);
+        std::fprintf(stderr, "\n");
+    }
     query_result r;
     r.best = hq->best;
     r.lid = hq->lid;

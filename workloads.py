@@ -120,16 +120,21 @@ def cfg5_descriptors(n: int, D: int, nq: int, seed: int = 5, dims_in: int = 125,
     rng = np.random.default_rng(seed)
     Q, _ = np.linalg.qr(rng.normal(size=(dims_in, dims_in)))
     scale = 0.9 ** (np.arange(dims_in) / 2.0)
-    y = rng.standard_normal((n, D), dtype=np.float32) * scale[:D].astype(np.float32)
-    lo, hi = y.min(0).astype(np.float64), y.max(0).astype(np.float64)
+    y = rng.standard_normal((n, D), dtype=np.float32)
+    y *= scale[:D].astype(np.float32)
+    lo, hi = y.min(0), y.max(0)
+    inv = (255.0 / (hi - lo)).astype(np.float32)
 
     def quant(v):
-        c = np.clip(v, lo, hi)
-        return np.floor(255.0 * (c - lo) / (hi - lo) + 0.5).astype(np.uint8)
+        c = np.clip(v.astype(np.float32), lo, hi)
+        c -= lo
+        c *= inv
+        c += np.float32(0.5)
+        return np.floor(c).astype(np.uint8)
 
     coords = np.empty((n, D), dtype=np.uint8)
-    for b in range(0, n, 1 << 20):
-        coords[b:b + (1 << 20)] = quant(y[b:b + (1 << 20)].astype(np.float64))
+    for b in range(0, n, 1 << 21):
+        coords[b:b + (1 << 21)] = quant(y[b:b + (1 << 21)])
     zq = rng.standard_normal((nq, dims_in))
     xq = (zq * scale) @ Q.T
     xq[rng.random((nq, dims_in)) < miss] = 0.0  # unknown -> mean (the distribution mean is 0)
