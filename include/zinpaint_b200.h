@@ -96,7 +96,8 @@ typedef struct {
     int32_t patch_size;
     int32_t width, height;
     double build_seconds;      /* device time of the last build (events) */
-    double eigen_seconds;      /* host eigen-solve part of it */
+    double eigen_seconds;      /* host wall time spent in the eigen-solve step (launch or host solve) */
+    int32_t pca_on_device;     /* 1: covariance + eigen-solve ran in k_pca (mc <= 224), 0: host solve */
 } zi_multi_index_info;
 
 typedef struct zi_ctx zi_ctx;                 /* one device + one stream + scratch */

@@ -54,7 +54,8 @@ class RunStats(C.Structure):
 class MultiIndexInfo(C.Structure):
     _fields_ = [("n", C.c_uint64), ("dims", C.c_int32), ("m", C.c_int32), ("channels", C.c_int32),
                 ("patch_size", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
-                ("build_seconds", C.c_double), ("eigen_seconds", C.c_double)]
+                ("build_seconds", C.c_double), ("eigen_seconds", C.c_double),
+                ("pca_on_device", C.c_int32)]
 
 
 # name -> (restype, argtypes); mirrors include/zinpaint_b200.h one to one

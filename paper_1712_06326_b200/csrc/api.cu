@@ -456,6 +456,7 @@ zi_status zi_multi_index_get_info(const zi_multi_index* mi, zi_multi_index_info*
         info->height = mi->h;
         info->build_seconds = mi->build_ms * 1e-3;
         info->eigen_seconds = mi->eigen_s;
+        info->pca_on_device = mi->device_pca ? 1 : 0;
     });
 }
 
@@ -470,6 +471,7 @@ zi_status zi_multi_index_layout(zi_multi_index* mi, int32_t layout, int32_t* rc,
                                 double* eigenvalues, double* lo, double* hi) {
     return guard([&] {
         require(layout >= 0 && layout < 8, "layout id must be in [0, 8)");
+        zi::sync_host_model(mi);
         const auto& L = mi->L[layout];
         if (rc) std::memcpy(rc, L.rc.data(), L.rc.size() * sizeof(int32_t));
         if (mean) std::memcpy(mean, L.mean.data(), L.mean.size() * sizeof(double));
@@ -496,6 +498,7 @@ zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index*
 
 zi_status zi_multi_index_moments(zi_multi_index* mi, int64_t* s_out, int64_t* S_out) {
     return guard([&] {
+        zi::sync_host_model(mi);
         if (s_out) std::memcpy(s_out, mi->s.data(), mi->s.size() * sizeof(int64_t));
         if (S_out) std::memcpy(S_out, mi->S.data(), mi->S.size() * sizeof(int64_t));
     });

@@ -4,17 +4,64 @@
 //   K1 collect_dictionary -> n keys (row-major)                       builder.cpp:74-108
 //   K2 exact int64 moments of the full K*K*C vector (one Gram serves
 //      all 8 layouts: each layout's covariance is a sub-block)        pca.cpp:20-37
-//   host: 8 eigen-solves in parallel threads (host_pca.cpp)            pca.cpp:39-67
+//   8 covariance + eigen-solves, one CTA per layout (k_pca.cu; host
+//      fallback host_pca.cpp when mc > 224 or ZI_HOST_PCA is set)      pca.cpp:39-67
 //   per layout: K3 project (fp64 canonical) -> min/max -> quantise +
 //      Morton interleave -> K4 onesweep radix sort -> K5 finalize      builder.cpp:159-195
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <thread>
 #include <vector>
 
 #include "common.cuh"
 
 namespace zi {
+
+// device moments -> host s, S (full symmetric; k_moments computes tile pairs ti <= tj only)
+static void sync_moments(zi_multi_index* mi) {
+    zi_ctx* ctx = mi->ctx;
+    const int F = mi->F;
+    const size_t nmom = static_cast<size_t>(F) + static_cast<size_t>(F) * F;
+    unsigned long long* hm = mi->hmom.ensure(nmom);
+    ZI_CUDA(cudaMemcpyAsync(hm, mi->moments.p, nmom * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    mi->s.assign(F, 0);
+    mi->S.assign(static_cast<size_t>(F) * F, 0);
+    for (int i = 0; i < F; ++i) mi->s[i] = static_cast<int64_t>(hm[i]);
+    constexpr int kTile = 128;
+    for (int i = 0; i < F; ++i)
+        for (int j = 0; j < F; ++j) {
+            const int a = (i / kTile <= j / kTile) ? i : j, b = (i / kTile <= j / kTile) ? j : i;
+            mi->S[static_cast<size_t>(i) * F + j] = static_cast<int64_t>(hm[F + static_cast<size_t>(a) * F + b]);
+        }
+}
+
+void sync_host_model(zi_multi_index* mi) {
+    if (mi->host_model || mi->n == 0) return;
+    zi_ctx* ctx = mi->ctx;
+    const int mc = mi->mc, D = mi->dims;
+    sync_moments(mi);
+    std::vector<double> hmean(static_cast<size_t>(8) * mc), hcomp(static_cast<size_t>(8) * mc * D),
+        heig(static_cast<size_t>(8) * D);
+    ZI_CUDA(cudaMemcpyAsync(hmean.data(), mi->pca_mean.p, hmean.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(hcomp.data(), mi->pca_comp.p, hcomp.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(heig.data(), mi->pca_eig.p, heig.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int l = 0; l < 8; ++l) {
+        auto& L = mi->L[l];
+        L.mean.assign(hmean.begin() + static_cast<size_t>(l) * mc, hmean.begin() + static_cast<size_t>(l + 1) * mc);
+        L.comp.assign(static_cast<size_t>(D) * mc, 0.0);
+        for (int j = 0; j < mc; ++j)
+            for (int d = 0; d < D; ++d)
+                L.comp[static_cast<size_t>(d) * mc + j] = hcomp[(static_cast<size_t>(l) * mc + j) * D + d];
+        L.eig.assign(heig.begin() + static_cast<size_t>(l) * D, heig.begin() + static_cast<size_t>(l + 1) * D);
+    }
+    mi->host_model = true;
+}
 
 void build_multi_index(zi_multi_index* mi) {
     zi_ctx* ctx = mi->ctx;
@@ -43,46 +90,61 @@ void build_multi_index(zi_multi_index* mi) {
     const size_t nmom = static_cast<size_t>(F) + static_cast<size_t>(F) * F;
     mi->moments.ensure(nmom);
     patch_moments(ctx, mi->image.p, w, C, K, mi->dict.p, n, mi->moments.p);
-    unsigned long long* hm = mi->hmom.ensure(nmom);
-    ZI_CUDA(cudaMemcpyAsync(hm, mi->moments.p, nmom * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
-    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
-    mi->s.assign(F, 0);
-    mi->S.assign(static_cast<size_t>(F) * F, 0);
-    for (int i = 0; i < F; ++i) mi->s[i] = static_cast<int64_t>(hm[i]);
-    constexpr int kTile = 128;  // k_moments computes tile pairs ti <= tj only
-    for (int i = 0; i < F; ++i)
-        for (int j = 0; j < F; ++j) {
-            const int a = (i / kTile <= j / kTile) ? i : j, b = (i / kTile <= j / kTile) ? j : i;
-            mi->S[static_cast<size_t>(i) * F + j] = static_cast<int64_t>(hm[F + static_cast<size_t>(a) * F + b]);
-        }
-
-    // host eigen-solves, one thread per layout
+    mi->pca_mean.ensure(static_cast<size_t>(8) * mc);
+    mi->pca_comp.ensure(static_cast<size_t>(8) * mc * D);
+    mi->host_model = false;
     const auto te0 = std::chrono::steady_clock::now();
-    std::vector<std::thread> th;
-    for (int l = 0; l < 8; ++l) {
-        th.emplace_back([mi, l, F, n, D, C, K, m] {
-            auto& L = mi->L[l];
-            std::vector<int32_t> cols;
-            for (int p = 0; p < m; ++p)
-                for (int ch = 0; ch < C; ++ch) cols.push_back((L.rc[2 * p] * K + L.rc[2 * p + 1]) * C + ch);
-            pca_fit_layout(mi->s, mi->S, F, n, cols, D, L.mean, L.comp, L.eig);
-        });
+    static const bool host_pca = std::getenv("ZI_HOST_PCA") != nullptr;
+    bool on_device = false;
+    if (!host_pca) {
+        if (!mi->pca_cols_ready) {
+            std::vector<int32_t> hc;
+            for (int l = 0; l < 8; ++l)
+                for (int p = 0; p < m; ++p)
+                    for (int ch = 0; ch < C; ++ch)
+                        hc.push_back((mi->L[l].rc[2 * p] * K + mi->L[l].rc[2 * p + 1]) * C + ch);
+            mi->pca_cols.ensure(hc.size());
+            ZI_CUDA(cudaMemcpy(mi->pca_cols.p, hc.data(), hc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            mi->pca_cols_ready = true;
+        }
+        mi->pca_eig.ensure(static_cast<size_t>(8) * 32);
+        mi->pca_work.ensure(pca_work_doubles(mc, D));
+        mi->pca_status.ensure(8);
+        on_device = pca_on_device(ctx, mi->moments.p, F, n, mi->pca_cols.p, mc, D, mi->pca_mean.p, mi->pca_comp.p,
+                                  mi->pca_eig.p, mi->pca_work.p, mi->pca_status.p);
     }
-    for (auto& t : th) t.join();
+    mi->device_pca = on_device;
+    if (!on_device) {
+        // host eigen-solves, one thread per layout
+        sync_moments(mi);
+        std::vector<std::thread> th;
+        for (int l = 0; l < 8; ++l) {
+            th.emplace_back([mi, l, F, n, D, C, K, m] {
+                auto& L = mi->L[l];
+                std::vector<int32_t> cols;
+                for (int p = 0; p < m; ++p)
+                    for (int ch = 0; ch < C; ++ch) cols.push_back((L.rc[2 * p] * K + L.rc[2 * p + 1]) * C + ch);
+                pca_fit_layout(mi->s, mi->S, F, n, cols, D, L.mean, L.comp, L.eig);
+            });
+        }
+        for (auto& t : th) t.join();
+        // upload the 8 models: mean [l][j], comp [l][j][d]
+        std::vector<double> hmean(static_cast<size_t>(8) * mc), hcomp(static_cast<size_t>(8) * mc * D);
+        for (int l = 0; l < 8; ++l) {
+            std::copy(mi->L[l].mean.begin(), mi->L[l].mean.end(), hmean.begin() + static_cast<size_t>(l) * mc);
+            for (int j = 0; j < mc; ++j)
+                for (int d = 0; d < D; ++d)
+                    hcomp[(static_cast<size_t>(l) * mc + j) * D + d] = mi->L[l].comp[static_cast<size_t>(d) * mc + j];
+        }
+        ZI_CUDA(cudaMemcpyAsync(mi->pca_mean.p, hmean.data(), hmean.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        ZI_CUDA(cudaMemcpyAsync(mi->pca_comp.p, hcomp.data(), hcomp.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));  // hmean / hcomp are pageable locals
+        mi->host_model = true;
+    }
     mi->eigen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - te0).count();
 
-    // upload the 8 models: mean [l][j], comp [l][j][d]
-    std::vector<double> hmean(static_cast<size_t>(8) * mc), hcomp(static_cast<size_t>(8) * mc * D);
-    for (int l = 0; l < 8; ++l) {
-        std::copy(mi->L[l].mean.begin(), mi->L[l].mean.end(), hmean.begin() + static_cast<size_t>(l) * mc);
-        for (int j = 0; j < mc; ++j)
-            for (int d = 0; d < D; ++d)
-                hcomp[(static_cast<size_t>(l) * mc + j) * D + d] = mi->L[l].comp[static_cast<size_t>(d) * mc + j];
-    }
-    mi->pca_mean.ensure(hmean.size());
-    mi->pca_comp.ensure(hcomp.size());
-    ZI_CUDA(cudaMemcpyAsync(mi->pca_mean.p, hmean.data(), hmean.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    ZI_CUDA(cudaMemcpyAsync(mi->pca_comp.p, hcomp.data(), hcomp.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     mi->minmax.ensure(static_cast<size_t>(8) * 2 * D);
 
     // per layout: project, lo/hi, quantise + interleave into one 8n-record array; then ONE

@@ -1,0 +1,563 @@
+// k_pca.cu -- the PCA fit of the 8 layout indices on the device (proj/src/pca.cpp:26-67).
+//
+// Input: the exact int64 moments (s, S) of the full K*K*C patch vector (k_build.cu).  Each
+// layout's covariance cov_ij = (n*S_ij - s_i*s_j) / (n*(n-1)) comes from the int128 numerator with
+// a correctly rounded int128 -> double conversion.  Three kernels, no host round trip:
+//
+//   k_pca_tri  one 8-CTA thread-block cluster per layout.  Householder tridiagonalisation with the
+//              full symmetric matrix distributed by rows over the cluster (row i on CTA i % 8, 28
+//              rows x 219 columns = 48 KB per CTA).  Per column: the pivot row's owner forms the
+//              reflector and broadcasts it through distributed shared memory; every CTA forms its
+//              rows of p = tau*A*v and broadcasts them; after a second cluster barrier every CTA
+//              applies the rank-2 update to its own rows.  v / p are double-buffered by column
+//              parity so two cluster barriers per column suffice.  Writes d, e, tau, reflectors.
+//   k_pca_vec  one CTA per (layout, component): the reflectors stream into shared memory by one
+//              TMA bulk copy while 128 lanes run multisection on Sturm counts for lambda_j; one
+//              thread then runs inverse iteration (LU factored once, 3 solves); one warp applies
+//              the reflectors with the vector held in registers.
+//   k_pca_fin  one CTA per layout: Gram-Schmidt inside clusters of close eigenvalues, the
+//              reference's sign rule (first max-|v| entry positive), eigenvalue clamp at 0, and
+//              the components written straight into the projection kernels' [j][d] layout.
+// The host eigen-solver (host_pca.cpp) remains for m*C > 224.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace zi {
+
+namespace cg = cooperative_groups;
+
+constexpr int kCl = 8;             // CTAs per layout (one cluster)
+constexpr int kTriThreads = 256;
+constexpr int kVecThreads = 128;
+constexpr int kPcaMaxN = 224;
+constexpr int kSlots = (kPcaMaxN + 31) / 32;  // vector entries per lane in the back-transform
+
+// reflector k (entries k+1 .. n-1 of column k) starts at refl_off(k)
+__host__ __device__ inline size_t refl_off(int k, int n) {
+    return static_cast<size_t>(k) * static_cast<size_t>(2 * n - k - 1) / 2;
+}
+__host__ __device__ inline size_t refl_stride(int n) { return (refl_off(n - 2, n) + 1) & ~static_cast<size_t>(1); }
+
+// correctly rounded (RN) conversion of a signed 128-bit integer
+__device__ inline double i128_to_double(__int128 x) {
+    if (x == 0) return 0.0;
+    const bool neg = x < 0;
+    unsigned __int128 u = neg ? static_cast<unsigned __int128>(-x) : static_cast<unsigned __int128>(x);
+    const unsigned long long hi = static_cast<unsigned long long>(u >> 64);
+    double r;
+    if (hi == 0) {
+        r = __ull2double_rn(static_cast<unsigned long long>(u));
+    } else {
+        const int lz = __clzll(hi);           // normalise so bit 127 is set
+        u <<= lz;
+        unsigned long long top = static_cast<unsigned long long>(u >> 64);
+        const unsigned long long rest = static_cast<unsigned long long>(u);
+        top |= rest != 0 ? 1ull : 0ull;       // sticky: 64 >= 53 + 2 bits, one RN is exact
+        r = scalbn(__ull2double_rn(top), 64 - lz);
+    }
+    return neg ? -r : r;
+}
+
+// 1/x to full double precision: MUFU seed + two Newton steps (no IEEE division on the chains)
+__device__ inline double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+// number of eigenvalues of T below x (Sturm sequence in ratio form, pivmin guard as dstebz)
+__device__ int sturm_count_dev(const double* d, const double* e2, int n, double x, double pivmin) {
+    int cnt = 0;
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0;
+    for (int i = 1; i < n; ++i) {
+        q = (d[i] - x) - e2[i - 1] * fast_rcp(q);
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0;
+    }
+    return cnt;
+}
+
+// LU of (T - sigma I) with partial pivoting, factored once per eigenvector:
+//   u1i = 1 / pivot, u2/u3 the two super-diagonals of U, mult the multipliers, piv the row swaps
+__device__ void tri_factor(const double* d, const double* e, int n, double sigma, double tiny, double* u1i,
+                           double* u2, double* u3, double* mult, unsigned char* piv) {
+    double dcur = d[0] - sigma;
+    double scur = n > 1 ? e[0] : 0.0;
+    for (int i = 0; i + 1 < n; ++i) {
+        const double a = e[i];
+        const double bn = d[i + 1] - sigma;
+        const double cn = i + 2 < n ? e[i + 1] : 0.0;
+        if (fabs(dcur) >= fabs(a)) {
+            if (dcur == 0.0) dcur = tiny;
+            const double r = fast_rcp(dcur);
+            const double m = a * r;
+            u1i[i] = fabs(dcur) < tiny ? fast_rcp(dcur < 0 ? -tiny : tiny) : r;
+            u2[i] = scur;
+            u3[i] = 0.0;
+            mult[i] = m;
+            piv[i] = 0;
+            dcur = bn - m * scur;
+            scur = cn;
+        } else {
+            const double r = fast_rcp(a);
+            const double m = dcur * r;
+            u1i[i] = fabs(a) < tiny ? fast_rcp(a < 0 ? -tiny : tiny) : r;
+            u2[i] = bn;
+            u3[i] = cn;
+            mult[i] = m;
+            piv[i] = 1;
+            dcur = scur - m * bn;
+            scur = -m * cn;
+        }
+    }
+    if (dcur == 0.0) dcur = tiny;
+    u1i[n - 1] = fast_rcp(fabs(dcur) < tiny ? (dcur < 0 ? -tiny : tiny) : dcur);
+}
+
+// b := (T - sigma I)^-1 b with the factors above; the recurrences carry their state in registers.
+// Returns max |b_i| of the result.
+__device__ double tri_apply(const double* u1i, const double* u2, const double* u3, const double* mult,
+                            const unsigned char* piv, int n, double* b) {
+    double cur = b[0];
+    for (int i = 0; i + 1 < n; ++i) {
+        double nxt = b[i + 1];
+        if (piv[i]) {
+            const double t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+        b[i] = cur;
+        cur = nxt - mult[i] * cur;
+    }
+    b[n - 1] = cur;
+    double x1 = 0.0, x2 = 0.0, mx = 0.0;
+    for (int i = n - 1; i >= 0; --i) {
+        const double xi = (b[i] - u2[i] * x1 - u3[i] * x2) * u1i[i];
+        b[i] = xi;
+        mx = fmax(mx, fabs(xi));
+        x2 = x1;
+        x1 = xi;
+    }
+    return mx;
+}
+
+__device__ inline void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// CTA-wide sum (fixed order -> deterministic), result in every thread
+template <int T>
+__device__ inline double cta_sum(double v, double* s_red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < T / 32; ++i) t += s_red[i];
+    return t;
+}
+
+__device__ inline double warp_allsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// work buffer layout (doubles), see pca_work_doubles
+struct pca_work_view {
+    double *d, *e, *tau, *tn, *lam, *X, *refl;
+    size_t rstride;
+};
+__host__ __device__ inline pca_work_view pca_work_split(double* w, int n, int D) {
+    pca_work_view v;
+    v.d = w;
+    v.e = v.d + 8 * n;
+    v.tau = v.e + 8 * n;
+    v.tn = v.tau + 8 * n;
+    v.lam = v.tn + 8;
+    v.X = v.lam + 8 * 32;
+    v.refl = v.X + static_cast<size_t>(8) * D * n;
+    v.refl += (reinterpret_cast<uintptr_t>(v.refl) & 15) ? 1 : 0;  // 16-byte aligned for TMA
+    v.rstride = refl_stride(n);
+    return v;
+}
+size_t pca_work_doubles(int mc, int D) {
+    return static_cast<size_t>(8) * (3 * mc + 1 + 32 + static_cast<size_t>(D) * mc) + 8 * refl_stride(mc) + 4;
+}
+
+struct tri_args {
+    const unsigned long long* moments;  // F (s) + F*F (S), int64 values, tile pairs ti <= tj
+    int F;
+    unsigned long long n;
+    const int32_t* cols;  // 8 * mc feature indices (layout-major)
+    int mc;
+    double* mean;  // 8 * mc
+    pca_work_view w;
+};
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca_tri(tri_args a) {
+    extern __shared__ double sm[];
+    __shared__ double s_red[kTriThreads / 32];
+    cg::cluster_group cl = cg::this_cluster();
+    const int n = a.mc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kTriThreads / 32;
+    const int rank = static_cast<int>(cl.block_rank());
+    const int l = blockIdx.x / kCl;
+    const int rows_max = (n + kCl - 1) / kCl;
+    const int nloc = rank < n ? (n - rank + kCl - 1) / kCl : 0;  // my rows: i = rank + kCl * li
+    double* A = sm;                                          // rows_max x n, full rows
+    double* v = A + static_cast<size_t>(rows_max) * n;       // [2][n] reflector, by column parity
+    double* p = v + 2 * n;                                   // [2][n] tau * A v
+    double* vpp = p + 2 * n;                                 // [2][kCl] per-CTA partials of v.p
+    double* scal = vpp + 2 * kCl;                            // [2][2] tau, alpha
+    const long long* s = reinterpret_cast<const long long*>(a.moments);
+    const long long* S = s + a.F;
+    const long long nn = static_cast<long long>(a.n);
+    const int32_t* cols = a.cols + l * n;
+    const double den = a.n > 1 ? static_cast<double>(a.n) * static_cast<double>(a.n - 1) : 1.0;
+    for (int idx = tid; idx < nloc * n; idx += kTriThreads) {
+        const int li = idx / n, j = idx - li * n, i = rank + kCl * li;
+        int ca = cols[i], cb = cols[j];
+        if (ca / 128 > cb / 128) {  // k_moments fills the 128x128 tile pairs ti <= tj only
+            const int t = ca;
+            ca = cb;
+            cb = t;
+        }
+        const __int128 num = static_cast<__int128>(nn) * S[static_cast<long long>(ca) * a.F + cb] -
+                             static_cast<__int128>(s[cols[i]]) * s[cols[j]];
+        A[idx] = i128_to_double(num) / den;
+    }
+    if (rank == 0)
+        for (int i = tid; i < n; i += kTriThreads)
+            a.mean[l * n + i] = static_cast<double>(s[cols[i]]) / static_cast<double>(a.n);
+    double* d_out = a.w.d + l * n;
+    double* e_out = a.w.e + l * n;
+    double* tau_out = a.w.tau + l * n;
+    double* refl = a.w.refl + l * a.w.rstride;
+    __syncthreads();
+    cluster_barrier();  // every CTA of the cluster runs before the first DSMEM store
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1, b = k & 1;
+        if (rank == k % kCl) {  // pivot row owner: reflector of column k (= row k right of the diagonal)
+            const double* row = A + static_cast<size_t>(k / kCl) * n + k + 1;
+            double part = 0.0;
+            for (int j = tid; j < m; j += kTriThreads) part = fma(row[j], row[j], part);
+            const double norm2 = cta_sum<kTriThreads>(part, s_red);
+            const double x0 = row[0];
+            double alpha = x0, tk = 0.0;
+            if (norm2 != 0.0) {
+                alpha = x0 >= 0 ? -sqrt(norm2) : sqrt(norm2);
+                tk = 1.0 / (norm2 - alpha * x0);  // 2 / |x - alpha e1|^2
+            }
+            for (int idx = tid; idx < m * kCl; idx += kTriThreads) {
+                const int j = idx / kCl, r = idx % kCl;
+                const double vj = (j == 0 && tk != 0.0) ? x0 - alpha : row[j];
+                cl.map_shared_rank(v, r)[b * n + j] = vj;
+                if (r == 0) refl[refl_off(k, n) + j] = vj;
+            }
+            if (tid < kCl) {
+                double* rs = cl.map_shared_rank(scal, tid);
+                rs[2 * b] = tk;
+                rs[2 * b + 1] = alpha;
+            }
+            if (tid == 0) {
+                e_out[k] = alpha;
+                tau_out[k] = tk;
+            }
+        }
+        cluster_barrier();
+        const double tk = scal[2 * b];
+        if (tk == 0.0) continue;  // column already reduced (uniform over the cluster)
+        const double* vb = v + b * n;
+        const int li0 = k + 1 > rank ? (k + 1 - rank + kCl - 1) / kCl : 0;  // first trailing row
+        double myvp = 0.0;
+        for (int li = li0 + warp; li < nloc; li += kWarps) {
+            const int t = rank + kCl * li - k - 1;
+            const double* row = A + static_cast<size_t>(li) * n + k + 1;
+            double acc = 0.0;
+            for (int j = lane; j < m; j += 32) acc = fma(row[j], vb[j], acc);
+            const double pt = tk * warp_allsum(acc);
+            if (lane < kCl) cl.map_shared_rank(p, lane)[b * n + t] = pt;
+            if (lane == 0) myvp = fma(vb[t], pt, myvp);
+        }
+        const double cvp = cta_sum<kTriThreads>(myvp, s_red);
+        if (tid < kCl) cl.map_shared_rank(vpp, tid)[b * kCl + rank] = cvp;
+        cluster_barrier();
+        double vp = 0.0;
+#pragma unroll
+        for (int r = 0; r < kCl; ++r) vp += vpp[b * kCl + r];
+        const double K2 = 0.5 * tk * vp;
+        const double* pb = p + b * n;
+        // A22 -= v w^T + w v^T, w = p - K2 v, on my full rows
+        for (int li = li0 + warp; li < nloc; li += kWarps) {
+            const int t = rank + kCl * li - k - 1;
+            double* row = A + static_cast<size_t>(li) * n + k + 1;
+            const double vt = vb[t], wt = fma(-K2, vt, pb[t]);
+            for (int j = lane; j < m; j += 32) {
+                const double wj = fma(-K2, vb[j], pb[j]);
+                row[j] = fma(-vt, wj, fma(-wt, vb[j], row[j]));
+            }
+        }
+        __syncthreads();
+    }
+    for (int li = tid; li < nloc; li += kTriThreads) {
+        const int i = rank + kCl * li;
+        d_out[i] = A[static_cast<size_t>(li) * n + i];
+        if (i == n - 1) {
+            e_out[n - 2] = A[static_cast<size_t>(li) * n + n - 2];
+            tau_out[n - 2] = 0.0;
+        }
+    }
+    cluster_barrier();  // no CTA leaves while a peer may still store into its shared memory
+}
+
+struct vec_args {
+    int mc, D;
+    pca_work_view w;
+};
+
+__device__ inline unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ int s_first[kVecThreads / 32];
+    __shared__ double s_scal[4];
+    const int n = a.mc, D = a.D, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int l = blockIdx.x / D, j = blockIdx.x % D;
+    const size_t nref = a.w.rstride;
+    double* R = sm;         // reflectors (TMA)
+    double* dd = R + nref;  // n
+    double* ee = dd + n;    // n
+    double* e2 = ee + n;    // n
+    double* tau = e2 + n;   // n
+    double* x = tau + n;    // n
+    double* f = x + n;      // 4n LU factors
+    unsigned char* piv = reinterpret_cast<unsigned char*>(f + 4 * n);
+    const double* src = a.w.refl + l * a.w.rstride;
+    const unsigned bytes = static_cast<unsigned>(nref * sizeof(double));
+    if (tid == 0) {
+        const unsigned bar = smem_u32(&s_bar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(R)),
+                     "l"(src), "r"(bytes), "r"(bar)
+                     : "memory");
+    }
+    for (int i = tid; i < n; i += kVecThreads) {
+        dd[i] = a.w.d[l * n + i];
+        const double ei = i + 1 < n ? a.w.e[l * n + i] : 0.0;
+        ee[i] = ei;
+        e2[i] = ei * ei;
+        tau[i] = a.w.tau[l * n + i];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double tn = 0.0, glo = DBL_MAX, ghi = -DBL_MAX;
+        for (int i = 0; i < n; ++i) {
+            const double r = (i > 0 ? fabs(ee[i - 1]) : 0.0) + (i + 1 < n ? fabs(ee[i]) : 0.0);
+            tn = fmax(tn, fabs(dd[i]) + r);
+            glo = fmin(glo, dd[i] - r);
+            ghi = fmax(ghi, dd[i] + r);
+        }
+        const double safe = tn > 0 ? tn : 1.0;
+        const double pivmin = DBL_MIN * 1e4 * fmax(1.0, safe * safe);
+        s_scal[0] = safe;
+        s_scal[1] = pivmin;
+        s_scal[2] = glo - 2 * DBL_EPSILON * safe - pivmin;
+        s_scal[3] = ghi + 2 * DBL_EPSILON * safe + pivmin;
+        if (j == 0) a.w.tn[l] = safe;
+    }
+    __syncthreads();
+    const double safe = s_scal[0], pivmin = s_scal[1];
+    // lambda_j (j-th largest) by multisection: 128 points per round
+    const int target = n - 1 - j;
+    double lo = s_scal[2], hi = s_scal[3];
+    for (int it = 0; it < 64; ++it) {
+        if (hi - lo <= 2 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+        const double xq = lo + (hi - lo) * (tid + 1) / static_cast<double>(kVecThreads + 1);
+        const bool above = sturm_count_dev(dd, e2, n, xq, pivmin) > target;
+        const unsigned bal = __ballot_sync(0xffffffffu, above);
+        if (lane == 0) s_first[warp] = bal ? warp * 32 + __ffs(bal) - 1 : kVecThreads;
+        __syncthreads();
+        int c = kVecThreads;
+#pragma unroll
+        for (int w = 0; w < kVecThreads / 32; ++w) c = min(c, s_first[w]);
+        __syncthreads();
+        const double nlo = c > 0 ? lo + (hi - lo) * c / static_cast<double>(kVecThreads + 1) : lo;
+        const double nhi = c < kVecThreads ? lo + (hi - lo) * (c + 1) / static_cast<double>(kVecThreads + 1) : hi;
+        if (!(nlo < nhi) || (nlo == lo && nhi == hi)) break;
+        lo = nlo;
+        hi = nhi;
+    }
+    const double lam = 0.5 * (lo + hi);
+    // inverse iteration: LU of (T - lambda I) once, three solves from a pseudo-random start
+    if (tid == 0) {
+        const double tiny = DBL_EPSILON * safe;
+        tri_factor(dd, ee, n, lam, tiny, f, f + n, f + 2 * n, f + 3 * n, piv);
+        for (int i = 0; i < n; ++i) {  // splitmix64: starts differ per component
+            unsigned long long z = (static_cast<unsigned long long>(j) << 32 | static_cast<unsigned>(i)) +
+                                   0x9E3779B97F4A7C15ull;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            z ^= z >> 31;
+            x[i] = static_cast<double>(z >> 11) * 0x1.0p-53 - 0.5;
+        }
+        for (int it = 0; it < 3; ++it) {
+            const double mx = tri_apply(f, f + n, f + 2 * n, f + 3 * n, piv, n, x);
+            const double sc = mx > 0.0 ? fast_rcp(mx) : 1.0;
+            for (int i = 0; i < n; ++i) x[i] *= sc;
+        }
+        double nrm = 0.0;
+        for (int i = 0; i < n; ++i) nrm = fma(x[i], x[i], nrm);
+        const double inv = 1.0 / sqrt(nrm);
+        for (int i = 0; i < n; ++i) x[i] *= inv;
+        a.w.lam[l * 32 + j] = lam;
+    }
+    __syncthreads();
+    // back-transformation x = H_0 ... H_{n-3} x, one warp, the vector in registers
+    if (warp == 0) {
+        const unsigned bar = smem_u32(&s_bar);
+        asm volatile(
+            "{\n .reg .pred P1;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+            " @!P1 bra WAIT_%=;\n}\n" ::"r"(bar)
+            : "memory");
+        double xr[kSlots];
+#pragma unroll
+        for (int q = 0; q < kSlots; ++q) xr[q] = lane + 32 * q < n ? x[lane + 32 * q] : 0.0;
+        for (int k = n - 3; k >= 0; --k) {
+            const double tk = tau[k];
+            if (tk == 0.0) continue;
+            const double* r = R + refl_off(k, n) - (k + 1);  // r[i], i > k
+            double part = 0.0;
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) {
+                const int i = lane + 32 * q;
+                if (i > k && i < n) part = fma(r[i], xr[q], part);
+            }
+            const double fct = tk * warp_allsum(part);
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) {
+                const int i = lane + 32 * q;
+                if (i > k && i < n) xr[q] = fma(-fct, r[i], xr[q]);
+            }
+        }
+        double* out = a.w.X + (static_cast<size_t>(l) * D + j) * n;
+#pragma unroll
+        for (int q = 0; q < kSlots; ++q)
+            if (lane + 32 * q < n) out[lane + 32 * q] = xr[q];
+    }
+}
+
+struct fin_args {
+    int mc, D;
+    pca_work_view w;
+    double* comp;  // 8 * mc * D, [l][i][d]
+    double* eig;   // 8 * D
+};
+
+__global__ void __launch_bounds__(256) k_pca_fin(fin_args a) {
+    extern __shared__ double sm[];
+    __shared__ double s_red[8];
+    const int n = a.mc, D = a.D, l = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* X = sm;  // D x n
+    const double* lam = a.w.lam + l * 32;
+    for (int i = tid; i < D * n; i += 256) X[i] = a.w.X[static_cast<size_t>(l) * D * n + i];
+    __syncthreads();
+    const double cluster = 1e-3 * a.w.tn[l];
+    // Gram-Schmidt inside clusters of close eigenvalues (component j against the earlier ones)
+    for (int j = 1; j < D; ++j) {
+        for (int q = 0; q < j; ++q) {
+            if (fabs(lam[q] - lam[j]) > cluster) continue;
+            double* xj = X + static_cast<size_t>(j) * n;
+            const double* xq = X + static_cast<size_t>(q) * n;
+            double part = 0.0;
+            for (int i = tid; i < n; i += 256) part = fma(xq[i], xj[i], part);
+            const double dot = cta_sum<256>(part, s_red);
+            for (int i = tid; i < n; i += 256) xj[i] = fma(-dot, xq[i], xj[i]);
+            __syncthreads();
+            part = 0.0;
+            for (int i = tid; i < n; i += 256) part = fma(xj[i], xj[i], part);
+            const double inv = 1.0 / sqrt(cta_sum<256>(part, s_red));
+            for (int i = tid; i < n; i += 256) xj[i] *= inv;
+            __syncthreads();
+        }
+    }
+    // sign rule: the first entry of largest magnitude is positive (strict '>' keeps the earliest)
+    for (int j = warp; j < D; j += 8) {
+        const double* x = X + static_cast<size_t>(j) * n;
+        double best = -1.0;
+        int arg = 0;
+        for (int i = lane; i < n; i += 32) {
+            const double ax = fabs(x[i]);
+            if (ax > best) {
+                best = ax;
+                arg = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+            if (ob > best || (ob == best && oa < arg)) {
+                best = ob;
+                arg = oa;
+            }
+        }
+        const double sgn = x[arg] < 0 ? -1.0 : 1.0;
+        for (int i = lane; i < n; i += 32) a.comp[(static_cast<size_t>(l) * n + i) * D + j] = sgn * x[i];
+        if (lane == 0) a.eig[l * D + j] = fmax(0.0, lam[j]);
+    }
+}
+
+bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint64_t n, const int32_t* d_cols, int mc,
+                   int D, double* d_mean, double* d_comp, double* d_eig, double* d_work, int* /*d_status*/) {
+    if (mc > kPcaMaxN || D > 32 || mc < 3) return false;
+    static int optin = -1;
+    if (optin < 0) ZI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    const size_t limit = static_cast<size_t>(optin) - 1024;
+    const int rows_max = (mc + kCl - 1) / kCl;
+    const size_t smem_tri = (static_cast<size_t>(rows_max) * mc + 4 * mc + 2 * kCl + 4) * sizeof(double);
+    const size_t smem_vec = (refl_stride(mc) + 9 * static_cast<size_t>(mc)) * sizeof(double) + mc + 16;
+    const size_t smem_fin = static_cast<size_t>(D) * mc * sizeof(double);
+    if (smem_tri > limit || smem_vec > limit || smem_fin > limit) return false;
+    static size_t attr_tri = 0, attr_vec = 0, attr_fin = 0;
+    if (smem_tri > attr_tri) {
+        ZI_CUDA(cudaFuncSetAttribute(k_pca_tri, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_tri)));
+        attr_tri = smem_tri;
+    }
+    if (smem_vec > attr_vec) {
+        ZI_CUDA(cudaFuncSetAttribute(k_pca_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_vec)));
+        attr_vec = smem_vec;
+    }
+    if (smem_fin > attr_fin) {
+        ZI_CUDA(cudaFuncSetAttribute(k_pca_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_fin)));
+        attr_fin = smem_fin;
+    }
+    const pca_work_view w = pca_work_split(d_work, mc, D);
+    tri_args ta{d_moments, F, n, d_cols, mc, d_mean, w};
+    ZI_LAUNCH(ctx, "pca_tridiag", k_pca_tri, 8 * kCl, kTriThreads, smem_tri, ta);
+    vec_args va{mc, D, w};
+    ZI_LAUNCH(ctx, "pca_vectors", k_pca_vec, 8 * D, kVecThreads, smem_vec, va);
+    fin_args fa{mc, D, w, d_comp, d_eig};
+    ZI_LAUNCH(ctx, "pca_finish", k_pca_fin, 8, 256, smem_fin, fa);
+    return true;
+}
+
+}  // namespace zi

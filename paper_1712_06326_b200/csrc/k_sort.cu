@@ -185,7 +185,7 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
     const size_t hist_words = static_cast<size_t>(npass) * 256;
     const size_t status_words = static_cast<size_t>(npass) * ntiles * 256;
     uint32_t* scr = reinterpret_cast<uint32_t*>(
-        ctx->scratch.ensure((alt_words + 2 * hist_words + status_words + npass + 64) * sizeof(uint32_t)));
+        ctx->scratch.ensure((alt_words + 2 * hist_words + status_words + 4 * npass + 64) * sizeof(uint32_t)));
     uint32_t* alt = scr;
     uint32_t* hist = alt + alt_words;
     uint32_t* bases = hist + hist_words;

@@ -145,6 +145,13 @@ struct zi_multi_index {
     zi::hbuf<uint8_t> hstage;            // pinned staging for targets/results
     zi::hbuf<unsigned long long> hmom;
     std::vector<int64_t> s, S;           // host copy of the moments
+    // device PCA (k_pca.cu): feature columns [8][mc], eigenvalues [8][D], eigenvector scratch
+    zi::dbuf<int32_t> pca_cols;
+    zi::dbuf<double> pca_eig, pca_work;
+    zi::dbuf<int> pca_status;
+    bool pca_cols_ready = false;
+    bool host_model = false;             // s, S, L[].mean/comp/eig mirror the device copies
+    bool device_pca = false;             // last build solved the eigenproblems on the device
     zi_layout_state L[8];
 };
 
@@ -219,6 +226,13 @@ void pca_fit_layout(const std::vector<int64_t>& s, const std::vector<int64_t>& S
                     const std::vector<int32_t>& cols, int dims, std::vector<double>& mean,
                     std::vector<double>& comp /* dims*mc, row d */, std::vector<double>& eig);
 void build_multi_index(zi_multi_index* mi);
+// copy the moments and the 8 PCA models to the host mirror (lazy: only the accessors need it)
+void sync_host_model(zi_multi_index* mi);
+// k_pca.cu: covariance + eigen-solve of all 8 layouts on the device; false if mc is too large.
+// d_work must hold pca_work_doubles(mc, D) doubles.
+size_t pca_work_doubles(int mc, int D);
+bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint64_t n, const int32_t* d_cols, int mc,
+                   int D, double* d_mean, double* d_comp, double* d_eig, double* d_work, int* d_status);
 
 // fill loop (host_engine.cpp): run_loop / inpaint (proj/src/engine.cpp:283-506)
 void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known, const zi_index_config& cfg,

@@ -173,28 +173,57 @@ def test_moments_exact(zb, golden):
         assert np.array_equal(s, rs) and np.array_equal(S, rS), tag
 
 
+def _check_pca(mi, K, ch, tag):
+    s, S = mi.moments()
+    for l in range(8):
+        lay = mi.layout(l)
+        cols = oracle.layout_columns(lay["pixels"], K, ch)
+        mean, cov = oracle.layout_covariance(s, S, mi.n, cols)
+        assert np.array_equal(lay["mean"], mean), (tag, l)
+        comp, eig = oracle.pca_from_cov(cov, mi.dims)
+        np.testing.assert_allclose(lay["eigenvalues"], eig, rtol=1e-9, atol=1e-9 * eig[0])
+        # orthonormal, eigen-residual small, and equal to the oracle's where the spectrum is simple
+        C = lay["components"]
+        np.testing.assert_allclose(C @ C.T, np.eye(mi.dims), atol=1e-10)
+        res = cov @ C.T - C.T * lay["eigenvalues"]
+        assert np.abs(res).max() <= 1e-9 * max(1.0, eig[0]), (tag, l)
+        gaps = np.abs(np.diff(eig))
+        for d in range(mi.dims):
+            g = min(gaps[d - 1] if d > 0 else np.inf, gaps[d] if d < len(gaps) else np.inf)
+            if g > 1e-6 * eig[0]:
+                np.testing.assert_allclose(C[d], comp[d], atol=1e-7)
+            # reference sign rule: the first largest-magnitude entry is positive
+            i = int(np.argmax(np.abs(C[d])))
+            assert C[d][i] > 0, (tag, l, d)
+
+
 def test_pca_matches_oracle_fit(zb, golden):
     for tag, img, kn in _images(golden)[:4]:
         mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8))
-        s, S = mi.moments()
-        ch = 1 if img.ndim == 2 else img.shape[2]
-        for l in range(8):
-            lay = mi.layout(l)
-            cols = oracle.layout_columns(lay["pixels"], 9, ch)
-            mean, cov = oracle.layout_covariance(s, S, mi.n, cols)
-            assert np.array_equal(lay["mean"], mean)
-            comp, eig = oracle.pca_from_cov(cov, mi.dims)
-            np.testing.assert_allclose(lay["eigenvalues"], eig, rtol=1e-9, atol=1e-9 * eig[0])
-            # orthonormal, eigen-residual small, and equal to the oracle's where the spectrum is simple
-            C = lay["components"]
-            np.testing.assert_allclose(C @ C.T, np.eye(mi.dims), atol=1e-10)
-            res = cov @ C.T - C.T * lay["eigenvalues"]
-            assert np.abs(res).max() <= 1e-9 * max(1.0, eig[0])
-            gaps = np.abs(np.diff(eig))
-            for d in range(mi.dims):
-                g = min(gaps[d - 1] if d > 0 else np.inf, gaps[d] if d < len(gaps) else np.inf)
-                if g > 1e-6 * eig[0]:
-                    np.testing.assert_allclose(C[d], comp[d], atol=1e-7)
+        assert mi.info.pca_on_device == 1
+        _check_pca(mi, 9, 1 if img.ndim == 2 else img.shape[2], tag)
+
+
+@pytest.mark.parametrize("K,dims,device", [(11, 12, 1), (11, 32, 1), (13, 12, 0), (3, 9, 1)])
+def test_pca_rgb_device_and_host_paths(zb, K, dims, device):
+    """mc = m*C: K=11 RGB -> 219 (device k_pca), K=13 RGB -> 303 (host fallback)."""
+    img, kn = workloads.small_image(80, 72, 3, seed=K + dims, hole_frac=0.1)
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=K, dims=dims))
+    assert mi.info.pca_on_device == device
+    _check_pca(mi, K, 3, (K, dims))
+
+
+def test_pca_constant_image(zb):
+    """Zero covariance: eigenvalues 0, components still orthonormal, build still bit-exact."""
+    img = np.full((30, 30), 77, np.uint8)
+    mi = zb.MultiIndex(img, np.ones((30, 30), np.uint8), zb.index_config(patch_size=5, dims=4))
+    for l in range(8):
+        lay = mi.layout(l)
+        assert (lay["eigenvalues"] == 0).all()
+        C = lay["components"]
+        np.testing.assert_allclose(C @ C.T, np.eye(mi.dims), atol=1e-10)
+        c, _ = mi.index_arrays(l)
+        assert (c == 0).all()
 
 
 def test_build_bitexact_against_oracle(zb, golden):
