@@ -37,7 +37,23 @@ zi_status guard(F&& f) {
 void require(bool ok, const char* msg) {
     if (!ok) throw zi::error(ZI_E_INVALID, msg);
 }
+
+// guard() with the handle's stream bound for stream-ordered allocations
+struct stream_scope {
+    cudaStream_t prev;
+    explicit stream_scope(cudaStream_t s) : prev(zi::tls_alloc_stream) { zi::tls_alloc_stream = s; }
+    ~stream_scope() { zi::tls_alloc_stream = prev; }
+};
+template <typename F>
+zi_status guard(const zi_ctx* ctx, F&& f) {
+    stream_scope sc(ctx ? ctx->stream : nullptr);
+    return guard(std::forward<F>(f));
+}
 }  // namespace
+
+namespace zi {
+thread_local cudaStream_t tls_alloc_stream = nullptr;
+}
 
 namespace zi {
 
@@ -145,6 +161,10 @@ zi_status zi_ctx_create(int device, zi_ctx** out) {
         ZI_CUDA(cudaGetDeviceProperties(&prop, device));
         c->num_sms = prop.multiProcessorCount;
         ZI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        ZI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = ~0ull;  // never trim: rebuilds reuse the pool's HBM
+        ZI_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         ZI_CUDA(cudaEventCreate(&c->t0));
         ZI_CUDA(cudaEventCreate(&c->t1));
         *out = c;
@@ -152,7 +172,7 @@ zi_status zi_ctx_create(int device, zi_ctx** out) {
 }
 
 zi_status zi_ctx_destroy(zi_ctx* ctx) {
-    return guard([&] {
+    return guard(ctx, [&] {
         if (!ctx) return;
         cudaStreamSynchronize(ctx->stream);
         for (auto& p : ctx->prof)
@@ -162,21 +182,25 @@ zi_status zi_ctx_destroy(zi_ctx* ctx) {
             }
         cudaEventDestroy(ctx->t0);
         cudaEventDestroy(ctx->t1);
+        ctx->scratch.release();  // stream-ordered frees before the stream goes away
+        ctx->counter.release();
+        ctx->flush.release();
+        cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
 }
 
 zi_status zi_ctx_synchronize(zi_ctx* ctx) {
-    return guard([&] { ZI_CUDA(cudaStreamSynchronize(ctx->stream)); });
+    return guard(ctx, [&] { ZI_CUDA(cudaStreamSynchronize(ctx->stream)); });
 }
 
 zi_status zi_timer_start(zi_ctx* ctx) {
-    return guard([&] { ZI_CUDA(cudaEventRecord(ctx->t0, ctx->stream)); });
+    return guard(ctx, [&] { ZI_CUDA(cudaEventRecord(ctx->t0, ctx->stream)); });
 }
 
 zi_status zi_timer_stop(zi_ctx* ctx, double* ms) {
-    return guard([&] {
+    return guard(ctx, [&] {
         ZI_CUDA(cudaEventRecord(ctx->t1, ctx->stream));
         ZI_CUDA(cudaEventSynchronize(ctx->t1));
         float f = 0.f;
@@ -188,7 +212,7 @@ zi_status zi_timer_stop(zi_ctx* ctx, double* ms) {
 uint64_t zi_ctx_kernel_launches(const zi_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 zi_status zi_ctx_flush_l2(zi_ctx* ctx) {
-    return guard([&] {
+    return guard(ctx, [&] {
         const size_t bytes = size_t(256) << 20;
         uint8_t* p = ctx->flush.ensure(bytes);
         ZI_CUDA(cudaMemsetAsync(p, ctx->flush_toggle++ & 0xff, bytes, ctx->stream));
@@ -196,7 +220,7 @@ zi_status zi_ctx_flush_l2(zi_ctx* ctx) {
 }
 
 zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on) {
-    return guard([&] {
+    return guard(ctx, [&] {
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));
         ctx->profiling = on != 0;
         for (auto& p : ctx->prof) {
@@ -207,7 +231,7 @@ zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on) {
 }
 
 zi_status zi_ctx_profile(const zi_ctx* ctx, int slot, double* ms, uint64_t* launches, const char** name) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(slot >= 0 && static_cast<size_t>(slot) < ctx->prof.size(), "profile slot out of range");
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));
         const auto& p = ctx->prof[slot];
@@ -269,7 +293,7 @@ zi_status zi_index_config_validate(const zi_index_config* cfg, int channels) {
 // ---------------------------------------------------------------- z-curve index
 zi_status zi_index_from_descriptors(zi_ctx* ctx, const uint8_t* coords, const uint32_t* keys, uint64_t n, uint32_t dims,
                                     uint32_t layout_id, zi_index** out) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && out, "null argument");
         if (dims == 0 || dims > 32) throw zi::error(ZI_E_INVALID, "zcurve_index: dims must be in [1, 32]");
         require(n == 0 || (coords && keys), "null argument");
@@ -306,11 +330,11 @@ zi_status zi_index_from_descriptors(zi_ctx* ctx, const uint8_t* coords, const ui
 }
 
 zi_status zi_index_destroy(zi_index* idx) {
-    return guard([&] { delete idx; });
+    return guard(idx ? idx->ctx : nullptr, [&] { delete idx; });
 }
 
 zi_status zi_index_size(const zi_index* idx, uint64_t* n, uint32_t* dims) {
-    return guard([&] {
+    return guard(idx ? idx->ctx : nullptr, [&] {
         if (n) *n = idx->n;
         if (dims) *dims = idx->dims;
     });
@@ -335,12 +359,12 @@ static void export_index(zi_index* idx, uint8_t* coords_out, uint32_t* keys_out)
 }
 
 zi_status zi_index_export(zi_index* idx, uint8_t* coords_out, uint32_t* keys_out) {
-    return guard([&] { export_index(idx, coords_out, keys_out); });
+    return guard(idx ? idx->ctx : nullptr, [&] { export_index(idx, coords_out, keys_out); });
 }
 
 zi_status zi_knn_search(zi_index* idx, const uint8_t* query, uint32_t k, uint32_t mu, int32_t norm, uint64_t* packed_out,
                         uint32_t* count_out) {
-    return guard([&] {
+    return guard(idx ? idx->ctx : nullptr, [&] {
         require(idx && query && packed_out && count_out, "null argument");
         require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
         (void)mu;  // leaf threshold of the CPU traversal; the GPU scan has no leaves
@@ -350,7 +374,7 @@ zi_status zi_knn_search(zi_index* idx, const uint8_t* query, uint32_t k, uint32_
 
 zi_status zi_knn_search_batch(zi_index* idx, const uint8_t* queries, uint64_t nq, uint32_t k, int32_t norm,
                               uint64_t* packed_out, uint32_t* counts_out) {
-    return guard([&] {
+    return guard(idx ? idx->ctx : nullptr, [&] {
         require(idx && (nq == 0 || (queries && packed_out && counts_out)), "null argument");
         require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
         zi::knn_search_batch(idx, queries, nq, k, norm, packed_out, counts_out);
@@ -359,7 +383,7 @@ zi_status zi_knn_search_batch(zi_index* idx, const uint8_t* queries, uint64_t nq
 
 zi_status zi_knn_batch_bench(zi_index* idx, const uint8_t* queries, uint64_t nq, uint32_t k, int32_t norm, int32_t reps,
                              double* ms_per_batch, uint64_t* stats3, uint64_t* packed_out, uint32_t* counts_out) {
-    return guard([&] {
+    return guard(idx ? idx->ctx : nullptr, [&] {
         require(idx && queries && ms_per_batch && nq > 0 && reps > 0, "bad argument");
         require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
         require(k >= 1 && k <= 256, "batch bench supports 1 <= k <= 256");
@@ -390,16 +414,20 @@ zi_status zi_knn_batch_bench(zi_index* idx, const uint8_t* queries, uint64_t nq,
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         *ms_per_batch = total / reps;
-        if (stats3) ZI_CUDA(cudaMemcpy(stats3, dstats.p, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
-        if (packed_out) ZI_CUDA(cudaMemcpy(packed_out, dout.p, nq * k * sizeof(uint64_t), cudaMemcpyDeviceToHost));
-        if (counts_out) ZI_CUDA(cudaMemcpy(counts_out, dcnt.p, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        if (stats3)
+            ZI_CUDA(cudaMemcpyAsync(stats3, dstats.p, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        if (packed_out)
+            ZI_CUDA(cudaMemcpyAsync(packed_out, dout.p, nq * k * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        if (counts_out)
+            ZI_CUDA(cudaMemcpyAsync(counts_out, dcnt.p, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
 
 // ---------------------------------------------------------------- dictionary
 zi_status zi_dictionary_collect(zi_ctx* ctx, const uint8_t* known, int32_t w, int32_t h, int32_t K, uint32_t* keys_out,
                                 uint64_t cap, uint64_t* n_out) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && known && n_out, "null argument");
         require(w > 0 && h > 0 && w <= 65535 && h <= 65535, "mask_image: bad dimensions");
         require(K >= 1, "patch size must be positive");
@@ -421,7 +449,7 @@ zi_status zi_dictionary_collect(zi_ctx* ctx, const uint8_t* known, int32_t w, in
 // ---------------------------------------------------------------- multi-index
 zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h,
                                int32_t C, const zi_index_config* cfg, zi_multi_index** out) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(out != nullptr, "null argument");
         zi_multi_index* mi = new_multi_index(ctx, image, known, w, h, C, cfg);
         try {
@@ -435,18 +463,18 @@ zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t*
 }
 
 zi_status zi_multi_index_rebuild(zi_multi_index* mi) {
-    return guard([&] { zi::build_multi_index(mi); });
+    return guard(mi ? mi->ctx : nullptr, [&] { zi::build_multi_index(mi); });
 }
 
 zi_status zi_multi_index_destroy(zi_multi_index* mi) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         if (mi) cudaStreamSynchronize(mi->ctx->stream);
         delete mi;
     });
 }
 
 zi_status zi_multi_index_get_info(const zi_multi_index* mi, zi_multi_index_info* info) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         info->n = mi->n;
         info->dims = mi->dims;
         info->m = mi->m;
@@ -461,7 +489,7 @@ zi_status zi_multi_index_get_info(const zi_multi_index* mi, zi_multi_index_info*
 }
 
 zi_status zi_multi_index_dictionary(zi_multi_index* mi, uint32_t* keys_out) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         ZI_CUDA(cudaMemcpyAsync(keys_out, mi->dict.p, mi->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, mi->ctx->stream));
         ZI_CUDA(cudaStreamSynchronize(mi->ctx->stream));
     });
@@ -469,7 +497,7 @@ zi_status zi_multi_index_dictionary(zi_multi_index* mi, uint32_t* keys_out) {
 
 zi_status zi_multi_index_layout(zi_multi_index* mi, int32_t layout, int32_t* rc, double* mean, double* components,
                                 double* eigenvalues, double* lo, double* hi) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         require(layout >= 0 && layout < 8, "layout id must be in [0, 8)");
         zi::sync_host_model(mi);
         const auto& L = mi->L[layout];
@@ -483,21 +511,21 @@ zi_status zi_multi_index_layout(zi_multi_index* mi, int32_t layout, int32_t* rc,
 }
 
 zi_status zi_multi_index_layout_index(zi_multi_index* mi, int32_t layout, uint8_t* coords_out, uint32_t* keys_out) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         require(layout >= 0 && layout < 8, "layout id must be in [0, 8)");
         export_index(&mi->L[layout].index, coords_out, keys_out);
     });
 }
 
 zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index** out) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         require(layout >= 0 && layout < 8, "layout id must be in [0, 8)");
         *out = &mi->L[layout].index;
     });
 }
 
 zi_status zi_multi_index_moments(zi_multi_index* mi, int64_t* s_out, int64_t* S_out) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         zi::sync_host_model(mi);
         if (s_out) std::memcpy(s_out, mi->s.data(), mi->s.size() * sizeof(int64_t));
         if (S_out) std::memcpy(S_out, mi->S.data(), mi->S.size() * sizeof(int64_t));
@@ -507,7 +535,7 @@ zi_status zi_multi_index_moments(zi_multi_index* mi, int64_t* s_out, int64_t* S_
 // ---------------------------------------------------------------- query
 zi_status zi_query_best_patch(zi_multi_index* mi, const uint8_t* tv, const uint8_t* tk, uint32_t k, int32_t norm,
                               zi_best_patch* out, uint64_t* knn_out) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         require(mi && tv && tk && out, "null argument");
         require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
         const zi::query_result r = zi::query_best_patch(mi, tv, tk, k, norm, knn_out);
@@ -520,7 +548,7 @@ zi_status zi_query_best_patch(zi_multi_index* mi, const uint8_t* tv, const uint8
 }
 
 zi_status zi_brute_force_best(zi_multi_index* mi, const uint8_t* tv, const uint8_t* tk, int32_t norm, zi_best_patch* out) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         require(mi && tv && tk && out, "null argument");
         require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
         const uint64_t b = zi::brute_force_best(mi, tv, tk, norm);
@@ -542,7 +570,7 @@ static void fill_stats_defaults(zi_run_stats* st) {
 zi_status zi_inpaint(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h, int32_t C,
                      const zi_index_config* cfg, const zi_inpaint_config* icfg, uint8_t* image_out,
                      zi_iteration_record* records, uint64_t cap, uint64_t* n_records, zi_run_stats* stats) {
-    return guard([&] {
+    return guard(ctx, [&] {
         require(ctx && image && known && cfg && icfg && image_out && n_records && stats, "null argument");
         require(w > 0 && h > 0 && (C == 1 || C == 3), "raster_image: bad dimensions");
         zi::validate_config(*cfg, C);
@@ -578,7 +606,7 @@ zi_status zi_inpaint(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, in
 zi_status zi_inpaint_with_index(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
                                 const zi_index_config* cfg, const zi_inpaint_config* icfg, uint8_t* image_out,
                                 zi_iteration_record* records, uint64_t cap, uint64_t* n_records, zi_run_stats* stats) {
-    return guard([&] {
+    return guard(mi ? mi->ctx : nullptr, [&] {
         require(mi && image && known && cfg && icfg && image_out && n_records && stats, "null argument");
         fill_stats_defaults(stats);
         *n_records = 0;

@@ -104,7 +104,9 @@ void build_multi_index(zi_multi_index* mi) {
                     for (int ch = 0; ch < C; ++ch)
                         hc.push_back((mi->L[l].rc[2 * p] * K + mi->L[l].rc[2 * p + 1]) * C + ch);
             mi->pca_cols.ensure(hc.size());
-            ZI_CUDA(cudaMemcpy(mi->pca_cols.p, hc.data(), hc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            ZI_CUDA(cudaMemcpyAsync(mi->pca_cols.p, hc.data(), hc.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));  // hc is a pageable local
             mi->pca_cols_ready = true;
         }
         mi->pca_eig.ensure(static_cast<size_t>(8) * 32);

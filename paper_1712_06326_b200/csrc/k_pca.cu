@@ -23,6 +23,8 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -31,7 +33,7 @@ namespace zi {
 namespace cg = cooperative_groups;
 
 constexpr int kCl = 8;             // CTAs per layout (one cluster)
-constexpr int kTriThreads = 256;
+constexpr int kTriThreads = 512;
 constexpr int kVecThreads = 128;
 constexpr int kPcaMaxN = 224;
 constexpr int kSlots = (kPcaMaxN + 31) / 32;  // vector entries per lane in the back-transform
@@ -205,6 +207,7 @@ struct tri_args {
     int mc;
     double* mean;  // 8 * mc
     pca_work_view w;
+    long long* dbg;  // optional per-phase clock totals (ZI_DEBUG_PCA)
 };
 
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca_tri(tri_args a) {
@@ -220,8 +223,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
     double* A = sm;                                          // rows_max x n, full rows
     double* v = A + static_cast<size_t>(rows_max) * n;       // [2][n] reflector, by column parity
     double* p = v + 2 * n;                                   // [2][n] tau * A v
-    double* vpp = p + 2 * n;                                 // [2][kCl] per-CTA partials of v.p
-    double* scal = vpp + 2 * kCl;                            // [2][2] tau, alpha
+    double* npart = p + 2 * n;                               // [2][kCl][warps] partial |column|^2
     const long long* s = reinterpret_cast<const long long*>(a.moments);
     const long long* S = s + a.F;
     const long long nn = static_cast<long long>(a.n);
@@ -248,70 +250,139 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
     double* refl = a.w.refl + l * a.w.rstride;
     __syncthreads();
     cluster_barrier();  // every CTA of the cluster runs before the first DSMEM store
+    long long tacc[6] = {0, 0, 0, 0, 0, 0};
+    long long tc = clock64();
+#define TRI_T(i)                          \
+    {                                     \
+        const long long t2_ = clock64();  \
+        tacc[i] += t2_ - tc;              \
+        tc = t2_;                         \
+    }
+    // Column c's sub-diagonal entries A(i, c), i > c, live in the rows' owners (full rows): each
+    // warp pushes the entries of its rows and its partial |.|^2 to every CTA, so the next
+    // reflector is assembled everywhere without a single-owner broadcast and without CTA barriers.
+    constexpr int kParts = kCl * kWarps;
+    auto push_entry = [&](int c, int bb, int i, double y) {  // warp-uniform call
+        if (lane < kCl) cl.map_shared_rank(v, lane)[bb * n + (i - c - 1)] = y;
+    };
+    auto push_partial = [&](int bb, double part) {
+        if (lane < kCl) cl.map_shared_rank(npart, lane)[bb * kParts + rank * kWarps + warp] = part;
+    };
+    {
+        double part = 0.0;
+        const int first = 1 > rank ? 1 : 0;
+        for (int li = first + warp; li < nloc; li += kWarps) {
+            const double y = A[static_cast<size_t>(li) * n];
+            push_entry(0, 0, rank + kCl * li, y);
+            part = fma(y, y, part);
+        }
+        push_partial(0, part);
+    }
+    cluster_barrier();
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1, b = k & 1;
-        if (rank == k % kCl) {  // pivot row owner: reflector of column k (= row k right of the diagonal)
-            const double* row = A + static_cast<size_t>(k / kCl) * n + k + 1;
-            double part = 0.0;
-            for (int j = tid; j < m; j += kTriThreads) part = fma(row[j], row[j], part);
-            const double norm2 = cta_sum<kTriThreads>(part, s_red);
-            const double x0 = row[0];
-            double alpha = x0, tk = 0.0;
-            if (norm2 != 0.0) {
-                alpha = x0 >= 0 ? -sqrt(norm2) : sqrt(norm2);
-                tk = 1.0 / (norm2 - alpha * x0);  // 2 / |x - alpha e1|^2
-            }
-            for (int idx = tid; idx < m * kCl; idx += kTriThreads) {
-                const int j = idx / kCl, r = idx % kCl;
-                const double vj = (j == 0 && tk != 0.0) ? x0 - alpha : row[j];
-                cl.map_shared_rank(v, r)[b * n + j] = vj;
-                if (r == 0) refl[refl_off(k, n) + j] = vj;
-            }
-            if (tid < kCl) {
-                double* rs = cl.map_shared_rank(scal, tid);
-                rs[2 * b] = tk;
-                rs[2 * b + 1] = alpha;
-            }
-            if (tid == 0) {
+        const double* vb = v + b * n;
+        // |column k|^2 from the per-warp partials, summed in the same order by every warp
+        double np = 0.0;
+#pragma unroll
+        for (int q = 0; q < kParts / 32; ++q) np += npart[b * kParts + lane + 32 * q];
+        const double norm2 = warp_allsum(np);
+        const double x0 = vb[0];
+        double alpha = x0, tk = 0.0;
+        if (norm2 != 0.0) {
+            alpha = x0 >= 0 ? -sqrt(norm2) : sqrt(norm2);
+            tk = 1.0 / (norm2 - alpha * x0);  // 2 / |x - alpha e1|^2
+        }
+        const double v0 = tk != 0.0 ? x0 - alpha : x0;
+        double vr[kSlots];
+#pragma unroll
+        for (int q = 0; q < kSlots; ++q) {
+            const int j = lane + 32 * q;
+            vr[q] = j < m ? vb[j] : 0.0;
+        }
+        if (lane == 0) vr[0] = v0;
+        if (rank == 0 && warp == 0) {
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q)
+                if (lane + 32 * q < m) refl[refl_off(k, n) + lane + 32 * q] = vr[q];
+            if (lane == 0) {
                 e_out[k] = alpha;
                 tau_out[k] = tk;
             }
         }
-        cluster_barrier();
-        const double tk = scal[2 * b];
-        if (tk == 0.0) continue;  // column already reduced (uniform over the cluster)
-        const double* vb = v + b * n;
         const int li0 = k + 1 > rank ? (k + 1 - rank + kCl - 1) / kCl : 0;  // first trailing row
-        double myvp = 0.0;
-        for (int li = li0 + warp; li < nloc; li += kWarps) {
-            const int t = rank + kCl * li - k - 1;
-            const double* row = A + static_cast<size_t>(li) * n + k + 1;
-            double acc = 0.0;
-            for (int j = lane; j < m; j += 32) acc = fma(row[j], vb[j], acc);
-            const double pt = tk * warp_allsum(acc);
-            if (lane < kCl) cl.map_shared_rank(p, lane)[b * n + t] = pt;
-            if (lane == 0) myvp = fma(vb[t], pt, myvp);
-        }
-        const double cvp = cta_sum<kTriThreads>(myvp, s_red);
-        if (tid < kCl) cl.map_shared_rank(vpp, tid)[b * kCl + rank] = cvp;
-        cluster_barrier();
-        double vp = 0.0;
+        const bool next = k + 3 < n;  // column k+1 is a Householder column
+        double part = 0.0;
+        TRI_T(0);
+        if (tk != 0.0) {
+            // p_i = tau * (A v)_i for my trailing rows, pushed to every CTA
+            for (int li = li0 + warp; li < nloc; li += kWarps) {
+                const int t = rank + kCl * li - k - 1;
+                const double* row = A + static_cast<size_t>(li) * n + k + 1;
+                double acc = 0.0;
 #pragma unroll
-        for (int r = 0; r < kCl; ++r) vp += vpp[b * kCl + r];
-        const double K2 = 0.5 * tk * vp;
-        const double* pb = p + b * n;
-        // A22 -= v w^T + w v^T, w = p - K2 v, on my full rows
-        for (int li = li0 + warp; li < nloc; li += kWarps) {
-            const int t = rank + kCl * li - k - 1;
-            double* row = A + static_cast<size_t>(li) * n + k + 1;
-            const double vt = vb[t], wt = fma(-K2, vt, pb[t]);
-            for (int j = lane; j < m; j += 32) {
-                const double wj = fma(-K2, vb[j], pb[j]);
-                row[j] = fma(-vt, wj, fma(-wt, vb[j], row[j]));
+                for (int q = 0; q < kSlots; ++q) {
+                    const int j = lane + 32 * q;
+                    if (j < m) acc = fma(row[j], vr[q], acc);
+                }
+                const double pt = tk * warp_allsum(acc);
+                if (lane < kCl) cl.map_shared_rank(p, lane)[b * n + t] = pt;
+            }
+            TRI_T(1);
+            cluster_barrier();
+            TRI_T(2);
+            const double* pb = p + b * n;
+            double wr[kSlots];
+            double vp = 0.0;
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) {
+                const int j = lane + 32 * q;
+                wr[q] = j < m ? pb[j] : 0.0;
+                vp = fma(vr[q], wr[q], vp);
+            }
+            const double K2 = 0.5 * tk * warp_allsum(vp);
+#pragma unroll
+            for (int q = 0; q < kSlots; ++q) wr[q] = fma(-K2, vr[q], wr[q]);  // w = p - K2 v
+            // A22 -= v w^T + w v^T on my full rows; the new column k+1 entries go out at once
+            for (int li = li0 + warp; li < nloc; li += kWarps) {
+                const int t = rank + kCl * li - k - 1;
+                double* row = A + static_cast<size_t>(li) * n + k + 1;
+                const double vt = t == 0 ? v0 : vb[t];
+                const double wt = fma(-K2, vt, pb[t]);
+                double y0 = 0.0;
+#pragma unroll
+                for (int q = 0; q < kSlots; ++q) {
+                    const int j = lane + 32 * q;
+                    if (j < m) {
+                        const double y = fma(-vt, wr[q], fma(-wt, vr[q], row[j]));
+                        row[j] = y;
+                        if (q == 0) y0 = y;
+                    }
+                }
+                if (next && t >= 1) {
+                    y0 = __shfl_sync(0xffffffffu, y0, 0);
+                    push_entry(k + 1, b ^ 1, t + k + 1, y0);
+                    part = fma(y0, y0, part);
+                }
+            }
+            TRI_T(3);
+        } else if (next) {
+            for (int li = li0 + warp; li < nloc; li += kWarps) {
+                const int i = rank + kCl * li;
+                if (i < k + 2) continue;
+                const double y = A[static_cast<size_t>(li) * n + k + 1];
+                push_entry(k + 1, b ^ 1, i, y);
+                part = fma(y, y, part);
             }
         }
-        __syncthreads();
+        if (next) push_partial(b ^ 1, part);
+        TRI_T(4);
+        cluster_barrier();
+        TRI_T(5);
     }
+    if (a.dbg && tid == 0)
+        for (int i = 0; i < 6; ++i) a.dbg[blockIdx.x * 8 + i] = tacc[i];
+#undef TRI_T
     for (int li = tid; li < nloc; li += kTriThreads) {
         const int i = rank + kCl * li;
         d_out[i] = A[static_cast<size_t>(li) * n + i];
@@ -533,7 +604,7 @@ bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint
     if (optin < 0) ZI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     const size_t limit = static_cast<size_t>(optin) - 1024;
     const int rows_max = (mc + kCl - 1) / kCl;
-    const size_t smem_tri = (static_cast<size_t>(rows_max) * mc + 4 * mc + 2 * kCl + 4) * sizeof(double);
+    const size_t smem_tri = (static_cast<size_t>(rows_max) * mc + 4 * mc + 2 * kCl * (kTriThreads / 32)) * sizeof(double);
     const size_t smem_vec = (refl_stride(mc) + 9 * static_cast<size_t>(mc)) * sizeof(double) + mc + 16;
     const size_t smem_fin = static_cast<size_t>(D) * mc * sizeof(double);
     if (smem_tri > limit || smem_vec > limit || smem_fin > limit) return false;
@@ -551,8 +622,22 @@ bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint
         attr_fin = smem_fin;
     }
     const pca_work_view w = pca_work_split(d_work, mc, D);
-    tri_args ta{d_moments, F, n, d_cols, mc, d_mean, w};
+    tri_args ta{d_moments, F, n, d_cols, mc, d_mean, w, nullptr};
+    static const bool debug = std::getenv("ZI_DEBUG_PCA") != nullptr;
+    static dbuf<long long> dbg;
+    if (debug) {
+        ta.dbg = dbg.ensure(8 * kCl * 8);
+        ZI_CUDA(cudaMemsetAsync(ta.dbg, 0, 8 * kCl * 8 * sizeof(long long), ctx->stream));
+    }
     ZI_LAUNCH(ctx, "pca_tridiag", k_pca_tri, 8 * kCl, kTriThreads, smem_tri, ta);
+    if (debug) {
+        long long h[8 * kCl * 8];
+        ZI_CUDA(cudaMemcpyAsync(h, ta.dbg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int c = 0; c < 2 * kCl; ++c)
+            std::fprintf(stderr, "tri cta %2d: start %lld B %lld bar1 %lld C %lld push %lld bar2 %lld\n", c, h[c * 8],
+                         h[c * 8 + 1], h[c * 8 + 2], h[c * 8 + 3], h[c * 8 + 4], h[c * 8 + 5]);
+    }
     vec_args va{mc, D, w};
     ZI_LAUNCH(ctx, "pca_vectors", k_pca_vec, 8 * D, kVecThreads, smem_vec, va);
     fin_args fa{mc, D, w, d_comp, d_eig};

@@ -33,17 +33,24 @@ inline void check_launch(const char* name) {
     if (e != cudaSuccess) throw error(ZI_E_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
 }
 
-// Growable device buffer (cudaMalloc'd, never shrinks).
+// Stream of the API call in progress on this thread (set by api.cu's guard): device buffers are
+// allocated and freed stream-ordered on it, from the device's default memory pool, which keeps
+// its memory (release threshold = max) -- building index after index reuses the same HBM without
+// cudaMalloc / cudaFree round trips.
+extern thread_local cudaStream_t tls_alloc_stream;
+
+// Growable device buffer (pool allocated, never shrinks).
 template <typename T>
 struct dbuf {
     T* p = nullptr;
     size_t cap = 0;
+    cudaStream_t s = nullptr;  // stream the buffer was allocated on (frees are ordered after its work)
     dbuf() = default;
     dbuf(const dbuf&) = delete;
     dbuf& operator=(const dbuf&) = delete;
     ~dbuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         cap = 0;
     }
@@ -51,7 +58,8 @@ struct dbuf {
         if (n <= cap && p) return p;
         release();
         const size_t bytes = (n ? n : 1) * sizeof(T);
-        ZI_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), bytes));
+        s = tls_alloc_stream;
+        ZI_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s));
         cap = n ? n : 1;
         return p;
     }
