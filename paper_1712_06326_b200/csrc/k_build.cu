@@ -293,89 +293,111 @@ void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const
 // Y[d*n + i] = sum_j fma(comp[j][d], x_ij - mean_j) in the canonical order (j ascending,
 // starting from +0.0) -- bit-identical to the oracle's restatement of
 // proj/src/builder.cpp:166-167/180-181 (fill_chunk gather order :20-34).
-__host__ __device__ constexpr int project_ppt(int D) { return D <= 12 ? 4 : (D <= 24 ? 2 : 1); }
+// Projection on the FP64 tensor cores.  mma.sync.m8n8k4.f64 accumulates its four k-products
+// into C as four sequential round-to-nearest FMAs in k order -- bit-identical to the canonical
+// y = fma(comp[j][d], x_j - mean_j, y), j ascending (checked on B200 with random operands,
+// 4M elements, 0 differences; a single-rounding 4-term sum differs in ~40%).  So the canonical
+// order runs as Y(8 patches x 8 dims) += Xc(8 x 4 columns) * Comp(4 x 8), k-steps in column
+// order; columns past m*C are zero-padded in Comp (fma(x, 0, y) == y since y is never -0).
+// A warp owns kProjGroups groups of 8 consecutive dictionary patches (independent accumulator
+// chains); lane (r, c) = (lane/4, lane%4) gathers byte x[patch r][column 4*ks + c].
+constexpr int kProjThreads = 256;
+constexpr int kProjGroups = 4;  // 8-patch groups per warp
+constexpr int kProjPF = 3;      // gather prefetch distance (k-steps)
 
-// patches per thread: ZI_PROJECT_PPT overrides the default (1, 2 or 4) for tuning runs
-static int project_ppt_runtime(int D) {
-    static int env = [] {
-        const char* e = std::getenv("ZI_PROJECT_PPT");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (env >= 1 && env <= 4) return env;
-    return project_ppt(D);
+__device__ inline void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
 }
 
-// One thread projects PPT patches (i, i+T, ..., T = total threads) so every component row loaded
-// from shared memory feeds PPT*D independent fp64 FMA chains (the LDS pipe, not the FP64 pipe,
-// bounded the one-patch-per-thread version).
-constexpr int kProjThreads = 128;
-
-template <int D, int PPT>
-__global__ void __launch_bounds__(kProjThreads, PPT >= 4 ? 3 : (PPT == 3 ? 4 : 5)) k_project(const uint8_t* __restrict__ img, int w, int C,
-                                                 const uint32_t* __restrict__ keys, uint64_t n,
-                                                 const int32_t* __restrict__ off, int m,
-                                                 const double* __restrict__ mean,
-                                                 const double* __restrict__ comp, double* __restrict__ Y) {
+template <int D>
+__global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restrict__ img, int w, int C,
+                                                          const uint32_t* __restrict__ keys, uint64_t n,
+                                                          const int32_t* __restrict__ off, int m,
+                                                          const double* __restrict__ mean,
+                                                          const double* __restrict__ comp, double* __restrict__ Y) {
+    constexpr int NT = (D + 7) / 8;  // 8-dim tiles
+    constexpr int G = kProjGroups;
     extern __shared__ double sm[];
-    const int mc = m * C;
-    double* s_comp = sm;                 // mc*D  ([j][d])
-    double* s_mean = sm + mc * D;        // mc
-    int* s_joff = reinterpret_cast<int*>(s_mean + mc);  // mc: image byte offset of column j
-    for (int i = threadIdx.x; i < mc * D; i += blockDim.x) s_comp[i] = comp[i];
-    for (int i = threadIdx.x; i < mc; i += blockDim.x) {
-        s_mean[i] = mean[i];
-        s_joff[i] = off[i / C] + i % C;
+    const int mc = m * C, KS = (mc + 3) / 4;
+    double* s_B = sm;                                   // [KS][NT][32] B fragments (Comp, zero padded)
+    double* s_mean = s_B + static_cast<size_t>(KS) * NT * 32;  // [KS*4]
+    int* s_joff = reinterpret_cast<int*>(s_mean + KS * 4);     // [KS*4] byte offset of column j
+    for (int idx = threadIdx.x; idx < KS * NT * 32; idx += kProjThreads) {
+        const int ks = idx / (NT * 32), t = (idx / 32) % NT, ln = idx % 32;
+        const int j = ks * 4 + ln % 4, d = t * 8 + ln / 4;
+        s_B[idx] = (j < mc && d < D) ? comp[j * D + d] : 0.0;
+    }
+    for (int j = threadIdx.x; j < KS * 4; j += kProjThreads) {
+        s_mean[j] = j < mc ? mean[j] : 0.0;
+        s_joff[j] = j < mc ? off[j / C] + j % C : 0;
     }
     __syncthreads();
-    const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += T * PPT) {
-        const uint8_t* base[PPT];
-        bool ok[PPT];
+    const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kProjThreads / 32);
+    for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * (kProjThreads / 32) + (threadIdx.x >> 5)) * (8 * G);
+         base < n; base += warps * 8 * G) {
+        const uint8_t* pb[G];
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-            const uint64_t i = i0 + k * T;
-            ok[k] = i < n;
-            const uint32_t key = ok[k] ? keys[i] : 0u;
-            base[k] = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
+        for (int g = 0; g < G; ++g) {
+            const uint64_t i = base + 8 * g + r;
+            const uint32_t key = keys[i < n ? i : n - 1];
+            pb[g] = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
         }
-        double y[PPT][D];
+        double acc[G][NT][2];
 #pragma unroll
-        for (int k = 0; k < PPT; ++k)
+        for (int g = 0; g < G; ++g)
 #pragma unroll
-            for (int d = 0; d < D; ++d) y[k][d] = 0.0;
-        // software-pipelined gather: the bytes of column j+1 are in flight while column j's
-        // PPT*D FMAs issue
-        uint32_t xn[PPT];
+            for (int t = 0; t < NT; ++t) acc[g][t][0] = acc[g][t][1] = 0.0;
+        uint32_t xr[kProjPF][G];
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) xn[k] = __ldg(base[k] + s_joff[0]);
-        for (int j = 0; j < mc; ++j) {
-            uint32_t xcur[PPT];
+        for (int s = 0; s < kProjPF; ++s)
+            if (s < KS) {
+                const int o = s_joff[s * 4 + c];
 #pragma unroll
-            for (int k = 0; k < PPT; ++k) xcur[k] = xn[k];
-            if (j + 1 < mc) {
-                const int o = s_joff[j + 1];
-#pragma unroll
-                for (int k = 0; k < PPT; ++k) xn[k] = __ldg(base[k] + o);
+                for (int g = 0; g < G; ++g) xr[s][g] = __ldg(pb[g] + o);
             }
-            const double mj = s_mean[j];
-            double xc[PPT];
+        for (int ks0 = 0; ks0 < KS; ks0 += kProjPF) {
 #pragma unroll
-            for (int k = 0; k < PPT; ++k) xc[k] = __dsub_rn(static_cast<double>(xcur[k]), mj);
-            const double* cj = s_comp + j * D;
+            for (int s = 0; s < kProjPF; ++s) {
+                const int ks = ks0 + s;
+                if (ks < KS) {
+                    uint32_t xcur[G];
 #pragma unroll
-            for (int d = 0; d < D; ++d) {
-                const double c = cj[d];
+                    for (int g = 0; g < G; ++g) xcur[g] = xr[s][g];
+                    if (ks + kProjPF < KS) {
+                        const int o = s_joff[(ks + kProjPF) * 4 + c];
 #pragma unroll
-                for (int k = 0; k < PPT; ++k) y[k][d] = __fma_rn(c, xc[k], y[k][d]);
+                        for (int g = 0; g < G; ++g) xr[s][g] = __ldg(pb[g] + o);
+                    }
+                    const double mj = s_mean[ks * 4 + c];
+                    double bf[NT];
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) bf[t] = s_B[(ks * NT + t) * 32 + lane];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const double a = __dsub_rn(static_cast<double>(xcur[g]), mj);
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) dmma_8x8x4(acc[g][t][0], acc[g][t][1], a, bf[t]);
+                    }
+                }
             }
         }
+        // lane holds y[patch base + 8g + r][dim 8t + 2c + e]
 #pragma unroll
-        for (int k = 0; k < PPT; ++k)
-            if (ok[k]) {
-                const uint64_t i = i0 + k * T;
+        for (int g = 0; g < G; ++g) {
+            const uint64_t i = base + 8 * g + r;
+            if (i < n) {
 #pragma unroll
-                for (int d = 0; d < D; ++d) Y[static_cast<size_t>(d) * n + i] = y[k][d];
+                for (int t = 0; t < NT; ++t)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int d = 8 * t + 2 * c + e;
+                        if (d < D) Y[static_cast<size_t>(d) * n + i] = acc[g][t][e];
+                    }
             }
+        }
     }
 }
 
@@ -541,31 +563,22 @@ __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ k
 }
 
 // ============================================================== host launchers
-template <int D, int PPT>
-static void launch_project_ppt(zi_ctx* ctx, const uint8_t* img, int w, int C, const uint32_t* keys, uint64_t n,
-                               const int32_t* off, int m, const double* mean, const double* comp, double* Y) {
-    const size_t smem = static_cast<size_t>(m) * C * D * sizeof(double) + static_cast<size_t>(m) * C * sizeof(double) +
-                        static_cast<size_t>(m) * C * sizeof(int);
-    static bool attr_set = false;
-    if (!attr_set) {
-        ZI_CUDA(cudaFuncSetAttribute(k_project<D, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
-    }
-    const uint64_t threads = (n + PPT - 1) / PPT;
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((threads + kProjThreads - 1) / kProjThreads,
-                                                                   static_cast<uint64_t>(ctx->num_sms) * 16));
-    ZI_LAUNCH(ctx, "project", (k_project<D, PPT>), grid, kProjThreads, smem, img, w, C, keys, n, off, m, mean, comp, Y);
-}
-
 template <int D>
 static void launch_project_t(zi_ctx* ctx, const uint8_t* img, int w, int C, const uint32_t* keys, uint64_t n,
                              const int32_t* off, int m, const double* mean, const double* comp, double* Y) {
-    switch (project_ppt_runtime(D)) {
-        case 4: launch_project_ppt<D, 4>(ctx, img, w, C, keys, n, off, m, mean, comp, Y); break;
-        case 3: launch_project_ppt<D, 3>(ctx, img, w, C, keys, n, off, m, mean, comp, Y); break;
-        case 2: launch_project_ppt<D, 2>(ctx, img, w, C, keys, n, off, m, mean, comp, Y); break;
-        default: launch_project_ppt<D, 1>(ctx, img, w, C, keys, n, off, m, mean, comp, Y); break;
+    constexpr int NT = (D + 7) / 8;
+    const int KS = (m * C + 3) / 4;
+    const size_t smem = static_cast<size_t>(KS) * NT * 32 * sizeof(double) + static_cast<size_t>(KS) * 4 * sizeof(double) +
+                        static_cast<size_t>(KS) * 4 * sizeof(int);
+    static size_t attr = 0;
+    if (smem > attr) {
+        ZI_CUDA(cudaFuncSetAttribute(k_project<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = smem;
     }
+    const uint64_t warps = (n + 8 * kProjGroups - 1) / (8 * kProjGroups);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((warps + kProjThreads / 32 - 1) / (kProjThreads / 32),
+                                                                   static_cast<uint64_t>(ctx->num_sms) * 8));
+    ZI_LAUNCH(ctx, "project", k_project<D>, grid, kProjThreads, smem, img, w, C, keys, n, off, m, mean, comp, Y);
 }
 
 template <int D>
