@@ -146,15 +146,21 @@ uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, i
 
 // ============================================================== K2: exact patch moments
 // S = sum_p x_p x_p^T and s = sum_p x_p over the full K*K*C patch vectors (u8), exact.
-// Tensor cores (mma.sync m16n8k32 u8 x u8 -> s32): the Gram is X^T X with X (patches x F), so
-// both operands are the feature-major gather XT[f][p] staged in shared memory.  One CTA = one
-// 128x128 feature tile pair (ti <= tj) x one chunk of <= 8192 patches (int32 accumulators stay
-// exact: 8192 * 255^2 < 2^31); chunk partials are added into int64 with atomics (order-free =>
-// deterministic).
+// Two kernels:
+//   k_patch_matrix  the feature-major patch matrix XT[f][p] (Fpad x npad u8, zero padded) in HBM:
+//                   one warp writes 4 features x 128 consecutive patches (coalesced 16 B stores),
+//                   reading adjacent pixels of the image (L1/L2 resident).
+//   k_moments       X^T X on the tensor cores (mma.sync m16n8k32 u8 x u8 -> s32): one CTA = one
+//                   128x128 feature tile pair (ti <= tj) x one patch chunk; 128-patch stages
+//                   stream in with cp.async (3-stage ring, 144 B pitch -> conflict-free ldmatrix).
+//                   Chunks hold <= 65536 patches so the s32 accumulators, read as u32, are exact
+//                   (65536 * 255^2 < 2^32); chunk partials go into int64 with atomics
+//                   (order-free -> deterministic).
 constexpr int kMomTile = 128;
-constexpr int kMomBatch = 64;               // patches per smem stage (two k32 MMA steps)
-constexpr int kMomChunk = 8192;
-constexpr int kMomPitch = kMomBatch + 16;   // 80 B rows: 20 words -> conflict-free fragment loads
+constexpr int kMomStage = 128;              // patches per stage (four k32 MMA steps)
+constexpr int kMomStages = 3;
+constexpr int kMomPitch = kMomStage + 16;   // 144 B rows: 36 words -> conflict-free 8x16B reads
+constexpr uint64_t kMomMaxChunk = 65536;
 
 __device__ inline void mma_u8_16832(int (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
     asm volatile(
@@ -164,14 +170,62 @@ __device__ inline void mma_u8_16832(int (&d)[4], const uint32_t (&a)[4], const u
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
-__global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ img, int w, int C, int K, int F,
-                                                 const uint32_t* __restrict__ keys, uint64_t n, int ntile,
-                                                 unsigned long long* __restrict__ out) {
-    __shared__ int s_offi[kMomTile], s_offj[kMomTile];
-    __shared__ __align__(16) uint8_t s_xi[kMomTile * kMomPitch];
-    __shared__ __align__(16) uint8_t s_xj[kMomTile * kMomPitch];
-    __shared__ int s_base[kMomBatch];
+__device__ inline void ldmatrix_x4(uint32_t (&r)[4], const void* p) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a));
+}
 
+__device__ inline void cp_async16(void* dst, const void* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ inline void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_patch_matrix(const uint8_t* __restrict__ img, int w, int C, int K, int F,
+                                                      const uint32_t* __restrict__ keys, uint64_t n, uint64_t npad,
+                                                      uint8_t* __restrict__ XT) {
+    __shared__ int s_base[128];
+    const int tid = threadIdx.x;
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * 128;
+    if (tid < 128) {
+        const uint64_t p = p0 + tid;
+        if (p < n) {
+            const uint32_t key = keys[p];
+            s_base[tid] = static_cast<int>(((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C);
+        } else {
+            s_base[tid] = -1;
+        }
+    }
+    __shared__ __align__(16) uint8_t s_t[32 * 128];
+    __shared__ int s_off[32];
+    if (tid < 32) {
+        const int f = blockIdx.y * 32 + tid;
+        s_off[tid] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : -1;
+    }
+    __syncthreads();
+    // gather: a warp reads one feature of 32 consecutive patches (adjacent pixels)
+#pragma unroll 4
+    for (int e = tid; e < 32 * 128; e += 256) {
+        const int bs = s_base[e & 127], of = s_off[e >> 7];
+        uint8_t v = 0;
+        if (bs >= 0 && of >= 0) v = __ldg(img + bs + of);
+        s_t[e] = v;
+    }
+    __syncthreads();
+    const int fl = tid >> 3, c16 = (tid & 7) * 16;
+    *reinterpret_cast<uint4*>(XT + static_cast<size_t>(blockIdx.y * 32 + fl) * npad + p0 + c16) =
+        *reinterpret_cast<const uint4*>(s_t + fl * 128 + c16);
+}
+
+__global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ XT, uint64_t npad, int F, int ntile,
+                                                 uint64_t chunk, unsigned long long* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t sm_mom[];
     int pr = blockIdx.x, ti = 0;
     while (pr >= ntile - ti) {
         pr -= ntile - ti;
@@ -182,15 +236,28 @@ __global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ img
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp >> 2, wn = warp & 3;  // warp tile: rows wm*64..+64, cols wn*32..+32
-    if (tid < kMomTile) {
-        const int f = ti * kMomTile + tid;
-        s_offi[tid] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : -1;
-        const int f2 = tj * kMomTile + tid;
-        s_offj[tid] = f2 < F ? (((f2 / C) / K) * w + (f2 / C) % K) * C + f2 % C : -1;
+    const uint64_t c0 = static_cast<uint64_t>(blockIdx.y) * chunk;
+    const uint64_t c1 = c0 + chunk < npad ? c0 + chunk : npad;
+    const int nst = static_cast<int>((c1 - c0) / kMomStage);
+    constexpr int kTileBytes = kMomTile * kMomPitch;
+    const uint8_t* srcA = XT + static_cast<size_t>(ti) * kMomTile * npad + c0;
+    const uint8_t* srcB = XT + static_cast<size_t>(tj) * kMomTile * npad + c0;
+    auto load_stage = [&](int st) {
+        uint8_t* dA = sm_mom + (st % kMomStages) * 2 * kTileBytes;
+        uint8_t* dB = dA + kTileBytes;
+        const size_t so = static_cast<size_t>(st) * kMomStage;
+#pragma unroll
+        for (int e = tid; e < kMomTile * (kMomStage / 16); e += 256) {
+            const int r = e >> 3, c16 = (e & 7) * 16;
+            cp_async16(dA + r * kMomPitch + c16, srcA + static_cast<size_t>(r) * npad + so + c16);
+            if (!diag) cp_async16(dB + r * kMomPitch + c16, srcB + static_cast<size_t>(r) * npad + so + c16);
+        }
+    };
+#pragma unroll
+    for (int st = 0; st < kMomStages - 1; ++st) {
+        if (st < nst) load_stage(st);
+        cp_async_commit();
     }
-    const uint64_t c0 = static_cast<uint64_t>(blockIdx.y) * kMomChunk;
-    const uint64_t c1 = c0 + kMomChunk < n ? c0 + kMomChunk : n;
-
     int acc[4][4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -199,65 +266,45 @@ __global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ img
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[a][b][c] = 0;
     uint32_t rs = 0;  // row sum of row `tid` (diagonal CTAs, tid < 128)
-
-    for (uint64_t b0 = c0; b0 < c1; b0 += kMomBatch) {
-        __syncthreads();
-        if (tid < kMomBatch) {
-            const uint64_t idx = b0 + tid;
-            if (idx < c1) {
-                const uint32_t key = keys[idx];
-                s_base[tid] = static_cast<int>(((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C);
-            } else {
-                s_base[tid] = -1;
-            }
-        }
-        __syncthreads();
-        // gather: 2 x 128 rows x 16 groups of 4 patches, packed into u32 smem stores
-        for (int e = tid; e < kMomTile * (kMomBatch / 4); e += 256) {
-            const int f = e >> 4, p4 = (e & 15) * 4;
-            const int oi = s_offi[f], oj = s_offj[f];
-            uint32_t vi = 0, vj = 0;
+    // ldmatrix lane roles: matrix i = lane / 8, row lane % 8
+    const int mi = lane >> 3, mr = lane & 7;
+    for (int st = 0; st < nst; ++st) {
+        cp_async_wait<kMomStages - 2>();
+        __syncthreads();  // stage st landed; stage st-1's buffer is free
+        if (st + kMomStages - 1 < nst) load_stage(st + kMomStages - 1);
+        cp_async_commit();
+        const uint8_t* A = sm_mom + (st % kMomStages) * 2 * kTileBytes;
+        const uint8_t* B = diag ? A : A + kTileBytes;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int bs = s_base[p4 + q];
-                if (bs >= 0) {
-                    if (oi >= 0) vi |= static_cast<uint32_t>(__ldg(img + bs + oi)) << (8 * q);
-                    if (oj >= 0) vj |= static_cast<uint32_t>(__ldg(img + bs + oj)) << (8 * q);
-                }
-            }
-            *reinterpret_cast<uint32_t*>(s_xi + f * kMomPitch + p4) = vi;
-            *reinterpret_cast<uint32_t*>(s_xj + f * kMomPitch + p4) = vj;
-        }
-        __syncthreads();
+        for (int kk = 0; kk < kMomStage; kk += 32) {
+            uint32_t af[4][4], bq[2][4];
 #pragma unroll
-        for (int kk = 0; kk < kMomBatch; kk += 32) {
-            uint32_t af[4][4], bf[4][2];
+            for (int mt = 0; mt < 4; ++mt)
+                ldmatrix_x4(af[mt], A + (wm * 64 + mt * 16 + (mi & 1) * 8 + mr) * kMomPitch + kk + (mi >> 1) * 16);
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const uint8_t* r0 = s_xi + (wm * 64 + mt * 16 + g) * kMomPitch + kk + 4 * t;
-                const uint8_t* r1 = r0 + 8 * kMomPitch;
-                af[mt][0] = *reinterpret_cast<const uint32_t*>(r0);
-                af[mt][1] = *reinterpret_cast<const uint32_t*>(r1);
-                af[mt][2] = *reinterpret_cast<const uint32_t*>(r0 + 16);
-                af[mt][3] = *reinterpret_cast<const uint32_t*>(r1 + 16);
-            }
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-                const uint8_t* c = s_xj + (wn * 32 + nt * 8 + g) * kMomPitch + kk + 4 * t;
-                bf[nt][0] = *reinterpret_cast<const uint32_t*>(c);
-                bf[nt][1] = *reinterpret_cast<const uint32_t*>(c + 16);
-            }
+            for (int np = 0; np < 2; ++np)
+                ldmatrix_x4(bq[np], B + (wn * 32 + np * 16 + (mi >> 1) * 8 + mr) * kMomPitch + kk + (mi & 1) * 16);
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) mma_u8_16832(acc[mt][nt], af[mt], bf[nt]);
+                for (int nt = 0; nt < 4; ++nt) {
+                    const uint32_t bf[2] = {bq[nt >> 1][(nt & 1) * 2], bq[nt >> 1][(nt & 1) * 2 + 1]};
+                    mma_u8_16832(acc[mt][nt], af[mt], bf);
+                }
         }
         if (diag && tid < kMomTile) {
-            const uint8_t* row = s_xi + tid * kMomPitch;
+            const uint8_t* row = A + tid * kMomPitch;
 #pragma unroll
-            for (int q = 0; q < kMomBatch; q += 4) rs = __dp4a(*reinterpret_cast<const uint32_t*>(row + q), 0x01010101u, rs);
+            for (int q = 0; q < kMomStage; q += 16) {
+                const uint4 v = *reinterpret_cast<const uint4*>(row + q);
+                rs = __dp4a(v.x, 0x01010101u, rs);
+                rs = __dp4a(v.y, 0x01010101u, rs);
+                rs = __dp4a(v.z, 0x01010101u, rs);
+                rs = __dp4a(v.w, 0x01010101u, rs);
+            }
         }
     }
+    cp_async_wait<0>();
     // flush: D fragment (row g / g+8, cols 2t, 2t+1) of every 16x8 tile
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
@@ -267,8 +314,8 @@ __global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ img
             for (int c = 0; c < 4; ++c) {
                 const int fi = ti * kMomTile + wm * 64 + mt * 16 + g + (c >> 1) * 8;
                 const int fj = tj * kMomTile + wn * 32 + nt * 8 + 2 * t + (c & 1);
-                const int v = acc[mt][nt][c];
-                if (fi < F && fj < F && v) atomicAdd(out + F + static_cast<size_t>(fi) * F + fj, static_cast<unsigned long long>(static_cast<unsigned>(v)));
+                const unsigned v = static_cast<unsigned>(acc[mt][nt][c]);
+                if (fi < F && fj < F && v) atomicAdd(out + F + static_cast<size_t>(fi) * F + fj, static_cast<unsigned long long>(v));
             }
     if (diag && tid < kMomTile && rs) {
         const int fi = ti * kMomTile + tid;
@@ -283,10 +330,25 @@ void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const
                             ctx->stream));
     if (n == 0) return;
     const int ntile = (F + kMomTile - 1) / kMomTile;
+    const int Fpad = ntile * kMomTile;
+    const uint64_t npad = (n + kMomStage - 1) / kMomStage * kMomStage;
+    uint8_t* XT = ctx->scratch.ensure(static_cast<size_t>(Fpad) * npad);
+    ZI_LAUNCH(ctx, "patch_matrix", k_patch_matrix, dim3(static_cast<unsigned>(npad / 128), Fpad / 32), 256, 0, d_img,
+              w, C, K, F, d_keys, n, npad, XT);
     const int npairs = ntile * (ntile + 1) / 2;
-    const uint64_t nchunk = (n + kMomChunk - 1) / kMomChunk;
-    ZI_LAUNCH(ctx, "patch_moments", k_moments, dim3(npairs, static_cast<unsigned>(nchunk)), 256, 0, d_img, w, C, K, F,
-              d_keys, n, ntile, d_out);
+    // about two CTAs per SM in one wave; stage-aligned chunks of <= 65536 patches
+    const uint64_t want = std::max<uint64_t>(1, (2ull * ctx->num_sms + npairs - 1) / npairs);
+    uint64_t chunk = (npad + want - 1) / want;
+    chunk = std::min<uint64_t>(kMomMaxChunk, (chunk + kMomStage - 1) / kMomStage * kMomStage);
+    const uint64_t nchunk = (npad + chunk - 1) / chunk;
+    const size_t smem = static_cast<size_t>(kMomStages) * 2 * kMomTile * kMomPitch;
+    static bool attr = false;
+    if (!attr) {
+        ZI_CUDA(cudaFuncSetAttribute(k_moments, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = true;
+    }
+    ZI_LAUNCH(ctx, "patch_moments", k_moments, dim3(npairs, static_cast<unsigned>(nchunk)), 256, smem, XT, npad, F,
+              ntile, chunk, d_out);
 }
 
 // ============================================================== K3: projection
