@@ -123,6 +123,8 @@ __device__ void tri_factor(const double* d, const double* e, int n, double sigma
     }
     if (dcur == 0.0) dcur = tiny;
     u1i[n - 1] = fast_rcp(fabs(dcur) < tiny ? (dcur < 0 ? -tiny : tiny) : dcur);
+    u2[n - 1] = 0.0;  // read (times zero) by the first back-substitution step: never stale
+    u3[n - 1] = 0.0;
 }
 
 // b := (T - sigma I)^-1 b with the factors above; the recurrences carry their state in registers.

@@ -8,6 +8,8 @@
 //
 // Records are SoA: word k of every record is contiguous (coalesced loads per word).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -256,6 +258,270 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
             ZI_CUDA(cudaMemcpyAsync(words[k], cur[k], n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
+// ---------------------------------------------------------------------------- hybrid sort
+// MSD split + local sort.  msd_bytes() onesweep passes order the records by the top Morton bytes
+// (and, for the 8-layout build, the layout bits of the payload) -- segments of equal top bits
+// are then contiguous.  k_segsort finishes each segment in shared memory with the full
+// comparator (Morton key, payload).  The payload is unique, so this order is the unique stable
+// order whatever order the segment arrives in; the result is bit-identical to the all-LSD sort
+// at roughly a third of its HBM passes.
+static int msd_bytes() {
+    static const int v = [] {
+        const char* e = std::getenv("ZI_SORT_MSD");
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
+constexpr int kSegThreads = 256;
+
+template <int NW>
+struct seg_ctx {
+    uint32_t* w[kMaxWords];
+    uint64_t N;
+    int D, nb;
+    bool layouts;
+};
+
+template <int NW>
+__device__ inline uint64_t seg_key(const seg_ctx<NW>& c, uint64_t i) {
+    uint64_t k = c.layouts ? (c.w[NW - 1][i] >> 29) : 0u;
+    for (int p = c.D - 1; p >= c.D - c.nb && p >= 0; --p) k = (k << 8) | ((c.w[p >> 2][i] >> ((p & 3) * 8)) & 0xffu);
+    return k;
+}
+
+// first segment head at or after `from` (N if none); one warp
+template <int NW>
+__device__ inline uint64_t find_head(const seg_ctx<NW>& c, uint64_t from) {
+    const int lane = threadIdx.x & 31;
+    if (from == 0) return 0;
+    for (uint64_t b = from; b < c.N; b += 32) {
+        const uint64_t i = b + lane;
+        const bool h = i < c.N && seg_key(c, i) != seg_key(c, i - 1);
+        const unsigned m = __ballot_sync(0xffffffffu, h);
+        if (m) return b + __ffs(m) - 1;
+    }
+    return c.N;
+}
+
+// One CTA sorts one window: the records of the segments that start in [w*T, (w+1)*T) (so the
+// window is a union of whole segments), all passes of the global LSD sort replayed in shared
+// memory on a u16 permutation (the records themselves stay put), then written back in place.
+// Segments never change the segment key at any position, so neighbours reading a boundary
+// while this CTA writes see the same keys.
+template <int NW>
+__global__ void __launch_bounds__(kSegThreads) k_segsort(seg_ctx<NW> c, int T, int cap, int npass,
+                                                         const int2* __restrict__ passes,
+                                                         unsigned long long* __restrict__ big,
+                                                         uint32_t* __restrict__ nbig) {
+    extern __shared__ uint32_t s_w[];  // NW * cap words, then cur / nxt (u16 cap each)
+    uint16_t* s_cur = reinterpret_cast<uint16_t*>(s_w + static_cast<size_t>(NW) * cap);
+    uint16_t* s_nxt = s_cur + cap;
+    constexpr int kWarps = kSegThreads / 32;
+    __shared__ uint32_t s_hist[kWarps][256];
+    __shared__ uint32_t s_dstart[256];
+    __shared__ uint32_t s_wsum[kWarps];
+    __shared__ uint64_t s_range[2];
+    __shared__ int2 s_pass[40];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * T;
+    const uint64_t w1 = w0 + T < c.N ? w0 + T : c.N;
+    if (warp == 0) {
+        const uint64_t st = find_head(c, w0);
+        if (lane == 0) s_range[0] = st;
+    } else if (warp == 1) {
+        const uint64_t en = w1 >= c.N ? c.N : find_head(c, w1);
+        if (lane == 0) s_range[1] = en;
+    }
+    if (tid < npass) s_pass[tid] = passes[tid];
+    __syncthreads();
+    const uint64_t start = s_range[0], end = s_range[1];
+    if (start >= w1) return;  // no segment starts in this window
+    if (end - start > static_cast<uint64_t>(cap)) {  // longer than shared memory: global fallback
+        if (tid == 0) {
+            const uint32_t slot = atomicAdd(nbig, 1u);
+            big[2 * slot] = start;
+            big[2 * slot + 1] = end;
+        }
+        return;
+    }
+    const int len = static_cast<int>(end - start);
+    if (len <= 1) return;
+    __shared__ uint32_t s_and[NW], s_or[NW];
+    if (tid < NW) {
+        s_and[tid] = 0xffffffffu;
+        s_or[tid] = 0u;
+    }
+    __syncthreads();
+    uint32_t wand[NW], wor[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+        wand[k] = 0xffffffffu;
+        wor[k] = 0u;
+    }
+    for (int j = tid; j < len; j += kSegThreads) {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const uint32_t x = c.w[k][start + j];
+            s_w[k * cap + j] = x;
+            wand[k] &= x;
+            wor[k] |= x;
+        }
+        s_cur[j] = static_cast<uint16_t>(j);
+    }
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {  // digits equal over the whole window need no pass
+        atomicAnd(&s_and[k], wand[k]);
+        atomicOr(&s_or[k], wor[k]);
+    }
+    __syncthreads();
+    // warp w ranks the contiguous chunk [w*CH, (w+1)*CH) in rounds of 32 (stable order)
+    const int CH = ((len + kWarps - 1) / kWarps + 31) & ~31;
+    const int nround = CH / 32;
+    const uint32_t lt = (1u << lane) - 1u;
+    constexpr int kMaxRounds = 16;  // cap <= 4096 -> CH <= 512
+    for (int q = 0; q < npass; ++q) {
+        const int wk = s_pass[q].x, sh = s_pass[q].y;
+        if ((((s_and[wk] ^ s_or[wk]) >> sh) & 0xffu) == 0u) continue;  // uniform: constant digit
+        for (int i = tid; i < kWarps * 256; i += kSegThreads) (&s_hist[0][0])[i] = 0;
+        __syncthreads();
+        uint32_t dg[kMaxRounds], rk[kMaxRounds];
+#pragma unroll
+        for (int r = 0; r < kMaxRounds; ++r) {
+            if (r < nround) {
+                const int i = warp * CH + r * 32 + lane;
+                uint32_t d = 256u;
+                if (i < len) d = (s_w[wk * cap + s_cur[i]] >> sh) & 0xffu;
+                const uint32_t peers = __match_any_sync(0xffffffffu, d);
+                uint32_t old = 0;
+                if (d < 256u) old = s_hist[warp][d];
+                __syncwarp();
+                if (d < 256u && (peers >> lane) == 1u) s_hist[warp][d] = old + __popc(peers);
+                __syncwarp();
+                dg[r] = d;
+                rk[r] = old + __popc(peers & lt);
+            }
+        }
+        __syncthreads();
+        // digit-major exclusive offsets: warp w's run of digit d starts at dstart[d] + off[w][d]
+        {
+            const int d = tid;  // kSegThreads == 256 digits
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t t = s_hist[w][d];
+                s_hist[w][d] = run;
+                run += t;
+            }
+            uint32_t x = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_wsum[warp] = x;
+            __syncthreads();
+            uint32_t wp = 0;
+            for (int w = 0; w < warp; ++w) wp += s_wsum[w];
+            s_dstart[d] = wp + x - run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kMaxRounds; ++r) {
+            if (r < nround) {
+                const int i = warp * CH + r * 32 + lane;
+                if (dg[r] < 256u) s_nxt[s_dstart[dg[r]] + s_hist[warp][dg[r]] + rk[r]] = s_cur[i];
+            }
+        }
+        __syncthreads();
+        uint16_t* t = s_cur;
+        s_cur = s_nxt;
+        s_nxt = t;
+    }
+    for (int j = tid; j < len; j += kSegThreads) {
+        const int src = s_cur[j];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) c.w[k][start + j] = s_w[k * cap + src];
+    }
+}
+
+template <int NW>
+static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int D, int nb, bool layouts,
+                           const std::vector<int2>& passes, int2* d_passes, unsigned long long* big, uint32_t* nbig) {
+    seg_ctx<NW> c{};
+    for (int k = 0; k < NW; ++k) c.w[k] = words[k];
+    c.N = N;
+    c.D = D;
+    c.nb = nb;
+    c.layouts = layouts;
+    int cap = 4096;
+    while (cap > 1024 && static_cast<size_t>(cap) * (NW * 4 + 4) > 100 * 1024) cap >>= 1;
+    const int T = cap / 2;
+    const size_t smem = static_cast<size_t>(cap) * (NW * 4 + 4);
+    static size_t attr = 0;
+    if (smem > attr) {
+        ZI_CUDA(cudaFuncSetAttribute(k_segsort<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = smem;
+    }
+    ZI_CUDA(cudaMemcpyAsync(d_passes, passes.data(), passes.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
+    const unsigned grid = static_cast<unsigned>((N + T - 1) / T);
+    ZI_LAUNCH(ctx, "segment_sort", k_segsort<NW>, grid, kSegThreads, smem, c, T, cap, static_cast<int>(passes.size()),
+              d_passes, big, nbig);
+}
+
+// Sort (key words, payload) records by (Morton key, payload); `layouts`: the payload's top 3
+// bits are a layout id that orders first.
+static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts) {
+    const int nw = W + 1;
+    const int nb = std::min(msd_bytes(), D);
+    std::vector<int2> msd, all;
+    for (int p = D - nb; p < D; ++p) msd.push_back(make_int2(p >> 2, (p & 3) * 8));
+    for (int p = 0; p < D; ++p) all.push_back(make_int2(p >> 2, (p & 3) * 8));
+    if (layouts) {
+        msd.push_back(make_int2(W, 29));
+        all.push_back(make_int2(W, 29));
+    }
+    radix_sort_words(ctx, words, nw, N, msd);
+    // counters | big-segment list | pass table, in the context counter buffer
+    const size_t max_big = 4096;
+    uint32_t* cnt = ctx->counter.ensure(16 + 4 * max_big + 2 * 64);
+    unsigned long long* big = reinterpret_cast<unsigned long long*>(cnt + 16);
+    int2* d_passes = reinterpret_cast<int2*>(cnt + 16 + 4 * max_big);
+    ZI_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), ctx->stream));
+    switch (nw) {
+        case 2: launch_segsort<2>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        case 3: launch_segsort<3>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        case 4: launch_segsort<4>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        case 5: launch_segsort<5>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        case 6: launch_segsort<6>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        case 7: launch_segsort<7>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        case 8: launch_segsort<8>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        case 9: launch_segsort<9>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        default: throw error(ZI_E_INVALID, "radix sort: unsupported record width");
+    }
+    uint32_t hc[4] = {0, 0, 0, 0};
+    ZI_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint32_t nbig = hc[0];
+    static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
+    if (debug)
+        std::fprintf(stderr, "hybrid sort N=%llu nb=%d: oversized segments %u\n", static_cast<unsigned long long>(N),
+                     nb, nbig);
+    if (nbig == 0) return;
+    if (nbig > max_big) throw error(ZI_E_RUNTIME, "hybrid sort: too many oversized segments");
+    std::vector<unsigned long long> h(2 * nbig);
+    ZI_CUDA(cudaMemcpyAsync(h.data(), big, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    // oversized segments (equal top bytes, longer than shared memory): the remaining Morton
+    // bytes by the global LSD sort on that range (stable, so the payload order of ties stays)
+    std::vector<int2> rest;
+    for (int p = 0; p < D - nb; ++p) rest.push_back(make_int2(p >> 2, (p & 3) * 8));
+    for (uint32_t q = 0; q < nbig; ++q) {
+        uint32_t* sub[kMaxWords];
+        for (int k = 0; k < nw; ++k) sub[k] = words[k] + h[2 * q];
+        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], rest);
+    }
+}
+
 void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first) {
     const int W = (D + 3) / 4;
     uint32_t* words[kMaxWords];
@@ -273,10 +539,7 @@ void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_
     uint32_t* words[kMaxWords];
     for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * N;
     words[W] = d_val;
-    std::vector<int2> passes;
-    for (int p = 0; p < D; ++p) passes.push_back(make_int2(p >> 2, (p & 3) * 8));
-    passes.push_back(make_int2(W, 29));  // layout id (3 bits)
-    radix_sort_words(ctx, words, W + 1, N, passes);
+    morton_sort_hybrid(ctx, words, W, N, D, true);
 }
 
 }  // namespace zi
