@@ -186,17 +186,27 @@ class ClockSampler:
 # ---------------------------------------------------------------------------- roofline model
 def algorithmic_bytes(kernel: str, n: int, D: int, mc: int) -> float | None:
     """Algorithmic HBM bytes per launch; gathered pixels are L1/L2 served.
-    The radix sort runs once over the records of all 8 layouts (N = 8n)."""
+    The radix passes and the window sort run once over the records of all 8 layouts (N = 8n)."""
     W = (D + 3) // 4
     N = 8 * n
     return {
         "radix_onesweep": 2 * 4 * (W + 1) * N,          # read + write of (W key words + payload)
+        "segment_sort": 2 * 4 * (W + 1) * N,            # one read + one in-place write per record
         "radix_hist": 4 * (W + 1) * N,
-        "project": (4 + 8 * D) * n,                     # dictionary key in, fp64 projections out
         "proj_minmax": 8 * D * n,
         "quantize_interleave": (8 * D + 4 + 4 * (W + 1)) * n,
         "finalize_index": (4 * (W + 1) + 4 * (W + 1)) * n,
     }.get(kernel)
+
+
+def algorithmic_flops(kernel: str, n: int, D: int, mc: int) -> float | None:
+    """Useful fp64 flops per launch of the tensor-core kernels (2 per FMA; padding excluded)."""
+    return {"project": 2.0 * n * mc * D}.get(kernel)
+
+
+# B200 FP64 tensor-core peak: not in MEASURED_PEAKS.json (driver measures bf16 only) nor in the
+# profiling recipe -> NVIDIA's B200 datasheet figure.
+FP64_TENSOR_PEAK_TFLOPS = 40.0
 
 
 def candidate_scoring(zb, ctx, args, hbm_peak):
@@ -326,19 +336,36 @@ def main():
         pass
     breakdown = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                  for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
-    # the dominant HBM-bound kernel (the sort); fp64/int-compute kernels are listed in breakdown
-    hbm_kernels = {k: v for k, v in prof.items() if algorithmic_bytes(k, n, mi.dims, mc) is not None
-                   and k not in ("project",)}
-    if hbm_kernels:
-        kname, (kms, kl) = max(hbm_kernels.items(), key=lambda kv: kv[1][0])
+    # roofline of the dominant kernel of the step (the fp64 tensor-core projection) and, beside
+    # it, of the dominant HBM-bound kernel
+    def hbm_roofline(kname, kms, kl):
         per_launch_ms = kms / max(kl, 1)
         b = algorithmic_bytes(kname, n, mi.dims, mc)
         achieved = b / (per_launch_ms * 1e-3) / 1e9
         tr = traffic_db.get(args.config, {}).get(kname)
-        roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": achieved / hbm_peak, "traffic": tr, "bytes_per_launch": b,
-                    "avg_launch_ms": per_launch_ms,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+        return {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": tr, "bytes_per_launch": b,
+                "avg_launch_ms": per_launch_ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+
+    hbm_kernels = {k: v for k, v in prof.items() if algorithmic_bytes(k, n, mi.dims, mc) is not None}
+    roofline_hbm = None
+    if hbm_kernels:
+        kname, (kms, kl) = max(hbm_kernels.items(), key=lambda kv: kv[1][0])
+        roofline_hbm = hbm_roofline(kname, kms, kl)
+    if dom is not None and algorithmic_flops(dom[0], n, mi.dims, mc) is not None:
+        kname, (kms, kl) = dom
+        per_launch_ms = kms / max(kl, 1)
+        fl = algorithmic_flops(kname, n, mi.dims, mc)
+        achieved = fl / (per_launch_ms * 1e-3) / 1e12
+        roofline = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": FP64_TENSOR_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
+                    "traffic": traffic_db.get(args.config, {}).get(kname), "flops_per_launch": fl,
+                    "avg_launch_ms": per_launch_ms, "dtype": "f64 (mma.m8n8k4.f64)",
+                    "peak_source": "B200 datasheet FP64 Tensor Core 40 TFLOPS (no measured fp64 peak on this pool)",
+                    "note": "D=12 fills 12 of the 16 MMA columns, so the useful-flop ceiling is 0.75 of peak"}
+    else:
+        roofline = roofline_hbm
 
     # -------- e2e through the public C ABI with pinned host buffers
     e2e = None
@@ -421,7 +448,8 @@ def main():
                                    f"D={mi.dims}, 8 layout indices, n={n} dictionary patches per rank",
                        "global_batch": n_total, "parallelism": f"replicas x{world} (independent images)",
                        "l2": "flushed (256 MiB write) before every timed step"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "roofline_hbm": roofline_hbm, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
             "clocks": clk, "inpaint": inpaint, "candidate_scoring": knn,
             "breakdown": {"host_eigen_s_per_step": float(np.mean(host_eigen)), "kernels": breakdown},
         }

@@ -10,6 +10,8 @@ KEYS = ['gpu__time_duration.sum', 'sm__throughput.avg.pct_of_peak_sustained_elap
         'dram__throughput.avg.pct_of_peak_sustained_elapsed', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
         'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
         'sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active',
         'sm__warps_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread',
         'smsp__issue_active.avg.pct_of_peak_sustained_active', 'smsp__inst_executed.sum', 'launch__grid_size']
 
