@@ -378,7 +378,8 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restr
                                                           const uint32_t* __restrict__ keys, uint64_t n,
                                                           const int32_t* __restrict__ off, int m,
                                                           const double* __restrict__ mean,
-                                                          const double* __restrict__ comp, double* __restrict__ Y) {
+                                                          const double* __restrict__ comp, double* __restrict__ Y,
+                                                          unsigned long long* __restrict__ minmax) {
     constexpr int NT = (D + 7) / 8;  // 8-dim tiles
     constexpr int G = kProjGroups;
     extern __shared__ double sm[];
@@ -395,6 +396,10 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restr
         s_mean[j] = j < mc ? mean[j] : 0.0;
         s_joff[j] = j < mc ? off[j / C] + j % C : 0;
     }
+    // the quantiser's lo / hi: block-level ordered-u64 min / max in shared memory, folded in
+    // with shared atomics as each 8-patch group is stored (no running registers)
+    __shared__ unsigned long long s_mm[2][D];
+    if (threadIdx.x < 2 * D) s_mm[threadIdx.x / D][threadIdx.x % D] = threadIdx.x < D ? ~0ull : 0ull;
     __syncthreads();
     const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
     const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kProjThreads / 32);
@@ -456,44 +461,21 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restr
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int d = 8 * t + 2 * c + e;
-                        if (d < D) Y[static_cast<size_t>(d) * n + i] = acc[g][t][e];
+                        if (d < D) {
+                            const double y = acc[g][t][e];
+                            Y[static_cast<size_t>(d) * n + i] = y;
+                            const unsigned long long o = double_to_ordered(y);
+                            atomicMin(&s_mm[0][d], o);
+                            atomicMax(&s_mm[1][d], o);
+                        }
                     }
             }
         }
     }
-}
-
-// per-dimension min/max of Y -> ordered-u64 atomics (lo: atomicMin, hi: atomicMax)
-__global__ void __launch_bounds__(256) k_minmax(const double* __restrict__ Y, uint64_t n,
-                                                unsigned long long* __restrict__ minmax, int D) {
-    const int d = blockIdx.y;
-    const double* y = Y + static_cast<size_t>(d) * n;
-    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const double v = y[i];
-        lo = v < lo ? v : lo;
-        hi = v > hi ? v : hi;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
-        lo = a < lo ? a : lo;
-        hi = b > hi ? b : hi;
-    }
-    __shared__ double s_lo[8], s_hi[8];
-    if ((threadIdx.x & 31) == 0) {
-        s_lo[threadIdx.x >> 5] = lo;
-        s_hi[threadIdx.x >> 5] = hi;
-    }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) {
-            lo = s_lo[k] < lo ? s_lo[k] : lo;
-            hi = s_hi[k] > hi ? s_hi[k] : hi;
-        }
-        atomicMin(minmax + d, double_to_ordered(lo));
-        atomicMax(minmax + D + d, double_to_ordered(hi));
+    if (threadIdx.x < D) {
+        atomicMin(minmax + threadIdx.x, s_mm[0][threadIdx.x]);
+        atomicMax(minmax + D + threadIdx.x, s_mm[1][threadIdx.x]);
     }
 }
 
@@ -627,7 +609,8 @@ __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ k
 // ============================================================== host launchers
 template <int D>
 static void launch_project_t(zi_ctx* ctx, const uint8_t* img, int w, int C, const uint32_t* keys, uint64_t n,
-                             const int32_t* off, int m, const double* mean, const double* comp, double* Y) {
+                             const int32_t* off, int m, const double* mean, const double* comp, double* Y,
+                             unsigned long long* minmax) {
     constexpr int NT = (D + 7) / 8;
     const int KS = (m * C + 3) / 4;
     const size_t smem = static_cast<size_t>(KS) * NT * 32 * sizeof(double) + static_cast<size_t>(KS) * 4 * sizeof(double) +
@@ -640,7 +623,8 @@ static void launch_project_t(zi_ctx* ctx, const uint8_t* img, int w, int C, cons
     const uint64_t warps = (n + 8 * kProjGroups - 1) / (8 * kProjGroups);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((warps + kProjThreads / 32 - 1) / (kProjThreads / 32),
                                                                    static_cast<uint64_t>(ctx->num_sms) * 8));
-    ZI_LAUNCH(ctx, "project", k_project<D>, grid, kProjThreads, smem, img, w, C, keys, n, off, m, mean, comp, Y);
+    ZI_LAUNCH(ctx, "project", k_project<D>, grid, kProjThreads, smem, img, w, C, keys, n, off, m, mean, comp, Y,
+              minmax);
 }
 
 template <int D>
@@ -682,12 +666,11 @@ void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_
              const int32_t* d_off, int m, const double* d_mean, const double* d_comp, int D, double* d_Y,
              unsigned long long* d_minmax) {
     if (n == 0) return;
-    ZI_DIMS_SWITCH(D, launch_project_t, ctx, d_img, w, C, d_keys, n, d_off, m, d_mean, d_comp, d_Y);
-    // lo slots start at the ordered max, hi slots at the ordered min
+    // lo slots start at the ordered max, hi slots at the ordered min; the projection folds in
+    // its per-block min / max
     ZI_CUDA(cudaMemsetAsync(d_minmax, 0xff, D * sizeof(unsigned long long), ctx->stream));
     ZI_CUDA(cudaMemsetAsync(d_minmax + D, 0x00, D * sizeof(unsigned long long), ctx->stream));
-    const unsigned gx = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, std::max(1, ctx->num_sms * 16 / D)));
-    ZI_LAUNCH(ctx, "proj_minmax", k_minmax, dim3(gx, D), 256, 0, d_Y, n, d_minmax, D);
+    ZI_DIMS_SWITCH(D, launch_project_t, ctx, d_img, w, C, d_keys, n, d_off, m, d_mean, d_comp, d_Y, d_minmax);
 }
 
 void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax, uint64_t n, uint64_t N,

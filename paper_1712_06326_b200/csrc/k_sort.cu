@@ -453,7 +453,8 @@ static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int 
     c.D = D;
     c.nb = nb;
     c.layouts = layouts;
-    int cap = 4096;
+    static const int cap0 = [] { const char* e = std::getenv("ZI_SORT_CAP"); return e ? std::atoi(e) : 4096; }();
+    int cap = cap0;
     while (cap > 1024 && static_cast<size_t>(cap) * (NW * 4 + 4) > 100 * 1024) cap >>= 1;
     const int T = cap / 2;
     const size_t smem = static_cast<size_t>(cap) * (NW * 4 + 4);
