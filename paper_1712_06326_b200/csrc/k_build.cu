@@ -490,6 +490,18 @@ __global__ void __launch_bounds__(256) k_quantize(const double* __restrict__ Y,
                                                   uint32_t* __restrict__ val) {
     constexpr int W = (D + 3) / 4;
     __shared__ double s_lo[D], s_hi[D], s_rcp[D];
+    // spread table: bit L of q -> bit L*D (W words); dim d's contribution is spread(q) << (D-1-d)
+    __shared__ uint32_t s_spread[256][W];
+    {
+        const uint32_t q = threadIdx.x;  // blockDim.x == 256
+        uint32_t sp[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) sp[k] = 0;
+#pragma unroll
+        for (int L = 0; L < 8; ++L) sp[(L * D) >> 5] |= ((q >> L) & 1u) << ((L * D) & 31);
+#pragma unroll
+        for (int k = 0; k < W; ++k) s_spread[q][k] = sp[k];
+    }
     if (threadIdx.x < D) {
         const double l = ordered_to_double_hd(minmax[threadIdx.x]);
         const double h = ordered_to_double_hd(minmax[D + threadIdx.x]);
@@ -509,10 +521,13 @@ __global__ void __launch_bounds__(256) k_quantize(const double* __restrict__ Y,
 #pragma unroll
         for (int d = 0; d < D; ++d) {
             const uint32_t q = quantize_fast(s_lo[d], s_hi[d], s_rcp[d], y[d]);
+            const int sh = D - 1 - d;  // = morton_bit(0, d, D)
+            uint32_t prev = 0;
 #pragma unroll
-            for (int L = 0; L < 8; ++L) {
-                const int u = morton_bit(L, d, D);
-                kw[u >> 5] |= ((q >> L) & 1u) << (u & 31);
+            for (int k = 0; k < W; ++k) {
+                const uint32_t cur = s_spread[q][k];
+                kw[k] |= sh ? __funnelshift_l(prev, cur, sh) : cur;
+                prev = cur;
             }
         }
         const uint64_t e = static_cast<uint64_t>(layout) * n + i;
