@@ -185,6 +185,7 @@ zi_status zi_ctx_destroy(zi_ctx* ctx) {
         ctx->scratch.release();  // stream-ordered frees before the stream goes away
         ctx->counter.release();
         ctx->flush.release();
+        ctx->deint.release();
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
         delete ctx;

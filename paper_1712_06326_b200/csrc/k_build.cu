@@ -561,12 +561,34 @@ __global__ void __launch_bounds__(256) k_interleave(const uint8_t* __restrict__ 
 // Sorted Morton words -> dim planes (4 dims per u32), keys, and per-256-entry bboxes.
 // Entries [off, off+n) of a record array with word stride N; when dict != nullptr the payload
 // is a dictionary row (low 29 bits) and the key is gathered from dict.
+// De-interleave table: key byte B with value v contributes tab[(B*256 + v)*W + k] to plane word
+// k (bit j of the byte is key bit u = 8B + j = L*D + D-1-d -> bit L of dim d's plane byte).
+template <int D>
+__global__ void k_deinterleave_table(uint32_t* __restrict__ tab) {
+    constexpr int W = (D + 3) / 4;
+    const int B = blockIdx.x, v = threadIdx.x;
+    uint32_t w[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) w[k] = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int u = 8 * B + j;
+        if (((v >> j) & 1) && u < 8 * D) {
+            const int L = u / D, d = D - 1 - u % D;
+            w[d >> 2] |= 1u << (8 * (d & 3) + L);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) tab[(B * 256 + v) * W + k] = w[k];
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
                                                   uint64_t N, uint64_t off, uint64_t n,
                                                   const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
-                                                  uint32_t* __restrict__ bmax, uint64_t nblk) {
+                                                  uint32_t* __restrict__ bmax, uint64_t nblk,
+                                                  const uint32_t* __restrict__ tab) {
     constexpr int W = (D + 3) / 4, P = W;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
     const bool ok = i < n;
@@ -579,22 +601,19 @@ __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ k
     }
     __shared__ uint32_t s_mn[P][8], s_mx[P][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t pw[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) pw[p] = 0;
+#pragma unroll
+    for (int B = 0; B < D; ++B) {  // the key has D bytes
+        const uint32_t v = (kw[B >> 2] >> (8 * (B & 3))) & 0xffu;
+        const uint32_t* t = tab + (B * 256 + v) * W;
+#pragma unroll
+        for (int p = 0; p < P; ++p) pw[p] |= __ldg(t + p);
+    }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int d = p * 4 + b;
-            if (d < D) {
-                uint32_t c = 0;
-#pragma unroll
-                for (int L = 0; L < 8; ++L) {
-                    const int u = morton_bit(L, d, D);
-                    c |= ((kw[u >> 5] >> (u & 31)) & 1u) << L;
-                }
-                word |= c << (8 * b);
-            }
-        }
+        const uint32_t word = pw[p];
         if (ok) planes[static_cast<size_t>(p) * n + i] = word;
         uint32_t mn = ok ? word : 0xffffffffu, mx = ok ? word : 0u;
 #pragma unroll
@@ -673,8 +692,14 @@ static void launch_quantize_t(zi_ctx* ctx, const double* Y, const unsigned long 
 template <int D>
 static void launch_finalize_t(zi_ctx* ctx, const uint32_t* keyw, const uint32_t* val, uint64_t N, uint64_t off,
                               uint64_t n, const uint32_t* dict, zi_index* idx) {
+    constexpr int W = (D + 3) / 4;
+    if (ctx->deint_D != D) {
+        ctx->deint.ensure(static_cast<size_t>(D) * 256 * W);
+        ZI_LAUNCH(ctx, "deinterleave_table", k_deinterleave_table<D>, D, 256, 0, ctx->deint.p);
+        ctx->deint_D = D;
+    }
     ZI_LAUNCH(ctx, "finalize_index", k_finalize<D>, static_cast<unsigned>(idx->nblk), 256, 0, keyw, val, N, off, n,
-              dict, idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk);
+              dict, idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk, ctx->deint.p);
 }
 
 void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_keys, uint64_t n,

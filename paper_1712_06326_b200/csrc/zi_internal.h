@@ -109,6 +109,8 @@ struct zi_ctx {
     zi::dbuf<uint8_t> scratch;
     zi::dbuf<uint32_t> counter;  // small integer scratch (tile counters etc.)
     zi::dbuf<uint8_t> flush;     // L2 flush buffer (bench hygiene)
+    zi::dbuf<uint32_t> deint;    // Morton de-interleave table of dims deint_D (finalize)
+    int deint_D = 0;
     int flush_toggle = 1;
 };
 
