@@ -351,16 +351,20 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
                 double* row = A + static_cast<size_t>(li) * n + k + 1;
                 const double vt = t == 0 ? v0 : vb[t];
                 const double wt = fma(-K2, vt, pb[t]);
-                double y0 = 0.0;
+                double rv[kSlots];  // loads, math, stores in three batches (no smem aliasing chain)
 #pragma unroll
                 for (int q = 0; q < kSlots; ++q) {
                     const int j = lane + 32 * q;
-                    if (j < m) {
-                        const double y = fma(-vt, wr[q], fma(-wt, vr[q], row[j]));
-                        row[j] = y;
-                        if (q == 0) y0 = y;
-                    }
+                    rv[q] = j < m ? row[j] : 0.0;
                 }
+#pragma unroll
+                for (int q = 0; q < kSlots; ++q) rv[q] = fma(-vt, wr[q], fma(-wt, vr[q], rv[q]));
+#pragma unroll
+                for (int q = 0; q < kSlots; ++q) {
+                    const int j = lane + 32 * q;
+                    if (j < m) row[j] = rv[q];
+                }
+                double y0 = rv[0];
                 if (next && t >= 1) {
                     y0 = __shfl_sync(0xffffffffu, y0, 0);
                     push_entry(k + 1, b ^ 1, t + k + 1, y0);
