@@ -8,6 +8,7 @@
 //
 // Records are SoA: word k of every record is contiguous (coalesced loads per word).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -176,7 +177,28 @@ static void launch_onesweep(zi_ctx* ctx, const sort_words& io, int dw, int ds, c
 
 // Generic stable LSD sort of NW-word SoA records; passes are (word, shift) digits from the
 // least significant.  Trivial passes (all records share the digit) are skipped.
-void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes) {
+// digit histograms of every pass (host copy, pass-major 256 bins), one read of the records
+std::vector<uint32_t> pass_histograms(zi_ctx* ctx, uint32_t* const* words, int nw, uint64_t n,
+                                      const std::vector<int2>& passes) {
+    const int npass = static_cast<int>(passes.size());
+    const size_t hist_words = static_cast<size_t>(npass) * 256;
+    uint32_t* h = ctx->counter.ensure(hist_words + 4 * npass + 64);
+    int2* d_passes = reinterpret_cast<int2*>(h + hist_words + 8);
+    d_passes = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(d_passes) + 15) & ~uintptr_t(15));
+    ZI_CUDA(cudaMemsetAsync(h, 0, hist_words * sizeof(uint32_t), ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(d_passes, passes.data(), passes.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
+    sort_words io{};
+    for (int k = 0; k < nw; ++k) io.in[k] = words[k];
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 4));
+    ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hist_words * sizeof(uint32_t), io, npass, d_passes, n, h);
+    std::vector<uint32_t> out(hist_words);
+    ZI_CUDA(cudaMemcpyAsync(out.data(), h, hist_words * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    return out;
+}
+
+void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
+                      const uint32_t* hist_host) {
     if (n <= 1 || passes.empty()) return;
     if (n > kValMask) throw error(ZI_E_INVALID, "radix sort: more than 2^30 records");
     if (nw > kMaxWords) throw error(ZI_E_INVALID, "radix sort: too many words");
@@ -203,13 +225,15 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
         io.in[k] = words[k];
         io.out[k] = alt + static_cast<size_t>(k) * n;
     }
-    {
+    std::vector<uint32_t> h_hist(hist_words);
+    if (hist_host) {
+        std::copy(hist_host, hist_host + hist_words, h_hist.begin());
+    } else {
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 4));
         ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hist_words * sizeof(uint32_t), io, npass, d_passes, n, hist);
+        ZI_CUDA(cudaMemcpyAsync(h_hist.data(), hist, hist_words * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     }
-    std::vector<uint32_t> h_hist(hist_words);
-    ZI_CUDA(cudaMemcpyAsync(h_hist.data(), hist, hist_words * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     std::vector<int> active;
     std::vector<uint32_t> h_bases(hist_words, 0);
     for (int q = 0; q < npass; ++q) {
@@ -259,20 +283,21 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
 }
 
 // ---------------------------------------------------------------------------- hybrid sort
-// MSD split + local sort.  msd_bytes() onesweep passes order the records by the top Morton bytes
+// MSD split + local sort.  A few onesweep passes order the records by the top Morton bytes
 // (and, for the 8-layout build, the layout bits of the payload) -- segments of equal top bits
 // are then contiguous.  k_segsort finishes each segment in shared memory with the full
 // comparator (Morton key, payload).  The payload is unique, so this order is the unique stable
 // order whatever order the segment arrives in; the result is bit-identical to the all-LSD sort
 // at roughly a third of its HBM passes.
-static int msd_bytes() {
+static int msd_bytes_forced() {  // ZI_SORT_MSD overrides the histogram-driven MSD depth
     static const int v = [] {
         const char* e = std::getenv("ZI_SORT_MSD");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 0;
     }();
     return v;
 }
 constexpr int kSegThreads = 256;
+constexpr uint32_t kMaxBig = 64;  // oversized segments finished one by one; more -> full LSD
 
 template <int NW>
 struct seg_ctx {
@@ -289,18 +314,19 @@ __device__ inline uint64_t seg_key(const seg_ctx<NW>& c, uint64_t i) {
     return k;
 }
 
-// first segment head at or after `from` (N if none); one warp
+// first segment head in [from, limit) (limit if none); one warp
 template <int NW>
-__device__ inline uint64_t find_head(const seg_ctx<NW>& c, uint64_t from) {
+__device__ inline uint64_t find_head(const seg_ctx<NW>& c, uint64_t from, uint64_t limit) {
     const int lane = threadIdx.x & 31;
     if (from == 0) return 0;
-    for (uint64_t b = from; b < c.N; b += 32) {
+    if (limit > c.N) limit = c.N;
+    for (uint64_t b = from; b < limit; b += 32) {
         const uint64_t i = b + lane;
-        const bool h = i < c.N && seg_key(c, i) != seg_key(c, i - 1);
+        const bool h = i < limit && seg_key(c, i) != seg_key(c, i - 1);
         const unsigned m = __ballot_sync(0xffffffffu, h);
         if (m) return b + __ffs(m) - 1;
     }
-    return c.N;
+    return limit;
 }
 
 // One CTA sorts one window: the records of the segments that start in [w*T, (w+1)*T) (so the
@@ -325,22 +351,36 @@ __global__ void __launch_bounds__(kSegThreads) k_segsort(seg_ctx<NW> c, int T, i
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * T;
     const uint64_t w1 = w0 + T < c.N ? w0 + T : c.N;
+    // the segments starting in [w0, w1): start = first head, end = first head at or after w1;
+    // searches stop once the range cannot fit (no quadratic scans inside long segments)
     if (warp == 0) {
-        const uint64_t st = find_head(c, w0);
-        if (lane == 0) s_range[0] = st;
-    } else if (warp == 1) {
-        const uint64_t en = w1 >= c.N ? c.N : find_head(c, w1);
-        if (lane == 0) s_range[1] = en;
+        const uint64_t st = find_head(c, w0, w1);
+        uint64_t en = st;
+        if (st < w1) en = w1 >= c.N ? c.N : find_head(c, w1, st + cap + 1);
+        if (lane == 0) {
+            s_range[0] = st;
+            s_range[1] = en;
+        }
     }
     if (tid < npass) s_pass[tid] = passes[tid];
     __syncthreads();
-    const uint64_t start = s_range[0], end = s_range[1];
+    const uint64_t start = s_range[0];
+    uint64_t end = s_range[1];
     if (start >= w1) return;  // no segment starts in this window
     if (end - start > static_cast<uint64_t>(cap)) {  // longer than shared memory: global fallback
+        if (warp == 0) {
+            const uint64_t e2 = end >= c.N ? c.N : find_head(c, end, c.N);  // its real end (once per segment)
+            if (lane == 0) s_range[1] = e2;
+        }
+        __syncthreads();
+        end = s_range[1];
         if (tid == 0) {
             const uint32_t slot = atomicAdd(nbig, 1u);
-            big[2 * slot] = start;
-            big[2 * slot + 1] = end;
+            if (slot < kMaxBig) {
+                big[2 * slot] = start;
+                big[2 * slot + 1] = end;
+            }
+            atomicAdd(nbig + 1, static_cast<uint32_t>(end - start < 0xffffffffull ? end - start : 0xffffffffull));
         }
         return;
     }
@@ -473,20 +513,54 @@ static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int 
 // bits are a layout id that orders first.
 static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts) {
     const int nw = W + 1;
-    const int nb = std::min(msd_bytes(), D);
-    std::vector<int2> msd, all;
-    for (int p = D - nb; p < D; ++p) msd.push_back(make_int2(p >> 2, (p & 3) * 8));
+    std::vector<int2> all;
     for (int p = 0; p < D; ++p) all.push_back(make_int2(p >> 2, (p & 3) * 8));
+    if (layouts) all.push_back(make_int2(W, 29));
+    const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all);
+    // MSD depth: the fewest top bytes whose (marginal) entropies predict segments of <= 64
+    // records per layout; a clustered top (smooth images) pushes it up, and when the split
+    // would leave little for the windows the plain LSD sort is used.
+    auto entropy = [&](int q) {
+        double e = 0.0;
+        for (int b = 0; b < 256; ++b) {
+            const double pr = static_cast<double>(hist[static_cast<size_t>(q) * 256 + b]) / static_cast<double>(N);
+            if (pr > 0) e -= pr * std::log2(pr);
+        }
+        return e;
+    };
+    const double per_layout = static_cast<double>(N) / (layouts ? 8.0 : 1.0);
+    int nb = msd_bytes_forced();
+    if (nb <= 0) {
+        double bits = 0.0;
+        nb = 0;
+        while (nb < D && std::exp2(bits) * 64.0 < per_layout) {
+            bits += entropy(D - 1 - nb);
+            ++nb;
+        }
+        nb = std::max(nb, 2);
+    }
+    nb = std::min(nb, D);
+    static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
+    if (nb > D - 3) {  // little left for the windows: all-LSD with the histograms already taken
+        if (debug) std::fprintf(stderr, "hybrid sort N=%llu: MSD depth %d of %d -> LSD\n", static_cast<unsigned long long>(N), nb, D);
+        radix_sort_words(ctx, words, nw, N, all, hist.data());
+        return;
+    }
+    std::vector<int2> msd;
+    std::vector<uint32_t> msd_hist;
+    for (int p = D - nb; p < D; ++p) {
+        msd.push_back(make_int2(p >> 2, (p & 3) * 8));
+        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(p) * 256, hist.begin() + static_cast<size_t>(p + 1) * 256);
+    }
     if (layouts) {
         msd.push_back(make_int2(W, 29));
-        all.push_back(make_int2(W, 29));
+        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(D) * 256, hist.end());
     }
-    radix_sort_words(ctx, words, nw, N, msd);
+    radix_sort_words(ctx, words, nw, N, msd, msd_hist.data());
     // counters | big-segment list | pass table, in the context counter buffer
-    const size_t max_big = 4096;
-    uint32_t* cnt = ctx->counter.ensure(16 + 4 * max_big + 2 * 64);
+    uint32_t* cnt = ctx->counter.ensure(16 + 4 * kMaxBig + 2 * 64);
     unsigned long long* big = reinterpret_cast<unsigned long long*>(cnt + 16);
-    int2* d_passes = reinterpret_cast<int2*>(cnt + 16 + 4 * max_big);
+    int2* d_passes = reinterpret_cast<int2*>(cnt + 16 + 4 * kMaxBig);
     ZI_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), ctx->stream));
     switch (nw) {
         case 2: launch_segsort<2>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
@@ -503,12 +577,17 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     ZI_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     const uint32_t nbig = hc[0];
-    static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
     if (debug)
-        std::fprintf(stderr, "hybrid sort N=%llu nb=%d: oversized segments %u\n", static_cast<unsigned long long>(N),
-                     nb, nbig);
+        std::fprintf(stderr, "hybrid sort N=%llu nb=%d: oversized segments %u (%u records)\n",
+                     static_cast<unsigned long long>(N), nb, nbig, hc[1]);
     if (nbig == 0) return;
-    if (nbig > max_big) throw error(ZI_E_RUNTIME, "hybrid sort: too many oversized segments");
+    if (nbig > kMaxBig || static_cast<uint64_t>(hc[1]) * 8 > N) {
+        // top bytes too clustered for the split (smooth images): finish with the full LSD sort.
+        // Equal keys are already in payload order everywhere, so the stable passes from the
+        // current order give the reference permutation.
+        radix_sort_words(ctx, words, nw, N, all, nullptr);
+        return;
+    }
     std::vector<unsigned long long> h(2 * nbig);
     ZI_CUDA(cudaMemcpyAsync(h.data(), big, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -519,7 +598,7 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     for (uint32_t q = 0; q < nbig; ++q) {
         uint32_t* sub[kMaxWords];
         for (int k = 0; k < nw; ++k) sub[k] = words[k] + h[2 * q];
-        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], rest);
+        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], rest, nullptr);
     }
 }
 
@@ -532,7 +611,7 @@ void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int
     if (payload_first)
         for (int b = 0; b < 4; ++b) passes.push_back(make_int2(W, 8 * b));
     for (int p = 0; p < D; ++p) passes.push_back(make_int2(p >> 2, (p & 3) * 8));
-    radix_sort_words(ctx, words, W + 1, n, passes);
+    radix_sort_words(ctx, words, W + 1, n, passes, nullptr);
 }
 
 void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D) {

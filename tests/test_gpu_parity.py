@@ -447,6 +447,33 @@ def test_cfg2_build_properties(zb):
             assert np.array_equal(idx.knn(qv, 80), oracle.knn_linear(c, k, qv, 80))
 
 
+@pytest.mark.slow
+def test_cfg4_build_properties(zb):
+    """cfg4 (4096^2 gray, K=9, D=8, n ~ 15M): permutation, Morton order with key tie-break,
+    lo/hi bound the projections, sampled quantised bytes equal the oracle's, spot knn."""
+    img, kn, p = workloads.cfg4()
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8))
+    d = mi.dictionary
+    assert np.array_equal(d, oracle.collect_dictionary(kn, 9))
+    rng = np.random.default_rng(4)
+    for l in (0, 3, 7):
+        c, k = mi.index_arrays(l)
+        assert np.array_equal(np.sort(k), d)
+        assert is_morton_sorted(c, k)
+        lay = mi.layout(l)
+        sub = rng.choice(len(d), 2000, replace=False)
+        lo, hi, coords, y = oracle.project_build(img, d[sub], lay["pixels"], lay["mean"], lay["components"])
+        assert (y.min(0) >= lay["lo"]).all() and (y.max(0) <= lay["hi"]).all()
+        pos = np.searchsorted(d, d[sub])
+        order = np.argsort(k)
+        q = np.array([[oracle.quantize(lay["lo"][j], lay["hi"][j], y[i, j]) for j in range(mi.dims)] for i in range(200)])
+        assert np.array_equal(c[order[pos[:200]]], q)
+        idx = mi.index(l)
+        for t in range(2):
+            qv = c[rng.integers(0, len(k))]
+            assert np.array_equal(idx.knn(qv, 80), oracle.knn_linear(c, k, qv, 80))
+
+
 @pytest.mark.parametrize("D", [4, 8, 16])
 def test_knn_batch_cfg5_like_vs_oracle(zb, D):
     coords, queries = workloads.cfg5_descriptors(60000, D, 64, seed=D)
