@@ -529,7 +529,9 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         return e;
     };
     const double per_layout = static_cast<double>(N) / (layouts ? 8.0 : 1.0);
+    int& learnt = ctx->sort_depth[D][layouts ? 1 : 0];
     int nb = msd_bytes_forced();
+    if (nb <= 0 && learnt != 0) nb = learnt < 0 ? D : learnt;
     if (nb <= 0) {
         double bits = 0.0;
         nb = 0;
@@ -584,7 +586,9 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     if (nbig > kMaxBig || static_cast<uint64_t>(hc[1]) * 8 > N) {
         // top bytes too clustered for the split (smooth images): finish with the full LSD sort.
         // Equal keys are already in payload order everywhere, so the stable passes from the
-        // current order give the reference permutation.
+        // current order give the reference permutation.  Later builds with these dims go one
+        // byte deeper, or straight to LSD.
+        learnt = nb + 1 > D - 3 ? -1 : nb + 1;
         radix_sort_words(ctx, words, nw, N, all, nullptr);
         return;
     }
