@@ -159,6 +159,32 @@ __device__ inline void cluster_barrier() {
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+__device__ inline unsigned smem_addr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+// address of the same shared-memory location in CTA `rank` of the cluster
+__device__ inline unsigned peer_addr(unsigned local, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+// 8-byte store into a peer CTA that completes 8 transaction bytes on the peer's mbarrier
+__device__ inline void st_async_f64(unsigned raddr, double v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ inline void mbar_init(unsigned bar) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory"); }
+__device__ inline void mbar_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ inline void mbar_wait_cluster(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n WAITC_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAITC_%=;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
 // CTA-wide sum (fixed order -> deterministic), result in every thread
 template <int T>
 __device__ inline double cta_sum(double v, double* s_red) {
@@ -262,14 +288,30 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
     }
     // Column c's sub-diagonal entries A(i, c), i > c, live in the rows' owners (full rows): each
     // warp pushes the entries of its rows and its partial |.|^2 to every CTA, so the next
-    // reflector is assembled everywhere without a single-owner broadcast and without CTA barriers.
+    // reflector is assembled everywhere without a single-owner broadcast.  The exchanges are
+    // st.async stores that complete transaction bytes on the receiver's mbarrier (one per buffer
+    // parity for v and for p): a CTA proceeds as soon as its own bytes have landed, with no
+    // cluster-wide rendezvous per column.
     constexpr int kParts = kCl * kWarps;
+    __shared__ __align__(8) unsigned long long s_bar[4];  // v[0], v[1], p[0], p[1]
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(smem_addr(&s_bar[i]));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const unsigned v_local = smem_addr(v), p_local = smem_addr(p), np_local = smem_addr(npart);
+    const unsigned bar_local = smem_addr(&s_bar[0]);
     auto push_entry = [&](int c, int bb, int i, double y) {  // warp-uniform call
-        if (lane < kCl) cl.map_shared_rank(v, lane)[bb * n + (i - c - 1)] = y;
+        if (lane < kCl)
+            st_async_f64(peer_addr(v_local + 8u * (bb * n + (i - c - 1)), lane), y, peer_addr(bar_local + 8u * bb, lane));
     };
     auto push_partial = [&](int bb, double part) {
-        if (lane < kCl) cl.map_shared_rank(npart, lane)[bb * kParts + rank * kWarps + warp] = part;
+        if (lane < kCl)
+            st_async_f64(peer_addr(np_local + 8u * (bb * kParts + rank * kWarps + warp), lane), part,
+                         peer_addr(bar_local + 8u * bb, lane));
     };
+    unsigned ph_v[2] = {0u, 0u}, ph_p[2] = {0u, 0u};
+    __syncthreads();
+    cluster_barrier();  // every mbarrier of the cluster is initialised before the first push
     {
         double part = 0.0;
         const int first = 1 > rank ? 1 : 0;
@@ -280,10 +322,14 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
         }
         push_partial(0, part);
     }
-    cluster_barrier();
     for (int k = 0; k + 2 < n; ++k) {
         const int m = n - k - 1, b = k & 1;
         const double* vb = v + b * n;
+        __syncthreads();  // this CTA's row updates of the previous column are visible to all warps
+        // column k: m entries + the partials, from every CTA
+        if (tid == 0) mbar_expect(bar_local + 8u * b, 8u * static_cast<unsigned>(m + kParts));
+        mbar_wait_cluster(bar_local + 8u * b, ph_v[b]);
+        ph_v[b] ^= 1u;
         // |column k|^2 from the per-warp partials, summed in the same order by every warp
         double np = 0.0;
 #pragma unroll
@@ -328,10 +374,13 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
                     if (j < m) acc = fma(row[j], vr[q], acc);
                 }
                 const double pt = tk * warp_allsum(acc);
-                if (lane < kCl) cl.map_shared_rank(p, lane)[b * n + t] = pt;
+                if (lane < kCl)
+                    st_async_f64(peer_addr(p_local + 8u * (b * n + t), lane), pt, peer_addr(bar_local + 8u * (2 + b), lane));
             }
             TRI_T(1);
-            cluster_barrier();
+            if (tid == 0) mbar_expect(bar_local + 8u * (2 + b), 8u * static_cast<unsigned>(m));
+            mbar_wait_cluster(bar_local + 8u * (2 + b), ph_p[b]);
+            ph_p[b] ^= 1u;
             TRI_T(2);
             const double* pb = p + b * n;
             double wr[kSlots];
@@ -371,6 +420,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
                     part = fma(y0, y0, part);
                 }
             }
+            if (next) push_partial(b ^ 1, part);
             TRI_T(3);
         } else if (next) {
             for (int li = li0 + warp; li < nloc; li += kWarps) {
@@ -380,12 +430,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
                 push_entry(k + 1, b ^ 1, i, y);
                 part = fma(y, y, part);
             }
+            push_partial(b ^ 1, part);
         }
-        if (next) push_partial(b ^ 1, part);
         TRI_T(4);
-        cluster_barrier();
         TRI_T(5);
     }
+    __syncthreads();  // own rows final before the d / e read-out
     if (a.dbg && tid == 0)
         for (int i = 0; i < 6; ++i) a.dbg[blockIdx.x * 8 + i] = tacc[i];
 #undef TRI_T
