@@ -74,6 +74,35 @@ __device__ inline double fast_rcp(double x) {
     return fma(r, e, r);
 }
 
+// 1/x to ~2^-40 relative (one Newton step): ample for a Sturm count's sign decisions
+__device__ inline double rcp_1nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+// Sturm counts at 4 points at once (4 independent dependency chains per thread)
+__device__ inline void sturm_count4(const double* d, const double* e2, int n, const double (&x)[4], double pivmin,
+                                    int (&cnt)[4]) {
+    double q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        q[u] = d[0] - x[u];
+        if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+        cnt[u] = q[u] < 0;
+    }
+    for (int i = 1; i < n; ++i) {
+        const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            q[u] = (di - x[u]) - ei * rcp_1nr(q[u]);
+            if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+            cnt[u] += q[u] < 0;
+        }
+    }
+}
+
 // number of eigenvalues of T below x (Sturm sequence in ratio form, pivmin guard as dstebz)
 __device__ int sturm_count_dev(const double* d, const double* e2, int n, double x, double pivmin) {
     int cnt = 0;
@@ -453,6 +482,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
 struct vec_args {
     int mc, D;
     pca_work_view w;
+    long long* dbg;  // optional phase clocks (ZI_DEBUG_PCA): per CTA 4 values
 };
 
 __device__ inline unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -464,6 +494,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
     __shared__ double s_scal[4];
     const int n = a.mc, D = a.D, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int l = blockIdx.x / D, j = blockIdx.x % D;
+    const long long t_start = clock64();
     const size_t nref = a.w.rstride;
     double* R = sm;         // reflectors (TMA)
     double* dd = R + nref;  // n
@@ -512,27 +543,41 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
     }
     __syncthreads();
     const double safe = s_scal[0], pivmin = s_scal[1];
-    // lambda_j (j-th largest) by multisection: 128 points per round
+    // lambda_j (j-th largest) by multisection: 4 points per lane, 512 per round
+    constexpr int kPts = 4 * kVecThreads;
     const int target = n - 1 - j;
     double lo = s_scal[2], hi = s_scal[3];
+    // stop at ~1e-10 relative: the Rayleigh quotient of the inverse-iteration vector below gives
+    // the eigenvalue to working precision
     for (int it = 0; it < 64; ++it) {
-        if (hi - lo <= 2 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) break;
-        const double xq = lo + (hi - lo) * (tid + 1) / static_cast<double>(kVecThreads + 1);
-        const bool above = sturm_count_dev(dd, e2, n, xq, pivmin) > target;
-        const unsigned bal = __ballot_sync(0xffffffffu, above);
-        if (lane == 0) s_first[warp] = bal ? warp * 32 + __ffs(bal) - 1 : kVecThreads;
+        if (hi - lo <= 1e-10 * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+        double xq[4];
+        int cq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xq[u] = lo + (hi - lo) * (4 * tid + u + 1) / static_cast<double>(kPts + 1);
+        sturm_count4(dd, e2, n, xq, pivmin, cq);
+        // first point past lambda_j: counts are monotone in the point index
+        int first = kPts;
+#pragma unroll
+        for (int u = 3; u >= 0; --u)
+            if (cq[u] > target) first = 4 * tid + u;
+        first = min(first, kPts);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+        if (lane == 0) s_first[warp] = first;
         __syncthreads();
-        int c = kVecThreads;
+        int c = kPts;
 #pragma unroll
         for (int w = 0; w < kVecThreads / 32; ++w) c = min(c, s_first[w]);
         __syncthreads();
-        const double nlo = c > 0 ? lo + (hi - lo) * c / static_cast<double>(kVecThreads + 1) : lo;
-        const double nhi = c < kVecThreads ? lo + (hi - lo) * (c + 1) / static_cast<double>(kVecThreads + 1) : hi;
+        const double nlo = c > 0 ? lo + (hi - lo) * c / static_cast<double>(kPts + 1) : lo;
+        const double nhi = c < kPts ? lo + (hi - lo) * (c + 1) / static_cast<double>(kPts + 1) : hi;
         if (!(nlo < nhi) || (nlo == lo && nhi == hi)) break;
         lo = nlo;
         hi = nhi;
     }
     const double lam = 0.5 * (lo + hi);
+    const long long t_bis = clock64();
     // inverse iteration: LU of (T - lambda I) once, three solves from a pseudo-random start
     if (tid == 0) {
         const double tiny = DBL_EPSILON * safe;
@@ -545,7 +590,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
             z ^= z >> 31;
             x[i] = static_cast<double>(z >> 11) * 0x1.0p-53 - 0.5;
         }
-        for (int it = 0; it < 3; ++it) {
+        for (int it = 0; it < 2; ++it) {  // the shift is exact to working precision: two solves
             const double mx = tri_apply(f, f + n, f + 2 * n, f + 3 * n, piv, n, x);
             const double sc = mx > 0.0 ? fast_rcp(mx) : 1.0;
             for (int i = 0; i < n; ++i) x[i] *= sc;
@@ -554,9 +599,13 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
         for (int i = 0; i < n; ++i) nrm = fma(x[i], x[i], nrm);
         const double inv = 1.0 / sqrt(nrm);
         for (int i = 0; i < n; ++i) x[i] *= inv;
-        a.w.lam[l * 32 + j] = lam;
+        // Rayleigh quotient x^T T x (|x| = 1): eigenvalue error ~ residual^2 / gap
+        double rq = dd[0] * x[0] * x[0];
+        for (int i = 1; i < n; ++i) rq = fma(dd[i] * x[i], x[i], fma(2.0 * ee[i - 1] * x[i - 1], x[i], rq));
+        a.w.lam[l * 32 + j] = rq;
     }
     __syncthreads();
+    const long long t_inv = clock64();
     // back-transformation x = H_0 ... H_{n-3} x, one warp, the vector in registers
     if (warp == 0) {
         const unsigned bar = smem_u32(&s_bar);
@@ -584,6 +633,11 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
                 const int i = lane + 32 * q;
                 if (i > k && i < n) xr[q] = fma(-fct, r[i], xr[q]);
             }
+        }
+        if (a.dbg && lane == 0) {
+            a.dbg[blockIdx.x * 4 + 0] = t_bis - t_start;
+            a.dbg[blockIdx.x * 4 + 1] = t_inv - t_bis;
+            a.dbg[blockIdx.x * 4 + 2] = clock64() - t_inv;
         }
         double* out = a.w.X + (static_cast<size_t>(l) * D + j) * n;
 #pragma unroll
@@ -695,8 +749,18 @@ bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint
             std::fprintf(stderr, "tri cta %2d: start %lld B %lld bar1 %lld C %lld push %lld bar2 %lld\n", c, h[c * 8],
                          h[c * 8 + 1], h[c * 8 + 2], h[c * 8 + 3], h[c * 8 + 4], h[c * 8 + 5]);
     }
-    vec_args va{mc, D, w};
+    vec_args va{mc, D, w, nullptr};
+    static dbuf<long long> vdbg;
+    if (debug) va.dbg = vdbg.ensure(8 * 32 * 4);
     ZI_LAUNCH(ctx, "pca_vectors", k_pca_vec, 8 * D, kVecThreads, smem_vec, va);
+    if (debug) {
+        std::vector<long long> h(static_cast<size_t>(8) * D * 4);
+        ZI_CUDA(cudaMemcpyAsync(h.data(), va.dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int c = 0; c < 3; ++c)
+            std::fprintf(stderr, "vec cta %d: bisect %lld inverse %lld backtransform %lld\n", c, h[c * 4], h[c * 4 + 1],
+                         h[c * 4 + 2]);
+    }
     fin_args fa{mc, D, w, d_comp, d_eig};
     ZI_LAUNCH(ctx, "pca_finish", k_pca_fin, 8, 256, smem_fin, fa);
     return true;
