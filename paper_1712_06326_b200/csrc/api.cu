@@ -469,7 +469,10 @@ zi_status zi_multi_index_rebuild(zi_multi_index* mi) {
 
 zi_status zi_multi_index_destroy(zi_multi_index* mi) {
     return guard(mi ? mi->ctx : nullptr, [&] {
-        if (mi) cudaStreamSynchronize(mi->ctx->stream);
+        if (!mi) return;
+        cudaStreamSynchronize(mi->ctx->stream);
+        if (mi->ev0) cudaEventDestroy(mi->ev0);
+        if (mi->ev1) cudaEventDestroy(mi->ev1);
         delete mi;
     });
 }
@@ -483,6 +486,7 @@ zi_status zi_multi_index_get_info(const zi_multi_index* mi, zi_multi_index_info*
         info->patch_size = mi->K;
         info->width = mi->w;
         info->height = mi->h;
+        zi::finish_build_timing(const_cast<zi_multi_index*>(mi));
         info->build_seconds = mi->build_ms * 1e-3;
         info->eigen_seconds = mi->eigen_s;
         info->pca_on_device = mi->device_pca ? 1 : 0;

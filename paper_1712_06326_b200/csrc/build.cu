@@ -37,7 +37,32 @@ static void sync_moments(zi_multi_index* mi) {
         }
 }
 
+void finish_build_timing(zi_multi_index* mi) {
+    if (!mi->build_ms_pending) return;
+    ZI_CUDA(cudaEventSynchronize(mi->ev1));
+    float ms = 0.f;
+    ZI_CUDA(cudaEventElapsedTime(&ms, mi->ev0, mi->ev1));
+    mi->build_ms = ms;
+    mi->build_ms_pending = false;
+}
+
 void sync_host_model(zi_multi_index* mi) {
+    if (!mi->host_lohi && mi->n > 0) {
+        const int D = mi->dims;
+        std::vector<unsigned long long> hmm(static_cast<size_t>(8) * 2 * D);
+        ZI_CUDA(cudaMemcpyAsync(hmm.data(), mi->minmax.p, hmm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                mi->ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(mi->ctx->stream));
+        for (int l = 0; l < 8; ++l) {
+            mi->L[l].lo.resize(D);
+            mi->L[l].hi.resize(D);
+            for (int d = 0; d < D; ++d) {
+                mi->L[l].lo[d] = ordered_to_double(hmm[static_cast<size_t>(l) * 2 * D + d]);
+                mi->L[l].hi[d] = ordered_to_double(hmm[static_cast<size_t>(l) * 2 * D + D + d]);
+            }
+        }
+        mi->host_lohi = true;
+    }
     if (mi->host_model || mi->n == 0) return;
     zi_ctx* ctx = mi->ctx;
     const int mc = mi->mc, D = mi->dims;
@@ -66,19 +91,16 @@ void sync_host_model(zi_multi_index* mi) {
 void build_multi_index(zi_multi_index* mi) {
     zi_ctx* ctx = mi->ctx;
     const auto wall0 = std::chrono::steady_clock::now();
-    cudaEvent_t e0, e1;
-    ZI_CUDA(cudaEventCreate(&e0));
-    ZI_CUDA(cudaEventCreate(&e1));
-    ZI_CUDA(cudaEventRecord(e0, ctx->stream));
+    if (!mi->ev0) {
+        ZI_CUDA(cudaEventCreate(&mi->ev0));
+        ZI_CUDA(cudaEventCreate(&mi->ev1));
+    }
+    ZI_CUDA(cudaEventRecord(mi->ev0, ctx->stream));
     const int K = mi->K, C = mi->C, w = mi->w, h = mi->h;
 
     // K1
     mi->n = collect_dictionary(ctx, mi->known.p, w, h, K, mi->dict);
-    if (mi->n == 0) {
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        throw error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
-    }
+    if (mi->n == 0) throw error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
     const uint64_t n = mi->n;
     mi->dims = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(mi->cfg.dims),
                                                    std::min<uint64_t>(static_cast<uint64_t>(mi->mc), n)));
@@ -172,25 +194,10 @@ void build_multi_index(zi_multi_index* mi) {
         mi->L[l].index.layout_id = static_cast<uint32_t>(l);
         finalize_index(ctx, keyw, val, N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p, &mi->L[l].index);
     }
-    std::vector<unsigned long long> hmm(static_cast<size_t>(8) * 2 * D);
-    ZI_CUDA(cudaMemcpyAsync(hmm.data(), mi->minmax.p, hmm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    ZI_CUDA(cudaEventRecord(e1, ctx->stream));
-    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (int l = 0; l < 8; ++l) {
-        mi->L[l].lo.resize(D);
-        mi->L[l].hi.resize(D);
-        for (int d = 0; d < D; ++d) {
-            mi->L[l].lo[d] = ordered_to_double(hmm[static_cast<size_t>(l) * 2 * D + d]);
-            mi->L[l].hi[d] = ordered_to_double(hmm[static_cast<size_t>(l) * 2 * D + D + d]);
-        }
-    }
-    float ms = 0.f;
-    ZI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    mi->build_ms = ms;
+    ZI_CUDA(cudaEventRecord(mi->ev1, ctx->stream));
+    mi->build_ms_pending = true;
+    mi->host_lohi = false;
     mi->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
 }
 
 }  // namespace zi

@@ -164,6 +164,9 @@ struct zi_multi_index {
     zi::dbuf<int> pca_status;
     bool pca_cols_ready = false;
     bool host_model = false;             // s, S, L[].mean/comp/eig mirror the device copies
+    bool host_lohi = false;              // L[].lo/hi mirror the device min/max
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // build timing, read lazily (no sync at build end)
+    bool build_ms_pending = false;
     bool device_pca = false;             // last build solved the eigenproblems on the device
     zi_layout_state L[8];
 };
@@ -239,8 +242,10 @@ void pca_fit_layout(const std::vector<int64_t>& s, const std::vector<int64_t>& S
                     const std::vector<int32_t>& cols, int dims, std::vector<double>& mean,
                     std::vector<double>& comp /* dims*mc, row d */, std::vector<double>& eig);
 void build_multi_index(zi_multi_index* mi);
-// copy the moments and the 8 PCA models to the host mirror (lazy: only the accessors need it)
+// copy the moments, the 8 PCA models and the quantiser ranges to the host mirror (lazy: only
+// the accessors need them); finish_build_timing reads the build's event pair
 void sync_host_model(zi_multi_index* mi);
+void finish_build_timing(zi_multi_index* mi);
 // k_pca.cu: covariance + eigen-solve of all 8 layouts on the device; false if mc is too large.
 // d_work must hold pca_work_doubles(mc, D) doubles.
 size_t pca_work_doubles(int mc, int D);
