@@ -1550,7 +1550,7 @@ __global__ void __launch_bounds__(32 * kBatchWarps) k_knn_batch(index_view v, co
 
 // ===================================================================== host side
 void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
-                      const uint32_t* hist_host);
+                      const uint32_t* hist_host, bool device_bases);
 
 static index_view view_of(const zi_index* idx) {
     index_view v;
@@ -1645,7 +1645,7 @@ static bool run_knn(zi_ctx* ctx, const views8& V, uint64_t n, uint64_t nblk, con
     std::vector<int2> passes;
     for (int b = 0; b < 4; ++b) passes.push_back(make_int2(0, 8 * b));
     for (int b = 0; b < 4; ++b) passes.push_back(make_int2(1, 8 * b));
-    radix_sort_words(ctx, words, 2, n, passes, nullptr);
+    radix_sort_words(ctx, words, 2, n, passes, nullptr, false);
     const uint32_t cnt = static_cast<uint32_t>(std::min<uint64_t>(k, n));
     ZI_LAUNCH(ctx, "knn_gather_topk", k_gather_topk, (cnt + 255) / 256, 256, 0, lo, hi, cnt, s.ws, s.out);
     return false;

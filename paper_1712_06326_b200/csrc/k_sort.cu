@@ -49,6 +49,25 @@ __global__ void __launch_bounds__(256) k_sort_hist(sort_words io, int npass, con
         if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
 }
 
+// exclusive scans of the digit histograms (one block per pass): the onesweep bases, on the
+// device, when the host does not need to see the histograms
+__global__ void __launch_bounds__(256) k_sort_bases(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases) {
+    __shared__ uint32_t s_w[8];
+    const int q = blockIdx.x, d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    const uint32_t c = hist[q * 256 + d];
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t wp = 0;
+    for (int w = 0; w < warp; ++w) wp += s_w[w];
+    bases[q * 256 + d] = wp + x - c;
+}
+
 template <int NW>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(sort_words io, int dw, int ds,
                                                            const uint32_t* __restrict__ digit_base,
@@ -198,7 +217,7 @@ std::vector<uint32_t> pass_histograms(zi_ctx* ctx, uint32_t* const* words, int n
 }
 
 void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
-                      const uint32_t* hist_host) {
+                      const uint32_t* hist_host, bool device_bases) {
     if (n <= 1 || passes.empty()) return;
     if (n > kValMask) throw error(ZI_E_INVALID, "radix sort: more than 2^30 records");
     if (nw > kMaxWords) throw error(ZI_E_INVALID, "radix sort: too many words");
@@ -226,7 +245,14 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
         io.out[k] = alt + static_cast<size_t>(k) * n;
     }
     std::vector<uint32_t> h_hist(hist_words);
-    if (hist_host) {
+    std::vector<int> active;
+    std::vector<uint32_t> h_bases(hist_words, 0);
+    if (device_bases) {  // no host round trip: every pass runs (trivial ones are a copy)
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 4));
+        ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hist_words * sizeof(uint32_t), io, npass, d_passes, n, hist);
+        ZI_LAUNCH(ctx, "radix_bases", k_sort_bases, npass, 256, 0, hist, bases);
+        for (int q = 0; q < npass; ++q) active.push_back(q);
+    } else if (hist_host) {
         std::copy(hist_host, hist_host + hist_words, h_hist.begin());
     } else {
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 4));
@@ -234,9 +260,7 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
         ZI_CUDA(cudaMemcpyAsync(h_hist.data(), hist, hist_words * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     }
-    std::vector<int> active;
-    std::vector<uint32_t> h_bases(hist_words, 0);
-    for (int q = 0; q < npass; ++q) {
+    for (int q = 0; q < npass && !device_bases; ++q) {
         bool trivial = false;
         uint32_t run = 0;
         for (int dgt = 0; dgt < 256; ++dgt) {
@@ -248,7 +272,8 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
         if (!trivial) active.push_back(q);
     }
     if (active.empty()) return;
-    ZI_CUDA(cudaMemcpyAsync(bases, h_bases.data(), hist_words * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (!device_bases)
+        ZI_CUDA(cudaMemcpyAsync(bases, h_bases.data(), hist_words * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
     ZI_CUDA(cudaMemsetAsync(status, 0, status_words * sizeof(uint32_t), ctx->stream));
     ZI_CUDA(cudaMemsetAsync(ctr, 0, npass * sizeof(uint32_t), ctx->stream));
     uint32_t* cur[kMaxWords];
@@ -509,56 +534,11 @@ static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int 
               d_passes, big, nbig);
 }
 
-// Sort (key words, payload) records by (Morton key, payload); `layouts`: the payload's top 3
-// bits are a layout id that orders first.
-static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts) {
+// window sort + oversized-segment handling after the MSD passes
+static void finish_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, int nb, bool layouts,
+                          const std::vector<int2>& all, int& learnt) {
     const int nw = W + 1;
-    std::vector<int2> all;
-    for (int p = 0; p < D; ++p) all.push_back(make_int2(p >> 2, (p & 3) * 8));
-    if (layouts) all.push_back(make_int2(W, 29));
-    const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all);
-    // MSD depth: the fewest top bytes whose (marginal) entropies predict segments of <= 64
-    // records per layout; a clustered top (smooth images) pushes it up, and when the split
-    // would leave little for the windows the plain LSD sort is used.
-    auto entropy = [&](int q) {
-        double e = 0.0;
-        for (int b = 0; b < 256; ++b) {
-            const double pr = static_cast<double>(hist[static_cast<size_t>(q) * 256 + b]) / static_cast<double>(N);
-            if (pr > 0) e -= pr * std::log2(pr);
-        }
-        return e;
-    };
-    const double per_layout = static_cast<double>(N) / (layouts ? 8.0 : 1.0);
-    int& learnt = ctx->sort_depth[D][layouts ? 1 : 0];
-    int nb = msd_bytes_forced();
-    if (nb <= 0 && learnt != 0) nb = learnt < 0 ? D : learnt;
-    if (nb <= 0) {
-        double bits = 0.0;
-        nb = 0;
-        while (nb < D && std::exp2(bits) * 64.0 < per_layout) {
-            bits += entropy(D - 1 - nb);
-            ++nb;
-        }
-        nb = std::max(nb, 2);
-    }
-    nb = std::min(nb, D);
     static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
-    if (nb > D - 3) {  // little left for the windows: all-LSD with the histograms already taken
-        if (debug) std::fprintf(stderr, "hybrid sort N=%llu: MSD depth %d of %d -> LSD\n", static_cast<unsigned long long>(N), nb, D);
-        radix_sort_words(ctx, words, nw, N, all, hist.data());
-        return;
-    }
-    std::vector<int2> msd;
-    std::vector<uint32_t> msd_hist;
-    for (int p = D - nb; p < D; ++p) {
-        msd.push_back(make_int2(p >> 2, (p & 3) * 8));
-        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(p) * 256, hist.begin() + static_cast<size_t>(p + 1) * 256);
-    }
-    if (layouts) {
-        msd.push_back(make_int2(W, 29));
-        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(D) * 256, hist.end());
-    }
-    radix_sort_words(ctx, words, nw, N, msd, msd_hist.data());
     // counters | big-segment list | pass table, in the context counter buffer
     uint32_t* cnt = ctx->counter.ensure(16 + 4 * kMaxBig + 2 * 64);
     unsigned long long* big = reinterpret_cast<unsigned long long*>(cnt + 16);
@@ -589,7 +569,7 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         // current order give the reference permutation.  Later builds with these dims go one
         // byte deeper, or straight to LSD.
         learnt = nb + 1 > D - 3 ? -1 : nb + 1;
-        radix_sort_words(ctx, words, nw, N, all, nullptr);
+        radix_sort_words(ctx, words, nw, N, all, nullptr, false);
         return;
     }
     std::vector<unsigned long long> h(2 * nbig);
@@ -602,8 +582,73 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     for (uint32_t q = 0; q < nbig; ++q) {
         uint32_t* sub[kMaxWords];
         for (int k = 0; k < nw; ++k) sub[k] = words[k] + h[2 * q];
-        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], rest, nullptr);
+        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], rest, nullptr, false);
     }
+}
+
+// Sort (key words, payload) records by (Morton key, payload); `layouts`: the payload's top 3
+// bits are a layout id that orders first.
+static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts) {
+    const int nw = W + 1;
+    std::vector<int2> all;
+    for (int p = 0; p < D; ++p) all.push_back(make_int2(p >> 2, (p & 3) * 8));
+    if (layouts) all.push_back(make_int2(W, 29));
+    int& learnt = ctx->sort_depth[D][layouts ? 1 : 0];
+    if (learnt > 0 && msd_bytes_forced() <= 0 && learnt <= D - 3) {
+        // depth known from an earlier build: MSD passes with device-side digit bases, no
+        // histogram round trip to the host
+        const int nb = learnt;
+        std::vector<int2> msd;
+        for (int p = D - nb; p < D; ++p) msd.push_back(make_int2(p >> 2, (p & 3) * 8));
+        if (layouts) msd.push_back(make_int2(W, 29));
+        radix_sort_words(ctx, words, nw, N, msd, nullptr, true);
+        finish_hybrid(ctx, words, W, N, D, nb, layouts, all, learnt);
+        return;
+    }
+    const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all);
+    // MSD depth: the fewest top bytes whose (marginal) entropies predict segments of <= 64
+    // records per layout; a clustered top (smooth images) pushes it up, and when the split
+    // would leave little for the windows the plain LSD sort is used.
+    auto entropy = [&](int q) {
+        double e = 0.0;
+        for (int b = 0; b < 256; ++b) {
+            const double pr = static_cast<double>(hist[static_cast<size_t>(q) * 256 + b]) / static_cast<double>(N);
+            if (pr > 0) e -= pr * std::log2(pr);
+        }
+        return e;
+    };
+    const double per_layout = static_cast<double>(N) / (layouts ? 8.0 : 1.0);
+    int nb = msd_bytes_forced();
+    if (nb <= 0 && learnt != 0) nb = learnt < 0 ? D : learnt;
+    if (nb <= 0) {
+        double bits = 0.0;
+        nb = 0;
+        while (nb < D && std::exp2(bits) * 64.0 < per_layout) {
+            bits += entropy(D - 1 - nb);
+            ++nb;
+        }
+        nb = std::max(nb, 2);
+    }
+    nb = std::min(nb, D);
+    static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
+    if (nb > D - 3) {  // little left for the windows: all-LSD with the histograms already taken
+        if (debug) std::fprintf(stderr, "hybrid sort N=%llu: MSD depth %d of %d -> LSD\n", static_cast<unsigned long long>(N), nb, D);
+        radix_sort_words(ctx, words, nw, N, all, hist.data(), false);
+        return;
+    }
+    std::vector<int2> msd;
+    std::vector<uint32_t> msd_hist;
+    for (int p = D - nb; p < D; ++p) {
+        msd.push_back(make_int2(p >> 2, (p & 3) * 8));
+        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(p) * 256, hist.begin() + static_cast<size_t>(p + 1) * 256);
+    }
+    if (layouts) {
+        msd.push_back(make_int2(W, 29));
+        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(D) * 256, hist.end());
+    }
+    radix_sort_words(ctx, words, nw, N, msd, msd_hist.data(), false);
+    if (learnt == 0) learnt = nb;  // remembered: later builds skip the histogram round trip
+    finish_hybrid(ctx, words, W, N, D, nb, layouts, all, learnt);
 }
 
 void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first) {
@@ -615,7 +660,7 @@ void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int
     if (payload_first)
         for (int b = 0; b < 4; ++b) passes.push_back(make_int2(W, 8 * b));
     for (int p = 0; p < D; ++p) passes.push_back(make_int2(p >> 2, (p & 3) * 8));
-    radix_sort_words(ctx, words, W + 1, n, passes, nullptr);
+    radix_sort_words(ctx, words, W + 1, n, passes, nullptr, false);
 }
 
 void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D) {
