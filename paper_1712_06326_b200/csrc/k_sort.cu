@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) k_sort_bases(const uint32_t* __restrict__
 }
 
 template <int NW>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(sort_words io, int dw, int ds,
+__global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort_words io, int dw, int ds,
                                                            const uint32_t* __restrict__ digit_base,
                                                            uint32_t* __restrict__ status,
                                                            uint32_t* __restrict__ tile_ctr, uint64_t n) {
