@@ -367,6 +367,19 @@ def main():
     else:
         roofline = roofline_hbm
 
+    # whole-step floor (SURVEY.md §8(d) model): max(HBM bytes / BW, fp64 flops / FP64 tensor peak)
+    # with this pipeline's own algorithmic bytes (every counted kernel, per step) and the one
+    # projection pass it performs
+    step_bytes = sum(algorithmic_bytes(k, n, mi.dims, mc) * v[1] / args.steps for k, v in prof.items()
+                     if algorithmic_bytes(k, n, mi.dims, mc) is not None)
+    step_flops = 8 * algorithmic_flops("project", n, mi.dims, mc)
+    floor_ms = max(step_bytes / (hbm_peak * 1e9), step_flops / (FP64_TENSOR_PEAK_TFLOPS * 1e12)) * 1e3
+    step_roofline = {"floor_ms": floor_ms, "measured_ms": total_ms / args.steps,
+                     "frac": floor_ms / (total_ms / args.steps), "hbm_bytes_per_step": step_bytes,
+                     "fp64_flops_per_step": step_flops,
+                     "binding": "fp64" if step_flops / (FP64_TENSOR_PEAK_TFLOPS * 1e12) > step_bytes / (hbm_peak * 1e9)
+                     else "hbm"}
+
     # -------- e2e through the public C ABI with pinned host buffers
     e2e = None
     try:
@@ -449,7 +462,8 @@ def main():
                                    f"D={mi.dims}, 8 layout indices, n={n} dictionary patches per rank",
                        "global_batch": n_total, "parallelism": f"replicas x{world} (independent images)",
                        "l2": "flushed (256 MiB write) before every timed step"},
-            "roofline": roofline, "roofline_hbm": roofline_hbm, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "roofline_hbm": roofline_hbm, "step_roofline": step_roofline,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk, "inpaint": inpaint, "candidate_scoring": knn,
             "breakdown": {"host_eigen_s_per_step": float(np.mean(host_eigen)), "kernels": breakdown},
