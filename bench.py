@@ -370,8 +370,15 @@ def main():
     # whole-step floor (SURVEY.md §8(d) model): max(HBM bytes / BW, fp64 flops / FP64 tensor peak)
     # with this pipeline's own algorithmic bytes (every counted kernel, per step) and the one
     # projection pass it performs
-    step_bytes = sum(algorithmic_bytes(k, n, mi.dims, mc) * v[1] / args.steps for k, v in prof.items()
-                     if algorithmic_bytes(k, n, mi.dims, mc) is not None)
+    F = p["patch_size"] ** 2 * (1 if img.ndim == 2 else img.shape[2])
+    Fpad = (F + 127) // 128 * 128
+    extra = {"project": (4 + 8 * mi.dims) * n,        # dictionary keys in, fp64 projections out
+             "patch_matrix": (4 + Fpad) * n,            # keys in, feature-major patch matrix out
+             "patch_moments": Fpad * n}                 # the patch matrix read once
+    def step_b(k):
+        b = algorithmic_bytes(k, n, mi.dims, mc)
+        return b if b is not None else extra.get(k)
+    step_bytes = sum(step_b(k) * v[1] / args.steps for k, v in prof.items() if step_b(k) is not None)
     step_flops = 8 * algorithmic_flops("project", n, mi.dims, mc)
     floor_ms = max(step_bytes / (hbm_peak * 1e9), step_flops / (FP64_TENSOR_PEAK_TFLOPS * 1e12)) * 1e3
     step_roofline = {"floor_ms": floor_ms, "measured_ms": total_ms / args.steps,
