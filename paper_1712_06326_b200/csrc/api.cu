@@ -473,6 +473,7 @@ zi_status zi_multi_index_destroy(zi_multi_index* mi) {
         cudaStreamSynchronize(mi->ctx->stream);
         if (mi->ev0) cudaEventDestroy(mi->ev0);
         if (mi->ev1) cudaEventDestroy(mi->ev1);
+        if (mi->hres) cudaFreeHost(mi->hres);
         delete mi;
     });
 }

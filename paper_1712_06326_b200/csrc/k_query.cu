@@ -13,6 +13,7 @@
 // above such a bound, or if k smaller entries exist in the same CTA buffer.  Packed values are
 // unique (keys are), so the final k smallest are exactly the reference's knn_search result.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -41,6 +42,15 @@ struct qws {
     uint32_t gcount;            // k_query_one: candidates appended to the compact global list
     unsigned long long final_bound;
     unsigned long long tphase[10];  // debug: %globaltimer at phase boundaries (CTA 0 / last CTA)
+};
+
+// Fill-loop query result in mapped pinned host memory: written by the last CTA of k_query_one,
+// then `seq` is published after a system-scope fence -- the host spins on it instead of a D2H copy
+// plus a stream synchronisation.
+struct qres {
+    unsigned long long best;
+    uint32_t lid, count, overflow;
+    volatile uint32_t seq;
 };
 
 struct index_view {
@@ -925,7 +935,8 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
                                                           const uint8_t* __restrict__ target, qws* ws, uint32_t k,
                                                           int norm, uint32_t* __restrict__ cand_cnt,
                                                           unsigned long long* __restrict__ cand,
-                                                          unsigned long long* __restrict__ out) {
+                                                          unsigned long long* __restrict__ out, qres* res,
+                                                          uint32_t seq) {
     extern __shared__ unsigned long long s_buf[];  // kOneCap | sel (kOneMaxK) | tmp | hist | xc | comp | target
     unsigned long long* sel = s_buf + kOneCap;
     unsigned long long* tmp = sel + kOneMaxK;
@@ -1161,6 +1172,12 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
         if (tid == 0) {
             ws->overflow = 2;
             cand_cnt[0] = total;  // the compact list as ONE list for k_knn_merge
+            if (res) {
+                res->lid = static_cast<uint32_t>(lid);
+                res->overflow = 2;
+                __threadfence_system();
+                res->seq = seq;
+            }
         }
         return;  // host: k_knn_merge + k_refine over the same list
     }
@@ -1170,7 +1187,15 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
     if (tid == 0) {
         ws->count = static_cast<uint32_t>(cnt);
         ws->overflow = 0;
-        ws->bound = kU64Max;
+        ws->bound = kU64Max;  // the workspace is left ready for the next query (no host memsets)
+        if (res) {
+            res->best = ws->best;
+            res->lid = static_cast<uint32_t>(lid);
+            res->count = static_cast<uint32_t>(cnt);
+            res->overflow = 0;
+            __threadfence_system();
+            res->seq = seq;
+        }
     }
 }
 
@@ -1821,11 +1846,28 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
     const size_t one_smem = (kOneCap + kOneMaxK + kOneBinCap) * sizeof(unsigned long long) + (kOneBins + 2) * sizeof(uint32_t) +
                             static_cast<size_t>(mi->mc) * (mi->dims + 1) * sizeof(double) + tbytes + 16;
     bool done = false;
-    if (k <= kOneMaxK && one_smem <= 220 * 1024 && !std::getenv("ZI_QUERY_MULTI")) {
+    static const bool force_multi = std::getenv("ZI_QUERY_MULTI") != nullptr;
+    static const bool debug_query = std::getenv("ZI_DEBUG_QUERY") != nullptr;
+    // mapped pinned result (fast path: no D2H copy, no stream synchronisation)
+    if (!mi->hres) {
+        ZI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mi->hres), sizeof(qres), cudaHostAllocMapped));
+        std::memset(mi->hres, 0, sizeof(qres));
+        ZI_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mi->dres), mi->hres, 0));
+    }
+    qres* hr = reinterpret_cast<qres*>(mi->hres);
+    if (s.ws != mi->qws_last) {  // new or moved workspace: contents unknown
+        mi->qws_clean = false;
+        mi->qws_last = s.ws;
+    }
+    if (k <= kOneMaxK && one_smem <= 220 * 1024 && !force_multi) {
         const int G1 = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(nblk, 1),
                                                            std::min<uint64_t>(static_cast<uint64_t>(s.G), 2ull * ctx->num_sms)));
-        ZI_CUDA(cudaMemsetAsync(&s.ws->bound, 0xff, sizeof(unsigned long long), ctx->stream));
-        ZI_CUDA(cudaMemsetAsync(&s.ws->done, 0, 2 * sizeof(uint32_t), ctx->stream));  // done + gcount
+        if (!mi->qws_clean) {
+            ZI_CUDA(cudaMemsetAsync(&s.ws->bound, 0xff, sizeof(unsigned long long), ctx->stream));
+            ZI_CUDA(cudaMemsetAsync(&s.ws->done, 0, 2 * sizeof(uint32_t), ctx->stream));  // done + gcount
+        }
+        const uint32_t seq = ++mi->qseq;
+        qres* dres = reinterpret_cast<qres*>(mi->dres);
         switch (mv.idx[0].P) {
 #define ZI_ONE_CASE(PP)                                                                                              \
     case PP: {                                                                                                       \
@@ -1835,7 +1877,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
             attr = true;                                                                                             \
         }                                                                                                            \
         ZI_LAUNCH(ctx, "query_one", k_query_one<PP>, G1, kOneThreads, one_smem, mv, mi->image.p, mi->w, s.target, s.ws, \
-                  k, norm, s.cand_cnt, s.cand, s.out);                                                               \
+                  k, norm, s.cand_cnt, s.cand, s.out, dres, seq);                                                    \
         break;                                                                                                       \
     }
             ZI_ONE_CASE(1) ZI_ONE_CASE(2) ZI_ONE_CASE(3) ZI_ONE_CASE(4)
@@ -1843,9 +1885,29 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
 #undef ZI_ONE_CASE
             default: throw error(ZI_E_INVALID, "dims above 32");
         }
-        ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
-        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (debug_query || ctx->profiling) {
+            ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        } else {
+            // spin on the published sequence number; a fault or a finished stream without it is
+            // reported instead of spinning forever
+            unsigned spins = 0;
+            while (hr->seq != seq) {
+                if ((++spins & 1023u) == 0) {
+                    const cudaError_t e = cudaStreamQuery(ctx->stream);
+                    if (e != cudaSuccess && e != cudaErrorNotReady) ZI_CUDA(e);
+                    if (e == cudaSuccess && hr->seq != seq) throw error(ZI_E_RUNTIME, "query result not published");
+                }
+            }
+            std::atomic_thread_fence(std::memory_order_acquire);
+            hq->best = hr->best;
+            hq->lid = hr->lid;
+            hq->count = hr->count;
+            hq->overflow = hr->overflow;
+        }
+        mi->qws_clean = hq->overflow == 0;
         if (hq->overflow == 2) {  // rare: the merge did not fit -> chunked merge over the same CTA lists
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));
             query_scratch s1 = s;
             s1.G = 1;
             knn_fallback(ctx, s1, k, norm, &ra, rsmem);
@@ -1854,6 +1916,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
         }
         done = true;
     }
+    if (!done) mi->qws_clean = false;  // the multi-launch paths leave the workspace as they please
     if (!done && !fused_query(mi, s, mv, k, norm, hq, knn_out != nullptr)) {
         const int win = seed_window(k);
         const size_t prep_smem = seed_smem_words(k) * sizeof(unsigned long long) +
@@ -1881,7 +1944,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
             ZI_CUDA(cudaStreamSynchronize(ctx->stream));
         }
     }
-    if (std::getenv("ZI_DEBUG_QUERY")) {
+    if (debug_query) {
         std::fprintf(stderr, "query lid=%u bound_dist=%u total=%u m=%u count=%u overflow=%u phases_us:", hq->lid,
                      static_cast<unsigned>(hq->final_bound >> 32), hq->dbg_total, hq->dbg_m, hq->count, hq->overflow);
         for (int i = 1; i < 10; ++i)

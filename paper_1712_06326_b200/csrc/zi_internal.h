@@ -156,6 +156,11 @@ struct zi_multi_index {
     zi::dbuf<uint32_t> recs;             // (W+1)*n sort records (Morton words + payload)
     zi::dbuf<uint8_t> qscratch;          // query scratch
     zi::hbuf<uint8_t> hstage;            // pinned staging for targets/results
+    void* hres = nullptr;                // mapped pinned query result (k_query_one publishes it)
+    void* dres = nullptr;
+    uint32_t qseq = 0;
+    const void* qws_last = nullptr;      // query workspace of the last launch
+    bool qws_clean = false;              // the last k_query_one left it reset
     zi::hbuf<unsigned long long> hmom;
     std::vector<int64_t> s, S;           // host copy of the moments
     // device PCA (k_pca.cu): feature columns [8][mc], eigenvalues [8][D], eigenvector scratch
