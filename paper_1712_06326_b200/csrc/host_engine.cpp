@@ -54,31 +54,61 @@ double channel_mean(const uint8_t* p, int C) {
     return static_cast<double>(sum) / C;
 }
 
-// proj/src/engine.cpp:83-94
+// proj/src/engine.cpp:83-94.  conf is 0 at unknown pixels, so adding it there is exact (x + 0.0
+// == x) and the known test is not needed inside the window.
 double confidence_term(const mask& m, const std::vector<double>& conf, int cx, int cy, int K) {
     const int r = (K - 1) / 2;
     double sum = 0.0;
-    for (int y = cy - r; y <= cy + r; ++y)
-        for (int x = cx - r; x <= cx + r; ++x) {
-            if (!m.in_bounds(x, y) || !m.is_known(x, y)) continue;
-            sum += conf[m.idx(x, y)];
-        }
+    const int y0 = std::max(cy - r, 0), y1 = std::min(cy + r, m.h - 1);
+    const int x0 = std::max(cx - r, 0), x1 = std::min(cx + r, m.w - 1);
+    for (int y = y0; y <= y1; ++y) {
+        const double* row = conf.data() + static_cast<size_t>(y) * m.w;
+        for (int x = x0; x <= x1; ++x) sum += row[x];
+    }
     return sum / (static_cast<double>(K) * K);
 }
 
+// Per-pixel caches of the data term's inputs, kept current across pastes:
+//   inten[i] = channel_mean (int channel sum / C as double, proj/src/engine.cpp:24-28)
+//   gflag[i] = interior pixel whose 4 neighbours and itself are known (engine.cpp:110-121)
+struct grad_cache {
+    std::vector<double> inten;
+    std::vector<uint8_t> gflag;
+    void init(const raster& img, const mask& m) {
+        inten.assign(static_cast<size_t>(m.w) * m.h, 0.0);
+        gflag.assign(static_cast<size_t>(m.w) * m.h, 0);
+        for (int y = 0; y < m.h; ++y)
+            for (int x = 0; x < m.w; ++x) inten[m.idx(x, y)] = channel_mean(img.at(x, y), img.C);
+        refresh(m, 0, 0, m.w - 1, m.h - 1);
+    }
+    void set_pixel(const raster& img, const mask& m, int x, int y) { inten[m.idx(x, y)] = channel_mean(img.at(x, y), img.C); }
+    void refresh(const mask& m, int xa, int ya, int xb, int yb) {
+        xa = std::max(xa, 0);
+        ya = std::max(ya, 0);
+        xb = std::min(xb, m.w - 1);
+        yb = std::min(yb, m.h - 1);
+        for (int y = ya; y <= yb; ++y)
+            for (int x = xa; x <= xb; ++x)
+                gflag[m.idx(x, y)] = x >= 1 && y >= 1 && x + 1 < m.w && y + 1 < m.h && m.is_known(x, y) &&
+                                     m.is_known(x - 1, y) && m.is_known(x + 1, y) && m.is_known(x, y - 1) &&
+                                     m.is_known(x, y + 1);
+    }
+};
+
 // proj/src/engine.cpp:96-146
-double compute_priority(const raster& img, const mask& m, const std::vector<double>& conf, int cx, int cy, int K) {
+double compute_priority(const raster& img, const mask& m, const std::vector<double>& conf, const grad_cache& gc,
+                        int cx, int cy, int K) {
     const int r = (K - 1) / 2;
     const double cterm = confidence_term(m, conf, cx, cy, K);
     double best_sq = -1.0, bgx = 0.0, bgy = 0.0;
-    for (int y = cy - r; y <= cy + r; ++y)
-        for (int x = cx - r; x <= cx + r; ++x) {
-            if (x < 1 || y < 1 || x + 1 >= img.w || y + 1 >= img.h) continue;
-            if (!m.is_known(x, y) || !m.is_known(x - 1, y) || !m.is_known(x + 1, y) || !m.is_known(x, y - 1) ||
-                !m.is_known(x, y + 1))
-                continue;
-            const double gx = (channel_mean(img.at(x + 1, y), img.C) - channel_mean(img.at(x - 1, y), img.C)) / 2.0;
-            const double gy = (channel_mean(img.at(x, y + 1), img.C) - channel_mean(img.at(x, y - 1), img.C)) / 2.0;
+    const int y0 = std::max(cy - r, 0), y1 = std::min(cy + r, m.h - 1);
+    const int x0 = std::max(cx - r, 0), x1 = std::min(cx + r, m.w - 1);
+    for (int y = y0; y <= y1; ++y) {
+        const size_t row = static_cast<size_t>(y) * m.w;
+        for (int x = x0; x <= x1; ++x) {
+            if (!gc.gflag[row + x]) continue;
+            const double gx = (gc.inten[row + x + 1] - gc.inten[row + x - 1]) / 2.0;
+            const double gy = (gc.inten[row + m.w + x] - gc.inten[row - m.w + x]) / 2.0;
             const double sq = gx * gx + gy * gy;
             if (sq > best_sq) {
                 best_sq = sq;
@@ -86,6 +116,8 @@ double compute_priority(const raster& img, const mask& m, const std::vector<doub
                 bgy = gy;
             }
         }
+    }
+    (void)img;
     auto unknown_at = [&](int x, int y) {
         x = std::clamp(x, 0, m.w - 1);
         y = std::clamp(y, 0, m.h - 1);
@@ -117,6 +149,7 @@ public:
         : img_(img), m_(m), K_(K), conf_(static_cast<size_t>(m.w) * m.h, 0.0),
           cached_(static_cast<size_t>(m.w) * m.h, 0.0), in_front_(static_cast<size_t>(m.w) * m.h, 0) {
         for (size_t i = 0; i < conf_.size(); ++i) conf_[i] = m.known[i] ? 1.0 : 0.0;
+        gc_.init(img_, m_);
         for (int y = 0; y < m.h; ++y)
             for (int x = 0; x < m.w; ++x)
                 if (is_fillfront_pixel(m_, x, y)) add(x, y);
@@ -143,9 +176,11 @@ public:
                 for (int c = 0; c < img_.C; ++c) d[c] = s[c];
                 m_.known[m_.idx(x, y)] = 1;
                 conf_[m_.idx(x, y)] = cc;
+                gc_.set_pixel(img_, m_, x, y);
                 ++filled;
             }
         }
+        if (filled) gc_.refresh(m_, cx - r - 1, cy - r - 1, cx + r + 1, cy + r + 1);
         const int refresh = K_ - 1;
         for (int y = cy - refresh; y <= cy + refresh; ++y) {
             if (y < 0 || y >= m_.h) continue;
@@ -166,7 +201,7 @@ public:
 private:
     void add(int x, int y) {
         const size_t i = m_.idx(x, y);
-        cached_[i] = compute_priority(img_, m_, conf_, x, y, K_);
+        cached_[i] = compute_priority(img_, m_, conf_, gc_, x, y, K_);
         in_front_[i] = 1;
         queue_.emplace(cached_[i], static_cast<uint32_t>(i));
     }
@@ -177,7 +212,7 @@ private:
     }
     void refresh_one(int x, int y) {
         const size_t i = m_.idx(x, y);
-        const double fresh = compute_priority(img_, m_, conf_, x, y, K_);
+        const double fresh = compute_priority(img_, m_, conf_, gc_, x, y, K_);
         if (fresh != cached_[i]) {
             queue_.erase({cached_[i], static_cast<uint32_t>(i)});
             cached_[i] = fresh;
@@ -190,6 +225,7 @@ private:
     std::vector<double> conf_, cached_;
     std::vector<uint8_t> in_front_;
     std::set<std::pair<double, uint32_t>, by_priority> queue_;
+    grad_cache gc_;
 };
 
 // extract_patch_clamped (proj/src/image.cpp:7-47)
@@ -305,7 +341,7 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
     stats->iterations = it;
     stats->inpaint_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (ae_contrib > 0) stats->mean_ae = ae_sum / static_cast<double>(ae_contrib);
-    if (std::getenv("ZI_DEBUG_QUERY"))
+    if (std::getenv("ZI_DEBUG_QUERY") || std::getenv("ZI_DEBUG_FILL"))
         std::fprintf(stderr, "fill loop: %llu iterations, query %.1f us/it, paste+priorities %.1f us/it\n",
                      static_cast<unsigned long long>(it), 1e6 * t_query / it, 1e6 * t_paste / it);
     stats->ae_excluded = ae_excl;
