@@ -924,6 +924,113 @@ __global__ void k_gather_topk(const uint32_t* __restrict__ lo, const uint32_t* _
 // Morton range of blocks, seeds a local bound from its best block by bbox lower bound, shares it
 // through atomicMin on ws->bound, and keeps its exact local top-k; the last CTA to finish
 // (threadfence + ticket) selects the global top-k, refines it and resets the ticket/bound.
+// masked costs (proj/src/engine.cpp:48-76) of list[0..cnt) into s_cost, CTA-cooperative: all
+// (candidate, known pixel) pairs in parallel, four image loads in flight per thread
+__device__ void cost_candidates(const uint8_t* __restrict__ img, int w, int C, int K, const uint8_t* s_tv,
+                                const uint16_t* s_loc, int nloc, const unsigned long long* list, int cnt, int norm,
+                                uint32_t* s_cost) {
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) s_cost[e] = 0;
+    __syncthreads();
+    const int pairs = cnt * nloc;
+    const int stride = blockDim.x;
+    for (int p0 = threadIdx.x; p0 < pairs; p0 += 4 * stride) {
+        uint8_t sv[4][3];
+        int pe[4], pl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int pi = p0 + u * stride;
+            pe[u] = -1;
+            if (pi < pairs) {
+                const int e = pi / nloc, li = pi - e * nloc;
+                const uint32_t key = static_cast<uint32_t>(list[e] & 0xffffffffu);
+                const int l = s_loc[li];
+                const uint8_t* src = img + (static_cast<size_t>((key >> 16) + l / K) * w + (key & 0xffff) + l % K) * C;
+                pe[u] = e;
+                pl[u] = l;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) sv[u][c] = c < C ? __ldg(src + c) : 0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (pe[u] < 0) continue;
+            const uint8_t* t = s_tv + pl[u] * C;
+            uint32_t acc = 0;
+            for (int c = 0; c < C; ++c) {
+                const int d = static_cast<int>(t[c]) - static_cast<int>(sv[u][c]);
+                acc += norm == 0 ? static_cast<uint32_t>(d * d) : static_cast<uint32_t>(d < 0 ? -d : d);
+            }
+            atomicAdd(&s_cost[pe[u]], acc);
+        }
+    }
+    __syncthreads();
+}
+
+// k-th smallest of m unique packed values in buf (kU64Max when m <= k): distance histogram ->
+// boundary bin -> exact rank inside it.  Returns kU64Max - 1 on a degenerate boundary bin
+// (more than tmp_cap values), which the caller treats as an overflow.
+__device__ unsigned long long kth_packed(const unsigned long long* buf, int m, uint32_t k, unsigned long long* tmp,
+                                         int tmp_cap, uint32_t* hist, int nbins, uint32_t maxd) {
+    __shared__ int s_ntmp, s_B, s_cumB;
+    __shared__ unsigned long long s_T;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+    if (m <= static_cast<int>(k)) return kU64Max;
+    for (int i = tid; i <= nbins; i += nt) hist[i] = 0;
+    if (tid == 0) {
+        s_ntmp = 0;
+        s_B = -1;
+        s_T = kU64Max - 1;
+    }
+    __syncthreads();
+    const uint64_t scale = (static_cast<uint64_t>(nbins) << 32) / (static_cast<uint64_t>(maxd) + 1);
+    for (int i = tid; i < m; i += nt) {
+        const uint32_t bin = static_cast<uint32_t>(((buf[i] >> 32) * scale) >> 32);
+        atomicAdd(&hist[bin < static_cast<uint32_t>(nbins) ? bin : nbins - 1], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t run = 0;
+        for (int base = 0; base < nbins; base += 32) {
+            uint32_t x = base + lane < nbins ? hist[base + lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, run + x >= k);
+            if (hit) {
+                const int src = __ffs(hit) - 1;
+                const uint32_t incl = __shfl_sync(0xffffffffu, x, src);
+                if (lane == 0) {
+                    s_B = base + src;
+                    s_cumB = static_cast<int>(run + incl - hist[base + src]);
+                }
+                break;
+            }
+            run += __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+    __syncthreads();
+    const int B = s_B, cumB = s_cumB;
+    if (B < 0 || static_cast<int>(hist[B]) > tmp_cap) return kU64Max - 1;
+    for (int i = tid; i < m; i += nt) {
+        const unsigned long long c = buf[i];
+        const uint32_t bin0 = static_cast<uint32_t>(((c >> 32) * scale) >> 32);
+        const int bin = static_cast<int>(bin0 < static_cast<uint32_t>(nbins) ? bin0 : nbins - 1);
+        if (bin == B) tmp[atomicAdd(&s_ntmp, 1)] = c;
+    }
+    __syncthreads();
+    const int ntmp = s_ntmp, need = static_cast<int>(k) - cumB;  // need-th smallest (1-based) in tmp
+    for (int i = tid; i < ntmp; i += nt) {
+        const unsigned long long c = tmp[i];
+        int r = 0;
+        for (int u = 0; u < ntmp; ++u) r += tmp[u] < c;
+        if (r == need - 1) s_T = c;
+    }
+    __syncthreads();
+    return s_T;
+}
+
 constexpr int kOneThreads = 256;
 constexpr int kOneCap = 4096;
 constexpr uint32_t kOneMaxK = 1024;
@@ -935,16 +1042,21 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
                                                           const uint8_t* __restrict__ target, qws* ws, uint32_t k,
                                                           int norm, uint32_t* __restrict__ cand_cnt,
                                                           unsigned long long* __restrict__ cand,
+                                                          uint32_t* __restrict__ ccost,
                                                           unsigned long long* __restrict__ out, qres* res,
-                                                          uint32_t seq) {
-    extern __shared__ unsigned long long s_buf[];  // kOneCap | sel (kOneMaxK) | tmp | hist | xc | comp | target
+                                                          uint32_t seq, int want_list) {
+    // kOneCap | sel (kOneMaxK) | tmp | hist | costs (kOneCap u32) | xc | comp | target | locals
+    extern __shared__ unsigned long long s_buf[];
     unsigned long long* sel = s_buf + kOneCap;
     unsigned long long* tmp = sel + kOneMaxK;
     uint32_t* hist = reinterpret_cast<uint32_t*>(tmp + kOneBinCap);
+    uint32_t* s_cost = hist + kOneBins + 2;
     const int KK = mv.K * mv.K, mc = mv.m * mv.C, C = mv.C, D = mv.D;
-    double* s_xc = reinterpret_cast<double*>(hist + kOneBins + 2);
+    double* s_xc = reinterpret_cast<double*>(s_cost + kOneCap);
     double* s_comp = s_xc + mc;
     uint8_t* s_t = reinterpret_cast<uint8_t*>(s_comp + static_cast<size_t>(mc) * D);
+    uint16_t* s_loc = reinterpret_cast<uint16_t*>(s_t + ((KK * C + KK + 1) & ~1));
+    __shared__ int s_nloc;
     __shared__ int s_ov[8];
     __shared__ int s_lid, s_cnt, s_last;
     __shared__ uint8_t s_q[32];
@@ -957,6 +1069,16 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
     if (tid < 32) s_q[tid] = 0;
     if (tid == 0) s_cnt = 0;
     __syncthreads();
+    if (warp == 0) {  // known locals, ascending (known_locals_of, engine.cpp:16-22), via ballots
+        int c = 0;
+        for (int base = 0; base < KK; base += 32) {
+            const bool kn = base + lane < KK && s_t[KK * C + base + lane] != 0;
+            const unsigned mk = __ballot_sync(0xffffffffu, kn);
+            if (kn) s_loc[c + __popc(mk & ((1u << lane) - 1u))] = static_cast<uint16_t>(base + lane);
+            c += __popc(mk);
+        }
+        if (lane == 0) s_nloc = c;
+    }
     const uint8_t* tv = s_t;
     const uint8_t* tk = s_t + KK * C;
     {  // select_index (engine.cpp:162-176)
@@ -1106,21 +1228,39 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
             for (int t = tid; t < cnt; t += kOneThreads) sel[t] = s_buf[t];
             __syncthreads();
         }
-        __shared__ unsigned long long s_kth;
-        if (tid == 0) s_kth = 0;
-        __syncthreads();
-        __shared__ uint32_t s_gbase;
-        if (tid == 0) s_gbase = atomicAdd(&ws->gcount, static_cast<uint32_t>(cnt));
-        __syncthreads();
-        unsigned long long kth = 0;
-        for (int t = tid; t < cnt; t += kOneThreads) {
-            cand[s_gbase + t] = sel[t];
-            kth = sel[t] > kth ? sel[t] : kth;
+        __shared__ unsigned long long s_kth, s_gb;
+        __shared__ int s_keep;
+        if (tid == 0) {
+            s_kth = 0;
+            s_keep = 0;
         }
-        if (cnt >= static_cast<int>(k)) {  // this CTA's k-th is a valid global bound
+        __syncthreads();
+        // publish this CTA's k-th first (a valid global bound when it holds k candidates), then
+        // keep only the local winners that can still make the global top-k
+        unsigned long long kth = 0;
+        for (int t = tid; t < cnt; t += kOneThreads) kth = sel[t] > kth ? sel[t] : kth;
+        if (cnt >= static_cast<int>(k)) {
             atomicMax(&s_kth, kth);
             __syncthreads();
             if (tid == 0) atomicMin(&ws->bound, s_kth);
+        }
+        __syncthreads();
+        if (tid == 0) s_gb = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+        __syncthreads();
+        const unsigned long long gb = s_gb;
+        for (int t = tid; t < cnt; t += kOneThreads)
+            if (sel[t] <= gb) tmp[atomicAdd(&s_keep, 1)] = sel[t];
+        __syncthreads();
+        const int keep = s_keep;
+        // refine ahead of the merge: every CTA costs its own surviving winners (in parallel across
+        // CTAs), so the last CTA only selects the global k and takes the min over their costs
+        cost_candidates(img, w, C, mv.K, s_t, s_loc, s_nloc, tmp, keep, norm, s_cost);
+        __shared__ uint32_t s_gbase;
+        if (tid == 0) s_gbase = atomicAdd(&ws->gcount, static_cast<uint32_t>(keep));
+        __syncthreads();
+        for (int t = tid; t < keep; t += kOneThreads) {
+            cand[s_gbase + t] = tmp[t];
+            ccost[s_gbase + t] = s_cost[t];
         }
     }
     ZI_TPHASE(4)
@@ -1148,7 +1288,10 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
             const unsigned long long c = cand[f];
             if (c <= bound) {
                 const int slot = atomicAdd(&s_m, 1);
-                if (slot < kOneCap) s_buf[slot] = c;
+                if (slot < kOneCap) {
+                    s_buf[slot] = c;
+                    s_cost[slot] = ccost[f];
+                }
                 atomicMax(&s_maxd, static_cast<uint32_t>(c >> 32));
             }
         }
@@ -1158,7 +1301,10 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
         (void)s_pref;
     }
     ZI_TPHASE(7)
-    int cnt = m > kOneCap ? -1 : select_sorted_topk(s_buf, m, k, sel, tmp, kOneBinCap, hist, 256, maxd);
+    // the global k-th packed value; winners = candidates <= it; best = min (cost, key) over them
+    const unsigned long long T = m > kOneCap ? kU64Max - 1 : kth_packed(s_buf, m, k, tmp, kOneBinCap, hist, 256, maxd);
+    int cnt = T == kU64Max - 1 ? -1 : (m < static_cast<int>(k) ? m : static_cast<int>(k));
+    if (cnt >= 0 && want_list) cnt = select_sorted_topk(s_buf, m, k, sel, tmp, kOneBinCap, hist, 256, maxd);
     ZI_TPHASE(8)
     if (tid == 0) {
         ws->lid = static_cast<uint32_t>(lid);
@@ -1181,8 +1327,23 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
         }
         return;  // host: k_knn_merge + k_refine over the same list
     }
-    for (int i = tid; i < cnt; i += kOneThreads) out[i] = sel[i];
-    refine_list(img, w, C, KK > 0 ? mv.K : 1, target, sel, cnt, norm, reinterpret_cast<uint8_t*>(s_buf), ws);
+    if (want_list)
+        for (int i = tid; i < cnt; i += kOneThreads) out[i] = sel[i];
+    {
+        __shared__ unsigned long long s_best;
+        if (tid == 0) s_best = kU64Max;
+        __syncthreads();
+        unsigned long long mine = kU64Max;
+        for (int i = tid; i < m; i += kOneThreads)
+            if (s_buf[i] <= T) {
+                const unsigned long long c = pack_candidate(s_cost[i], static_cast<uint32_t>(s_buf[i] & 0xffffffffu));
+                mine = c < mine ? c : mine;
+            }
+        mine = warp_min(mine);
+        if (lane == 0) atomicMin(&s_best, mine);
+        __syncthreads();
+        if (tid == 0) ws->best = s_best;
+    }
     ZI_TPHASE(9)
     if (tid == 0) {
         ws->count = static_cast<uint32_t>(cnt);
@@ -1600,6 +1761,7 @@ struct query_scratch {
     qws* ws;
     uint32_t* cand_cnt;
     unsigned long long* cand;
+    uint32_t* ccost;  // k_query_one: masked cost of each cand entry
     unsigned long long* out;
     uint8_t* target;
     int G;
@@ -1619,12 +1781,14 @@ static query_scratch carve(dbuf<uint8_t>& buf, const zi_ctx* ctx, uint64_t nblk,
     const size_t o_ws = take(sizeof(qws));
     const size_t o_cc = take(s.G * sizeof(uint32_t));
     const size_t o_c = take(static_cast<size_t>(s.G) * kscan * sizeof(unsigned long long));
+    const size_t o_cc2 = take(static_cast<size_t>(s.G) * kscan * sizeof(uint32_t));
     const size_t o_out = take(kk * sizeof(unsigned long long));
     const size_t o_t = take(target_bytes + 64);
     uint8_t* b = buf.ensure(off);
     s.ws = reinterpret_cast<qws*>(b + o_ws);
     s.cand_cnt = reinterpret_cast<uint32_t*>(b + o_cc);
     s.cand = reinterpret_cast<unsigned long long*>(b + o_c);
+    s.ccost = reinterpret_cast<uint32_t*>(b + o_cc2);
     s.out = reinterpret_cast<unsigned long long*>(b + o_out);
     s.target = b + o_t;
     return s;
@@ -1843,8 +2007,9 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
     qws* hq = reinterpret_cast<qws*>(stage + res_off);
     const size_t rsmem = ((KK * mi->C + 1) & ~size_t(1)) + (KK + 16) * sizeof(uint16_t) + kRefineSlots * sizeof(uint32_t) + 32;
     const refine_args ra{mi->image.p, mi->w, mi->C, mi->K};
-    const size_t one_smem = (kOneCap + kOneMaxK + kOneBinCap) * sizeof(unsigned long long) + (kOneBins + 2) * sizeof(uint32_t) +
-                            static_cast<size_t>(mi->mc) * (mi->dims + 1) * sizeof(double) + tbytes + 16;
+    const size_t one_smem = (kOneCap + kOneMaxK + kOneBinCap) * sizeof(unsigned long long) +
+                            (kOneBins + 2 + kOneCap) * sizeof(uint32_t) +
+                            static_cast<size_t>(mi->mc) * (mi->dims + 1) * sizeof(double) + tbytes + 2 + KK * 2 + 16;
     bool done = false;
     static const bool force_multi = std::getenv("ZI_QUERY_MULTI") != nullptr;
     static const bool debug_query = std::getenv("ZI_DEBUG_QUERY") != nullptr;
@@ -1877,7 +2042,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
             attr = true;                                                                                             \
         }                                                                                                            \
         ZI_LAUNCH(ctx, "query_one", k_query_one<PP>, G1, kOneThreads, one_smem, mv, mi->image.p, mi->w, s.target, s.ws, \
-                  k, norm, s.cand_cnt, s.cand, s.out, dres, seq);                                                    \
+                  k, norm, s.cand_cnt, s.cand, s.ccost, s.out, dres, seq, knn_out != nullptr ? 1 : 0);             \
         break;                                                                                                       \
     }
             ZI_ONE_CASE(1) ZI_ONE_CASE(2) ZI_ONE_CASE(3) ZI_ONE_CASE(4)
