@@ -98,6 +98,8 @@ typedef struct {
     double build_seconds;      /* device time of the last build (events) */
     double eigen_seconds;      /* host wall time spent in the eigen-solve step (launch or host solve) */
     int32_t pca_on_device;     /* 1: covariance + eigen-solve ran in k_pca (mc <= 224), 0: host solve */
+    double coverage;           /* layout coverage c */
+    int32_t loaded;            /* 1: read from a ZIDX1 file */
 } zi_multi_index_info;
 
 typedef struct zi_ctx zi_ctx;                 /* one device + one stream + scratch */
@@ -180,6 +182,15 @@ zi_status zi_multi_index_layout_index(zi_multi_index* mi, int32_t layout, uint8_
                                       uint32_t* keys_out);
 /* borrowed view of one layout's zcurve_index (valid until mi is destroyed or rebuilt) */
 zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index** out);
+/* ZIDX1 persistence (io_index.hpp:21-22, io_index.cpp:133-154): eight blocks, layout 0 first,
+ * "ZIDX1" | u32 K | f64 coverage | u32 D | u32 layout | u64 n | u32 C | mean | components (D
+ * rows) | eigenvalues | lo | hi | n x (D bytes, u32 x, u32 y).  Load re-sorts each block on the
+ * device and recovers the dictionary from layout 0; `image` is the picture queries are refined
+ * against (its channel count must match the file).  Errors: ZI_E_RUNTIME for bad magic / header,
+ * truncation, key out of range or disagreeing blocks (the reference's std::runtime_error). */
+zi_status zi_multi_index_save(zi_multi_index* mi, const char* path);
+zi_status zi_multi_index_load(zi_ctx* ctx, const char* path, const uint8_t* image, int32_t w, int32_t h,
+                              int32_t C, zi_multi_index** out);
 /* exact int64 moments of the full K*K*C patch vector (s[F], S[F*F]) behind the PCA fit */
 zi_status zi_multi_index_moments(zi_multi_index* mi, int64_t* s_out, int64_t* S_out);
 

@@ -18,10 +18,10 @@ import numpy as np
 
 from . import _lib
 from ._lib import (BestPatch, EmptyDictionaryError, IndexConfig, InpaintConfig, IterationRecord, MultiIndexInfo,
-                   RunStats, check, lib, ptr, u8p, u32p, u64p, i32p, i64p, f64p)
+                   RunStats, ZIError, check, lib, ptr, u8p, u32p, u64p, i32p, i64p, f64p)
 
 __all__ = ["inpaint", "knn_search", "subset_layouts", "morton_less", "less_most_significant_bit", "Context",
-           "ZCurveIndex", "MultiIndex", "EmptyDictionaryError", "index_config", "NORMS"]
+           "ZCurveIndex", "MultiIndex", "EmptyDictionaryError", "ZIError", "index_config", "NORMS"]
 
 NORMS = {"l2": 0, "l1": 1}
 
@@ -230,6 +230,31 @@ class MultiIndex:
                                          self.channels, C.byref(self.cfg), C.byref(h)))
         self.h = h
         self._refresh_info()
+
+    def save(self, path) -> None:
+        """save_multi_index (proj/src/io_index.cpp:133-137): ZIDX1, eight blocks, layout 0 first."""
+        check(lib().zi_multi_index_save(self.h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path, image, known=None, ctx: Optional[Context] = None) -> "MultiIndex":
+        """load_multi_index (proj/src/io_index.cpp:139-154) plus the image queries are refined
+        against; `known` (optional) is kept as the default mask for inpaint()."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or Context.default()
+        img = _u8(image)
+        if img.ndim not in (2, 3):
+            raise ValueError("image must be (H, W) or (H, W, 3) uint8")
+        self.height, self.width = img.shape[:2]
+        self.channels = 1 if img.ndim == 2 else img.shape[2]
+        self._img = img
+        self._known = _u8(known) if known is not None else np.ones((self.height, self.width), np.uint8)
+        h = C.c_void_p()
+        check(lib().zi_multi_index_load(self.ctx.h, str(path).encode(), ptr(img, u8p), self.width, self.height,
+                                        self.channels, C.byref(h)))
+        self.h = h
+        self._refresh_info()
+        self.cfg = index_config(patch_size=self.info.patch_size, coverage=self.info.coverage, dims=self.dims)
+        return self
 
     def _refresh_info(self):
         info = MultiIndexInfo()

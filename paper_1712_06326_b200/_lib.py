@@ -55,7 +55,7 @@ class MultiIndexInfo(C.Structure):
     _fields_ = [("n", C.c_uint64), ("dims", C.c_int32), ("m", C.c_int32), ("channels", C.c_int32),
                 ("patch_size", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
                 ("build_seconds", C.c_double), ("eigen_seconds", C.c_double),
-                ("pca_on_device", C.c_int32)]
+                ("pca_on_device", C.c_int32), ("coverage", C.c_double), ("loaded", C.c_int32)]
 
 
 # name -> (restype, argtypes); mirrors include/zinpaint_b200.h one to one
@@ -89,6 +89,8 @@ SIGNATURES = {
     "zi_multi_index_build": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig),
                                        C.POINTER(vp)]),
     "zi_multi_index_rebuild": (C.c_int, [vp]),
+    "zi_multi_index_save": (C.c_int, [vp, C.c_char_p]),
+    "zi_multi_index_load": (C.c_int, [vp, C.c_char_p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]),
     "zi_multi_index_destroy": (C.c_int, [vp]),
     "zi_multi_index_get_info": (C.c_int, [vp, C.POINTER(MultiIndexInfo)]),
     "zi_multi_index_dictionary": (C.c_int, [vp, u32p]),

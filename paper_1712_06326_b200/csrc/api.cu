@@ -463,8 +463,42 @@ zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t*
     });
 }
 
+zi_status zi_multi_index_save(zi_multi_index* mi, const char* path) {
+    return guard(mi ? mi->ctx : nullptr, [&] {
+        require(mi && path, "null argument");
+        zi::save_multi_index(mi, path);
+    });
+}
+
+zi_status zi_multi_index_load(zi_ctx* ctx, const char* path, const uint8_t* image, int32_t w, int32_t h, int32_t C,
+                              zi_multi_index** out) {
+    return guard(ctx, [&] {
+        require(ctx && path && image && out, "null argument");
+        require(w > 0 && h > 0 && (C == 1 || C == 3), "raster_image: bad dimensions");
+        require(w <= 65535 && h <= 65535, "image side above the 16-bit patch_key range");
+        const zi::zidx_header hd = zi::zidx_peek(path);
+        zi_index_config cfg;
+        zi_index_config_default(&cfg);
+        cfg.patch_size = hd.K;
+        cfg.coverage = hd.coverage;
+        cfg.dims = hd.D;
+        std::vector<uint8_t> known(static_cast<size_t>(w) * h, 1);  // the mask is not part of an index
+        zi_multi_index* mi = new_multi_index(ctx, image, known.data(), w, h, C, &cfg);
+        try {
+            zi::load_multi_index_into(mi, path);
+        } catch (...) {
+            delete mi;
+            throw;
+        }
+        *out = mi;
+    });
+}
+
 zi_status zi_multi_index_rebuild(zi_multi_index* mi) {
-    return guard(mi ? mi->ctx : nullptr, [&] { zi::build_multi_index(mi); });
+    return guard(mi ? mi->ctx : nullptr, [&] {
+        require(mi && !mi->loaded, "rebuild needs the build inputs; this index was loaded from a file");
+        zi::build_multi_index(mi);
+    });
 }
 
 zi_status zi_multi_index_destroy(zi_multi_index* mi) {
@@ -491,6 +525,8 @@ zi_status zi_multi_index_get_info(const zi_multi_index* mi, zi_multi_index_info*
         info->build_seconds = mi->build_ms * 1e-3;
         info->eigen_seconds = mi->eigen_s;
         info->pca_on_device = mi->device_pca ? 1 : 0;
+        info->coverage = mi->cfg.coverage;
+        info->loaded = mi->loaded ? 1 : 0;
     });
 }
 
@@ -532,6 +568,7 @@ zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index*
 
 zi_status zi_multi_index_moments(zi_multi_index* mi, int64_t* s_out, int64_t* S_out) {
     return guard(mi ? mi->ctx : nullptr, [&] {
+        require(!mi->loaded, "patch moments are not stored in an index file");
         zi::sync_host_model(mi);
         if (s_out) std::memcpy(s_out, mi->s.data(), mi->s.size() * sizeof(int64_t));
         if (S_out) std::memcpy(S_out, mi->S.data(), mi->S.size() * sizeof(int64_t));

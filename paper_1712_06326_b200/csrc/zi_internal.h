@@ -172,6 +172,7 @@ struct zi_multi_index {
     bool host_lohi = false;              // L[].lo/hi mirror the device min/max
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // build timing, read lazily (no sync at build end)
     bool build_ms_pending = false;
+    bool loaded = false;                 // read from a ZIDX1 file (no mask, no moments)
     bool device_pca = false;             // last build solved the eigenproblems on the device
     zi_layout_state L[8];
 };
@@ -256,6 +257,17 @@ void finish_build_timing(zi_multi_index* mi);
 size_t pca_work_doubles(int mc, int D);
 bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint64_t n, const int32_t* d_cols, int mc,
                    int D, double* d_mean, double* d_comp, double* d_eig, double* d_work, int* d_status);
+
+// ZIDX1 persistence (persist.cpp, proj/src/io_index.cpp)
+struct zidx_header {
+    int K = 0, D = 0, C = 0;
+    double coverage = 0.0;
+    uint64_t count = 0;
+};
+zidx_header zidx_peek(const char* path);
+void save_multi_index(zi_multi_index* mi, const char* path);
+// mi: created for the file's (K, coverage, dims) with layouts and image uploaded
+void load_multi_index_into(zi_multi_index* mi, const char* path);
 
 // fill loop (host_engine.cpp): run_loop / inpaint (proj/src/engine.cpp:283-506)
 void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known, const zi_index_config& cfg,

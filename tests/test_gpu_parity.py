@@ -487,3 +487,99 @@ def test_knn_batch_cfg5_like_vs_oracle(zb, D):
         for i in range(0, 64, 7):
             ref = oracle.knn_linear(sc, sk, queries[i], k)
             assert cnt[i] == ref.size and np.array_equal(out[i, :cnt[i]], ref), (k, i)
+
+
+# ------------------------------------------------------------------ ZIDX1 persistence
+def _parse_zidx1(path, K, C):
+    """Restated reader of the reference's format (proj/include/zinpaint/io_index.hpp:10-17)."""
+    import struct
+    raw = open(path, "rb").read()
+    off, blocks = 0, []
+    for _ in range(8):
+        assert raw[off:off + 5] == b"ZIDX1"
+        off += 5
+        k, cov, D, lid, n, ch = struct.unpack_from("<IdIIQI", raw, off)
+        off += struct.calcsize("<IdIIQI")
+        m = oracle.subset_layouts(k, cov)[0].shape[0] * ch
+        f = lambda cnt: np.frombuffer(raw, np.float64, cnt, off)
+        mean = f(m); off += 8 * m
+        comp = f(D * m).reshape(D, m); off += 8 * D * m
+        eig = f(D); off += 8 * D
+        lo = f(D); off += 8 * D
+        hi = f(D); off += 8 * D
+        ent = np.frombuffer(raw, np.uint8, n * (D + 8), off).reshape(n, D + 8); off += n * (D + 8)
+        coords = ent[:, :D].copy()
+        xy = ent[:, D:].copy().view(np.uint32)
+        keys = (xy[:, 1] << 16) | xy[:, 0]
+        blocks.append(dict(K=k, coverage=cov, D=D, layout=lid, n=n, C=ch, mean=mean, comp=comp, eig=eig, lo=lo,
+                           hi=hi, coords=coords, keys=keys))
+    assert off == len(raw)
+    return blocks
+
+
+def test_zidx1_save_format_and_load_roundtrip(zb, golden, tmp_path):
+    tag = "eval_48x40_c_s101_m102"
+    img, kn = golden[tag + "__image"], golden[tag + "__known"]
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8))
+    path = tmp_path / "idx.zidx"
+    mi.save(path)
+    blocks = _parse_zidx1(path, 9, 3)
+    for l, b in enumerate(blocks):
+        lay = mi.layout(l)
+        c, k = mi.index_arrays(l)
+        assert (b["K"], b["D"], b["layout"], b["n"], b["C"]) == (9, mi.dims, l, mi.n, 3)
+        assert b["coverage"] == 0.6
+        for f in ("mean", "eig", "lo", "hi"):
+            np.testing.assert_array_equal(b[f], lay["eigenvalues" if f == "eig" else f])
+        np.testing.assert_array_equal(b["comp"], lay["components"])
+        assert np.array_equal(b["coords"], c) and np.array_equal(b["keys"], k)
+    # load: same indices, models and query answers; the loaded object can run the fill loop
+    ml = zb.MultiIndex.load(path, img, known=kn)
+    assert ml.info.loaded == 1 and ml.n == mi.n and ml.dims == mi.dims
+    assert np.array_equal(ml.dictionary, mi.dictionary)
+    for l in range(8):
+        for f in ("mean", "components", "eigenvalues", "lo", "hi"):
+            assert np.array_equal(ml.layout(l)[f], mi.layout(l)[f])
+        a, b = mi.index_arrays(l), ml.index_arrays(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for tv, tk in _query_cases(img, kn, stride=7):
+        assert mi.query_best_patch(tv, tk) == ml.query_best_patch(tv, tk)
+    o1, r1, _ = mi.inpaint()
+    o2, r2, _ = ml.inpaint()
+    assert np.array_equal(o1, o2) and np.array_equal(r1["source_key"], r2["source_key"])
+
+
+def test_zidx1_load_resorts_and_rejects_bad_files(zb, golden, tmp_path):
+    import struct
+    tag = "eval_64x64_g_s90_m91"
+    img, kn = golden[tag + "__image"].squeeze(-1), golden[tag + "__known"]
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=6))
+    path = tmp_path / "a.zidx"
+    mi.save(path)
+    raw = bytearray(open(path, "rb").read())
+    # shuffle the entries of block 0: load re-sorts (io_index.cpp:120)
+    hdr = 5 + struct.calcsize("<IdIIQI")
+    k, cov, D, lid, n, ch = struct.unpack_from("<IdIIQI", raw, 5)
+    m = oracle.subset_layouts(k, cov)[0].shape[0] * ch
+    e0 = hdr + 8 * (m + D * m + 3 * D)
+    ent = np.frombuffer(bytes(raw[e0:e0 + n * (D + 8)]), np.uint8).reshape(n, D + 8)
+    perm = np.random.default_rng(0).permutation(n)
+    raw[e0:e0 + n * (D + 8)] = ent[perm].tobytes()
+    shuffled = tmp_path / "s.zidx"
+    open(shuffled, "wb").write(bytes(raw))
+    ml = zb.MultiIndex.load(shuffled, img)
+    a, b = mi.index_arrays(0), ml.index_arrays(0)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # bad magic, truncation, bad header -> runtime errors (std::runtime_error in the reference)
+    bad = tmp_path / "b.zidx"
+    open(bad, "wb").write(b"ZIDX2" + bytes(raw[5:]))
+    with pytest.raises(zb.ZIError):
+        zb.MultiIndex.load(bad, img)
+    open(bad, "wb").write(bytes(raw[: len(raw) - 7]))
+    with pytest.raises(zb.ZIError):
+        zb.MultiIndex.load(bad, img)
+    hb = bytearray(raw)
+    struct.pack_into("<I", hb, 5 + 4 + 8 + 4, 9)  # layout id 9
+    open(bad, "wb").write(bytes(hb))
+    with pytest.raises(zb.ZIError):
+        zb.MultiIndex.load(bad, img)
