@@ -182,6 +182,29 @@ zi_status zi_multi_index_layout_index(zi_multi_index* mi, int32_t layout, uint8_
                                       uint32_t* keys_out);
 /* borrowed view of one layout's zcurve_index (valid until mi is destroyed or rebuilt) */
 zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index** out);
+/* ---- cfg5: index over fp32 feature vectors (BASELINE.json configs[4]) ----
+ * The reference's patch-index semantics with every coordinate a pixel: PCA fit (pca.cpp:20-67,
+ * canonical fp64 order in 32768-row stripes), project + quantise (builder.cpp:55-72,159-187),
+ * from_descriptors keyed by row (bindings.cpp:109-125).  X: n x dim fp32, host memory; effective
+ * dims = min(dims, dim, n).  Queries: unknown coordinate (known[j] == 0) -> mean (make_query,
+ * builder.cpp:110-127), then the exact k-NN of zi_knn_search_batch. */
+typedef struct zi_vector_index zi_vector_index;
+zi_status zi_vector_index_build(zi_ctx* ctx, const float* X, uint64_t n, int32_t dim, int32_t dims,
+                                zi_vector_index** out);
+zi_status zi_vector_index_destroy(zi_vector_index* vi);
+/* dims after the clamp; mean (dim), components (dims rows of dim), eigenvalues, lo, hi (dims);
+ * NULL pointers are skipped; build_ms = device time of the build */
+zi_status zi_vector_index_model(zi_vector_index* vi, int32_t* dims, double* mean, double* components,
+                                double* eigenvalues, double* lo, double* hi, double* build_ms);
+/* borrowed view of the z-curve index (keys = row ids); valid until vi is destroyed */
+zi_status zi_vector_index_get_index(zi_vector_index* vi, zi_index** out);
+/* queries (nq x dim fp32 + nq x dim known flags) -> quantised descriptors (nq x dims) */
+zi_status zi_vector_make_queries(zi_vector_index* vi, const float* queries, const uint8_t* known, uint64_t nq,
+                                 uint8_t* descriptors_out);
+/* make_queries + exact k-NN: packed (dist<<32 | row) ascending, nq x k, counts[nq] */
+zi_status zi_vector_knn_batch(zi_vector_index* vi, const float* queries, const uint8_t* known, uint64_t nq,
+                              uint32_t k, int32_t norm, uint64_t* packed_out, uint32_t* counts_out);
+
 /* ZIDX1 persistence (io_index.hpp:21-22, io_index.cpp:133-154): eight blocks, layout 0 first,
  * "ZIDX1" | u32 K | f64 coverage | u32 D | u32 layout | u64 n | u32 C | mean | components (D
  * rows) | eigenvalues | lo | hi | n x (D bytes, u32 x, u32 y).  Load re-sorts each block on the

@@ -74,6 +74,10 @@ def lib():
         L.zo_layout_covariance.argtypes = [_i64p, _i64p, C.c_int, C.c_int64, _ip, C.c_int, _f64p, _f64p]
         L.zo_pca_from_cov.restype = C.c_int
         L.zo_pca_from_cov.argtypes = [_f64p, C.c_int, C.c_int, _f64p, _f64p]
+        _f32p = C.POINTER(C.c_float)
+        L.zo_vec_mean_cov.argtypes = [_f32p, C.c_int64, C.c_int, C.c_int64, _f64p, _f64p]
+        L.zo_vec_project.argtypes = [_f32p, C.c_int64, C.c_int, _f64p, _f64p, C.c_int, _f64p, _f64p, _u8p]
+        L.zo_vec_make_query.argtypes = [_f32p, _u8p, C.c_int, _f64p, _f64p, _f64p, _f64p, C.c_int, _u8p]
         L.zo_quantize.restype = C.c_uint8
         L.zo_quantize.argtypes = [C.c_double, C.c_double, C.c_double]
         L.zo_project_build.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, _u32p, C.c_int64, _ip, C.c_int,
@@ -397,3 +401,44 @@ def inpaint(img, known, K=9, coverage=0.6, dims=10, knn=80, norm=L2, brute_force
         raise RuntimeError(lib().zo_error().decode())
     arr = np.ctypeslib.as_array(recs)[:n].copy()
     return out, arr
+
+
+# ------------------------------------------------------------------ cfg5 vector index
+VEC_STRIPE = 32768  # canonical stripe of paper_1712_06326_b200/csrc/k_vector.cu
+
+
+def vec_mean_cov(X, stripe=VEC_STRIPE):
+    """Mean and covariance of fp32 rows in the device build's canonical fp64 order."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n, dim = X.shape
+    mean = np.zeros(dim)
+    cov = np.zeros((dim, dim))
+    lib().zo_vec_mean_cov(X.ctypes.data_as(C.POINTER(C.c_float)), n, dim, stripe, _p(mean, _f64p), _p(cov, _f64p))
+    return mean, cov
+
+
+def vec_project(X, mean, comp):
+    """(lo, hi, coords n x D) -- projection + quantiser of the vector index (canonical order)."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n, dim = X.shape
+    mean = np.ascontiguousarray(mean, dtype=np.float64)
+    comp = np.ascontiguousarray(comp, dtype=np.float64)
+    D = comp.shape[0]
+    lo, hi = np.zeros(D), np.zeros(D)
+    coords = np.zeros((n, D), dtype=np.uint8)
+    lib().zo_vec_project(X.ctypes.data_as(C.POINTER(C.c_float)), n, dim, _p(mean, _f64p), _p(comp, _f64p), D,
+                         _p(lo, _f64p), _p(hi, _f64p), _p(coords, _u8p))
+    return lo, hi, coords
+
+
+def vec_make_query(x, known, mean, comp, lo, hi):
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    known = _u8(known)
+    D = comp.shape[0]
+    out = np.zeros(D, dtype=np.uint8)
+    lib().zo_vec_make_query(x.ctypes.data_as(C.POINTER(C.c_float)), _p(known, _u8p), x.shape[0],
+                            _p(np.ascontiguousarray(mean, dtype=np.float64), _f64p),
+                            _p(np.ascontiguousarray(comp, dtype=np.float64), _f64p),
+                            _p(np.ascontiguousarray(lo, dtype=np.float64), _f64p),
+                            _p(np.ascontiguousarray(hi, dtype=np.float64), _f64p), D, _p(out, _u8p))
+    return out

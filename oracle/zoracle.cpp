@@ -749,3 +749,72 @@ int64_t zo_inpaint(const zo_mi* mi, const uint8_t* img0, const uint8_t* known0, 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- cfg5 vector index
+// Test infrastructure: the canonical order the device build (k_vector.cu) is pinned to.
+// proj/src/pca.cpp:20-37 (mean, covariance) restated with a fixed summation order.
+extern "C" void zo_vec_mean_cov(const float* X, int64_t n, int dim, int64_t stripe, double* mean, double* cov) {
+    std::vector<double> tot(dim, 0.0);
+    for (int64_t s0 = 0; s0 < n; s0 += stripe) {
+        const int64_t s1 = std::min<int64_t>(n, s0 + stripe);
+        for (int j = 0; j < dim; ++j) {
+            double s = 0.0;
+            for (int64_t r = s0; r < s1; ++r) s += static_cast<double>(X[r * dim + j]);
+            tot[j] += s;
+        }
+    }
+    for (int j = 0; j < dim; ++j) mean[j] = tot[j] / static_cast<double>(n);
+    std::vector<double> G(static_cast<size_t>(dim) * dim, 0.0), Gs(static_cast<size_t>(dim) * dim);
+    std::vector<double> xc(dim);
+    for (int64_t s0 = 0; s0 < n; s0 += stripe) {
+        const int64_t s1 = std::min<int64_t>(n, s0 + stripe);
+        std::fill(Gs.begin(), Gs.end(), 0.0);
+        for (int64_t r = s0; r < s1; ++r) {
+            for (int j = 0; j < dim; ++j) xc[j] = static_cast<double>(X[r * dim + j]) - mean[j];
+            for (int i = 0; i < dim; ++i)
+                for (int j = i; j < dim; ++j) Gs[static_cast<size_t>(i) * dim + j] = std::fma(xc[i], xc[j], Gs[static_cast<size_t>(i) * dim + j]);
+        }
+        for (size_t q = 0; q < G.size(); ++q) G[q] += Gs[q];
+    }
+    for (int i = 0; i < dim; ++i)
+        for (int j = i; j < dim; ++j) {
+            const double g = G[static_cast<size_t>(i) * dim + j];
+            const double v = n > 1 ? g / static_cast<double>(n - 1) : g;
+            cov[static_cast<size_t>(i) * dim + j] = v;
+            cov[static_cast<size_t>(j) * dim + i] = v;
+        }
+}
+
+// proj/src/pca.cpp:7-11 + builder.cpp:55-61,159-187 for vectors
+extern "C" void zo_vec_project(const float* X, int64_t n, int dim, const double* mean, const double* comp, int D,
+                               double* lo, double* hi, uint8_t* coords) {
+    std::vector<double> y(static_cast<size_t>(n) * D);
+    for (int d = 0; d < D; ++d) {
+        lo[d] = std::numeric_limits<double>::infinity();
+        hi[d] = -std::numeric_limits<double>::infinity();
+    }
+    for (int64_t r = 0; r < n; ++r)
+        for (int d = 0; d < D; ++d) {
+            double acc = 0.0;
+            for (int j = 0; j < dim; ++j)
+                acc = std::fma(comp[static_cast<size_t>(d) * dim + j], static_cast<double>(X[r * dim + j]) - mean[j], acc);
+            y[static_cast<size_t>(r) * D + d] = acc;
+            lo[d] = std::min(lo[d], acc);
+            hi[d] = std::max(hi[d], acc);
+        }
+    for (int64_t r = 0; r < n; ++r)
+        for (int d = 0; d < D; ++d) coords[r * D + d] = zo_quantize(lo[d], hi[d], y[static_cast<size_t>(r) * D + d]);
+}
+
+// proj/src/builder.cpp:110-127 for vectors: unknown coordinate -> mean
+extern "C" void zo_vec_make_query(const float* x, const uint8_t* known, int dim, const double* mean, const double* comp,
+                                  const double* lo, const double* hi, int D, uint8_t* out) {
+    for (int d = 0; d < D; ++d) {
+        double acc = 0.0;
+        for (int j = 0; j < dim; ++j) {
+            const double v = known[j] ? static_cast<double>(x[j]) : mean[j];
+            acc = std::fma(comp[static_cast<size_t>(d) * dim + j], v - mean[j], acc);
+        }
+        out[d] = zo_quantize(lo[d], hi[d], acc);
+    }
+}

@@ -132,6 +132,15 @@ int64_t zo_inpaint(const zo_mi* mi, const uint8_t* img, const uint8_t* known, in
                    int C, int K, int64_t knn, int norm, int brute_force, int oracle,
                    int64_t oracle_stride, uint8_t* img_out, zo_record* records, int64_t cap);
 
+/* cfg5 vector index, in the canonical fp64 order of paper_1712_06326_b200/csrc/k_vector.cu:
+ * column sums and the Gram as row-ordered chains inside stripes of `stripe` rows, stripe
+ * partials added in order; cov = G / (n - 1).  comp: D rows of dim (the reference's columns). */
+void zo_vec_mean_cov(const float* X, int64_t n, int dim, int64_t stripe, double* mean, double* cov);
+void zo_vec_project(const float* X, int64_t n, int dim, const double* mean, const double* comp, int D,
+                    double* lo, double* hi, uint8_t* coords);
+void zo_vec_make_query(const float* x, const uint8_t* known, int dim, const double* mean, const double* comp,
+                       const double* lo, const double* hi, int D, uint8_t* out);
+
 const char* zo_error(void);
 
 #ifdef __cplusplus

@@ -18,10 +18,10 @@ import numpy as np
 
 from . import _lib
 from ._lib import (BestPatch, EmptyDictionaryError, IndexConfig, InpaintConfig, IterationRecord, MultiIndexInfo,
-                   RunStats, ZIError, check, lib, ptr, u8p, u32p, u64p, i32p, i64p, f64p)
+                   RunStats, ZIError, check, lib, ptr, u8p, u32p, u64p, i32p, i64p, f64p, f32p)
 
 __all__ = ["inpaint", "knn_search", "subset_layouts", "morton_less", "less_most_significant_bit", "Context",
-           "ZCurveIndex", "MultiIndex", "EmptyDictionaryError", "ZIError", "index_config", "NORMS"]
+           "ZCurveIndex", "MultiIndex", "VectorIndex", "EmptyDictionaryError", "ZIError", "index_config", "NORMS"]
 
 NORMS = {"l2": 0, "l1": 1}
 
@@ -206,6 +206,61 @@ class ZCurveIndex:
         h = getattr(self, "h", None)
         if h and self._owner is None:
             lib().zi_index_destroy(h)
+        self.h = None
+
+
+# ------------------------------------------------------------------ cfg5 vector index
+class VectorIndex:
+    """Index over fp32 feature vectors (BASELINE configs[4]): PCA fit, projection, quantiser and
+    Morton sort on the device; rows are the keys (proj/python/bindings.cpp:109-125)."""
+
+    def __init__(self, X, dims: int, ctx: Optional[Context] = None):
+        self.ctx = ctx or Context.default()
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        if X.ndim != 2:
+            raise ValueError("X must be (n, dim) float32")
+        self.n, self.dim = X.shape
+        h = C.c_void_p()
+        check(lib().zi_vector_index_build(self.ctx.h, ptr(X, f32p), self.n, self.dim, dims, C.byref(h)))
+        self.h = h
+        d = C.c_int32()
+        bms = C.c_double()
+        check(lib().zi_vector_index_model(self.h, C.byref(d), None, None, None, None, None, C.byref(bms)))
+        self.dims, self.build_ms = d.value, bms.value
+
+    def model(self) -> dict:
+        D, dim = self.dims, self.dim
+        mean, comp, eig, lo, hi = np.zeros(dim), np.zeros((D, dim)), np.zeros(D), np.zeros(D), np.zeros(D)
+        check(lib().zi_vector_index_model(self.h, None, ptr(mean, f64p), ptr(comp, f64p), ptr(eig, f64p),
+                                          ptr(lo, f64p), ptr(hi, f64p), None))
+        return {"mean": mean, "components": comp, "eigenvalues": eig, "lo": lo, "hi": hi}
+
+    def index(self) -> "ZCurveIndex":
+        h = C.c_void_p()
+        check(lib().zi_vector_index_get_index(self.h, C.byref(h)))
+        return ZCurveIndex(h, owner=self, ctx=self.ctx)
+
+    def make_queries(self, Q, known) -> np.ndarray:
+        Q = np.ascontiguousarray(Q, dtype=np.float32)
+        kn = _u8(known)
+        out = np.zeros((Q.shape[0], self.dims), dtype=np.uint8)
+        check(lib().zi_vector_make_queries(self.h, ptr(Q, f32p), ptr(kn, u8p), Q.shape[0], ptr(out, u8p)))
+        return out
+
+    def knn(self, Q, known, k: int = 80, norm="l2"):
+        Q = np.ascontiguousarray(Q, dtype=np.float32)
+        kn = _u8(known)
+        nq = Q.shape[0]
+        out = np.zeros((nq, max(k, 1)), dtype=np.uint64)
+        cnt = np.zeros(nq, dtype=np.uint32)
+        check(lib().zi_vector_knn_batch(self.h, ptr(Q, f32p), ptr(kn, u8p), nq, k, _norm(norm), ptr(out, u64p),
+                                        ptr(cnt, u32p)))
+        return out, cnt
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().zi_vector_index_destroy(h)
         self.h = None
 
 

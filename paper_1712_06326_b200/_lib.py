@@ -12,6 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libzinpaint_b200.so")
 
 u8p = C.POINTER(C.c_uint8)
+f32p = C.POINTER(C.c_float)
 u32p = C.POINTER(C.c_uint32)
 u64p = C.POINTER(C.c_uint64)
 i32p = C.POINTER(C.c_int32)
@@ -89,6 +90,12 @@ SIGNATURES = {
     "zi_multi_index_build": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig),
                                        C.POINTER(vp)]),
     "zi_multi_index_rebuild": (C.c_int, [vp]),
+    "zi_vector_index_build": (C.c_int, [vp, f32p, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(vp)]),
+    "zi_vector_index_destroy": (C.c_int, [vp]),
+    "zi_vector_index_model": (C.c_int, [vp, i32p, f64p, f64p, f64p, f64p, f64p, f64p]),
+    "zi_vector_index_get_index": (C.c_int, [vp, C.POINTER(vp)]),
+    "zi_vector_make_queries": (C.c_int, [vp, f32p, u8p, C.c_uint64, u8p]),
+    "zi_vector_knn_batch": (C.c_int, [vp, f32p, u8p, C.c_uint64, C.c_uint32, C.c_int32, u64p, u32p]),
     "zi_multi_index_save": (C.c_int, [vp, C.c_char_p]),
     "zi_multi_index_load": (C.c_int, [vp, C.c_char_p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]),
     "zi_multi_index_destroy": (C.c_int, [vp]),

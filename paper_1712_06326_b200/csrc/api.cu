@@ -463,6 +463,104 @@ zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t*
     });
 }
 
+// ---------------------------------------------------------------- vector index (cfg5)
+zi_status zi_vector_index_build(zi_ctx* ctx, const float* X, uint64_t n, int32_t dim, int32_t dims,
+                                zi_vector_index** out) {
+    return guard(ctx, [&] {
+        require(ctx && X && out, "null argument");
+        require(n > 0, "vector index: empty input");
+        require(dim >= 3 && dim <= 224, "vector index: dim must be in [3, 224]");
+        require(dims >= 1 && dims <= 32, "vector index: dims must be in [1, 32]");
+        require(n < (1ull << 29), "vector index: more than 2^29 rows");
+        auto* vi = new zi_vector_index();
+        vi->ctx = ctx;
+        vi->n = n;
+        vi->dim = dim;
+        vi->dims = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(dims), std::min<uint64_t>(dim, n)));
+        try {
+            cudaEvent_t e0, e1;
+            ZI_CUDA(cudaEventCreate(&e0));
+            ZI_CUDA(cudaEventCreate(&e1));
+            vi->X.ensure(n * dim);
+            ZI_CUDA(cudaMemcpyAsync(vi->X.p, X, n * dim * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+            ZI_CUDA(cudaEventRecord(e0, ctx->stream));
+            zi::build_vector_index_device(vi);
+            ZI_CUDA(cudaEventRecord(e1, ctx->stream));
+            ZI_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            ZI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            vi->build_ms = ms;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        } catch (...) {
+            delete vi;
+            throw;
+        }
+        *out = vi;
+    });
+}
+
+zi_status zi_vector_index_destroy(zi_vector_index* vi) {
+    return guard(vi ? vi->ctx : nullptr, [&] { delete vi; });
+}
+
+zi_status zi_vector_index_model(zi_vector_index* vi, int32_t* dims, double* mean, double* components,
+                                double* eigenvalues, double* lo, double* hi, double* build_ms) {
+    return guard(vi ? vi->ctx : nullptr, [&] {
+        require(vi != nullptr, "null argument");
+        zi::vector_sync_host_model(vi);
+        if (dims) *dims = vi->dims;
+        if (mean) std::memcpy(mean, vi->h_mean.data(), vi->h_mean.size() * sizeof(double));
+        if (components) std::memcpy(components, vi->h_comp.data(), vi->h_comp.size() * sizeof(double));
+        if (eigenvalues) std::memcpy(eigenvalues, vi->h_eig.data(), vi->h_eig.size() * sizeof(double));
+        if (lo) std::memcpy(lo, vi->h_lo.data(), vi->h_lo.size() * sizeof(double));
+        if (hi) std::memcpy(hi, vi->h_hi.data(), vi->h_hi.size() * sizeof(double));
+        if (build_ms) *build_ms = vi->build_ms;
+    });
+}
+
+zi_status zi_vector_index_get_index(zi_vector_index* vi, zi_index** out) {
+    return guard(vi ? vi->ctx : nullptr, [&] {
+        require(vi && out, "null argument");
+        *out = &vi->index;
+    });
+}
+
+static uint8_t* vector_queries_to_device(zi_vector_index* vi, const float* Q, const uint8_t* known, uint64_t nq) {
+    zi_ctx* ctx = vi->ctx;
+    const size_t qb = nq * vi->dim * sizeof(float), kb = nq * vi->dim, ob = nq * vi->dims;
+    uint8_t* b = vi->qbuf.ensure(qb + kb + ob + 64);
+    ZI_CUDA(cudaMemcpyAsync(b, Q, qb, cudaMemcpyHostToDevice, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(b + qb, known, kb, cudaMemcpyHostToDevice, ctx->stream));
+    zi::vector_make_queries(vi, reinterpret_cast<const float*>(b), b + qb, nq, b + qb + kb);
+    return b + qb + kb;
+}
+
+zi_status zi_vector_make_queries(zi_vector_index* vi, const float* queries, const uint8_t* known, uint64_t nq,
+                                 uint8_t* descriptors_out) {
+    return guard(vi ? vi->ctx : nullptr, [&] {
+        require(vi && (nq == 0 || (queries && known && descriptors_out)), "null argument");
+        if (nq == 0) return;
+        const uint8_t* d = vector_queries_to_device(vi, queries, known, nq);
+        ZI_CUDA(cudaMemcpyAsync(descriptors_out, d, nq * vi->dims, cudaMemcpyDeviceToHost, vi->ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(vi->ctx->stream));
+    });
+}
+
+zi_status zi_vector_knn_batch(zi_vector_index* vi, const float* queries, const uint8_t* known, uint64_t nq,
+                              uint32_t k, int32_t norm, uint64_t* packed_out, uint32_t* counts_out) {
+    return guard(vi ? vi->ctx : nullptr, [&] {
+        require(vi && (nq == 0 || (queries && known && packed_out && counts_out)), "null argument");
+        require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
+        if (nq == 0) return;
+        const uint8_t* d = vector_queries_to_device(vi, queries, known, nq);
+        std::vector<uint8_t> h(nq * vi->dims);
+        ZI_CUDA(cudaMemcpyAsync(h.data(), d, h.size(), cudaMemcpyDeviceToHost, vi->ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(vi->ctx->stream));
+        zi::knn_search_batch(&vi->index, h.data(), nq, k, norm, packed_out, counts_out);
+    });
+}
+
 zi_status zi_multi_index_save(zi_multi_index* mi, const char* path) {
     return guard(mi ? mi->ctx : nullptr, [&] {
         require(mi && path, "null argument");

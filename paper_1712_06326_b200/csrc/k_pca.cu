@@ -265,11 +265,12 @@ struct tri_args {
     double* mean;  // 8 * mc
     pca_work_view w;
     long long* dbg;  // optional per-phase clock totals (ZI_DEBUG_PCA)
+    const double* cov;  // optional: precomputed covariance per model (mc x mc, row-major); the
+                        // moments, cols and mean are then unused
 };
 
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca_tri(tri_args a) {
     extern __shared__ double sm[];
-    __shared__ double s_red[kTriThreads / 32];
     cg::cluster_group cl = cg::this_cluster();
     const int n = a.mc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int kWarps = kTriThreads / 32;
@@ -288,6 +289,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
     const double den = a.n > 1 ? static_cast<double>(a.n) * static_cast<double>(a.n - 1) : 1.0;
     for (int idx = tid; idx < nloc * n; idx += kTriThreads) {
         const int li = idx / n, j = idx - li * n, i = rank + kCl * li;
+        if (a.cov) {
+            A[idx] = a.cov[(static_cast<size_t>(l) * n + i) * n + j];
+            continue;
+        }
         int ca = cols[i], cb = cols[j];
         if (ca / 128 > cb / 128) {  // k_moments fills the 128x128 tile pairs ti <= tj only
             const int t = ca;
@@ -298,7 +303,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
                              static_cast<__int128>(s[cols[i]]) * s[cols[j]];
         A[idx] = i128_to_double(num) / den;
     }
-    if (rank == 0)
+    if (rank == 0 && !a.cov)
         for (int i = tid; i < n; i += kTriThreads)
             a.mean[l * n + i] = static_cast<double>(s[cols[i]]) / static_cast<double>(a.n);
     double* d_out = a.w.d + l * n;
@@ -707,8 +712,23 @@ __global__ void __launch_bounds__(256) k_pca_fin(fin_args a) {
     }
 }
 
+static bool pca_launch(zi_ctx* ctx, int nl, const double* d_cov, const unsigned long long* d_moments, int F, uint64_t n,
+                       const int32_t* d_cols, int mc, int D, double* d_mean, double* d_comp, double* d_eig,
+                       double* d_work);
+
 bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint64_t n, const int32_t* d_cols, int mc,
                    int D, double* d_mean, double* d_comp, double* d_eig, double* d_work, int* /*d_status*/) {
+    return pca_launch(ctx, 8, nullptr, d_moments, F, n, d_cols, mc, D, d_mean, d_comp, d_eig, d_work);
+}
+
+bool pca_from_cov_on_device(zi_ctx* ctx, const double* d_cov, int mc, int D, double* d_comp, double* d_eig,
+                            double* d_work) {
+    return pca_launch(ctx, 1, d_cov, nullptr, 0, 0, nullptr, mc, D, nullptr, d_comp, d_eig, d_work);
+}
+
+static bool pca_launch(zi_ctx* ctx, int nl, const double* d_cov, const unsigned long long* d_moments, int F, uint64_t n,
+                       const int32_t* d_cols, int mc, int D, double* d_mean, double* d_comp, double* d_eig,
+                       double* d_work) {
     if (mc > kPcaMaxN || D > 32 || mc < 3) return false;
     static int optin = -1;
     if (optin < 0) ZI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
@@ -733,14 +753,14 @@ bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint
         attr_fin = smem_fin;
     }
     const pca_work_view w = pca_work_split(d_work, mc, D);
-    tri_args ta{d_moments, F, n, d_cols, mc, d_mean, w, nullptr};
+    tri_args ta{d_moments, F, n, d_cols, mc, d_mean, w, nullptr, d_cov};
     static const bool debug = std::getenv("ZI_DEBUG_PCA") != nullptr;
     static dbuf<long long> dbg;
     if (debug) {
         ta.dbg = dbg.ensure(8 * kCl * 8);
         ZI_CUDA(cudaMemsetAsync(ta.dbg, 0, 8 * kCl * 8 * sizeof(long long), ctx->stream));
     }
-    ZI_LAUNCH(ctx, "pca_tridiag", k_pca_tri, 8 * kCl, kTriThreads, smem_tri, ta);
+    ZI_LAUNCH(ctx, "pca_tridiag", k_pca_tri, nl * kCl, kTriThreads, smem_tri, ta);
     if (debug) {
         long long h[8 * kCl * 8];
         ZI_CUDA(cudaMemcpyAsync(h, ta.dbg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
@@ -752,7 +772,7 @@ bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint
     vec_args va{mc, D, w, nullptr};
     static dbuf<long long> vdbg;
     if (debug) va.dbg = vdbg.ensure(8 * 32 * 4);
-    ZI_LAUNCH(ctx, "pca_vectors", k_pca_vec, 8 * D, kVecThreads, smem_vec, va);
+    ZI_LAUNCH(ctx, "pca_vectors", k_pca_vec, nl * D, kVecThreads, smem_vec, va);
     if (debug) {
         std::vector<long long> h(static_cast<size_t>(8) * D * 4);
         ZI_CUDA(cudaMemcpyAsync(h.data(), va.dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
@@ -762,7 +782,7 @@ bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint
                          h[c * 4 + 2]);
     }
     fin_args fa{mc, D, w, d_comp, d_eig};
-    ZI_LAUNCH(ctx, "pca_finish", k_pca_fin, 8, 256, smem_fin, fa);
+    ZI_LAUNCH(ctx, "pca_finish", k_pca_fin, nl, 256, smem_fin, fa);
     return true;
 }
 

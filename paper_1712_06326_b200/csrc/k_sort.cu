@@ -663,6 +663,14 @@ void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int
     radix_sort_words(ctx, words, W + 1, n, passes, nullptr, false);
 }
 
+void morton_sort_rows(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D) {
+    const int W = (D + 3) / 4;
+    uint32_t* words[kMaxWords];
+    for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * n;
+    words[W] = d_val;
+    morton_sort_hybrid(ctx, words, W, n, D, false);
+}
+
 void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D) {
     const int W = (D + 3) / 4;
     uint32_t* words[kMaxWords];

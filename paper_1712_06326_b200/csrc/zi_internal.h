@@ -177,6 +177,22 @@ struct zi_multi_index {
     zi_layout_state L[8];
 };
 
+// cfg5: z-curve index over fp32 feature vectors (k_vector.cu)
+struct zi_vector_index {
+    zi_ctx* ctx = nullptr;
+    uint64_t n = 0;
+    int dim = 0, dims = 0;
+    zi::dbuf<float> X;                  // n x dim, device resident
+    zi::dbuf<double> mean, cov, comp, eig, pca_work, Y, scratch;
+    zi::dbuf<unsigned long long> minmax;
+    zi::dbuf<uint32_t> recs;
+    zi::dbuf<uint8_t> qbuf;             // query staging
+    zi_index index;
+    bool host_model = false;
+    std::vector<double> h_mean, h_comp, h_eig, h_lo, h_hi;
+    double build_ms = 0.0;
+};
+
 namespace zi {
 
 // ---- kernel entry points (implemented in the .cu files) ----
@@ -255,8 +271,19 @@ void finish_build_timing(zi_multi_index* mi);
 // k_pca.cu: covariance + eigen-solve of all 8 layouts on the device; false if mc is too large.
 // d_work must hold pca_work_doubles(mc, D) doubles.
 size_t pca_work_doubles(int mc, int D);
+// one model from a precomputed covariance (mc x mc, row-major, device): comp [j][d], eig [D]
+bool pca_from_cov_on_device(zi_ctx* ctx, const double* d_cov, int mc, int D, double* d_comp, double* d_eig,
+                            double* d_work);
 bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint64_t n, const int32_t* d_cols, int mc,
                    int D, double* d_mean, double* d_comp, double* d_eig, double* d_work, int* d_status);
+
+// vector index (k_vector.cu): upload + build, device-resident build, queries, host mirrors
+void vector_index_build(zi_vector_index* vi, const float* h_X);
+void build_vector_index_device(zi_vector_index* vi);
+void vector_make_queries(zi_vector_index* vi, const float* d_Q, const uint8_t* d_known, uint64_t nq, uint8_t* d_out);
+void vector_sync_host_model(zi_vector_index* vi);
+// hybrid Morton sort of a single index (payload = row id, ties by row) -- k_sort.cu
+void morton_sort_rows(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D);
 
 // ZIDX1 persistence (persist.cpp, proj/src/io_index.cpp)
 struct zidx_header {

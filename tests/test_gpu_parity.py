@@ -583,3 +583,39 @@ def test_zidx1_load_resorts_and_rejects_bad_files(zb, golden, tmp_path):
     open(bad, "wb").write(bytes(hb))
     with pytest.raises(zb.ZIError):
         zb.MultiIndex.load(bad, img)
+
+
+# ------------------------------------------------------------------ cfg5 vector index
+@pytest.mark.parametrize("n,dim,D", [(40000, 125, 8), (5000, 13, 16), (33000, 125, 16)])
+def test_vector_index_vs_oracle(zb, n, dim, D):
+    """Mean / covariance bit-exact in the canonical stripe order (FP64 MMA chains == sequential
+    fma); PCA by tolerance; projection, quantiser, sort, make_query and k-NN bit-exact with the
+    device PCA injected into the oracle."""
+    X = workloads.cfg5_points(n, dims_in=dim, seed=n + dim)
+    vi = zb.VectorIndex(X, D)
+    assert vi.dims == min(D, dim, n)
+    mod = vi.model()
+    mean, cov = oracle.vec_mean_cov(X)
+    assert np.array_equal(mod["mean"], mean)
+    comp, eig = oracle.pca_from_cov(cov, vi.dims)
+    np.testing.assert_allclose(mod["eigenvalues"], eig, rtol=1e-9, atol=1e-9 * eig[0])
+    Cm = mod["components"]
+    np.testing.assert_allclose(Cm @ Cm.T, np.eye(vi.dims), atol=1e-10)
+    res = cov @ Cm.T - Cm.T * mod["eigenvalues"]
+    assert np.abs(res).max() <= 1e-9 * max(1.0, eig[0])
+    lo, hi, coords = oracle.vec_project(X, mod["mean"], Cm)
+    assert np.array_equal(lo, mod["lo"]) and np.array_equal(hi, mod["hi"])
+    rows = np.arange(n, dtype=np.uint32)
+    rc, rk = oracle.from_descriptors(coords, rows)
+    c, k = vi.index().export()
+    assert np.array_equal(c, rc) and np.array_equal(k, rk)
+    rng = np.random.default_rng(7)
+    Q = workloads.cfg5_points(32, dims_in=dim, seed=99)
+    known = (rng.random(Q.shape) >= 0.4).astype(np.uint8)
+    qd = vi.make_queries(Q, known)
+    for i in range(Q.shape[0]):
+        assert np.array_equal(qd[i], oracle.vec_make_query(Q[i], known[i], mod["mean"], Cm, lo, hi))
+    out, cnt = vi.knn(Q, known, k=80)
+    for i in range(0, 32, 5):
+        ref = oracle.knn_linear(rc, rk, qd[i], 80)
+        assert cnt[i] == ref.size and np.array_equal(out[i, :cnt[i]], ref)
