@@ -191,6 +191,9 @@ zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index*
 typedef struct zi_vector_index zi_vector_index;
 zi_status zi_vector_index_build(zi_ctx* ctx, const float* X, uint64_t n, int32_t dim, int32_t dims,
                                 zi_vector_index** out);
+/* same, rows already in device memory (read during the build only; not retained) */
+zi_status zi_vector_index_build_device(zi_ctx* ctx, const float* d_X, uint64_t n, int32_t dim, int32_t dims,
+                                       zi_vector_index** out);
 zi_status zi_vector_index_destroy(zi_vector_index* vi);
 /* dims after the clamp; mean (dim), components (dims rows of dim), eigenvalues, lo, hi (dims);
  * NULL pointers are skipped; build_ms = device time of the build */

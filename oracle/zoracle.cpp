@@ -755,12 +755,18 @@ int64_t zo_inpaint(const zo_mi* mi, const uint8_t* img0, const uint8_t* known0, 
 // proj/src/pca.cpp:20-37 (mean, covariance) restated with a fixed summation order.
 extern "C" void zo_vec_mean_cov(const float* X, int64_t n, int dim, int64_t stripe, double* mean, double* cov) {
     std::vector<double> tot(dim, 0.0);
+    const int64_t sub = 4096;  // stripe sums add their 4096-row sub-chunk sums in order
     for (int64_t s0 = 0; s0 < n; s0 += stripe) {
         const int64_t s1 = std::min<int64_t>(n, s0 + stripe);
         for (int j = 0; j < dim; ++j) {
-            double s = 0.0;
-            for (int64_t r = s0; r < s1; ++r) s += static_cast<double>(X[r * dim + j]);
-            tot[j] += s;
+            double st = 0.0;
+            for (int64_t u0 = s0; u0 < s1; u0 += sub) {
+                const int64_t u1 = std::min<int64_t>(s1, u0 + sub);
+                double s = 0.0;
+                for (int64_t r = u0; r < u1; ++r) s += static_cast<double>(X[r * dim + j]);
+                st += s;
+            }
+            tot[j] += st;
         }
     }
     for (int j = 0; j < dim; ++j) mean[j] = tot[j] / static_cast<double>(n);

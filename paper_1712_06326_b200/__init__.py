@@ -215,13 +215,21 @@ class VectorIndex:
     Morton sort on the device; rows are the keys (proj/python/bindings.cpp:109-125)."""
 
     def __init__(self, X, dims: int, ctx: Optional[Context] = None):
+        """X: (n, dim) float32 -- a numpy array, or a CUDA tensor (built from device memory)."""
         self.ctx = ctx or Context.default()
-        X = np.ascontiguousarray(X, dtype=np.float32)
-        if X.ndim != 2:
-            raise ValueError("X must be (n, dim) float32")
-        self.n, self.dim = X.shape
         h = C.c_void_p()
-        check(lib().zi_vector_index_build(self.ctx.h, ptr(X, f32p), self.n, self.dim, dims, C.byref(h)))
+        if hasattr(X, "is_cuda") and X.is_cuda:
+            if X.dtype.__str__() != "torch.float32" or X.dim() != 2 or not X.is_contiguous():
+                raise ValueError("X must be a contiguous (n, dim) float32 tensor")
+            self.n, self.dim = int(X.shape[0]), int(X.shape[1])
+            check(lib().zi_vector_index_build_device(self.ctx.h, C.c_void_p(X.data_ptr()), self.n, self.dim, dims,
+                                                     C.byref(h)))
+        else:
+            X = np.ascontiguousarray(X, dtype=np.float32)
+            if X.ndim != 2:
+                raise ValueError("X must be (n, dim) float32")
+            self.n, self.dim = X.shape
+            check(lib().zi_vector_index_build(self.ctx.h, ptr(X, f32p), self.n, self.dim, dims, C.byref(h)))
         self.h = h
         d = C.c_int32()
         bms = C.c_double()
@@ -259,8 +267,11 @@ class VectorIndex:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h:
-            lib().zi_vector_index_destroy(h)
+        try:
+            if h:
+                lib().zi_vector_index_destroy(h)
+        except TypeError:  # interpreter shutdown
+            pass
         self.h = None
 
 

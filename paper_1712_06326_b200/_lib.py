@@ -91,6 +91,7 @@ SIGNATURES = {
                                        C.POINTER(vp)]),
     "zi_multi_index_rebuild": (C.c_int, [vp]),
     "zi_vector_index_build": (C.c_int, [vp, f32p, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(vp)]),
+    "zi_vector_index_build_device": (C.c_int, [vp, vp, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(vp)]),
     "zi_vector_index_destroy": (C.c_int, [vp]),
     "zi_vector_index_model": (C.c_int, [vp, i32p, f64p, f64p, f64p, f64p, f64p, f64p]),
     "zi_vector_index_get_index": (C.c_int, [vp, C.POINTER(vp)]),

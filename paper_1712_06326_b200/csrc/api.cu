@@ -464,8 +464,8 @@ zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t*
 }
 
 // ---------------------------------------------------------------- vector index (cfg5)
-zi_status zi_vector_index_build(zi_ctx* ctx, const float* X, uint64_t n, int32_t dim, int32_t dims,
-                                zi_vector_index** out) {
+static zi_status vector_build(zi_ctx* ctx, const float* X, bool device_rows, uint64_t n, int32_t dim, int32_t dims,
+                              zi_vector_index** out) {
     return guard(ctx, [&] {
         require(ctx && X && out, "null argument");
         require(n > 0, "vector index: empty input");
@@ -481,8 +481,13 @@ zi_status zi_vector_index_build(zi_ctx* ctx, const float* X, uint64_t n, int32_t
             cudaEvent_t e0, e1;
             ZI_CUDA(cudaEventCreate(&e0));
             ZI_CUDA(cudaEventCreate(&e1));
-            vi->X.ensure(n * dim);
-            ZI_CUDA(cudaMemcpyAsync(vi->X.p, X, n * dim * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+            if (device_rows) {
+                vi->Xd = X;  // caller's device buffer: must outlive the build only
+            } else {
+                vi->X.ensure(n * dim);
+                ZI_CUDA(cudaMemcpyAsync(vi->X.p, X, n * dim * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+                vi->Xd = vi->X.p;
+            }
             ZI_CUDA(cudaEventRecord(e0, ctx->stream));
             zi::build_vector_index_device(vi);
             ZI_CUDA(cudaEventRecord(e1, ctx->stream));
@@ -498,6 +503,16 @@ zi_status zi_vector_index_build(zi_ctx* ctx, const float* X, uint64_t n, int32_t
         }
         *out = vi;
     });
+}
+
+zi_status zi_vector_index_build(zi_ctx* ctx, const float* X, uint64_t n, int32_t dim, int32_t dims,
+                                zi_vector_index** out) {
+    return vector_build(ctx, X, false, n, dim, dims, out);
+}
+
+zi_status zi_vector_index_build_device(zi_ctx* ctx, const float* d_X, uint64_t n, int32_t dim, int32_t dims,
+                                       zi_vector_index** out) {
+    return vector_build(ctx, d_X, true, n, dim, dims, out);
 }
 
 zi_status zi_vector_index_destroy(zi_vector_index* vi) {

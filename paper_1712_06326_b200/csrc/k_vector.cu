@@ -6,8 +6,8 @@
 // (proj/src/builder.cpp:110-127), knn_search.
 //
 // Canonical fp64 order (pinned in oracle/zoracle.cpp zo_vec_*; Eigen's order is unpinned):
-//   * rows are processed in stripes of kStripe = 32768; mean_j = (sum over stripes, in order, of
-//     the stripe's row-ordered column sum) / n;
+//   * rows are processed in stripes of kStripe = 32768; a stripe's column sum adds, in order, the
+//     row-ordered sums of its 4096-row sub-chunks; mean_j = (stripe sums added in order) / n;
 //   * Gram G = sum over stripes (in order) of the stripe's row-ordered fma chain of
 //     xc_i * xc_j (xc = (double)x - mean); cov = G / (n - 1);  the per-stripe chains run on the
 //     FP64 tensor cores (mma.m8n8k4.f64 == four sequential fma's in k order);
@@ -32,15 +32,39 @@ __device__ inline void dmma(double& d0, double& d1, double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-// per-stripe column sums, row order: part[s * dim + j]
-__global__ void __launch_bounds__(256) k_vec_colsum(const float* __restrict__ X, uint64_t n, int dim,
-                                                    double* __restrict__ part) {
+// per-stripe column sums: row-ordered sums of kSub-row sub-chunks, added in sub-chunk order
+// (the canonical order: oracle zo_vec_mean_cov).  Thread (sub-chunk u, column j); part[s * dim + j]
+constexpr int kSub = 4096;
+constexpr int kSubs = kStripe / kSub;  // 8
+__global__ void __launch_bounds__(1024) k_vec_colsum(const float* __restrict__ X, uint64_t n, int dim,
+                                                     double* __restrict__ part) {
+    __shared__ double s_sub[kSubs][128];
     const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kStripe;
-    const uint64_t r1 = r0 + kStripe < n ? r0 + kStripe : n;
-    for (int j = threadIdx.x; j < dim; j += blockDim.x) {
-        double s = 0.0;
-        for (uint64_t r = r0; r < r1; ++r) s = __dadd_rn(s, static_cast<double>(__ldg(X + r * dim + j)));
-        part[static_cast<size_t>(blockIdx.x) * dim + j] = s;
+    for (int j0 = 0; j0 < dim; j0 += 128) {
+        const int u = threadIdx.x / 128, j = j0 + threadIdx.x % 128;
+        if (j < dim) {
+            const uint64_t a = r0 + static_cast<uint64_t>(u) * kSub;
+            const uint64_t lim = r0 + kStripe < n ? r0 + kStripe : n;
+            const uint64_t e = a + kSub < lim ? a + kSub : lim;
+            double s = 0.0;
+            uint64_t r = a;
+            for (; r + 8 <= e; r += 8) {  // 8 loads in flight, then the row-ordered adds
+                float v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = __ldg(X + (r + q) * dim + j);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s = __dadd_rn(s, static_cast<double>(v[q]));
+            }
+            for (; r < e; ++r) s = __dadd_rn(s, static_cast<double>(__ldg(X + r * dim + j)));
+            s_sub[u][threadIdx.x % 128] = s;  // a sub-chunk past the end sums to +0.0
+        }
+        __syncthreads();
+        if (threadIdx.x < 128 && j0 + static_cast<int>(threadIdx.x) < dim) {
+            double t = 0.0;
+            for (int q = 0; q < kSubs; ++q) t = __dadd_rn(t, s_sub[q][threadIdx.x]);
+            part[static_cast<size_t>(blockIdx.x) * dim + j0 + threadIdx.x] = t;
+        }
+        __syncthreads();
     }
 }
 
@@ -52,61 +76,89 @@ __global__ void k_vec_mean(const double* __restrict__ part, int nstripe, int dim
     mean[j] = __ddiv_rn(s, static_cast<double>(n));
 }
 
+__device__ inline void cp_async16_v(void* dst, const void* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+
 // Per-stripe Gram tiles (ti <= tj, 8x8) on the FP64 tensor cores: k = data rows in order.
-// part[(s * ntiles + tile) * 64 + r * 8 + c] = G_s[8 ti + r][8 tj + c]
-__global__ void __launch_bounds__(kGramThreads) k_vec_gram(const float* __restrict__ X, uint64_t n, int dim, int Pd,
-                                                           const double* __restrict__ mean, int ntiles,
+// part[(s * ntiles + tile) * 64 + r * 8 + c] = G_s[8 ti + r][8 tj + c].
+// Rounds of kGramRows rows: the raw fp32 rows of round b+1 stream in with cp.async (one
+// contiguous 16-byte-aligned block) while round b's k-steps run; each round is converted once
+// to xc = (double)x - mean in shared memory (fp64, 32-byte row skew: conflict-free fragments).
+template <int PW>
+__global__ void __launch_bounds__(kGramThreads, 2) k_vec_gram(const float* __restrict__ X, uint64_t n, int dim, int Pd,
+                                                           const double* __restrict__ mean, int ntiles, int tiles_per_cta,
                                                            double* __restrict__ part) {
-    extern __shared__ double s_x[];  // kGramRows x (Pd + 4)
-    const int ld = Pd + 4;           // 32-byte row skew: the 4 fragment rows hit different banks
+    extern __shared__ __align__(16) double s_x[];  // kGramRows x (Pd + 4) fp64, then 2 raw fp32 rounds
+    const int ld = Pd + 4;
+    float* s_raw = reinterpret_cast<float*>(s_x + kGramRows * ld);
+    const int raw_words = ((kGramRows * dim + 3) / 4) * 4;  // per buffer, 16-byte multiple
     const int T = Pd / 8;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = lane >> 2, c = lane & 3;
     const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kStripe;
     const uint64_t r1 = r0 + kStripe < n ? r0 + kStripe : n;
-    const int t0 = blockIdx.y * kGramTilesPerCta;
-    const int t1 = min(ntiles, t0 + kGramTilesPerCta);
-    constexpr int kPerWarp = kGramTilesPerCta / (kGramThreads / 32);
-    int ti[kPerWarp], tj[kPerWarp];
-    double acc[kPerWarp][2];
+    const int t0 = blockIdx.y * tiles_per_cta;
+    const int t1 = min(ntiles, t0 + tiles_per_cta);
+    int offA[PW], offB[PW];
+    double acc[PW][2];
+    int nq = 0;
 #pragma unroll
-    for (int q = 0; q < kPerWarp; ++q) {
+    for (int q = 0; q < PW; ++q) {
         const int t = t0 + warp + 8 * q;
-        // tile index -> (ti, tj), ti <= tj, row-major over the upper triangle
-        int a = 0, rem = t;
+        int a = 0, rem = t;  // tile index -> (ti, tj), ti <= tj, row-major over the upper triangle
         while (a < T && rem >= T - a) {
             rem -= T - a;
             ++a;
         }
-        ti[q] = t < t1 ? a : -1;
-        tj[q] = t < t1 ? a + rem : -1;
+        offA[q] = c * ld + a * 8 + r;          // A[i][k] = xc[row k][feature 8 ti + r]
+        offB[q] = c * ld + (a + rem) * 8 + r;  // B[k][j] = xc[row k][feature 8 tj + r]
         acc[q][0] = acc[q][1] = 0.0;
+        if (t < t1) nq = q + 1;
     }
-    for (uint64_t b = r0; b < r1; b += kGramRows) {
-        __syncthreads();
+    // round b -> raw buffer (b / kGramRows) & 1; a round is rows [b, b + kGramRows) of the stripe
+    auto issue = [&](uint64_t b, int buf) {
+        const uint64_t rows = b + kGramRows <= r1 ? kGramRows : r1 - b;
+        const uint64_t words = rows * dim;                 // contiguous fp32 words
+        const float* src = X + b * dim;                    // b * dim * 4 is a 16-byte multiple (kGramRows * 4 | 16)
+        float* dst = s_raw + buf * raw_words;
+        const uint64_t full = words / 4;
+        for (uint64_t e = tid; e < full; e += kGramThreads) cp_async16_v(dst + 4 * e, src + 4 * e);
+        for (uint64_t e = full * 4 + tid; e < words; e += kGramThreads) dst[e] = __ldg(src + e);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    issue(r0, 0);
+    int buf = 0;
+    for (uint64_t b = r0; b < r1; b += kGramRows, buf ^= 1) {
+        if (b + kGramRows < r1) {
+            issue(b + kGramRows, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();  // round b landed; the previous round's k-steps are done
+        const float* raw = s_raw + buf * raw_words;
+        const uint64_t rows = b + kGramRows <= r1 ? kGramRows : r1 - b;
         for (int e = tid; e < kGramRows * Pd; e += kGramThreads) {
             const int rr = e / Pd, j = e - rr * Pd;
-            const uint64_t row = b + rr;
-            double v = 0.0;  // rows past the stripe / columns past dim contribute exact zeros
-            if (row < r1 && j < dim) v = __dsub_rn(static_cast<double>(__ldg(X + row * dim + j)), mean[j]);
-            s_x[rr * ld + j] = v;
+            // rows past the stripe / columns past dim contribute exact zeros
+            s_x[rr * ld + j] = (rr < static_cast<int>(rows) && j < dim)
+                                   ? __dsub_rn(static_cast<double>(raw[rr * dim + j]), mean[j])
+                                   : 0.0;
         }
         __syncthreads();
-#pragma unroll
+#pragma unroll 1
         for (int ks = 0; ks < kGramRows / 4; ++ks) {
             const double* xr = s_x + (ks * 4) * ld;
 #pragma unroll
-            for (int q = 0; q < kPerWarp; ++q) {
-                if (ti[q] < 0) continue;
-                const double av = xr[c * ld + ti[q] * 8 + r];  // A[i][k] = xc[row k][feature i]
-                const double bv = xr[c * ld + tj[q] * 8 + r];  // B[k][j] = xc[row k][feature j]
-                dmma(acc[q][0], acc[q][1], av, bv);
-            }
+            for (int q = 0; q < PW; ++q)
+                if (q < nq) dmma(acc[q][0], acc[q][1], xr[offA[q]], xr[offB[q]]);
         }
     }
 #pragma unroll
-    for (int q = 0; q < kPerWarp; ++q) {
-        if (ti[q] < 0) continue;
+    for (int q = 0; q < PW; ++q) {
+        if (q >= nq) continue;
         const int t = t0 + warp + 8 * q;
         double* o = part + (static_cast<size_t>(blockIdx.x) * ntiles + t) * 64 + r * 8 + 2 * c;
         o[0] = acc[q][0];
@@ -264,6 +316,7 @@ void vector_index_build(zi_vector_index* vi, const float* h_X) {
     const int dim = vi->dim;
     vi->X.ensure(n * dim);
     ZI_CUDA(cudaMemcpyAsync(vi->X.p, h_X, n * dim * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    vi->Xd = vi->X.p;
     build_vector_index_device(vi);
 }
 
@@ -271,24 +324,40 @@ void build_vector_index_device(zi_vector_index* vi) {
     zi_ctx* ctx = vi->ctx;
     const uint64_t n = vi->n;
     const int dim = vi->dim, D = vi->dims;
-    const float* X = vi->X.p;
+    const float* X = vi->Xd;
     const int nstripe = static_cast<int>((n + kStripe - 1) / kStripe);
     // mean
     vi->mean.ensure(dim);
     dbuf<double>& part = vi->scratch;
     const int Pd = (dim + 7) / 8 * 8, T = Pd / 8, ntiles = T * (T + 1) / 2;
     part.ensure(std::max<size_t>(static_cast<size_t>(nstripe) * dim, static_cast<size_t>(nstripe) * ntiles * 64));
-    ZI_LAUNCH(ctx, "vec_colsum", k_vec_colsum, nstripe, std::min(256, (dim + 31) / 32 * 32), 0, X, n, dim, part.p);
+    ZI_LAUNCH(ctx, "vec_colsum", k_vec_colsum, nstripe, 1024, 0, X, n, dim, part.p);
     ZI_LAUNCH(ctx, "vec_mean", k_vec_mean, (dim + 127) / 128, 128, 0, part.p, nstripe, dim, n, vi->mean.p);
     // covariance
-    const size_t gsmem = static_cast<size_t>(kGramRows) * (Pd + 4) * sizeof(double);
-    static size_t gattr = 0;
-    if (gsmem > gattr) {
-        ZI_CUDA(cudaFuncSetAttribute(k_vec_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
-        gattr = gsmem;
+    const size_t raw_words = ((static_cast<size_t>(kGramRows) * dim + 3) / 4) * 4;
+    const size_t gsmem = static_cast<size_t>(kGramRows) * (Pd + 4) * sizeof(double) + 2 * raw_words * sizeof(float);
+    // few stripes: split the tiles over more CTAs so every SM has work
+    const bool split = static_cast<uint64_t>(nstripe) * ((ntiles + kGramTilesPerCta - 1) / kGramTilesPerCta) <
+                       static_cast<uint64_t>(ctx->num_sms);
+    const int tpc = split ? kGramTilesPerCta / 4 : kGramTilesPerCta;
+    const unsigned gy = static_cast<unsigned>((ntiles + tpc - 1) / tpc);
+    if (split) {
+        static size_t gattr = 0;
+        if (gsmem > gattr) {
+            ZI_CUDA(cudaFuncSetAttribute(k_vec_gram<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
+            gattr = gsmem;
+        }
+        ZI_LAUNCH(ctx, "vec_gram", k_vec_gram<5>, dim3(nstripe, gy), kGramThreads, gsmem, X, n, dim, Pd, vi->mean.p, ntiles,
+                  tpc, part.p);
+    } else {
+        static size_t gattr = 0;
+        if (gsmem > gattr) {
+            ZI_CUDA(cudaFuncSetAttribute(k_vec_gram<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
+            gattr = gsmem;
+        }
+        ZI_LAUNCH(ctx, "vec_gram", k_vec_gram<17>, dim3(nstripe, gy), kGramThreads, gsmem, X, n, dim, Pd, vi->mean.p,
+                  ntiles, tpc, part.p);
     }
-    const unsigned gy = static_cast<unsigned>((ntiles + kGramTilesPerCta - 1) / kGramTilesPerCta);
-    ZI_LAUNCH(ctx, "vec_gram", k_vec_gram, dim3(nstripe, gy), kGramThreads, gsmem, X, n, dim, Pd, vi->mean.p, ntiles, part.p);
     vi->cov.ensure(static_cast<size_t>(dim) * dim);
     ZI_LAUNCH(ctx, "vec_gram_reduce", k_vec_gram_reduce, ntiles, 64, 0, part.p, nstripe, ntiles, T, dim, n, vi->cov.p);
     // eigen-solve (k_pca.cu), components [j][d]

@@ -182,7 +182,8 @@ struct zi_vector_index {
     zi_ctx* ctx = nullptr;
     uint64_t n = 0;
     int dim = 0, dims = 0;
-    zi::dbuf<float> X;                  // n x dim, device resident
+    zi::dbuf<float> X;                  // n x dim, device resident (owned copy)
+    const float* Xd = nullptr;          // the rows the build reads (X.p or a caller's device buffer)
     zi::dbuf<double> mean, cov, comp, eig, pca_work, Y, scratch;
     zi::dbuf<unsigned long long> minmax;
     zi::dbuf<uint32_t> recs;
