@@ -22,9 +22,7 @@
 namespace zi {
 
 constexpr int kStripe = 32768;      // canonical stripe of the mean / Gram sums
-constexpr int kGramThreads = 256;
 constexpr int kGramRows = 32;       // rows staged in shared memory per round (8 k-steps)
-constexpr int kGramTilesPerCta = 136;  // 8x8 tiles per CTA (17 per warp)
 
 __device__ inline void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -81,51 +79,59 @@ __device__ inline void cp_async16_v(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
 }
 
-// Per-stripe Gram tiles (ti <= tj, 8x8) on the FP64 tensor cores: k = data rows in order.
-// part[(s * ntiles + tile) * 64 + r * 8 + c] = G_s[8 ti + r][8 tj + c].
-// Rounds of kGramRows rows: the raw fp32 rows of round b+1 stream in with cp.async (one
-// contiguous 16-byte-aligned block) while round b's k-steps run; each round is converted once
-// to xc = (double)x - mean in shared memory (fp64, 32-byte row skew: conflict-free fragments).
-template <int PW>
-__global__ void __launch_bounds__(kGramThreads, 2) k_vec_gram(const float* __restrict__ X, uint64_t n, int dim, int Pd,
-                                                           const double* __restrict__ mean, int ntiles, int tiles_per_cta,
-                                                           double* __restrict__ part) {
+// Per-stripe Gram tiles (ti <= tj, 8x8) on the FP64 tensor cores: k = data rows in order;
+// part[(s * ntiles + tile) * 64 + r * 8 + c] = G_s[8 ti + r][8 tj + c].  Rounds of kGramRows rows:
+// the raw fp32 rows of round b+1 stream in with cp.async (one contiguous 16-byte-aligned block)
+// while round b's k-steps run; each round is converted once to xc = (double)x - mean in shared
+// memory (fp64, 32-byte row skew: conflict-free fragments).
+// Blocked variant: warp w owns a 4x4 block of 8x8 tiles (block (bi, bj), bi <= bj, of the upper
+// triangle), so a k-step loads 4 A and 4 B fragments for 16 MMAs (the per-tile variant loads 2
+// per MMA and is shared-memory bound).  Tiles below the diagonal of a diagonal block are computed
+// but not stored.  One warp per block, up to 16 blocks per CTA.
+constexpr int kGramMaxWarps = 16;
+__global__ void __launch_bounds__(kGramMaxWarps * 32, 1) k_vec_gram_blk(const float* __restrict__ X, uint64_t n, int dim,
+                                                                        int Pd, const double* __restrict__ mean,
+                                                                        int nblocks, double* __restrict__ part) {
     extern __shared__ __align__(16) double s_x[];  // kGramRows x (Pd + 4) fp64, then 2 raw fp32 rounds
     const int ld = Pd + 4;
     float* s_raw = reinterpret_cast<float*>(s_x + kGramRows * ld);
-    const int raw_words = ((kGramRows * dim + 3) / 4) * 4;  // per buffer, 16-byte multiple
-    const int T = Pd / 8;
+    const int raw_words = ((kGramRows * dim + 3) / 4) * 4;
+    const int T = Pd / 8, Tb = (T + 3) / 4, ntiles = T * (T + 1) / 2;
+    const int nthr = blockDim.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = lane >> 2, c = lane & 3;
     const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kStripe;
     const uint64_t r1 = r0 + kStripe < n ? r0 + kStripe : n;
-    const int t0 = blockIdx.y * tiles_per_cta;
-    const int t1 = min(ntiles, t0 + tiles_per_cta);
-    int offA[PW], offB[PW];
-    double acc[PW][2];
-    int nq = 0;
-#pragma unroll
-    for (int q = 0; q < PW; ++q) {
-        const int t = t0 + warp + 8 * q;
-        int a = 0, rem = t;  // tile index -> (ti, tj), ti <= tj, row-major over the upper triangle
-        while (a < T && rem >= T - a) {
-            rem -= T - a;
-            ++a;
+    const int blk = blockIdx.y * kGramMaxWarps + warp;
+    const bool active = blk < nblocks;
+    int bi = 0, bj = 0;
+    {
+        int rem = active ? blk : 0;
+        while (bi < Tb && rem >= Tb - bi) {
+            rem -= Tb - bi;
+            ++bi;
         }
-        offA[q] = c * ld + a * 8 + r;          // A[i][k] = xc[row k][feature 8 ti + r]
-        offB[q] = c * ld + (a + rem) * 8 + r;  // B[k][j] = xc[row k][feature 8 tj + r]
-        acc[q][0] = acc[q][1] = 0.0;
-        if (t < t1) nq = q + 1;
+        bj = bi + rem;
     }
-    // round b -> raw buffer (b / kGramRows) & 1; a round is rows [b, b + kGramRows) of the stripe
+    int offA[4], offB[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        offA[u] = c * ld + (4 * bi + u) * 8 + r;
+        offB[u] = c * ld + (4 * bj + u) * 8 + r;
+    }
+    double acc[4][4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
     auto issue = [&](uint64_t b, int buf) {
         const uint64_t rows = b + kGramRows <= r1 ? kGramRows : r1 - b;
-        const uint64_t words = rows * dim;                 // contiguous fp32 words
-        const float* src = X + b * dim;                    // b * dim * 4 is a 16-byte multiple (kGramRows * 4 | 16)
+        const uint64_t words = rows * dim;
+        const float* src = X + b * dim;
         float* dst = s_raw + buf * raw_words;
         const uint64_t full = words / 4;
-        for (uint64_t e = tid; e < full; e += kGramThreads) cp_async16_v(dst + 4 * e, src + 4 * e);
-        for (uint64_t e = full * 4 + tid; e < words; e += kGramThreads) dst[e] = __ldg(src + e);
+        for (uint64_t e = tid; e < full; e += nthr) cp_async16_v(dst + 4 * e, src + 4 * e);
+        for (uint64_t e = full * 4 + tid; e < words; e += nthr) dst[e] = __ldg(src + e);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     issue(r0, 0);
@@ -137,33 +143,43 @@ __global__ void __launch_bounds__(kGramThreads, 2) k_vec_gram(const float* __res
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
-        __syncthreads();  // round b landed; the previous round's k-steps are done
+        __syncthreads();
         const float* raw = s_raw + buf * raw_words;
-        const uint64_t rows = b + kGramRows <= r1 ? kGramRows : r1 - b;
-        for (int e = tid; e < kGramRows * Pd; e += kGramThreads) {
+        const int rows = static_cast<int>(b + kGramRows <= r1 ? kGramRows : r1 - b);
+        for (int e = tid; e < kGramRows * Pd; e += nthr) {
             const int rr = e / Pd, j = e - rr * Pd;
-            // rows past the stripe / columns past dim contribute exact zeros
-            s_x[rr * ld + j] = (rr < static_cast<int>(rows) && j < dim)
-                                   ? __dsub_rn(static_cast<double>(raw[rr * dim + j]), mean[j])
-                                   : 0.0;
+            s_x[rr * ld + j] = (rr < rows && j < dim) ? __dsub_rn(static_cast<double>(raw[rr * dim + j]), mean[j]) : 0.0;
         }
         __syncthreads();
-#pragma unroll 1
-        for (int ks = 0; ks < kGramRows / 4; ++ks) {
-            const double* xr = s_x + (ks * 4) * ld;
+        if (active) {
+#pragma unroll 2
+            for (int ks = 0; ks < kGramRows / 4; ++ks) {
+                const double* xr = s_x + (ks * 4) * ld;
+                double af[4], bf[4];
 #pragma unroll
-            for (int q = 0; q < PW; ++q)
-                if (q < nq) dmma(acc[q][0], acc[q][1], xr[offA[q]], xr[offB[q]]);
+                for (int u = 0; u < 4; ++u) {
+                    af[u] = xr[offA[u]];
+                    bf[u] = xr[offB[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) dmma(acc[u][v][0], acc[u][v][1], af[u], bf[v]);
+            }
         }
     }
+    if (!active) return;
 #pragma unroll
-    for (int q = 0; q < PW; ++q) {
-        if (q >= nq) continue;
-        const int t = t0 + warp + 8 * q;
-        double* o = part + (static_cast<size_t>(blockIdx.x) * ntiles + t) * 64 + r * 8 + 2 * c;
-        o[0] = acc[q][0];
-        o[1] = acc[q][1];
-    }
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int ti = 4 * bi + u, tj = 4 * bj + v;
+            if (ti >= T || tj >= T || ti > tj) continue;
+            const int t = ti * T - ti * (ti - 1) / 2 + (tj - ti);  // upper-triangle row-major index
+            double* o = part + (static_cast<size_t>(blockIdx.x) * ntiles + t) * 64 + r * 8 + 2 * c;
+            o[0] = acc[u][v][0];
+            o[1] = acc[u][v][1];
+        }
 }
 
 // cov[i][j] = cov[j][i] = (sum over stripes, in order) / (n - 1)
@@ -336,27 +352,17 @@ void build_vector_index_device(zi_vector_index* vi) {
     // covariance
     const size_t raw_words = ((static_cast<size_t>(kGramRows) * dim + 3) / 4) * 4;
     const size_t gsmem = static_cast<size_t>(kGramRows) * (Pd + 4) * sizeof(double) + 2 * raw_words * sizeof(float);
-    // few stripes: split the tiles over more CTAs so every SM has work
-    const bool split = static_cast<uint64_t>(nstripe) * ((ntiles + kGramTilesPerCta - 1) / kGramTilesPerCta) <
-                       static_cast<uint64_t>(ctx->num_sms);
-    const int tpc = split ? kGramTilesPerCta / 4 : kGramTilesPerCta;
-    const unsigned gy = static_cast<unsigned>((ntiles + tpc - 1) / tpc);
-    if (split) {
+    {
+        const int Tb = (T + 3) / 4, nblocks = Tb * (Tb + 1) / 2;
+        const int warps = std::min(nblocks, kGramMaxWarps);
+        const unsigned gy = static_cast<unsigned>((nblocks + kGramMaxWarps - 1) / kGramMaxWarps);
         static size_t gattr = 0;
         if (gsmem > gattr) {
-            ZI_CUDA(cudaFuncSetAttribute(k_vec_gram<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
+            ZI_CUDA(cudaFuncSetAttribute(k_vec_gram_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
             gattr = gsmem;
         }
-        ZI_LAUNCH(ctx, "vec_gram", k_vec_gram<5>, dim3(nstripe, gy), kGramThreads, gsmem, X, n, dim, Pd, vi->mean.p, ntiles,
-                  tpc, part.p);
-    } else {
-        static size_t gattr = 0;
-        if (gsmem > gattr) {
-            ZI_CUDA(cudaFuncSetAttribute(k_vec_gram<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
-            gattr = gsmem;
-        }
-        ZI_LAUNCH(ctx, "vec_gram", k_vec_gram<17>, dim3(nstripe, gy), kGramThreads, gsmem, X, n, dim, Pd, vi->mean.p,
-                  ntiles, tpc, part.p);
+        ZI_LAUNCH(ctx, "vec_gram", k_vec_gram_blk, dim3(nstripe, gy), warps * 32, gsmem, X, n, dim, Pd, vi->mean.p,
+                  nblocks, part.p);
     }
     vi->cov.ensure(static_cast<size_t>(dim) * dim);
     ZI_LAUNCH(ctx, "vec_gram_reduce", k_vec_gram_reduce, ntiles, 64, 0, part.p, nstripe, ntiles, T, dim, n, vi->cov.p);
