@@ -373,6 +373,82 @@ __device__ inline void dmma_8x8x4(double& d0, double& d1, double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// One warp's G groups of 8 patches starting at dictionary row `base`.
+template <int D, int G>
+__device__ __forceinline__ void project_groups(const uint8_t* __restrict__ img, int w, int C,
+                                               const uint32_t* __restrict__ keys, uint64_t n, uint64_t base, int KS,
+                                               const double* s_B, const double* s_mean, const int* s_joff,
+                                               double* __restrict__ Y, unsigned long long (*s_mm)[D]) {
+    constexpr int NT = (D + 7) / 8;
+    const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+    const uint8_t* pb[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const uint64_t i = base + 8 * g + r;
+        const uint32_t key = keys[i < n ? i : n - 1];
+        pb[g] = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
+    }
+    double acc[G][NT][2];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[g][t][0] = acc[g][t][1] = 0.0;
+    uint32_t xr[kProjPF][G];
+#pragma unroll
+    for (int s = 0; s < kProjPF; ++s)
+        if (s < KS) {
+            const int o = s_joff[s * 4 + c];
+#pragma unroll
+            for (int g = 0; g < G; ++g) xr[s][g] = __ldg(pb[g] + o);
+        }
+    for (int ks0 = 0; ks0 < KS; ks0 += kProjPF) {
+#pragma unroll
+        for (int s = 0; s < kProjPF; ++s) {
+            const int ks = ks0 + s;
+            if (ks < KS) {
+                uint32_t xcur[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) xcur[g] = xr[s][g];
+                if (ks + kProjPF < KS) {
+                    const int o = s_joff[(ks + kProjPF) * 4 + c];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) xr[s][g] = __ldg(pb[g] + o);
+                }
+                const double mj = s_mean[ks * 4 + c];
+                double bf[NT];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) bf[t] = s_B[(ks * NT + t) * 32 + lane];
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const double a = __dsub_rn(static_cast<double>(xcur[g]), mj);
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) dmma_8x8x4(acc[g][t][0], acc[g][t][1], a, bf[t]);
+                }
+            }
+        }
+    }
+    // lane holds y[patch base + 8g + r][dim 8t + 2c + e]
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const uint64_t i = base + 8 * g + r;
+        if (i < n) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int d = 8 * t + 2 * c + e;
+                    if (d < D) {
+                        const double y = acc[g][t][e];
+                        Y[static_cast<size_t>(d) * n + i] = y;
+                        const unsigned long long o = double_to_ordered(y);
+                        atomicMin(&s_mm[0][d], o);
+                        atomicMax(&s_mm[1][d], o);
+                    }
+                }
+        }
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restrict__ img, int w, int C,
                                                           const uint32_t* __restrict__ keys, uint64_t n,
@@ -381,10 +457,9 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restr
                                                           const double* __restrict__ comp, double* __restrict__ Y,
                                                           unsigned long long* __restrict__ minmax) {
     constexpr int NT = (D + 7) / 8;  // 8-dim tiles
-    constexpr int G = kProjGroups;
     extern __shared__ double sm[];
     const int mc = m * C, KS = (mc + 3) / 4;
-    double* s_B = sm;                                   // [KS][NT][32] B fragments (Comp, zero padded)
+    double* s_B = sm;                                          // [KS][NT][32] B fragments (Comp, zero padded)
     double* s_mean = s_B + static_cast<size_t>(KS) * NT * 32;  // [KS*4]
     int* s_joff = reinterpret_cast<int*>(s_mean + KS * 4);     // [KS*4] byte offset of column j
     for (int idx = threadIdx.x; idx < KS * NT * 32; idx += kProjThreads) {
@@ -401,77 +476,10 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restr
     __shared__ unsigned long long s_mm[2][D];
     if (threadIdx.x < 2 * D) s_mm[threadIdx.x / D][threadIdx.x % D] = threadIdx.x < D ? ~0ull : 0ull;
     __syncthreads();
-    const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
     const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kProjThreads / 32);
-    for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * (kProjThreads / 32) + (threadIdx.x >> 5)) * (8 * G);
-         base < n; base += warps * 8 * G) {
-        const uint8_t* pb[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const uint64_t i = base + 8 * g + r;
-            const uint32_t key = keys[i < n ? i : n - 1];
-            pb[g] = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
-        }
-        double acc[G][NT][2];
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int t = 0; t < NT; ++t) acc[g][t][0] = acc[g][t][1] = 0.0;
-        uint32_t xr[kProjPF][G];
-#pragma unroll
-        for (int s = 0; s < kProjPF; ++s)
-            if (s < KS) {
-                const int o = s_joff[s * 4 + c];
-#pragma unroll
-                for (int g = 0; g < G; ++g) xr[s][g] = __ldg(pb[g] + o);
-            }
-        for (int ks0 = 0; ks0 < KS; ks0 += kProjPF) {
-#pragma unroll
-            for (int s = 0; s < kProjPF; ++s) {
-                const int ks = ks0 + s;
-                if (ks < KS) {
-                    uint32_t xcur[G];
-#pragma unroll
-                    for (int g = 0; g < G; ++g) xcur[g] = xr[s][g];
-                    if (ks + kProjPF < KS) {
-                        const int o = s_joff[(ks + kProjPF) * 4 + c];
-#pragma unroll
-                        for (int g = 0; g < G; ++g) xr[s][g] = __ldg(pb[g] + o);
-                    }
-                    const double mj = s_mean[ks * 4 + c];
-                    double bf[NT];
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) bf[t] = s_B[(ks * NT + t) * 32 + lane];
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const double a = __dsub_rn(static_cast<double>(xcur[g]), mj);
-#pragma unroll
-                        for (int t = 0; t < NT; ++t) dmma_8x8x4(acc[g][t][0], acc[g][t][1], a, bf[t]);
-                    }
-                }
-            }
-        }
-        // lane holds y[patch base + 8g + r][dim 8t + 2c + e]
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const uint64_t i = base + 8 * g + r;
-            if (i < n) {
-#pragma unroll
-                for (int t = 0; t < NT; ++t)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int d = 8 * t + 2 * c + e;
-                        if (d < D) {
-                            const double y = acc[g][t][e];
-                            Y[static_cast<size_t>(d) * n + i] = y;
-                            const unsigned long long o = double_to_ordered(y);
-                            atomicMin(&s_mm[0][d], o);
-                            atomicMax(&s_mm[1][d], o);
-                        }
-                    }
-            }
-        }
-    }
+    for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * (kProjThreads / 32) + (threadIdx.x >> 5)) * (8 * kProjGroups);
+         base < n; base += warps * 8 * kProjGroups)
+        project_groups<D, kProjGroups>(img, w, C, keys, n, base, KS, s_B, s_mean, s_joff, Y, s_mm);
     __syncthreads();
     if (threadIdx.x < D) {
         atomicMin(minmax + threadIdx.x, s_mm[0][threadIdx.x]);
