@@ -324,19 +324,25 @@ static int msd_bytes_forced() {  // ZI_SORT_MSD overrides the histogram-driven M
 constexpr int kSegThreads = 256;
 constexpr uint32_t kMaxBig = 64;  // oversized segments finished one by one; more -> full LSD
 
+// segmask[k]: the bits of record word k that form the segment key (the top nb Morton bytes, and
+// the payload's layout bits); cmpmask[k] (k < 3): the bits of key word k below the segment key.
+// When the remaining bytes fit (D - nb <= 12) a record's order inside its segment is the 128-bit
+// compare key ((w2 & m2):(w1 & m1), (w0 & m0):payload).
 template <int NW>
 struct seg_ctx {
     uint32_t* w[kMaxWords];
     uint64_t N;
-    int D, nb;
-    bool layouts;
+    uint32_t segmask[kMaxWords];
+    uint32_t cmpmask[3];
+    bool can_count;
 };
 
 template <int NW>
-__device__ inline uint64_t seg_key(const seg_ctx<NW>& c, uint64_t i) {
-    uint64_t k = c.layouts ? (c.w[NW - 1][i] >> 29) : 0u;
-    for (int p = c.D - 1; p >= c.D - c.nb && p >= 0; --p) k = (k << 8) | ((c.w[p >> 2][i] >> ((p & 3) * 8)) & 0xffu);
-    return k;
+__device__ inline bool seg_differs(const seg_ctx<NW>& c, uint64_t i, uint64_t j) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) d |= (c.w[k][i] ^ c.w[k][j]) & c.segmask[k];
+    return d != 0;
 }
 
 // first segment head in [from, limit) (limit if none); one warp
@@ -347,32 +353,65 @@ __device__ inline uint64_t find_head(const seg_ctx<NW>& c, uint64_t from, uint64
     if (limit > c.N) limit = c.N;
     for (uint64_t b = from; b < limit; b += 32) {
         const uint64_t i = b + lane;
-        const bool h = i < limit && seg_key(c, i) != seg_key(c, i - 1);
+        const bool h = i < limit && seg_differs(c, i, i - 1);
         const unsigned m = __ballot_sync(0xffffffffu, h);
         if (m) return b + __ffs(m) - 1;
     }
     return limit;
 }
 
+// Shared-memory record layout of the window sort: array-of-records, P words per record (16-byte
+// aligned for NW > 2) so a whole record is one or two vector loads.
+template <int NW>
+struct seg_rec {
+    static constexpr int P = NW <= 2 ? 2 : (NW + 3) & ~3;
+    __device__ static inline void load(const uint32_t* p, uint32_t (&r)[NW]) {
+        if constexpr (P == 2) {
+            const uint2 v = *reinterpret_cast<const uint2*>(p);
+            r[0] = v.x;
+            if constexpr (NW > 1) r[NW - 1] = v.y;
+        } else {
+#pragma unroll
+            for (int q = 0; q < P / 4; ++q) {
+                const uint4 v = *reinterpret_cast<const uint4*>(p + 4 * q);
+                if (4 * q + 0 < NW) r[(4 * q + 0) % NW] = v.x;
+                if (4 * q + 1 < NW) r[(4 * q + 1) % NW] = v.y;
+                if (4 * q + 2 < NW) r[(4 * q + 2) % NW] = v.z;
+                if (4 * q + 3 < NW) r[(4 * q + 3) % NW] = v.w;
+            }
+        }
+    }
+};
+
 // One CTA sorts one window: the records of the segments that start in [w*T, (w+1)*T) (so the
-// window is a union of whole segments), all passes of the global LSD sort replayed in shared
-// memory on a u16 permutation (the records themselves stay put), then written back in place.
+// window is a union of whole segments), loaded into shared memory and written back in place.
 // Segments never change the segment key at any position, so neighbours reading a boundary
-// while this CTA writes see the same keys.
+// while this CTA writes see the same keys.  Two ways to order a window:
+//  * rank by counting (short segments, the common case): record j of segment [ss, se) goes to
+//    ss + #{k in [ss, se) : rec_k < rec_j} under the full comparator -- sum of L^2 compares,
+//    no passes; segment bounds come from a head bitmask (last head <= j, first head > j);
+//  * all passes of the global LSD sort replayed on a u16 permutation (long segments).
+// The record-weighted mean segment length (sum L^2 / len) picks the way per window.
+constexpr int kSegCountMean = 24;
+
 template <int NW>
 __global__ void __launch_bounds__(kSegThreads) k_segsort(seg_ctx<NW> c, int T, int cap, int npass,
                                                          const int2* __restrict__ passes,
                                                          unsigned long long* __restrict__ big,
-                                                         uint32_t* __restrict__ nbig) {
-    extern __shared__ uint32_t s_w[];  // NW * cap words, then cur / nxt (u16 cap each)
-    uint16_t* s_cur = reinterpret_cast<uint16_t*>(s_w + static_cast<size_t>(NW) * cap);
+                                                         uint32_t* __restrict__ nbig, int count_mean,
+                                                         unsigned long long* __restrict__ sumL) {
+    using R = seg_rec<NW>;
+    extern __shared__ uint32_t s_w[];  // cap records of R::P words, cur / nxt (u16 cap each), head bits
+    uint16_t* s_cur = reinterpret_cast<uint16_t*>(s_w + static_cast<size_t>(R::P) * cap);
     uint16_t* s_nxt = s_cur + cap;
+    uint32_t* s_head = reinterpret_cast<uint32_t*>(s_nxt + cap);  // (cap + kSegThreads + 32) / 32 words
     constexpr int kWarps = kSegThreads / 32;
     __shared__ uint32_t s_hist[kWarps][256];
     __shared__ uint32_t s_dstart[256];
     __shared__ uint32_t s_wsum[kWarps];
     __shared__ uint64_t s_range[2];
     __shared__ int2 s_pass[40];
+    __shared__ unsigned long long s_sumL;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * T;
     const uint64_t w1 = w0 + T < c.N ? w0 + T : c.N;
@@ -388,6 +427,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segsort(seg_ctx<NW> c, int T, i
         }
     }
     if (tid < npass) s_pass[tid] = passes[tid];
+    if (tid == 0) s_sumL = 0;
     __syncthreads();
     const uint64_t start = s_range[0];
     uint64_t end = s_range[1];
@@ -423,22 +463,107 @@ __global__ void __launch_bounds__(kSegThreads) k_segsort(seg_ctx<NW> c, int T, i
         wand[k] = 0xffffffffu;
         wor[k] = 0u;
     }
-    for (int j = tid; j < len; j += kSegThreads) {
+    // batches of kLoadRounds rounds: all of a batch's global loads are in flight together
+    constexpr int kLoadRounds = 4;
+    for (int j0 = 0; j0 < len; j0 += kSegThreads * kLoadRounds) {
+        uint32_t v[kLoadRounds][NW];
 #pragma unroll
-        for (int k = 0; k < NW; ++k) {
-            const uint32_t x = c.w[k][start + j];
-            s_w[k * cap + j] = x;
-            wand[k] &= x;
-            wor[k] |= x;
+        for (int r = 0; r < kLoadRounds; ++r) {
+            const int j = j0 + r * kSegThreads + tid;
+            if (j < len)
+#pragma unroll
+                for (int k = 0; k < NW; ++k) v[r][k] = c.w[k][start + j];
         }
-        s_cur[j] = static_cast<uint16_t>(j);
+#pragma unroll
+        for (int r = 0; r < kLoadRounds; ++r) {
+            const int j = j0 + r * kSegThreads + tid;
+            if (j < len) {
+#pragma unroll
+                for (int k = 0; k < NW; ++k) {
+                    s_w[j * R::P + k] = v[r][k];
+                    wand[k] &= v[r][k];
+                    wor[k] |= v[r][k];
+                }
+                s_cur[j] = static_cast<uint16_t>(j);
+            }
+        }
     }
 #pragma unroll
     for (int k = 0; k < NW; ++k) {  // digits equal over the whole window need no pass
         atomicAnd(&s_and[k], wand[k]);
         atomicOr(&s_or[k], wor[k]);
     }
+    // segment heads; bit len is a sentinel head
+    for (int b = 0; b <= len; b += kSegThreads) {
+        const int j = b + tid;
+        bool h = j == len;
+        if (j < len) {
+            if (j == 0) {
+                h = true;
+            } else {
+                uint32_t a[NW], p[NW], d = 0;
+                R::load(s_w + j * R::P, a);
+                R::load(s_w + (j - 1) * R::P, p);
+#pragma unroll
+                for (int k = 0; k < NW; ++k) d |= (a[k] ^ p[k]) & c.segmask[k];
+                h = d != 0;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, h);
+        if (lane == 0) s_head[j >> 5] = m;
+    }
     __syncthreads();
+    auto seg_start = [&](int j) {
+        int wi = j >> 5;
+        unsigned m = s_head[wi] & (0xffffffffu >> (31 - (j & 31)));
+        while (m == 0) m = s_head[--wi];
+        return (wi << 5) + 31 - __clz(m);
+    };
+    auto seg_end = [&](int j) {
+        int wi = j >> 5;
+        unsigned m = (j & 31) == 31 ? 0u : s_head[wi] & (0xfffffffeu << (j & 31));
+        while (m == 0) m = s_head[++wi];
+        return (wi << 5) + __ffs(m) - 1;
+    };
+    {
+        unsigned long long sl = 0;
+        for (int j = tid; j < len; j += kSegThreads) sl += static_cast<unsigned>(seg_end(j) - seg_start(j));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o);
+        if (lane == 0) atomicAdd(&s_sumL, sl);
+    }
+    __syncthreads();
+    if (tid == 0) atomicAdd(sumL, s_sumL);
+    if (c.can_count && s_sumL <= static_cast<unsigned long long>(count_mean) * static_cast<unsigned long long>(len)) {
+        ulonglong2* s_ck = reinterpret_cast<ulonglong2*>(
+            (reinterpret_cast<uintptr_t>(s_head + (cap + kSegThreads + 32) / 32) + 15) & ~static_cast<uintptr_t>(15));
+        for (int j = tid; j < len; j += kSegThreads) {
+            uint32_t r[NW];
+            R::load(s_w + j * R::P, r);
+            const uint32_t w1 = NW > 2 ? r[NW > 2 ? 1 : 0] & c.cmpmask[1] : 0u;
+            const uint32_t w2 = NW > 3 ? r[NW > 3 ? 2 : 0] & c.cmpmask[2] : 0u;
+            s_ck[j] = make_ulonglong2((static_cast<unsigned long long>(r[0] & c.cmpmask[0]) << 32) | r[NW - 1],
+                                      (static_cast<unsigned long long>(w2) << 32) | w1);
+        }
+        __syncthreads();
+        for (int j = tid; j < len; j += kSegThreads) {
+            const int ss = seg_start(j), se = seg_end(j);
+            const ulonglong2 me = s_ck[j];
+            int rank = 0;
+            for (int k = ss; k < se; ++k) {
+                const ulonglong2 o = s_ck[k];
+                rank += (o.y < me.y || (o.y == me.y && o.x < me.x)) ? 1 : 0;
+            }
+            s_nxt[ss + rank] = static_cast<uint16_t>(j);
+        }
+        __syncthreads();
+        for (int j = tid; j < len; j += kSegThreads) {
+            const int src = s_nxt[j];
+#pragma unroll
+            for (int k = 0; k < NW; ++k) c.w[k][start + j] = s_w[src * R::P + k];
+        }
+        return;
+    }
     // warp w ranks the contiguous chunk [w*CH, (w+1)*CH) in rounds of 32 (stable order)
     const int CH = ((len + kWarps - 1) / kWarps + 31) & ~31;
     const int nround = CH / 32;
@@ -455,7 +580,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segsort(seg_ctx<NW> c, int T, i
             if (r < nround) {
                 const int i = warp * CH + r * 32 + lane;
                 uint32_t d = 256u;
-                if (i < len) d = (s_w[wk * cap + s_cur[i]] >> sh) & 0xffu;
+                if (i < len) d = (s_w[s_cur[i] * R::P + wk] >> sh) & 0xffu;
                 const uint32_t peers = __match_any_sync(0xffffffffu, d);
                 uint32_t old = 0;
                 if (d < 256u) old = s_hist[warp][d];
@@ -505,24 +630,33 @@ __global__ void __launch_bounds__(kSegThreads) k_segsort(seg_ctx<NW> c, int T, i
     for (int j = tid; j < len; j += kSegThreads) {
         const int src = s_cur[j];
 #pragma unroll
-        for (int k = 0; k < NW; ++k) c.w[k][start + j] = s_w[k * cap + src];
+        for (int k = 0; k < NW; ++k) c.w[k][start + j] = s_w[src * R::P + k];
     }
 }
 
 template <int NW>
 static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int D, int nb, bool layouts,
-                           const std::vector<int2>& passes, int2* d_passes, unsigned long long* big, uint32_t* nbig) {
+                           const std::vector<int2>& passes, int2* d_passes, unsigned long long* big, uint32_t* nbig,
+                           unsigned long long* sumL) {
     seg_ctx<NW> c{};
     for (int k = 0; k < NW; ++k) c.w[k] = words[k];
     c.N = N;
-    c.D = D;
-    c.nb = nb;
-    c.layouts = layouts;
+    for (int p = std::max(D - nb, 0); p < D; ++p) c.segmask[p >> 2] |= 0xffu << ((p & 3) * 8);
+    if (layouts) c.segmask[NW - 1] = 0xe0000000u;
+    for (int p = 0; p < D - nb && p < 12; ++p) c.cmpmask[p >> 2] |= 0xffu << ((p & 3) * 8);
+    c.can_count = D - nb <= 12;
     static const int cap0 = [] { const char* e = std::getenv("ZI_SORT_CAP"); return e ? std::atoi(e) : 4096; }();
+    static const int count_mean = [] { const char* e = std::getenv("ZI_SORT_COUNT"); return e ? std::atoi(e) : kSegCountMean; }();
+    constexpr int P = seg_rec<NW>::P;
+    // records | cur, nxt | head bits | 16-byte compare keys
+    auto bytes = [](int cp) {
+        return static_cast<size_t>(cp) * (P * 4 + 4) + static_cast<size_t>(cp + kSegThreads + 32) / 32 * 4 + 16 +
+               static_cast<size_t>(cp) * 16;
+    };
     int cap = cap0;
-    while (cap > 1024 && static_cast<size_t>(cap) * (NW * 4 + 4) > 100 * 1024) cap >>= 1;
+    while (cap > 1024 && bytes(cap) > 112 * 1024) cap >>= 1;
     const int T = cap / 2;
-    const size_t smem = static_cast<size_t>(cap) * (NW * 4 + 4);
+    const size_t smem = bytes(cap);
     static size_t attr = 0;
     if (smem > attr) {
         ZI_CUDA(cudaFuncSetAttribute(k_segsort<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -531,7 +665,7 @@ static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int 
     ZI_CUDA(cudaMemcpyAsync(d_passes, passes.data(), passes.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
     const unsigned grid = static_cast<unsigned>((N + T - 1) / T);
     ZI_LAUNCH(ctx, "segment_sort", k_segsort<NW>, grid, kSegThreads, smem, c, T, cap, static_cast<int>(passes.size()),
-              d_passes, big, nbig);
+              d_passes, big, nbig, count_mean, sumL);
 }
 
 // window sort + oversized-segment handling after the MSD passes
@@ -543,25 +677,32 @@ static void finish_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int 
     uint32_t* cnt = ctx->counter.ensure(16 + 4 * kMaxBig + 2 * 64);
     unsigned long long* big = reinterpret_cast<unsigned long long*>(cnt + 16);
     int2* d_passes = reinterpret_cast<int2*>(cnt + 16 + 4 * kMaxBig);
+    unsigned long long* sumL = reinterpret_cast<unsigned long long*>(cnt + 2);  // sum of L^2 over segments
     ZI_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), ctx->stream));
     switch (nw) {
-        case 2: launch_segsort<2>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
-        case 3: launch_segsort<3>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
-        case 4: launch_segsort<4>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
-        case 5: launch_segsort<5>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
-        case 6: launch_segsort<6>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
-        case 7: launch_segsort<7>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
-        case 8: launch_segsort<8>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
-        case 9: launch_segsort<9>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt); break;
+        case 2: launch_segsort<2>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
+        case 3: launch_segsort<3>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
+        case 4: launch_segsort<4>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
+        case 5: launch_segsort<5>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
+        case 6: launch_segsort<6>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
+        case 7: launch_segsort<7>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
+        case 8: launch_segsort<8>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
+        case 9: launch_segsort<9>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
         default: throw error(ZI_E_INVALID, "radix sort: unsupported record width");
     }
     uint32_t hc[4] = {0, 0, 0, 0};
     ZI_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     const uint32_t nbig = hc[0];
+    const double mean_len = static_cast<double>((static_cast<uint64_t>(hc[3]) << 32) | hc[2]) / static_cast<double>(N);
     if (debug)
-        std::fprintf(stderr, "hybrid sort N=%llu nb=%d: oversized segments %u (%u records)\n",
-                     static_cast<unsigned long long>(N), nb, nbig, hc[1]);
+        std::fprintf(stderr, "hybrid sort N=%llu nb=%d: oversized segments %u (%u records), record-weighted mean segment %.1f\n",
+                     static_cast<unsigned long long>(N), nb, nbig, hc[1], mean_len);
+    // windows rank by counting while segments are short; long ones replay the LSD passes at
+    // several times the cost -- later builds with these dims split one byte deeper
+    if (nbig == 0 && mean_len > kSegCountMean && msd_bytes_forced() <= 0 && learnt >= 0 && nb + 1 <= D - 3 &&
+        D - (nb + 1) <= 12)
+        learnt = nb + 1;
     if (nbig == 0) return;
     if (nbig > kMaxBig || static_cast<uint64_t>(hc[1]) * 8 > N) {
         // top bytes too clustered for the split (smooth images): finish with the full LSD sort.
@@ -606,7 +747,7 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         return;
     }
     const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all);
-    // MSD depth: the fewest top bytes whose (marginal) entropies predict segments of <= 64
+    // MSD depth: the fewest top bytes whose (marginal) entropies predict segments of <= 16
     // records per layout; a clustered top (smooth images) pushes it up, and when the split
     // would leave little for the windows the plain LSD sort is used.
     auto entropy = [&](int q) {
@@ -623,7 +764,7 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     if (nb <= 0) {
         double bits = 0.0;
         nb = 0;
-        while (nb < D && std::exp2(bits) * 64.0 < per_layout) {
+        while (nb < D && std::exp2(bits) * 16.0 < per_layout) {
             bits += entropy(D - 1 - nb);
             ++nb;
         }
