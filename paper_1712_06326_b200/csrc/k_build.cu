@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_patch_matrix(const uint8_t* __restrict_
     __shared__ int s_off[32];
     if (tid < 32) {
         const int f = blockIdx.y * 32 + tid;
-        s_off[tid] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : -1;
+        s_off[tid] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : (f == F ? -2 : -1);
     }
     __syncthreads();
     // gather: a warp reads one feature of 32 consecutive patches (adjacent pixels)
@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(256) k_patch_matrix(const uint8_t* __restrict_
         const int bs = s_base[e & 127], of = s_off[e >> 7];
         uint8_t v = 0;
         if (bs >= 0 && of >= 0) v = __ldg(img + bs + of);
+        else if (bs >= 0 && of == -2) v = 1;  // row F: all ones (the tensor-core path's first moments)
         s_t[e] = v;
     }
     __syncthreads();
@@ -329,12 +330,18 @@ void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const
     ZI_CUDA(cudaMemsetAsync(d_out, 0, (static_cast<size_t>(F) + static_cast<size_t>(F) * F) * sizeof(unsigned long long),
                             ctx->stream));
     if (n == 0) return;
-    const int ntile = (F + kMomTile - 1) / kMomTile;
+    // Fpad > F: row F of XT is all ones over the real patches (G[f][F] = first moments)
+    const int ntile = (F + 1 + kMomTile - 1) / kMomTile;
     const int Fpad = ntile * kMomTile;
     const uint64_t npad = (n + kMomStage - 1) / kMomStage * kMomStage;
     uint8_t* XT = ctx->scratch.ensure(static_cast<size_t>(Fpad) * npad);
     ZI_LAUNCH(ctx, "patch_matrix", k_patch_matrix, dim3(static_cast<unsigned>(npad / 128), Fpad / 32), 256, 0, d_img,
               w, C, K, F, d_keys, n, npad, XT);
+    static const bool use_mma = std::getenv("ZI_MOMENTS_MMA") != nullptr;  // legacy mma.sync path (A/B checks)
+    if (!use_mma) {
+        gram_u8_tc(ctx, XT, F, Fpad, npad, d_out);
+        return;
+    }
     const int npairs = ntile * (ntile + 1) / 2;
     // about two CTAs per SM in one wave; stage-aligned chunks of <= 65536 patches
     const uint64_t want = std::max<uint64_t>(1, (2ull * ctx->num_sms + npairs - 1) / npairs);

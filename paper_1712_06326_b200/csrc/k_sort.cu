@@ -321,6 +321,10 @@ static int msd_bytes_forced() {  // ZI_SORT_MSD overrides the histogram-driven M
     }();
     return v;
 }
+static bool verify_on() {
+    static const bool v = std::getenv("ZI_SORT_VERIFY") != nullptr;
+    return v;
+}
 constexpr int kSegThreads = 256;
 constexpr uint32_t kMaxBig = 64;  // oversized segments finished one by one; more -> full LSD
 
@@ -493,6 +497,7 @@ __global__ void __launch_bounds__(kSegThreads) k_segsort(seg_ctx<NW> c, int T, i
         atomicAnd(&s_and[k], wand[k]);
         atomicOr(&s_or[k], wor[k]);
     }
+    __syncthreads();  // records and the constant-digit masks are complete
     // segment heads; bit len is a sentinel head
     for (int b = 0; b <= len; b += kSegThreads) {
         const int j = b + tid;
@@ -716,15 +721,40 @@ static void finish_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int 
     std::vector<unsigned long long> h(2 * nbig);
     ZI_CUDA(cudaMemcpyAsync(h.data(), big, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
-    // oversized segments (equal top bytes, longer than shared memory): the remaining Morton
-    // bytes by the global LSD sort on that range (stable, so the payload order of ties stays)
-    std::vector<int2> rest;
-    for (int p = 0; p < D - nb; ++p) rest.push_back(make_int2(p >> 2, (p & 3) * 8));
+    // oversized ranges (whole segments, the last one running past shared memory): the global
+    // LSD sort on that range with every pass (stable, so the payload order of ties stays; the
+    // range can hold several segments, so the top bytes take part too)
     for (uint32_t q = 0; q < nbig; ++q) {
         uint32_t* sub[kMaxWords];
         for (int k = 0; k < nw; ++k) sub[k] = words[k] + h[2 * q];
-        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], rest, nullptr, false);
+        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], all, nullptr, false);
     }
+}
+
+// ZI_SORT_VERIFY: check the (layout, Morton key, payload) order of the finished records on the host
+static void verify_sorted(zi_ctx* ctx, uint32_t* const* words, int W, uint64_t N, int D, int nb, bool layouts) {
+    const int nw = W + 1;
+    std::vector<std::vector<uint32_t>> h(nw, std::vector<uint32_t>(N));
+    for (int k = 0; k < nw; ++k)
+        ZI_CUDA(cudaMemcpyAsync(h[k].data(), words[k], N * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    auto less = [&](uint64_t a, uint64_t b) {
+        if (layouts && (h[W][a] >> 29) != (h[W][b] >> 29)) return (h[W][a] >> 29) < (h[W][b] >> 29);
+        for (int k = W - 1; k >= 0; --k)
+            if (h[k][a] != h[k][b]) return h[k][a] < h[k][b];
+        return h[W][a] < h[W][b];
+    };
+    for (uint64_t i = 1; i < N; ++i)
+        if (!less(i - 1, i)) {
+            std::fprintf(stderr, "ZI_SORT_VERIFY: order broken at %llu of %llu (D=%d nb=%d layouts=%d)\n",
+                         static_cast<unsigned long long>(i), static_cast<unsigned long long>(N), D, nb, layouts ? 1 : 0);
+            for (uint64_t j = i > 3 ? i - 3 : 0; j < std::min<uint64_t>(N, i + 3); ++j) {
+                std::fprintf(stderr, "  [%llu]", static_cast<unsigned long long>(j));
+                for (int k = nw - 1; k >= 0; --k) std::fprintf(stderr, " %08x", h[k][j]);
+                std::fprintf(stderr, "\n");
+            }
+            throw error(ZI_E_CUDA, "hybrid sort order broken");
+        }
 }
 
 // Sort (key words, payload) records by (Morton key, payload); `layouts`: the payload's top 3
@@ -744,6 +774,7 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         if (layouts) msd.push_back(make_int2(W, 29));
         radix_sort_words(ctx, words, nw, N, msd, nullptr, true);
         finish_hybrid(ctx, words, W, N, D, nb, layouts, all, learnt);
+        if (verify_on()) verify_sorted(ctx, words, W, N, D, nb, layouts);
         return;
     }
     const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all);
@@ -790,6 +821,7 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     radix_sort_words(ctx, words, nw, N, msd, msd_hist.data(), false);
     if (learnt == 0) learnt = nb;  // remembered: later builds skip the histogram round trip
     finish_hybrid(ctx, words, W, N, D, nb, layouts, all, learnt);
+    if (verify_on()) verify_sorted(ctx, words, W, N, D, nb, layouts);
 }
 
 void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first) {

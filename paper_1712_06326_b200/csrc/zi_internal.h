@@ -205,6 +205,7 @@ uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, i
                             dbuf<uint32_t>& keys_out);
 
 // exact moments s (F) and S (F*F, full symmetric) of the K*K*C patch vectors
+void gram_u8_tc(zi_ctx* ctx, const uint8_t* XT, int F, int Fpad, uint64_t npad, unsigned long long* out);
 void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const uint32_t* d_keys,
                    uint64_t n, unsigned long long* d_out /* F + F*F */);
 

@@ -619,3 +619,19 @@ def test_vector_index_vs_oracle(zb, n, dim, D):
     for i in range(0, 32, 5):
         ref = oracle.knn_linear(rc, rk, qd[i], 80)
         assert cnt[i] == ref.size and np.array_equal(out[i, :cnt[i]], ref)
+
+
+@pytest.mark.gpu
+def test_build_deterministic_repeats(zb):
+    """Window sort / tensor-core moments: repeated builds of one image are byte-identical
+    (shared-memory or TMEM races show up as run-to-run differences)."""
+    img, kn = workloads.small_image(70, 90, 3, seed=21, hole_frac=0.08)
+    ref = None
+    for _ in range(12):
+        mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=8))
+        got = [mi.index_arrays(l) for l in range(8)] + [mi.moments()]
+        if ref is None:
+            ref = got
+            continue
+        for a, b in zip(ref, got):
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
