@@ -494,6 +494,47 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restr
     }
 }
 
+// Morton de-interleave by 8x8 bit-matrix transposes, no tables (a lookup per key byte and plane
+// word was 12% slower in finalize; the quantiser keeps its spread table, which measured faster).  Key bit L*D + D-1-d
+// is bit L of dim d (proj/include/zinpaint/morton.hpp:14-29); dims go in chunks of 8: chunk c
+// holds dims 8c..8c+7, and its level-L byte (bit 7-r = bit L of dim 8c+r) sits at key bit
+// L*D + D-8-8c (a negative offset drops the bits of dims >= D, which are zero).
+__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {  // byte i bit j <-> byte j bit i
+    x = (x & 0xAA55AA55AA55AA55ull) | ((x & 0x00AA00AA00AA00AAull) << 7) | ((x >> 7) & 0x00AA00AA00AA00AAull);
+    x = (x & 0xCCCC3333CCCC3333ull) | ((x & 0x0000CCCC0000CCCCull) << 14) | ((x >> 14) & 0x0000CCCC0000CCCCull);
+    x = (x & 0xF0F0F0F00F0F0F0Full) | ((x & 0x00000000F0F0F0F0ull) << 28) | ((x >> 28) & 0x00000000F0F0F0F0ull);
+    return x;
+}
+
+template <int D>
+__device__ __forceinline__ void morton_deinterleave8(const uint32_t (&kw)[(D + 3) / 4], uint32_t (&pw)[(D + 3) / 4]) {
+    constexpr int W = (D + 3) / 4;
+#pragma unroll
+    for (int k = 0; k < W; ++k) pw[k] = 0;
+#pragma unroll
+    for (int c = 0; c < (D + 7) / 8; ++c) {
+        uint64_t m = 0;
+#pragma unroll
+        for (int L = 0; L < 8; ++L) {
+            const int sh = D - 8 - 8 * c;
+            const int pos = L * D + (sh >= 0 ? sh : 0);
+            const int nb = sh >= 0 ? 8 : 8 + sh;  // bits of this level byte present in the key
+            const int wd = pos >> 5, off = pos & 31;
+            uint32_t v = kw[wd] >> off;
+            if (off + nb > 32 && wd + 1 < W) v |= kw[wd + 1] << (32 - off);
+            v &= (1u << nb) - 1u;
+            if (sh < 0) v <<= -sh;
+            m |= static_cast<uint64_t>(v) << (8 * L);
+        }
+        m = transpose8x8(m);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int d = 8 * c + r;
+            if (d < D) pw[d >> 2] |= (static_cast<uint32_t>(m >> (8 * (7 - r))) & 0xffu) << (8 * (d & 3));
+        }
+    }
+}
+
 // quantise (proj/src/builder.cpp:55-61) and interleave to the 8*D-bit Morton key
 // (proj/include/zinpaint/morton.hpp:14-29): bit L of dim d -> key bit L*D + D-1-d.
 // Records of all 8 layouts share one array of N = 8n entries (layout-major); word k of entry
@@ -576,34 +617,12 @@ __global__ void __launch_bounds__(256) k_interleave(const uint8_t* __restrict__ 
 // Sorted Morton words -> dim planes (4 dims per u32), keys, and per-256-entry bboxes.
 // Entries [off, off+n) of a record array with word stride N; when dict != nullptr the payload
 // is a dictionary row (low 29 bits) and the key is gathered from dict.
-// De-interleave table: key byte B with value v contributes tab[(B*256 + v)*W + k] to plane word
-// k (bit j of the byte is key bit u = 8B + j = L*D + D-1-d -> bit L of dim d's plane byte).
-template <int D>
-__global__ void k_deinterleave_table(uint32_t* __restrict__ tab) {
-    constexpr int W = (D + 3) / 4;
-    const int B = blockIdx.x, v = threadIdx.x;
-    uint32_t w[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) w[k] = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int u = 8 * B + j;
-        if (((v >> j) & 1) && u < 8 * D) {
-            const int L = u / D, d = D - 1 - u % D;
-            w[d >> 2] |= 1u << (8 * (d & 3) + L);
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < W; ++k) tab[(B * 256 + v) * W + k] = w[k];
-}
-
 template <int D>
 __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
                                                   uint64_t N, uint64_t off, uint64_t n,
                                                   const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
-                                                  uint32_t* __restrict__ bmax, uint64_t nblk,
-                                                  const uint32_t* __restrict__ tab) {
+                                                  uint32_t* __restrict__ bmax, uint64_t nblk) {
     constexpr int W = (D + 3) / 4, P = W;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
     const bool ok = i < n;
@@ -617,15 +636,7 @@ __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ k
     __shared__ uint32_t s_mn[P][8], s_mx[P][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t pw[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) pw[p] = 0;
-#pragma unroll
-    for (int B = 0; B < D; ++B) {  // the key has D bytes
-        const uint32_t v = (kw[B >> 2] >> (8 * (B & 3))) & 0xffu;
-        const uint32_t* t = tab + (B * 256 + v) * W;
-#pragma unroll
-        for (int p = 0; p < P; ++p) pw[p] |= __ldg(t + p);
-    }
+    morton_deinterleave8<D>(kw, pw);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
         const uint32_t word = pw[p];
@@ -707,14 +718,8 @@ static void launch_quantize_t(zi_ctx* ctx, const double* Y, const unsigned long 
 template <int D>
 static void launch_finalize_t(zi_ctx* ctx, const uint32_t* keyw, const uint32_t* val, uint64_t N, uint64_t off,
                               uint64_t n, const uint32_t* dict, zi_index* idx) {
-    constexpr int W = (D + 3) / 4;
-    if (ctx->deint_D != D) {
-        ctx->deint.ensure(static_cast<size_t>(D) * 256 * W);
-        ZI_LAUNCH(ctx, "deinterleave_table", k_deinterleave_table<D>, D, 256, 0, ctx->deint.p);
-        ctx->deint_D = D;
-    }
     ZI_LAUNCH(ctx, "finalize_index", k_finalize<D>, static_cast<unsigned>(idx->nblk), 256, 0, keyw, val, N, off, n,
-              dict, idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk, ctx->deint.p);
+              dict, idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk);
 }
 
 void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_keys, uint64_t n,

@@ -109,11 +109,9 @@ struct zi_ctx {
     zi::dbuf<uint8_t> scratch;
     zi::dbuf<uint32_t> counter;  // small integer scratch (tile counters etc.)
     zi::dbuf<uint8_t> flush;     // L2 flush buffer (bench hygiene)
-    zi::dbuf<uint32_t> deint;    // Morton de-interleave table of dims deint_D (finalize)
     // hybrid sort depth learnt per (dims, layouts): 0 = from the byte entropies, -1 = all-LSD;
     // raised when a build's MSD split left too many records in oversized segments
     int sort_depth[33][2] = {};
-    int deint_D = 0;
     int flush_toggle = 1;
 };
 
