@@ -189,7 +189,8 @@ __device__ inline void cp_async_wait() {
 
 __global__ void __launch_bounds__(256) k_patch_matrix(const uint8_t* __restrict__ img, int w, int C, int K, int F,
                                                       const uint32_t* __restrict__ keys, uint64_t n, uint64_t npad,
-                                                      uint8_t* __restrict__ XT) {
+                                                      int Fpad, uint8_t* __restrict__ XT) {
+    extern __shared__ int s_off[];  // Fpad byte offsets (-1: zero row, -2: the ones row F)
     __shared__ int s_base[128];
     const int tid = threadIdx.x;
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * 128;
@@ -202,26 +203,24 @@ __global__ void __launch_bounds__(256) k_patch_matrix(const uint8_t* __restrict_
             s_base[tid] = -1;
         }
     }
-    __shared__ __align__(16) uint8_t s_t[32 * 128];
-    __shared__ int s_off[32];
-    if (tid < 32) {
-        const int f = blockIdx.y * 32 + tid;
-        s_off[tid] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : (f == F ? -2 : -1);
-    }
+    for (int f = tid; f < Fpad; f += 256)
+        s_off[f] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : (f == F ? -2 : -1);
     __syncthreads();
-    // gather: a warp reads one feature of 32 consecutive patches (adjacent pixels)
-#pragma unroll 4
-    for (int e = tid; e < 32 * 128; e += 256) {
-        const int bs = s_base[e & 127], of = s_off[e >> 7];
-        uint8_t v = 0;
-        if (bs >= 0 && of >= 0) v = __ldg(img + bs + of);
-        else if (bs >= 0 && of == -2) v = 1;  // row F: all ones (the tensor-core path's first moments)
-        s_t[e] = v;
+    // 8 threads per feature, 16 consecutive patches (adjacent pixels) each: 16 gathered bytes ->
+    // one 16-byte store; a warp writes 4 features x 128 patches
+    const int g = tid & 7;
+    for (int f = tid >> 3; f < Fpad; f += 32) {
+        const int of = s_off[f];
+        uint32_t wv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int bs = s_base[16 * g + i];
+            uint32_t v = 0;
+            if (bs >= 0) v = of >= 0 ? static_cast<uint32_t>(__ldg(img + bs + of)) : (of == -2 ? 1u : 0u);
+            wv[i >> 2] |= v << (8 * (i & 3));
+        }
+        *reinterpret_cast<uint4*>(XT + static_cast<size_t>(f) * npad + p0 + 16 * g) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
     }
-    __syncthreads();
-    const int fl = tid >> 3, c16 = (tid & 7) * 16;
-    *reinterpret_cast<uint4*>(XT + static_cast<size_t>(blockIdx.y * 32 + fl) * npad + p0 + c16) =
-        *reinterpret_cast<const uint4*>(s_t + fl * 128 + c16);
 }
 
 __global__ void __launch_bounds__(256) k_moments(const uint8_t* __restrict__ XT, uint64_t npad, int F, int ntile,
@@ -335,8 +334,8 @@ void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const
     const int Fpad = ntile * kMomTile;
     const uint64_t npad = (n + kMomStage - 1) / kMomStage * kMomStage;
     uint8_t* XT = ctx->scratch.ensure(static_cast<size_t>(Fpad) * npad);
-    ZI_LAUNCH(ctx, "patch_matrix", k_patch_matrix, dim3(static_cast<unsigned>(npad / 128), Fpad / 32), 256, 0, d_img,
-              w, C, K, F, d_keys, n, npad, XT);
+    ZI_LAUNCH(ctx, "patch_matrix", k_patch_matrix, static_cast<unsigned>(npad / 128), 256, Fpad * sizeof(int), d_img, w,
+              C, K, F, d_keys, n, npad, Fpad, XT);
     static const bool use_mma = std::getenv("ZI_MOMENTS_MMA") != nullptr;  // legacy mma.sync path (A/B checks)
     if (!use_mma) {
         gram_u8_tc(ctx, XT, F, Fpad, npad, d_out);
