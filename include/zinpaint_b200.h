@@ -231,6 +231,49 @@ zi_status zi_query_best_patch(zi_multi_index* mi, const uint8_t* target_values,
 zi_status zi_brute_force_best(zi_multi_index* mi, const uint8_t* target_values,
                               const uint8_t* target_known, int32_t norm, zi_best_patch* out);
 
+/* masked-cost refine of a caller-given candidate list: the refine step of query_best_patch
+ * (engine.cpp:195-212) on its own, for the sharded query (the per-shard k-NN lists are merged
+ * by the host, then the global top-k is refined here).  cands: packed (dist<<32 | key) */
+zi_status zi_refine_best(zi_multi_index* mi, const uint8_t* target_values, const uint8_t* target_known,
+                         const uint64_t* cands, uint32_t count, int32_t norm, zi_best_patch* out);
+
+/* ---- range-partitioned multi_index over G ranks ----
+ * No reference counterpart (the reference is one host process); the result is rank r holding
+ * positions shard_ranges(n, G)[r] of every layout of multi_index::build (builder.cpp:202-224),
+ * byte-identical.  The caller runs the collectives between the stages (sharding.py: NCCL over
+ * torch.distributed); d_* are DEVICE pointers (the send buffers are owned by the shard, valid
+ * until the next stage; the receive buffers are the caller's).  Stages, in order:
+ *   create -> moments (all-reduce SUM of F+F*F int64) -> fit_project (all-reduce MIN lo, MAX hi:
+ *   8*dims order-preserving int64 each) -> quantize_sort (all-gather 8*S sample rows of words+1
+ *   u32) -> zi_shard_splitters -> partition (all-gather counts [G][8]; all-to-all records,
+ *   words+1 u32 each) -> receive (all-gather counts2; all-to-all) -> finish.
+ * After finish, zi_shard_multi_index() is a multi_index whose 8 indices and dictionary are this
+ * rank's slice: zi_query_best_patch with knn_out gives the local k-NN list, zi_brute_force_best
+ * scans the slice, zi_refine_best refines a merged list. */
+typedef struct zi_shard zi_shard;
+zi_status zi_shard_create(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h,
+                          int32_t C, const zi_index_config* cfg, int32_t rank, int32_t world, zi_shard** out);
+zi_status zi_shard_destroy(zi_shard* sh);
+/* info[10]: n_total, row_begin, row_end, F, dims, words, rank, world, stage, records held */
+zi_status zi_shard_info(const zi_shard* sh, uint64_t* info);
+zi_status zi_shard_moments(zi_shard* sh, int64_t* moments_out);
+zi_status zi_shard_fit_project(zi_shard* sh, const int64_t* moments, int64_t* lo_out, int64_t* hi_out);
+zi_status zi_shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uint32_t samples_per_layout,
+                                 uint32_t* samples_out);
+/* host only: G-1 splitters per layout from all ranks' samples (count rows) */
+zi_status zi_shard_splitters(const uint32_t* samples, uint64_t count, int32_t words, int32_t world,
+                             uint32_t* splitters_out);
+zi_status zi_shard_partition(zi_shard* sh, const uint32_t* splitters, uint64_t* counts_out,
+                             const uint32_t** d_send);
+/* host only: what rank `me` sends where after the first exchange (all_counts [src][dst][8]) */
+zi_status zi_shard_rebalance_plan(const uint64_t* all_counts, int32_t world, uint64_t n_total, int32_t me,
+                                  uint64_t* send_counts, uint64_t* send_starts);
+zi_status zi_shard_receive(zi_shard* sh, const uint32_t* d_recv, const uint64_t* all_counts,
+                           uint64_t* counts2_out, const uint32_t** d_send2);
+zi_status zi_shard_finish(zi_shard* sh, const uint32_t* d_recv2, const uint64_t* all_counts2);
+/* borrowed multi_index view of the shard (valid until zi_shard_destroy) */
+zi_status zi_shard_multi_index(zi_shard* sh, zi_multi_index** out);
+
 /* ---- inpaint (engine.hpp:112-118, engine.cpp:442-506) ----
  * records: capacity `cap` (the iteration count never exceeds the unknown pixel count). */
 zi_status zi_inpaint(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t width,

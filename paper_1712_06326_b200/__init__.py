@@ -411,9 +411,9 @@ class MultiIndex:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h:
+        if h and not getattr(self, "_borrowed", False):
             lib().zi_multi_index_destroy(h)
-            self.h = None
+        self.h = None
 
 
 # ------------------------------------------------------------------ reference binding mirror

@@ -108,6 +108,20 @@ SIGNATURES = {
     "zi_multi_index_moments": (C.c_int, [vp, i64p, i64p]),
     "zi_query_best_patch": (C.c_int, [vp, u8p, u8p, C.c_uint32, C.c_int32, C.POINTER(BestPatch), u64p]),
     "zi_brute_force_best": (C.c_int, [vp, u8p, u8p, C.c_int32, C.POINTER(BestPatch)]),
+    "zi_refine_best": (C.c_int, [vp, u8p, u8p, u64p, C.c_uint32, C.c_int32, C.POINTER(BestPatch)]),
+    "zi_shard_create": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig), C.c_int32,
+                                  C.c_int32, C.POINTER(vp)]),
+    "zi_shard_destroy": (C.c_int, [vp]),
+    "zi_shard_info": (C.c_int, [vp, u64p]),
+    "zi_shard_moments": (C.c_int, [vp, i64p]),
+    "zi_shard_fit_project": (C.c_int, [vp, i64p, i64p, i64p]),
+    "zi_shard_quantize_sort": (C.c_int, [vp, i64p, i64p, C.c_uint32, u32p]),
+    "zi_shard_splitters": (C.c_int, [u32p, C.c_uint64, C.c_int32, C.c_int32, u32p]),
+    "zi_shard_partition": (C.c_int, [vp, u32p, u64p, C.POINTER(vp)]),
+    "zi_shard_rebalance_plan": (C.c_int, [u64p, C.c_int32, C.c_uint64, C.c_int32, u64p, u64p]),
+    "zi_shard_receive": (C.c_int, [vp, vp, u64p, u64p, C.POINTER(vp)]),
+    "zi_shard_finish": (C.c_int, [vp, vp, u64p]),
+    "zi_shard_multi_index": (C.c_int, [vp, C.POINTER(vp)]),
     "zi_inpaint": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig),
                              C.POINTER(InpaintConfig), u8p, C.POINTER(IterationRecord), C.c_uint64, u64p,
                              C.POINTER(RunStats)]),

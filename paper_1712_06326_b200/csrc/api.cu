@@ -578,6 +578,7 @@ zi_status zi_vector_knn_batch(zi_vector_index* vi, const float* queries, const u
 zi_status zi_multi_index_save(zi_multi_index* mi, const char* path) {
     return guard(mi ? mi->ctx : nullptr, [&] {
         require(mi && path, "null argument");
+        require(!mi->shard, "ZIDX1 holds whole layout indices; save the unsharded multi_index");
         zi::save_multi_index(mi, path);
     });
 }
@@ -609,6 +610,7 @@ zi_status zi_multi_index_load(zi_ctx* ctx, const char* path, const uint8_t* imag
 zi_status zi_multi_index_rebuild(zi_multi_index* mi) {
     return guard(mi ? mi->ctx : nullptr, [&] {
         require(mi && !mi->loaded, "rebuild needs the build inputs; this index was loaded from a file");
+        require(!mi->shard, "a shard is built by the zi_shard_* stages");
         zi::build_multi_index(mi);
     });
 }
@@ -644,7 +646,7 @@ zi_status zi_multi_index_get_info(const zi_multi_index* mi, zi_multi_index_info*
 
 zi_status zi_multi_index_dictionary(zi_multi_index* mi, uint32_t* keys_out) {
     return guard(mi ? mi->ctx : nullptr, [&] {
-        ZI_CUDA(cudaMemcpyAsync(keys_out, mi->dict.p, mi->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, mi->ctx->stream));
+        ZI_CUDA(cudaMemcpyAsync(keys_out, mi->dict.p + mi->row_begin, mi->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, mi->ctx->stream));
         ZI_CUDA(cudaStreamSynchronize(mi->ctx->stream));
     });
 }
@@ -715,6 +717,120 @@ zi_status zi_brute_force_best(zi_multi_index* mi, const uint8_t* tv, const uint8
     });
 }
 
+zi_status zi_refine_best(zi_multi_index* mi, const uint8_t* tv, const uint8_t* tk, const uint64_t* cands, uint32_t count,
+                         int32_t norm, zi_best_patch* out) {
+    return guard(mi ? mi->ctx : nullptr, [&] {
+        require(mi && tv && tk && out && (cands || count == 0), "null argument");
+        require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
+        const uint64_t b = zi::refine_candidates(mi, tv, tk, cands, count, norm);
+        out->key = static_cast<uint32_t>(b & 0xffffffffu);
+        out->cost = static_cast<uint32_t>(b >> 32);
+        out->error = norm == ZI_NORM_L2 ? std::sqrt(static_cast<double>(out->cost)) : static_cast<double>(out->cost);
+        out->layout_id = 0;
+        out->candidates = count;
+    });
+}
+
+// ---------------------------------------------------------------- range-partitioned shards
+zi_status zi_shard_create(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h, int32_t C,
+                          const zi_index_config* cfg, int32_t rank, int32_t world, zi_shard** out) {
+    return guard(ctx, [&] {
+        require(out != nullptr, "null argument");
+        require(world >= 1 && world <= 64 && rank >= 0 && rank < world, "shard: rank / world out of range");
+        zi_multi_index* mi = new_multi_index(ctx, image, known, w, h, C, cfg);
+        try {
+            *out = zi::shard_create(mi, rank, world);
+        } catch (...) {
+            delete mi;
+            throw;
+        }
+    });
+}
+
+zi_status zi_shard_destroy(zi_shard* sh) {
+    if (!sh) return ZI_OK;
+    zi_multi_index* mi = zi::shard_multi_index(sh);
+    return guard(mi->ctx, [&] {
+        zi::shard_destroy(sh);
+        zi_multi_index_destroy(mi);
+    });
+}
+
+zi_status zi_shard_info(const zi_shard* sh, uint64_t* info) {
+    return guard([&] {
+        require(sh && info, "null argument");
+        zi::shard_info(sh, info);
+    });
+}
+
+zi_status zi_shard_moments(zi_shard* sh, int64_t* out) {
+    return guard(sh ? zi::shard_multi_index(sh)->ctx : nullptr, [&] {
+        require(sh && out, "null argument");
+        zi::shard_moments(sh, out);
+    });
+}
+
+zi_status zi_shard_fit_project(zi_shard* sh, const int64_t* moments, int64_t* lo, int64_t* hi) {
+    return guard(sh ? zi::shard_multi_index(sh)->ctx : nullptr, [&] {
+        require(sh && moments && lo && hi, "null argument");
+        zi::shard_fit_project(sh, moments, lo, hi);
+    });
+}
+
+zi_status zi_shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uint32_t S, uint32_t* samples) {
+    return guard(sh ? zi::shard_multi_index(sh)->ctx : nullptr, [&] {
+        require(sh && lo && hi && (samples || S == 0), "null argument");
+        require(S <= 65536, "shard: at most 65536 samples per layout");
+        zi::shard_quantize_sort(sh, lo, hi, S, samples);
+    });
+}
+
+zi_status zi_shard_splitters(const uint32_t* samples, uint64_t count, int32_t words, int32_t world, uint32_t* out) {
+    return guard([&] {
+        require((samples || count == 0) && (out || world == 1), "null argument");
+        require(words >= 1 && words <= 8 && world >= 1 && world <= 64, "shard: words / world out of range");
+        zi::shard_splitters(samples, count, words, world, out);
+    });
+}
+
+zi_status zi_shard_partition(zi_shard* sh, const uint32_t* splitters, uint64_t* counts, const uint32_t** d_send) {
+    return guard(sh ? zi::shard_multi_index(sh)->ctx : nullptr, [&] {
+        require(sh && counts && d_send, "null argument");
+        zi::shard_partition(sh, splitters, counts, d_send);
+    });
+}
+
+zi_status zi_shard_rebalance_plan(const uint64_t* all_counts, int32_t world, uint64_t n_total, int32_t me,
+                                  uint64_t* send_counts, uint64_t* send_starts) {
+    return guard([&] {
+        require(all_counts && send_counts && send_starts, "null argument");
+        require(world >= 1 && world <= 64 && me >= 0 && me < world, "shard: rank / world out of range");
+        zi::shard_rebalance_plan(all_counts, world, n_total, me, send_counts, send_starts);
+    });
+}
+
+zi_status zi_shard_receive(zi_shard* sh, const uint32_t* d_recv, const uint64_t* all_counts, uint64_t* counts2,
+                           const uint32_t** d_send2) {
+    return guard(sh ? zi::shard_multi_index(sh)->ctx : nullptr, [&] {
+        require(sh && all_counts && counts2 && d_send2, "null argument");
+        zi::shard_receive(sh, d_recv, all_counts, counts2, d_send2);
+    });
+}
+
+zi_status zi_shard_finish(zi_shard* sh, const uint32_t* d_recv2, const uint64_t* all_counts2) {
+    return guard(sh ? zi::shard_multi_index(sh)->ctx : nullptr, [&] {
+        require(sh && all_counts2, "null argument");
+        zi::shard_finish(sh, d_recv2, all_counts2);
+    });
+}
+
+zi_status zi_shard_multi_index(zi_shard* sh, zi_multi_index** out) {
+    return guard([&] {
+        require(sh && out, "null argument");
+        *out = zi::shard_multi_index(sh);
+    });
+}
+
 // ---------------------------------------------------------------- inpaint
 static void fill_stats_defaults(zi_run_stats* st) {
     std::memset(st, 0, sizeof(*st));
@@ -763,6 +879,7 @@ zi_status zi_inpaint_with_index(zi_multi_index* mi, const uint8_t* image, const 
                                 zi_iteration_record* records, uint64_t cap, uint64_t* n_records, zi_run_stats* stats) {
     return guard(mi ? mi->ctx : nullptr, [&] {
         require(mi && image && known && cfg && icfg && image_out && n_records && stats, "null argument");
+        require(!mi->shard, "the fill loop needs the whole index (sharding.ShardedMultiIndex.query_best_patch merges shards)");
         fill_stats_defaults(stats);
         *n_records = 0;
         uint64_t unknown = 0;

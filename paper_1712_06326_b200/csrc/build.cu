@@ -88,30 +88,9 @@ void sync_host_model(zi_multi_index* mi) {
     mi->host_model = true;
 }
 
-void build_multi_index(zi_multi_index* mi) {
+void fit_models(zi_multi_index* mi, uint64_t n) {
     zi_ctx* ctx = mi->ctx;
-    const auto wall0 = std::chrono::steady_clock::now();
-    if (!mi->ev0) {
-        ZI_CUDA(cudaEventCreate(&mi->ev0));
-        ZI_CUDA(cudaEventCreate(&mi->ev1));
-    }
-    ZI_CUDA(cudaEventRecord(mi->ev0, ctx->stream));
-    const int K = mi->K, C = mi->C, w = mi->w, h = mi->h;
-
-    // K1
-    mi->n = collect_dictionary(ctx, mi->known.p, w, h, K, mi->dict);
-    if (mi->n == 0) throw error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
-    const uint64_t n = mi->n;
-    mi->dims = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(mi->cfg.dims),
-                                                   std::min<uint64_t>(static_cast<uint64_t>(mi->mc), n)));
-    const int D = mi->dims, mc = mi->mc, m = mi->m;
-
-    // K2
-    const int F = K * K * C;
-    mi->F = F;
-    const size_t nmom = static_cast<size_t>(F) + static_cast<size_t>(F) * F;
-    mi->moments.ensure(nmom);
-    patch_moments(ctx, mi->image.p, w, C, K, mi->dict.p, n, mi->moments.p);
+    const int K = mi->K, C = mi->C, F = mi->F, D = mi->dims, mc = mi->mc, m = mi->m;
     mi->pca_mean.ensure(static_cast<size_t>(8) * mc);
     mi->pca_comp.ensure(static_cast<size_t>(8) * mc * D);
     mi->host_model = false;
@@ -168,6 +147,34 @@ void build_multi_index(zi_multi_index* mi) {
         mi->host_model = true;
     }
     mi->eigen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - te0).count();
+
+}
+
+void build_multi_index(zi_multi_index* mi) {
+    zi_ctx* ctx = mi->ctx;
+    const auto wall0 = std::chrono::steady_clock::now();
+    if (!mi->ev0) {
+        ZI_CUDA(cudaEventCreate(&mi->ev0));
+        ZI_CUDA(cudaEventCreate(&mi->ev1));
+    }
+    ZI_CUDA(cudaEventRecord(mi->ev0, ctx->stream));
+    const int K = mi->K, C = mi->C, w = mi->w, h = mi->h;
+
+    // K1
+    mi->n = collect_dictionary(ctx, mi->known.p, w, h, K, mi->dict);
+    if (mi->n == 0) throw error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
+    const uint64_t n = mi->n;
+    mi->dims = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(mi->cfg.dims),
+                                                   std::min<uint64_t>(static_cast<uint64_t>(mi->mc), n)));
+    const int D = mi->dims, mc = mi->mc, m = mi->m;
+
+    // K2
+    const int F = K * K * C;
+    mi->F = F;
+    const size_t nmom = static_cast<size_t>(F) + static_cast<size_t>(F) * F;
+    mi->moments.ensure(nmom);
+    patch_moments(ctx, mi->image.p, w, C, K, mi->dict.p, n, mi->moments.p);
+    fit_models(mi, n);
 
     mi->minmax.ensure(static_cast<size_t>(8) * 2 * D);
 

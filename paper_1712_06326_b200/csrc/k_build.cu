@@ -541,8 +541,8 @@ __device__ __forceinline__ void morton_deinterleave8(const uint32_t (&kw)[(D + 3
 template <int D>
 __global__ void __launch_bounds__(256) k_quantize(const double* __restrict__ Y,
                                                   const unsigned long long* __restrict__ minmax, uint64_t n,
-                                                  uint64_t N, uint32_t layout, uint32_t* __restrict__ keyw,
-                                                  uint32_t* __restrict__ val) {
+                                                  uint64_t N, uint32_t layout, uint32_t row_base,
+                                                  uint32_t* __restrict__ keyw, uint32_t* __restrict__ val) {
     constexpr int W = (D + 3) / 4;
     __shared__ double s_lo[D], s_hi[D], s_rcp[D];
     // spread table: bit L of q -> bit L*D (W words); dim d's contribution is spread(q) << (D-1-d)
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(256) k_quantize(const double* __restrict__ Y,
         const uint64_t e = static_cast<uint64_t>(layout) * n + i;
 #pragma unroll
         for (int k = 0; k < W; ++k) keyw[static_cast<size_t>(k) * N + e] = kw[k];
-        val[e] = (layout << 29) | static_cast<uint32_t>(i);
+        val[e] = (layout << 29) | (row_base + static_cast<uint32_t>(i));
     }
 }
 
@@ -688,9 +688,9 @@ static void launch_project_t(zi_ctx* ctx, const uint8_t* img, int w, int C, cons
 
 template <int D>
 static void launch_quantize_t(zi_ctx* ctx, const double* Y, const unsigned long long* mm, uint64_t n, uint64_t N,
-                              uint32_t layout, uint32_t* keyw, uint32_t* val) {
+                              uint32_t layout, uint32_t row_base, uint32_t* keyw, uint32_t* val) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 16));
-    ZI_LAUNCH(ctx, "quantize_interleave", k_quantize<D>, grid, 256, 0, Y, mm, n, N, layout, keyw, val);
+    ZI_LAUNCH(ctx, "quantize_interleave", k_quantize<D>, grid, 256, 0, Y, mm, n, N, layout, row_base, keyw, val);
 }
 
 #define ZI_DIMS_SWITCH(D, FN, ...)                                                        \
@@ -733,9 +733,9 @@ void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_
 }
 
 void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax, uint64_t n, uint64_t N,
-                         uint32_t layout, int D, uint32_t* d_keyw, uint32_t* d_val) {
+                         uint32_t layout, int D, uint32_t* d_keyw, uint32_t* d_val, uint32_t row_base) {
     if (n == 0) return;
-    ZI_DIMS_SWITCH(D, launch_quantize_t, ctx, d_Y, d_minmax, n, N, layout, d_keyw, d_val);
+    ZI_DIMS_SWITCH(D, launch_quantize_t, ctx, d_Y, d_minmax, n, N, layout, row_base, d_keyw, d_val);
 }
 
 void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_keys_in, uint64_t n, int D,

@@ -2140,12 +2140,43 @@ uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t
     ZI_CUDA(cudaMemsetAsync(&s.ws->best, 0xff, sizeof(unsigned long long), ctx->stream));
     const size_t smem = ((KK * mi->C + 1) & ~size_t(1)) + KK * sizeof(uint16_t) + 16;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((mi->n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
-    ZI_LAUNCH(ctx, "brute_force", k_brute, grid, 256, smem, mi->image.p, mi->w, mi->C, mi->K, mi->dict.p, mi->n, s.target,
-              norm, &s.ws->best);
+    ZI_LAUNCH(ctx, "brute_force", k_brute, grid, 256, smem, mi->image.p, mi->w, mi->C, mi->K, mi->dict.p + mi->row_begin,
+              mi->n, s.target, norm, &s.ws->best);
     unsigned long long* hb = reinterpret_cast<unsigned long long*>(stage + res_off);
     ZI_CUDA(cudaMemcpyAsync(hb, &s.ws->best, 8, cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     return *hb;
+}
+
+// masked-cost refine of a caller-given candidate list (query_best_patch's refine step,
+// proj/src/engine.cpp:195-212): the sharded query merges the per-shard k-NN lists on the host
+// and refines the global top-k here.  Returns packed (cost<<32 | key), UINT64_MAX if empty.
+uint64_t refine_candidates(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, const uint64_t* h_cands,
+                           uint32_t count, int norm) {
+    zi_ctx* ctx = mi->ctx;
+    if (count == 0) return ~0ull;
+    const size_t KK = static_cast<size_t>(mi->K) * mi->K;
+    const size_t tbytes = KK * mi->C + KK;
+    const query_scratch s = carve(mi->qscratch, ctx, 1, count, tbytes);
+    mi->qws_clean = false;  // the fill-loop workspace is reused below
+    const size_t res_off = (tbytes + 255) & ~size_t(255);
+    const size_t list_off = res_off + ((sizeof(qws) + 255) & ~size_t(255));
+    uint8_t* stage = mi->hstage.ensure(list_off + count * sizeof(uint64_t));
+    std::memcpy(stage, h_tv, KK * mi->C);
+    std::memcpy(stage + KK * mi->C, h_tk, KK);
+    std::memcpy(stage + list_off, h_cands, count * sizeof(uint64_t));
+    qws* hq = reinterpret_cast<qws*>(stage + res_off);
+    std::memset(hq, 0, sizeof(qws));
+    hq->count = count;
+    hq->best = ~0ull;
+    ZI_CUDA(cudaMemcpyAsync(s.target, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(s.ws, hq, sizeof(qws), cudaMemcpyHostToDevice, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(s.out, stage + list_off, count * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    const size_t rsmem = ((KK * mi->C + 1) & ~size_t(1)) + (KK + 16) * sizeof(uint16_t) + kRefineSlots * sizeof(uint32_t) + 32;
+    ZI_LAUNCH(ctx, "refine", k_refine, 1, 1024, rsmem, mi->image.p, mi->w, mi->C, mi->K, s.target, s.ws, s.out, norm);
+    ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    return hq->best;
 }
 
 }  // namespace zi

@@ -172,6 +172,11 @@ struct zi_multi_index {
     bool build_ms_pending = false;
     bool loaded = false;                 // read from a ZIDX1 file (no mask, no moments)
     bool device_pca = false;             // last build solved the eigenproblems on the device
+    // range-partitioned shard (shard.cu): this handle's indices hold one contiguous Morton range
+    // of every layout and its dictionary slice is rows [row_begin, row_begin + n) of the n_total
+    // dictionary rows in dict (every rank keeps the whole dictionary: payload rows are global)
+    bool shard = false;
+    uint64_t row_begin = 0, n_total = 0;
     zi_layout_state L[8];
 };
 
@@ -213,9 +218,11 @@ void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_
              double* d_Y, unsigned long long* d_minmax);
 
 // quantise + Morton interleave -> key words (SoA, W words) + payload = dictionary key
-// (records of all layouts in one array of N entries; this layout's entries start at layout*n)
+// (records of all layouts in one array of N entries; this layout's entries start at layout*n;
+// payload row = row_base + i, row_base > 0 for a shard's slice of the dictionary)
 void quantize_interleave(zi_ctx* ctx, const double* d_Y, const unsigned long long* d_minmax, uint64_t n,
-                         uint64_t N, uint32_t layout, int D, uint32_t* d_keyw, uint32_t* d_val);
+                         uint64_t N, uint32_t layout, int D, uint32_t* d_keyw, uint32_t* d_val,
+                         uint32_t row_base = 0);
 // row-major coords (n*D) -> Morton key words + payload copy
 void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_keys_in, uint64_t n,
                        int D, uint32_t* d_keyw, uint32_t* d_val);
@@ -246,6 +253,9 @@ struct query_result {
 query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk,
                               uint32_t k, int norm, uint64_t* knn_out);
 uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, int norm);
+// masked-cost refine of a given candidate list (packed dist<<32 | key) -> packed (cost<<32 | key)
+uint64_t refine_candidates(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, const uint64_t* h_cands,
+                           uint32_t count, int norm);
 // knn over a bare index (zcurve_index + query bytes)
 uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm, uint64_t* out);
 void knn_search_batch(zi_index* idx, const uint8_t* h_queries, uint64_t nq, uint32_t k, int norm,
@@ -254,6 +264,23 @@ void knn_search_batch(zi_index* idx, const uint8_t* h_queries, uint64_t nq, uint
 // entries scored, results}
 void knn_batch_device(zi_ctx* ctx, zi_index* idx, const uint8_t* d_queries, uint64_t nq, uint32_t k, int norm,
                       unsigned long long* d_out, uint32_t* d_counts, unsigned long long* d_stats);
+
+// ---- range-partitioned shard (shard.cu) ----
+void shard_ranges(uint64_t n, int world, int r, uint64_t* b, uint64_t* e);
+zi_shard* shard_create(zi_multi_index* mi, int rank, int world);
+void shard_moments(zi_shard* sh, int64_t* out);
+void shard_fit_project(zi_shard* sh, const int64_t* moments, int64_t* lo_out, int64_t* hi_out);
+void shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uint32_t S, uint32_t* samples_out);
+void shard_splitters(const uint32_t* samples, uint64_t count, int W, int world, uint32_t* out);
+void shard_partition(zi_shard* sh, const uint32_t* splitters, uint64_t* counts_out, const uint32_t** d_send);
+void shard_rebalance_plan(const uint64_t* all_counts, int world, uint64_t n_total, int me, uint64_t* send_counts,
+                          uint64_t* send_starts);
+void shard_receive(zi_shard* sh, const uint32_t* d_recv, const uint64_t* all_counts, uint64_t* counts2_out,
+                   const uint32_t** d_send2);
+void shard_finish(zi_shard* sh, const uint32_t* d_recv2, const uint64_t* all_counts2);
+zi_multi_index* shard_multi_index(zi_shard* sh);
+void shard_destroy(zi_shard* sh);
+void shard_info(const zi_shard* sh, uint64_t* v);
 
 // ---- host pieces ----
 int subset_pixel_count(int K, double c);
@@ -264,6 +291,9 @@ void pca_fit_layout(const std::vector<int64_t>& s, const std::vector<int64_t>& S
                     const std::vector<int32_t>& cols, int dims, std::vector<double>& mean,
                     std::vector<double>& comp /* dims*mc, row d */, std::vector<double>& eig);
 void build_multi_index(zi_multi_index* mi);
+// the 8 PCA models from the moments already in mi->moments over n_total patches (device solve,
+// host fallback for mc > 224); leaves mi->pca_mean / pca_comp on the device
+void fit_models(zi_multi_index* mi, uint64_t n_total);
 // copy the moments, the 8 PCA models and the quantiser ranges to the host mirror (lazy: only
 // the accessors need them); finish_build_timing reads the build's event pair
 void sync_host_model(zi_multi_index* mi);

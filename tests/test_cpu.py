@@ -439,3 +439,108 @@ def test_shard_ranges_cover():
             assert r[0][0] == 0 and r[-1][1] == n and all(r[i][1] == r[i + 1][0] for i in range(w - 1))
     lists = [np.array([5, 9], np.uint64), np.array([1, 7, 8], np.uint64), np.array([], np.uint64)]
     assert np.array_equal(sharding.merge_topk(lists, 3), [1, 5, 7])
+
+
+# ------------------------------------------------------------------ sharded build (§8(e)) on CPU
+def _shard_case():
+    img, known = workloads.small_image(40, 46, 1, seed=3, hole_frac=0.1)
+    return img, known, 5, 0.6, 6
+
+
+def _check_sharded(outs, world):
+    """Concatenated shard indices == the oracle's single-host multi_index::build."""
+    from paper_1712_06326_b200 import sharding
+    img, known, K, cov, D = _shard_case()
+    om = oracle.MultiIndex(img, known, K, cov, D)
+    ranges = sharding.shard_ranges(om.n, world)
+    for l in range(8):
+        ref = om.index(l)
+        for r in range(world):
+            b, e = ranges[r]
+            c, k = outs[r][l]
+            assert np.array_equal(c, ref.coords[b:e]) and np.array_equal(k, ref.keys[b:e]), (l, r)
+
+
+def _shard_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_1712_06326_b200 import sharding
+    from tests.helpers import OracleShard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        img, known, K, cov, D = _shard_case()
+        sh = OracleShard(img, known, K, cov, D, rank, world)
+        info = sharding.build_sharded([sh], sharding.TorchComm(), samples=8)
+        q.put((rank, {l: sh.index_arrays(l) for l in range(8)}, info))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_build_gloo_world2():
+    """Two processes over gloo run the sample-sort build (moments SUM, lo/hi MIN/MAX, sample
+    all-gather, two all-to-alls); rank r holds exactly positions shard_ranges(n, 2)[r]."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    outs = {r: o for r, o, _ in got}
+    _check_sharded(outs, 2)
+    assert got[0][2]["records_exchanged"] > 0
+
+
+@pytest.mark.parametrize("world", [1, 3, 5])
+def test_sharded_build_loopback_cpu(world):
+    from paper_1712_06326_b200 import sharding
+    from tests.helpers import OracleShard
+    img, known, K, cov, D = _shard_case()
+    shards = [OracleShard(img, known, K, cov, D, r, world) for r in range(world)]
+    sharding.build_sharded(shards, sharding.LoopbackComm(world), samples=4)
+    _check_sharded({r: {l: sh.index_arrays(l) for l in range(8)} for r, sh in enumerate(shards)}, world)
+
+
+def test_shard_splitters_and_rebalance_plan():
+    from paper_1712_06326_b200 import sharding
+    rng = np.random.default_rng(9)
+    W = 2
+    rows = rng.integers(0, 2**32, size=(300, W + 1), dtype=np.uint64).astype(np.uint32)
+    rows[:, W] = (rng.integers(0, 8, 300).astype(np.uint32) << 29) | np.arange(300, dtype=np.uint32)
+    rows[:5, W] = 0xFFFFFFFF  # "no sample" rows are ignored
+    for world in (1, 2, 4, 7):
+        sp = sharding.splitters_from_samples([rows], W, world)
+        assert sp.shape == (8 * (world - 1), W + 1)
+        for l in range(8):
+            mine = rows[(rows[:, W] != 0xFFFFFFFF) & ((rows[:, W] >> 29) == l)]
+            comp = sorted((int(r[1]) << 64) | (int(r[0]) << 32) | int(r[2]) for r in mine)
+            for j in range(1, world):
+                r = sp[l * (world - 1) + j - 1]
+                assert (int(r[1]) << 64) | (int(r[0]) << 32) | int(r[2]) == comp[j * len(comp) // world]
+    # plan: every rank's held range is cut exactly at the shard_ranges boundaries
+    for world in (1, 2, 3, 5):
+        n = 1000 + world
+        all_counts = rng.integers(0, 60, size=(world, world, 8)).astype(np.uint64)
+        all_counts[-1, -1, :] += np.uint64(n) - all_counts.sum(axis=(0, 1))  # every layout totals n
+        ranges = sharding.shard_ranges(n, world)
+        recv = np.zeros((world, 8), dtype=np.uint64)
+        for me in range(world):
+            cnt, st = sharding.rebalance_plan(all_counts, world, n, me)
+            held = all_counts[:, me, :].sum(0)
+            assert np.array_equal(cnt.sum(0), held)
+            recv += cnt
+        for g in range(world):
+            assert np.all(recv[g] == ranges[g][1] - ranges[g][0])
+
+
+def test_ordered_i64_roundtrip_and_order():
+    from paper_1712_06326_b200 import sharding
+    x = np.array([-np.inf, -1e300, -2.5, -0.0, 0.0, 1e-300, 3.0, np.inf])
+    o = sharding.double_to_ordered_i64(x)
+    assert np.all(np.diff(o) > 0)
+    assert np.array_equal(sharding.ordered_i64_to_double(o).view(np.uint64), x.view(np.uint64))

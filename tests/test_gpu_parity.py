@@ -635,3 +635,77 @@ def test_build_deterministic_repeats(zb):
             continue
         for a, b in zip(ref, got):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ------------------------------------------------------------------ range-partitioned shards (§8(e))
+def _sharded(zb, img, known, cfg, world, samples=64):
+    from paper_1712_06326_b200 import sharding
+    shards = [sharding.DeviceShard(img, known, cfg, r, world) for r in range(world)]
+    info = sharding.build_sharded(shards, sharding.LoopbackComm(world), samples=samples)
+    return sharding, shards, info
+
+
+@pytest.mark.parametrize("world,channels,dims,samples", [(1, 1, 8, 64), (2, 1, 8, 64), (3, 3, 12, 16),
+                                                         (4, 1, 4, 4), (5, 3, 8, 256)])
+def test_sharded_build_equals_single_gpu_build(zb, world, channels, dims, samples):
+    """Rank r's layout-l shard == positions shard_ranges(n, G)[r] of the single-GPU layout-l index
+    (coords, keys), with the same PCA models and quantiser ranges on every rank."""
+    img, known = workloads.small_image(72, 88, channels, seed=11 + world, hole_frac=0.08)
+    cfg = zb.index_config(patch_size=9 if channels == 1 else 7, dims=dims, knn=24)
+    mi = zb.MultiIndex(img, known, cfg)
+    sharding, shards, info = _sharded(zb, img, known, cfg, world, samples)
+    ranges = sharding.shard_ranges(mi.n, world)
+    for r, sh in enumerate(shards):
+        assert (sh.row_begin, sh.row_end) == ranges[r]
+        assert sh.multi_index.n == ranges[r][1] - ranges[r][0]
+        assert np.array_equal(sh.multi_index.dictionary, mi.dictionary[ranges[r][0]:ranges[r][1]])
+    for l in range(8):
+        c, k = mi.index_arrays(l)
+        ref = mi.layout(l)
+        for r, sh in enumerate(shards):
+            b, e = ranges[r]
+            cs, ks = sh.multi_index.index_arrays(l)
+            assert np.array_equal(cs, c[b:e]) and np.array_equal(ks, k[b:e]), (l, r)
+            lay = sh.multi_index.layout(l)
+            for f in ("mean", "components", "eigenvalues", "lo", "hi"):
+                assert np.array_equal(lay[f].view(np.uint64), ref[f].view(np.uint64)), (l, r, f)
+    if world > 1:
+        assert info["records_exchanged"] > 0
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_query_and_brute_force_equal_single_gpu(zb, world):
+    """Merged per-shard k-NN + one refine == query_best_patch on the whole index; packed-min of
+    the per-slice scans == brute_force_best (winner key and cost, every target)."""
+    img, known = workloads.small_image(80, 96, 3, seed=21, hole_frac=0.1)
+    cfg = zb.index_config(patch_size=7, dims=8, knn=32)
+    mi = zb.MultiIndex(img, known, cfg)
+    sharding, shards, _ = _sharded(zb, img, known, cfg, world)
+    comm = sharding.LoopbackComm(world)
+    targets = fillfront(known)[:12]
+    assert len(targets) > 0
+    for (x, y) in targets:
+        tv, tk = oracle.extract_patch_clamped(img, known, int(x), int(y), 7)
+        for k in (1, 32, 200):
+            want = mi.query_best_patch(tv, tk, k)
+            got = sharding.sharded_query(shards, comm, tv, tk, k, 0)
+            for g in got:
+                assert (g[0], g[1], g[3], g[4]) == (want[0], want[1], want[3], want[4]), (x, y, k)
+        bw = mi.brute_force_best(tv, tk)
+        for g in sharding.sharded_brute_force(shards, comm, tv, tk, 0):
+            assert g == (bw[0], bw[1])
+
+
+def test_sharded_build_cfg1(zb):
+    """cfg1 (256^2 gray, 48^2 hole, K=9, D=8) over 4 shards == the single-GPU build."""
+    img, known, _ = workloads.cfg1()
+    cfg = zb.index_config(patch_size=9, dims=8, knn=80)
+    mi = zb.MultiIndex(img, known, cfg)
+    sharding, shards, info = _sharded(zb, img, known, cfg, 4, samples=256)
+    for l in range(8):
+        c, k = mi.index_arrays(l)
+        cs = np.concatenate([sh.multi_index.index_arrays(l)[0] for sh in shards])
+        ks = np.concatenate([sh.multi_index.index_arrays(l)[1] for sh in shards])
+        assert np.array_equal(cs, c) and np.array_equal(ks, k), l
+    # the rebalancing exchange only moves the sample-sort imbalance
+    assert info["records_rebalanced"] < info["records_exchanged"]
