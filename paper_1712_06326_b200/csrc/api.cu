@@ -116,7 +116,7 @@ static void upload_layouts(zi_multi_index* mi) {
 
 static void upload_image(zi_multi_index* mi, const uint8_t* image, const uint8_t* known) {
     const size_t npx = static_cast<size_t>(mi->w) * mi->h;
-    mi->image.ensure(npx * mi->C);
+    mi->image.ensure(npx * mi->C + 16);  // +16: aligned word loads past the last byte (k_proj_tc gather)
     mi->known.ensure(npx);
     ZI_CUDA(cudaMemcpyAsync(mi->image.p, image, npx * mi->C, cudaMemcpyHostToDevice, mi->ctx->stream));
     ZI_CUDA(cudaMemcpyAsync(mi->known.p, known, npx, cudaMemcpyHostToDevice, mi->ctx->stream));

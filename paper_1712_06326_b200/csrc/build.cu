@@ -183,17 +183,19 @@ void build_multi_index(zi_multi_index* mi) {
     const int W = (D + 3) / 4;
     const uint64_t N = 8 * n;
     if (N > (1ull << 30)) throw error(ZI_E_INVALID, "dictionary above 2^27 patches");
-    mi->proj.ensure(static_cast<size_t>(D) * n);
     zi::dbuf<uint32_t>& recs = mi->recs;
     recs.ensure(static_cast<size_t>(W + 1) * N);
     uint32_t* keyw = recs.p;
     uint32_t* val = recs.p + static_cast<size_t>(W) * N;
-    for (int l = 0; l < 8; ++l) {
-        unsigned long long* mm = mi->minmax.p + static_cast<size_t>(l) * 2 * D;
-        project(ctx, mi->image.p, w, C, mi->dict.p, n, mi->layout_off.p + static_cast<size_t>(l) * m, m,
-                mi->pca_mean.p + static_cast<size_t>(l) * mc, mi->pca_comp.p + static_cast<size_t>(l) * mc * D, D,
-                mi->proj.p, mm);
-        quantize_interleave(ctx, mi->proj.p, mm, n, N, static_cast<uint32_t>(l), D, keyw, val);
+    if (!project_quantize_tc(mi, keyw, val, N)) {
+        for (int l = 0; l < 8; ++l) {
+            unsigned long long* mm = mi->minmax.p + static_cast<size_t>(l) * 2 * D;
+            mi->proj.ensure(static_cast<size_t>(D) * n);
+            project(ctx, mi->image.p, w, C, mi->dict.p, n, mi->layout_off.p + static_cast<size_t>(l) * m, m,
+                    mi->pca_mean.p + static_cast<size_t>(l) * mc, mi->pca_comp.p + static_cast<size_t>(l) * mc * D, D,
+                    mi->proj.p, mm);
+            quantize_interleave(ctx, mi->proj.p, mm, n, N, static_cast<uint32_t>(l), D, keyw, val);
+        }
     }
     morton_sort_layouts(ctx, keyw, val, N, D);
     for (int l = 0; l < 8; ++l) {

@@ -1,0 +1,717 @@
+// k_proj_tc.cu -- K3 projection + quantisation on the int8 tensor cores, with an exact fp64
+// fix-up: the same bytes as the canonical fp64 path (k_project + k_quantize, restating
+// proj/src/builder.cpp:159-187 and pca.cpp:7-11), at tensor-core speed.
+//
+// Filter.  Every component c (|c| <= 1) is held as t = rint(c * 2^38), split into five balanced
+// base-256 digits (int8).  For a u8 patch x the five column sums S_k = sum_j x_j digit_k(t_j) are
+// EXACT tcgen05.mma.kind::i8 results (u8 x s8 -> s32, |S_k| <= 255*128*384 < 2^31).  Then
+//     y' = sum_k S_k 2^(8k-38) - M,   M = sum_j mean_j c_j,
+// and |y' - y| <= E = 255 * mc * (2^-39 + 2^-44) for the canonical fp64 value y (the fixed-point
+// truncation bound plus a generous allowance for the fp64 roundings of y, M and y').
+//
+// Two passes over all patches (A tiles gathered from the L2-resident image straight into
+// 128B-swizzled shared memory, no patch matrix in HBM; the digit matrix B stays in shared memory;
+// one CTA per SM, two TMEM accumulators so the epilogue of tile i overlaps the MMAs of tile i+1):
+//   pass 0  exact min / max of y' per (layout, dim)  ->  amin, amax
+//   pass 1  the true lo, hi lie in [amin - E, amin + E], [amax - E, amax + E]; with z' =
+//           255 (y' - amin) / (amax - amin) the reference's quantised value is floor(z' + 1/2)
+//           unless z' + 1/2 is within Bz = 1.01 * 255 * 4E / (amax - amin) of an integer.  Such
+//           (patch, layout) pairs, and the rows within 2E of amin / amax (the only rows that can
+//           hold the true lo / hi), go to a list; everything else writes its Morton record now.
+// Fix-up (k_pt_exact): the listed pairs are projected in the canonical fp64 order (the same
+// sequential fma chain k_project runs on the FP64 MMA), giving the exact lo / hi (atomics over the
+// candidates) and then their exact quantised Morton records.
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace zi {
+
+constexpr int kPtRows = 128;
+constexpr int kPtGatherWarps = 8;                // warps 0-7: two threads per patch row
+constexpr int kPtEpiWarps = 8;                   // warps 8-15: TMEM lane quarter (w & 3), layout parity (w >> 2) & 1
+constexpr int kPtMmaWarp = kPtGatherWarps + kPtEpiWarps;
+constexpr int kPtThreads = (kPtMmaWarp + 1) * 32;
+constexpr int kPtMaxFpad = 384;
+constexpr int kPtMaxN = 256;
+constexpr int kPtDigits = 5;                     // t = rint(c * 2^38) in five balanced base-256 digits
+
+struct pt_params {
+    const uint8_t* img;
+    int w, C, KC, F, Fpad;
+    const uint32_t* keys;
+    uint64_t n;
+    uint32_t row_base;
+    const uint8_t* B;  // this group's digit matrix, pre-swizzled (Npad x Fpad)
+    int Npad, l0, nl;
+    const double* M;          // [8][D]
+    unsigned long long* amm;  // approx min / max of y', ordered u64 [8][2][D]
+    double E;
+    uint32_t* keyw;
+    uint32_t* val;
+    uint64_t Nrec;
+    uint32_t* list;  // (row << 3) | layout
+    uint32_t* list_count;
+    uint64_t ntiles;
+    const int2* wtab;  // Fpad/4 gather words (pt_gather)
+    int abl;           // dev ablation switch (ZI_PT_ABL): 1 no gather, 2 no epilogue math, 4 no MMA
+};
+
+// byte offset of (row r, K-byte f) in a K-major, 128B-swizzled operand of `rows` rows
+__host__ __device__ inline uint32_t sw128_off(int r, int f, int rows) {
+    return static_cast<uint32_t>((f >> 7) * (rows * 128) + (r >> 3) * 1024 + (r & 7) * 128 +
+                                 ((((f & 127) >> 4) ^ (r & 7)) << 4) + (f & 15));
+}
+
+__device__ __forceinline__ uint32_t pt_idesc(int N) {
+    return (2u << 4)        // D format S32
+           | (0u << 7)      // A unsigned 8-bit (u8 patches)
+           | (1u << 10)     // B signed 8-bit (digits)
+           | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(kPtRows >> 4) << 24);
+}
+
+__device__ __forceinline__ void pt_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+// 4 image bytes starting at byte address a (two aligned word loads; the device image carries 16
+// bytes of padding, so the second load never leaves the allocation)
+__device__ __forceinline__ uint32_t pt_ld4(const uint8_t* __restrict__ img, uint32_t a) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(img + (a & ~3u));
+    return __funnelshift_r(__ldg(p), __ldg(p + 1), (a & 3u) * 8u);
+}
+
+// A tile (128 patches x Fpad bytes, feature f = (rr*K + cc)*C + ch at byte f of the row) into the
+// swizzled A buffer.  One thread per patch row (warps 0-3).  Word ow of every row reads the same
+// patch-relative offsets, so they come from a warp-uniform table (pt_word_table): x = offset of
+// the word's first byte (-1: zero word); y = -1 when the 4 bytes lie in one patch row, else
+// (bytes taken from the first row) << 24 | offset of the next patch row (0xffffff: none).
+__device__ __forceinline__ void pt_gather(const pt_params& P, const int2* s_wtab, uint64_t tile, uint32_t sA_addr, int r,
+                                          int c0, int c1) {
+    const uint64_t i = tile * kPtRows + r;
+    uint32_t base = 0;
+    const bool valid = i < P.n;
+    if (valid) {
+        const uint32_t key = __ldg(P.keys + i);
+        base = ((key >> 16) * static_cast<uint32_t>(P.w) + (key & 0xffffu)) * static_cast<uint32_t>(P.C);
+    }
+#pragma unroll 2
+    for (int c = c0; c < c1; ++c) {
+        uint32_t wv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int2 e = s_wtab[4 * c + t];
+            uint32_t word = 0;
+            if (e.x >= 0) {
+                word = pt_ld4(P.img, base + static_cast<uint32_t>(e.x));
+                if (e.y >= 0) {
+                    const uint32_t sh = 8u * (static_cast<uint32_t>(e.y) >> 24), o1 = static_cast<uint32_t>(e.y) & 0xffffffu;
+                    word &= (1u << sh) - 1u;
+                    if (o1 != 0xffffffu) word |= pt_ld4(P.img, base + o1) << sh;
+                }
+            }
+            wv[t] = valid ? word : 0u;
+        }
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sA_addr + sw128_off(r, c << 4, kPtRows)), "r"(wv[0]),
+                     "r"(wv[1]), "r"(wv[2]), "r"(wv[3])
+                     : "memory");
+    }
+}
+
+// Static gather for a compile-time patch shape (K, C): half GH of a patch row (two threads per
+// row).  Every patch row (segment) of K*C bytes is read as aligned words, realigned with one funnel
+// shift per word and placed at its (static) byte position of the feature row; a 16-byte chunk is
+// stored as soon as its last segment is in.  Half 0 stores the chunks that end before segment K/2,
+// half 1 the rest (re-reading the segments the straddling chunk needs).
+template <int K, int C, int GH>
+__device__ __forceinline__ void pt_gather_static(const uint8_t* __restrict__ img, uint32_t base, uint32_t wC, bool valid,
+                                                 uint32_t sA_addr, int r) {
+    constexpr int KC = K * C, F = K * KC, FP = (F + 127) / 128 * 128, NCH = FP / 16;
+    constexpr int KH = K / 2;
+    constexpr int CSPLIT = (KH * KC) / 16;              // first chunk of half 1 (may straddle)
+    constexpr int C0 = GH ? CSPLIT : 0, C1 = GH ? NCH : CSPLIT;
+    constexpr int S0 = GH ? (16 * CSPLIT) / KC : 0, S1 = GH ? K : KH;
+    constexpr int RB = (KC + 3) / 4;                     // realigned words of a segment
+    constexpr int SW = (KC + 6) / 4;                     // aligned words covering it
+    constexpr int NO = 4 * (C1 - C0);                    // output words of this half
+    uint32_t out[NO];
+#pragma unroll
+    for (int i = 0; i < NO; ++i) out[i] = 0u;
+#pragma unroll
+    for (int rr = S0; rr < S1; ++rr) {
+        const uint32_t a = base + static_cast<uint32_t>(rr) * wC;
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(img + (a & ~3u));
+        const uint32_t sh = (a & 3u) * 8u;
+        uint32_t wv[SW];
+#pragma unroll
+        for (int i = 0; i < SW; ++i) wv[i] = valid ? __ldg(wp + i) : 0u;
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            uint32_t x = __funnelshift_r(wv[i], wv[i + 1], sh);
+            if (4 * i + 4 > KC) x &= (1u << (8 * (KC - 4 * i))) - 1u;  // bytes past the segment
+            const int o = rr * KC + 4 * i;                             // output byte of x's byte 0
+            const int ow = o / 4 - 4 * C0, t = o % 4;
+            if (ow >= 0 && ow < NO) out[ow] |= t ? (x << (8 * t)) : x;
+            if (t && ow + 1 >= 0 && ow + 1 < NO) out[ow + 1] |= x >> (32 - 8 * t);
+        }
+        // chunks whose last feature byte lies in this segment (or, past F, after the last one)
+#pragma unroll
+        for (int c = C0; c < C1; ++c) {
+            const int last = (16 * c + 15 < F ? 16 * c + 15 : F - 1) / KC;
+            const int when = 16 * c >= F ? S1 - 1 : (last < S1 ? last : S1 - 1);
+            if (when == rr) {
+                const int q = 4 * (c - C0);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sA_addr + sw128_off(r, c << 4, kPtRows)),
+                             "r"(out[q]), "r"(out[q + 1]), "r"(out[q + 2]), "r"(out[q + 3])
+                             : "memory");
+            }
+        }
+    }
+}
+
+template <int D, int MODE, int KT>
+__global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant__ pt_params P) {
+    constexpr int W = (D + 3) / 4;
+    extern __shared__ uint8_t pt_raw[];
+    uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(pt_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const uint32_t abytes = static_cast<uint32_t>(kPtRows * P.Fpad);
+    uint8_t* sA = sbase;
+    uint8_t* sB = sbase + 2 * abytes;
+    __shared__ __align__(8) uint64_t s_afull[2], s_aempty[2], s_accfull[2], s_accempty[2];
+    __shared__ uint32_t s_tmem;
+    __shared__ double s_M[8][D], s_lo[8][D], s_lo2[8][D], s_hi2[8][D], s_sc[8][D], s_bz[8][D];
+    __shared__ int s_degen[8][D];
+    __shared__ uint32_t s_spread[256][W];
+    __shared__ int2 s_wtab[kPtMaxFpad / 4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nl = P.nl;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem(&s_tmem)), "r"(512u)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            tc_mbar_init(tc_smem(&s_afull[s]), kPtGatherWarps);
+            tc_mbar_init(tc_smem(&s_aempty[s]), 1);
+            tc_mbar_init(tc_smem(&s_accfull[s]), 1);
+            tc_mbar_init(tc_smem(&s_accempty[s]), kPtEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    {  // the digit matrix (already in the swizzled layout) and the per-(layout, dim) constants
+        const uint4* src = reinterpret_cast<const uint4*>(P.B);
+        uint4* dst = reinterpret_cast<uint4*>(sB);
+        const int nv = P.Npad * P.Fpad / 16;
+        for (int i = tid; i < nv; i += kPtThreads) dst[i] = __ldg(src + i);
+        for (int i = tid; i < P.Fpad / 4; i += kPtThreads) s_wtab[i] = P.wtab[i];
+        for (int i = tid; i < nl * D; i += kPtThreads) {
+            const int li = i / D, d = i - li * D, l = P.l0 + li;
+            s_M[li][d] = P.M[l * D + d];
+            if (MODE == 1) {
+                const double lo = ordered_to_double_hd(P.amm[static_cast<size_t>(l) * 2 * D + d]);
+                const double hi = ordered_to_double_hd(P.amm[static_cast<size_t>(l) * 2 * D + D + d]);
+                const double R = hi - lo;
+                const bool degen = !(R > 4.0 * P.E);
+                s_lo[li][d] = lo;
+                s_lo2[li][d] = lo + 2.0 * P.E;
+                s_hi2[li][d] = hi - 2.0 * P.E;
+                s_degen[li][d] = degen ? 1 : 0;
+                s_sc[li][d] = degen ? 0.0 : 255.0 / R;
+                s_bz[li][d] = degen ? 1.0 : 1.01 * 255.0 * 4.0 * P.E / R + 1e-9;
+            }
+        }
+        if (MODE == 1 && tid < 256) {
+            uint32_t sp[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) sp[k] = 0;
+#pragma unroll
+            for (int L = 0; L < 8; ++L) sp[(L * D) >> 5] |= ((static_cast<uint32_t>(tid) >> L) & 1u) << ((L * D) & 31);
+#pragma unroll
+            for (int k = 0; k < W; ++k) s_spread[tid][k] = sp[k];
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    const uint64_t nloc = blockIdx.x < P.ntiles ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    // MODE 0: lane-distributed (layout, dim) slots of min / max T
+    long long tmn0 = LLONG_MAX, tmn1 = LLONG_MAX, tmx0 = LLONG_MIN, tmx1 = LLONG_MIN;
+    if (warp == kPtMmaWarp) {
+        if (lane == 0) {  // MMA issuer
+            const uint32_t idesc = pt_idesc(P.Npad);
+            const int KB = P.Fpad >> 7;
+            for (uint64_t i = 0; i < nloc; ++i) {
+                const int buf = static_cast<int>(i & 1);
+                const uint32_t use = static_cast<uint32_t>(i >> 1);
+                tc_mbar_wait(tc_smem(&s_afull[buf]), use & 1);
+                if (i >= 2) tc_mbar_wait(tc_smem(&s_accempty[buf]), (use - 1) & 1);
+                tc_fence_after();
+                const uint32_t acc = tmem + static_cast<uint32_t>(buf * 256);
+                const uint32_t a0 = tc_smem(sA + buf * abytes), b0 = tc_smem(sB);
+                for (int kb = 0; kb < KB; ++kb) {
+                    const uint64_t da = tc_desc_k128(a0 + kb * kPtRows * 128);
+                    const uint64_t db = tc_desc_k128(b0 + kb * P.Npad * 128);
+                    if (!(P.abl & 4)) {
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) pt_mma(acc, da + 2 * ks, db + 2 * ks, idesc, (kb | ks) != 0 ? 1u : 0u);
+                    }
+                }
+                tc_commit(tc_smem(&s_aempty[buf]));
+                tc_commit(tc_smem(&s_accfull[buf]));
+            }
+        }
+    } else if (warp < kPtGatherWarps) {  // gather: two threads per patch row (halves of the row)
+        const int nchunk = P.Fpad >> 4, hc = (nchunk + 1) >> 1;
+        const int gh = tid >> 7;
+        for (uint64_t i = 0; i < nloc; ++i) {
+            const int buf = static_cast<int>(i & 1);
+            const uint32_t use = static_cast<uint32_t>(i >> 1);
+            if (i >= 2) tc_mbar_wait(tc_smem(&s_aempty[buf]), (use - 1) & 1);
+            const uint64_t tile = blockIdx.x + i * gridDim.x;
+            if (P.abl & 1) {
+            } else if (KT == 0) {
+                pt_gather(P, s_wtab, tile, tc_smem(sA + buf * abytes), tid & 127, gh ? hc : 0, gh ? nchunk : hc);
+            } else {
+                const int r = tid & 127;
+                const uint64_t pr = tile * kPtRows + r;
+                const bool valid = pr < P.n;
+                uint32_t base = 0;
+                if (valid) {
+                    const uint32_t key = __ldg(P.keys + pr);
+                    base = ((key >> 16) * static_cast<uint32_t>(P.w) + (key & 0xffffu)) * static_cast<uint32_t>(P.C);
+                }
+                const uint32_t wC = static_cast<uint32_t>(P.w * P.C), sa = tc_smem(sA + buf * abytes);
+                if (KT == 1) {
+                    if (gh) pt_gather_static<9, 1, 1>(P.img, base, wC, valid, sa, r);
+                    else pt_gather_static<9, 1, 0>(P.img, base, wC, valid, sa, r);
+                } else {
+                    if (gh) pt_gather_static<11, 3, 1>(P.img, base, wC, valid, sa, r);
+                    else pt_gather_static<11, 3, 0>(P.img, base, wC, valid, sa, r);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tc_mbar_arrive(tc_smem(&s_afull[buf]));
+        }
+    } else {  // epilogue: TMEM lane quarter ew & 3, layouts of parity ew >> 2, one patch row per thread
+        const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;
+        for (uint64_t j = 0; j < nloc; ++j) {
+            const int buf = static_cast<int>(j & 1);
+            tc_mbar_wait(tc_smem(&s_accfull[buf]), static_cast<uint32_t>(j >> 1) & 1);
+            tc_fence_after();
+            const uint64_t tile = blockIdx.x + j * gridDim.x;
+            const uint64_t row = tile * kPtRows + q4 * 32 + lane;
+            const bool valid = row < P.n;
+            const uint32_t tbase = tmem + static_cast<uint32_t>(buf * 256) + (static_cast<uint32_t>(q4 * 32) << 16);
+            for (int li = lpar; li < nl; li += 2) {
+                constexpr int NC = kPtDigits * D;
+                uint32_t v[NC];
+                const uint32_t ta = tbase + static_cast<uint32_t>(li * NC);
+#pragma unroll
+                for (int c = 0; c + 4 <= NC; c += 4) {
+                    uint32_t t4[4];
+                    tc_ld_x4(ta + c, t4);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[c + u] = t4[u];
+                }
+#pragma unroll
+                for (int c = NC & ~3; c < NC; ++c) tc_ld_x1(ta + c, v[c]);
+                tc_ld_wait();
+                if (li + 2 >= nl) {  // TMEM of this buffer fully read: release it to the MMA warp early
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
+                }
+                if (P.abl & 2) {
+                    if (v[0] == 0x12345678u && v[NC - 1] == 0x9abcdefu) P.list_count[1] = 1;  // keep the loads
+                    continue;
+                }
+                uint32_t kw[W];
+#pragma unroll
+                for (int k = 0; k < W; ++k) kw[k] = 0;
+                bool flag = false, cand = false;
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    // T = sum_k S_k 2^(8k) in int64 (exact, |T| < 2^51); the fp64 conversions run at a
+                    // fraction of the integer rate, so the min / max pass stays integer and the
+                    // quantise pass converts once: y' = fl(T * 2^-38 - M) (T exact in a double)
+                    const uint32_t* vd = v + kPtDigits * d;
+                    const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
+                                        (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
+                                        (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
+                                        (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
+                                        static_cast<long long>(static_cast<int>(vd[0]));
+                    if (MODE == 0) {
+                        // y' is monotone in T: min / max on T
+                        const int th = static_cast<int>(T >> 32);
+                        const uint32_t tl = static_cast<uint32_t>(T);
+                        const int mh = __reduce_min_sync(0xffffffffu, valid ? th : 0x7fffffff);
+                        const uint32_t ml = __reduce_min_sync(0xffffffffu, (valid && th == mh) ? tl : 0xffffffffu);
+                        const int xh = __reduce_max_sync(0xffffffffu, valid ? th : static_cast<int>(0x80000000));
+                        const uint32_t xl = __reduce_max_sync(0xffffffffu, (valid && th == xh) ? tl : 0u);
+                        const long long wmn = (static_cast<long long>(mh) << 32) | ml;
+                        const long long wmx = (static_cast<long long>(xh) << 32) | xl;
+                        const int slot = (li >> 1) * D + d;  // this warp's (layout, dim) slot: lane slot & 31
+                        if ((slot & 31) == lane) {
+                            if (slot < 32) {
+                                tmn0 = wmn < tmn0 ? wmn : tmn0;
+                                tmx0 = wmx > tmx0 ? wmx : tmx0;
+                            } else {
+                                tmn1 = wmn < tmn1 ? wmn : tmn1;
+                                tmx1 = wmx > tmx1 ? wmx : tmx1;
+                            }
+                        }
+                    } else {
+                        uint32_t q = 0;
+                        if (s_degen[li][d]) {
+                            flag = true;
+                            cand = true;
+                        } else {
+                            const double y = __dsub_rn(__ll2double_rn(T) * 0x1p-38, s_M[li][d]);
+                            const double zf = __fma_rn(y - s_lo[li][d], s_sc[li][d], 0.5);
+                            // floor(zf) through the 2^52 rounding trick (no conversion): the nearest
+                            // integer to zf - 1/2; a tie only happens at an integer zf, which the
+                            // boundary test below flags anyway
+                            const double tq = __dadd_rn(zf, 4503599627370495.5);  // zf - 0.5 + 2^52
+                            const double qf = __dsub_rn(tq, 4503599627370496.0);
+                            const double fr = zf - qf;
+                            const double bz = s_bz[li][d];
+                            if (fr < bz || fr > 1.0 - bz) flag = true;
+                            if (y <= s_lo2[li][d] || y >= s_hi2[li][d]) cand = true;
+                            const int qi = static_cast<int>(static_cast<uint32_t>(__double_as_longlong(tq)));
+                            q = static_cast<uint32_t>(min(max(qi, 0), 255));
+                        }
+                        const int sh = D - 1 - d;
+                        uint32_t prev = 0;
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            const uint32_t cur = s_spread[q][k];
+                            kw[k] |= sh ? __funnelshift_l(prev, cur, sh) : cur;
+                            prev = cur;
+                        }
+                    }
+                }
+                if (MODE == 1) {
+                    const uint32_t l = static_cast<uint32_t>(P.l0 + li);
+                    if (valid) {
+                        const uint64_t e = static_cast<uint64_t>(l) * P.n + row;
+#pragma unroll
+                        for (int k = 0; k < W; ++k) P.keyw[static_cast<size_t>(k) * P.Nrec + e] = kw[k];
+                        P.val[e] = (l << 29) | (P.row_base + static_cast<uint32_t>(row));
+                    }
+                    flag = flag || cand;
+                    const uint32_t m = __ballot_sync(0xffffffffu, valid && flag);
+                    if (m) {
+                        uint32_t base = 0;
+                        if (lane == 0) base = atomicAdd(P.list_count, static_cast<uint32_t>(__popc(m)));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (valid && flag)
+                            P.list[base + __popc(m & ((1u << lane) - 1u))] =
+                                (static_cast<uint32_t>(row) << 4) | (cand ? 8u : 0u) | l;
+                    }
+                }
+            }
+        }
+    }
+    if (MODE == 0 && warp >= kPtGatherWarps && warp < kPtMmaWarp && (warp - kPtGatherWarps) < 8) {
+        const int lpar = ((warp - kPtGatherWarps) >> 2) & 1;
+        for (int k = 0; k < 2; ++k) {
+            const int slot = 32 * k + lane, li = 2 * (slot / D) + lpar, d = slot % D;
+            if (li < nl) {
+                const int l = P.l0 + li;
+                const long long tmn = k ? tmn1 : tmn0, tmx = k ? tmx1 : tmx0;
+                if (tmn <= tmx) {  // the slot saw a valid row: y' of the extreme T (one rounding, as in the epilogue)
+                    const double M = s_M[li][d];
+                    atomicMin(P.amm + static_cast<size_t>(l) * 2 * D + d,
+                              double_to_ordered(__dsub_rn(static_cast<double>(tmn) * 0x1p-38, M)));
+                    atomicMax(P.amm + static_cast<size_t>(l) * 2 * D + D + d,
+                              double_to_ordered(__dsub_rn(static_cast<double>(tmx) * 0x1p-38, M)));
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
+    }
+}
+
+// digit matrices of all groups (pre-zeroed) and M = sum_j mean_j c_j, from the device models
+__global__ void k_pt_prep(const double* __restrict__ mean, const double* __restrict__ comp,
+                          const int32_t* __restrict__ cols, int mc, int D, int nlmax, int Fpad,
+                          const int* __restrict__ goff, const int* __restrict__ gnpad, uint8_t* __restrict__ B,
+                          double* __restrict__ M) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int total = 8 * mc * D;
+    if (tid < total) {
+        const int l = tid / (mc * D), rem = tid - l * mc * D, j = rem / D, d = rem - j * D;
+        const double c = comp[(static_cast<size_t>(l) * mc + j) * D + d];
+        long long t = llrint(c * 274877906944.0);  // exact scaling by 2^38, then round to nearest
+        const int g = l / nlmax, li = l - g * nlmax;
+        const int f = cols[l * mc + j];
+        for (int k = 0; k < kPtDigits; ++k) {
+            long long dg = ((t + 128) & 255) - 128;  // balanced digit in [-128, 127]
+            t = (t - dg) >> 8;
+            const int row = (li * D + d) * kPtDigits + k;
+            B[goff[g] + sw128_off(row, f, gnpad[g])] = static_cast<uint8_t>(static_cast<int8_t>(dg));
+        }
+    }
+    if (tid < 8 * D) {
+        const int l = tid / D, d = tid - l * D;
+        double s = 0.0;
+        for (int j = 0; j < mc; ++j) s = __fma_rn(mean[l * mc + j], comp[(static_cast<size_t>(l) * mc + j) * D + d], s);
+        M[tid] = s;
+    }
+}
+
+// Canonical fp64 projection of the listed (patch, layout) pairs, one pair per thread (D
+// independent fma chains, j ascending from +0.0 -- the order k_project runs on the FP64 MMA).
+// MODE 0: exact lo / hi (ordered atomics); MODE 1: exact quantised Morton record.
+template <int D, int MODE>
+__global__ void __launch_bounds__(128) k_pt_exact(const uint8_t* __restrict__ img, int w, int C,
+                                                  const uint32_t* __restrict__ keys, uint64_t n, uint32_t row_base,
+                                                  const int32_t* __restrict__ off, int m,
+                                                  const double* __restrict__ mean, const double* __restrict__ comp,
+                                                  const uint32_t* __restrict__ list,
+                                                  const uint32_t* __restrict__ list_count,
+                                                  unsigned long long* __restrict__ minmax, uint32_t* __restrict__ keyw,
+                                                  uint32_t* __restrict__ val, uint64_t Nrec) {
+    constexpr int W = (D + 3) / 4;
+    const uint32_t cnt = *list_count;
+    const int mc = m * C;
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < cnt;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t ent = list[e];
+        const uint32_t row = ent >> 4, l = ent & 7;
+        if (MODE == 0 && !(ent & 8u)) continue;  // only the lo / hi candidates take part in the min / max
+        const uint32_t key = keys[row];
+        const uint8_t* pb = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
+        double y[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) y[d] = 0.0;
+        const double* mp = mean + static_cast<size_t>(l) * mc;
+        const double* cp = comp + static_cast<size_t>(l) * mc * D;
+        const int32_t* op = off + static_cast<size_t>(l) * m;
+        for (int p = 0; p < m; ++p) {
+            const int o = __ldg(op + p);
+            for (int ch = 0; ch < C; ++ch) {
+                const int j = p * C + ch;
+                const double xc = __dsub_rn(static_cast<double>(__ldg(pb + o + ch)), __ldg(mp + j));
+#pragma unroll
+                for (int d = 0; d < D; ++d) y[d] = __fma_rn(xc, __ldg(cp + static_cast<size_t>(j) * D + d), y[d]);
+            }
+        }
+        unsigned long long* mm = minmax + static_cast<size_t>(l) * 2 * D;
+        if (MODE == 0) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const unsigned long long o = double_to_ordered(y[d]);
+                atomicMin(mm + d, o);
+                atomicMax(mm + D + d, o);
+            }
+        } else {
+            uint32_t kw[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) kw[k] = 0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const double lo = ordered_to_double_hd(mm[d]), hi = ordered_to_double_hd(mm[D + d]);
+                const double rcp = hi > lo ? __ddiv_rn(1.0, __dsub_rn(hi, lo)) : 0.0;
+                const uint32_t q = quantize_fast(lo, hi, rcp, y[d]);
+#pragma unroll
+                for (int L = 0; L < 8; ++L) {
+                    const int pos = L * D + D - 1 - d;
+                    kw[pos >> 5] |= ((q >> L) & 1u) << (pos & 31);
+                }
+            }
+            const uint64_t er = static_cast<uint64_t>(l) * n + row;
+#pragma unroll
+            for (int k = 0; k < W; ++k) keyw[static_cast<size_t>(k) * Nrec + er] = kw[k];
+            val[er] = (l << 29) | (row_base + row);
+        }
+    }
+}
+
+template <int D>
+static void launch_pt_exact(zi_ctx* ctx, zi_multi_index* mi, const pt_params& P, int mode) {
+    const unsigned grid = static_cast<unsigned>(ctx->num_sms) * 4;
+    const uint32_t* keys = mi->dict.p + mi->row_begin;
+    const uint32_t rb = static_cast<uint32_t>(mi->row_begin);
+    if (mode == 0)
+        ZI_LAUNCH(ctx, "project_tc_exact_minmax", (k_pt_exact<D, 0>), grid, 128, 0, mi->image.p, mi->w, mi->C, keys, mi->n,
+                  rb, mi->layout_off.p, mi->m, mi->pca_mean.p, mi->pca_comp.p, P.list, P.list_count, mi->minmax.p, P.keyw,
+                  P.val, P.Nrec);
+    else
+        ZI_LAUNCH(ctx, "project_tc_fixup", (k_pt_exact<D, 1>), grid, 128, 0, mi->image.p, mi->w, mi->C, keys, mi->n, rb,
+                  mi->layout_off.p, mi->m, mi->pca_mean.p, mi->pca_comp.p, P.list, P.list_count, mi->minmax.p, P.keyw,
+                  P.val, P.Nrec);
+}
+
+template <int D, int KT>
+static void launch_pt_kt(zi_ctx* ctx, const pt_params& P, int mode, size_t smem) {
+    static bool attr[2] = {false, false};
+    if (!attr[mode]) {
+        if (mode == 0) ZI_CUDA(cudaFuncSetAttribute(k_proj_tc<D, 0, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        else ZI_CUDA(cudaFuncSetAttribute(k_proj_tc<D, 1, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr[mode] = true;
+    }
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(P.ntiles, static_cast<uint64_t>(ctx->num_sms)));
+    if (mode == 0) ZI_LAUNCH(ctx, "project_tc_minmax", (k_proj_tc<D, 0, KT>), grid, kPtThreads, smem, P);
+    else ZI_LAUNCH(ctx, "project_tc_quantize", (k_proj_tc<D, 1, KT>), grid, kPtThreads, smem, P);
+}
+
+// patch shapes with a static gather: (9, 1) -> 1 (cfg1, cfg4), (11, 3) -> 2 (cfg2); for the dims
+// those configs use, everything else takes the table-driven gather
+template <int D>
+static void launch_pt(zi_ctx* ctx, const pt_params& P, int mode, size_t smem) {
+    const int kt = P.KC == 9 && P.F == 81 ? 1 : (P.KC == 33 && P.F == 363 ? 2 : 0);
+    if (D == 8 && kt == 1) launch_pt_kt<D, 1>(ctx, P, mode, smem);
+    else if ((D == 12 || D == 8) && kt == 2) launch_pt_kt<D, 2>(ctx, P, mode, smem);
+    else launch_pt_kt<D, 0>(ctx, P, mode, smem);
+}
+
+bool project_quantize_tc(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec) {
+    zi_ctx* ctx = mi->ctx;
+    static const bool off_env = std::getenv("ZI_PROJ_FP64") != nullptr;
+    const int D = mi->dims, K = mi->K, C = mi->C, m = mi->m, mc = mi->mc;
+    const int F = K * K * C, Fpad = (F + 127) / 128 * 128;
+    const uint64_t n = mi->n;
+    if (off_env || D < 1 || D > 16 || Fpad > kPtMaxFpad || n == 0 || n >= (1ull << 27)) return false;
+    const int nlmax = std::min(8, kPtMaxN / (kPtDigits * D));
+    const int ng = (8 + nlmax - 1) / nlmax;
+    int goff[8], gnpad[8];
+    size_t btot = 0;
+    for (int g = 0; g < ng; ++g) {
+        const int nl = std::min(nlmax, 8 - g * nlmax);
+        gnpad[g] = (nl * kPtDigits * D + 15) / 16 * 16;
+        goff[g] = static_cast<int>(btot);
+        btot += static_cast<size_t>(gnpad[g]) * Fpad;
+    }
+    const size_t smem = 2 * static_cast<size_t>(kPtRows) * Fpad + static_cast<size_t>(kPtMaxN) * Fpad + 1024;
+    if (smem > 200 * 1024) return false;
+    if (!mi->pca_cols_ready) {
+        std::vector<int32_t> hc;
+        for (int l = 0; l < 8; ++l)
+            for (int p = 0; p < m; ++p)
+                for (int ch = 0; ch < C; ++ch) hc.push_back((mi->L[l].rc[2 * p] * K + mi->L[l].rc[2 * p + 1]) * C + ch);
+        mi->pca_cols.ensure(hc.size());
+        ZI_CUDA(cudaMemcpyAsync(mi->pca_cols.p, hc.data(), hc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        mi->pca_cols_ready = true;
+    }
+    // scratch: [goff/gnpad ints][B bytes][M doubles][amm][count][list]
+    const size_t o_int = 0, o_B = 256, o_M = (o_B + btot + 255) & ~size_t(255);
+    const size_t o_amm = o_M + 8 * 16 * sizeof(double), o_cnt = o_amm + 8 * 2 * 16 * sizeof(unsigned long long);
+    const size_t o_list = o_cnt + 256;
+    uint8_t* s = mi->pt_scratch.ensure(o_list + 8 * n * sizeof(uint32_t));
+    int hint[16];
+    for (int g = 0; g < 8; ++g) {
+        hint[g] = g < ng ? goff[g] : 0;
+        hint[8 + g] = g < ng ? gnpad[g] : 0;
+    }
+    ZI_CUDA(cudaMemcpyAsync(s + o_int, hint, sizeof(hint), cudaMemcpyHostToDevice, ctx->stream));
+    {  // gather word table: patch-relative byte offsets of every 4-byte word of the row
+        const int KC = K * C, wC = mi->w * C;
+        std::vector<int2> tab(Fpad / 4);
+        for (int ow = 0; ow < Fpad / 4; ++ow) {
+            const int f = 4 * ow;
+            if (f >= F) {
+                tab[ow] = make_int2(-1, -1);
+                continue;
+            }
+            const int rr = f / KC, k = f - rr * KC, rem = KC - k;
+            int y = -1;
+            if (rem < 4) y = (rem << 24) | (rr + 1 < K ? (rr + 1) * wC : 0xffffff);
+            tab[ow] = make_int2(rr * wC + k, y);
+        }
+        mi->pt_wtab.ensure(tab.size());
+        ZI_CUDA(cudaMemcpyAsync(mi->pt_wtab.p, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ZI_CUDA(cudaMemsetAsync(s + o_B, 0, btot, ctx->stream));
+    ZI_CUDA(cudaMemsetAsync(s + o_cnt, 0, sizeof(uint32_t), ctx->stream));
+    unsigned long long* amm = reinterpret_cast<unsigned long long*>(s + o_amm);
+    for (int l = 0; l < 8; ++l) {
+        ZI_CUDA(cudaMemsetAsync(amm + static_cast<size_t>(l) * 2 * D, 0xff, D * sizeof(unsigned long long), ctx->stream));
+        ZI_CUDA(cudaMemsetAsync(amm + static_cast<size_t>(l) * 2 * D + D, 0, D * sizeof(unsigned long long), ctx->stream));
+        ZI_CUDA(cudaMemsetAsync(mi->minmax.p + static_cast<size_t>(l) * 2 * D, 0xff, D * sizeof(unsigned long long), ctx->stream));
+        ZI_CUDA(cudaMemsetAsync(mi->minmax.p + static_cast<size_t>(l) * 2 * D + D, 0, D * sizeof(unsigned long long), ctx->stream));
+    }
+    const int* dgoff = reinterpret_cast<const int*>(s + o_int);
+    const int total = 8 * mc * D;
+    ZI_LAUNCH(ctx, "project_tc_prep", k_pt_prep, (total + 255) / 256, 256, 0, mi->pca_mean.p, mi->pca_comp.p,
+              mi->pca_cols.p, mc, D, nlmax, Fpad, dgoff, dgoff + 8, s + o_B, reinterpret_cast<double*>(s + o_M));
+    pt_params P{};
+    P.img = mi->image.p;
+    P.w = mi->w;
+    P.C = C;
+    P.KC = K * C;
+    P.F = F;
+    P.Fpad = Fpad;
+    P.keys = mi->dict.p + mi->row_begin;
+    P.n = n;
+    P.row_base = static_cast<uint32_t>(mi->row_begin);
+    P.M = reinterpret_cast<const double*>(s + o_M);
+    P.amm = amm;
+    P.E = 255.0 * mc * (0x1p-39 + 0x1p-44);
+    P.keyw = keyw;
+    P.val = val;
+    P.Nrec = Nrec;
+    P.list = reinterpret_cast<uint32_t*>(s + o_list);
+    P.list_count = reinterpret_cast<uint32_t*>(s + o_cnt);
+    P.ntiles = (n + kPtRows - 1) / kPtRows;
+    P.wtab = mi->pt_wtab.p;
+    static const int abl = std::getenv("ZI_PT_ABL") ? std::atoi(std::getenv("ZI_PT_ABL")) : 0;
+    P.abl = abl;
+    for (int mode = 0; mode < 2; ++mode)
+        for (int g = 0; g < ng; ++g) {
+            P.B = s + o_B + goff[g];
+            P.Npad = gnpad[g];
+            P.l0 = g * nlmax;
+            P.nl = std::min(nlmax, 8 - g * nlmax);
+            switch (D) {
+#define ZI_PT_CASE(DD) \
+    case DD: launch_pt<DD>(ctx, P, mode, smem); break;
+                ZI_PT_CASE(1) ZI_PT_CASE(2) ZI_PT_CASE(3) ZI_PT_CASE(4) ZI_PT_CASE(5) ZI_PT_CASE(6) ZI_PT_CASE(7)
+                ZI_PT_CASE(8) ZI_PT_CASE(9) ZI_PT_CASE(10) ZI_PT_CASE(11) ZI_PT_CASE(12) ZI_PT_CASE(13)
+                ZI_PT_CASE(14) ZI_PT_CASE(15) ZI_PT_CASE(16)
+#undef ZI_PT_CASE
+                default: return false;
+            }
+        }
+    static const bool debug = std::getenv("ZI_DEBUG_PT") != nullptr;
+    if (debug) {
+        uint32_t cnt = 0;
+        ZI_CUDA(cudaMemcpyAsync(&cnt, P.list_count, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::fprintf(stderr, "project_tc: n=%llu D=%d groups=%d fix-up list %u (%.4f%% of patch x layout pairs)\n",
+                     static_cast<unsigned long long>(n), D, ng, cnt, 100.0 * cnt / (8.0 * n));
+    }
+    for (int mode = 0; mode < 2; ++mode) switch (D) {
+#define ZI_PTX_CASE(DD) \
+    case DD: launch_pt_exact<DD>(ctx, mi, P, mode); break;
+            ZI_PTX_CASE(1) ZI_PTX_CASE(2) ZI_PTX_CASE(3) ZI_PTX_CASE(4) ZI_PTX_CASE(5) ZI_PTX_CASE(6) ZI_PTX_CASE(7)
+            ZI_PTX_CASE(8) ZI_PTX_CASE(9) ZI_PTX_CASE(10) ZI_PTX_CASE(11) ZI_PTX_CASE(12) ZI_PTX_CASE(13)
+            ZI_PTX_CASE(14) ZI_PTX_CASE(15) ZI_PTX_CASE(16)
+#undef ZI_PTX_CASE
+            default: break;
+        }
+    return true;
+}
+
+}  // namespace zi

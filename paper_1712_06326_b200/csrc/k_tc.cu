@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 #include "zi_internal.h"
 
 namespace zi {
@@ -30,40 +31,6 @@ constexpr int kTcStages = 6;
 constexpr int kTcTileBytes = kTcTile * kTcStageK;  // 16 KB
 constexpr uint64_t kTcMaxChunk = 65536;
 
-__device__ __forceinline__ uint32_t tc_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-
-__device__ __forceinline__ void tc_mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void tc_mbar_expect(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "TC_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra TC_WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tc_tma_load_2d(uint32_t dst, const CUtensorMap* tm, int x, int y, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar)
-        : "memory");
-}
-// UMMA shared-memory matrix descriptor: K-major, 128B swizzle (8-row x 128 B atoms, atoms 1024 B
-// apart), sm_100 version 1
-__device__ __forceinline__ uint64_t tc_desc_k128(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((saddr >> 4) & 0x3fffu);   // start address
-    d |= static_cast<uint64_t>(1u) << 16;                 // leading byte offset (unused for swizzled K-major)
-    d |= static_cast<uint64_t>(1024u >> 4) << 32;         // stride byte offset: next 8-row group
-    d |= static_cast<uint64_t>(1u) << 46;                 // descriptor version (sm_100)
-    d |= static_cast<uint64_t>(2u) << 61;                 // SWIZZLE_128B
-    return d;
-}
 // instruction descriptor: kind::i8, u8 x u8 -> s32, both K-major, M = N = 128
 constexpr uint32_t kTcIdesc = (2u << 4)                  // D format S32
                               | (0u << 7) | (0u << 10)   // A, B unsigned 8-bit
@@ -78,10 +45,6 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t tmem, uint64_t da, uint64_t d
         "l"(da), "l"(db), "r"(kTcIdesc), "r"(accumulate)
         : "memory");
 }
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
 __global__ void __launch_bounds__(128, 1) k_gram_tc(const __grid_constant__ CUtensorMap tm, int F, int ntile,
                                                     uint64_t npad, uint64_t chunk, unsigned long long* __restrict__ out) {
     extern __shared__ uint8_t tc_raw[];

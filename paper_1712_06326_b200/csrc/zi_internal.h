@@ -152,6 +152,8 @@ struct zi_multi_index {
     zi::dbuf<unsigned long long> moments;  // F + F*F (s, S)
     zi::dbuf<double> proj;               // D*n fp64 projections (reused across layouts)
     zi::dbuf<uint32_t> recs;             // (W+1)*n sort records (Morton words + payload)
+    zi::dbuf<uint8_t> pt_scratch;        // tensor-core projection: digit matrices, bounds, fix-up list
+    zi::dbuf<int2> pt_wtab;              // tensor-core projection: gather word table
     zi::dbuf<uint8_t> qscratch;          // query scratch
     zi::hbuf<uint8_t> hstage;            // pinned staging for targets/results
     void* hres = nullptr;                // mapped pinned query result (k_query_one publishes it)
@@ -234,6 +236,11 @@ void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int
 // all 8 layouts at once: N = 8n records, Morton passes then one pass on the layout bits of the
 // payload ((layout << 29) | row) -- stable, so each layout segment ends in reference order
 void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D);
+
+// projection + quantisation of all 8 layouts on the int8 tensor cores with the exact fp64 fix-up
+// (k_proj_tc.cu): records and exact lo/hi identical to project + quantize_interleave; false when
+// the configuration is outside its envelope (dims > 16, K*K*C > 384, ZI_PROJ_FP64 set)
+bool project_quantize_tc(zi_multi_index* mi, uint32_t* d_keyw, uint32_t* d_val, uint64_t N);
 
 // sorted key words + payload -> index planes, keys, bbox
 void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t off,

@@ -709,3 +709,31 @@ def test_sharded_build_cfg1(zb):
         assert np.array_equal(cs, c) and np.array_equal(ks, k), l
     # the rebalancing exchange only moves the sample-sort imbalance
     assert info["records_rebalanced"] < info["records_exchanged"]
+
+
+def test_sharded_multi_index_over_nccl_world1(zb):
+    """The torch.distributed path (NCCL, device tensors from the shard's own buffers) end to end
+    at world size 1: ShardedMultiIndex == MultiIndex, queries included."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1712_06326_b200 import sharding
+    from tests.test_cpu import _free_port
+    img, known = workloads.small_image(64, 72, 3, seed=31, hole_frac=0.1)
+    cfg = zb.index_config(patch_size=7, dims=8, knn=16)
+    mi = zb.MultiIndex(img, known, cfg)
+    store = dist.TCPStore("127.0.0.1", _free_port(), 1, True)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1)
+    try:
+        smi = sharding.ShardedMultiIndex(img, known, cfg)
+        for l in range(8):
+            a, b = smi.index_arrays(l), mi.index_arrays(l)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        for (x, y) in fillfront(known)[:6]:
+            tv, tk = oracle.extract_patch_clamped(img, known, int(x), int(y), 7)
+            got, want = smi.query_best_patch(tv, tk), mi.query_best_patch(tv, tk)
+            assert (got[0], got[1], got[3], got[4]) == (want[0], want[1], want[3], want[4])
+            assert smi.brute_force_best(tv, tk) == mi.brute_force_best(tv, tk)[:2]
+    finally:
+        dist.destroy_process_group()
