@@ -4,9 +4,10 @@ BASELINE.json config the metric is quoted on (configs[1] = cfg2: 1024^2 RGB, 11x
 D=12, 12 disk holes), synthetic seeded input.
 
 One step = multi_index::build (proj/src/builder.cpp:202-224) of one image already resident in
-HBM: dictionary collection, exact PCA moments, 8 host eigen-solves, 8 x (fp64 projection,
-quantisation, Morton onesweep radix sort, finalize).  L2 is flushed (256 MiB write) before every
-timed step, outside the timed interval.
+HBM: dictionary collection, exact PCA moments (int8 tensor cores), the 8 eigen-solves on the
+device, projection + quantisation of all 8 layouts (int8 tensor-core digit GEMM + exact fp64
+fix-up), one hybrid Morton sort over the records of all layouts, 8 finalizes.  L2 is flushed
+(256 MiB write) before every timed step, outside the timed interval.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config cfg2|cfg1|cfg4]
 
@@ -186,11 +187,26 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- roofline model
-def algorithmic_bytes(kernel: str, n: int, D: int, mc: int) -> float | None:
+def pt_groups(D: int):
+    """Layout groups of the int8 tensor-core projection (k_proj_tc.cu): five digit columns per
+    (layout, dim), at most 256 MMA columns per group, padded to a multiple of 16."""
+    nlmax = min(8, 256 // (5 * D))
+    out, l0 = [], 0
+    while l0 < 8:
+        nl = min(nlmax, 8 - l0)
+        out.append((nl, (nl * 5 * D + 15) // 16 * 16))
+        l0 += nl
+    return out
+
+
+def algorithmic_bytes(kernel: str, n: int, D: int, mc: int, F: int = 0) -> float | None:
     """Algorithmic HBM bytes per launch; gathered pixels are L1/L2 served.
-    The radix passes and the window sort run once over the records of all 8 layouts (N = 8n)."""
+    The radix passes and the window sort run once over the records of all 8 layouts (N = 8n);
+    the tensor-core projection launches once per (pass, layout group): keys in, and in the
+    quantise pass the Morton records of its layouts out (averaged over the groups)."""
     W = (D + 3) // 4
     N = 8 * n
+    g = len(pt_groups(D)) if D <= 16 else 1
     return {
         "radix_onesweep": 2 * 4 * (W + 1) * N,          # read + write of (W key words + payload)
         "segment_sort": 2 * 4 * (W + 1) * N,            # one read + one in-place write per record
@@ -198,17 +214,35 @@ def algorithmic_bytes(kernel: str, n: int, D: int, mc: int) -> float | None:
         "proj_minmax": 8 * D * n,
         "quantize_interleave": (8 * D + 4 + 4 * (W + 1)) * n,
         "finalize_index": (4 * (W + 1) + 4 * (W + 1)) * n,
+        "project_tc_minmax": 4 * n,
+        "project_tc_quantize": (4 * n * g + 4 * (W + 1) * N) / g,
     }.get(kernel)
 
 
-def algorithmic_flops(kernel: str, n: int, D: int, mc: int) -> float | None:
-    """Useful fp64 flops per launch of the tensor-core kernels (2 per FMA; padding excluded)."""
-    return {"project": 2.0 * n * mc * D}.get(kernel)
+def algorithmic_ops(kernel: str, n: int, D: int, mc: int, F: int = 0) -> float | None:
+    """Tensor-core ops per launch: the fp64 projection (2 per FMA over the layout's m*C columns),
+    or the int8 digit GEMM of the tensor-core projection (2 * n * Fpad * columns, averaged over
+    its layout groups)."""
+    if kernel == "project":
+        return 2.0 * n * mc * D
+    if kernel in ("project_tc_minmax", "project_tc_quantize") and D <= 16:
+        Fpad = (F + 127) // 128 * 128
+        gs = pt_groups(D)
+        return 2.0 * n * Fpad * sum(npad for _, npad in gs) / len(gs)
+    return None
 
 
 # B200 FP64 tensor-core peak: not in MEASURED_PEAKS.json (driver measures bf16 only) nor in the
-# profiling recipe -> NVIDIA's B200 datasheet figure.
+# profiling recipe -> NVIDIA's B200 datasheet figure.  The int8 dense tensor rate is twice the bf16
+# rate on B200 (datasheet 4.5 POPS vs 2.25 PFLOPS): 2 x the measured bf16 burst.
 FP64_TENSOR_PEAK_TFLOPS = 40.0
+
+
+def tensor_peak(kernel: str, peaks: dict):
+    if kernel.startswith("project_tc"):
+        bf = float(peaks.get("bf16_tflops", 2250.0))
+        return 2.0 * bf, "2 x MEASURED_PEAKS.json bf16_tflops (int8 = 2x bf16 dense on B200)", "s8/u8 -> s32 (tcgen05.mma kind::i8)"
+    return FP64_TENSOR_PEAK_TFLOPS, "B200 datasheet FP64 Tensor Core 40 TFLOPS (no measured fp64 peak)", "f64 (mma.m8n8k4.f64)"
 
 
 def vector_index_line(zb, ctx, args):
@@ -382,11 +416,11 @@ def main():
         pass
     breakdown = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                  for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
-    # roofline of the dominant kernel of the step (the fp64 tensor-core projection) and, beside
-    # it, of the dominant HBM-bound kernel
+    # roofline of the dominant tensor-core kernel of the step (the projection) and, beside it, of
+    # the dominant HBM-bound kernel
     def hbm_roofline(kname, kms, kl):
         per_launch_ms = kms / max(kl, 1)
-        b = algorithmic_bytes(kname, n, mi.dims, mc)
+        b = algorithmic_bytes(kname, n, mi.dims, mc, F)
         achieved = b / (per_launch_ms * 1e-3) / 1e9
         tr = traffic_db.get(args.config, {}).get(kname)
         return {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -394,44 +428,51 @@ def main():
                 "avg_launch_ms": per_launch_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
 
-    hbm_kernels = {k: v for k, v in prof.items() if algorithmic_bytes(k, n, mi.dims, mc) is not None}
+    F = p["patch_size"] ** 2 * (1 if img.ndim == 2 else img.shape[2])
+    Fpad = (F + 127) // 128 * 128
+    hbm_kernels = {k: v for k, v in prof.items() if algorithmic_ops(k, n, mi.dims, mc, F) is None
+                   and algorithmic_bytes(k, n, mi.dims, mc, F) is not None}
     roofline_hbm = None
     if hbm_kernels:
         kname, (kms, kl) = max(hbm_kernels.items(), key=lambda kv: kv[1][0])
         roofline_hbm = hbm_roofline(kname, kms, kl)
-    if dom is not None and algorithmic_flops(dom[0], n, mi.dims, mc) is not None:
-        kname, (kms, kl) = dom
+    tensor_kernels = {k: v for k, v in prof.items() if algorithmic_ops(k, n, mi.dims, mc, F) is not None}
+    if tensor_kernels and (dom is None or dom[0] in tensor_kernels or dom[0] not in hbm_kernels):
+        kname, (kms, kl) = max(tensor_kernels.items(), key=lambda kv: kv[1][0])
         per_launch_ms = kms / max(kl, 1)
-        fl = algorithmic_flops(kname, n, mi.dims, mc)
+        fl = algorithmic_ops(kname, n, mi.dims, mc, F)
         achieved = fl / (per_launch_ms * 1e-3) / 1e12
-        roofline = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": FP64_TENSOR_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
-                    "traffic": traffic_db.get(args.config, {}).get(kname), "flops_per_launch": fl,
-                    "avg_launch_ms": per_launch_ms, "dtype": "f64 (mma.m8n8k4.f64)",
-                    "peak_source": "B200 datasheet FP64 Tensor Core 40 TFLOPS (no measured fp64 peak on this pool)",
-                    "note": "D=12 fills 12 of the 16 MMA columns, so the useful-flop ceiling is 0.75 of peak"}
+        peak, src, dt = tensor_peak(kname, peaks)
+        roofline = {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": peak,
+                    "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": traffic_db.get(args.config, {}).get(kname), "ops_per_launch": fl,
+                    "avg_launch_ms": per_launch_ms, "dtype": dt, "peak_source": src,
+                    "note": "int8 digit GEMM (five balanced base-256 digits of the fp64 components) with the "
+                            "exact fp64 fix-up; the epilogue (integer min/max, bracket quantisation, Morton "
+                            "interleave) bounds it, not the MMA" if kname.startswith("project_tc") else
+                            "D=12 fills 12 of the 16 MMA columns, so the useful-flop ceiling is 0.75 of peak"}
     else:
         roofline = roofline_hbm
 
-    # whole-step floor (SURVEY.md §8(d) model): max(HBM bytes / BW, fp64 flops / FP64 tensor peak)
-    # with this pipeline's own algorithmic bytes (every counted kernel, per step) and the one
-    # projection pass it performs
-    F = p["patch_size"] ** 2 * (1 if img.ndim == 2 else img.shape[2])
-    Fpad = (F + 127) // 128 * 128
+    # whole-step floor: max(HBM bytes / BW, tensor ops / tensor peak) with this pipeline's own
+    # algorithmic bytes (every counted kernel, per step)
     extra = {"project": (4 + 8 * mi.dims) * n,        # dictionary keys in, fp64 projections out
              "patch_matrix": (4 + Fpad) * n,            # keys in, feature-major patch matrix out
              "patch_moments": Fpad * n}                 # the patch matrix read once
     def step_b(k):
-        b = algorithmic_bytes(k, n, mi.dims, mc)
+        b = algorithmic_bytes(k, n, mi.dims, mc, F)
         return b if b is not None else extra.get(k)
     step_bytes = sum(step_b(k) * v[1] / args.steps for k, v in prof.items() if step_b(k) is not None)
-    step_flops = 8 * algorithmic_flops("project", n, mi.dims, mc)
-    floor_ms = max(step_bytes / (hbm_peak * 1e9), step_flops / (FP64_TENSOR_PEAK_TFLOPS * 1e12)) * 1e3
+    step_t = 0.0
+    for k, v in prof.items():
+        o = algorithmic_ops(k, n, mi.dims, mc, F)
+        if o is not None:
+            step_t += o * v[1] / args.steps / (tensor_peak(k, peaks)[0] * 1e12)
+    floor_ms = max(step_bytes / (hbm_peak * 1e9), step_t) * 1e3
     step_roofline = {"floor_ms": floor_ms, "measured_ms": total_ms / args.steps,
                      "frac": floor_ms / (total_ms / args.steps), "hbm_bytes_per_step": step_bytes,
-                     "fp64_flops_per_step": step_flops,
-                     "binding": "fp64" if step_flops / (FP64_TENSOR_PEAK_TFLOPS * 1e12) > step_bytes / (hbm_peak * 1e9)
-                     else "hbm"}
+                     "tensor_ms_per_step": step_t * 1e3,
+                     "binding": "tensor" if step_t > step_bytes / (hbm_peak * 1e9) else "hbm"}
 
     # -------- e2e through the public C ABI with pinned host buffers
     e2e = None

@@ -32,8 +32,9 @@
 namespace zi {
 
 constexpr int kPtRows = 128;
-constexpr int kPtGatherWarps = 8;                // warps 0-7: two threads per patch row
-constexpr int kPtEpiWarps = 8;                   // warps 8-15: TMEM lane quarter (w & 3), layout parity (w >> 2) & 1
+constexpr int kPtGatherWarps = 4;                // warps 0-3: one thread per patch row
+constexpr int kPtEpiWarps = 12;                  // warps 4-15: TMEM lane quarter (w & 3), layouts li = (w >> 2) mod 3
+constexpr int kPtEpiSets = kPtEpiWarps / 4;
 constexpr int kPtMmaWarp = kPtGatherWarps + kPtEpiWarps;
 constexpr int kPtThreads = (kPtMmaWarp + 1) * 32;
 constexpr int kPtMaxFpad = 384;
@@ -188,9 +189,12 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
     uint8_t* sB = sbase + 2 * abytes;
     __shared__ __align__(8) uint64_t s_afull[2], s_aempty[2], s_accfull[2], s_accempty[2];
     __shared__ uint32_t s_tmem;
-    __shared__ double s_M[8][D], s_lo[8][D], s_lo2[8][D], s_hi2[8][D], s_sc[8][D], s_bz[8][D];
-    __shared__ int s_degen[8][D];
-    __shared__ uint32_t s_spread[256][W];
+    __shared__ double s_M[8][D];
+    // quantise constants per (layout, dim): {za, zb} {bz, tlo} {thi, -} as two-word vectors (16 B loads)
+    __shared__ __align__(16) double2 s_qc[8][D][3];
+    // Morton spread table, four copies 8 banks apart (lane group g = lane >> 3 reads copy g)
+    constexpr int kSpStride = 256 * W + 8;
+    __shared__ uint32_t s_spread[4 * kSpStride];
     __shared__ int2 s_wtab[kPtMaxFpad / 4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nl = P.nl;
@@ -223,12 +227,20 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
                 const double hi = ordered_to_double_hd(P.amm[static_cast<size_t>(l) * 2 * D + D + d]);
                 const double R = hi - lo;
                 const bool degen = !(R > 4.0 * P.E);
-                s_lo[li][d] = lo;
-                s_lo2[li][d] = lo + 2.0 * P.E;
-                s_hi2[li][d] = hi - 2.0 * P.E;
-                s_degen[li][d] = degen ? 1 : 0;
-                s_sc[li][d] = degen ? 0.0 : 255.0 / R;
-                s_bz[li][d] = degen ? 1.0 : 1.01 * 255.0 * 4.0 * P.E / R + 1e-9;
+                const double M = s_M[li][d];
+                // z' = T * za + zb = 255 (T 2^-38 - M - lo) / R + 1/2 (its rounding, ~1e-11 even
+                // with cancellation, is inside Bz's 1e-9 slack)
+                const double za = degen ? 0.0 : 255.0 * 0x1p-38 / R;
+                const double zb = degen ? 0.0 : 0.5 - 255.0 * (M + lo) / R;
+                const double bz = degen ? 1.0 : 1.01 * 255.0 * 4.0 * P.E / R + 1e-9;
+                // lo / hi candidates: y' <= lo + 2E or y' >= hi - 2E, as T thresholds widened by
+                // a margin (a superset is harmless: candidates only cost a fix-up)
+                const double tl = (lo + 2.0 * P.E + M) * 0x1p38, th = (hi - 2.0 * P.E + M) * 0x1p38;
+                const long long tlo = degen ? LLONG_MAX : static_cast<long long>(ceil(tl + fabs(tl) * 0x1p-40)) + 16;
+                const long long thi = degen ? LLONG_MAX : static_cast<long long>(floor(th - fabs(th) * 0x1p-40)) - 16;
+                s_qc[li][d][0] = make_double2(za, zb);
+                s_qc[li][d][1] = make_double2(bz, __longlong_as_double(tlo));
+                s_qc[li][d][2] = make_double2(__longlong_as_double(thi), 0.0);
             }
         }
         if (MODE == 1 && tid < 256) {
@@ -238,7 +250,9 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
 #pragma unroll
             for (int L = 0; L < 8; ++L) sp[(L * D) >> 5] |= ((static_cast<uint32_t>(tid) >> L) & 1u) << ((L * D) & 31);
 #pragma unroll
-            for (int k = 0; k < W; ++k) s_spread[tid][k] = sp[k];
+            for (int k = 0; k < W; ++k)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) s_spread[c * kSpStride + tid * W + k] = sp[k];
         }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -249,7 +263,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
     const uint64_t nloc = blockIdx.x < P.ntiles ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
     // MODE 0: lane-distributed (layout, dim) slots of min / max T
-    long long tmn0 = LLONG_MAX, tmn1 = LLONG_MAX, tmx0 = LLONG_MIN, tmx1 = LLONG_MIN;
+    long long tmn0 = LLONG_MAX, tmx0 = LLONG_MIN;
     if (warp == kPtMmaWarp) {
         if (lane == 0) {  // MMA issuer
             const uint32_t idesc = pt_idesc(P.Npad);
@@ -274,9 +288,8 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
                 tc_commit(tc_smem(&s_accfull[buf]));
             }
         }
-    } else if (warp < kPtGatherWarps) {  // gather: two threads per patch row (halves of the row)
-        const int nchunk = P.Fpad >> 4, hc = (nchunk + 1) >> 1;
-        const int gh = tid >> 7;
+    } else if (warp < kPtGatherWarps) {  // gather: one thread per patch row
+        const int nchunk = P.Fpad >> 4;
         for (uint64_t i = 0; i < nloc; ++i) {
             const int buf = static_cast<int>(i & 1);
             const uint32_t use = static_cast<uint32_t>(i >> 1);
@@ -284,7 +297,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
             const uint64_t tile = blockIdx.x + i * gridDim.x;
             if (P.abl & 1) {
             } else if (KT == 0) {
-                pt_gather(P, s_wtab, tile, tc_smem(sA + buf * abytes), tid & 127, gh ? hc : 0, gh ? nchunk : hc);
+                pt_gather(P, s_wtab, tile, tc_smem(sA + buf * abytes), tid, 0, nchunk);
             } else {
                 const int r = tid & 127;
                 const uint64_t pr = tile * kPtRows + r;
@@ -296,11 +309,11 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
                 }
                 const uint32_t wC = static_cast<uint32_t>(P.w * P.C), sa = tc_smem(sA + buf * abytes);
                 if (KT == 1) {
-                    if (gh) pt_gather_static<9, 1, 1>(P.img, base, wC, valid, sa, r);
-                    else pt_gather_static<9, 1, 0>(P.img, base, wC, valid, sa, r);
+                    pt_gather_static<9, 1, 0>(P.img, base, wC, valid, sa, r);
+                    pt_gather_static<9, 1, 1>(P.img, base, wC, valid, sa, r);
                 } else {
-                    if (gh) pt_gather_static<11, 3, 1>(P.img, base, wC, valid, sa, r);
-                    else pt_gather_static<11, 3, 0>(P.img, base, wC, valid, sa, r);
+                    pt_gather_static<11, 3, 0>(P.img, base, wC, valid, sa, r);
+                    pt_gather_static<11, 3, 1>(P.img, base, wC, valid, sa, r);
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
             if (lane == 0) tc_mbar_arrive(tc_smem(&s_afull[buf]));
         }
     } else {  // epilogue: TMEM lane quarter ew & 3, layouts of parity ew >> 2, one patch row per thread
-        const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;
+        const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;  // lpar in [0, kPtEpiSets)
         for (uint64_t j = 0; j < nloc; ++j) {
             const int buf = static_cast<int>(j & 1);
             tc_mbar_wait(tc_smem(&s_accfull[buf]), static_cast<uint32_t>(j >> 1) & 1);
@@ -317,7 +330,12 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
             const uint64_t row = tile * kPtRows + q4 * 32 + lane;
             const bool valid = row < P.n;
             const uint32_t tbase = tmem + static_cast<uint32_t>(buf * 256) + (static_cast<uint32_t>(q4 * 32) << 16);
-            for (int li = lpar; li < nl; li += 2) {
+            if (lpar >= nl) {  // no layout for this warp in this group: release the accumulator at once
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
+            }
+            for (int li = lpar; li < nl; li += kPtEpiSets) {
                 constexpr int NC = kPtDigits * D;
                 uint32_t v[NC];
                 const uint32_t ta = tbase + static_cast<uint32_t>(li * NC);
@@ -331,7 +349,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
 #pragma unroll
                 for (int c = NC & ~3; c < NC; ++c) tc_ld_x1(ta + c, v[c]);
                 tc_ld_wait();
-                if (li + 2 >= nl) {  // TMEM of this buffer fully read: release it to the MMA warp early
+                if (li + kPtEpiSets >= nl) {  // TMEM of this buffer fully read: release it to the MMA warp early
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
@@ -365,41 +383,33 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
                         const uint32_t xl = __reduce_max_sync(0xffffffffu, (valid && th == xh) ? tl : 0u);
                         const long long wmn = (static_cast<long long>(mh) << 32) | ml;
                         const long long wmx = (static_cast<long long>(xh) << 32) | xl;
-                        const int slot = (li >> 1) * D + d;  // this warp's (layout, dim) slot: lane slot & 31
-                        if ((slot & 31) == lane) {
-                            if (slot < 32) {
-                                tmn0 = wmn < tmn0 ? wmn : tmn0;
-                                tmx0 = wmx > tmx0 ? wmx : tmx0;
-                            } else {
-                                tmn1 = wmn < tmn1 ? wmn : tmn1;
-                                tmx1 = wmx > tmx1 ? wmx : tmx1;
-                            }
+                        const int slot = (li / kPtEpiSets) * D + d;  // this warp's (layout, dim) slot (< 32)
+                        if (slot == lane) {
+                            tmn0 = wmn < tmn0 ? wmn : tmn0;
+                            tmx0 = wmx > tmx0 ? wmx : tmx0;
                         }
                     } else {
-                        uint32_t q = 0;
-                        if (s_degen[li][d]) {
-                            flag = true;
-                            cand = true;
-                        } else {
-                            const double y = __dsub_rn(__ll2double_rn(T) * 0x1p-38, s_M[li][d]);
-                            const double zf = __fma_rn(y - s_lo[li][d], s_sc[li][d], 0.5);
-                            // floor(zf) through the 2^52 rounding trick (no conversion): the nearest
-                            // integer to zf - 1/2; a tie only happens at an integer zf, which the
-                            // boundary test below flags anyway
-                            const double tq = __dadd_rn(zf, 4503599627370495.5);  // zf - 0.5 + 2^52
-                            const double qf = __dsub_rn(tq, 4503599627370496.0);
-                            const double fr = zf - qf;
-                            const double bz = s_bz[li][d];
-                            if (fr < bz || fr > 1.0 - bz) flag = true;
-                            if (y <= s_lo2[li][d] || y >= s_hi2[li][d]) cand = true;
-                            const int qi = static_cast<int>(static_cast<uint32_t>(__double_as_longlong(tq)));
-                            q = static_cast<uint32_t>(min(max(qi, 0), 255));
-                        }
+                        // degenerate ranges (amax - amin <= 4E) carry bz = 1 and tlo = LLONG_MAX:
+                        // every row is flagged and a lo / hi candidate, with no branch here
+                        const double2 c0 = s_qc[li][d][0], c1 = s_qc[li][d][1];
+                        const double thi = s_qc[li][d][2].x;
+                        const double zf = __fma_rn(__ll2double_rn(T), c0.x, c0.y);
+                        // floor(zf) through the 2^52 rounding trick (no conversion): the nearest
+                        // integer to zf - 1/2; a tie only happens at an integer zf, which the
+                        // boundary test below flags anyway
+                        const double tq = __dadd_rn(zf, 4503599627370495.5);  // zf - 0.5 + 2^52
+                        const double qf = __dsub_rn(tq, 4503599627370496.0);
+                        const double fr = zf - qf;
+                        const double bz = c1.x;
+                        flag = flag || (fr < bz) || (fr > 1.0 - bz);
+                        cand = cand || (T <= __double_as_longlong(c1.y)) || (T >= __double_as_longlong(thi));
+                        const int qi = static_cast<int>(static_cast<uint32_t>(__double_as_longlong(tq)));
+                        const uint32_t q = static_cast<uint32_t>(min(max(qi, 0), 255));
                         const int sh = D - 1 - d;
                         uint32_t prev = 0;
 #pragma unroll
                         for (int k = 0; k < W; ++k) {
-                            const uint32_t cur = s_spread[q][k];
+                            const uint32_t cur = s_spread[(lane >> 3) * kSpStride + q * W + k];
                             kw[k] |= sh ? __funnelshift_l(prev, cur, sh) : cur;
                             prev = cur;
                         }
@@ -427,21 +437,15 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
             }
         }
     }
-    if (MODE == 0 && warp >= kPtGatherWarps && warp < kPtMmaWarp && (warp - kPtGatherWarps) < 8) {
-        const int lpar = ((warp - kPtGatherWarps) >> 2) & 1;
-        for (int k = 0; k < 2; ++k) {
-            const int slot = 32 * k + lane, li = 2 * (slot / D) + lpar, d = slot % D;
-            if (li < nl) {
-                const int l = P.l0 + li;
-                const long long tmn = k ? tmn1 : tmn0, tmx = k ? tmx1 : tmx0;
-                if (tmn <= tmx) {  // the slot saw a valid row: y' of the extreme T (one rounding, as in the epilogue)
-                    const double M = s_M[li][d];
-                    atomicMin(P.amm + static_cast<size_t>(l) * 2 * D + d,
-                              double_to_ordered(__dsub_rn(static_cast<double>(tmn) * 0x1p-38, M)));
-                    atomicMax(P.amm + static_cast<size_t>(l) * 2 * D + D + d,
-                              double_to_ordered(__dsub_rn(static_cast<double>(tmx) * 0x1p-38, M)));
-                }
-            }
+    if (MODE == 0 && warp >= kPtGatherWarps && warp < kPtMmaWarp) {
+        const int lpar = (warp - kPtGatherWarps) >> 2;
+        const int li = kPtEpiSets * (lane / D) + lpar, d = lane % D;
+        if (li < nl && tmn0 <= tmx0) {  // the slot saw a valid row: y' of the extreme T (one rounding, as in the epilogue)
+            const int l = P.l0 + li;
+            const double M = s_M[li][d];
+            atomicMin(P.amm + static_cast<size_t>(l) * 2 * D + d, double_to_ordered(__dsub_rn(static_cast<double>(tmn0) * 0x1p-38, M)));
+            atomicMax(P.amm + static_cast<size_t>(l) * 2 * D + D + d,
+                      double_to_ordered(__dsub_rn(static_cast<double>(tmx0) * 0x1p-38, M)));
         }
     }
     tc_fence_before();
@@ -480,85 +484,91 @@ __global__ void k_pt_prep(const double* __restrict__ mean, const double* __restr
     }
 }
 
-// Canonical fp64 projection of the listed (patch, layout) pairs, one pair per thread (D
-// independent fma chains, j ascending from +0.0 -- the order k_project runs on the FP64 MMA).
-// MODE 0: exact lo / hi (ordered atomics); MODE 1: exact quantised Morton record.
+// Canonical fp64 projection of the listed (patch, layout) pairs: one warp per pair.  The lanes
+// gather the pair's centred pixel values xc_j = x_j - mean_j into shared memory (independent
+// loads), then lane d runs the dimension's fma chain over j ascending from +0.0 -- the order
+// k_project runs on the FP64 MMA -- with the component loads pipelined ahead of the chain.
+// MODE 0: exact lo / hi (ordered atomics, candidates only); MODE 1: exact quantised record.
+constexpr int kPtxWarps = 4;
 template <int D, int MODE>
-__global__ void __launch_bounds__(128) k_pt_exact(const uint8_t* __restrict__ img, int w, int C,
-                                                  const uint32_t* __restrict__ keys, uint64_t n, uint32_t row_base,
-                                                  const int32_t* __restrict__ off, int m,
-                                                  const double* __restrict__ mean, const double* __restrict__ comp,
-                                                  const uint32_t* __restrict__ list,
-                                                  const uint32_t* __restrict__ list_count,
-                                                  unsigned long long* __restrict__ minmax, uint32_t* __restrict__ keyw,
-                                                  uint32_t* __restrict__ val, uint64_t Nrec) {
+__global__ void __launch_bounds__(kPtxWarps * 32) k_pt_exact(const uint8_t* __restrict__ img, int w, int C,
+                                                             const uint32_t* __restrict__ keys, uint64_t n,
+                                                             uint32_t row_base, const int32_t* __restrict__ off, int m,
+                                                             const double* __restrict__ mean,
+                                                             const double* __restrict__ comp,
+                                                             const uint32_t* __restrict__ list,
+                                                             const uint32_t* __restrict__ list_count,
+                                                             unsigned long long* __restrict__ minmax,
+                                                             uint32_t* __restrict__ keyw, uint32_t* __restrict__ val,
+                                                             uint64_t Nrec) {
     constexpr int W = (D + 3) / 4;
+    __shared__ double s_xc[kPtxWarps][232];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t cnt = *list_count;
     const int mc = m * C;
-    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < cnt;
-         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double* xc = s_xc[wib];
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * kPtxWarps + wib; e < cnt;
+         e += static_cast<uint64_t>(gridDim.x) * kPtxWarps) {
         const uint32_t ent = list[e];
-        const uint32_t row = ent >> 4, l = ent & 7;
         if (MODE == 0 && !(ent & 8u)) continue;  // only the lo / hi candidates take part in the min / max
+        const uint32_t row = ent >> 4, l = ent & 7;
         const uint32_t key = keys[row];
         const uint8_t* pb = img + static_cast<size_t>((key >> 16) * static_cast<uint32_t>(w) + (key & 0xffffu)) * C;
-        double y[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) y[d] = 0.0;
-        const double* mp = mean + static_cast<size_t>(l) * mc;
-        const double* cp = comp + static_cast<size_t>(l) * mc * D;
-        const int32_t* op = off + static_cast<size_t>(l) * m;
-        for (int p = 0; p < m; ++p) {
-            const int o = __ldg(op + p);
-            for (int ch = 0; ch < C; ++ch) {
-                const int j = p * C + ch;
-                const double xc = __dsub_rn(static_cast<double>(__ldg(pb + o + ch)), __ldg(mp + j));
-#pragma unroll
-                for (int d = 0; d < D; ++d) y[d] = __fma_rn(xc, __ldg(cp + static_cast<size_t>(j) * D + d), y[d]);
-            }
+        for (int j = lane; j < mc; j += 32) {
+            const int p = j / C, ch = j - p * C;
+            xc[j] = __dsub_rn(static_cast<double>(__ldg(pb + __ldg(off + l * m + p) + ch)), __ldg(mean + l * mc + j));
         }
+        __syncwarp();
+        double y = 0.0;
+        if (lane < D) {
+            const double* cp = comp + static_cast<size_t>(l) * mc * D + lane;
+#pragma unroll 8
+            for (int j = 0; j < mc; ++j) y = __fma_rn(xc[j], __ldg(cp + static_cast<size_t>(j) * D), y);
+        }
+        __syncwarp();
         unsigned long long* mm = minmax + static_cast<size_t>(l) * 2 * D;
         if (MODE == 0) {
-#pragma unroll
-            for (int d = 0; d < D; ++d) {
-                const unsigned long long o = double_to_ordered(y[d]);
-                atomicMin(mm + d, o);
-                atomicMax(mm + D + d, o);
+            if (lane < D) {
+                const unsigned long long o = double_to_ordered(y);
+                atomicMin(mm + lane, o);
+                atomicMax(mm + D + lane, o);
             }
         } else {
-            uint32_t kw[W];
-#pragma unroll
-            for (int k = 0; k < W; ++k) kw[k] = 0;
-#pragma unroll
-            for (int d = 0; d < D; ++d) {
-                const double lo = ordered_to_double_hd(mm[d]), hi = ordered_to_double_hd(mm[D + d]);
+            uint32_t q = 0;
+            if (lane < D) {
+                const double lo = ordered_to_double_hd(mm[lane]), hi = ordered_to_double_hd(mm[D + lane]);
                 const double rcp = hi > lo ? __ddiv_rn(1.0, __dsub_rn(hi, lo)) : 0.0;
-                const uint32_t q = quantize_fast(lo, hi, rcp, y[d]);
-#pragma unroll
-                for (int L = 0; L < 8; ++L) {
-                    const int pos = L * D + D - 1 - d;
-                    kw[pos >> 5] |= ((q >> L) & 1u) << (pos & 31);
-                }
+                q = quantize_fast(lo, hi, rcp, y);
             }
             const uint64_t er = static_cast<uint64_t>(l) * n + row;
 #pragma unroll
-            for (int k = 0; k < W; ++k) keyw[static_cast<size_t>(k) * Nrec + er] = kw[k];
-            val[er] = (l << 29) | (row_base + row);
+            for (int k = 0; k < W; ++k) {
+                uint32_t part = 0;
+                if (lane < D)
+#pragma unroll
+                    for (int L = 0; L < 8; ++L) {
+                        const int pos = L * D + D - 1 - lane;
+                        if ((pos >> 5) == k) part |= ((q >> L) & 1u) << (pos & 31);
+                    }
+                const uint32_t word = __reduce_or_sync(0xffffffffu, part);
+                if (lane == 0) keyw[static_cast<size_t>(k) * Nrec + er] = word;
+            }
+            if (lane == 0) val[er] = (l << 29) | (row_base + row);
         }
     }
 }
 
 template <int D>
 static void launch_pt_exact(zi_ctx* ctx, zi_multi_index* mi, const pt_params& P, int mode) {
-    const unsigned grid = static_cast<unsigned>(ctx->num_sms) * 4;
+    const unsigned grid = static_cast<unsigned>(ctx->num_sms) * 8;
     const uint32_t* keys = mi->dict.p + mi->row_begin;
     const uint32_t rb = static_cast<uint32_t>(mi->row_begin);
     if (mode == 0)
-        ZI_LAUNCH(ctx, "project_tc_exact_minmax", (k_pt_exact<D, 0>), grid, 128, 0, mi->image.p, mi->w, mi->C, keys, mi->n,
+        ZI_LAUNCH(ctx, "project_tc_exact_minmax", (k_pt_exact<D, 0>), grid, kPtxWarps * 32, 0, mi->image.p, mi->w, mi->C, keys, mi->n,
                   rb, mi->layout_off.p, mi->m, mi->pca_mean.p, mi->pca_comp.p, P.list, P.list_count, mi->minmax.p, P.keyw,
                   P.val, P.Nrec);
     else
-        ZI_LAUNCH(ctx, "project_tc_fixup", (k_pt_exact<D, 1>), grid, 128, 0, mi->image.p, mi->w, mi->C, keys, mi->n, rb,
+        ZI_LAUNCH(ctx, "project_tc_fixup", (k_pt_exact<D, 1>), grid, kPtxWarps * 32, 0, mi->image.p, mi->w, mi->C, keys, mi->n, rb,
                   mi->layout_off.p, mi->m, mi->pca_mean.p, mi->pca_comp.p, P.list, P.list_count, mi->minmax.p, P.keyw,
                   P.val, P.Nrec);
 }
@@ -581,9 +591,13 @@ static void launch_pt_kt(zi_ctx* ctx, const pt_params& P, int mode, size_t smem)
 template <int D>
 static void launch_pt(zi_ctx* ctx, const pt_params& P, int mode, size_t smem) {
     const int kt = P.KC == 9 && P.F == 81 ? 1 : (P.KC == 33 && P.F == 363 ? 2 : 0);
-    if (D == 8 && kt == 1) launch_pt_kt<D, 1>(ctx, P, mode, smem);
-    else if ((D == 12 || D == 8) && kt == 2) launch_pt_kt<D, 2>(ctx, P, mode, smem);
-    else launch_pt_kt<D, 0>(ctx, P, mode, smem);
+    if constexpr (D == 8) {
+        if (kt == 1) return launch_pt_kt<D, 1>(ctx, P, mode, smem);
+    }
+    if constexpr (D == 8 || D == 12) {
+        if (kt == 2) return launch_pt_kt<D, 2>(ctx, P, mode, smem);
+    }
+    launch_pt_kt<D, 0>(ctx, P, mode, smem);
 }
 
 bool project_quantize_tc(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec) {
@@ -592,7 +606,7 @@ bool project_quantize_tc(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint
     const int D = mi->dims, K = mi->K, C = mi->C, m = mi->m, mc = mi->mc;
     const int F = K * K * C, Fpad = (F + 127) / 128 * 128;
     const uint64_t n = mi->n;
-    if (off_env || D < 1 || D > 16 || Fpad > kPtMaxFpad || n == 0 || n >= (1ull << 27)) return false;
+    if (off_env || D < 1 || D > 16 || Fpad > kPtMaxFpad || mc > 232 || n == 0 || n >= (1ull << 27)) return false;
     const int nlmax = std::min(8, kPtMaxN / (kPtDigits * D));
     const int ng = (8 + nlmax - 1) / nlmax;
     int goff[8], gnpad[8];
