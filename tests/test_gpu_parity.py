@@ -737,3 +737,75 @@ def test_sharded_multi_index_over_nccl_world1(zb):
             assert smi.brute_force_best(tv, tk) == mi.brute_force_best(tv, tk)[:2]
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ tensor-core projection filter
+_FP64_DUMP = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1712_06326_b200 as zb, workloads
+img, kn, p = getattr(workloads, sys.argv[2])()
+mi = zb.MultiIndex(img, kn, zb.index_config(**p))
+out = {}
+for l in range(8):
+    c, k = mi.index_arrays(l); lay = mi.layout(l)
+    out[f"c{l}"], out[f"k{l}"], out[f"lo{l}"], out[f"hi{l}"] = c, k, lay["lo"], lay["hi"]
+np.savez(sys.argv[3], **out)
+"""
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+def test_projection_tc_equals_fp64_path(zb, cfg, tmp_path):
+    """The int8 tensor-core filter + fix-up writes the same index bytes and quantiser ranges as the
+    canonical FP64-MMA path (ZI_PROJ_FP64=1, another process) at full config size."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dump = tmp_path / "fp64.npz"
+    env = dict(os.environ, ZI_PROJ_FP64="1")
+    subprocess.run([sys.executable, "-c", _FP64_DUMP, root, cfg, str(dump)], env=env, check=True, timeout=600)
+    ref = np.load(dump)
+    img, kn, p = getattr(workloads, cfg)()
+    mi = zb.MultiIndex(img, kn, zb.index_config(**p))
+    for l in range(8):
+        c, k = mi.index_arrays(l)
+        lay = mi.layout(l)
+        assert np.array_equal(lay["lo"].view(np.uint64), ref[f"lo{l}"].view(np.uint64)), l
+        assert np.array_equal(lay["hi"].view(np.uint64), ref[f"hi{l}"].view(np.uint64)), l
+        assert np.array_equal(c, ref[f"c{l}"]) and np.array_equal(k, ref[f"k{l}"]), l
+
+
+@pytest.mark.parametrize("case", ["two_level", "rgb_k7_d16", "rgb_k5_d1", "gray_k9_d13", "stripes_k11_rgb"])
+def test_projection_tc_edge_cases_vs_oracle(zb, case):
+    """Degenerate ranges (every pair re-projected exactly), the generic table gather (K*C not
+    specialised), D = 1 and D = 16, ties at the extremes -- byte-equal to the oracle fed the
+    build's PCA model."""
+    rng = np.random.default_rng(17)
+    if case == "two_level":
+        img = (rng.random((40, 52)) < 0.5).astype(np.uint8) * 200 + 20
+        K, D, C = 5, 4, 1
+    elif case == "rgb_k7_d16":
+        img, _ = workloads.small_image(56, 64, 3, seed=3, hole_frac=0.0)
+        K, D, C = 7, 16, 3
+    elif case == "rgb_k5_d1":
+        img, _ = workloads.small_image(40, 48, 3, seed=4, hole_frac=0.0)
+        K, D, C = 5, 1, 3
+    elif case == "gray_k9_d13":
+        img, _ = workloads.small_image(64, 72, 1, seed=5, hole_frac=0.0)
+        K, D, C = 9, 13, 1
+    else:  # vertical stripes: most components see a handful of distinct values
+        x = np.arange(60)[None, :, None]
+        img = np.broadcast_to(((x // 3) % 4 * 60).astype(np.uint8), (50, 60, 3)).copy()
+        K, D, C = 11, 12, 3
+    kn = np.ones(img.shape[:2], np.uint8)
+    kn[img.shape[0] // 3: img.shape[0] // 3 + 6, 10:18] = 0
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=K, dims=D))
+    pm, pc = pca_of(mi)
+    om = oracle.MultiIndex(img, kn, K, 0.6, D, pca_mean=pm, pca_comp=pc)
+    for l in range(8):
+        c, k = mi.index_arrays(l)
+        ref = om.index(l)
+        lay = mi.layout(l)
+        assert np.array_equal(lay["lo"], ref.lo) and np.array_equal(lay["hi"], ref.hi), (case, l)
+        assert np.array_equal(c, ref.coords) and np.array_equal(k, ref.keys), (case, l)
