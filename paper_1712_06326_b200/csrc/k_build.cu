@@ -148,8 +148,8 @@ uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, i
 // S = sum_p x_p x_p^T and s = sum_p x_p over the full K*K*C patch vectors (u8), exact.
 // Two kernels:
 //   k_patch_matrix  the feature-major patch matrix XT[f][p] (Fpad x npad u8, zero padded) in HBM:
-//                   one warp writes 4 features x 128 consecutive patches (coalesced 16 B stores),
-//                   reading adjacent pixels of the image (L1/L2 resident).
+//                   one warp writes one feature x 128 consecutive patches (one coalesced 128 B
+//                   store), reading adjacent pixels of the image (L1/L2 resident).
 //   k_moments       X^T X on the tensor cores (mma.sync m16n8k32 u8 x u8 -> s32): one CTA = one
 //                   128x128 feature tile pair (ti <= tj) x one patch chunk; 128-patch stages
 //                   stream in with cp.async (3-stage ring, 144 B pitch -> conflict-free ldmatrix).
@@ -206,20 +206,22 @@ __global__ void __launch_bounds__(256) k_patch_matrix(const uint8_t* __restrict_
     for (int f = tid; f < Fpad; f += 256)
         s_off[f] = f < F ? (((f / C) / K) * w + (f / C) % K) * C + f % C : (f == F ? -2 : -1);
     __syncthreads();
-    // 8 threads per feature, 16 consecutive patches (adjacent pixels) each: 16 gathered bytes ->
-    // one 16-byte store; a warp writes 4 features x 128 patches
-    const int g = tid & 7;
-    for (int f = tid >> 3; f < Fpad; f += 32) {
-        const int of = s_off[f];
-        uint32_t wv[4] = {0u, 0u, 0u, 0u};
+    // one warp per feature row, lane l = patches 4l..4l+3: the warp's loads of one feature cover
+    // 128 adjacent pixels (a few 128-byte lines per instruction) and it stores 128 contiguous bytes
+    const int lane = tid & 31, warp = tid >> 5;
+    int bs[4];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int bs = s_base[16 * g + i];
+    for (int j = 0; j < 4; ++j) bs[j] = s_base[4 * lane + j];
+    for (int f = warp; f < Fpad; f += 8) {
+        const int of = s_off[f];
+        uint32_t wv = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
             uint32_t v = 0;
-            if (bs >= 0) v = of >= 0 ? static_cast<uint32_t>(__ldg(img + bs + of)) : (of == -2 ? 1u : 0u);
-            wv[i >> 2] |= v << (8 * (i & 3));
+            if (bs[j] >= 0) v = of >= 0 ? static_cast<uint32_t>(__ldg(img + bs[j] + of)) : (of == -2 ? 1u : 0u);
+            wv |= v << (8 * j);
         }
-        *reinterpret_cast<uint4*>(XT + static_cast<size_t>(f) * npad + p0 + 16 * g) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        *reinterpret_cast<uint32_t*>(XT + static_cast<size_t>(f) * npad + p0 + 4 * lane) = wv;
     }
 }
 
