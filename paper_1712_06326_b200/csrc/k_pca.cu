@@ -18,6 +18,11 @@
 //   k_pca_fin  one CTA per layout: Gram-Schmidt inside clusters of close eigenvalues, the
 //              reference's sign rule (first max-|v| entry positive), eigenvalue clamp at 0, and
 //              the components written straight into the projection kernels' [j][d] layout.
+//   k_pca_lz   (first, when ZI_PCA_LZ is not 0) the Lanczos fast path: K = max(32, 2D+8) steps
+//              with full reorthogonalisation on the same distributed rows, then k_pca_vec in
+//              Lanczos mode solves T_K and forms the Ritz vectors; a layout whose Ritz residuals
+//              are not below 1e-12 |T| (or whose Krylov space broke down early) runs the
+//              Householder kernels above, which skip every layout the fast path delivered.
 // The host eigen-solver (host_pca.cpp) remains for m*C > 224.
 #include <cooperative_groups.h>
 
@@ -235,9 +240,11 @@ __device__ inline double warp_allsum(double v) {
 }
 
 // work buffer layout (doubles), see pca_work_doubles
+constexpr int kLzMax = 64;  // Lanczos steps at most
 struct pca_work_view {
     double *d, *e, *tau, *tn, *lam, *X, *refl;
     size_t rstride;
+    double *lzab, *lzk, *lzQ, *stat;  // Lanczos: alpha/beta [8][2][kLzMax], steps [8], Q [8][kLzMax][n], status [8]
 };
 __host__ __device__ inline pca_work_view pca_work_split(double* w, int n, int D) {
     pca_work_view v;
@@ -250,10 +257,15 @@ __host__ __device__ inline pca_work_view pca_work_split(double* w, int n, int D)
     v.refl = v.X + static_cast<size_t>(8) * D * n;
     v.refl += (reinterpret_cast<uintptr_t>(v.refl) & 15) ? 1 : 0;  // 16-byte aligned for TMA
     v.rstride = refl_stride(n);
+    v.lzab = v.refl + 8 * v.rstride;
+    v.lzk = v.lzab + 8 * 2 * kLzMax;
+    v.stat = v.lzk + 8;
+    v.lzQ = v.stat + 8;
     return v;
 }
 size_t pca_work_doubles(int mc, int D) {
-    return static_cast<size_t>(8) * (3 * mc + 1 + 32 + static_cast<size_t>(D) * mc) + 8 * refl_stride(mc) + 4;
+    return static_cast<size_t>(8) * (3 * mc + 1 + 32 + static_cast<size_t>(D) * mc) + 8 * refl_stride(mc) + 4 +
+           8 * (2 * kLzMax + 2 + static_cast<size_t>(kLzMax) * mc);
 }
 
 struct tri_args {
@@ -267,27 +279,19 @@ struct tri_args {
     long long* dbg;  // optional per-phase clock totals (ZI_DEBUG_PCA)
     const double* cov;  // optional: precomputed covariance per model (mc x mc, row-major); the
                         // moments, cols and mean are then unused
+    int lzk;            // Lanczos steps (0: Householder path only)
 };
 
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca_tri(tri_args a) {
-    extern __shared__ double sm[];
-    cg::cluster_group cl = cg::this_cluster();
-    const int n = a.mc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int kWarps = kTriThreads / 32;
-    const int rank = static_cast<int>(cl.block_rank());
-    const int l = blockIdx.x / kCl;
-    const int rows_max = (n + kCl - 1) / kCl;
-    const int nloc = rank < n ? (n - rank + kCl - 1) / kCl : 0;  // my rows: i = rank + kCl * li
-    double* A = sm;                                          // rows_max x n, full rows
-    double* v = A + static_cast<size_t>(rows_max) * n;       // [2][n] reflector, by column parity
-    double* p = v + 2 * n;                                   // [2][n] tau * A v
-    double* npart = p + 2 * n;                               // [2][kCl][warps] partial |column|^2
+// this CTA's rows i = rank + kCl*li of layout l's covariance (int128 numerators, correctly rounded)
+// or of a precomputed covariance; rank 0 also writes the layout's mean
+__device__ void pca_load_rows(const tri_args& a, int l, int rank, int n, int nloc, double* A) {
+    const int tid = threadIdx.x;
     const long long* s = reinterpret_cast<const long long*>(a.moments);
     const long long* S = s + a.F;
     const long long nn = static_cast<long long>(a.n);
     const int32_t* cols = a.cols + l * n;
     const double den = a.n > 1 ? static_cast<double>(a.n) * static_cast<double>(a.n - 1) : 1.0;
-    for (int idx = tid; idx < nloc * n; idx += kTriThreads) {
+    for (int idx = tid; idx < nloc * n; idx += blockDim.x) {
         const int li = idx / n, j = idx - li * n, i = rank + kCl * li;
         if (a.cov) {
             A[idx] = a.cov[(static_cast<size_t>(l) * n + i) * n + j];
@@ -304,8 +308,25 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
         A[idx] = i128_to_double(num) / den;
     }
     if (rank == 0 && !a.cov)
-        for (int i = tid; i < n; i += kTriThreads)
+        for (int i = tid; i < n; i += blockDim.x)
             a.mean[l * n + i] = static_cast<double>(s[cols[i]]) / static_cast<double>(a.n);
+}
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca_tri(tri_args a) {
+    extern __shared__ double sm[];
+    if (a.lzk > 0 && a.w.stat[blockIdx.x / kCl] == 0.0) return;  // the Lanczos path delivered this layout
+    cg::cluster_group cl = cg::this_cluster();
+    const int n = a.mc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kTriThreads / 32;
+    const int rank = static_cast<int>(cl.block_rank());
+    const int l = blockIdx.x / kCl;
+    const int rows_max = (n + kCl - 1) / kCl;
+    const int nloc = rank < n ? (n - rank + kCl - 1) / kCl : 0;  // my rows: i = rank + kCl * li
+    double* A = sm;                                          // rows_max x n, full rows
+    double* v = A + static_cast<size_t>(rows_max) * n;       // [2][n] reflector, by column parity
+    double* p = v + 2 * n;                                   // [2][n] tau * A v
+    double* npart = p + 2 * n;                               // [2][kCl][warps] partial |column|^2
+    pca_load_rows(a, l, rank, n, nloc, A);
     double* d_out = a.w.d + l * n;
     double* e_out = a.w.e + l * n;
     double* tau_out = a.w.tau + l * n;
@@ -484,10 +505,183 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca
     cluster_barrier();  // no CTA leaves while a peer may still store into its shared memory
 }
 
+// ------------------------------------------------------------------ Lanczos fast path
+// k_pca_lz: one 8-CTA cluster per layout runs K steps of Lanczos with full reorthogonalisation
+// (classical Gram-Schmidt twice, DGKS) on the covariance, rows distributed as in k_pca_tri.  The
+// top eigenpairs of image-patch covariances converge in ~30 steps (they need only the leading
+// part of the spectrum, against the 219 columns of a full tridiagonalisation).  Per step, three
+// cluster exchanges, each st.async stores completing bytes on the receivers' mbarriers:
+//   A  partial Q^T w      -> c1 (w -= Q c1)
+//   B  partial Q^T w, |w|^2 -> c2 (w -= Q c2), beta^2 = |w|^2 - |c2|^2
+//   C  the rows of q_{j+1} = w / beta into every CTA's full vector
+// Every sum runs in a fixed order, so all CTAs hold identical alpha / beta.  k_pca_vec (Lanczos
+// mode) then solves T_K, checks every Ritz residual |beta_K s_K| and falls the layout back to
+// the Householder path (k_pca_tri + k_pca_vec) when one is not negligible.
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTriThreads) k_pca_lz(tri_args a) {
+    extern __shared__ double sm[];
+    __shared__ double s_red[kTriThreads / 32];
+    __shared__ double s_ab[2 * kLzMax];
+    __shared__ __align__(8) unsigned long long s_bar[3];
+    __shared__ int s_k;
+    cg::cluster_group cl = cg::this_cluster();
+    const int n = a.mc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kTriThreads / 32;
+    constexpr int RS = kLzMax + 2;  // stride of a CTA's partials
+    const int rank = static_cast<int>(cl.block_rank());
+    const int l = blockIdx.x / kCl;
+    const int rows_max = (n + kCl - 1) / kCl;
+    const int nloc = rank < n ? (n - rank + kCl - 1) / kCl : 0;  // my rows: i = rank + kCl * li
+    const int K = min(n, a.lzk);
+    double* A = sm;                                      // rows_max x n
+    double* Q = A + static_cast<size_t>(rows_max) * n;   // [kLzMax][rows_max]
+    double* qf = Q + static_cast<size_t>(kLzMax) * rows_max;  // [2][n] full Lanczos vector
+    double* wl = qf + 2 * n;                             // rows_max
+    double* red0 = wl + rows_max;                        // [kCl][RS]
+    double* red1 = red0 + kCl * RS;                      // [kCl][RS]
+    double* part = red1 + kCl * RS;                      // RS
+    double* c1 = part + RS;                              // RS
+    double* c2 = c1 + RS;                                // RS
+    pca_load_rows(a, l, rank, n, nloc, A);
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init(smem_addr(&s_bar[i]));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_k = K;
+    }
+    // deterministic start vector (identical on every CTA)
+    double p0 = 0.0;
+    for (int i = tid; i < n; i += kTriThreads) {
+        const double f = 1.0 + 0.25 * sin(1.6180339887498949 * i);
+        qf[i] = f;
+        p0 = fma(f, f, p0);
+    }
+    const double inv0 = 1.0 / sqrt(cta_sum<kTriThreads>(p0, s_red));
+    for (int i = tid; i < n; i += kTriThreads) qf[i] *= inv0;
+    __syncthreads();
+    for (int li = tid; li < nloc; li += kTriThreads) Q[li] = qf[rank + kCl * li];
+    const unsigned red0_l = smem_addr(red0), red1_l = smem_addr(red1), qf_l = smem_addr(qf);
+    const unsigned barA = smem_addr(&s_bar[0]), barB = smem_addr(&s_bar[1]), barC = smem_addr(&s_bar[2]);
+    unsigned ph = 0;  // the three barriers complete once per step each: one shared phase bit
+    __syncthreads();
+    cluster_barrier();  // every mbarrier of the cluster is initialised before the first push
+    for (int j = 0; j < K; ++j) {
+        const int b = j & 1, nt = j + 1;
+        const double* q = qf + b * n;
+        // (1) my rows of w = A q
+        for (int li = warp; li < nloc; li += kWarps) {
+            double acc = 0.0;
+            for (int c = lane; c < n; c += 32) acc = fma(A[static_cast<size_t>(li) * n + c], q[c], acc);
+            acc = warp_allsum(acc);
+            if (lane == 0) wl[li] = acc;
+        }
+        __syncthreads();
+        // (2) round A: partial Q^T w over my rows -> every CTA
+        if (tid < nt) {
+            double acc = 0.0;
+            for (int li = 0; li < nloc; ++li) acc = fma(Q[tid * rows_max + li], wl[li], acc);
+            part[tid] = acc;
+        }
+        __syncthreads();
+        if (tid == 0) mbar_expect(barA, static_cast<unsigned>(kCl * nt * 8));
+        for (int idx = tid; idx < kCl * nt; idx += kTriThreads) {
+            const int pr = idx / nt, t = idx - pr * nt;
+            st_async_f64(peer_addr(red0_l + 8u * (rank * RS + t), pr), part[t], peer_addr(barA, pr));
+        }
+        mbar_wait_cluster(barA, ph);
+        if (tid < nt) {
+            double acc = 0.0;
+#pragma unroll
+            for (int r = 0; r < kCl; ++r) acc += red0[r * RS + tid];
+            c1[tid] = acc;
+        }
+        __syncthreads();
+        if (tid < nloc) {
+            double w = wl[tid];
+            for (int t = 0; t < nt; ++t) w = fma(-c1[t], Q[t * rows_max + tid], w);
+            wl[tid] = w;
+        }
+        __syncthreads();
+        // (3) round B: partial Q^T w and |w|^2
+        if (tid <= nt) {
+            double acc = 0.0;
+            if (tid < nt)
+                for (int li = 0; li < nloc; ++li) acc = fma(Q[tid * rows_max + li], wl[li], acc);
+            else
+                for (int li = 0; li < nloc; ++li) acc = fma(wl[li], wl[li], acc);
+            part[tid] = acc;
+        }
+        __syncthreads();
+        if (tid == 0) mbar_expect(barB, static_cast<unsigned>(kCl * (nt + 1) * 8));
+        for (int idx = tid; idx < kCl * (nt + 1); idx += kTriThreads) {
+            const int pr = idx / (nt + 1), t = idx - pr * (nt + 1);
+            st_async_f64(peer_addr(red1_l + 8u * (rank * RS + t), pr), part[t], peer_addr(barB, pr));
+        }
+        mbar_wait_cluster(barB, ph);
+        if (tid <= nt) {
+            double acc = 0.0;
+#pragma unroll
+            for (int r = 0; r < kCl; ++r) acc += red1[r * RS + tid];
+            c2[tid] = acc;
+        }
+        __syncthreads();
+        if (tid < nloc) {
+            double w = wl[tid];
+            for (int t = 0; t < nt; ++t) w = fma(-c2[t], Q[t * rows_max + tid], w);
+            wl[tid] = w;
+        }
+        double b2 = c2[nt];
+        for (int t = 0; t < nt; ++t) b2 = fma(-c2[t], c2[t], b2);
+        const double beta = sqrt(fmax(b2, 0.0));
+        if (tid == 0) {
+            s_ab[j] = c1[j] + c2[j];
+            s_ab[kLzMax + j] = beta;
+        }
+        double anorm = 0.0;
+        for (int t = 0; t <= j; ++t) anorm = fmax(anorm, fabs(c1[t] + c2[t]));
+        __syncthreads();
+        if (j + 1 == K || !(beta > 1e-13 * anorm)) {  // done, or an invariant subspace
+            if (tid == 0) s_k = j + 1;
+            break;
+        }
+        // (4) round C: my rows of q_{j+1} into every CTA's full vector
+        const double ib = 1.0 / beta;
+        if (tid == 0) mbar_expect(barC, static_cast<unsigned>(n * 8));
+        const unsigned qn = qf_l + 8u * static_cast<unsigned>((b ^ 1) * n);
+        for (int idx = tid; idx < kCl * nloc; idx += kTriThreads) {
+            const int pr = idx / nloc, li = idx - pr * nloc;
+            const double v = wl[li] * ib;
+            if (pr == 0) Q[(j + 1) * rows_max + li] = v;
+            st_async_f64(peer_addr(qn + 8u * static_cast<unsigned>(rank + kCl * li), pr), v, peer_addr(barC, pr));
+        }
+        mbar_wait_cluster(barC, ph);
+        ph ^= 1;
+        __syncthreads();
+    }
+    __syncthreads();
+    const int k = s_k;
+    if (rank == 0) {
+        for (int t = tid; t < k; t += kTriThreads) {
+            a.w.lzab[l * 2 * kLzMax + t] = s_ab[t];
+            a.w.lzab[l * 2 * kLzMax + kLzMax + t] = s_ab[kLzMax + t];
+        }
+        if (tid == 0) {
+            a.w.lzk[l] = static_cast<double>(k);
+            a.w.stat[l] = 0.0;
+        }
+    }
+    double* Qg = a.w.lzQ + static_cast<size_t>(l) * kLzMax * n;
+    for (int idx = tid; idx < k * nloc; idx += kTriThreads) {
+        const int t = idx / nloc, li = idx - t * nloc;
+        Qg[static_cast<size_t>(t) * n + rank + kCl * li] = Q[t * rows_max + li];
+    }
+    cluster_barrier();  // no CTA leaves while a peer may still store into its shared memory
+}
+
 struct vec_args {
     int mc, D;
     pca_work_view w;
     long long* dbg;  // optional phase clocks (ZI_DEBUG_PCA): per CTA 4 values
+    int lzmode;      // 1: eigenpairs of the Lanczos T_K and Ritz vectors Q s; 0: Householder path
+    int lztried;     // Householder mode: skip the layouts the Lanczos path delivered
 };
 
 __device__ inline unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -497,8 +691,15 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
     __shared__ __align__(8) unsigned long long s_bar;
     __shared__ int s_first[kVecThreads / 32];
     __shared__ double s_scal[4];
-    const int n = a.mc, D = a.D, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = a.D, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int l = blockIdx.x / D, j = blockIdx.x % D;
+    if (!a.lzmode && a.lztried && a.w.stat[l] == 0.0) return;  // the Lanczos path delivered this layout
+    // the tridiagonal: Householder's T (size mc) or Lanczos' T_K (size K)
+    const int n = a.lzmode ? static_cast<int>(a.w.lzk[l]) : a.mc;
+    if (a.lzmode && j >= n) {  // fewer Lanczos vectors than components: Householder path
+        if (tid == 0) a.w.stat[l] = 1.0;
+        return;
+    }
     const long long t_start = clock64();
     const size_t nref = a.w.rstride;
     double* R = sm;         // reflectors (TMA)
@@ -511,7 +712,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
     unsigned char* piv = reinterpret_cast<unsigned char*>(f + 4 * n);
     const double* src = a.w.refl + l * a.w.rstride;
     const unsigned bytes = static_cast<unsigned>(nref * sizeof(double));
-    if (tid == 0) {
+    if (tid == 0 && !a.lzmode) {
         const unsigned bar = smem_u32(&s_bar);
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -523,11 +724,20 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
                      : "memory");
     }
     for (int i = tid; i < n; i += kVecThreads) {
-        dd[i] = a.w.d[l * n + i];
-        const double ei = i + 1 < n ? a.w.e[l * n + i] : 0.0;
-        ee[i] = ei;
-        e2[i] = ei * ei;
-        tau[i] = a.w.tau[l * n + i];
+        if (a.lzmode) {
+            const double* ab = a.w.lzab + l * 2 * kLzMax;
+            dd[i] = ab[i];
+            const double ei = i + 1 < n ? ab[kLzMax + i] : 0.0;
+            ee[i] = ei;
+            e2[i] = ei * ei;
+            tau[i] = 0.0;
+        } else {
+            dd[i] = a.w.d[l * n + i];
+            const double ei = i + 1 < n ? a.w.e[l * n + i] : 0.0;
+            ee[i] = ei;
+            e2[i] = ei * ei;
+            tau[i] = a.w.tau[l * n + i];
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -608,9 +818,24 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
         double rq = dd[0] * x[0] * x[0];
         for (int i = 1; i < n; ++i) rq = fma(dd[i] * x[i], x[i], fma(2.0 * ee[i - 1] * x[i - 1], x[i], rq));
         a.w.lam[l * 32 + j] = rq;
+        if (a.lzmode) {  // Ritz residual |A y - theta y| = |beta_K s_K| (full reorthogonalisation)
+            const double res = fabs(a.w.lzab[l * 2 * kLzMax + kLzMax + n - 1] * x[n - 1]);
+            if (!(res <= 1e-12 * safe)) a.w.stat[l] = 1.0;
+        }
     }
     __syncthreads();
     const long long t_inv = clock64();
+    if (a.lzmode) {  // Ritz vector y = Q_K s
+        const int nn = a.mc;
+        const double* Qg = a.w.lzQ + static_cast<size_t>(l) * kLzMax * nn;
+        double* out = a.w.X + (static_cast<size_t>(l) * D + j) * nn;
+        for (int i = tid; i < nn; i += kVecThreads) {
+            double acc = 0.0;
+            for (int t = 0; t < n; ++t) acc = fma(Qg[static_cast<size_t>(t) * nn + i], x[t], acc);
+            out[i] = acc;
+        }
+        return;
+    }
     // back-transformation x = H_0 ... H_{n-3} x, one warp, the vector in registers
     if (warp == 0) {
         const unsigned bar = smem_u32(&s_bar);
@@ -753,7 +978,22 @@ static bool pca_launch(zi_ctx* ctx, int nl, const double* d_cov, const unsigned 
         attr_fin = smem_fin;
     }
     const pca_work_view w = pca_work_split(d_work, mc, D);
-    tri_args ta{d_moments, F, n, d_cols, mc, d_mean, w, nullptr, d_cov};
+    static const char* lz_env = std::getenv("ZI_PCA_LZ");
+    const bool lz_on = !(lz_env && lz_env[0] == '0');
+    const int lzk = lz_on ? std::min(std::min(mc, kLzMax), std::max(32, 2 * D + 8)) : 0;
+    tri_args ta{d_moments, F, n, d_cols, mc, d_mean, w, nullptr, d_cov, lzk};
+    if (lzk > 0) {
+        const size_t smem_lz = (static_cast<size_t>(rows_max) * mc + static_cast<size_t>(kLzMax) * rows_max + 2 * mc +
+                                rows_max + (2 * kCl + 3) * (kLzMax + 2)) * sizeof(double);
+        static size_t attr_lz = 0;
+        if (smem_lz > attr_lz) {
+            ZI_CUDA(cudaFuncSetAttribute(k_pca_lz, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_lz)));
+            attr_lz = smem_lz;
+        }
+        ZI_LAUNCH(ctx, "pca_lanczos", k_pca_lz, nl * kCl, kTriThreads, smem_lz, ta);
+        vec_args la{mc, D, w, nullptr, 1, 0};
+        ZI_LAUNCH(ctx, "pca_ritz", k_pca_vec, nl * D, kVecThreads, smem_vec, la);
+    }
     static const bool debug = std::getenv("ZI_DEBUG_PCA") != nullptr;
     static dbuf<long long> dbg;
     if (debug) {
@@ -769,7 +1009,7 @@ static bool pca_launch(zi_ctx* ctx, int nl, const double* d_cov, const unsigned 
             std::fprintf(stderr, "tri cta %2d: start %lld B %lld bar1 %lld C %lld push %lld bar2 %lld\n", c, h[c * 8],
                          h[c * 8 + 1], h[c * 8 + 2], h[c * 8 + 3], h[c * 8 + 4], h[c * 8 + 5]);
     }
-    vec_args va{mc, D, w, nullptr};
+    vec_args va{mc, D, w, nullptr, 0, lzk > 0 ? 1 : 0};
     static dbuf<long long> vdbg;
     if (debug) va.dbg = vdbg.ensure(8 * 32 * 4);
     ZI_LAUNCH(ctx, "pca_vectors", k_pca_vec, nl * D, kVecThreads, smem_vec, va);

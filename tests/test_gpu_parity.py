@@ -809,3 +809,19 @@ def test_projection_tc_edge_cases_vs_oracle(zb, case):
         lay = mi.layout(l)
         assert np.array_equal(lay["lo"], ref.lo) and np.array_equal(lay["hi"], ref.hi), (case, l)
         assert np.array_equal(c, ref.coords) and np.array_equal(k, ref.keys), (case, l)
+
+
+def test_pca_householder_path_still_green():
+    """The Lanczos fast path delivers the PCA models on every config here, so re-run the PCA and
+    build parity tests with it disabled (ZI_PCA_LZ=0): the Householder path (k_pca_tri +
+    k_pca_vec), which the fast path falls back to, stays within the same tolerances."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ZI_PCA_LZ="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k",
+                        "pca_matches or pca_rgb or build_bitexact or cfg1_end_to_end",
+                        os.path.join(root, "tests", "test_gpu_parity.py")],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
