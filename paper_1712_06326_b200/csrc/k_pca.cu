@@ -21,7 +21,7 @@
 //   k_pca_lz   (first, when ZI_PCA_LZ is not 0) the Lanczos fast path: K = max(32, 2D+8) steps
 //              with full reorthogonalisation on the same distributed rows, then k_pca_vec in
 //              Lanczos mode solves T_K and forms the Ritz vectors; a layout whose Ritz residuals
-//              are not below 1e-12 |T| (or whose Krylov space broke down early) runs the
+//              are not below 1e-10 |T| (or whose Krylov space broke down early) runs the
 //              Householder kernels above, which skip every layout the fast path delivered.
 // The host eigen-solver (host_pca.cpp) remains for m*C > 224.
 #include <cooperative_groups.h>
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pca_vec(vec_args a) {
         a.w.lam[l * 32 + j] = rq;
         if (a.lzmode) {  // Ritz residual |A y - theta y| = |beta_K s_K| (full reorthogonalisation)
             const double res = fabs(a.w.lzab[l * 2 * kLzMax + kLzMax + n - 1] * x[n - 1]);
-            if (!(res <= 1e-12 * safe)) a.w.stat[l] = 1.0;
+            if (!(res <= 1e-10 * safe)) a.w.stat[l] = 1.0;  // vector error ~ res / gap: far inside the 1e-7 budget
         }
     }
     __syncthreads();
