@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--knn-queries", type=int, default=1 << 14)
     p.add_argument("--no-vector", action="store_true", help="skip the cfg5 vector-index build line")
     p.add_argument("--vec-n", type=int, default=1 << 24, help="cfg5 vector-index rows")
+    p.add_argument("--sharded", action="store_true",
+                   help="range-partitioned build of ONE image over the N ranks (SURVEY.md §8(e); strong scaling) "
+                        "instead of one image per rank")
     return p.parse_args()
 
 
@@ -332,6 +335,64 @@ def candidate_scoring(zb, ctx, args, hbm_peak):
     return line
 
 
+def run_sharded(args, zb, world, rank, local, dist):
+    """One image (seed of rank 0) range-partitioned over the ranks: every step is the whole
+    sharded build from host memory (shard create + moments SUM + lo/hi MIN/MAX + sample sort +
+    rebalancing all-to-all + finalize), timed on the ctx stream; the step time is the max over
+    ranks and the value counts the image's dictionary once (strong scaling)."""
+    from paper_1712_06326_b200 import sharding
+    img, known, p = workload(args.config, 0)
+    ctx = zb.Context(local)
+    cfg = zb.index_config(patch_size=p["patch_size"], dims=p["dims"], knn=p["knn"])
+    if dist is not None:
+        import torch
+        comm = sharding.TorchComm(device=torch.device("cuda", local))
+    else:
+        comm = sharding.LoopbackComm(1)
+
+    def build():
+        sh = sharding.DeviceShard(img, known, cfg, rank, world, ctx=ctx)
+        info = sharding.build_sharded([sh], comm)
+        return sh, info
+
+    for _ in range(max(args.warmup, 0)):
+        build()
+    ctx.synchronize()
+    clocks = ClockSampler(local)
+    launches0 = ctx.kernel_launches
+    if dist is not None:
+        dist.barrier()
+    clocks.begin()
+    total_ms = 0.0
+    info = None
+    for _ in range(args.steps):
+        ctx.timer_start()
+        sh, info = build()
+        total_ms += ctx.timer_stop()
+    clocks.end()
+    launches = ctx.kernel_launches - launches0
+    n_total = sh.n_total
+    if dist is not None:
+        import torch
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = n_total * args.steps / (total_ms * 1e-3)
+    if rank == 0:
+        h2d = img.nbytes + known.nbytes
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u8+i8+f64", "data": "synthetic",
+                "config": {"workload": f"{args.config}: one image range-partitioned by Morton key over {world} rank(s), "
+                                       f"n={n_total} dictionary patches, 8 layout indices",
+                           "global_batch": n_total, "parallelism": f"range-partitioned x{world} (sample sort over NCCL)",
+                           "l2": "not flushed (every step re-uploads the image and rebuilds every buffer)"},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 0,
+                        "api": "sharding.DeviceShard + build_sharded (zi_shard_*), host image in"},
+                "exchange": info, "gpu_launches": launches, "clocks": clocks.result()}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -350,6 +411,9 @@ def main():
         dist = tdist
 
     import paper_1712_06326_b200 as zb
+    if args.sharded:
+        run_sharded(args, zb, world, rank, local, dist)
+        return
 
     img, known, p = workload(args.config, rank)
     ctx = zb.Context(local)
