@@ -197,11 +197,12 @@ void build_multi_index(zi_multi_index* mi) {
             quantize_interleave(ctx, mi->proj.p, mm, n, N, static_cast<uint32_t>(l), D, keyw, val);
         }
     }
-    morton_sort_layouts(ctx, keyw, val, N, D);
+    uint32_t* sorted[10];  // the sorted records, possibly in the sort's scratch (no copy back)
+    morton_sort_layouts(ctx, keyw, val, N, D, sorted);
     for (int l = 0; l < 8; ++l) {
         mi->L[l].index.ctx = ctx;
         mi->L[l].index.layout_id = static_cast<uint32_t>(l);
-        finalize_index(ctx, keyw, val, N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p, &mi->L[l].index);
+        finalize_index(ctx, sorted[0], sorted[W], N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p, &mi->L[l].index);
     }
     ZI_CUDA(cudaEventRecord(mi->ev1, ctx->stream));
     mi->build_ms_pending = true;

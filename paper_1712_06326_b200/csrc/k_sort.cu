@@ -216,8 +216,12 @@ std::vector<uint32_t> pass_histograms(zi_ctx* ctx, uint32_t* const* words, int n
     return out;
 }
 
+// result (optional): receives the buffers holding the sorted words -- the scratch copy after an
+// odd number of passes -- instead of copying them back into `words`
 void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
-                      const uint32_t* hist_host, bool device_bases) {
+                      const uint32_t* hist_host, bool device_bases, uint32_t** result) {
+    if (result)
+        for (int k = 0; k < nw; ++k) result[k] = words[k];
     if (n <= 1 || passes.empty()) return;
     if (n > kValMask) throw error(ZI_E_INVALID, "radix sort: more than 2^30 records");
     if (nw > kMaxWords) throw error(ZI_E_INVALID, "radix sort: too many words");
@@ -302,9 +306,17 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
         }
         for (int k = 0; k < nw; ++k) std::swap(cur[k], oth[k]);
     }
-    if (active.size() % 2 == 1)
+    if (result) {
+        for (int k = 0; k < nw; ++k) result[k] = cur[k];
+    } else if (active.size() % 2 == 1) {
         for (int k = 0; k < nw; ++k)
             ZI_CUDA(cudaMemcpyAsync(words[k], cur[k], n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+}
+
+void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
+                      const uint32_t* hist_host, bool device_bases) {
+    radix_sort_words(ctx, words, nw, n, passes, hist_host, device_bases, nullptr);
 }
 
 // ---------------------------------------------------------------------------- hybrid sort
@@ -674,8 +686,8 @@ static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int 
 }
 
 // window sort + oversized-segment handling after the MSD passes
-static void finish_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, int nb, bool layouts,
-                          const std::vector<int2>& all, int& learnt) {
+static void finish_hybrid(zi_ctx* ctx, uint32_t** words, uint32_t** orig, int W, uint64_t N, int D, int nb,
+                          bool layouts, const std::vector<int2>& all, int& learnt) {
     const int nw = W + 1;
     static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
     // counters | big-segment list | pass table, in the context counter buffer
@@ -709,6 +721,12 @@ static void finish_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int 
         D - (nb + 1) <= 12)
         learnt = nb + 1;
     if (nbig == 0) return;
+    if (words[0] != orig[0]) {  // the nested sorts below use the scratch buffer the records sit in
+        for (int k = 0; k < nw; ++k) {
+            ZI_CUDA(cudaMemcpyAsync(orig[k], words[k], N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+            words[k] = orig[k];
+        }
+    }
     if (nbig > kMaxBig || static_cast<uint64_t>(hc[1]) * 8 > N) {
         // top bytes too clustered for the split (smooth images): finish with the full LSD sort.
         // Equal keys are already in payload order everywhere, so the stable passes from the
@@ -759,8 +777,19 @@ static void verify_sorted(zi_ctx* ctx, uint32_t* const* words, int W, uint64_t N
 
 // Sort (key words, payload) records by (Morton key, payload); `layouts`: the payload's top 3
 // bits are a layout id that orders first.
-static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts) {
+// result (optional, see radix_sort_words): the buffers holding the sorted records
+static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts,
+                               uint32_t** result = nullptr) {
     const int nw = W + 1;
+    uint32_t* cur[kMaxWords];
+    auto done = [&] {  // hand the final buffers to the caller, or move them into `words`
+        if (result) {
+            for (int k = 0; k < nw; ++k) result[k] = cur[k];
+        } else if (cur[0] != words[0]) {
+            for (int k = 0; k < nw; ++k)
+                ZI_CUDA(cudaMemcpyAsync(words[k], cur[k], N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+    };
     std::vector<int2> all;
     for (int p = 0; p < D; ++p) all.push_back(make_int2(p >> 2, (p & 3) * 8));
     if (layouts) all.push_back(make_int2(W, 29));
@@ -772,9 +801,10 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         std::vector<int2> msd;
         for (int p = D - nb; p < D; ++p) msd.push_back(make_int2(p >> 2, (p & 3) * 8));
         if (layouts) msd.push_back(make_int2(W, 29));
-        radix_sort_words(ctx, words, nw, N, msd, nullptr, true);
-        finish_hybrid(ctx, words, W, N, D, nb, layouts, all, learnt);
-        if (verify_on()) verify_sorted(ctx, words, W, N, D, nb, layouts);
+        radix_sort_words(ctx, words, nw, N, msd, nullptr, true, cur);
+        finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, learnt);
+        if (verify_on()) verify_sorted(ctx, cur, W, N, D, nb, layouts);
+        done();
         return;
     }
     const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all);
@@ -805,7 +835,8 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
     if (nb > D - 3) {  // little left for the windows: all-LSD with the histograms already taken
         if (debug) std::fprintf(stderr, "hybrid sort N=%llu: MSD depth %d of %d -> LSD\n", static_cast<unsigned long long>(N), nb, D);
-        radix_sort_words(ctx, words, nw, N, all, hist.data(), false);
+        radix_sort_words(ctx, words, nw, N, all, hist.data(), false, cur);
+        done();
         return;
     }
     std::vector<int2> msd;
@@ -818,10 +849,11 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         msd.push_back(make_int2(W, 29));
         msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(D) * 256, hist.end());
     }
-    radix_sort_words(ctx, words, nw, N, msd, msd_hist.data(), false);
+    radix_sort_words(ctx, words, nw, N, msd, msd_hist.data(), false, cur);
     if (learnt == 0) learnt = nb;  // remembered: later builds skip the histogram round trip
-    finish_hybrid(ctx, words, W, N, D, nb, layouts, all, learnt);
-    if (verify_on()) verify_sorted(ctx, words, W, N, D, nb, layouts);
+    finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, learnt);
+    if (verify_on()) verify_sorted(ctx, cur, W, N, D, nb, layouts);
+    done();
 }
 
 void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first) {
@@ -844,12 +876,12 @@ void morton_sort_rows(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n
     morton_sort_hybrid(ctx, words, W, n, D, false);
 }
 
-void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D) {
+void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D, uint32_t** out) {
     const int W = (D + 3) / 4;
     uint32_t* words[kMaxWords];
     for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * N;
     words[W] = d_val;
-    morton_sort_hybrid(ctx, words, W, N, D, true);
+    morton_sort_hybrid(ctx, words, W, N, D, true, out);
 }
 
 }  // namespace zi

@@ -235,7 +235,10 @@ void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_k
 void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first);
 // all 8 layouts at once: N = 8n records, Morton passes then one pass on the layout bits of the
 // payload ((layout << 29) | row) -- stable, so each layout segment ends in reference order
-void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D);
+// out (optional): the buffers holding the sorted words (out[k] = out[0] + k*N, the payload at
+// out[W]) -- the sort's scratch buffer after an odd number of passes, valid until the next use
+// of the context scratch; without it the records end in d_keyw / d_val
+void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D, uint32_t** out = nullptr);
 
 // projection + quantisation of all 8 layouts on the int8 tensor cores with the exact fp64 fix-up
 // (k_proj_tc.cu): records and exact lo/hi identical to project + quantize_interleave; false when
