@@ -59,7 +59,6 @@ struct pt_params {
     uint32_t* list_count;
     uint64_t ntiles;
     const int2* wtab;  // Fpad/4 gather words (pt_gather)
-    int abl;           // dev ablation switch (ZI_PT_ABL): 1 no gather, 2 no epilogue math, 4 no MMA
 };
 
 // byte offset of (row r, K-byte f) in a K-major, 128B-swizzled operand of `rows` rows
@@ -279,10 +278,8 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
                 for (int kb = 0; kb < KB; ++kb) {
                     const uint64_t da = tc_desc_k128(a0 + kb * kPtRows * 128);
                     const uint64_t db = tc_desc_k128(b0 + kb * P.Npad * 128);
-                    if (!(P.abl & 4)) {
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) pt_mma(acc, da + 2 * ks, db + 2 * ks, idesc, (kb | ks) != 0 ? 1u : 0u);
-                    }
+                    for (int ks = 0; ks < 4; ++ks) pt_mma(acc, da + 2 * ks, db + 2 * ks, idesc, (kb | ks) != 0 ? 1u : 0u);
                 }
                 tc_commit(tc_smem(&s_aempty[buf]));
                 tc_commit(tc_smem(&s_accfull[buf]));
@@ -295,8 +292,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
             const uint32_t use = static_cast<uint32_t>(i >> 1);
             if (i >= 2) tc_mbar_wait(tc_smem(&s_aempty[buf]), (use - 1) & 1);
             const uint64_t tile = blockIdx.x + i * gridDim.x;
-            if (P.abl & 1) {
-            } else if (KT == 0) {
+            if (KT == 0) {
                 pt_gather(P, s_wtab, tile, tc_smem(sA + buf * abytes), tid, 0, nchunk);
             } else {
                 const int r = tid & 127;
@@ -353,10 +349,6 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
-                }
-                if (P.abl & 2) {
-                    if (v[0] == 0x12345678u && v[NC - 1] == 0x9abcdefu) P.list_count[1] = 1;  // keep the loads
-                    continue;
                 }
                 uint32_t kw[W];
 #pragma unroll
@@ -690,8 +682,6 @@ bool project_quantize_tc(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint
     P.list_count = reinterpret_cast<uint32_t*>(s + o_cnt);
     P.ntiles = (n + kPtRows - 1) / kPtRows;
     P.wtab = mi->pt_wtab.p;
-    static const int abl = std::getenv("ZI_PT_ABL") ? std::atoi(std::getenv("ZI_PT_ABL")) : 0;
-    P.abl = abl;
     for (int mode = 0; mode < 2; ++mode)
         for (int g = 0; g < ng; ++g) {
             P.B = s + o_B + goff[g];

@@ -1,4 +1,5 @@
 """Dev probe: cfg2 multi-index builds with wall-clock timing (and for ncu captures of build kernels)."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import time
 import paper_1712_06326_b200 as zb
 import workloads

@@ -1,4 +1,5 @@
 """dev probe: fill loop after repeated rebuilds and an e2e-style build/destroy loop (bench order)."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import time
 import paper_1712_06326_b200 as zb
 import workloads

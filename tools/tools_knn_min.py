@@ -1,4 +1,5 @@
 """dev repro: bare-index knn on the golden uniform_D4 vectors."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import numpy as np
 
 import paper_1712_06326_b200 as zb

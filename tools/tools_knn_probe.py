@@ -1,4 +1,5 @@
 """dev probe: batched k-NN on cfg5-like descriptors (used under ncu)."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import sys
 import time
 

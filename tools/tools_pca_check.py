@@ -1,4 +1,5 @@
 """Dev probe: moments exactness and PCA finiteness over the parity images, repeated builds."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import numpy as np
 import oracle
 import paper_1712_06326_b200 as zb

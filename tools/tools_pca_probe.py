@@ -1,4 +1,5 @@
 """Dev probe: phase clocks of k_pca on cfg2 (ZI_DEBUG_PCA=1) and build timing."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import os, time
 os.environ.setdefault("ZI_DEBUG_PCA", "1")
 import numpy as np

@@ -1,7 +1,7 @@
 """Dev probe: per-kernel device time of the cfg2/cfg4 builds (tensor-core projection vs fp64)."""
 import os
 import sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1712_06326_b200 as zb
 import workloads
 

@@ -1,4 +1,5 @@
 """dev probe: a few cfg2 fill-loop queries with ZI_DEBUG_QUERY output."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import numpy as np
 
 import oracle

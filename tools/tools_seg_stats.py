@@ -1,4 +1,5 @@
 """Dev probe: cfg2 MSD segment-length statistics (layout + top nb Morton bytes) per depth."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import numpy as np
 import paper_1712_06326_b200 as zb
 import workloads

@@ -1,4 +1,5 @@
 """Dev probe: repeat small builds and compare the tensor-core moments with the oracle each time."""
+import os as _os, sys as _sys; _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import sys
 import numpy as np
 sys.path.insert(0, "tests")
