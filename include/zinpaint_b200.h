@@ -244,7 +244,8 @@ zi_status zi_refine_best(zi_multi_index* mi, const uint8_t* target_values, const
  * torch.distributed); d_* are DEVICE pointers (the send buffers are owned by the shard, valid
  * until the next stage; the receive buffers are the caller's).  Stages, in order:
  *   create -> moments (all-reduce SUM of F+F*F int64) -> fit_project (all-reduce MIN lo, MAX hi:
- *   8*dims order-preserving int64 each) -> quantize_sort (all-gather 8*S sample rows of words+1
+ *   8*dims order-preserving int64 each) -> refine_ranges (all-reduce MIN / MAX again) ->
+ *   quantize_sort (all-gather 8*S sample rows of words+1
  *   u32) -> zi_shard_splitters -> partition (all-gather counts [G][8]; all-to-all records,
  *   words+1 u32 each) -> receive (all-gather counts2; all-to-all) -> finish.
  * After finish, zi_shard_multi_index() is a multi_index whose 8 indices and dictionary are this
@@ -258,6 +259,10 @@ zi_status zi_shard_destroy(zi_shard* sh);
 zi_status zi_shard_info(const zi_shard* sh, uint64_t* info);
 zi_status zi_shard_moments(zi_shard* sh, int64_t* moments_out);
 zi_status zi_shard_fit_project(zi_shard* sh, const int64_t* moments, int64_t* lo_out, int64_t* hi_out);
+/* the global ranges of fit_project (approximate on the tensor-core path) -> this rank's exact
+ * partial lo / hi (all-reduce MIN / MAX again before quantize_sort) */
+zi_status zi_shard_refine_ranges(zi_shard* sh, const int64_t* lo, const int64_t* hi, int64_t* lo_out,
+                                 int64_t* hi_out);
 zi_status zi_shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uint32_t samples_per_layout,
                                  uint32_t* samples_out);
 /* host only: G-1 splitters per layout from all ranks' samples (count rows) */

@@ -115,6 +115,7 @@ SIGNATURES = {
     "zi_shard_info": (C.c_int, [vp, u64p]),
     "zi_shard_moments": (C.c_int, [vp, i64p]),
     "zi_shard_fit_project": (C.c_int, [vp, i64p, i64p, i64p]),
+    "zi_shard_refine_ranges": (C.c_int, [vp, i64p, i64p, i64p, i64p]),
     "zi_shard_quantize_sort": (C.c_int, [vp, i64p, i64p, C.c_uint32, u32p]),
     "zi_shard_splitters": (C.c_int, [u32p, C.c_uint64, C.c_int32, C.c_int32, u32p]),
     "zi_shard_partition": (C.c_int, [vp, u32p, u64p, C.POINTER(vp)]),

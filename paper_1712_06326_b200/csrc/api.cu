@@ -777,6 +777,13 @@ zi_status zi_shard_fit_project(zi_shard* sh, const int64_t* moments, int64_t* lo
     });
 }
 
+zi_status zi_shard_refine_ranges(zi_shard* sh, const int64_t* lo, const int64_t* hi, int64_t* lo_out, int64_t* hi_out) {
+    return guard(sh ? zi::shard_multi_index(sh)->ctx : nullptr, [&] {
+        require(sh && lo && hi && lo_out && hi_out, "null argument");
+        zi::shard_refine_ranges(sh, lo, hi, lo_out, hi_out);
+    });
+}
+
 zi_status zi_shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uint32_t S, uint32_t* samples) {
     return guard(sh ? zi::shard_multi_index(sh)->ctx : nullptr, [&] {
         require(sh && lo && hi && (samples || S == 0), "null argument");

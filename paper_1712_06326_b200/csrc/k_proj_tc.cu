@@ -592,25 +592,106 @@ static void launch_pt(zi_ctx* ctx, const pt_params& P, int mode, size_t smem) {
     launch_pt_kt<D, 0>(ctx, P, mode, smem);
 }
 
-bool project_quantize_tc(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec) {
-    zi_ctx* ctx = mi->ctx;
+// The plan of one projection: eligibility, layout groups, scratch offsets, kernel parameters.
+struct pt_plan {
+    bool ok = false;
+    uint8_t* s = nullptr;  // the scratch the offsets below point into
+    int D = 0, ng = 0, nlmax = 0, goff[8] = {}, gnpad[8] = {};
+    size_t smem = 0, btot = 0, o_B = 0, o_M = 0, o_amm = 0, o_cnt = 0, o_list = 0;
+    pt_params P{};
+};
+
+// eligibility depends on the configuration only (dims, patch shape, the dictionary size), never on
+// this rank's slice, so every shard of a sharded build takes the same path
+static pt_plan pt_make_plan(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec) {
+    pt_plan pl;
     static const bool off_env = std::getenv("ZI_PROJ_FP64") != nullptr;
-    const int D = mi->dims, K = mi->K, C = mi->C, m = mi->m, mc = mi->mc;
+    const int D = mi->dims, K = mi->K, C = mi->C, mc = mi->mc;
     const int F = K * K * C, Fpad = (F + 127) / 128 * 128;
-    const uint64_t n = mi->n;
-    if (off_env || D < 1 || D > 16 || Fpad > kPtMaxFpad || mc > 232 || n == 0 || n >= (1ull << 27)) return false;
-    const int nlmax = std::min(8, kPtMaxN / (kPtDigits * D));
-    const int ng = (8 + nlmax - 1) / nlmax;
-    int goff[8], gnpad[8];
-    size_t btot = 0;
-    for (int g = 0; g < ng; ++g) {
-        const int nl = std::min(nlmax, 8 - g * nlmax);
-        gnpad[g] = (nl * kPtDigits * D + 15) / 16 * 16;
-        goff[g] = static_cast<int>(btot);
-        btot += static_cast<size_t>(gnpad[g]) * Fpad;
+    const uint64_t n = mi->n, ntot = mi->shard ? mi->n_total : mi->n;
+    if (off_env || D < 1 || D > 16 || Fpad > kPtMaxFpad || mc > 232 || ntot == 0 || ntot >= (1ull << 27)) return pl;
+    pl.D = D;
+    pl.nlmax = std::min(8, kPtMaxN / (kPtDigits * D));
+    pl.ng = (8 + pl.nlmax - 1) / pl.nlmax;
+    for (int g = 0; g < pl.ng; ++g) {
+        const int nl = std::min(pl.nlmax, 8 - g * pl.nlmax);
+        pl.gnpad[g] = (nl * kPtDigits * D + 15) / 16 * 16;
+        pl.goff[g] = static_cast<int>(pl.btot);
+        pl.btot += static_cast<size_t>(pl.gnpad[g]) * Fpad;
     }
-    const size_t smem = 2 * static_cast<size_t>(kPtRows) * Fpad + static_cast<size_t>(kPtMaxN) * Fpad + 1024;
-    if (smem > 200 * 1024) return false;
+    pl.smem = 2 * static_cast<size_t>(kPtRows) * Fpad + static_cast<size_t>(kPtMaxN) * Fpad + 1024;
+    if (pl.smem > 200 * 1024) return pl;
+    // scratch: [goff/gnpad ints][B bytes][M doubles][amm][count][list]
+    pl.o_B = 256;
+    pl.o_M = (pl.o_B + pl.btot + 255) & ~size_t(255);
+    pl.o_amm = pl.o_M + 8 * 16 * sizeof(double);
+    pl.o_cnt = pl.o_amm + 8 * 2 * 16 * sizeof(unsigned long long);
+    pl.o_list = pl.o_cnt + 256;
+    uint8_t* s = mi->pt_scratch.ensure(pl.o_list + 8 * (n ? n : 1) * sizeof(uint32_t));
+    pl.s = s;
+    pt_params& P = pl.P;
+    P.img = mi->image.p;
+    P.w = mi->w;
+    P.C = C;
+    P.KC = K * C;
+    P.F = F;
+    P.Fpad = Fpad;
+    P.keys = mi->dict.p + mi->row_begin;
+    P.n = n;
+    P.row_base = static_cast<uint32_t>(mi->row_begin);
+    P.M = reinterpret_cast<const double*>(s + pl.o_M);
+    P.amm = reinterpret_cast<unsigned long long*>(s + pl.o_amm);
+    P.E = 255.0 * mc * (0x1p-39 + 0x1p-44);
+    P.keyw = keyw;
+    P.val = val;
+    P.Nrec = Nrec;
+    P.list = reinterpret_cast<uint32_t*>(s + pl.o_list);
+    P.list_count = reinterpret_cast<uint32_t*>(s + pl.o_cnt);
+    P.ntiles = (n + kPtRows - 1) / kPtRows;
+    P.wtab = mi->pt_wtab.p;
+    pl.ok = true;
+    return pl;
+}
+
+static void pt_launch_pass(zi_ctx* ctx, pt_plan& pl, int mode) {
+    if (pl.P.n == 0) return;
+    for (int g = 0; g < pl.ng; ++g) {
+        pt_params P = pl.P;
+        P.B = pl.s + pl.o_B + pl.goff[g];
+        P.Npad = pl.gnpad[g];
+        P.l0 = g * pl.nlmax;
+        P.nl = std::min(pl.nlmax, 8 - g * pl.nlmax);
+        switch (pl.D) {
+#define ZI_PT_CASE(DD) \
+    case DD: launch_pt<DD>(ctx, P, mode, pl.smem); break;
+            ZI_PT_CASE(1) ZI_PT_CASE(2) ZI_PT_CASE(3) ZI_PT_CASE(4) ZI_PT_CASE(5) ZI_PT_CASE(6) ZI_PT_CASE(7)
+            ZI_PT_CASE(8) ZI_PT_CASE(9) ZI_PT_CASE(10) ZI_PT_CASE(11) ZI_PT_CASE(12) ZI_PT_CASE(13)
+            ZI_PT_CASE(14) ZI_PT_CASE(15) ZI_PT_CASE(16)
+#undef ZI_PT_CASE
+            default: throw error(ZI_E_INVALID, "projection: dims above 16");
+        }
+    }
+}
+
+static void pt_launch_exact(zi_ctx* ctx, zi_multi_index* mi, pt_plan& pl, int mode) {
+    if (pl.P.n == 0) return;
+    switch (pl.D) {
+#define ZI_PTX_CASE(DD) \
+    case DD: launch_pt_exact<DD>(ctx, mi, pl.P, mode); break;
+        ZI_PTX_CASE(1) ZI_PTX_CASE(2) ZI_PTX_CASE(3) ZI_PTX_CASE(4) ZI_PTX_CASE(5) ZI_PTX_CASE(6) ZI_PTX_CASE(7)
+        ZI_PTX_CASE(8) ZI_PTX_CASE(9) ZI_PTX_CASE(10) ZI_PTX_CASE(11) ZI_PTX_CASE(12) ZI_PTX_CASE(13)
+        ZI_PTX_CASE(14) ZI_PTX_CASE(15) ZI_PTX_CASE(16)
+#undef ZI_PTX_CASE
+        default: break;
+    }
+}
+
+// phase A: digit matrices, gather table, identity ranges, the min / max pass -> approximate
+// ranges (ordered u64) in the plan's scratch
+static void pt_phase_a(zi_multi_index* mi, pt_plan& pl) {
+    zi_ctx* ctx = mi->ctx;
+    const int D = pl.D, K = mi->K, C = mi->C, m = mi->m, mc = mi->mc;
+    const int F = K * K * C, Fpad = pl.P.Fpad;
     if (!mi->pca_cols_ready) {
         std::vector<int32_t> hc;
         for (int l = 0; l < 8; ++l)
@@ -621,17 +702,13 @@ bool project_quantize_tc(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));
         mi->pca_cols_ready = true;
     }
-    // scratch: [goff/gnpad ints][B bytes][M doubles][amm][count][list]
-    const size_t o_int = 0, o_B = 256, o_M = (o_B + btot + 255) & ~size_t(255);
-    const size_t o_amm = o_M + 8 * 16 * sizeof(double), o_cnt = o_amm + 8 * 2 * 16 * sizeof(unsigned long long);
-    const size_t o_list = o_cnt + 256;
-    uint8_t* s = mi->pt_scratch.ensure(o_list + 8 * n * sizeof(uint32_t));
+    uint8_t* s = pl.s;
     int hint[16];
     for (int g = 0; g < 8; ++g) {
-        hint[g] = g < ng ? goff[g] : 0;
-        hint[8 + g] = g < ng ? gnpad[g] : 0;
+        hint[g] = g < pl.ng ? pl.goff[g] : 0;
+        hint[8 + g] = g < pl.ng ? pl.gnpad[g] : 0;
     }
-    ZI_CUDA(cudaMemcpyAsync(s + o_int, hint, sizeof(hint), cudaMemcpyHostToDevice, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(s, hint, sizeof(hint), cudaMemcpyHostToDevice, ctx->stream));
     {  // gather word table: patch-relative byte offsets of every 4-byte word of the row
         const int KC = K * C, wC = mi->w * C;
         std::vector<int2> tab(Fpad / 4);
@@ -648,74 +725,76 @@ bool project_quantize_tc(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint
         }
         mi->pt_wtab.ensure(tab.size());
         ZI_CUDA(cudaMemcpyAsync(mi->pt_wtab.p, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
+        pl.P.wtab = mi->pt_wtab.p;
     }
-    ZI_CUDA(cudaMemsetAsync(s + o_B, 0, btot, ctx->stream));
-    ZI_CUDA(cudaMemsetAsync(s + o_cnt, 0, sizeof(uint32_t), ctx->stream));
-    unsigned long long* amm = reinterpret_cast<unsigned long long*>(s + o_amm);
+    ZI_CUDA(cudaMemsetAsync(s + pl.o_B, 0, pl.btot, ctx->stream));
+    ZI_CUDA(cudaMemsetAsync(s + pl.o_cnt, 0, sizeof(uint32_t), ctx->stream));
+    unsigned long long* amm = pl.P.amm;
     for (int l = 0; l < 8; ++l) {
         ZI_CUDA(cudaMemsetAsync(amm + static_cast<size_t>(l) * 2 * D, 0xff, D * sizeof(unsigned long long), ctx->stream));
         ZI_CUDA(cudaMemsetAsync(amm + static_cast<size_t>(l) * 2 * D + D, 0, D * sizeof(unsigned long long), ctx->stream));
         ZI_CUDA(cudaMemsetAsync(mi->minmax.p + static_cast<size_t>(l) * 2 * D, 0xff, D * sizeof(unsigned long long), ctx->stream));
         ZI_CUDA(cudaMemsetAsync(mi->minmax.p + static_cast<size_t>(l) * 2 * D + D, 0, D * sizeof(unsigned long long), ctx->stream));
     }
-    const int* dgoff = reinterpret_cast<const int*>(s + o_int);
+    const int* dgoff = reinterpret_cast<const int*>(s);
     const int total = 8 * mc * D;
     ZI_LAUNCH(ctx, "project_tc_prep", k_pt_prep, (total + 255) / 256, 256, 0, mi->pca_mean.p, mi->pca_comp.p,
-              mi->pca_cols.p, mc, D, nlmax, Fpad, dgoff, dgoff + 8, s + o_B, reinterpret_cast<double*>(s + o_M));
-    pt_params P{};
-    P.img = mi->image.p;
-    P.w = mi->w;
-    P.C = C;
-    P.KC = K * C;
-    P.F = F;
-    P.Fpad = Fpad;
-    P.keys = mi->dict.p + mi->row_begin;
-    P.n = n;
-    P.row_base = static_cast<uint32_t>(mi->row_begin);
-    P.M = reinterpret_cast<const double*>(s + o_M);
-    P.amm = amm;
-    P.E = 255.0 * mc * (0x1p-39 + 0x1p-44);
-    P.keyw = keyw;
-    P.val = val;
-    P.Nrec = Nrec;
-    P.list = reinterpret_cast<uint32_t*>(s + o_list);
-    P.list_count = reinterpret_cast<uint32_t*>(s + o_cnt);
-    P.ntiles = (n + kPtRows - 1) / kPtRows;
-    P.wtab = mi->pt_wtab.p;
-    for (int mode = 0; mode < 2; ++mode)
-        for (int g = 0; g < ng; ++g) {
-            P.B = s + o_B + goff[g];
-            P.Npad = gnpad[g];
-            P.l0 = g * nlmax;
-            P.nl = std::min(nlmax, 8 - g * nlmax);
-            switch (D) {
-#define ZI_PT_CASE(DD) \
-    case DD: launch_pt<DD>(ctx, P, mode, smem); break;
-                ZI_PT_CASE(1) ZI_PT_CASE(2) ZI_PT_CASE(3) ZI_PT_CASE(4) ZI_PT_CASE(5) ZI_PT_CASE(6) ZI_PT_CASE(7)
-                ZI_PT_CASE(8) ZI_PT_CASE(9) ZI_PT_CASE(10) ZI_PT_CASE(11) ZI_PT_CASE(12) ZI_PT_CASE(13)
-                ZI_PT_CASE(14) ZI_PT_CASE(15) ZI_PT_CASE(16)
-#undef ZI_PT_CASE
-                default: return false;
-            }
-        }
+              mi->pca_cols.p, mc, D, pl.nlmax, Fpad, dgoff, dgoff + 8, s + pl.o_B, reinterpret_cast<double*>(s + pl.o_M));
+    pt_launch_pass(ctx, pl, 0);
+}
+
+// phase B: the quantise pass with the (global) approximate ranges, then the exact lo / hi over the
+// listed candidates into mi->minmax
+static void pt_phase_b(zi_multi_index* mi, pt_plan& pl) {
+    pt_launch_pass(mi->ctx, pl, 1);
     static const bool debug = std::getenv("ZI_DEBUG_PT") != nullptr;
     if (debug) {
         uint32_t cnt = 0;
-        ZI_CUDA(cudaMemcpyAsync(&cnt, P.list_count, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
-        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        ZI_CUDA(cudaMemcpyAsync(&cnt, pl.P.list_count, sizeof(cnt), cudaMemcpyDeviceToHost, mi->ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(mi->ctx->stream));
         std::fprintf(stderr, "project_tc: n=%llu D=%d groups=%d fix-up list %u (%.4f%% of patch x layout pairs)\n",
-                     static_cast<unsigned long long>(n), D, ng, cnt, 100.0 * cnt / (8.0 * n));
+                     static_cast<unsigned long long>(pl.P.n), pl.D, pl.ng, cnt, 100.0 * cnt / (8.0 * std::max<uint64_t>(pl.P.n, 1)));
     }
-    for (int mode = 0; mode < 2; ++mode) switch (D) {
-#define ZI_PTX_CASE(DD) \
-    case DD: launch_pt_exact<DD>(ctx, mi, P, mode); break;
-            ZI_PTX_CASE(1) ZI_PTX_CASE(2) ZI_PTX_CASE(3) ZI_PTX_CASE(4) ZI_PTX_CASE(5) ZI_PTX_CASE(6) ZI_PTX_CASE(7)
-            ZI_PTX_CASE(8) ZI_PTX_CASE(9) ZI_PTX_CASE(10) ZI_PTX_CASE(11) ZI_PTX_CASE(12) ZI_PTX_CASE(13)
-            ZI_PTX_CASE(14) ZI_PTX_CASE(15) ZI_PTX_CASE(16)
-#undef ZI_PTX_CASE
-            default: break;
-        }
+    pt_launch_exact(mi->ctx, mi, pl, 0);
+}
+
+// phase C: the exact records of the listed pairs with the (global) exact lo / hi
+static void pt_phase_c(zi_multi_index* mi, pt_plan& pl) { pt_launch_exact(mi->ctx, mi, pl, 1); }
+
+bool project_quantize_tc(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec) {
+    pt_plan pl = pt_make_plan(mi, keyw, val, Nrec);
+    if (!pl.ok) return false;
+    pt_phase_a(mi, pl);
+    pt_phase_b(mi, pl);
+    pt_phase_c(mi, pl);
     return true;
+}
+
+// sharded build (shard.cu): the same three phases with all-reduces between them
+bool shard_tc_begin(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec, unsigned long long* amm_out) {
+    pt_plan pl = pt_make_plan(mi, keyw, val, Nrec);
+    if (!pl.ok) return false;
+    pt_phase_a(mi, pl);
+    ZI_CUDA(cudaMemcpyAsync(amm_out, pl.P.amm, static_cast<size_t>(8) * 2 * pl.D * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, mi->ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(mi->ctx->stream));
+    return true;
+}
+
+void shard_tc_quantize(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec, const unsigned long long* amm,
+                       unsigned long long* exact_out) {
+    pt_plan pl = pt_make_plan(mi, keyw, val, Nrec);
+    ZI_CUDA(cudaMemcpyAsync(pl.P.amm, amm, static_cast<size_t>(8) * 2 * pl.D * sizeof(unsigned long long),
+                            cudaMemcpyHostToDevice, mi->ctx->stream));
+    pt_phase_b(mi, pl);
+    ZI_CUDA(cudaMemcpyAsync(exact_out, mi->minmax.p, static_cast<size_t>(8) * 2 * pl.D * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, mi->ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(mi->ctx->stream));
+}
+
+void shard_tc_fixup(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec) {
+    pt_plan pl = pt_make_plan(mi, keyw, val, Nrec);
+    pt_phase_c(mi, pl);
 }
 
 }  // namespace zi

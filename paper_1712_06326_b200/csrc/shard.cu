@@ -9,9 +9,15 @@
 //   moments      exact int64 partial Gram of the rank's rows            -> all-reduce SUM
 //                (integer sums: the total is bit-identical for any G)
 //   fit_project  8 PCA models from the global moments (identical on every rank, same device
-//                code as the single-GPU build), fp64 projections of the rank's rows, partial
-//                quantiser ranges as order-preserving int64               -> all-reduce MIN / MAX
-//   quantize     global lo/hi -> Morton records of the rank's rows (payload = global row),
+//                code as the single-GPU build) and the min / max pass of the tensor-core
+//                projection (k_proj_tc.cu) over the rank's rows: partial approximate ranges as
+//                order-preserving int64                                  -> all-reduce MIN / MAX
+//   refine       the quantise pass with the global approximate ranges (records of every pair
+//                the bracket decides; candidates and ambiguous pairs listed), exact lo / hi over
+//                the rank's candidates                                   -> all-reduce MIN / MAX
+//                (configurations outside the tensor-core envelope project in fp64 at
+//                fit_project, return exact ranges there and pass them through here)
+//   quantize     global exact lo/hi -> the listed pairs' exact records (payload = global row),
 //                local hybrid sort, regular samples                      -> all-gather samples
 //   partition    splitters (zi_shard_splitters) -> lower bounds in the local sorted layouts,
 //                send buffer packed destination-major                    -> all-gather counts,
@@ -43,6 +49,8 @@ struct zi_shard {
     zi::dbuf<uint64_t> pos;         // lower bounds of the splitters
     zi::dbuf<uint32_t> small;       // splitters / samples / segment tables
     uint64_t held = 0;              // records held after the first exchange
+    bool tc = false;                // projection on the int8 tensor cores (k_proj_tc.cu)
+    bool refined = false;           // refine_ranges ran after fit_project
 };
 
 namespace zi {
@@ -214,34 +222,68 @@ void shard_fit_project(zi_shard* sh, const int64_t* moments, int64_t* lo_out, in
     ZI_CUDA(cudaMemcpyAsync(mi->moments.p, moments, nmom * sizeof(unsigned long long), cudaMemcpyHostToDevice,
                             ctx->stream));
     fit_models(mi, sh->n_total);
-    const uint64_t n = mi->n;
+    const uint64_t n = mi->n, N = 8 * n;
+    const int W = sh->W;
     mi->minmax.ensure(static_cast<size_t>(8) * 2 * D);
-    // empty slices keep the identity ranges (lo = +max, hi = -max in the ordered encoding)
-    for (int l = 0; l < 8; ++l) {
-        ZI_CUDA(cudaMemsetAsync(mi->minmax.p + static_cast<size_t>(l) * 2 * D, 0xff, D * sizeof(unsigned long long), ctx->stream));
-        ZI_CUDA(cudaMemsetAsync(mi->minmax.p + static_cast<size_t>(l) * 2 * D + D, 0, D * sizeof(unsigned long long), ctx->stream));
-    }
-    sh->Y.ensure(static_cast<size_t>(8) * D * (n ? n : 1));
-    for (int l = 0; l < 8; ++l)
-        project(ctx, mi->image.p, mi->w, mi->C, mi->dict.p + sh->row_b, n, mi->layout_off.p + static_cast<size_t>(l) * m, m,
-                mi->pca_mean.p + static_cast<size_t>(l) * mc, mi->pca_comp.p + static_cast<size_t>(l) * mc * D, D,
-                sh->Y.p + static_cast<size_t>(l) * D * n, mi->minmax.p + static_cast<size_t>(l) * 2 * D);
     std::vector<unsigned long long> hmm(static_cast<size_t>(8) * 2 * D);
-    ZI_CUDA(cudaMemcpyAsync(hmm.data(), mi->minmax.p, hmm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    // tensor-core path: the records are written by the quantise pass (phase B), so they exist now
+    mi->recs.ensure(static_cast<size_t>(W + 1) * (N ? N : 1));
+    sh->tc = shard_tc_begin(mi, mi->recs.p, mi->recs.p + static_cast<size_t>(W) * N, N, hmm.data());
+    if (!sh->tc) {
+        // empty slices keep the identity ranges (lo = +max, hi = -max in the ordered encoding)
+        for (int l = 0; l < 8; ++l) {
+            ZI_CUDA(cudaMemsetAsync(mi->minmax.p + static_cast<size_t>(l) * 2 * D, 0xff, D * sizeof(unsigned long long), ctx->stream));
+            ZI_CUDA(cudaMemsetAsync(mi->minmax.p + static_cast<size_t>(l) * 2 * D + D, 0, D * sizeof(unsigned long long), ctx->stream));
+        }
+        sh->Y.ensure(static_cast<size_t>(8) * D * (n ? n : 1));
+        for (int l = 0; l < 8; ++l)
+            project(ctx, mi->image.p, mi->w, mi->C, mi->dict.p + sh->row_b, n, mi->layout_off.p + static_cast<size_t>(l) * m, m,
+                    mi->pca_mean.p + static_cast<size_t>(l) * mc, mi->pca_comp.p + static_cast<size_t>(l) * mc * D, D,
+                    sh->Y.p + static_cast<size_t>(l) * D * n, mi->minmax.p + static_cast<size_t>(l) * 2 * D);
+        ZI_CUDA(cudaMemcpyAsync(hmm.data(), mi->minmax.p, hmm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     for (int l = 0; l < 8; ++l)
         for (int d = 0; d < D; ++d) {
             lo_out[l * D + d] = ordered_to_i64(hmm[static_cast<size_t>(l) * 2 * D + d]);
             hi_out[l * D + d] = ordered_to_i64(hmm[static_cast<size_t>(l) * 2 * D + D + d]);
         }
+    sh->refined = false;
     mi->host_model = false;
     mi->host_lohi = false;
     sh->stage = 2;
 }
 
+void shard_refine_ranges(zi_shard* sh, const int64_t* lo, const int64_t* hi, int64_t* lo_out, int64_t* hi_out) {
+    if (sh->stage != 2 || sh->refined) throw error(ZI_E_INVALID, "shard: refine_ranges out of order");
+    const int D = sh->D;
+    if (!sh->tc) {  // the fp64 path's ranges are exact already
+        std::copy(lo, lo + 8 * D, lo_out);
+        std::copy(hi, hi + 8 * D, hi_out);
+        sh->refined = true;
+        return;
+    }
+    zi_multi_index* mi = sh->mi;
+    const int W = sh->W;
+    const uint64_t N = 8 * mi->n;
+    std::vector<unsigned long long> amm(static_cast<size_t>(8) * 2 * D), ex(static_cast<size_t>(8) * 2 * D);
+    for (int l = 0; l < 8; ++l)
+        for (int d = 0; d < D; ++d) {
+            amm[static_cast<size_t>(l) * 2 * D + d] = i64_to_ordered(lo[l * D + d]);
+            amm[static_cast<size_t>(l) * 2 * D + D + d] = i64_to_ordered(hi[l * D + d]);
+        }
+    shard_tc_quantize(mi, mi->recs.p, mi->recs.p + static_cast<size_t>(W) * N, N, amm.data(), ex.data());
+    for (int l = 0; l < 8; ++l)
+        for (int d = 0; d < D; ++d) {
+            lo_out[l * D + d] = ordered_to_i64(ex[static_cast<size_t>(l) * 2 * D + d]);
+            hi_out[l * D + d] = ordered_to_i64(ex[static_cast<size_t>(l) * 2 * D + D + d]);
+        }
+    sh->refined = true;
+}
+
 void shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uint32_t S, uint32_t* samples_out) {
-    if (sh->stage != 2) throw error(ZI_E_INVALID, "shard: quantize before fit_project");
+    if (sh->stage != 2 || !sh->refined) throw error(ZI_E_INVALID, "shard: quantize before fit_project / refine_ranges");
     zi_multi_index* mi = sh->mi;
     zi_ctx* ctx = mi->ctx;
     const int D = sh->D, W = sh->W;
@@ -257,9 +299,13 @@ void shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uin
     mi->recs.ensure(static_cast<size_t>(W + 1) * (N ? N : 1));
     uint32_t* keyw = mi->recs.p;
     uint32_t* val = mi->recs.p + static_cast<size_t>(W) * N;
-    for (int l = 0; l < 8; ++l)
-        quantize_interleave(ctx, sh->Y.p + static_cast<size_t>(l) * D * n, mi->minmax.p + static_cast<size_t>(l) * 2 * D, n,
-                            N, static_cast<uint32_t>(l), D, keyw, val, static_cast<uint32_t>(sh->row_b));
+    if (sh->tc) {
+        shard_tc_fixup(mi, keyw, val, N);  // the exact records of the listed pairs
+    } else {
+        for (int l = 0; l < 8; ++l)
+            quantize_interleave(ctx, sh->Y.p + static_cast<size_t>(l) * D * n, mi->minmax.p + static_cast<size_t>(l) * 2 * D,
+                                n, N, static_cast<uint32_t>(l), D, keyw, val, static_cast<uint32_t>(sh->row_b));
+    }
     if (N) morton_sort_layouts(ctx, keyw, val, N, D);
     if (S) {
         uint32_t* d = sh->small.ensure(static_cast<size_t>(8) * S * (W + 1));
@@ -374,7 +420,8 @@ void shard_receive(zi_shard* sh, const uint32_t* d_recv, const uint64_t* all_cou
     mi->recs.ensure(static_cast<size_t>(W + 1) * (N1 ? N1 : 1));
     if (N1) {
         move_segments(sh, d_recv, 0, mi->recs.p, N1, {{0ull, 0ull, N1}}, N1);  // AoS -> SoA
-        morton_sort_layouts(ctx, mi->recs.p, mi->recs.p + static_cast<size_t>(W) * N1, N1, sh->D);
+        // one rank receives its own locally sorted records back in order: nothing to merge
+        if (G > 1) morton_sort_layouts(ctx, mi->recs.p, mi->recs.p + static_cast<size_t>(W) * N1, N1, sh->D);
     }
     std::vector<uint64_t> starts(static_cast<size_t>(G) * 8);
     shard_rebalance_plan(all_counts, G, sh->n_total, me, counts2_out, starts.data());

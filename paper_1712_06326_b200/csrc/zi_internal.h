@@ -244,6 +244,14 @@ void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_
 // (k_proj_tc.cu): records and exact lo/hi identical to project + quantize_interleave; false when
 // the configuration is outside its envelope (dims > 16, K*K*C > 384, ZI_PROJ_FP64 set)
 bool project_quantize_tc(zi_multi_index* mi, uint32_t* d_keyw, uint32_t* d_val, uint64_t N);
+// the same three phases for a shard, all-reduces in between: begin -> approximate ranges (ordered
+// u64, 8 x 2 x dims; false: not eligible, use the fp64 path); quantize(global approximate
+// ranges) -> exact lo / hi over the local candidates; fixup (with the global exact lo / hi in
+// mi->minmax)
+bool shard_tc_begin(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec, unsigned long long* amm_out);
+void shard_tc_quantize(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec, const unsigned long long* amm,
+                       unsigned long long* exact_out);
+void shard_tc_fixup(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec);
 
 // sorted key words + payload -> index planes, keys, bbox
 void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t off,
@@ -280,6 +288,7 @@ void shard_ranges(uint64_t n, int world, int r, uint64_t* b, uint64_t* e);
 zi_shard* shard_create(zi_multi_index* mi, int rank, int world);
 void shard_moments(zi_shard* sh, int64_t* out);
 void shard_fit_project(zi_shard* sh, const int64_t* moments, int64_t* lo_out, int64_t* hi_out);
+void shard_refine_ranges(zi_shard* sh, const int64_t* lo, const int64_t* hi, int64_t* lo_out, int64_t* hi_out);
 void shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uint32_t S, uint32_t* samples_out);
 void shard_splitters(const uint32_t* samples, uint64_t count, int W, int world, uint32_t* out);
 void shard_partition(zi_shard* sh, const uint32_t* splitters, uint64_t* counts_out, const uint32_t** d_send);

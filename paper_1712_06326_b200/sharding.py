@@ -7,7 +7,9 @@ The hot path shards naturally:
                the reference's global windows.  The stages run on the device (zi_shard_*, C ABI;
                shard.cu); between them this module runs the collectives:
                  moments       all-reduce SUM  (exact int64: bit-identical for any G)
-                 lo / hi       all-reduce MIN / MAX (order-preserving int64 of the fp64 ranges)
+                 lo / hi       all-reduce MIN / MAX (order-preserving int64 of the fp64 ranges):
+                               approximate ranges of the tensor-core projection's min / max
+                               pass, then the exact ranges over every rank's candidates
                  samples       all-gather, splitters on the host (zi_shard_splitters)
                  records       all-to-all (sample sort), then an all-to-all that rebalances the
                                received Morton ranges to the exact shard ranges
@@ -256,6 +258,15 @@ class DeviceShard:
         check(lib().zi_shard_fit_project(self.h, ptr(m, i64p), ptr(lo, i64p), ptr(hi, i64p)))
         return lo, hi
 
+    def refine_ranges(self, lo, hi):
+        """Global (approximate, on the tensor-core path) ranges -> this rank's exact partial ranges."""
+        lo = np.ascontiguousarray(lo, dtype=np.int64)
+        hi = np.ascontiguousarray(hi, dtype=np.int64)
+        lo2 = np.zeros_like(lo)
+        hi2 = np.zeros_like(hi)
+        check(lib().zi_shard_refine_ranges(self.h, ptr(lo, i64p), ptr(hi, i64p), ptr(lo2, i64p), ptr(hi2, i64p)))
+        return lo2, hi2
+
     def quantize_sort(self, lo, hi, samples: int) -> np.ndarray:
         lo = np.ascontiguousarray(lo, dtype=np.int64)
         hi = np.ascontiguousarray(hi, dtype=np.int64)
@@ -345,6 +356,9 @@ def build_sharded(shards: list, comm: Comm, samples: int = 256) -> dict:
     world = comm.world
     mom = comm.allreduce([sh.moments() for sh in shards], "sum")
     lohi = [sh.fit_project(m) for sh, m in zip(shards, mom)]
+    lo = comm.allreduce([x[0] for x in lohi], "min")
+    hi = comm.allreduce([x[1] for x in lohi], "max")
+    lohi = [sh.refine_ranges(a, b) for sh, a, b in zip(shards, lo, hi)]  # exact ranges (tensor-core path)
     lo = comm.allreduce([x[0] for x in lohi], "min")
     hi = comm.allreduce([x[1] for x in lohi], "max")
     samp = [sh.quantize_sort(a, b, samples if world > 1 else 0) for sh, a, b in zip(shards, lo, hi)]
