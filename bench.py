@@ -429,7 +429,20 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    # -------- one profiled build outside the timed region: every kernel's launches and device time
+    # (the breakdown and the step's algorithmic bytes); timing all ~40 launches costs ~8 % of the
+    # step in event records, so the timed region below times only the step's largest kernels
+    ctx.flush_l2()
+    ctx.set_profile_filter(None)
+    ctx.set_profiling(True)
+    mi.rebuild()
+    ctx.synchronize()
+    prof_all = ctx.profile()
+    ctx.set_profiling(False)
+    timed_kernels = [k for k, _ in sorted(prof_all.items(), key=lambda kv: -kv[1][0])[:4]]
+
     # -------- timed region: K builds from the HBM-resident image
+    ctx.set_profile_filter(timed_kernels)
     ctx.set_profiling(True)
     launches0 = ctx.kernel_launches
     barrier()
@@ -449,6 +462,7 @@ def main():
     launches = ctx.kernel_launches - launches0
     prof = ctx.profile()
     ctx.set_profiling(False)
+    ctx.set_profile_filter(None)
     total_ms = sum(step_ms)
     n_total = n
     if dist is not None:
@@ -478,8 +492,8 @@ def main():
             traffic_db = json.load(f)
     except OSError:
         pass
-    breakdown = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
-                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    breakdown = {k: {"ms_per_step": v[0], "launches_per_step": v[1]}
+                 for k, v in sorted(prof_all.items(), key=lambda kv: -kv[1][0])}
     # roofline of the dominant tensor-core kernel of the step (the projection) and, beside it, of
     # the dominant HBM-bound kernel
     def hbm_roofline(kname, kms, kl):
@@ -526,12 +540,12 @@ def main():
     def step_b(k):
         b = algorithmic_bytes(k, n, mi.dims, mc, F)
         return b if b is not None else extra.get(k)
-    step_bytes = sum(step_b(k) * v[1] / args.steps for k, v in prof.items() if step_b(k) is not None)
+    step_bytes = sum(step_b(k) * v[1] for k, v in prof_all.items() if step_b(k) is not None)
     step_t = 0.0
-    for k, v in prof.items():
+    for k, v in prof_all.items():
         o = algorithmic_ops(k, n, mi.dims, mc, F)
         if o is not None:
-            step_t += o * v[1] / args.steps / (tensor_peak(k, peaks)[0] * 1e12)
+            step_t += o * v[1] / (tensor_peak(k, peaks)[0] * 1e12)
     floor_ms = max(step_bytes / (hbm_peak * 1e9), step_t) * 1e3
     step_roofline = {"floor_ms": floor_ms, "measured_ms": total_ms / args.steps,
                      "frac": floor_ms / (total_ms / args.steps), "hbm_bytes_per_step": step_bytes,

@@ -122,6 +122,8 @@ zi_status zi_ctx_flush_l2(zi_ctx* ctx);
 uint64_t zi_ctx_kernel_launches(const zi_ctx* ctx);
 /* per-kernel device time accumulated while profiling is on (name-indexed, see api.cu) */
 zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on);
+/* time only these kernels (comma-separated launch names; NULL or "": every kernel) */
+zi_status zi_ctx_set_profile_filter(zi_ctx* ctx, const char* names);
 zi_status zi_ctx_profile(const zi_ctx* ctx, int slot, double* ms, uint64_t* launches,
                          const char** name);
 

@@ -110,6 +110,10 @@ class Context:
     def set_profiling(self, on: bool):
         check(lib().zi_ctx_set_profiling(self.h, int(on)))
 
+    def set_profile_filter(self, names=None):
+        """Time only these kernels while profiling (None: every kernel)."""
+        check(lib().zi_ctx_set_profile_filter(self.h, ",".join(names).encode() if names else None))
+
     def profile(self) -> dict:
         """{kernel name: (total device ms, launches)} since set_profiling(True)."""
         out = {}

@@ -57,9 +57,17 @@ thread_local cudaStream_t tls_alloc_stream = nullptr;
 
 namespace zi {
 
+static bool profiled(const zi_ctx* ctx, const char* name) {
+    if (!ctx->profiling) return false;
+    if (ctx->prof_filter.empty()) return true;
+    for (const auto& f : ctx->prof_filter)
+        if (f == name) return true;
+    return false;
+}
+
 void launch_begin(zi_ctx* ctx, const char* name) {
     ++ctx->launches;
-    if (!ctx->profiling) return;
+    if (!profiled(ctx, name)) return;
     prof_slot* s = nullptr;
     for (auto& p : ctx->prof)
         if (std::strcmp(p.name, name) == 0) s = &p;
@@ -83,7 +91,7 @@ void launch_end(zi_ctx* ctx, const char* name) {
         const cudaError_t e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) throw error(ZI_E_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
     }
-    if (!ctx->profiling) return;
+    if (!profiled(ctx, name)) return;
     for (auto& p : ctx->prof)
         if (std::strcmp(p.name, name) == 0) {
             ZI_CUDA(cudaEventRecord(p.events[p.used].second, ctx->stream));
@@ -226,6 +234,24 @@ zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on) {
         for (auto& p : ctx->prof) {
             p.used = 0;
             p.launches = 0;
+        }
+    });
+}
+
+zi_status zi_ctx_set_profile_filter(zi_ctx* ctx, const char* names) {
+    return guard(ctx, [&] {
+        require(ctx != nullptr, "null argument");
+        ctx->prof_filter.clear();
+        if (!names) return;
+        std::string cur;
+        for (const char* c = names;; ++c) {
+            if (*c == ',' || *c == 0) {
+                if (!cur.empty()) ctx->prof_filter.push_back(cur);
+                cur.clear();
+                if (*c == 0) break;
+            } else {
+                cur += *c;
+            }
         }
     });
 }

@@ -104,6 +104,7 @@ struct zi_ctx {
     uint64_t launches = 0;
     bool profiling = false;
     std::vector<zi::prof_slot> prof;
+    std::vector<std::string> prof_filter;  // kernels to time while profiling (empty: every kernel)
     int num_sms = 148;
     // shared scratch for sorts / collection
     zi::dbuf<uint8_t> scratch;
