@@ -825,3 +825,23 @@ def test_pca_householder_path_still_green():
                         os.path.join(root, "tests", "test_gpu_parity.py")],
                        env=env, cwd=root, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_sharded_build_with_empty_shards(zb):
+    """More ranks than dictionary patches: the empty slices take part in every collective with
+    identity ranges and sentinel samples; the non-empty shards still equal the single-GPU build."""
+    rng = np.random.default_rng(41)
+    img = rng.integers(0, 256, (11, 13), dtype=np.uint8)  # K = 9: 3 x 5 = 15 windows
+    kn = np.ones_like(img)
+    kn[0, 4] = 0  # removes the windows covering (0, 4)
+    cfg = zb.index_config(patch_size=9, dims=4, knn=4)
+    mi = zb.MultiIndex(img, kn, cfg)
+    world = mi.n + 3
+    sharding, shards, _ = _sharded(zb, img, kn, cfg, world, samples=4)
+    ranges = sharding.shard_ranges(mi.n, world)
+    assert any(e == b for b, e in ranges)
+    for l in range(8):
+        c, k = mi.index_arrays(l)
+        cs = np.concatenate([sh.multi_index.index_arrays(l)[0] for sh in shards])
+        ks = np.concatenate([sh.multi_index.index_arrays(l)[1] for sh in shards])
+        assert np.array_equal(cs, c) and np.array_equal(ks, k), l
