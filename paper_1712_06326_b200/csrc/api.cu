@@ -193,6 +193,7 @@ zi_status zi_ctx_destroy(zi_ctx* ctx) {
         ctx->scratch.release();  // stream-ordered frees before the stream goes away
         ctx->counter.release();
         ctx->flush.release();
+        ctx->gm_wtab.release();
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
         delete ctx;

@@ -331,6 +331,8 @@ void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const
     ZI_CUDA(cudaMemsetAsync(d_out, 0, (static_cast<size_t>(F) + static_cast<size_t>(F) * F) * sizeof(unsigned long long),
                             ctx->stream));
     if (n == 0) return;
+    // the fused tensor-core path (k_proj_tc.cu): no patch matrix in HBM
+    if (patch_moments_fused(ctx, d_img, w, C, K, d_keys, n, d_out, ctx->gm_wtab)) return;
     // Fpad > F: row F of XT is all ones over the real patches (G[f][F] = first moments)
     const int ntile = (F + 1 + kMomTile - 1) / kMomTile;
     const int Fpad = ntile * kMomTile;

@@ -119,6 +119,9 @@ __device__ __forceinline__ void pt_gather(const pt_params& P, const int2* s_wtab
                     if (o1 != 0xffffffu) word |= pt_ld4(P.img, base + o1) << sh;
                 }
             }
+            // feature F (the first padding byte) is 1 for every real patch: the fused Gram reads
+            // its column as the first moments; the projection's digits there are zero
+            if (4 * c + t == (static_cast<int>(P.F) >> 2)) word |= 1u << (8 * (P.F & 3));
             wv[t] = valid ? word : 0u;
         }
         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sA_addr + sw128_off(r, c << 4, kPtRows)), "r"(wv[0]),
@@ -146,6 +149,9 @@ __device__ __forceinline__ void pt_gather_static(const uint8_t* __restrict__ img
     uint32_t out[NO];
 #pragma unroll
     for (int i = 0; i < NO; ++i) out[i] = 0u;
+    if constexpr (F / 4 - 4 * C0 >= 0 && F / 4 - 4 * C0 < NO) {  // feature F = 1: the ones column
+        if (valid) out[F / 4 - 4 * C0] |= 1u << (8 * (F % 4));
+    }
 #pragma unroll
     for (int rr = S0; rr < S1; ++rr) {
         const uint32_t a = base + static_cast<uint32_t>(rr) * wC;
@@ -446,6 +452,223 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
     }
+}
+
+// ------------------------------------------------------------------ fused exact moments
+// K2 without the patch matrix: the same 128-patch A tiles as the projection (gathered from the
+// L2-resident image into 128B-swizzled shared memory, feature F = 1 for real patches), used as
+// BOTH operands of X^T X through the MN-major (transposed) UMMA descriptors: per tile and per
+// 128x128 feature-tile pair (ti <= tj) four tcgen05.mma.kind::i8 (K = 32 patches each) into a
+// 128-column TMEM accumulator.  Each CTA (one per SM, more when an SM would get more than 512
+// tiles: 65536 patches keep the u32 view of the s32 sums exact) sums its tiles and folds them into
+// the int64 moments with atomics (order-free, deterministic).  Two gather groups of 8 warps keep
+// two tiles' gathers in flight.  At most 4 pairs (512 TMEM columns) per launch.
+constexpr int kGmPairs = 4;
+constexpr int kGmChunk = 512;
+struct gm_params {
+    pt_params P;  // gather fields: img, w, C, KC, F, Fpad, keys, n, ntiles, wtab
+    int npair;
+    int pti[kGmPairs], ptj[kGmPairs];
+    unsigned long long* out;  // F + F*F
+};
+
+__device__ __forceinline__ uint64_t tc_desc_mn128(uint32_t saddr) {  // MN-major, 128B swizzle
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3fffu);
+    d |= static_cast<uint64_t>(1u) << 16;            // leading byte offset (one 128-byte atom along M)
+    d |= static_cast<uint64_t>(1024u >> 4) << 32;    // stride byte offset: next 8 patches
+    d |= static_cast<uint64_t>(1u) << 46;
+    d |= static_cast<uint64_t>(2u) << 61;
+    return d;
+}
+
+constexpr int kGmGroups = 2;                         // gather groups (tiles i, i + 1 in flight together)
+constexpr int kGmThreads = (8 * kGmGroups + 1) * 32;  // 8 gather warps per group + the MMA warp
+
+template <int KT>
+__global__ void __launch_bounds__(kGmThreads, 1) k_gram_fused(const __grid_constant__ gm_params G) {
+    const pt_params& P = G.P;
+    extern __shared__ uint8_t gm_raw[];
+    uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const uint32_t abytes = static_cast<uint32_t>(kPtRows * P.Fpad);
+    constexpr int NB = 2 * kGmGroups;  // a 2-buffer ring per gather group
+    __shared__ __align__(8) uint64_t s_afull[NB], s_aempty[NB], s_done;
+    __shared__ uint32_t s_tmem;
+    __shared__ int2 s_wtab[kPtMaxFpad / 4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kMmaWarp = 8 * kGmGroups;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem(&s_tmem)), "r"(512u)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int b = 0; b < NB; ++b) {
+            tc_mbar_init(tc_smem(&s_afull[b]), 8);
+            tc_mbar_init(tc_smem(&s_aempty[b]), 1);
+        }
+        tc_mbar_init(tc_smem(&s_done), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < P.Fpad / 4; i += blockDim.x) s_wtab[i] = P.wtab[i];
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    // this CTA's tiles: blockIdx.x + i * gridDim.x, i < nloc <= kGmChunk (the host sizes the grid)
+    const uint64_t nloc = blockIdx.x < P.ntiles ? (P.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    if (warp == kMmaWarp) {
+        if (lane == 0) {  // MMA issuer: tile i sits in buffer (i % groups) * 2 + ((i / groups) & 1)
+            const uint32_t idesc = (2u << 4) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+            for (uint64_t i = 0; i < nloc; ++i) {
+                const uint64_t j = i / kGmGroups;
+                const int b = static_cast<int>(i % kGmGroups) * 2 + static_cast<int>(j & 1);
+                tc_mbar_wait(tc_smem(&s_afull[b]), static_cast<uint32_t>((j >> 1) & 1));
+                tc_fence_after();
+                const uint32_t a0 = tc_smem(sA + b * abytes);
+                for (int p = 0; p < G.npair; ++p) {
+                    const uint32_t ta = a0 + static_cast<uint32_t>(G.pti[p]) * kPtRows * 128;
+                    const uint32_t tb = a0 + static_cast<uint32_t>(G.ptj[p]) * kPtRows * 128;
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        pt_mma(tmem + static_cast<uint32_t>(p * 128), tc_desc_mn128(ta + ks * 4096), tc_desc_mn128(tb + ks * 4096),
+                               idesc, (i | ks) != 0 ? 1u : 0u);
+                }
+                tc_commit(tc_smem(&s_aempty[b]));
+            }
+            tc_commit(tc_smem(&s_done));
+        }
+    } else {  // gather group g = warp / 8 takes tiles g, g + groups, ...: two threads per patch row
+        const int g = warp / 8, gw = warp % 8;
+        const int nchunk = P.Fpad >> 4, hc = (nchunk + 1) >> 1;
+        const int r = (gw * 32 + lane) & 127, gh = gw >> 2;
+        for (uint64_t i = g, j = 0; i < nloc; i += kGmGroups, ++j) {
+            const int b = g * 2 + static_cast<int>(j & 1);
+            if (j >= 2) tc_mbar_wait(tc_smem(&s_aempty[b]), static_cast<uint32_t>(((j >> 1) - 1) & 1));
+            const uint64_t tile = blockIdx.x + i * gridDim.x;
+            const uint32_t sa = tc_smem(sA + b * abytes);
+            if (KT == 0) {
+                pt_gather(P, s_wtab, tile, sa, r, gh ? hc : 0, gh ? nchunk : hc);
+            } else {
+                const uint64_t pr = tile * kPtRows + r;
+                const bool valid = pr < P.n;
+                uint32_t base = 0;
+                if (valid) {
+                    const uint32_t key = __ldg(P.keys + pr);
+                    base = ((key >> 16) * static_cast<uint32_t>(P.w) + (key & 0xffffu)) * static_cast<uint32_t>(P.C);
+                }
+                const uint32_t wC = static_cast<uint32_t>(P.w * P.C);
+                if (KT == 1) {
+                    if (gh) pt_gather_static<9, 1, 1>(P.img, base, wC, valid, sa, r);
+                    else pt_gather_static<9, 1, 0>(P.img, base, wC, valid, sa, r);
+                } else {
+                    if (gh) pt_gather_static<11, 3, 1>(P.img, base, wC, valid, sa, r);
+                    else pt_gather_static<11, 3, 0>(P.img, base, wC, valid, sa, r);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tc_mbar_arrive(tc_smem(&s_afull[b]));
+        }
+        if (warp < 4 && nloc > 0) {  // epilogue: TMEM lanes 32 * warp .. + 31 = feature rows of tile ti
+            tc_mbar_wait(tc_smem(&s_done), 0);
+            tc_fence_after();
+            for (int p = 0; p < G.npair; ++p) {
+                const int fi = G.pti[p] * kPtRows + warp * 32 + lane;
+                for (int cb = 0; cb < 128; cb += 4) {
+                    uint32_t v[4];
+                    tc_ld_x4(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(p * 128 + cb), v);
+                    tc_ld_wait();
+                    if (fi < P.F) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int fj = G.ptj[p] * kPtRows + cb + q;
+                            if (v[q] == 0u) continue;
+                            if (fj < P.F) atomicAdd(G.out + P.F + static_cast<size_t>(fi) * P.F + fj, static_cast<unsigned long long>(v[q]));
+                            else if (fj == P.F) atomicAdd(G.out + fi, static_cast<unsigned long long>(v[q]));
+                        }
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
+    }
+}
+
+template <int KT>
+static void launch_gram(zi_ctx* ctx, const gm_params& G, size_t smem) {
+    static bool attr = false;
+    if (!attr) {
+        ZI_CUDA(cudaFuncSetAttribute(k_gram_fused<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = true;
+    }
+    // one CTA per SM, more when an SM would sum more than kGmChunk tiles (65536 patches: the
+    // u32 view of the s32 accumulators stays exact)
+    const uint64_t want = std::max<uint64_t>(static_cast<uint64_t>(ctx->num_sms), (G.P.ntiles + kGmChunk - 1) / kGmChunk);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(G.P.ntiles, want));
+    ZI_LAUNCH(ctx, "patch_moments_fused", k_gram_fused<KT>, grid, kGmThreads, smem, G);
+}
+
+// exact moments of the n patches at d_keys (row-major key order) straight from the image;
+// false when the patch shape is outside the envelope (F >= Fpad or Fpad > 384)
+bool patch_moments_fused(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const uint32_t* d_keys, uint64_t n,
+                         unsigned long long* d_out, dbuf<int2>& wtab) {
+    static const bool off_env = std::getenv("ZI_MOMENTS_TMA") != nullptr;
+    const int F = K * K * C, Fpad = (F + 127) / 128 * 128;
+    if (off_env || F >= Fpad || Fpad > kPtMaxFpad || n == 0 || n >= (1ull << 31)) return false;
+    {  // gather word table (as the projection's)
+        const int KC = K * C, wC = w * C;
+        std::vector<int2> tab(Fpad / 4);
+        for (int ow = 0; ow < Fpad / 4; ++ow) {
+            const int f = 4 * ow;
+            if (f >= F) {
+                tab[ow] = make_int2(-1, -1);
+                continue;
+            }
+            const int rr = f / KC, k = f - rr * KC, rem = KC - k;
+            int y = -1;
+            if (rem < 4) y = (rem << 24) | (rr + 1 < K ? (rr + 1) * wC : 0xffffff);
+            tab[ow] = make_int2(rr * wC + k, y);
+        }
+        wtab.ensure(tab.size());
+        ZI_CUDA(cudaMemcpyAsync(wtab.p, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    gm_params G{};
+    G.P.img = d_img;
+    G.P.w = w;
+    G.P.C = C;
+    G.P.KC = K * C;
+    G.P.F = F;
+    G.P.Fpad = Fpad;
+    G.P.keys = d_keys;
+    G.P.n = n;
+    G.P.ntiles = (n + kPtRows - 1) / kPtRows;
+    G.P.wtab = wtab.p;
+    G.out = d_out;
+    const int nt = Fpad / 128;
+    const int kt = K * C == 9 && F == 81 ? 1 : (K * C == 33 && F == 363 ? 2 : 0);
+    // >= 116 KB: one CTA per SM, so no second CTA waits on the first one's 512 TMEM columns
+    const size_t smem = std::max<size_t>(2 * kGmGroups * static_cast<size_t>(kPtRows) * Fpad + 1024, 116 * 1024);
+    if (smem > 220 * 1024) return false;
+    std::vector<int2> pairs;
+    for (int ti = 0; ti < nt; ++ti)
+        for (int tj = ti; tj < nt; ++tj) pairs.push_back(make_int2(ti, tj));
+    for (size_t p0 = 0; p0 < pairs.size(); p0 += kGmPairs) {
+        G.npair = static_cast<int>(std::min<size_t>(kGmPairs, pairs.size() - p0));
+        for (int p = 0; p < G.npair; ++p) {
+            G.pti[p] = pairs[p0 + p].x;
+            G.ptj[p] = pairs[p0 + p].y;
+        }
+        if (kt == 1) launch_gram<1>(ctx, G, smem);
+        else if (kt == 2) launch_gram<2>(ctx, G, smem);
+        else launch_gram<0>(ctx, G, smem);
+    }
+    return true;
 }
 
 // digit matrices of all groups (pre-zeroed) and M = sum_j mean_j c_j, from the device models

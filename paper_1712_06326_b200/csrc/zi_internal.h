@@ -114,6 +114,7 @@ struct zi_ctx {
     // raised when a build's MSD split left too many records in oversized segments
     int sort_depth[33][2] = {};
     int flush_toggle = 1;
+    zi::dbuf<int2> gm_wtab;      // fused moments: gather word table
 };
 
 // One z-curve-sorted index, device resident.
@@ -214,6 +215,9 @@ uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, i
 void gram_u8_tc(zi_ctx* ctx, const uint8_t* XT, int F, int Fpad, uint64_t npad, unsigned long long* out);
 void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const uint32_t* d_keys,
                    uint64_t n, unsigned long long* d_out /* F + F*F */);
+// the fused path of patch_moments (k_proj_tc.cu); false: outside its envelope
+bool patch_moments_fused(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const uint32_t* d_keys, uint64_t n,
+                         unsigned long long* d_out, dbuf<int2>& wtab);
 
 // projection pass: Y[d*n + i] fp64 and ordered-u64 lo/hi in minmax (2*D)
 void project(zi_ctx* ctx, const uint8_t* d_img, int w, int C, const uint32_t* d_keys, uint64_t n,
