@@ -602,10 +602,10 @@ __global__ void __launch_bounds__(kGmThreads, 1) k_gram_fused(const __grid_const
 
 template <int KT>
 static void launch_gram(zi_ctx* ctx, const gm_params& G, size_t smem) {
-    static bool attr = false;
-    if (!attr) {
+    static size_t attr = 0;
+    if (smem > attr) {
         ZI_CUDA(cudaFuncSetAttribute(k_gram_fused<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
+        attr = smem;
     }
     // one CTA per SM, more when an SM would sum more than kGmChunk tiles (65536 patches: the
     // u32 view of the s32 accumulators stays exact)
