@@ -612,6 +612,40 @@ def main():
                            "per iteration), through MultiIndex.inpaint / zi_inpaint_with_index; the faster of "
                            "two runs (the host part varies by ~15 % between runs)"}
 
+    # -------- the exhaustive masked-L2 scan (brute_force_best, the original method's comparison
+    # path, proj/src/engine.cpp:220-236) over the whole dictionary, rank 0
+    brute = None
+    if rank == 0 and not args.no_inpaint:
+        ys, xs = np.nonzero(known == 0)
+        K = p["patch_size"]
+        pick = np.linspace(0, len(xs) - 1, 16).astype(int)
+        targets = []
+        for t in pick:  # windows centred on unknown pixels near known ones (fill-front-like)
+            x0, y0 = int(xs[t]) - K // 2, int(ys[t]) - K // 2
+            tv = np.zeros((K, K) + img.shape[2:], np.uint8)
+            tk = np.zeros((K, K), np.uint8)
+            for r in range(K):
+                for c in range(K):
+                    yy, xx = y0 + r, x0 + c
+                    if 0 <= yy < img.shape[0] and 0 <= xx < img.shape[1] and known[yy, xx]:
+                        tv[r, c] = img[yy, xx]
+                        tk[r, c] = 1
+            targets.append((tv.reshape(-1), tk.reshape(-1)))
+        mi.brute_force_best(*targets[0])  # warm-up
+        t0 = time.perf_counter()
+        for tv, tk in targets:
+            mi.brute_force_best(tv, tk)
+        dt = (time.perf_counter() - t0) / len(targets)
+        C = 1 if img.ndim == 2 else img.shape[2]
+        known_vals = float(np.mean([int(tk.sum()) for _, tk in targets])) * C
+        ops = 3.0 * n * known_vals  # subtract, square (multiply-add) per known value, per dictionary patch
+        int_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12  # TOPS, nominal INT32 rate
+        brute = {"queries_per_s": 1.0 / dt, "us_per_query": dt * 1e6, "dictionary": n,
+                 "mean_known_values": known_vals, "int_ops_per_query": ops,
+                 "achieved_TOPS": ops / dt / 1e12, "int32_peak_TOPS": int_peak, "frac_of_int32": ops / dt / 1e12 / int_peak,
+                 "note": "host wall time per zi_brute_force_best call (H2D of the target, one scan kernel, D2H of "
+                         "the packed winner); INT-compute-bound, not an HBM roofline (SURVEY.md §8(d))"}
+
     knn = None
     if rank == 0 and not args.no_knn:
         try:
@@ -648,7 +682,7 @@ def main():
             "roofline": roofline, "roofline_hbm": roofline_hbm, "step_roofline": step_roofline,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk, "inpaint": inpaint, "candidate_scoring": knn, "vector_index": vec,
+            "clocks": clk, "inpaint": inpaint, "brute_force": brute, "candidate_scoring": knn, "vector_index": vec,
             "breakdown": {"host_eigen_s_per_step": float(np.mean(host_eigen)), "kernels": breakdown},
         }
         print(json.dumps(line), flush=True)
