@@ -856,36 +856,54 @@ __global__ void __launch_bounds__(256) k_brute(const uint8_t* __restrict__ img, 
                                                const uint32_t* __restrict__ dict, uint64_t n,
                                                const uint8_t* __restrict__ target, int norm,
                                                unsigned long long* __restrict__ best) {
+    // shared: the known target values in known-local order (known_locals_of, engine.cpp:16-22)
+    // and each value's byte offset from the patch origin, so the scan loop is two broadcast loads,
+    // one image byte and one multiply-add per value
     extern __shared__ uint8_t s_t[];
-    __shared__ int s_nloc;
+    __shared__ int s_nv;
     __shared__ unsigned long long s_best;
     const int KK = K * K;
-    uint16_t* s_loc = reinterpret_cast<uint16_t*>(s_t + ((KK * C + 1) & ~1));
-    for (int i = threadIdx.x; i < KK * C; i += blockDim.x) s_t[i] = target[i];
-    if (threadIdx.x == 0) {
-        int c = 0;
-        for (int l = 0; l < KK; ++l)
-            if (target[KK * C + l]) s_loc[c++] = static_cast<uint16_t>(l);
-        s_nloc = c;
-        s_best = kU64Max;
+    int* s_off = reinterpret_cast<int*>(s_t + ((KK * C + 3) & ~3));
+    if (threadIdx.x < 32) {  // warp 0: ballot-compacted known locals, ascending
+        int cnt = 0;
+        for (int base = 0; base < KK; base += 32) {
+            const int l = base + threadIdx.x;
+            const bool kn = l < KK && target[KK * C + l] != 0;
+            const unsigned m = __ballot_sync(0xffffffffu, kn);
+            if (kn) {
+                const int slot = cnt + __popc(m & ((1u << threadIdx.x) - 1u));
+                const int ly = l / K, lx = l - ly * K;
+                for (int c = 0; c < C; ++c) {
+                    s_t[slot * C + c] = target[l * C + c];
+                    s_off[slot * C + c] = (ly * w + lx) * C + c;
+                }
+            }
+            cnt += __popc(m);
+        }
+        if (threadIdx.x == 0) {
+            s_nv = cnt * C;
+            s_best = kU64Max;
+        }
     }
     __syncthreads();
-    const int nloc = s_nloc;
+    const int nv = s_nv;
     unsigned long long mine = kU64Max;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint32_t key = dict[i];
-        const int sx = key & 0xffff, sy = key >> 16;
-        const uint8_t* base = img + (static_cast<size_t>(sy) * w + sx) * C;
+        const uint8_t* base = img + (static_cast<size_t>(key >> 16) * w + (key & 0xffffu)) * C;
         uint32_t acc = 0;
-        for (int li = 0; li < nloc; ++li) {
-            const int l = s_loc[li];
-            const int ly = l / K, lx = l % K;
-            const uint8_t* s = base + (static_cast<size_t>(ly) * w + lx) * C;
-            const uint8_t* t = s_t + l * C;
-            for (int c = 0; c < C; ++c) {
-                const int d = static_cast<int>(t[c]) - static_cast<int>(__ldg(s + c));
-                acc += norm == 0 ? static_cast<uint32_t>(d * d) : static_cast<uint32_t>(d < 0 ? -d : d);
+        if (norm == 0) {
+#pragma unroll 4
+            for (int v = 0; v < nv; ++v) {
+                const int d = static_cast<int>(s_t[v]) - static_cast<int>(__ldg(base + s_off[v]));
+                acc += static_cast<uint32_t>(d * d);
+            }
+        } else {
+#pragma unroll 4
+            for (int v = 0; v < nv; ++v) {
+                const int d = static_cast<int>(s_t[v]) - static_cast<int>(__ldg(base + s_off[v]));
+                acc += static_cast<uint32_t>(d < 0 ? -d : d);
             }
         }
         const unsigned long long c = pack_candidate(acc, key);
@@ -2138,7 +2156,7 @@ uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t
     std::memcpy(stage + KK * mi->C, h_tk, KK);
     ZI_CUDA(cudaMemcpyAsync(s.target, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
     ZI_CUDA(cudaMemsetAsync(&s.ws->best, 0xff, sizeof(unsigned long long), ctx->stream));
-    const size_t smem = ((KK * mi->C + 1) & ~size_t(1)) + KK * sizeof(uint16_t) + 16;
+    const size_t smem = ((KK * mi->C + 3) & ~size_t(3)) + KK * mi->C * sizeof(int) + 16;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((mi->n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
     ZI_LAUNCH(ctx, "brute_force", k_brute, grid, 256, smem, mi->image.p, mi->w, mi->C, mi->K, mi->dict.p + mi->row_begin,
               mi->n, s.target, norm, &s.ws->best);
