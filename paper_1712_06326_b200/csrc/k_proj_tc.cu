@@ -460,9 +460,10 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
 // BOTH operands of X^T X through the MN-major (transposed) UMMA descriptors: per tile and per
 // 128x128 feature-tile pair (ti <= tj) four tcgen05.mma.kind::i8 (K = 32 patches each) into a
 // 128-column TMEM accumulator.  Each CTA (one per SM, more when an SM would get more than 512
-// tiles: 65536 patches keep the u32 view of the s32 sums exact) sums its tiles and folds them into
-// the int64 moments with atomics (order-free, deterministic).  Two gather groups of 8 warps keep
-// two tiles' gathers in flight.  At most 4 pairs (512 TMEM columns) per launch.
+// tiles: 65536 patches keep the u32 view of the s32 sums exact) sums its tiles and writes its
+// partial Gram; k_gram_reduce adds the partials in int64 (fixed order, no atomics).  Two gather
+// groups of 8 warps keep two tiles' gathers in flight.  At most 4 pairs (512 TMEM columns) per
+// launch.
 constexpr int kGmPairs = 4;
 constexpr int kGmChunk = 512;
 struct gm_params {
@@ -470,6 +471,7 @@ struct gm_params {
     int npair;
     int pti[kGmPairs], ptj[kGmPairs];
     unsigned long long* out;  // F + F*F
+    uint32_t* part;           // per-CTA partial Grams [cta][pair][128][128] (k_gram_reduce folds them)
 };
 
 __device__ __forceinline__ uint64_t tc_desc_mn128(uint32_t saddr) {  // MN-major, 128B swizzle
@@ -570,24 +572,21 @@ __global__ void __launch_bounds__(kGmThreads, 1) k_gram_fused(const __grid_const
             __syncwarp();
             if (lane == 0) tc_mbar_arrive(tc_smem(&s_afull[b]));
         }
-        if (warp < 4 && nloc > 0) {  // epilogue: TMEM lanes 32 * warp .. + 31 = feature rows of tile ti
-            tc_mbar_wait(tc_smem(&s_done), 0);
-            tc_fence_after();
+        if (warp < 4) {  // epilogue: this CTA's partial Gram (TMEM lane = feature row of tile ti), u32 exact
+            if (nloc > 0) {
+                tc_mbar_wait(tc_smem(&s_done), 0);
+                tc_fence_after();
+            }
+            const int row = warp * 32 + lane;
             for (int p = 0; p < G.npair; ++p) {
-                const int fi = G.pti[p] * kPtRows + warp * 32 + lane;
+                uint4* dst = reinterpret_cast<uint4*>(G.part + ((static_cast<size_t>(blockIdx.x) * G.npair + p) * kPtRows + row) * 128);
                 for (int cb = 0; cb < 128; cb += 4) {
-                    uint32_t v[4];
-                    tc_ld_x4(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(p * 128 + cb), v);
-                    tc_ld_wait();
-                    if (fi < P.F) {
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int fj = G.ptj[p] * kPtRows + cb + q;
-                            if (v[q] == 0u) continue;
-                            if (fj < P.F) atomicAdd(G.out + P.F + static_cast<size_t>(fi) * P.F + fj, static_cast<unsigned long long>(v[q]));
-                            else if (fj == P.F) atomicAdd(G.out + fi, static_cast<unsigned long long>(v[q]));
-                        }
+                    uint32_t v[4] = {0u, 0u, 0u, 0u};
+                    if (nloc > 0) {
+                        tc_ld_x4(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(p * 128 + cb), v);
+                        tc_ld_wait();
                     }
+                    dst[cb >> 2] = make_uint4(v[0], v[1], v[2], v[3]);
                 }
             }
         }
@@ -598,6 +597,22 @@ __global__ void __launch_bounds__(kGmThreads, 1) k_gram_fused(const __grid_const
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
     }
+}
+
+// sum of the per-CTA partial Grams in int64 into the moments (every output has one owner: no atomics)
+__global__ void __launch_bounds__(256) k_gram_reduce(const uint32_t* __restrict__ part, int nblocks, int npair,
+                                                     const int* __restrict__ pti, const int* __restrict__ ptj, int F,
+                                                     unsigned long long* __restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= npair * 128 * 128) return;
+    const int p = idx >> 14, r = (idx >> 7) & 127, c = idx & 127;
+    const int fi = pti[p] * kPtRows + r, fj = ptj[p] * kPtRows + c;
+    if (fi >= F || fj > F) return;
+    unsigned long long acc = 0;
+    const size_t stride = static_cast<size_t>(npair) * 128 * 128;
+    for (int b = 0; b < nblocks; ++b) acc += __ldg(part + b * stride + idx);
+    if (fj < F) out[F + static_cast<size_t>(fi) * F + fj] += acc;
+    else out[fi] += acc;
 }
 
 template <int KT>
@@ -611,7 +626,19 @@ static void launch_gram(zi_ctx* ctx, const gm_params& G, size_t smem) {
     // u32 view of the s32 accumulators stays exact)
     const uint64_t want = std::max<uint64_t>(static_cast<uint64_t>(ctx->num_sms), (G.P.ntiles + kGmChunk - 1) / kGmChunk);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(G.P.ntiles, want));
-    ZI_LAUNCH(ctx, "patch_moments_fused", k_gram_fused<KT>, grid, kGmThreads, smem, G);
+    gm_params g = G;
+    g.part = reinterpret_cast<uint32_t*>(ctx->scratch.ensure(static_cast<size_t>(grid) * G.npair * 128 * 128 * 4 + 256));
+    int* pp = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(g.part) + static_cast<size_t>(grid) * G.npair * 128 * 128 * 4);
+    ZI_LAUNCH(ctx, "patch_moments_fused", k_gram_fused<KT>, grid, kGmThreads, smem, g);
+    int hp[2 * kGmPairs];
+    for (int i = 0; i < kGmPairs; ++i) {
+        hp[i] = G.pti[i];
+        hp[kGmPairs + i] = G.ptj[i];
+    }
+    ZI_CUDA(cudaMemcpyAsync(pp, hp, sizeof(hp), cudaMemcpyHostToDevice, ctx->stream));
+    const int outs = G.npair * 128 * 128;
+    ZI_LAUNCH(ctx, "patch_moments_reduce", k_gram_reduce, (outs + 255) / 256, 256, 0, g.part, static_cast<int>(grid), G.npair,
+              pp, pp + kGmPairs, G.P.F, G.out);
 }
 
 // exact moments of the n patches at d_keys (row-major key order) straight from the image;
