@@ -845,3 +845,19 @@ def test_sharded_build_with_empty_shards(zb):
         cs = np.concatenate([sh.multi_index.index_arrays(l)[0] for sh in shards])
         ks = np.concatenate([sh.multi_index.index_arrays(l)[1] for sh in shards])
         assert np.array_equal(cs, c) and np.array_equal(ks, k), l
+
+
+def test_moments_patch_matrix_path_still_green():
+    """The fused tensor-core moments cover every configuration here; re-run the moment and build
+    parity tests on the patch-matrix + TMA Gram path (ZI_MOMENTS_TMA=1), the fallback for patch
+    shapes outside the fused kernel's envelope."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ZI_MOMENTS_TMA="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k",
+                        "moments_exact or build_bitexact or cfg1_end_to_end",
+                        os.path.join(root, "tests", "test_gpu_parity.py")],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
