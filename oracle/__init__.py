@@ -104,7 +104,7 @@ def lib():
                                           C.c_int]
         L.zo_mi_build.restype = C.c_void_p
         L.zo_mi_build.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
-                                  _f64p, _f64p]
+                                  _f64p, _f64p, C.c_int, C.c_int]
         L.zo_mi_free.argtypes = [C.c_void_p]
         for fn in ("zo_mi_size",):
             getattr(L, fn).restype = C.c_int64
@@ -120,7 +120,8 @@ def lib():
         L.zo_mi_query_best_patch.argtypes = [C.c_void_p, _u8p, _u8p, _u8p, C.c_int64, C.c_int, _ip, _i64p, _u64p]
         L.zo_inpaint.restype = C.c_int64
         L.zo_inpaint.argtypes = [C.c_void_p, _u8p, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64,
-                                 C.c_int, C.c_int, C.c_int, C.c_int64, _u8p, C.POINTER(Record), C.c_int64]
+                                 C.c_int, C.c_int, C.c_int, C.c_int64, _u8p, C.POINTER(Record), C.c_int64,
+                                 C.c_int64]
         L.zo_error.restype = C.c_char_p
         _lib = L
     return _lib
@@ -152,12 +153,62 @@ def ref():
         R.zr_index_knn_batch.restype = C.c_int64
         R.zr_index_knn_batch.argtypes = [C.c_void_p, _u8p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.c_int, _u64p]
+        R.zr_index_knn_batch_mt.restype = C.c_int64
+        R.zr_index_knn_batch_mt.argtypes = [C.c_void_p, _u8p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.c_int, _u64p, _u32p]
         R.zr_extract_patch_clamped.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                                C.c_int, _u8p, _u8p]
         R.zr_fillfront.restype = C.c_int64
         R.zr_fillfront.argtypes = [_u8p, C.c_int, C.c_int, _ip]
         _ref = R
     return _ref
+
+
+class RefIndex:
+    """The reference's own ``zcurve_index`` (proj/src/zcurve.cpp, compiled unmodified into
+    oracle/_ref/libzref.so): ``from_descriptors`` at construction, ``knn_search`` per query."""
+
+    def __init__(self, coords, keys):
+        coords = np.ascontiguousarray(coords, dtype=np.uint8)
+        keys = np.ascontiguousarray(keys, dtype=np.uint32)
+        self.n, self.dims = coords.shape
+        self.h_ = ref().zr_index_create(_p(coords, _u8p), _p(keys, _u32p), self.n, self.dims)
+        if not self.h_:
+            raise ValueError("zcurve_index::from_descriptors rejected the input")
+
+    def __del__(self):
+        h = getattr(self, "h_", None)
+        if h:
+            ref().zr_index_free(h)
+            self.h_ = None
+
+    def export(self):
+        c = np.zeros((self.n, self.dims), dtype=np.uint8)
+        k = np.zeros(self.n, dtype=np.uint32)
+        ref().zr_index_export(self.h_, _p(c, _u8p), _p(k, _u32p))
+        return c, k
+
+    def knn(self, query, k, norm=L2, mu=256, nu=2048, workers=1):
+        q = np.ascontiguousarray(query, dtype=np.uint8)
+        out = np.zeros(max(1, k), dtype=np.uint64)
+        cnt = ref().zr_index_knn(self.h_, _p(q, _u8p), k, mu, nu, norm, workers, _p(out, _u64p))
+        return out[:cnt].copy()
+
+    def knn_batch(self, queries, k, norm=L2, mu=256, nu=2048, threads=None):
+        """(packed nq x k, counts nq); queries split over host threads, sequential traversal each."""
+        q = np.ascontiguousarray(queries, dtype=np.uint8)
+        nq = q.shape[0]
+        out = np.zeros((nq, max(1, k)), dtype=np.uint64)
+        cnt = np.zeros(nq, dtype=np.uint32)
+        threads = threads or (os.cpu_count() or 1)
+        ref().zr_index_knn_batch_mt(self.h_, _p(q, _u8p), nq, k, mu, nu, norm, threads, _p(out, _u64p),
+                                    _p(cnt, _u32p))
+        return out, cnt
+
+
+def ref_from_descriptors(coords, keys):
+    """Sorted (coords, keys) from the reference's compiled ``from_descriptors``."""
+    return RefIndex(coords, keys).export()
 
 
 # ------------------------------------------------------------------ numpy-level helpers
@@ -326,7 +377,10 @@ class LayoutIndex:
 class MultiIndex:
     """Restated ``multi_index::build`` (proj/src/builder.cpp:202-224)."""
 
-    def __init__(self, img, known, K=9, coverage=0.6, dims=10, pca_mean=None, pca_comp=None):
+    def __init__(self, img, known, K=9, coverage=0.6, dims=10, pca_mean=None, pca_comp=None, layouts=None,
+                 threads=None):
+        """layouts: the layout ids to build (default all 8; the others stay empty); threads:
+        layouts built concurrently (default: one per host core, at most 8)."""
         self.img, self.w, self.h, self.ch = _img_dims(img)
         self.known = _u8(known)
         self.K = K
@@ -336,8 +390,11 @@ class MultiIndex:
             self._pm = np.ascontiguousarray(pca_mean, dtype=np.float64)
             self._pc = np.ascontiguousarray(pca_comp, dtype=np.float64)
             pm, pc = _p(self._pm, _f64p), _p(self._pc, _f64p)
+        mask = 0xFF if layouts is None else sum(1 << int(l) for l in layouts)
+        if threads is None:
+            threads = min(8, os.cpu_count() or 1)
         self.h_ = L.zo_mi_build(_p(self.img, _u8p), _p(self.known, _u8p), self.w, self.h, self.ch, K, coverage,
-                                dims, pm, pc)
+                                dims, pm, pc, mask, threads)
         if not self.h_:
             raise ValueError(L.zo_error().decode())
         self.n = L.zo_mi_size(self.h_)
@@ -383,9 +440,10 @@ class MultiIndex:
 
 
 def inpaint(img, known, K=9, coverage=0.6, dims=10, knn=80, norm=L2, brute_force=False, oracle=False,
-            oracle_stride=1, mi: MultiIndex | None = None, pca_mean=None, pca_comp=None):
+            oracle_stride=1, mi: MultiIndex | None = None, pca_mean=None, pca_comp=None, max_iter=0):
     """Restated ``inpaint`` / ``run_loop`` (proj/src/engine.cpp:371-506).
 
+    max_iter > 0 stops after that many iterations (the first records of the full run).
     Returns (image_out, records ndarray of Record).
     """
     img, w, h, ch = _img_dims(img)
@@ -394,9 +452,12 @@ def inpaint(img, known, K=9, coverage=0.6, dims=10, knn=80, norm=L2, brute_force
         mi = MultiIndex(img, known, K, coverage, dims, pca_mean, pca_comp)
     out = np.zeros_like(img)
     cap = int((known == 0).sum()) + 1
+    if max_iter > 0:
+        cap = min(cap, int(max_iter))
     recs = (Record * cap)()
     n = lib().zo_inpaint(mi.h_ if mi is not None else None, _p(img, _u8p), _p(known, _u8p), w, h, ch, K, knn,
-                         norm, int(brute_force), int(oracle), oracle_stride, _p(out, _u8p), recs, cap)
+                         norm, int(brute_force), int(oracle), oracle_stride, _p(out, _u8p), recs, cap,
+                         int(max_iter))
     if n < 0:
         raise RuntimeError(lib().zo_error().decode())
     arr = np.ctypeslib.as_array(recs)[:n].copy()

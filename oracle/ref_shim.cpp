@@ -1,12 +1,13 @@
 // ref_shim.cpp -- C ABI over the reference's OWN compiled sources (TEST INFRASTRUCTURE ONLY).
 //
-// oracle/build_ref.sh compiles this file together with the unmodified reference sources
+// `make -C oracle ref` (oracle/Makefile) compiles this file together with the unmodified reference sources
 //   /root/reference/proj/src/{zcurve,pool,layouts,image}.cpp
 // (the Eigen-free part of the reference) into oracle/_ref/libzref.so.
 // No reference source is copied into this repository; this shim only calls it.
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "zinpaint/image.hpp"
@@ -113,6 +114,38 @@ int64_t zr_index_knn_batch(void* h, const uint8_t* queries, int64_t nq, int k, i
         for (size_t i = 0; i < found.size(); ++i) out[q * k + static_cast<int64_t>(i)] = pack_candidate(found[i].distance, found[i].key);
         total += static_cast<int64_t>(found.size());
     }
+    return total;
+}
+
+// the same over `threads` host threads, queries split into contiguous blocks (each query is a
+// sequential traversal, as above; the result does not depend on the split)
+int64_t zr_index_knn_batch_mt(void* h, const uint8_t* queries, int64_t nq, int k, int mu, int nu, int norm,
+                              int threads, uint64_t* out, uint32_t* counts) {
+    const auto* idx = static_cast<zcurve_index*>(h);
+    search_params sp;
+    sp.k = static_cast<uint32_t>(k);
+    sp.mu = static_cast<uint32_t>(mu);
+    sp.nu = static_cast<uint32_t>(nu);
+    sp.norm = norm == 0 ? norm_kind::l2 : norm_kind::l1;
+    const int T = threads < 1 ? 1 : threads;
+    std::vector<int64_t> tot(T, 0);
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([&, t] {
+            knn_list list(sp.k);
+            for (int64_t q = nq * t / T; q < nq * (t + 1) / T; ++q) {
+                list.reset(sp.k);
+                knn_search(*idx, queries + q * idx->dims(), sp, list);
+                const auto found = list.sorted();
+                for (size_t i = 0; i < found.size(); ++i)
+                    out[q * k + static_cast<int64_t>(i)] = pack_candidate(found[i].distance, found[i].key);
+                if (counts) counts[q] = static_cast<uint32_t>(found.size());
+                tot[t] += static_cast<int64_t>(found.size());
+            }
+        });
+    for (auto& x : th) x.join();
+    int64_t total = 0;
+    for (auto v : tot) total += v;
     return total;
 }
 

@@ -13,6 +13,7 @@
 #include <numeric>
 #include <set>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -310,14 +311,50 @@ static inline uint32_t point_distance(const uint8_t* a, const uint8_t* b, int D,
     return acc;
 }
 
+// Exact top-k by a plain scan: every entry's packed (distance, key) against a bounded max-heap
+// (insert iff < the k-th value of a full heap, the knn_list rule of zcurve.cpp:33-49).  Large
+// inputs are split over host threads, each with its own heap, and merged: the packed values are
+// unique, so the result does not depend on the split.
+static void knn_scan_range(const uint8_t* coords, const uint32_t* keys, int64_t b, int64_t e, int D,
+                           const uint8_t* query, size_t keep, int norm, std::vector<uint64_t>& heap) {
+    heap.clear();
+    heap.reserve(keep + 1);
+    for (int64_t i = b; i < e; ++i) {
+        const uint64_t c =
+            (static_cast<uint64_t>(point_distance(query, coords + static_cast<size_t>(i) * D, D, norm)) << 32) | keys[i];
+        if (heap.size() < keep) {
+            heap.push_back(c);
+            std::push_heap(heap.begin(), heap.end());
+        } else if (c < heap.front()) {
+            std::pop_heap(heap.begin(), heap.end());
+            heap.back() = c;
+            std::push_heap(heap.begin(), heap.end());
+        }
+    }
+}
+
 int64_t zo_knn_linear(const uint8_t* coords, const uint32_t* keys, int64_t n, int D,
                       const uint8_t* query, int64_t k, int norm, uint64_t* out) {
-    std::vector<uint64_t> packed(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i)
-        packed[i] = (static_cast<uint64_t>(point_distance(query, coords + static_cast<size_t>(i) * D, D, norm)) << 32) | keys[i];
     const int64_t keep = std::min<int64_t>(std::max<int64_t>(k, 1), n);
-    std::partial_sort(packed.begin(), packed.begin() + keep, packed.end());
-    std::memcpy(out, packed.data(), static_cast<size_t>(keep) * sizeof(uint64_t));
+    if (keep <= 0) return 0;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int T = n >= (1 << 20) ? static_cast<int>(std::min<unsigned>(hw, 32)) : 1;
+    std::vector<std::vector<uint64_t>> heaps(T);
+    if (T == 1) {
+        knn_scan_range(coords, keys, 0, n, D, query, static_cast<size_t>(keep), norm, heaps[0]);
+    } else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                knn_scan_range(coords, keys, n * t / T, n * (t + 1) / T, D, query, static_cast<size_t>(keep), norm,
+                               heaps[t]);
+            });
+        for (auto& x : th) x.join();
+    }
+    std::vector<uint64_t> all;
+    for (auto& hp : heaps) all.insert(all.end(), hp.begin(), hp.end());
+    std::partial_sort(all.begin(), all.begin() + keep, all.end());
+    std::memcpy(out, all.data(), static_cast<size_t>(keep) * sizeof(uint64_t));
     return keep;
 }
 
@@ -481,7 +518,8 @@ extern "C" {
 
 // proj/src/builder.cpp:129-224 (build_index x 8 over one dictionary)
 zo_mi* zo_mi_build(const uint8_t* img, const uint8_t* known, int w, int h, int C, int K,
-                   double coverage, int dims, const double* pca_mean, const double* pca_comp) {
+                   double coverage, int dims, const double* pca_mean, const double* pca_comp,
+                   int layout_mask, int threads) {
     auto mi = new zo_mi();
     mi->w = w; mi->h = h; mi->C = C; mi->K = K; mi->coverage = coverage;
     mi->m = zo_subset_pixel_count(K, coverage);
@@ -501,7 +539,11 @@ zo_mi* zo_mi_build(const uint8_t* img, const uint8_t* known, int w, int h, int C
         S.resize(static_cast<size_t>(F) * F);
         zo_patch_moments(img, w, h, C, K, mi->dictionary.data(), n, s.data(), S.data());
     }
-    for (int l = 0; l < 8; ++l) {
+    std::vector<int> todo;
+    for (int l = 0; l < 8; ++l)
+        if (layout_mask & (1 << l)) todo.push_back(l);
+    std::vector<int> failed(8, 0);
+    auto build_layout = [&](int l) {
         auto& L = mi->idx[l];
         const int* rc = mi->rc.data() + static_cast<size_t>(l) * mi->m * 2;
         L.mean.resize(mi->mc);
@@ -518,8 +560,8 @@ zo_mi* zo_mi_build(const uint8_t* img, const uint8_t* known, int w, int h, int C
             std::vector<double> cov(static_cast<size_t>(mi->mc) * mi->mc);
             zo_layout_covariance(s.data(), S.data(), F, n, cols.data(), mi->mc, L.mean.data(), cov.data());
             if (zo_pca_from_cov(cov.data(), mi->mc, mi->dims, L.comp.data(), L.eig.data()) != 0) {
-                delete mi;
-                return nullptr;
+                failed[l] = 1;
+                return;
             }
         }
         L.lo.resize(mi->dims);
@@ -530,7 +572,24 @@ zo_mi* zo_mi_build(const uint8_t* img, const uint8_t* known, int w, int h, int C
         L.coords.resize(coords.size());
         L.keys.resize(static_cast<size_t>(n));
         zo_from_descriptors(coords.data(), mi->dictionary.data(), n, mi->dims, L.coords.data(), L.keys.data());
+    };
+    const int T = std::max(1, std::min<int>(threads, static_cast<int>(todo.size())));
+    if (T == 1) {
+        for (int l : todo) build_layout(l);
+    } else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                for (size_t i = t; i < todo.size(); i += T) build_layout(todo[i]);
+            });
+        for (auto& x : th) x.join();
     }
+    for (int l = 0; l < 8; ++l)
+        if (failed[l]) {
+            set_err("pca: eigen-solve failed");
+            delete mi;
+            return nullptr;
+        }
     return mi;
 }
 
@@ -688,7 +747,8 @@ extern "C" {
 // proj/src/engine.cpp:371-506 (run_loop + inpaint)
 int64_t zo_inpaint(const zo_mi* mi, const uint8_t* img0, const uint8_t* known0, int w, int h,
                    int C, int K, int64_t knn, int norm, int brute_force, int oracle,
-                   int64_t oracle_stride, uint8_t* img_out, zo_record* records, int64_t cap) {
+                   int64_t oracle_stride, uint8_t* img_out, zo_record* records, int64_t cap,
+                   int64_t max_iter) {
     std::vector<uint8_t> img(img0, img0 + static_cast<size_t>(w) * h * C);
     std::vector<uint8_t> known(known0, known0 + static_cast<size_t>(w) * h);
     size_t unknown_left = 0;
@@ -707,7 +767,7 @@ int64_t zo_inpaint(const zo_mi* mi, const uint8_t* img0, const uint8_t* known0, 
     fill_driver drv(img, known, w, h, C, K);
     std::vector<uint8_t> tv(static_cast<size_t>(K) * K * C), tk(static_cast<size_t>(K) * K);
     int64_t it = 0;
-    while (unknown_left > 0) {
+    while (unknown_left > 0 && (max_iter <= 0 || it < max_iter)) {
         if (drv.queue.empty()) { set_err("inpaint: unknown pixels unreachable from the fillfront"); return -1; }
         const uint32_t pos = drv.queue.begin()->second;
         const int tx = static_cast<int>(pos % w), ty = static_cast<int>(pos / w);

@@ -97,9 +97,13 @@ double zo_compute_priority(const uint8_t* img, const uint8_t* known, int w, int 
 /* ---- multi-index + fill loop ---- */
 typedef struct zo_mi zo_mi;
 /* pca_mean: 8*mc doubles, pca_comp: 8*D*mc doubles (row-major per layout) or NULL for the
- * oracle's own Jacobi fit.  Returns NULL on error (zo_error() tells why). */
+ * oracle's own Jacobi fit.  layout_mask: bit l set -> build layout l (0xff: all eight; the
+ * others stay empty); threads: layouts built concurrently (the reference builds the eight
+ * indices on its priority_pool, proj/src/builder.cpp:212-218; results do not depend on it).
+ * Returns NULL on error (zo_error() tells why). */
 zo_mi* zo_mi_build(const uint8_t* img, const uint8_t* known, int w, int h, int C, int K,
-                   double coverage, int dims, const double* pca_mean, const double* pca_comp);
+                   double coverage, int dims, const double* pca_mean, const double* pca_comp,
+                   int layout_mask, int threads);
 void zo_mi_free(zo_mi* mi);
 int64_t zo_mi_size(const zo_mi* mi);
 int zo_mi_dims(const zo_mi* mi);
@@ -127,10 +131,13 @@ typedef struct {
 } zo_record;
 
 /* inpaint / run_loop (proj/src/engine.cpp:371-506).  mi may be NULL when brute_force.
+ * max_iter > 0 stops after that many iterations (a prefix of the full run; img_out then holds
+ * the partially filled picture) -- test-only, the reference always runs to completion.
  * Returns number of records (iterations) or -1 (error; zo_error()). */
 int64_t zo_inpaint(const zo_mi* mi, const uint8_t* img, const uint8_t* known, int w, int h,
                    int C, int K, int64_t knn, int norm, int brute_force, int oracle,
-                   int64_t oracle_stride, uint8_t* img_out, zo_record* records, int64_t cap);
+                   int64_t oracle_stride, uint8_t* img_out, zo_record* records, int64_t cap,
+                   int64_t max_iter);
 
 /* cfg5 vector index, in the canonical fp64 order of paper_1712_06326_b200/csrc/k_vector.cu:
  * column sums and the Gram as row-ordered chains inside stripes of `stripe` rows, stripe
