@@ -1,7 +1,9 @@
 #!/usr/bin/env python
-"""Headline benchmark: 8-layout SFC multi-index build ("dictionary patches indexed/s") on the
-BASELINE.json config the metric is quoted on (configs[1] = cfg2: 1024^2 RGB, 11x11x3 patches,
-D=12, 12 disk holes), synthetic seeded input.
+"""Headline benchmark: 8-layout SFC multi-index build ("dictionary patches indexed/s").
+BASELINE.json's metric names no config, so the N=1 line runs the largest single-GPU config:
+configs[3] = cfg4 (4096^2 u16-range value noise -> u8, 9x9 patches, D=8, 5% of the 16x16 blocks
+removed, n = 14.9 M dictionary patches), synthetic seeded input; cfg2
+(configs[1]) and cfg1 stay available through --config.
 
 One step = multi_index::build (proj/src/builder.cpp:202-224) of one image already resident in
 HBM: dictionary collection, exact PCA moments (int8 tensor cores), the 8 eigen-solves on the
@@ -43,7 +45,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4"])
+    p.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg4"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-inpaint", action="store_true")
     p.add_argument("--no-knn", action="store_true")
@@ -110,12 +112,55 @@ def cpu_build_sample(img, known, p, n_sample: int, threads: int):
     return n / dt, dt, kind, sample
 
 
+BUILD_SAMPLE = {"cfg1": 58368, "cfg2": 131072, "cfg4": 262144}
+
+
+def cpu_inpaint_baseline(mi, img, known, p, max_iter: int):
+    """The reference's fill loop on the host: the restated run_loop (engine.cpp:371-438; priorities,
+    std::set order, make_query, masked-cost refine, paste) whose k-NN queries go to the reference's
+    OWN compiled knn_search (zcurve.cpp:429-452) over its own zcurve_index per layout, on a
+    priority_pool of nproc - 1 threads (run_loop's default workers = cores, engine.cpp:454-458).
+    The 8 indices are the device build's (bit-identical to the reference's, tests/test_gpu_scale.py),
+    re-sorted by the compiled from_descriptors; timed over the first max_iter iterations."""
+    import oracle
+    K, D = p["patch_size"], mi.dims
+    pm = np.stack([mi.layout(l)["mean"] for l in range(8)])
+    pc = np.stack([mi.layout(l)["components"] for l in range(8)])
+    om = oracle.MultiIndex(img, known, K, 0.6, D, pca_mean=pm, pca_comp=pc, layouts=[])
+    for l in range(8):
+        lay = mi.layout(l)
+        c, k = mi.index_arrays(l)
+        om.set_layout(l, lay["mean"], lay["components"], lay["lo"], lay["hi"], c, k)
+    workers = om.use_reference_knn()
+    t0 = time.perf_counter()
+    _, recs = oracle.inpaint(img, known, K, 0.6, D, knn=p["knn"], mi=om, max_iter=max_iter)
+    dt = time.perf_counter() - t0
+    return {"value": len(recs) / dt, "unit": "iterations/s", "cores": workers, "kind": "reference",
+            "seconds": dt, "iterations": int(len(recs)),
+            "sample": f"the first {len(recs)} fill-loop iterations of this config; query = the reference's compiled "
+                      f"knn_search (mu=256, nu=2048) on priority_pool({workers - 1}), fill loop / make_query / refine "
+                      f"= oracle restatement of engine.cpp (Eigen absent)"}
+
+
+def cpu_brute_baseline(img, targets, keys, K, n_queries: int = 2):
+    """The reference's brute_force_best (engine.cpp:220-236) is single-threaded: the restated scan
+    over the whole dictionary, timed on the first n_queries targets."""
+    import oracle
+    t0 = time.perf_counter()
+    for tv, tk in targets[:n_queries]:
+        oracle.brute_force_best(img, tv, tk, K, keys)
+    dt = (time.perf_counter() - t0) / n_queries
+    return {"value": 1.0 / dt, "unit": "queries/s", "cores": 1, "kind": "port", "us_per_query": dt * 1e6,
+            "sample": f"{n_queries} of the {len(targets)} targets, whole dictionary ({keys.size} patches), "
+                      f"restated single-thread brute_force_best"}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
     img, known, p = workload(args.config, 0)
     threads = max(1, min(8, os.cpu_count() or 1))
-    n_sample = 131072 if args.config != "cfg1" else 58368
+    n_sample = BUILD_SAMPLE[args.config]
     for _ in range(args.warmup):
         cpu_build_sample(img, known, p, n_sample, threads)
     vals = []
@@ -128,8 +173,10 @@ def run_reference(args, rank):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u8",
-            "data": "synthetic", "config": {"workload": f"{args.config} (BASELINE.json configs[1]) sample",
-                                            "parallelism": "cpu threads"},
+            "data": "synthetic", "config": {"workload": f"{args.config}: bounded sample of its dictionary "
+                                                        f"({n_sample} patches x 8 layouts per step)",
+                                            "parallelism": f"cpu threads x{threads} (one per layout, "
+                                                           f"multi_index::build's pool)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -606,11 +653,18 @@ def main():
         ctx.set_profiling(False)
         it = max(int(st.iterations), 1)
         inpaint = {"iterations": int(st.iterations), "seconds": dt, "iterations_per_s": st.iterations / dt,
+                   "first_2000_iterations_per_s": min(2000, len(recs)) / float(np.sum(recs["elapsed_seconds"][:2000])),
                    "unit": "iterations/s", "mean_iteration_us": 1e6 * float(np.mean(recs["elapsed_seconds"])),
                    "device_us_per_iteration": {k: 1e3 * v[0] / it for k, v in kp.items()},
                    "note": "sequential fill loop over the built index (host priorities + one device query "
                            "per iteration), through MultiIndex.inpaint / zi_inpaint_with_index; the faster of "
-                           "two runs (the host part varies by ~15 % between runs)"}
+                           "two runs (the host part varies by ~15 % between runs); first_2000_iterations_per_s sums "
+                           "the per-iteration wall times of the first 2000 (the CPU baseline's sample)"}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                inpaint["cpu_baseline"] = cpu_inpaint_baseline(mi, img, known, p, 2000)
+            except Exception as ex:  # noqa: BLE001
+                inpaint["cpu_baseline"] = {"error": repr(ex)}
 
     # -------- the exhaustive masked-L2 scan (brute_force_best, the original method's comparison
     # path, proj/src/engine.cpp:220-236) over the whole dictionary, rank 0
@@ -636,15 +690,30 @@ def main():
         for tv, tk in targets:
             mi.brute_force_best(tv, tk)
         dt = (time.perf_counter() - t0) / len(targets)
+        ctx.set_profile_filter(["brute_force"])  # device time of the scan kernel alone
+        ctx.set_profiling(True)
+        for tv, tk in targets:
+            mi.brute_force_best(tv, tk)
+        bp = ctx.profile().get("brute_force", (0.0, 1))
+        ctx.set_profiling(False)
+        ctx.set_profile_filter(None)
+        dev_dt = bp[0] * 1e-3 / max(bp[1], 1)
         C = 1 if img.ndim == 2 else img.shape[2]
         known_vals = float(np.mean([int(tk.sum()) for _, tk in targets])) * C
         ops = 3.0 * n * known_vals  # subtract, square (multiply-add) per known value, per dictionary patch
         int_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12  # TOPS, nominal INT32 rate
-        brute = {"queries_per_s": 1.0 / dt, "us_per_query": dt * 1e6, "dictionary": n,
-                 "mean_known_values": known_vals, "int_ops_per_query": ops,
-                 "achieved_TOPS": ops / dt / 1e12, "int32_peak_TOPS": int_peak, "frac_of_int32": ops / dt / 1e12 / int_peak,
-                 "note": "host wall time per zi_brute_force_best call (H2D of the target, one scan kernel, D2H of "
-                         "the packed winner); INT-compute-bound, not an HBM roofline (SURVEY.md §8(d))"}
+        brute = {"queries_per_s": 1.0 / dt, "us_per_query": dt * 1e6, "device_us_per_query": dev_dt * 1e6,
+                 "dictionary": n, "mean_known_values": known_vals, "int_ops_per_query": ops,
+                 "achieved_TOPS": ops / dev_dt / 1e12, "int32_peak_TOPS": int_peak,
+                 "frac_of_int32": ops / dev_dt / 1e12 / int_peak,
+                 "note": "queries_per_s / us_per_query: host wall time per zi_brute_force_best call (target H2D, "
+                         "one scan kernel, winner D2H); achieved_TOPS from the kernel's own CUDA-event time. "
+                         "INT-compute-bound, not an HBM roofline (SURVEY.md §8(d))"}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                brute["cpu_baseline"] = cpu_brute_baseline(img, targets, mi.dictionary, K)
+            except Exception as ex:  # noqa: BLE001
+                brute["cpu_baseline"] = {"error": repr(ex)}
 
     knn = None
     if rank == 0 and not args.no_knn:
@@ -664,7 +733,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = max(1, min(8, os.cpu_count() or 1))
-            v, dt, kind, sample = cpu_build_sample(img, known, p, 131072 if args.config != "cfg1" else n, threads)
+            v, dt, kind, sample = cpu_build_sample(img, known, p, min(BUILD_SAMPLE[args.config], n), threads)
             cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample, "seconds": dt}
         except Exception as ex:  # noqa: BLE001
             cpu = {"error": repr(ex)}

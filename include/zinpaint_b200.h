@@ -103,6 +103,7 @@ typedef struct {
 } zi_multi_index_info;
 
 typedef struct zi_ctx zi_ctx;                 /* one device + one stream + scratch */
+typedef struct zi_patch_index zi_patch_index; /* patch_index (proj/include/zinpaint/builder.hpp:60-75) */
 typedef struct zi_index zi_index;             /* zcurve_index (proj/include/zinpaint/zcurve.hpp:117-145) */
 typedef struct zi_multi_index zi_multi_index; /* multi_index (proj/include/zinpaint/builder.hpp:84-92) */
 
@@ -133,6 +134,9 @@ int zi_morton_less(const uint8_t* a, const uint8_t* b, uint32_t dims);   /* mort
 int zi_subset_pixel_count(int patch_size, double coverage);             /* layouts.cpp:9-11 */
 /* build_subset_layouts (layouts.cpp:13-60); rc_out holds 8*m*2 int32 (row, col) */
 zi_status zi_subset_layouts(int patch_size, double coverage, int32_t* rc_out, int32_t* m_out);
+/* subset_layout::anchor of layouts 0..7 (layouts.cpp: N, E, S, W edge midpoints, then NW, NE, SW,
+ * SE corners); rc_out holds 8*2 int32 (row, col) */
+zi_status zi_subset_layout_anchors(int patch_size, int32_t* rc_out);
 zi_status zi_index_config_validate(const zi_index_config* cfg, int channels); /* builder.cpp:38-53 */
 void zi_index_config_default(zi_index_config* cfg);
 
@@ -184,6 +188,38 @@ zi_status zi_multi_index_layout_index(zi_multi_index* mi, int32_t layout, uint8_
                                       uint32_t* keys_out);
 /* borrowed view of one layout's zcurve_index (valid until mi is destroyed or rebuilt) */
 zi_status zi_multi_index_get_index(zi_multi_index* mi, int32_t layout, zi_index** out);
+/* ---- one layout: build_index (builder.hpp:77-81, builder.cpp:129-195) ----
+ * The reference's per-layout entry point over a caller-given dictionary (keys packed y<<16|x,
+ * every window inside the image) and subset layout (layout_rc: m (row, col) pairs).  The PCA fit
+ * (moments of the dictionary restricted to the layout, pca.cpp:20-67), projection, quantiser and
+ * Morton sort run on the device.  Errors: ZI_E_INVALID (config / layout / window outside the
+ * image), ZI_E_EMPTY_DICT (n == 0). */
+zi_status zi_index_build(zi_ctx* ctx, const uint8_t* image, int32_t width, int32_t height, int32_t channels,
+                         const uint32_t* keys, uint64_t n, const int32_t* layout_rc, int32_t m,
+                         const zi_index_config* cfg, zi_patch_index** out);
+zi_status zi_patch_index_destroy(zi_patch_index* pi);
+/* patch_index fields: dims (effective D), mc (= m*channels); mean (mc), components (dims rows of
+ * mc), eigenvalues (dims), quantizer lo / hi (dims); build_seconds (device time of the whole
+ * build) and sort_seconds (the sort + finalize).  NULL pointers are skipped. */
+zi_status zi_patch_index_model(const zi_patch_index* pi, int32_t* dims, int32_t* mc, double* mean, double* components,
+                               double* eigenvalues, double* lo, double* hi, double* build_seconds,
+                               double* sort_seconds);
+/* borrowed view of the layout's zcurve_index (valid until pi is destroyed) */
+zi_status zi_patch_index_get_index(zi_patch_index* pi, zi_index** out);
+/* patch_index::make_query (builder.hpp:72, builder.cpp:110-127): target K*K*C values + K*K known
+ * flags -> dims quantised bytes; unknown layout pixels take the PCA mean.  On the device, in the
+ * canonical fp64 order of the build. */
+zi_status zi_make_query(zi_patch_index* pi, const uint8_t* target_values, const uint8_t* target_known, uint8_t* out);
+/* the same for layout `layout` of a multi-index (multi_index::indices[layout].make_query) */
+zi_status zi_multi_index_make_query(zi_multi_index* mi, int32_t layout, const uint8_t* target_values,
+                                    const uint8_t* target_known, uint8_t* out);
+/* brute_force_best(image, target, dictionary, norm) (engine.hpp:98-99, engine.cpp:220-236) over a
+ * caller-given image and dictionary (uploaded per call; the multi-index form below reuses the
+ * device-resident ones).  An empty dictionary returns cost 0xffffffff. */
+zi_status zi_brute_force_scan(zi_ctx* ctx, const uint8_t* image, int32_t width, int32_t height, int32_t channels,
+                              const uint32_t* keys, uint64_t n, const uint8_t* target_values,
+                              const uint8_t* target_known, int32_t patch_size, int32_t norm, zi_best_patch* out);
+
 /* ---- cfg5: index over fp32 feature vectors (BASELINE.json configs[4]) ----
  * The reference's patch-index semantics with every coordinate a pixel: PCA fit (pca.cpp:20-67,
  * canonical fp64 order in 32768-row stripes), project + quantise (builder.cpp:55-72,159-187),

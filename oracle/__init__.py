@@ -106,6 +106,8 @@ def lib():
         L.zo_mi_build.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                   _f64p, _f64p, C.c_int, C.c_int]
         L.zo_mi_free.argtypes = [C.c_void_p]
+        L.zo_mi_set_knn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.zo_mi_set_layout.argtypes = [C.c_void_p, C.c_int, _f64p, _f64p, _f64p, _f64p, _u8p, _u32p]
         for fn in ("zo_mi_size",):
             getattr(L, fn).restype = C.c_int64
             getattr(L, fn).argtypes = [C.c_void_p]
@@ -156,6 +158,9 @@ def ref():
         R.zr_index_knn_batch_mt.restype = C.c_int64
         R.zr_index_knn_batch_mt.argtypes = [C.c_void_p, _u8p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
                                             C.c_int, _u64p, _u32p]
+        R.zr_hook_create.restype = C.c_void_p
+        R.zr_hook_create.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int]
+        R.zr_hook_free.argtypes = [C.c_void_p]
         R.zr_extract_patch_clamped.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                                C.c_int, _u8p, _u8p]
         R.zr_fillfront.restype = C.c_int64
@@ -325,6 +330,20 @@ def knn_linear(coords, keys, query, k, norm=L2):
     return out[:cnt].copy()
 
 
+def make_query(tv, tk, K, C, rc, mean, comp, lo, hi):
+    """patch_index::make_query (proj/src/builder.cpp:110-127): D quantised bytes."""
+    tv, tk = _u8(tv), _u8(tk)
+    rc = np.ascontiguousarray(rc, dtype=np.int32)
+    comp = np.ascontiguousarray(comp, dtype=np.float64)
+    D = comp.shape[0]
+    out = np.zeros(D, dtype=np.uint8)
+    lib().zo_make_query(_p(tv, _u8p), _p(tk, _u8p), K, C, _p(rc, _ip), rc.shape[0],
+                        _p(np.ascontiguousarray(mean, dtype=np.float64), _f64p), _p(comp, _f64p),
+                        _p(np.ascontiguousarray(lo, dtype=np.float64), _f64p),
+                        _p(np.ascontiguousarray(hi, dtype=np.float64), _f64p), D, _p(out, _u8p))
+    return out
+
+
 def masked_cost_at(img, tv, tk, K, key, norm=L2):
     img, w, h, ch = _img_dims(img)
     tv, tk = _u8(tv), _u8(tk)
@@ -407,6 +426,10 @@ class MultiIndex:
         if h:
             lib().zo_mi_free(h)
             self.h_ = None
+        hk = getattr(self, "_hook", None)
+        if hk:
+            ref().zr_hook_free(hk)
+            self._hook = None
 
     def dictionary(self):
         out = np.zeros(self.n, dtype=np.uint32)
@@ -427,6 +450,37 @@ class MultiIndex:
         keys = np.zeros(self.n, dtype=np.uint32)
         L.zo_mi_index(self.h_, l, _p(coords, _u8p), _p(keys, _u32p))
         return LayoutIndex(rc, mean, comp, eig, lo, hi, coords, keys)
+
+    def set_layout(self, l, mean, comp, lo, hi, coords, keys):
+        """Replace layout l's model, quantiser and sorted index (e.g. with a device build's)."""
+        self._keep = getattr(self, "_keep", {})
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (mean, comp, lo, hi)]
+        coords = np.ascontiguousarray(coords, dtype=np.uint8)
+        keys = np.ascontiguousarray(keys, dtype=np.uint32)
+        lib().zo_mi_set_layout(self.h_, l, *[_p(a, _f64p) for a in arrs], _p(coords, _u8p), _p(keys, _u32p))
+
+    def use_reference_knn(self, workers=None, mu=256, nu=2048):
+        """Answer the fill loop's k-NN queries with the reference's compiled knn_search over its own
+        zcurve_index per layout (built by the compiled from_descriptors from this index's arrays),
+        on a priority_pool of workers - 1 threads (run_loop's default: workers = host cores)."""
+        import threading
+        workers = workers or (os.cpu_count() or 1)
+        refs = [None] * 8
+        def mk(l):
+            ix = self.index(l)
+            refs[l] = RefIndex(ix.coords, ix.keys)
+        th = [threading.Thread(target=mk, args=(l,)) for l in range(8)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        handles = (C.c_void_p * 8)(*[r.h_ for r in refs])
+        self._refs = refs
+        self._hook = ref().zr_hook_create(handles, workers, mu, nu)
+        fn = C.cast(ref().zr_hook_knn, C.c_void_p)
+        lib().zo_mi_set_knn(self.h_, fn, self._hook)
+        self._hook_fn = fn
+        return workers
 
     def query_best_patch(self, img, tv, tk, k, norm=L2):
         img = _u8(img)

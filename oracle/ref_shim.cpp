@@ -149,6 +149,37 @@ int64_t zr_index_knn_batch_mt(void* h, const uint8_t* queries, int64_t nq, int k
     return total;
 }
 
+// k-NN hook for the restated fill loop (zoracle.h zo_knn_fn): the reference's knn_search over its
+// own zcurve_index per layout, on a priority_pool of `workers - 1` background threads like
+// run_loop's (engine.cpp:454-458); mu / nu as in index_config.
+struct zr_hook {
+    zcurve_index* idx[8];
+    std::unique_ptr<priority_pool> pool;
+    search_params sp;
+};
+
+void* zr_hook_create(void* const* idx8, int workers, int mu, int nu) {
+    auto* h = new zr_hook();
+    for (int l = 0; l < 8; ++l) h->idx[l] = static_cast<zcurve_index*>(idx8[l]);
+    if (workers > 1) h->pool = std::make_unique<priority_pool>(static_cast<unsigned>(workers - 1));
+    h->sp.mu = static_cast<uint32_t>(mu);
+    h->sp.nu = static_cast<uint32_t>(nu);
+    h->sp.pool = h->pool.get();
+    return h;
+}
+
+void zr_hook_free(void* h) { delete static_cast<zr_hook*>(h); }
+
+int64_t zr_hook_knn(void* user, int layout, const uint8_t* query, int64_t k, int norm, uint64_t* out) {
+    auto* h = static_cast<zr_hook*>(user);
+    search_params sp = h->sp;
+    sp.k = static_cast<uint32_t>(k);
+    sp.norm = norm == 0 ? norm_kind::l2 : norm_kind::l1;
+    const auto found = knn_search(*h->idx[layout], query, sp);
+    for (size_t i = 0; i < found.size(); ++i) out[i] = pack_candidate(found[i].distance, found[i].key);
+    return static_cast<int64_t>(found.size());
+}
+
 // extract_patch_clamped (proj/src/image.cpp:44-47)
 void zr_extract_patch_clamped(const uint8_t* img, const uint8_t* known, int w, int h, int C, int cx,
                               int cy, int K, uint8_t* tv, uint8_t* tk) {

@@ -512,6 +512,8 @@ struct zo_mi {
         std::vector<uint8_t> coords;
         std::vector<uint32_t> keys;
     } idx[8];
+    zo_knn_fn knn_fn = nullptr;  // optional k-NN of a layout (the compiled reference's knn_search)
+    void* knn_user = nullptr;
 };
 
 extern "C" {
@@ -594,6 +596,24 @@ zo_mi* zo_mi_build(const uint8_t* img, const uint8_t* known, int w, int h, int C
 }
 
 void zo_mi_free(zo_mi* mi) { delete mi; }
+
+void zo_mi_set_knn(zo_mi* mi, zo_knn_fn fn, void* user) {
+    mi->knn_fn = fn;
+    mi->knn_user = user;
+}
+
+void zo_mi_set_layout(zo_mi* mi, int l, const double* mean, const double* comp, const double* lo, const double* hi,
+                      const uint8_t* coords, const uint32_t* keys) {
+    auto& L = mi->idx[l];
+    const size_t n = mi->dictionary.size(), D = static_cast<size_t>(mi->dims), mc = static_cast<size_t>(mi->mc);
+    L.mean.assign(mean, mean + mc);
+    L.comp.assign(comp, comp + D * mc);
+    L.eig.assign(D, 0.0);
+    L.lo.assign(lo, lo + D);
+    L.hi.assign(hi, hi + D);
+    L.coords.assign(coords, coords + n * D);
+    L.keys.assign(keys, keys + n);
+}
 int64_t zo_mi_size(const zo_mi* mi) { return static_cast<int64_t>(mi->dictionary.size()); }
 int zo_mi_dims(const zo_mi* mi) { return mi->dims; }
 int zo_mi_mc(const zo_mi* mi) { return mi->mc; }
@@ -630,7 +650,9 @@ uint64_t zo_mi_query_best_patch(const zo_mi* mi, const uint8_t* img, const uint8
                   L.comp.data(), L.lo.data(), L.hi.data(), mi->dims, q.data());
     const int64_t n = static_cast<int64_t>(L.keys.size());
     std::vector<uint64_t> cand(static_cast<size_t>(std::min<int64_t>(std::max<int64_t>(k, 1), n)));
-    const int64_t cnt = zo_knn_linear(L.coords.data(), L.keys.data(), n, mi->dims, q.data(), k, norm, cand.data());
+    const int64_t cnt = mi->knn_fn ? mi->knn_fn(mi->knn_user, lid, q.data(), k, norm, cand.data())
+                                   : zo_knn_linear(L.coords.data(), L.keys.data(), n, mi->dims, q.data(), k, norm,
+                                                   cand.data());
     uint64_t best = ~0ull;
     for (int64_t i = 0; i < cnt; ++i) {
         const uint32_t key = static_cast<uint32_t>(cand[i] & 0xffffffffu);

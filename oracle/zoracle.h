@@ -105,6 +105,14 @@ zo_mi* zo_mi_build(const uint8_t* img, const uint8_t* known, int w, int h, int C
                    double coverage, int dims, const double* pca_mean, const double* pca_comp,
                    int layout_mask, int threads);
 void zo_mi_free(zo_mi* mi);
+/* k-NN of layout `layout` for the fill loop: packed (dist<<32|key) ascending into out, returns the
+ * count.  Default (fn NULL): the linear scan.  bench.py plugs in the compiled reference's
+ * knn_search (oracle/_ref, zr_hook_knn) to time the reference's own fill loop query. */
+typedef int64_t (*zo_knn_fn)(void* user, int layout, const uint8_t* query, int64_t k, int norm, uint64_t* out);
+void zo_mi_set_knn(zo_mi* mi, zo_knn_fn fn, void* user);
+/* replace layout l's model, quantiser and sorted index (n = dictionary size entries) */
+void zo_mi_set_layout(zo_mi* mi, int l, const double* mean, const double* comp, const double* lo,
+                      const double* hi, const uint8_t* coords, const uint32_t* keys);
 int64_t zo_mi_size(const zo_mi* mi);
 int zo_mi_dims(const zo_mi* mi);
 int zo_mi_mc(const zo_mi* mi);

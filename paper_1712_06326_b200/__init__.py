@@ -213,6 +213,72 @@ class ZCurveIndex:
         self.h = None
 
 
+class PatchIndex:
+    """build_index (proj/include/zinpaint/builder.hpp:77-81, proj/src/builder.cpp:129-195): ONE
+    layout index over a caller-given dictionary, fitted, projected and sorted on the device."""
+
+    def __init__(self, image, keys, layout_rc, cfg: Optional[IndexConfig] = None, ctx: Optional[Context] = None,
+                 **kw):
+        self.ctx = ctx or Context.default()
+        self.cfg = cfg if cfg is not None else index_config(**kw)
+        img = _u8(image)
+        self.height, self.width = img.shape[:2]
+        self.channels = 1 if img.ndim == 2 else img.shape[2]
+        keys = np.ascontiguousarray(keys, dtype=np.uint32)
+        rc = np.ascontiguousarray(layout_rc, dtype=np.int32).reshape(-1, 2)
+        self.m = rc.shape[0]
+        h = C.c_void_p()
+        check(lib().zi_index_build(self.ctx.h, ptr(img, u8p), self.width, self.height, self.channels,
+                                   ptr(keys, u32p), keys.size, ptr(rc, i32p), self.m, C.byref(self.cfg), C.byref(h)))
+        self.h = h
+        d, mc = C.c_int32(), C.c_int32()
+        check(lib().zi_patch_index_model(self.h, C.byref(d), C.byref(mc), None, None, None, None, None, None, None))
+        self.dims, self.mc, self.n = d.value, mc.value, keys.size
+
+    def model(self) -> dict:
+        D, mc = self.dims, self.mc
+        mean, comp, eig, lo, hi = np.zeros(mc), np.zeros((D, mc)), np.zeros(D), np.zeros(D), np.zeros(D)
+        bs, ss = C.c_double(), C.c_double()
+        check(lib().zi_patch_index_model(self.h, None, None, ptr(mean, f64p), ptr(comp, f64p), ptr(eig, f64p),
+                                         ptr(lo, f64p), ptr(hi, f64p), C.byref(bs), C.byref(ss)))
+        return {"mean": mean, "components": comp, "eigenvalues": eig, "lo": lo, "hi": hi,
+                "build_seconds": bs.value, "sort_seconds": ss.value}
+
+    def index(self) -> "ZCurveIndex":
+        h = C.c_void_p()
+        check(lib().zi_patch_index_get_index(self.h, C.byref(h)))
+        return ZCurveIndex(h, owner=self)
+
+    def make_query(self, target_values, target_known) -> np.ndarray:
+        """patch_index::make_query (proj/src/builder.cpp:110-127), on the device."""
+        tv, tk = _u8(target_values), _u8(target_known)
+        out = np.zeros(self.dims, dtype=np.uint8)
+        check(lib().zi_make_query(self.h, ptr(tv, u8p), ptr(tk, u8p), ptr(out, u8p)))
+        return out
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().zi_patch_index_destroy(h)
+            self.h = None
+
+
+def brute_force_scan(image, keys, target_values, target_known, patch_size: int, norm="l2",
+                     ctx: Optional[Context] = None):
+    """brute_force_best(image, target, dictionary, norm) (proj/src/engine.cpp:220-236) over a caller
+    dictionary -> (key, cost, error)."""
+    ctx = ctx or Context.default()
+    img = _u8(image)
+    h, w = img.shape[:2]
+    ch = 1 if img.ndim == 2 else img.shape[2]
+    keys = np.ascontiguousarray(keys, dtype=np.uint32)
+    tv, tk = _u8(target_values), _u8(target_known)
+    bp = BestPatch()
+    check(lib().zi_brute_force_scan(ctx.h, ptr(img, u8p), w, h, ch, ptr(keys, u32p), keys.size, ptr(tv, u8p),
+                                    ptr(tk, u8p), patch_size, _norm(norm), C.byref(bp)))
+    return bp.key, bp.cost, bp.error
+
+
 # ------------------------------------------------------------------ cfg5 vector index
 class VectorIndex:
     """Index over fp32 feature vectors (BASELINE configs[4]): PCA fit, projection, quantiser and
@@ -386,6 +452,13 @@ class MultiIndex:
         if return_candidates:
             return res, knn[:bp.candidates].copy()
         return res
+
+    def make_query(self, layout: int, target_values, target_known) -> np.ndarray:
+        """indices[layout].make_query (proj/src/builder.cpp:110-127), on the device."""
+        tv, tk = _u8(target_values), _u8(target_known)
+        out = np.zeros(self.dims, dtype=np.uint8)
+        check(lib().zi_multi_index_make_query(self.h, layout, ptr(tv, u8p), ptr(tk, u8p), ptr(out, u8p)))
+        return out
 
     def brute_force_best(self, target_values, target_known, norm=None):
         """brute_force_best (proj/src/engine.cpp:220-236) -> (key, cost, error)."""

@@ -77,6 +77,7 @@ SIGNATURES = {
     "zi_morton_less": (C.c_int, [u8p, u8p, C.c_uint32]),
     "zi_subset_pixel_count": (C.c_int, [C.c_int, C.c_double]),
     "zi_subset_layouts": (C.c_int, [C.c_int, C.c_double, i32p, i32p]),
+    "zi_subset_layout_anchors": (C.c_int, [C.c_int, i32p]),
     "zi_index_config_validate": (C.c_int, [C.POINTER(IndexConfig), C.c_int]),
     "zi_index_config_default": (None, [C.POINTER(IndexConfig)]),
     "zi_index_from_descriptors": (C.c_int, [vp, u8p, u32p, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(vp)]),
@@ -87,6 +88,15 @@ SIGNATURES = {
     "zi_knn_search_batch": (C.c_int, [vp, u8p, C.c_uint64, C.c_uint32, C.c_int32, u64p, C.POINTER(C.c_uint32)]),
     "zi_knn_batch_bench": (C.c_int, [vp, u8p, C.c_uint64, C.c_uint32, C.c_int32, C.c_int32, f64p, u64p, u64p,
                                      C.POINTER(C.c_uint32)]),
+    "zi_index_build": (C.c_int, [vp, u8p, C.c_int32, C.c_int32, C.c_int32, u32p, C.c_uint64, i32p, C.c_int32,
+                                 C.POINTER(IndexConfig), C.POINTER(vp)]),
+    "zi_patch_index_destroy": (C.c_int, [vp]),
+    "zi_patch_index_model": (C.c_int, [vp, i32p, i32p, f64p, f64p, f64p, f64p, f64p, f64p, f64p]),
+    "zi_patch_index_get_index": (C.c_int, [vp, C.POINTER(vp)]),
+    "zi_make_query": (C.c_int, [vp, u8p, u8p, u8p]),
+    "zi_multi_index_make_query": (C.c_int, [vp, C.c_int32, u8p, u8p, u8p]),
+    "zi_brute_force_scan": (C.c_int, [vp, u8p, C.c_int32, C.c_int32, C.c_int32, u32p, C.c_uint64, u8p, u8p,
+                                      C.c_int32, C.c_int32, C.POINTER(BestPatch)]),
     "zi_dictionary_collect": (C.c_int, [vp, u8p, C.c_int32, C.c_int32, C.c_int32, u32p, C.c_uint64, u64p]),
     "zi_multi_index_build": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig),
                                        C.POINTER(vp)]),

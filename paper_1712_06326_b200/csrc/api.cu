@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -38,21 +40,45 @@ void require(bool ok, const char* msg) {
     if (!ok) throw zi::error(ZI_E_INVALID, msg);
 }
 
-// guard() with the handle's stream bound for stream-ordered allocations
-struct stream_scope {
+// guard() with the handle's device current and its stream + pool bound for stream-ordered
+// allocations; the caller's current device is restored on exit
+struct ctx_scope {
     cudaStream_t prev;
-    explicit stream_scope(cudaStream_t s) : prev(zi::tls_alloc_stream) { zi::tls_alloc_stream = s; }
-    ~stream_scope() { zi::tls_alloc_stream = prev; }
+    cudaMemPool_t prev_pool;
+    int prev_dev = -1;
+    explicit ctx_scope(const zi_ctx* ctx) : prev(zi::tls_alloc_stream), prev_pool(zi::tls_alloc_pool) {
+        zi::tls_alloc_stream = ctx ? ctx->stream : nullptr;
+        zi::tls_alloc_pool = ctx ? ctx->pool : nullptr;
+        int d = -1;
+        if (ctx && cudaGetDevice(&d) == cudaSuccess && d != ctx->device && cudaSetDevice(ctx->device) == cudaSuccess)
+            prev_dev = d;
+    }
+    ~ctx_scope() {
+        zi::tls_alloc_stream = prev;
+        zi::tls_alloc_pool = prev_pool;
+        if (prev_dev >= 0) cudaSetDevice(prev_dev);
+    }
 };
 template <typename F>
 zi_status guard(const zi_ctx* ctx, F&& f) {
-    stream_scope sc(ctx ? ctx->stream : nullptr);
+    ctx_scope sc(ctx);
     return guard(std::forward<F>(f));
 }
 }  // namespace
 
 namespace zi {
 thread_local cudaStream_t tls_alloc_stream = nullptr;
+thread_local cudaMemPool_t tls_alloc_pool = nullptr;
+
+void set_smem_attr(const void* fn, int device, size_t bytes) {
+    static std::mutex mx;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    std::lock_guard<std::mutex> lk(mx);
+    size_t& have = done[{fn, device}];
+    if (bytes <= have) return;
+    ZI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    have = bytes;
+}
 }
 
 namespace zi {
@@ -169,10 +195,15 @@ zi_status zi_ctx_create(int device, zi_ctx** out) {
         ZI_CUDA(cudaGetDeviceProperties(&prop, device));
         c->num_sms = prop.multiProcessorCount;
         ZI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        cudaMemPool_t pool;
-        ZI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        // a private pool: the no-trim threshold applies to this ctx's allocations only, not to the
+        // device's default pool that other libraries in the process (torch, NCCL) allocate from
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        ZI_CUDA(cudaMemPoolCreate(&c->pool, &props));
         uint64_t keep = ~0ull;  // never trim: rebuilds reuse the pool's HBM
-        ZI_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        ZI_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
         ZI_CUDA(cudaEventCreate(&c->t0));
         ZI_CUDA(cudaEventCreate(&c->t1));
         *out = c;
@@ -196,6 +227,7 @@ zi_status zi_ctx_destroy(zi_ctx* ctx) {
         ctx->gm_wtab.release();
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
+        if (ctx->pool) cudaMemPoolDestroy(ctx->pool);  // released once its last allocation is freed
         delete ctx;
     });
 }
@@ -300,6 +332,14 @@ zi_status zi_subset_layouts(int patch_size, double coverage, int32_t* rc_out, in
         const int m = zi::subset_layouts(patch_size, coverage, rc);
         if (rc_out) std::memcpy(rc_out, rc.data(), rc.size() * sizeof(int32_t));
         if (m_out) *m_out = m;
+    });
+}
+
+zi_status zi_subset_layout_anchors(int patch_size, int32_t* rc_out) {
+    return guard([&] {
+        require(rc_out != nullptr, "null argument");
+        if (patch_size < 3 || patch_size % 2 == 0) throw zi::error(ZI_E_INVALID, "subset layouts: K must be odd and >= 3");
+        zi::layout_anchors(patch_size, rc_out);
     });
 }
 
@@ -486,6 +526,157 @@ zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t*
             throw;
         }
         *out = mi;
+    });
+}
+
+// ---------------------------------------------------------------- one layout (build_index)
+zi_status zi_index_build(zi_ctx* ctx, const uint8_t* image, int32_t w, int32_t h, int32_t C, const uint32_t* keys,
+                         uint64_t n, const int32_t* layout_rc, int32_t m, const zi_index_config* cfg,
+                         zi_patch_index** out) {
+    return guard(ctx, [&] {
+        require(ctx && image && keys && layout_rc && cfg && out, "null argument");
+        require(w > 0 && h > 0 && (C == 1 || C == 3), "raster_image: bad dimensions");
+        require(w <= 65535 && h <= 65535, "image side above the 16-bit patch_key range");
+        zi::validate_config(*cfg, C);
+        if (n == 0) throw zi::error(ZI_E_EMPTY_DICT, "build_index: empty dictionary");
+        require(n < (1ull << 29), "build_index: dictionary above 2^29 patches");
+        const int K = cfg->patch_size;
+        require(m >= 1 && m <= K * K, "build_index: layout pixel count out of range");
+        for (int p = 0; p < m; ++p)
+            require(layout_rc[2 * p] >= 0 && layout_rc[2 * p] < K && layout_rc[2 * p + 1] >= 0 &&
+                        layout_rc[2 * p + 1] < K,
+                    "build_index: layout offset outside the patch");
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint32_t x = keys[i] & 0xffffu, y = keys[i] >> 16;
+            require(x + K <= static_cast<uint32_t>(w) && y + K <= static_cast<uint32_t>(h),
+                    "build_index: dictionary window outside the image");
+        }
+        auto* pi = new zi_patch_index();
+        try {
+            pi->ctx = ctx;
+            pi->cfg = *cfg;
+            pi->w = w;
+            pi->h = h;
+            pi->C = C;
+            pi->K = K;
+            pi->m = m;
+            pi->mc = m * C;
+            pi->n = n;
+            pi->rc.assign(layout_rc, layout_rc + 2 * m);
+            std::vector<int32_t> off(m), loc(m), cols;
+            for (int p = 0; p < m; ++p) {
+                const int r = layout_rc[2 * p], c = layout_rc[2 * p + 1];
+                off[p] = (r * w + c) * C;
+                loc[p] = r * K + c;
+                for (int ch = 0; ch < C; ++ch) cols.push_back((r * K + c) * C + ch);
+            }
+            const size_t npx = static_cast<size_t>(w) * h;
+            pi->image.ensure(npx * C + 16);
+            pi->dict.ensure(n);
+            pi->off.ensure(m);
+            pi->local.ensure(m);
+            pi->cols.ensure(cols.size());
+            ZI_CUDA(cudaMemcpyAsync(pi->image.p, image, npx * C, cudaMemcpyHostToDevice, ctx->stream));
+            ZI_CUDA(cudaMemcpyAsync(pi->dict.p, keys, n * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+            ZI_CUDA(cudaMemcpyAsync(pi->off.p, off.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+            ZI_CUDA(cudaMemcpyAsync(pi->local.p, loc.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+            ZI_CUDA(cudaMemcpyAsync(pi->cols.p, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));  // pageable sources
+            zi::build_patch_index(pi);
+        } catch (...) {
+            delete pi;
+            throw;
+        }
+        *out = pi;
+    });
+}
+
+zi_status zi_patch_index_destroy(zi_patch_index* pi) {
+    return guard(pi ? pi->ctx : nullptr, [&] { delete pi; });
+}
+
+zi_status zi_patch_index_model(const zi_patch_index* pi, int32_t* dims, int32_t* mc, double* mean, double* components,
+                               double* eigenvalues, double* lo, double* hi, double* build_seconds,
+                               double* sort_seconds) {
+    return guard(pi ? pi->ctx : nullptr, [&] {
+        require(pi != nullptr, "null argument");
+        if (dims) *dims = pi->dims;
+        if (mc) *mc = pi->mc;
+        auto put = [](double* dst, const std::vector<double>& v) {
+            if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+        };
+        put(mean, pi->h_mean);
+        put(components, pi->h_comp);
+        put(eigenvalues, pi->h_eig);
+        put(lo, pi->h_lo);
+        put(hi, pi->h_hi);
+        if (build_seconds) *build_seconds = pi->build_ms * 1e-3;
+        if (sort_seconds) *sort_seconds = pi->sort_ms * 1e-3;
+    });
+}
+
+zi_status zi_patch_index_get_index(zi_patch_index* pi, zi_index** out) {
+    return guard(pi ? pi->ctx : nullptr, [&] {
+        require(pi && out, "null argument");
+        *out = &pi->index;
+    });
+}
+
+zi_status zi_make_query(zi_patch_index* pi, const uint8_t* target_values, const uint8_t* target_known, uint8_t* out) {
+    return guard(pi ? pi->ctx : nullptr, [&] {
+        require(pi && target_values && target_known && out, "null argument");
+        zi::make_query(pi->ctx, target_values, target_known, pi->K, pi->C, pi->local.p, pi->m, pi->mean.p, pi->comp.p,
+                       pi->minmax.p, pi->dims, out, pi->qbuf, pi->hstage);
+    });
+}
+
+zi_status zi_multi_index_make_query(zi_multi_index* mi, int32_t layout, const uint8_t* target_values,
+                                    const uint8_t* target_known, uint8_t* out) {
+    return guard(mi ? mi->ctx : nullptr, [&] {
+        require(mi && target_values && target_known && out, "null argument");
+        require(layout >= 0 && layout < 8, "layout id out of range");
+        require(mi->n > 0, "empty multi-index");
+        const size_t mc = static_cast<size_t>(mi->mc), D = static_cast<size_t>(mi->dims);
+        zi::make_query(mi->ctx, target_values, target_known, mi->K, mi->C, mi->layout_local.p + layout * mi->m, mi->m,
+                       mi->pca_mean.p + layout * mc, mi->pca_comp.p + layout * mc * D, mi->minmax.p + layout * 2 * D,
+                       mi->dims, out, mi->qscratch, mi->hstage);
+        mi->qws_clean = false;
+    });
+}
+
+zi_status zi_brute_force_scan(zi_ctx* ctx, const uint8_t* image, int32_t w, int32_t h, int32_t C, const uint32_t* keys,
+                              uint64_t n, const uint8_t* target_values, const uint8_t* target_known, int32_t K,
+                              int32_t norm, zi_best_patch* out) {
+    return guard(ctx, [&] {
+        require(ctx && image && target_values && target_known && out && (n == 0 || keys), "null argument");
+        require(w > 0 && h > 0 && (C == 1 || C == 3), "raster_image: bad dimensions");
+        require(K >= 1 && K <= 255, "patch size out of range");
+        require(norm == ZI_NORM_L2 || norm == ZI_NORM_L1, "norm must be l2 or l1");
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint32_t x = keys[i] & 0xffffu, y = keys[i] >> 16;
+            require(x + K <= static_cast<uint32_t>(w) && y + K <= static_cast<uint32_t>(h),
+                    "brute_force_best: dictionary window outside the image");
+        }
+        const size_t npx = static_cast<size_t>(w) * h;
+        zi::dbuf<uint8_t> dimg, scratch;
+        zi::dbuf<uint32_t> ddict;
+        zi::hbuf<uint8_t> stage;
+        dimg.ensure(npx * C + 16);
+        ddict.ensure(n ? n : 1);
+        ZI_CUDA(cudaMemcpyAsync(dimg.p, image, npx * C, cudaMemcpyHostToDevice, ctx->stream));
+        if (n) ZI_CUDA(cudaMemcpyAsync(ddict.p, keys, n * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+        const uint64_t best =
+            zi::brute_force_scan(ctx, dimg.p, w, C, K, ddict.p, n, target_values, target_known, norm, scratch, stage);
+        out->key = static_cast<uint32_t>(best & 0xffffffffu);
+        out->cost = static_cast<uint32_t>(best >> 32);
+        out->error = norm == ZI_NORM_L2 ? std::sqrt(static_cast<double>(out->cost)) : static_cast<double>(out->cost);
+        out->layout_id = 0;
+        out->candidates = n;
+        if (n == 0) {
+            out->key = 0;
+            out->cost = 0xffffffffu;
+        }
     });
 }
 

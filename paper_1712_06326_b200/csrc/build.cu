@@ -19,23 +19,24 @@
 namespace zi {
 
 // device moments -> host s, S (full symmetric; k_moments computes tile pairs ti <= tj only)
-static void sync_moments(zi_multi_index* mi) {
-    zi_ctx* ctx = mi->ctx;
-    const int F = mi->F;
+static void moments_to_host(zi_ctx* ctx, const unsigned long long* d_mom, int F, hbuf<unsigned long long>& stage,
+                            std::vector<int64_t>& s, std::vector<int64_t>& S) {
     const size_t nmom = static_cast<size_t>(F) + static_cast<size_t>(F) * F;
-    unsigned long long* hm = mi->hmom.ensure(nmom);
-    ZI_CUDA(cudaMemcpyAsync(hm, mi->moments.p, nmom * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long* hm = stage.ensure(nmom);
+    ZI_CUDA(cudaMemcpyAsync(hm, d_mom, nmom * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
-    mi->s.assign(F, 0);
-    mi->S.assign(static_cast<size_t>(F) * F, 0);
-    for (int i = 0; i < F; ++i) mi->s[i] = static_cast<int64_t>(hm[i]);
+    s.assign(F, 0);
+    S.assign(static_cast<size_t>(F) * F, 0);
+    for (int i = 0; i < F; ++i) s[i] = static_cast<int64_t>(hm[i]);
     constexpr int kTile = 128;
     for (int i = 0; i < F; ++i)
         for (int j = 0; j < F; ++j) {
             const int a = (i / kTile <= j / kTile) ? i : j, b = (i / kTile <= j / kTile) ? j : i;
-            mi->S[static_cast<size_t>(i) * F + j] = static_cast<int64_t>(hm[F + static_cast<size_t>(a) * F + b]);
+            S[static_cast<size_t>(i) * F + j] = static_cast<int64_t>(hm[F + static_cast<size_t>(a) * F + b]);
         }
 }
+
+static void sync_moments(zi_multi_index* mi) { moments_to_host(mi->ctx, mi->moments.p, mi->F, mi->hmom, mi->s, mi->S); }
 
 void finish_build_timing(zi_multi_index* mi) {
     if (!mi->build_ms_pending) return;
@@ -208,6 +209,102 @@ void build_multi_index(zi_multi_index* mi) {
     mi->build_ms_pending = true;
     mi->host_lohi = false;
     mi->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+}
+
+// build_index (proj/src/builder.cpp:129-195) for ONE layout over the caller's dictionary: the
+// moments of the full K*K*C vector (the layout's covariance is a sub-block), one device
+// eigen-solve, the canonical fp64 projection + min/max, quantise + Morton interleave, the hybrid
+// Morton sort and finalize.  The reference's per-layout entry point (builder.hpp:77-81); the
+// multi-index path (build_multi_index) runs the same stages for eight layouts at once.
+void build_patch_index(zi_patch_index* pi) {
+    zi_ctx* ctx = pi->ctx;
+    const int K = pi->K, C = pi->C, m = pi->m, mc = pi->mc, F = K * K * C;
+    const uint64_t n = pi->n;
+    pi->F = F;
+    pi->dims = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(pi->cfg.dims),
+                                                   std::min<uint64_t>(static_cast<uint64_t>(mc), n)));
+    const int D = pi->dims;
+    cudaEvent_t e0, e1, e2;
+    ZI_CUDA(cudaEventCreate(&e0));
+    ZI_CUDA(cudaEventCreate(&e1));
+    ZI_CUDA(cudaEventCreate(&e2));
+    ZI_CUDA(cudaEventRecord(e0, ctx->stream));
+    pi->moments.ensure(static_cast<size_t>(F) + static_cast<size_t>(F) * F);
+    patch_moments(ctx, pi->image.p, pi->w, C, K, pi->dict.p, n, pi->moments.p);
+    pi->mean.ensure(mc);
+    pi->comp.ensure(static_cast<size_t>(mc) * D);
+    pi->eig.ensure(32);
+    pi->work.ensure(pca_work_doubles(mc, D));
+    static const bool host_pca = std::getenv("ZI_HOST_PCA") != nullptr;
+    pi->device_pca = !host_pca && pca_on_device_n(ctx, 1, pi->moments.p, F, n, pi->cols.p, mc, D, pi->mean.p,
+                                                  pi->comp.p, pi->eig.p, pi->work.p);
+    if (!pi->device_pca) {
+        hbuf<unsigned long long> stage;
+        std::vector<int64_t> hs, hS;
+        moments_to_host(ctx, pi->moments.p, F, stage, hs, hS);
+        std::vector<int32_t> cols;
+        for (int p = 0; p < m; ++p)
+            for (int ch = 0; ch < C; ++ch) cols.push_back((pi->rc[2 * p] * K + pi->rc[2 * p + 1]) * C + ch);
+        std::vector<double> mean, comp, eig;
+        pca_fit_layout(hs, hS, F, n, cols, D, mean, comp, eig);
+        std::vector<double> cjd(static_cast<size_t>(mc) * D);
+        for (int j = 0; j < mc; ++j)
+            for (int d = 0; d < D; ++d) cjd[static_cast<size_t>(j) * D + d] = comp[static_cast<size_t>(d) * mc + j];
+        ZI_CUDA(cudaMemcpyAsync(pi->mean.p, mean.data(), mc * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        ZI_CUDA(cudaMemcpyAsync(pi->comp.p, cjd.data(), cjd.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        ZI_CUDA(cudaMemcpyAsync(pi->eig.p, eig.data(), D * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        ZI_CUDA(cudaStreamSynchronize(ctx->stream));  // pageable locals
+    }
+    pi->minmax.ensure(static_cast<size_t>(2) * D);
+    pi->proj.ensure(static_cast<size_t>(D) * n);
+    const int W = (D + 3) / 4;
+    pi->recs.ensure(static_cast<size_t>(W + 1) * n);
+    uint32_t* keyw = pi->recs.p;
+    uint32_t* val = pi->recs.p + static_cast<size_t>(W) * n;
+    project(ctx, pi->image.p, pi->w, C, pi->dict.p, n, pi->off.p, m, pi->mean.p, pi->comp.p, D, pi->proj.p,
+            pi->minmax.p);
+    quantize_interleave(ctx, pi->proj.p, pi->minmax.p, n, n, 0, D, keyw, val);
+    ZI_CUDA(cudaEventRecord(e1, ctx->stream));
+    uint32_t* sorted[10];
+    morton_sort_layouts(ctx, keyw, val, n, D, sorted);
+    pi->index.ctx = ctx;
+    pi->index.layout_id = 0;
+    finalize_index(ctx, sorted[0], sorted[W], n, 0, n, D, pi->dict.p, &pi->index);
+    ZI_CUDA(cudaEventRecord(e2, ctx->stream));
+    ZI_CUDA(cudaEventSynchronize(e2));
+    float a = 0.f, b = 0.f;
+    ZI_CUDA(cudaEventElapsedTime(&a, e0, e2));
+    ZI_CUDA(cudaEventElapsedTime(&b, e1, e2));
+    pi->build_ms = a;
+    pi->sort_ms = b;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    patch_index_sync_host(pi);
+}
+
+void patch_index_sync_host(zi_patch_index* pi) {
+    zi_ctx* ctx = pi->ctx;
+    const int mc = pi->mc, D = pi->dims;
+    std::vector<double> cjd(static_cast<size_t>(mc) * D);
+    std::vector<unsigned long long> mm(static_cast<size_t>(2) * D);
+    pi->h_mean.resize(mc);
+    pi->h_eig.resize(D);
+    ZI_CUDA(cudaMemcpyAsync(pi->h_mean.data(), pi->mean.p, mc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(cjd.data(), pi->comp.p, cjd.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(pi->h_eig.data(), pi->eig.p, D * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(mm.data(), pi->minmax.p, mm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    pi->h_comp.assign(static_cast<size_t>(D) * mc, 0.0);
+    for (int j = 0; j < mc; ++j)
+        for (int d = 0; d < D; ++d) pi->h_comp[static_cast<size_t>(d) * mc + j] = cjd[static_cast<size_t>(j) * D + d];
+    pi->h_lo.resize(D);
+    pi->h_hi.resize(D);
+    for (int d = 0; d < D; ++d) {
+        pi->h_lo[d] = ordered_to_double(mm[d]);
+        pi->h_hi[d] = ordered_to_double(mm[D + d]);
+    }
 }
 
 }  // namespace zi

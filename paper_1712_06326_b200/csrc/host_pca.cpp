@@ -23,15 +23,24 @@ namespace zi {
 
 int subset_pixel_count(int K, double c) { return static_cast<int>(std::llround(c * K * K)); }
 
+void layout_anchors(int K, int32_t* rc) {
+    const int mid = (K - 1) / 2;
+    // edge midpoints N, E, S, W then corners NW, NE, SW, SE
+    const int a[8][2] = {{0, mid}, {mid, K - 1}, {K - 1, mid}, {mid, 0}, {0, 0}, {0, K - 1}, {K - 1, 0}, {K - 1, K - 1}};
+    for (int l = 0; l < 8; ++l) {
+        rc[2 * l] = a[l][0];
+        rc[2 * l + 1] = a[l][1];
+    }
+}
+
 int subset_layouts(int K, double c, std::vector<int32_t>& rc) {
     if (K < 3 || K % 2 == 0) throw error(ZI_E_INVALID, "subset layouts: K must be odd and >= 3");
     if (!(c > 0.0 && c <= 1.0)) throw error(ZI_E_INVALID, "subset layouts: coverage must be in (0, 1]");
     const int count = subset_pixel_count(K, c);
     if (count < 1) throw error(ZI_E_INVALID, "subset layouts: coverage keeps no pixels");
-    const int mid = (K - 1) / 2;
-    // anchors: edge midpoints N, E, S, W then corners NW, NE, SW, SE
-    const int anchors[8][2] = {{0, mid}, {mid, K - 1}, {K - 1, mid}, {mid, 0},
-                               {0, 0},   {0, K - 1},   {K - 1, 0},   {K - 1, K - 1}};
+    int32_t anch[16];
+    layout_anchors(K, anch);
+    const int(*anchors)[2] = reinterpret_cast<const int(*)[2]>(anch);
     rc.assign(static_cast<size_t>(8) * count * 2, 0);
     std::vector<int> order(static_cast<size_t>(K) * K);
     for (int id = 0; id < 8; ++id) {

@@ -352,11 +352,7 @@ void patch_moments(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const
     chunk = std::min<uint64_t>(kMomMaxChunk, (chunk + kMomStage - 1) / kMomStage * kMomStage);
     const uint64_t nchunk = (npad + chunk - 1) / chunk;
     const size_t smem = static_cast<size_t>(kMomStages) * 2 * kMomTile * kMomPitch;
-    static bool attr = false;
-    if (!attr) {
-        ZI_CUDA(cudaFuncSetAttribute(k_moments, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-    }
+    smem_attr(ctx->device, k_moments, smem);
     ZI_LAUNCH(ctx, "patch_moments", k_moments, dim3(npairs, static_cast<unsigned>(nchunk)), 256, smem, XT, npad, F,
               ntile, chunk, d_out);
 }
@@ -678,11 +674,7 @@ static void launch_project_t(zi_ctx* ctx, const uint8_t* img, int w, int C, cons
     const int KS = (m * C + 3) / 4;
     const size_t smem = static_cast<size_t>(KS) * NT * 32 * sizeof(double) + static_cast<size_t>(KS) * 4 * sizeof(double) +
                         static_cast<size_t>(KS) * 4 * sizeof(int);
-    static size_t attr = 0;
-    if (smem > attr) {
-        ZI_CUDA(cudaFuncSetAttribute(k_project<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = smem;
-    }
+    smem_attr(ctx->device, k_project<D>, smem);
     const uint64_t warps = (n + 8 * kProjGroups - 1) / (8 * kProjGroups);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((warps + kProjThreads / 32 - 1) / (kProjThreads / 32),
                                                                    static_cast<uint64_t>(ctx->num_sms) * 8));

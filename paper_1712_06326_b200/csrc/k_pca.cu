@@ -946,6 +946,12 @@ bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint
     return pca_launch(ctx, 8, nullptr, d_moments, F, n, d_cols, mc, D, d_mean, d_comp, d_eig, d_work);
 }
 
+bool pca_on_device_n(zi_ctx* ctx, int layouts, const unsigned long long* d_moments, int F, uint64_t n,
+                     const int32_t* d_cols, int mc, int D, double* d_mean, double* d_comp, double* d_eig,
+                     double* d_work) {
+    return pca_launch(ctx, layouts, nullptr, d_moments, F, n, d_cols, mc, D, d_mean, d_comp, d_eig, d_work);
+}
+
 bool pca_from_cov_on_device(zi_ctx* ctx, const double* d_cov, int mc, int D, double* d_comp, double* d_eig,
                             double* d_work) {
     return pca_launch(ctx, 1, d_cov, nullptr, 0, 0, nullptr, mc, D, nullptr, d_comp, d_eig, d_work);
@@ -955,28 +961,18 @@ static bool pca_launch(zi_ctx* ctx, int nl, const double* d_cov, const unsigned 
                        const int32_t* d_cols, int mc, int D, double* d_mean, double* d_comp, double* d_eig,
                        double* d_work) {
     if (mc > kPcaMaxN || D > 32 || mc < 3) return false;
-    static int optin = -1;
-    if (optin < 0) ZI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    int optin = 0;
+    ZI_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     const size_t limit = static_cast<size_t>(optin) - 1024;
     const int rows_max = (mc + kCl - 1) / kCl;
     const size_t smem_tri = (static_cast<size_t>(rows_max) * mc + 4 * mc + 2 * kCl * (kTriThreads / 32)) * sizeof(double);
     const size_t smem_vec = (refl_stride(mc) + 9 * static_cast<size_t>(mc)) * sizeof(double) + mc + 16;
     const size_t smem_fin = static_cast<size_t>(D) * mc * sizeof(double);
     if (smem_tri > limit || smem_vec > limit || smem_fin > limit) return false;
-    static size_t attr_tri = 0, attr_vec = 0, attr_fin = 0;
-    if (smem_tri > attr_tri) {
-        ZI_CUDA(cudaFuncSetAttribute(k_pca_tri, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_tri)));
-        if (kCl > 8) ZI_CUDA(cudaFuncSetAttribute(k_pca_tri, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr_tri = smem_tri;
-    }
-    if (smem_vec > attr_vec) {
-        ZI_CUDA(cudaFuncSetAttribute(k_pca_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_vec)));
-        attr_vec = smem_vec;
-    }
-    if (smem_fin > attr_fin) {
-        ZI_CUDA(cudaFuncSetAttribute(k_pca_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_fin)));
-        attr_fin = smem_fin;
-    }
+    smem_attr(ctx->device, k_pca_tri, smem_tri);
+    if (kCl > 8) ZI_CUDA(cudaFuncSetAttribute(k_pca_tri, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    smem_attr(ctx->device, k_pca_vec, smem_vec);
+    smem_attr(ctx->device, k_pca_fin, smem_fin);
     const pca_work_view w = pca_work_split(d_work, mc, D);
     static const char* lz_env = std::getenv("ZI_PCA_LZ");
     const bool lz_on = !(lz_env && lz_env[0] == '0');
@@ -985,11 +981,7 @@ static bool pca_launch(zi_ctx* ctx, int nl, const double* d_cov, const unsigned 
     if (lzk > 0) {
         const size_t smem_lz = (static_cast<size_t>(rows_max) * mc + static_cast<size_t>(kLzMax) * rows_max + 2 * mc +
                                 rows_max + (2 * kCl + 3) * (kLzMax + 2)) * sizeof(double);
-        static size_t attr_lz = 0;
-        if (smem_lz > attr_lz) {
-            ZI_CUDA(cudaFuncSetAttribute(k_pca_lz, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_lz)));
-            attr_lz = smem_lz;
-        }
+        smem_attr(ctx->device, k_pca_lz, smem_lz);
         ZI_LAUNCH(ctx, "pca_lanczos", k_pca_lz, nl * kCl, kTriThreads, smem_lz, ta);
         vec_args la{mc, D, w, nullptr, 1, 0};
         ZI_LAUNCH(ctx, "pca_ritz", k_pca_vec, nl * D, kVecThreads, smem_vec, la);

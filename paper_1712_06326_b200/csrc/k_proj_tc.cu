@@ -617,11 +617,7 @@ __global__ void __launch_bounds__(256) k_gram_reduce(const uint32_t* __restrict_
 
 template <int KT>
 static void launch_gram(zi_ctx* ctx, const gm_params& G, size_t smem) {
-    static size_t attr = 0;
-    if (smem > attr) {
-        ZI_CUDA(cudaFuncSetAttribute(k_gram_fused<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = smem;
-    }
+    smem_attr(ctx->device, k_gram_fused<KT>, smem);
     // one CTA per SM, more when an SM would sum more than kGmChunk tiles (65536 patches: the
     // u32 view of the s32 accumulators stays exact)
     const uint64_t want = std::max<uint64_t>(static_cast<uint64_t>(ctx->num_sms), (G.P.ntiles + kGmChunk - 1) / kGmChunk);
@@ -817,12 +813,8 @@ static void launch_pt_exact(zi_ctx* ctx, zi_multi_index* mi, const pt_params& P,
 
 template <int D, int KT>
 static void launch_pt_kt(zi_ctx* ctx, const pt_params& P, int mode, size_t smem) {
-    static bool attr[2] = {false, false};
-    if (!attr[mode]) {
-        if (mode == 0) ZI_CUDA(cudaFuncSetAttribute(k_proj_tc<D, 0, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        else ZI_CUDA(cudaFuncSetAttribute(k_proj_tc<D, 1, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr[mode] = true;
-    }
+    if (mode == 0) smem_attr(ctx->device, k_proj_tc<D, 0, KT>, 200 * 1024);
+    else smem_attr(ctx->device, k_proj_tc<D, 1, KT>, 200 * 1024);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(P.ntiles, static_cast<uint64_t>(ctx->num_sms)));
     if (mode == 0) ZI_LAUNCH(ctx, "project_tc_minmax", (k_proj_tc<D, 0, KT>), grid, kPtThreads, smem, P);
     else ZI_LAUNCH(ctx, "project_tc_quantize", (k_proj_tc<D, 1, KT>), grid, kPtThreads, smem, P);

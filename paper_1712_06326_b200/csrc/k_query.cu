@@ -1832,11 +1832,7 @@ static bool run_knn(zi_ctx* ctx, const views8& V, uint64_t n, uint64_t nblk, con
 #undef ZI_SCAN_CASE
             default: throw error(ZI_E_INVALID, "dims above 32");
         }
-        static bool attr = false;
-        if (!attr) {
-            ZI_CUDA(cudaFuncSetAttribute(k_knn_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr = true;
-        }
+        smem_attr(ctx->device, k_knn_select, 200 * 1024);
         const size_t smem = (kSelCap + 2048 + kSelBinCap) * sizeof(unsigned long long) + (kSelBins + 1) * sizeof(uint32_t);
         ZI_LAUNCH(ctx, "knn_select", k_knn_select, 1, kSelThreads, smem, s.ws, k, s.G, s.cand_cnt, s.cand, s.out,
                   ra ? ra->img : nullptr, ra ? ra->w : 0, ra ? ra->C : 1, ra ? ra->K : 1, ra ? s.target : nullptr, norm);
@@ -1865,15 +1861,12 @@ static void knn_fallback(zi_ctx* ctx, const query_scratch& s, uint32_t k, int no
     if (ra) ZI_LAUNCH(ctx, "refine", k_refine, 1, 1024, rsmem, ra->img, ra->w, ra->C, ra->K, s.target, s.ws, s.out, norm);
 }
 
-static void ensure_smem_attr() {
-    static bool done = false;
-    if (done) return;
-#define ZI_ATTR(PP)                                                                                            \
-    ZI_CUDA(cudaFuncSetAttribute(k_seed_query<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8));     \
-    ZI_CUDA(cudaFuncSetAttribute(k_query_prep<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+static void ensure_smem_attr(const zi_ctx* ctx) {
+#define ZI_ATTR(PP)                                                    \
+    smem_attr(ctx->device, k_seed_query<PP>, 4096 * 8);                \
+    smem_attr(ctx->device, k_query_prep<PP>, 220 * 1024);
     ZI_ATTR(1) ZI_ATTR(2) ZI_ATTR(3) ZI_ATTR(4) ZI_ATTR(5) ZI_ATTR(6) ZI_ATTR(7) ZI_ATTR(8)
 #undef ZI_ATTR
-    done = true;
 }
 
 static int seed_smem_words(uint32_t k) { return std::max(seed_window(k), 2048); }
@@ -1882,7 +1875,7 @@ uint32_t knn_search(zi_index* idx, const uint8_t* h_query, uint32_t k, int norm,
     zi_ctx* ctx = idx->ctx;
     k = std::max<uint32_t>(k, 1);  // knn_list capacity = max(k, 1) (proj/src/zcurve.cpp:25-31)
     if (idx->n == 0) return 0;
-    ensure_smem_attr();
+    ensure_smem_attr(ctx);
     views8 V;
     for (int l = 0; l < 8; ++l) V.v[l] = view_of(idx);
     const query_scratch s = carve(idx->qscratch, ctx, idx->nblk, k, 32);
@@ -1988,11 +1981,7 @@ static bool fused_query(zi_multi_index* mi, const query_scratch& s, const mi_vie
     switch (mv.idx[0].P) {
 #define ZI_FUSED_CASE(PP)                                                                                          \
     case PP: {                                                                                                     \
-        static bool attr = false;                                                                                  \
-        if (!attr) {                                                                                               \
-            ZI_CUDA(cudaFuncSetAttribute(k_query_fused<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)); \
-            attr = true;                                                                                           \
-        }                                                                                                          \
+        smem_attr(ctx->device, k_query_fused<PP>, 220 * 1024);                                                     \
         ZI_LAUNCH(ctx, "query_fused", k_query_fused<PP>, 1, kFusedThreads, smem, mv, mi->image.p, mi->w, s.target, s.ws, \
                   k, norm, want_list ? s.out : nullptr);                                                           \
         break;                                                                                                     \
@@ -2011,7 +2000,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
                               uint64_t* knn_out) {
     zi_ctx* ctx = mi->ctx;
     k = std::max<uint32_t>(k, 1);
-    ensure_smem_attr();
+    ensure_smem_attr(ctx);
     const size_t KK = static_cast<size_t>(mi->K) * mi->K;
     const size_t tbytes = KK * mi->C + KK;
     const uint64_t nblk = mi->L[0].index.nblk;
@@ -2054,11 +2043,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
         switch (mv.idx[0].P) {
 #define ZI_ONE_CASE(PP)                                                                                              \
     case PP: {                                                                                                       \
-        static bool attr = false;                                                                                    \
-        if (!attr) {                                                                                                 \
-            ZI_CUDA(cudaFuncSetAttribute(k_query_one<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));  \
-            attr = true;                                                                                             \
-        }                                                                                                            \
+        smem_attr(ctx->device, k_query_one<PP>, 220 * 1024);                                                         \
         ZI_LAUNCH(ctx, "query_one", k_query_one<PP>, G1, kOneThreads, one_smem, mv, mi->image.p, mi->w, s.target, s.ws, \
                   k, norm, s.cand_cnt, s.cand, s.ccost, s.out, dres, seq, knn_out != nullptr ? 1 : 0);             \
         break;                                                                                                       \
@@ -2145,25 +2130,74 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
     return r;
 }
 
-uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, int norm) {
-    zi_ctx* ctx = mi->ctx;
-    const size_t KK = static_cast<size_t>(mi->K) * mi->K;
-    const size_t tbytes = KK * mi->C + KK;
-    const query_scratch s = carve(mi->qscratch, ctx, 1, 1, tbytes);
+uint64_t brute_force_scan(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const uint32_t* d_dict, uint64_t n,
+                          const uint8_t* h_tv, const uint8_t* h_tk, int norm, dbuf<uint8_t>& scratch,
+                          hbuf<uint8_t>& hstage) {
+    const size_t KK = static_cast<size_t>(K) * K;
+    const size_t tbytes = KK * C + KK;
+    const query_scratch s = carve(scratch, ctx, 1, 1, tbytes);
     const size_t res_off = (tbytes + 255) & ~size_t(255);
-    uint8_t* stage = mi->hstage.ensure(res_off + sizeof(qws));
-    std::memcpy(stage, h_tv, KK * mi->C);
-    std::memcpy(stage + KK * mi->C, h_tk, KK);
+    uint8_t* stage = hstage.ensure(res_off + sizeof(qws));
+    std::memcpy(stage, h_tv, KK * C);
+    std::memcpy(stage + KK * C, h_tk, KK);
     ZI_CUDA(cudaMemcpyAsync(s.target, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
     ZI_CUDA(cudaMemsetAsync(&s.ws->best, 0xff, sizeof(unsigned long long), ctx->stream));
-    const size_t smem = ((KK * mi->C + 3) & ~size_t(3)) + KK * mi->C * sizeof(int) + 16;
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((mi->n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
-    ZI_LAUNCH(ctx, "brute_force", k_brute, grid, 256, smem, mi->image.p, mi->w, mi->C, mi->K, mi->dict.p + mi->row_begin,
-              mi->n, s.target, norm, &s.ws->best);
+    const size_t smem = ((KK * C + 3) & ~size_t(3)) + KK * C * sizeof(int) + 16;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
+    if (n > 0)
+        ZI_LAUNCH(ctx, "brute_force", k_brute, grid, 256, smem, d_img, w, C, K, d_dict, n, s.target, norm, &s.ws->best);
     unsigned long long* hb = reinterpret_cast<unsigned long long*>(stage + res_off);
     ZI_CUDA(cudaMemcpyAsync(hb, &s.ws->best, 8, cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     return *hb;
+}
+
+uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, int norm) {
+    return brute_force_scan(mi->ctx, mi->image.p, mi->w, mi->C, mi->K, mi->dict.p + mi->row_begin, mi->n, h_tv, h_tk,
+                            norm, mi->qscratch, mi->hstage);
+}
+
+// make_query (proj/src/builder.cpp:110-127) for one layout model: unknown layout pixels take the
+// mean (xc = +0.0 exactly), then the canonical fp64 fma chain per dim and the quantiser.
+__global__ void __launch_bounds__(256) k_make_query(const uint8_t* __restrict__ target, int K, int C,
+                                                    const int32_t* __restrict__ local, int m,
+                                                    const double* __restrict__ mean, const double* __restrict__ comp,
+                                                    const unsigned long long* __restrict__ minmax, int D,
+                                                    uint8_t* __restrict__ out) {
+    extern __shared__ double s_xc[];
+    const int KK = K * K, mc = m * C;
+    const uint8_t* tv = target;
+    const uint8_t* tk = target + KK * C;
+    for (int j = threadIdx.x; j < mc; j += blockDim.x) {
+        const int l = local[j / C];
+        const double mj = mean[j];
+        const double x = tk[l] ? static_cast<double>(tv[l * C + j % C]) : mj;
+        s_xc[j] = __dsub_rn(x, mj);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        double y = 0.0;
+        for (int j = 0; j < mc; ++j) y = __fma_rn(comp[static_cast<size_t>(j) * D + d], s_xc[j], y);
+        out[d] = quantize_rn(ordered_to_double_hd(minmax[d]), ordered_to_double_hd(minmax[D + d]), y);
+    }
+}
+
+void make_query(zi_ctx* ctx, const uint8_t* h_tv, const uint8_t* h_tk, int K, int C, const int32_t* d_local, int m,
+                const double* d_mean, const double* d_comp, const unsigned long long* d_minmax, int D, uint8_t* h_out,
+                dbuf<uint8_t>& scratch, hbuf<uint8_t>& hstage) {
+    const size_t KK = static_cast<size_t>(K) * K;
+    const size_t tbytes = KK * C + KK;
+    const size_t out_off = (tbytes + 255) & ~size_t(255);
+    uint8_t* stage = hstage.ensure(out_off + 64);
+    uint8_t* dev = scratch.ensure(out_off + 64);
+    std::memcpy(stage, h_tv, KK * C);
+    std::memcpy(stage + KK * C, h_tk, KK);
+    ZI_CUDA(cudaMemcpyAsync(dev, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
+    ZI_LAUNCH(ctx, "make_query", k_make_query, 1, 256, static_cast<size_t>(m) * C * sizeof(double), dev, K, C, d_local,
+              m, d_mean, d_comp, d_minmax, D, dev + out_off);
+    ZI_CUDA(cudaMemcpyAsync(stage + out_off, dev + out_off, D, cudaMemcpyDeviceToHost, ctx->stream));
+    ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(h_out, stage + out_off, D);
 }
 
 // masked-cost refine of a caller-given candidate list (query_best_patch's refine step,

@@ -185,12 +185,7 @@ template <int NW>
 static void launch_onesweep(zi_ctx* ctx, const sort_words& io, int dw, int ds, const uint32_t* base, uint32_t* status,
                             uint32_t* ctr, uint64_t n, unsigned ntiles) {
     const size_t smem = static_cast<size_t>(NW) * kSortTile * sizeof(uint32_t);
-    static bool attr = false;
-    if (!attr) {
-        ZI_CUDA(cudaFuncSetAttribute(k_onesweep<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kMaxWords * kSortTile * sizeof(uint32_t))));
-        attr = true;
-    }
+    smem_attr(ctx->device, k_onesweep<NW>, kMaxWords * kSortTile * sizeof(uint32_t));
     ZI_LAUNCH(ctx, "radix_onesweep", k_onesweep<NW>, ntiles, kSortThreads, smem, io, dw, ds, base, status, ctr, n);
 }
 
@@ -674,11 +669,7 @@ static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int 
     while (cap > 1024 && bytes(cap) > 112 * 1024) cap >>= 1;
     const int T = cap / 2;
     const size_t smem = bytes(cap);
-    static size_t attr = 0;
-    if (smem > attr) {
-        ZI_CUDA(cudaFuncSetAttribute(k_segsort<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = smem;
-    }
+    smem_attr(ctx->device, k_segsort<NW>, smem);
     ZI_CUDA(cudaMemcpyAsync(d_passes, passes.data(), passes.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
     const unsigned grid = static_cast<unsigned>((N + T - 1) / T);
     ZI_LAUNCH(ctx, "segment_sort", k_segsort<NW>, grid, kSegThreads, smem, c, T, cap, static_cast<int>(passes.size()),

@@ -174,11 +174,7 @@ void gram_u8_tc(zi_ctx* ctx, const uint8_t* XT, int F, int Fpad, uint64_t npad, 
     chunk = std::min<uint64_t>(kTcMaxChunk, (chunk + kTcStageK - 1) / kTcStageK * kTcStageK);
     const uint64_t nchunk = (npad + chunk - 1) / chunk;
     const size_t smem = static_cast<size_t>(kTcStages) * 2 * kTcTileBytes + 1024;
-    static bool attr = false;
-    if (!attr) {
-        ZI_CUDA(cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-    }
+    smem_attr(ctx->device, k_gram_tc, smem);
     ZI_LAUNCH(ctx, "patch_moments", k_gram_tc, dim3(npairs, static_cast<unsigned>(nchunk)), 128, smem, tm, F, ntile, npad,
               chunk, out);
 }

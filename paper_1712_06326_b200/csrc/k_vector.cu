@@ -315,11 +315,7 @@ static void launch_vec_project(zi_ctx* ctx, const float* X, uint64_t n, int dim,
     constexpr int NT = (D + 7) / 8;
     const int KS = (dim + 3) / 4;
     const size_t smem = (static_cast<size_t>(KS) * NT * 32 + static_cast<size_t>(KS) * 4) * sizeof(double);
-    static size_t attr = 0;
-    if (smem > attr) {
-        ZI_CUDA(cudaFuncSetAttribute(k_vec_project<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = smem;
-    }
+    smem_attr(ctx->device, k_vec_project<D>, smem);
     const uint64_t warps = (n + 8 * kVpGroups - 1) / (8 * kVpGroups);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((warps + kVpThreads / 32 - 1) / (kVpThreads / 32),
                                                                    static_cast<uint64_t>(ctx->num_sms) * 8));
@@ -356,11 +352,7 @@ void build_vector_index_device(zi_vector_index* vi) {
         const int Tb = (T + 3) / 4, nblocks = Tb * (Tb + 1) / 2;
         const int warps = std::min(nblocks, kGramMaxWarps);
         const unsigned gy = static_cast<unsigned>((nblocks + kGramMaxWarps - 1) / kGramMaxWarps);
-        static size_t gattr = 0;
-        if (gsmem > gattr) {
-            ZI_CUDA(cudaFuncSetAttribute(k_vec_gram_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
-            gattr = gsmem;
-        }
+        smem_attr(ctx->device, k_vec_gram_blk, gsmem);
         ZI_LAUNCH(ctx, "vec_gram", k_vec_gram_blk, dim3(nstripe, gy), warps * 32, gsmem, X, n, dim, Pd, vi->mean.p,
                   nblocks, part.p);
     }

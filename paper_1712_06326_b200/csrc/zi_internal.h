@@ -38,6 +38,8 @@ inline void check_launch(const char* name) {
 // its memory (release threshold = max) -- building index after index reuses the same HBM without
 // cudaMalloc / cudaFree round trips.
 extern thread_local cudaStream_t tls_alloc_stream;
+// the ctx's private memory pool (nullptr: the device's current pool)
+extern thread_local cudaMemPool_t tls_alloc_pool;
 
 // Growable device buffer (pool allocated, never shrinks).
 template <typename T>
@@ -59,7 +61,8 @@ struct dbuf {
         release();
         const size_t bytes = (n ? n : 1) * sizeof(T);
         s = tls_alloc_stream;
-        ZI_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s));
+        if (tls_alloc_pool) ZI_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), bytes, tls_alloc_pool, s));
+        else ZI_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s));
         cap = n ? n : 1;
         return p;
     }
@@ -86,6 +89,14 @@ struct hbuf {
     }
 };
 
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on `device` (the attribute is
+// per function and per device); thread-safe, remembers what each (function, device) already has.
+void set_smem_attr(const void* fn, int device, size_t bytes);
+template <typename F>
+inline void smem_attr(int device, F* fn, size_t bytes) {
+    set_smem_attr(reinterpret_cast<const void*>(fn), device, bytes);
+}
+
 // Per-kernel device timing (CUDA events on the ctx stream), used by bench.py for the
 // roofline's "average launch duration measured live".
 struct prof_slot {
@@ -106,6 +117,7 @@ struct zi_ctx {
     std::vector<zi::prof_slot> prof;
     std::vector<std::string> prof_filter;  // kernels to time while profiling (empty: every kernel)
     int num_sms = 148;
+    cudaMemPool_t pool = nullptr;  // private stream-ordered pool (never trimmed; rebuilds reuse its HBM)
     // shared scratch for sorts / collection
     zi::dbuf<uint8_t> scratch;
     zi::dbuf<uint32_t> counter;  // small integer scratch (tile counters etc.)
@@ -182,6 +194,31 @@ struct zi_multi_index {
     bool shard = false;
     uint64_t row_begin = 0, n_total = 0;
     zi_layout_state L[8];
+};
+
+// One layout index over a caller-given dictionary: build_index (proj/src/builder.cpp:129-195),
+// the per-layout entry point of the reference (builder.hpp:77-81).  Same device pipeline as one
+// layout of zi_multi_index: exact int64 moments, device eigen-solve, canonical fp64 projection,
+// quantiser, Morton sort, finalize.
+struct zi_patch_index {
+    zi_ctx* ctx = nullptr;
+    zi_index_config cfg{};
+    int32_t w = 0, h = 0, C = 1, K = 9, m = 0, mc = 0, F = 0, dims = 0;
+    uint64_t n = 0;
+    std::vector<int32_t> rc;                 // m*2 (row, col)
+    zi::dbuf<uint8_t> image;
+    zi::dbuf<uint32_t> dict;
+    zi::dbuf<int32_t> off, local, cols;      // pixel offsets, local r*K+c, feature columns
+    zi::dbuf<unsigned long long> moments, minmax;
+    zi::dbuf<double> mean, comp, eig, work, proj;
+    zi::dbuf<int> status;
+    zi::dbuf<uint32_t> recs;
+    zi::dbuf<uint8_t> qbuf;                  // make_query staging
+    zi::hbuf<uint8_t> hstage;
+    std::vector<double> h_mean, h_comp, h_eig, h_lo, h_hi;  // comp: dims rows of mc
+    bool device_pca = false;
+    double build_ms = 0.0, sort_ms = 0.0;
+    zi_index index;
 };
 
 // cfg5: z-curve index over fp32 feature vectors (k_vector.cu)
@@ -276,6 +313,16 @@ struct query_result {
 query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk,
                               uint32_t k, int norm, uint64_t* knn_out);
 uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, int norm);
+// the exhaustive scan over any device image + dictionary (brute_force_best with the reference's
+// (image, target, dictionary, norm) arguments, engine.hpp:98-99)
+uint64_t brute_force_scan(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K, const uint32_t* d_dict, uint64_t n,
+                          const uint8_t* h_tv, const uint8_t* h_tk, int norm, dbuf<uint8_t>& scratch,
+                          hbuf<uint8_t>& stage);
+// patch_index::make_query (proj/src/builder.cpp:110-127) on the device for one layout model:
+// d_local m local pixel indices, d_mean mc, d_comp [j][d], d_minmax 2*D ordered lo / hi
+void make_query(zi_ctx* ctx, const uint8_t* h_tv, const uint8_t* h_tk, int K, int C, const int32_t* d_local, int m,
+                const double* d_mean, const double* d_comp, const unsigned long long* d_minmax, int D, uint8_t* h_out,
+                dbuf<uint8_t>& scratch, hbuf<uint8_t>& stage);
 // masked-cost refine of a given candidate list (packed dist<<32 | key) -> packed (cost<<32 | key)
 uint64_t refine_candidates(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, const uint64_t* h_cands,
                            uint32_t count, int norm);
@@ -309,6 +356,7 @@ void shard_info(const zi_shard* sh, uint64_t* v);
 // ---- host pieces ----
 int subset_pixel_count(int K, double c);
 int subset_layouts(int K, double c, std::vector<int32_t>& rc);  // returns m
+void layout_anchors(int K, int32_t* rc);                         // 8 (row, col) anchors
 void validate_config(const zi_index_config& cfg, int channels);
 // covariance + eigen-solve + sign rule for one layout (host, deterministic)
 void pca_fit_layout(const std::vector<int64_t>& s, const std::vector<int64_t>& S, int F, uint64_t n,
@@ -330,6 +378,13 @@ bool pca_from_cov_on_device(zi_ctx* ctx, const double* d_cov, int mc, int D, dou
                             double* d_work);
 bool pca_on_device(zi_ctx* ctx, const unsigned long long* d_moments, int F, uint64_t n, const int32_t* d_cols, int mc,
                    int D, double* d_mean, double* d_comp, double* d_eig, double* d_work, int* d_status);
+// the same for `layouts` models (d_cols holds layouts*mc columns)
+bool pca_on_device_n(zi_ctx* ctx, int layouts, const unsigned long long* d_moments, int F, uint64_t n,
+                     const int32_t* d_cols, int mc, int D, double* d_mean, double* d_comp, double* d_eig,
+                     double* d_work);
+// build_index for one layout (build.cu)
+void build_patch_index(zi_patch_index* pi);
+void patch_index_sync_host(zi_patch_index* pi);
 
 // vector index (k_vector.cu): upload + build, device-resident build, queries, host mirrors
 void vector_index_build(zi_vector_index* vi, const float* h_X);

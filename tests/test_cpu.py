@@ -544,3 +544,24 @@ def test_ordered_i64_roundtrip_and_order():
     o = sharding.double_to_ordered_i64(x)
     assert np.all(np.diff(o) > 0)
     assert np.array_equal(sharding.ordered_i64_to_double(o).view(np.uint64), x.view(np.uint64))
+
+
+def test_oracle_fill_loop_with_compiled_reference_knn(golden):
+    """The restated run_loop with its k-NN answered by the reference's compiled knn_search (the
+    CPU baseline bench.py times) gives the same run as with the linear-scan oracle."""
+    tag = "eval_48x40_c_s101_m102"
+    img, kn = golden[tag + "__image"], golden[tag + "__known"]
+    base = oracle.MultiIndex(img, kn, 9, 0.6, 8)
+    out1, r1 = oracle.inpaint(img, kn, 9, 0.6, 8, knn=12, mi=base)
+    om = oracle.MultiIndex(img, kn, 9, 0.6, 8)
+    om.use_reference_knn(workers=3)
+    out2, r2 = oracle.inpaint(img, kn, 9, 0.6, 8, knn=12, mi=om)
+    assert len(r1) == len(r2) > 0
+    for f in ("tx", "ty", "sx", "sy", "cost", "layout_id", "candidates"):
+        assert np.array_equal(r1[f], r2[f]), f
+    assert np.array_equal(out1, out2)
+    # set_layout round trip: a layout replaced by its own arrays answers identically
+    L = base.index(3)
+    om2 = oracle.MultiIndex(img, kn, 9, 0.6, 8)
+    om2.set_layout(3, L.mean, L.comp, L.lo, L.hi, L.coords, L.keys)
+    assert np.array_equal(om2.index(3).coords, L.coords) and np.array_equal(om2.index(3).hi, L.hi)

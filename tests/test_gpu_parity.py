@@ -861,3 +861,73 @@ def test_moments_patch_matrix_path_still_green():
                         os.path.join(root, "tests", "test_gpu_parity.py")],
                        env=env, cwd=root, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+# ------------------------------------------------------------------ build_index / make_query / brute force (C ABI)
+@pytest.mark.parametrize("case", range(4))
+def test_build_index_one_layout_vs_oracle(zb, golden, case):
+    """zi_index_build (build_index, builder.hpp:77-81) over a caller dictionary and layout: the
+    device model injected into the oracle restatement gives the same lo / hi, coords and keys;
+    on the multi-index's dictionary and layouts the model and bytes equal the multi-index's."""
+    tag, img, kn = _images(golden)[case]
+    C = 1 if img.ndim == 2 else img.shape[2]
+    cfg = zb.index_config(patch_size=9, dims=8)
+    mi = zb.MultiIndex(img, kn, cfg)
+    d = mi.dictionary
+    for l in (0, 4, 7):
+        lay = mi.layout(l)
+        pi = zb.PatchIndex(img, d, lay["pixels"], cfg)
+        mod = pi.model()
+        assert np.array_equal(mod["mean"], lay["mean"]), (tag, l)
+        np.testing.assert_allclose(mod["components"], lay["components"], atol=1e-9)
+        lo, hi, coords, _ = oracle.project_build(img, d, lay["pixels"], mod["mean"], mod["components"])
+        assert np.array_equal(lo, mod["lo"]) and np.array_equal(hi, mod["hi"]), (tag, l)
+        rc, rk = oracle.from_descriptors(coords, d)
+        c, k = pi.index().export()
+        assert np.array_equal(c, rc) and np.array_equal(k, rk), (tag, l)
+        if np.array_equal(mod["components"], lay["components"]):
+            assert np.array_equal(c, mi.index_arrays(l)[0]) and np.array_equal(k, mi.index_arrays(l)[1])
+        for tv, tk in _query_cases(img, kn, 11):
+            q = pi.make_query(tv, tk)
+            assert np.array_equal(q, oracle.make_query(tv, tk, 9, C, lay["pixels"], mod["mean"], mod["components"],
+                                                       lo, hi)), (tag, l)
+            # the multi-index layout's make_query, same arithmetic
+            mq = mi.make_query(l, tv, tk)
+            assert np.array_equal(mq, oracle.make_query(tv, tk, 9, C, lay["pixels"], lay["mean"], lay["components"],
+                                                        lay["lo"], lay["hi"]))
+
+
+def test_build_index_custom_layout_and_subset_dictionary(zb, golden):
+    """A layout that is not one of the eight (the first 30 row-major offsets) over every third
+    dictionary key; D clamps to min(dims, m*C, n)."""
+    img, kn = workloads.small_image(64, 80, 3, seed=5, hole_frac=0.08)
+    cfg = zb.index_config(patch_size=7, dims=12)
+    d = oracle.collect_dictionary(kn, 7)[::3].copy()
+    rc = np.array([(i // 7, i % 7) for i in range(30)], dtype=np.int32)
+    pi = zb.PatchIndex(img, d, rc, cfg)
+    mod = pi.model()
+    assert pi.dims == 12 and pi.mc == 90
+    lo, hi, coords, _ = oracle.project_build(img, d, rc, mod["mean"], mod["components"])
+    assert np.array_equal(lo, mod["lo"]) and np.array_equal(hi, mod["hi"])
+    c, k = pi.index().export()
+    rcs, rks = oracle.from_descriptors(coords, d)
+    assert np.array_equal(c, rcs) and np.array_equal(k, rks)
+    tiny = zb.PatchIndex(img, d[:3], rc, cfg)
+    assert tiny.dims == 3
+    with pytest.raises(zb.EmptyDictionaryError):
+        zb.PatchIndex(img, d[:0], rc, cfg)
+    with pytest.raises(ValueError):
+        zb.PatchIndex(img, np.array([(63 << 16) | 79], np.uint32), rc, cfg)  # window outside the image
+
+
+@pytest.mark.parametrize("norm", ["l2", "l1"])
+def test_brute_force_scan_caller_dictionary(zb, golden, norm):
+    """zi_brute_force_scan (brute_force_best(image, target, dictionary, norm)) over a subset of the
+    dictionary equals the oracle's scan of the same subset."""
+    tag, img, kn = _images(golden)[1]
+    d = oracle.collect_dictionary(kn, 9)
+    sub = d[(np.arange(d.size) % 5) != 2].copy()
+    nrm = L2 if norm == "l2" else L1
+    for tv, tk in _query_cases(img, kn, 6):
+        key, cost, _ = zb.brute_force_scan(img, sub, tv, tk, 9, norm)
+        assert (cost << 32 | key) == oracle.brute_force_best(img, tv, tk, 9, sub, nrm)
