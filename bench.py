@@ -258,8 +258,11 @@ def algorithmic_bytes(kernel: str, n: int, D: int, mc: int, F: int = 0) -> float
     N = 8 * n
     g = len(pt_groups(D)) if D <= 16 else 1
     return {
-        "radix_onesweep": 2 * 4 * (W + 1) * N,          # read + write of (W key words + payload)
+        "radix_onesweep": 2 * 4 * (W + 1) * N,          # legacy LSD sort: read + write of (W key words + payload)
         "segment_sort": 2 * 4 * (W + 1) * N,            # one read + one in-place write per record
+        "ssort_count": 4 * (W + 1) * N,                 # splitter sort: records read, bucket histograms
+        "ssort_scatter": 2 * 4 * (W + 1) * N,           # records read + written to their buckets
+        "ssort_local": 2 * 4 * (W + 1) * N,             # every bucket read + written back in order
         "radix_hist": 4 * (W + 1) * N,
         "proj_minmax": 8 * D * n,
         "quantize_interleave": (8 * D + 4 + 4 * (W + 1)) * n,
@@ -524,6 +527,14 @@ def main():
 
     # -------- roofline of the dominant kernel (live CUDA-event durations over the timed region)
     mc = mi.m * mi.channels
+    breakdown = {k: {"ms_per_step": v[0], "launches_per_step": v[1]}
+                 for k, v in sorted(prof_all.items(), key=lambda kv: -kv[1][0])}
+    # kernels timed in the region (>0 launches); with the splitter sort the onesweep passes only
+    # sort its ~N/70 samples, so their per-N byte count does not apply
+    prof = {k: v for k, v in prof.items() if v[1] > 0 and v[0] > 0}
+    if "ssort_local" in prof_all:
+        prof.pop("radix_onesweep", None)
+        prof_all = {k: v for k, v in prof_all.items() if k != "radix_onesweep" or v[1] == 0}
     dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else None
     roofline = None
     peaks = {}
@@ -539,8 +550,6 @@ def main():
             traffic_db = json.load(f)
     except OSError:
         pass
-    breakdown = {k: {"ms_per_step": v[0], "launches_per_step": v[1]}
-                 for k, v in sorted(prof_all.items(), key=lambda kv: -kv[1][0])}
     # roofline of the dominant tensor-core kernel of the step (the projection) and, beside it, of
     # the dominant HBM-bound kernel
     def hbm_roofline(kname, kms, kl):

@@ -222,6 +222,7 @@ zi_status zi_ctx_destroy(zi_ctx* ctx) {
         cudaEventDestroy(ctx->t0);
         cudaEventDestroy(ctx->t1);
         ctx->scratch.release();  // stream-ordered frees before the stream goes away
+        ctx->ss_buf.release();
         ctx->counter.release();
         ctx->flush.release();
         ctx->gm_wtab.release();
@@ -382,8 +383,9 @@ zi_status zi_index_from_descriptors(zi_ctx* ctx, const uint8_t* coords, const ui
                 uint32_t* keyw = recs.p;
                 uint32_t* val = recs.p + static_cast<size_t>(W) * n;
                 zi::interleave_coords(ctx, dc.p, keys_in, n, static_cast<int>(dims), keyw, val);
-                zi::morton_sort(ctx, keyw, val, n, static_cast<int>(dims), !ascending);
-                zi::finalize_index(ctx, keyw, val, n, 0, n, static_cast<int>(dims), nullptr, idx);
+                uint32_t* sorted[10];
+                zi::morton_sort_records(ctx, keyw, val, n, 1, static_cast<int>(dims), false, sorted, ascending);
+                zi::finalize_index(ctx, sorted[0], sorted[W], n, 0, n, static_cast<int>(dims), nullptr, idx);
                 ZI_CUDA(cudaStreamSynchronize(ctx->stream));
             } else {
                 zi::finalize_index(ctx, nullptr, nullptr, 0, 0, 0, static_cast<int>(dims), nullptr, idx);

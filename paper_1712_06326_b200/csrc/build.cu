@@ -199,7 +199,7 @@ void build_multi_index(zi_multi_index* mi) {
         }
     }
     uint32_t* sorted[10];  // the sorted records, possibly in the sort's scratch (no copy back)
-    morton_sort_layouts(ctx, keyw, val, N, D, sorted);
+    morton_sort_records(ctx, keyw, val, n, 8, D, true, sorted);
     for (int l = 0; l < 8; ++l) {
         mi->L[l].index.ctx = ctx;
         mi->L[l].index.layout_id = static_cast<uint32_t>(l);
@@ -266,7 +266,7 @@ void build_patch_index(zi_patch_index* pi) {
     quantize_interleave(ctx, pi->proj.p, pi->minmax.p, n, n, 0, D, keyw, val);
     ZI_CUDA(cudaEventRecord(e1, ctx->stream));
     uint32_t* sorted[10];
-    morton_sort_layouts(ctx, keyw, val, n, D, sorted);
+    morton_sort_records(ctx, keyw, val, n, 1, D, false, sorted);
     pi->index.ctx = ctx;
     pi->index.layout_id = 0;
     finalize_index(ctx, sorted[0], sorted[W], n, 0, n, D, pi->dict.p, &pi->index);

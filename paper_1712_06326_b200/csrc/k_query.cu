@@ -1378,6 +1378,385 @@ __global__ void __launch_bounds__(kOneThreads) k_query_one(mi_view mv, const uin
     }
 }
 
+// ===================================================================== low-latency fill-loop query
+// query_best_patch (engine.cpp:178-213) in ONE launch, tuned for latency (k <= kLatMaxK):
+//  * the target (K*K*C values + K*K flags) travels in the kernel parameters: no H2D copy;
+//  * every CTA redoes select_index + make_query (a few hundred FMAs);
+//  * blocks are dealt round-robin (block b -> CTA b % G), so the dense Morton region around the
+//    query is spread over all CTAs instead of landing on one;
+//  * each thread computes the bbox lower bounds of its blocks at once; the CTA scores its best
+//    block for a local k-th bound (atomicMin into the global bound), compacts the blocks whose
+//    bound can still win, and its 16 warps score them independently (no per-block barriers);
+//  * the CTA's exact local top-k is costed (refine ahead of the merge) and appended to a global
+//    list; the last CTA (ticket) takes the global k-th and the (cost, key) minimum, resets the
+//    workspace and publishes the result to mapped host memory.
+// Exactness: as k_query_one -- every bound is the k-th packed value of a subset of the index.
+constexpr int kLatThreads = 512;
+constexpr int kLatWarps = kLatThreads / 32;
+constexpr int kLatCap = 8192;  // a power of two: compact_buffer sorts the whole buffer
+constexpr uint32_t kLatMaxK = 256;
+constexpr int kLatMaxTarget = 1024;
+constexpr int kLatBlkRegs = 8;  // bbox bounds per thread (shared memory): nblk <= G * 512 * 8
+
+struct qlat_params {
+    mi_view mv;
+    const uint8_t* img;
+    int w;
+    qws* ws;
+    uint32_t k;
+    int norm;
+    unsigned long long* cand;
+    uint32_t* ccost;
+    unsigned long long* out;
+    qres* res;
+    uint32_t seq;
+    int want_list;
+    int tbytes;
+    uint8_t target[kLatMaxTarget];
+};
+
+template <int P>
+__global__ void __launch_bounds__(kLatThreads, P <= 3 ? 2 : 1) k_query_lat(const __grid_constant__ qlat_params prm) {
+    // s_buf kLatCap | sel kLatMaxK | tmp kOneBinCap | hist | costs kLatCap | xc | target | locals;
+    // the survivor list (<= kLatThreads * kLatBlkRegs blocks) aliases sel .. costs, which are only
+    // used after the scoring
+    extern __shared__ unsigned long long s_buf[];
+    unsigned long long* sel = s_buf + kLatCap;
+    unsigned long long* tmp = sel + kLatMaxK;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(tmp + kOneBinCap);
+    uint32_t* s_cost = hist + 256 + 2;
+    unsigned long long* s_surv = sel;
+    static_assert((kLatMaxK + kOneBinCap) * 8 + (258 + kLatCap) * 4 >= kLatThreads * kLatBlkRegs * 8, "survivor list");
+    const mi_view& mv = prm.mv;
+    const int KK = mv.K * mv.K, mc = mv.m * mv.C, C = mv.C, D = mv.D;
+    double* s_xc = reinterpret_cast<double*>(s_cost + kLatCap);
+    uint8_t* s_t = reinterpret_cast<uint8_t*>(s_xc + mc);
+    uint16_t* s_loc = reinterpret_cast<uint16_t*>(s_t + ((KK * C + KK + 1) & ~1));
+    __shared__ int s_nloc, s_lid, s_cnt, s_last, s_nsurv, s_ovf;
+    __shared__ int s_ov[8];
+    __shared__ uint8_t s_q[32];
+    __shared__ unsigned long long s_bound, s_wmin[kLatWarps];
+    qws* ws = prm.ws;
+    const uint32_t k = prm.k;
+    const int norm = prm.norm;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    ZI_TPHASE(0)
+    for (int i = tid; i < prm.tbytes; i += kLatThreads) s_t[i] = prm.target[i];
+    if (tid < 32) s_q[tid] = 0;
+    if (tid == 0) {
+        s_cnt = 0;
+        s_nsurv = 0;
+        s_ovf = 0;
+    }
+    __syncthreads();
+    const uint8_t* tv = s_t;
+    const uint8_t* tk = s_t + KK * C;
+    if (warp == 8) {  // known locals, ascending (known_locals_of, engine.cpp:16-22)
+        int c = 0;
+        for (int base = 0; base < KK; base += 32) {
+            const bool kn = base + lane < KK && tk[base + lane] != 0;
+            const unsigned mk = __ballot_sync(0xffffffffu, kn);
+            if (kn) s_loc[c + __popc(mk & ((1u << lane) - 1u))] = static_cast<uint16_t>(base + lane);
+            c += __popc(mk);
+        }
+        if (lane == 0) s_nloc = c;
+    }
+    if (warp < 8) {  // select_index (engine.cpp:162-176)
+        int ov = 0;
+        for (int p = lane; p < mv.m; p += 32) ov += tk[mv.local[warp * mv.m + p]] != 0;
+        ov = __reduce_add_sync(0xffffffffu, ov);
+        if (lane == 0) s_ov[warp] = ov;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int best = 0, bid = 0;
+        for (int l = 0; l < 8; ++l)
+            if (s_ov[l] > best) {
+                best = s_ov[l];
+                bid = l;
+            }
+        s_lid = bid;
+    }
+    __syncthreads();
+    const int lid = s_lid;
+    {  // make_query (builder.cpp:110-127): x - mean staged, then the canonical fp64 chain per dim
+        const double* mean = mv.mean + static_cast<size_t>(lid) * mc;
+        const int32_t* loc = mv.local + lid * mv.m;
+        for (int j = tid; j < mc; j += kLatThreads) {
+            const int l = loc[j / C];
+            const double mj = mean[j];
+            const double x = tk[l] ? static_cast<double>(tv[l * C + j % C]) : mj;
+            s_xc[j] = __dsub_rn(x, mj);
+        }
+    }
+    __syncthreads();
+    if (tid < D) {
+        const double* comp = mv.comp + static_cast<size_t>(lid) * mc * D + tid;
+        double y = 0.0;
+        int j = 0;
+        for (; j + 8 <= mc; j += 8) {  // eight component loads in flight ahead of the chain
+            double cc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cc[u] = __ldg(comp + static_cast<size_t>(j + u) * D);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) y = __fma_rn(cc[u], s_xc[j + u], y);
+        }
+        for (; j < mc; ++j) y = __fma_rn(__ldg(comp + static_cast<size_t>(j) * D), s_xc[j], y);
+        const unsigned long long* mm = mv.minmax + static_cast<size_t>(lid) * 2 * D;
+        s_q[tid] = quantize_rn(ordered_to_double_hd(mm[tid]), ordered_to_double_hd(mm[D + tid]), y);
+    }
+    __syncthreads();
+    uint32_t q4[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+        q4[p] = static_cast<uint32_t>(s_q[4 * p]) | (static_cast<uint32_t>(s_q[4 * p + 1]) << 8) |
+                (static_cast<uint32_t>(s_q[4 * p + 2]) << 16) | (static_cast<uint32_t>(s_q[4 * p + 3]) << 24);
+    ZI_TPHASE(1)
+    const index_view v = mv.idx[lid];
+    const uint64_t nblk = v.nblk, G = gridDim.x, c0 = blockIdx.x;
+    // bbox lower bounds of this CTA's blocks b = c0 + G*i, i = tid + kLatThreads*r, kept as packed
+    // (lb<<32 | b) in the upper half of s_buf (the candidates start at its bottom)
+    unsigned long long* s_lbb = s_buf + (kLatCap - kLatThreads * kLatBlkRegs);
+    unsigned long long mine = kU64Max;
+#pragma unroll 4
+    for (int r = 0; r < kLatBlkRegs; ++r) {
+        const uint64_t b = c0 + G * (static_cast<uint64_t>(tid) + static_cast<uint64_t>(kLatThreads) * r);
+        unsigned long long e = kU64Max;
+        if (b < nblk) {
+            uint32_t lb = 0;
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                lb = gap4(q4[p], __ldg(v.bmin + static_cast<size_t>(p) * nblk + b),
+                          __ldg(v.bmax + static_cast<size_t>(p) * nblk + b), norm, lb);
+            e = (static_cast<unsigned long long>(lb) << 32) | b;
+            mine = e < mine ? e : mine;
+        }
+        s_lbb[tid + kLatThreads * r] = e;
+    }
+    mine = warp_min(mine);
+    if (lane == 0) s_wmin[warp] = mine;
+    __syncthreads();
+    const unsigned long long seed = [&] {
+        unsigned long long m = kU64Max;
+#pragma unroll
+        for (int w = 0; w < kLatWarps; ++w) m = s_wmin[w] < m ? s_wmin[w] : m;
+        return m;
+    }();
+    if (warp == 0) {  // score the best block: its k-th distance bounds the answer
+        unsigned long long c[8];
+        if (seed != kU64Max) {
+            score_block<P>(v, seed & 0xffffffffull, q4, norm, c);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c[e] = kU64Max;
+        }
+        int valid = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) valid += c[e] != kU64Max;
+        valid = __reduce_add_sync(0xffffffffu, valid);
+        unsigned long long lbound = kU64Max;
+        if (valid >= static_cast<int>(k)) {  // k-th smallest distance by radix descent
+            uint32_t T = 0;
+            int need = static_cast<int>(k);
+            for (int bit = 31; bit >= 0; --bit) {
+                int cnt = 0;
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    cnt += c[e] != kU64Max && (static_cast<uint32_t>(c[e] >> 32) >> bit) == (T >> bit);
+                cnt = __reduce_add_sync(0xffffffffu, cnt);
+                if (cnt < need) {
+                    need -= cnt;
+                    T |= 1u << bit;
+                }
+            }
+            lbound = (static_cast<unsigned long long>(T) << 32) | 0xffffffffull;
+        }
+        const unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+        const unsigned long long bnd = g < lbound ? g : lbound;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)  // the seed block's own candidates
+            if (c[e] != kU64Max && c[e] <= bnd) s_buf[atomicAdd(&s_cnt, 1)] = c[e];
+        if (lane == 0) {
+            s_bound = lbound;
+            if (lbound < g) atomicMin(&ws->bound, lbound);
+        }
+    }
+    __syncthreads();
+    ZI_TPHASE(2)
+    {  // blocks that can still hold a winner (the seed block is done)
+        const unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+        const unsigned long long bnd = g < s_bound ? g : s_bound;
+        for (int r = 0; r < kLatBlkRegs; ++r) {
+            const unsigned long long e = s_lbb[tid + kLatThreads * r];
+            if (e != kU64Max && e != seed && (e & 0xffffffff00000000ull) <= bnd) s_surv[atomicAdd(&s_nsurv, 1)] = e;
+        }
+    }
+    __syncthreads();
+    const int nsurv = s_nsurv;
+    // score the survivors, kLatWarps blocks at a time; a round never overfills the buffer
+    for (int s0 = 0; s0 < nsurv; s0 += kLatWarps) {
+        const int si = s0 + warp;
+        if (si < nsurv) {
+            const unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+            const unsigned long long bnd = g < s_bound ? g : s_bound;
+            const unsigned long long e0 = s_surv[si];
+            if ((e0 & 0xffffffff00000000ull) <= bnd) {
+                unsigned long long c[8];
+                score_block<P>(v, e0 & 0xffffffffull, q4, norm, c);
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (c[e] != kU64Max && c[e] <= bnd) s_buf[atomicAdd(&s_cnt, 1)] = c[e];
+            }
+        }
+        if (s0 + kLatWarps < nsurv) {
+            __syncthreads();
+            if (s_cnt > kLatCap - kLatWarps * 256) compact_buffer(s_buf, &s_cnt, &s_bound, k, ws, true);
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    ZI_TPHASE(3)
+    {  // exact local top-k (unsorted), then the winners that can still make the global top-k
+        const int m0 = s_cnt;
+        uint32_t mx = 0;
+        for (int t = tid; t < m0; t += kLatThreads) mx = max(mx, static_cast<uint32_t>(s_buf[t] >> 32));
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        __shared__ uint32_t s_mx;
+        if (tid == 0) s_mx = 0;
+        __syncthreads();
+        if (lane == 0) atomicMax(&s_mx, mx);
+        __syncthreads();
+        int cnt = select_topk(s_buf, m0, k, sel, tmp, kOneBinCap, hist, 256, s_mx, false);
+        if (cnt < 0) {  // degenerate boundary bin: exact sort-based compaction instead
+            compact_buffer(s_buf, &s_cnt, &s_bound, k, ws, true);
+            cnt = s_cnt;
+            for (int t = tid; t < cnt; t += kLatThreads) sel[t] = s_buf[t];
+            __syncthreads();
+        }
+        __shared__ unsigned long long s_kth, s_gb;
+        __shared__ int s_keep;
+        if (tid == 0) {
+            s_kth = 0;
+            s_keep = 0;
+        }
+        __syncthreads();
+        unsigned long long kth = 0;
+        for (int t = tid; t < cnt; t += kLatThreads) kth = sel[t] > kth ? sel[t] : kth;
+        if (cnt >= static_cast<int>(k)) {
+            atomicMax(&s_kth, kth);
+            __syncthreads();
+            if (tid == 0) atomicMin(&ws->bound, s_kth);
+        }
+        __syncthreads();
+        if (tid == 0) s_gb = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+        __syncthreads();
+        const unsigned long long gb = s_gb;
+        for (int t = tid; t < cnt; t += kLatThreads)
+            if (sel[t] <= gb) tmp[atomicAdd(&s_keep, 1)] = sel[t];
+        __syncthreads();
+        const int keep = s_keep;
+        cost_candidates(prm.img, prm.w, C, mv.K, s_t, s_loc, s_nloc, tmp, keep, norm, s_cost);
+        __shared__ uint32_t s_gbase;
+        if (tid == 0) s_gbase = atomicAdd(&ws->gcount, static_cast<uint32_t>(keep));
+        __syncthreads();
+        for (int t = tid; t < keep; t += kLatThreads) {
+            prm.cand[s_gbase + t] = tmp[t];
+            prm.ccost[s_gbase + t] = s_cost[t];
+        }
+    }
+    ZI_TPHASE(4)
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&ws->done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    ZI_TPHASE(6)
+    int m;
+    uint32_t maxd, total;
+    {  // compact global list -> candidates <= the final bound
+        __shared__ int s_m;
+        __shared__ uint32_t s_maxd;
+        if (tid == 0) {
+            s_m = 0;
+            s_maxd = 0;
+        }
+        __syncthreads();
+        total = *reinterpret_cast<volatile uint32_t*>(&ws->gcount);
+        const unsigned long long bound = *reinterpret_cast<volatile unsigned long long*>(&ws->bound);
+        for (uint32_t f = tid; f < total; f += kLatThreads) {
+            const unsigned long long c = __ldcg(prm.cand + f);
+            if (c <= bound) {
+                const int slot = atomicAdd(&s_m, 1);
+                if (slot < kLatCap) {
+                    s_buf[slot] = c;
+                    s_cost[slot] = __ldcg(prm.ccost + f);
+                }
+                atomicMax(&s_maxd, static_cast<uint32_t>(c >> 32));
+            }
+        }
+        __syncthreads();
+        m = s_m;
+        maxd = s_maxd;
+    }
+    ZI_TPHASE(7)
+    const unsigned long long T = m > kLatCap ? kU64Max - 1 : kth_packed(s_buf, m, k, tmp, kOneBinCap, hist, 256, maxd);
+    int cnt = T == kU64Max - 1 ? -1 : (m < static_cast<int>(k) ? m : static_cast<int>(k));
+    if (cnt >= 0 && prm.want_list) cnt = select_sorted_topk(s_buf, m, k, sel, tmp, kOneBinCap, hist, 256, maxd);
+    ZI_TPHASE(8)
+    if (tid == 0) {
+        ws->lid = static_cast<uint32_t>(lid);
+        ws->dbg_total = total;
+        ws->dbg_m = static_cast<uint32_t>(m);
+        ws->final_bound = ws->bound;
+        ws->done = 0;
+        ws->gcount = 0;
+    }
+    if (cnt < 0) {
+        if (tid == 0) {
+            ws->overflow = 2;
+            if (prm.res) {
+                prm.res->lid = static_cast<uint32_t>(lid);
+                prm.res->overflow = 2;
+                __threadfence_system();
+                prm.res->seq = prm.seq;
+            }
+        }
+        return;  // host: the multi-launch path re-runs this query
+    }
+    if (prm.want_list)
+        for (int i = tid; i < cnt; i += kLatThreads) prm.out[i] = sel[i];
+    {
+        __shared__ unsigned long long s_best;
+        if (tid == 0) s_best = kU64Max;
+        __syncthreads();
+        unsigned long long best = kU64Max;
+        for (int i = tid; i < m; i += kLatThreads)
+            if (s_buf[i] <= T) {
+                const unsigned long long c = pack_candidate(s_cost[i], static_cast<uint32_t>(s_buf[i] & 0xffffffffu));
+                best = c < best ? c : best;
+            }
+        best = warp_min(best);
+        if (lane == 0) atomicMin(&s_best, best);
+        __syncthreads();
+        if (tid == 0) ws->best = s_best;
+    }
+    ZI_TPHASE(9)
+    if (tid == 0) {
+        ws->count = static_cast<uint32_t>(cnt);
+        ws->overflow = 0;
+        ws->bound = kU64Max;  // the workspace is left ready for the next query
+        if (prm.res) {
+            prm.res->best = ws->best;
+            prm.res->lid = static_cast<uint32_t>(lid);
+            prm.res->count = static_cast<uint32_t>(cnt);
+            prm.res->overflow = 0;
+            __threadfence_system();
+            prm.res->seq = prm.seq;
+        }
+    }
+}
+
 // ===================================================================== fused single-CTA query
 // The fill loop's per-iteration query in ONE launch (1024 threads): stage the target,
 // select_index, make_query, seed the bound from the 8 blocks with the smallest bbox lower bound,
@@ -2009,7 +2388,12 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
     uint8_t* stage = mi->hstage.ensure(res_off + sizeof(qws));
     std::memcpy(stage, h_tv, KK * mi->C);
     std::memcpy(stage + KK * mi->C, h_tk, KK);
-    ZI_CUDA(cudaMemcpyAsync(s.target, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
+    bool target_on_device = false;  // the low-latency kernel takes the target in its parameters
+    auto upload_target = [&] {
+        if (target_on_device) return;
+        ZI_CUDA(cudaMemcpyAsync(s.target, stage, tbytes, cudaMemcpyHostToDevice, ctx->stream));
+        target_on_device = true;
+    };
     const mi_view mv = mi_view_of(mi);
     qws* hq = reinterpret_cast<qws*>(stage + res_off);
     const size_t rsmem = ((KK * mi->C + 1) & ~size_t(1)) + (KK + 16) * sizeof(uint16_t) + kRefineSlots * sizeof(uint32_t) + 32;
@@ -2031,7 +2415,71 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
         mi->qws_clean = false;
         mi->qws_last = s.ws;
     }
-    if (k <= kOneMaxK && one_smem <= 220 * 1024 && !force_multi) {
+    static const bool use_one = std::getenv("ZI_QUERY_ONE") != nullptr;
+    static const int lat_g = [] { const char* e = std::getenv("ZI_QLAT_G"); return e ? std::atoi(e) : 0; }();
+    const size_t lat_smem = (kLatCap + kLatMaxK + kOneBinCap) * sizeof(unsigned long long) +
+                            (256 + 2 + kLatCap) * sizeof(uint32_t) + static_cast<size_t>(mi->mc) * sizeof(double) +
+                            tbytes + 2 + KK * 2 + 16;
+    const uint64_t lat_g_max = static_cast<uint64_t>(std::min(s.G, 2 * ctx->num_sms));
+    const uint64_t G2 = std::min<uint64_t>(std::max<uint64_t>(nblk, 1),
+                                           lat_g > 0 ? static_cast<uint64_t>(lat_g) : lat_g_max);
+    if (!use_one && !force_multi && k <= kLatMaxK && tbytes <= static_cast<size_t>(kLatMaxTarget) &&
+        lat_smem <= 112 * 1024 && nblk <= G2 * kLatThreads * kLatBlkRegs) {
+        if (!mi->qws_clean) {
+            ZI_CUDA(cudaMemsetAsync(&s.ws->bound, 0xff, sizeof(unsigned long long), ctx->stream));
+            ZI_CUDA(cudaMemsetAsync(&s.ws->done, 0, 2 * sizeof(uint32_t), ctx->stream));  // done + gcount
+        }
+        const uint32_t seq = ++mi->qseq;
+        qlat_params prm;
+        prm.mv = mv;
+        prm.img = mi->image.p;
+        prm.w = mi->w;
+        prm.ws = s.ws;
+        prm.k = k;
+        prm.norm = norm;
+        prm.cand = s.cand;
+        prm.ccost = s.ccost;
+        prm.out = s.out;
+        prm.res = reinterpret_cast<qres*>(mi->dres);
+        prm.seq = seq;
+        prm.want_list = knn_out != nullptr ? 1 : 0;
+        prm.tbytes = static_cast<int>(tbytes);
+        std::memcpy(prm.target, h_tv, KK * mi->C);
+        std::memcpy(prm.target + KK * mi->C, h_tk, KK);
+        switch (mv.idx[0].P) {
+#define ZI_LAT_CASE(PP)                                                                                     \
+    case PP:                                                                                                \
+        smem_attr(ctx->device, k_query_lat<PP>, lat_smem);                                                  \
+        ZI_LAUNCH(ctx, "query_one", k_query_lat<PP>, static_cast<unsigned>(G2), kLatThreads, lat_smem, prm); \
+        break;
+            ZI_LAT_CASE(1) ZI_LAT_CASE(2) ZI_LAT_CASE(3) ZI_LAT_CASE(4)
+            ZI_LAT_CASE(5) ZI_LAT_CASE(6) ZI_LAT_CASE(7) ZI_LAT_CASE(8)
+#undef ZI_LAT_CASE
+            default: throw error(ZI_E_INVALID, "dims above 32");
+        }
+        if (debug_query || ctx->profiling) {
+            ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        } else {
+            unsigned spins = 0;
+            while (hr->seq != seq) {
+                if ((++spins & 1023u) == 0) {
+                    const cudaError_t e = cudaStreamQuery(ctx->stream);
+                    if (e != cudaSuccess && e != cudaErrorNotReady) ZI_CUDA(e);
+                    if (e == cudaSuccess && hr->seq != seq) throw error(ZI_E_RUNTIME, "query result not published");
+                }
+            }
+            std::atomic_thread_fence(std::memory_order_acquire);
+            hq->best = hr->best;
+            hq->lid = hr->lid;
+            hq->count = hr->count;
+            hq->overflow = hr->overflow;
+        }
+        mi->qws_clean = hq->overflow == 0;
+        if (hq->overflow == 0) done = true;  // else: the multi-launch path below answers it
+    }
+    if (!done) upload_target();
+    if (!done && k <= kOneMaxK && one_smem <= 220 * 1024 && !force_multi) {
         const int G1 = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(nblk, 1),
                                                            std::min<uint64_t>(static_cast<uint64_t>(s.G), 2ull * ctx->num_sms)));
         if (!mi->qws_clean) {

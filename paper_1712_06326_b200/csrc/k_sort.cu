@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -29,28 +30,63 @@ struct sort_words {
     uint32_t* out[kMaxWords];
 };
 
-// Histograms of every pass in one read: hist[q*256 + digit]
+// Histograms of every pass in one read: hist[(q*G + g)*256 + digit] for records in groups of gn
+// (group g = records [g*gn, (g+1)*gn)).  Each CTA reads a contiguous chunk (at most a few group
+// changes, flushed as they come); per pass a warp's equal digits are merged with match_any, so a
+// hot digit (the clustered top Morton bytes) costs one shared atomic per warp, not 32.
 __global__ void __launch_bounds__(256) k_sort_hist(sort_words io, int npass, const int2* __restrict__ passes,
-                                                   uint64_t n, uint32_t* __restrict__ hist) {
+                                                   uint64_t n, uint64_t gn, int G, uint32_t* __restrict__ hist) {
     extern __shared__ uint32_t s_hist[];  // npass*256
     __shared__ int2 s_pass[40];
-    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) s_hist[i] = 0;
+    const int nb = npass * 256;
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s_hist[i] = 0;
     if (threadIdx.x < npass) s_pass[threadIdx.x] = passes[threadIdx.x];
     __syncthreads();
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        for (int q = 0; q < npass; ++q) {
-            const uint32_t d = (io.in[s_pass[q].x][i] >> s_pass[q].y) & 0xffu;
-            atomicAdd(&s_hist[q * 256 + d], 1u);
+    const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t c0 = static_cast<uint64_t>(blockIdx.x) * chunk;
+    const uint64_t c1 = c0 + chunk < n ? c0 + chunk : n;
+    auto flush = [&](int g) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+            const uint32_t v = s_hist[i];
+            if (v) {
+                atomicAdd(&hist[(static_cast<size_t>(i >> 8) * G + g) * 256 + (i & 255)], v);
+                s_hist[i] = 0;
+            }
         }
+        __syncthreads();
+    };
+    uint64_t seg = c0;
+    while (seg < c1) {  // the part of the chunk inside one group
+        const int g = G > 1 ? static_cast<int>(seg / gn) : 0;
+        const uint64_t gend = G > 1 ? (static_cast<uint64_t>(g) + 1) * gn : n;
+        const uint64_t e = gend < c1 ? gend : c1;
+        constexpr int U = 4;  // records per thread per round (loads in flight)
+        for (uint64_t b = seg; b < e; b += static_cast<uint64_t>(blockDim.x) * U) {  // whole warps (match_any)
+            for (int q = 0; q < npass; ++q) {
+                const uint32_t* wq = io.in[s_pass[q].x];
+                const int sh = s_pass[q].y;
+                uint32_t v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint64_t i = b + static_cast<uint64_t>(u) * blockDim.x + threadIdx.x;
+                    v[u] = i < e ? (__ldg(wq + i) >> sh) & 0xffu : 256u;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t peers = __match_any_sync(0xffffffffu, v[u]);
+                    if (v[u] < 256u && (__ffs(peers) - 1) == lane) atomicAdd(&s_hist[q * 256 + v[u]], __popc(peers));
+                }
+            }
+        }
+        flush(g);
+        seg = e;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x)
-        if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
 }
 
-// exclusive scans of the digit histograms (one block per pass): the onesweep bases, on the
-// device, when the host does not need to see the histograms
+// exclusive scans of the digit histograms (one block per (pass, group)): the onesweep bases, on
+// the device, when the host does not need to see the histograms
 __global__ void __launch_bounds__(256) k_sort_bases(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases) {
     __shared__ uint32_t s_w[8];
     const int q = blockIdx.x, d = threadIdx.x, lane = d & 31, warp = d >> 5;
@@ -68,11 +104,15 @@ __global__ void __launch_bounds__(256) k_sort_bases(const uint32_t* __restrict__
     bases[q * 256 + d] = wp + x - c;
 }
 
+// One stable digit pass.  Records come in groups of gn (group-major; G = 1: one group); a group
+// is tiled on its own (tpg tiles) and sorted on its own: digit_base holds the exclusive digit
+// prefix of each group ([g][256]), the decoupled look-back stops at the group's first tile.
 template <int NW>
 __global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort_words io, int dw, int ds,
                                                            const uint32_t* __restrict__ digit_base,
                                                            uint32_t* __restrict__ status,
-                                                           uint32_t* __restrict__ tile_ctr, uint64_t n) {
+                                                           uint32_t* __restrict__ tile_ctr, uint64_t gn,
+                                                           uint32_t tpg) {
     extern __shared__ uint32_t s_stage[];  // NW * kSortTile
     __shared__ uint32_t s_hist[kSortWarps][256];
     __shared__ uint32_t s_start[256];
@@ -85,7 +125,10 @@ __global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort
     if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
-    const uint64_t tbase = static_cast<uint64_t>(tile) * kSortTile;
+    const uint32_t grp = tile / tpg, tig = tile - grp * tpg;  // group, tile inside the group
+    const uint64_t gbase = static_cast<uint64_t>(grp) * gn;
+    const uint64_t tbase = gbase + static_cast<uint64_t>(tig) * kSortTile;
+    const uint64_t n = gbase + gn;  // end of the group
     const uint64_t wbase = tbase + warp * (kSortItems * 32);
 
     // every word of the tile's records is loaded up front (maximum loads in flight)
@@ -127,7 +170,7 @@ __global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort
     }
     const uint32_t tile_cnt = run;
     volatile uint32_t* vstatus = status;
-    if (tile == 0) vstatus[d] = kFlagInc | tile_cnt;
+    if (tig == 0) vstatus[static_cast<size_t>(tile) * 256 + d] = kFlagInc | tile_cnt;
     else vstatus[static_cast<size_t>(tile) * 256 + d] = kFlagAgg | tile_cnt;
 
     // tile-local exclusive scan over digits
@@ -147,7 +190,7 @@ __global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort
 
     // decoupled look-back for the prefix of digit d over the previous tiles
     uint32_t prefix = 0;
-    if (tile > 0) {
+    if (tig > 0) {
         int64_t j = static_cast<int64_t>(tile) - 1;
         while (true) {
             const uint32_t v = vstatus[static_cast<size_t>(j) * 256 + d];
@@ -159,7 +202,7 @@ __global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort
         }
         vstatus[static_cast<size_t>(tile) * 256 + d] = kFlagInc | (prefix + tile_cnt);
     }
-    s_gofs[d] = digit_base[d] + prefix;
+    s_gofs[d] = static_cast<uint32_t>(gbase) + digit_base[grp * 256 + d] + prefix;
     __syncthreads();
 
     // stage records in tile-sorted order
@@ -183,19 +226,21 @@ __global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort
 
 template <int NW>
 static void launch_onesweep(zi_ctx* ctx, const sort_words& io, int dw, int ds, const uint32_t* base, uint32_t* status,
-                            uint32_t* ctr, uint64_t n, unsigned ntiles) {
+                            uint32_t* ctr, uint64_t gn, unsigned tpg, unsigned ntiles) {
     const size_t smem = static_cast<size_t>(NW) * kSortTile * sizeof(uint32_t);
     smem_attr(ctx->device, k_onesweep<NW>, kMaxWords * kSortTile * sizeof(uint32_t));
-    ZI_LAUNCH(ctx, "radix_onesweep", k_onesweep<NW>, ntiles, kSortThreads, smem, io, dw, ds, base, status, ctr, n);
+    ZI_LAUNCH(ctx, "radix_onesweep", k_onesweep<NW>, ntiles, kSortThreads, smem, io, dw, ds, base, status, ctr, gn,
+              tpg);
 }
 
 // Generic stable LSD sort of NW-word SoA records; passes are (word, shift) digits from the
-// least significant.  Trivial passes (all records share the digit) are skipped.
-// digit histograms of every pass (host copy, pass-major 256 bins), one read of the records
+// least significant.  Trivial passes (every group's records share the digit) are skipped.
+// G groups of n/G records (group-major) are sorted each on its own (no pass on a group digit).
+// digit histograms of every pass (host copy, [pass][group][256]), one read of the records
 std::vector<uint32_t> pass_histograms(zi_ctx* ctx, uint32_t* const* words, int nw, uint64_t n,
-                                      const std::vector<int2>& passes) {
+                                      const std::vector<int2>& passes, int G) {
     const int npass = static_cast<int>(passes.size());
-    const size_t hist_words = static_cast<size_t>(npass) * 256;
+    const size_t hist_words = static_cast<size_t>(npass) * G * 256;
     uint32_t* h = ctx->counter.ensure(hist_words + 4 * npass + 64);
     int2* d_passes = reinterpret_cast<int2*>(h + hist_words + 8);
     d_passes = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(d_passes) + 15) & ~uintptr_t(15));
@@ -204,27 +249,35 @@ std::vector<uint32_t> pass_histograms(zi_ctx* ctx, uint32_t* const* words, int n
     sort_words io{};
     for (int k = 0; k < nw; ++k) io.in[k] = words[k];
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 4));
-    ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hist_words * sizeof(uint32_t), io, npass, d_passes, n, h);
+    smem_attr(ctx->device, k_sort_hist, static_cast<size_t>(npass) * 256 * sizeof(uint32_t));
+    ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, static_cast<size_t>(npass) * 256 * sizeof(uint32_t), io, npass,
+              d_passes, n, n / G, G, h);
     std::vector<uint32_t> out(hist_words);
     ZI_CUDA(cudaMemcpyAsync(out.data(), h, hist_words * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     return out;
 }
 
+// groups G > 1: at most 40 passes, digit bases per (pass, group) in the scratch
+static bool groups_fit(int npass, int G) { return npass <= 40 && G <= 8; }
+
 // result (optional): receives the buffers holding the sorted words -- the scratch copy after an
 // odd number of passes -- instead of copying them back into `words`
 void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
-                      const uint32_t* hist_host, bool device_bases, uint32_t** result) {
+                      const uint32_t* hist_host, bool device_bases, uint32_t** result, int G) {
     if (result)
         for (int k = 0; k < nw; ++k) result[k] = words[k];
     if (n <= 1 || passes.empty()) return;
     if (n > kValMask) throw error(ZI_E_INVALID, "radix sort: more than 2^30 records");
     if (nw > kMaxWords) throw error(ZI_E_INVALID, "radix sort: too many words");
+    if (G < 1 || n % G != 0) throw error(ZI_E_INVALID, "radix sort: records do not split into equal groups");
     const int npass = static_cast<int>(passes.size());
-    const unsigned ntiles = static_cast<unsigned>((n + kSortTile - 1) / kSortTile);
-    // scratch layout: alt words (nw*n) | hist (npass*256) | bases (npass*256) | status (npass*ntiles*256) | ctr
+    const uint64_t gn = n / G;
+    const unsigned tpg = static_cast<unsigned>((gn + kSortTile - 1) / kSortTile);
+    const unsigned ntiles = tpg * static_cast<unsigned>(G);
+    // scratch layout: alt words (nw*n) | hist (npass*G*256) | bases (same) | status (npass*ntiles*256) | ctr
     const size_t alt_words = static_cast<size_t>(nw) * n;
-    const size_t hist_words = static_cast<size_t>(npass) * 256;
+    const size_t hist_words = static_cast<size_t>(npass) * G * 256;
     const size_t status_words = static_cast<size_t>(npass) * ntiles * 256;
     uint32_t* scr = reinterpret_cast<uint32_t*>(
         ctx->scratch.ensure((alt_words + 2 * hist_words + status_words + 4 * npass + 64) * sizeof(uint32_t)));
@@ -246,27 +299,36 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
     std::vector<uint32_t> h_hist(hist_words);
     std::vector<int> active;
     std::vector<uint32_t> h_bases(hist_words, 0);
-    if (device_bases) {  // no host round trip: every pass runs (trivial ones are a copy)
+    auto run_hist = [&] {
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 4));
-        ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hist_words * sizeof(uint32_t), io, npass, d_passes, n, hist);
-        ZI_LAUNCH(ctx, "radix_bases", k_sort_bases, npass, 256, 0, hist, bases);
+        const size_t hsm = static_cast<size_t>(npass) * 256 * sizeof(uint32_t);
+        smem_attr(ctx->device, k_sort_hist, hsm);
+        ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hsm, io, npass, d_passes, n, gn, G, hist);
+    };
+    if (device_bases) {  // no host round trip: every pass runs (trivial ones are a copy)
+        run_hist();
+        ZI_LAUNCH(ctx, "radix_bases", k_sort_bases, static_cast<unsigned>(npass * G), 256, 0, hist, bases);
         for (int q = 0; q < npass; ++q) active.push_back(q);
     } else if (hist_host) {
         std::copy(hist_host, hist_host + hist_words, h_hist.begin());
     } else {
-        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 4));
-        ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hist_words * sizeof(uint32_t), io, npass, d_passes, n, hist);
+        run_hist();
         ZI_CUDA(cudaMemcpyAsync(h_hist.data(), hist, hist_words * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));
     }
     for (int q = 0; q < npass && !device_bases; ++q) {
-        bool trivial = false;
-        uint32_t run = 0;
-        for (int dgt = 0; dgt < 256; ++dgt) {
-            const uint32_t c = h_hist[q * 256 + dgt];
-            if (c == n) trivial = true;
-            h_bases[q * 256 + dgt] = run;
-            run += c;
+        bool trivial = true;
+        for (int g = 0; g < G; ++g) {
+            bool gt = false;
+            uint32_t run = 0;
+            for (int dgt = 0; dgt < 256; ++dgt) {
+                const size_t at = (static_cast<size_t>(q) * G + g) * 256 + dgt;
+                const uint32_t c = h_hist[at];
+                if (c == gn) gt = true;
+                h_bases[at] = run;
+                run += c;
+            }
+            trivial = trivial && gt;
         }
         if (!trivial) active.push_back(q);
     }
@@ -288,15 +350,17 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
             io.out[k] = oth[k];
         }
         uint32_t* st = status + static_cast<size_t>(q) * ntiles * 256;
+        const uint32_t* qb = bases + static_cast<size_t>(q) * G * 256;
+        const int dw = passes[q].x, ds = passes[q].y;
         switch (nw) {
-            case 2: launch_onesweep<2>(ctx, io, passes[q].x, passes[q].y, bases + q * 256, st, ctr + q, n, ntiles); break;
-            case 3: launch_onesweep<3>(ctx, io, passes[q].x, passes[q].y, bases + q * 256, st, ctr + q, n, ntiles); break;
-            case 4: launch_onesweep<4>(ctx, io, passes[q].x, passes[q].y, bases + q * 256, st, ctr + q, n, ntiles); break;
-            case 5: launch_onesweep<5>(ctx, io, passes[q].x, passes[q].y, bases + q * 256, st, ctr + q, n, ntiles); break;
-            case 6: launch_onesweep<6>(ctx, io, passes[q].x, passes[q].y, bases + q * 256, st, ctr + q, n, ntiles); break;
-            case 7: launch_onesweep<7>(ctx, io, passes[q].x, passes[q].y, bases + q * 256, st, ctr + q, n, ntiles); break;
-            case 8: launch_onesweep<8>(ctx, io, passes[q].x, passes[q].y, bases + q * 256, st, ctr + q, n, ntiles); break;
-            case 9: launch_onesweep<9>(ctx, io, passes[q].x, passes[q].y, bases + q * 256, st, ctr + q, n, ntiles); break;
+            case 2: launch_onesweep<2>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
+            case 3: launch_onesweep<3>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
+            case 4: launch_onesweep<4>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
+            case 5: launch_onesweep<5>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
+            case 6: launch_onesweep<6>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
+            case 7: launch_onesweep<7>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
+            case 8: launch_onesweep<8>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
+            case 9: launch_onesweep<9>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
             default: throw error(ZI_E_INVALID, "radix sort: unsupported record width");
         }
         for (int k = 0; k < nw; ++k) std::swap(cur[k], oth[k]);
@@ -310,8 +374,13 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
 }
 
 void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
+                      const uint32_t* hist_host, bool device_bases, uint32_t** result) {
+    radix_sort_words(ctx, words, nw, n, passes, hist_host, device_bases, result, 1);
+}
+
+void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
                       const uint32_t* hist_host, bool device_bases) {
-    radix_sort_words(ctx, words, nw, n, passes, hist_host, device_bases, nullptr);
+    radix_sort_words(ctx, words, nw, n, passes, hist_host, device_bases, nullptr, 1);
 }
 
 // ---------------------------------------------------------------------------- hybrid sort
@@ -677,8 +746,11 @@ static void launch_segsort(zi_ctx* ctx, uint32_t* const* words, uint64_t N, int 
 }
 
 // window sort + oversized-segment handling after the MSD passes
+// all: the passes of the full (grouped, G > 1: no layout digit) LSD sort; all_full: every pass,
+// layout digit included (the window replay and sub-range sorts, which can straddle two layouts)
 static void finish_hybrid(zi_ctx* ctx, uint32_t** words, uint32_t** orig, int W, uint64_t N, int D, int nb,
-                          bool layouts, const std::vector<int2>& all, int& learnt) {
+                          bool layouts, const std::vector<int2>& all, const std::vector<int2>& all_full, int G,
+                          int& learnt) {
     const int nw = W + 1;
     static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
     // counters | big-segment list | pass table, in the context counter buffer
@@ -688,14 +760,14 @@ static void finish_hybrid(zi_ctx* ctx, uint32_t** words, uint32_t** orig, int W,
     unsigned long long* sumL = reinterpret_cast<unsigned long long*>(cnt + 2);  // sum of L^2 over segments
     ZI_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), ctx->stream));
     switch (nw) {
-        case 2: launch_segsort<2>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
-        case 3: launch_segsort<3>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
-        case 4: launch_segsort<4>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
-        case 5: launch_segsort<5>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
-        case 6: launch_segsort<6>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
-        case 7: launch_segsort<7>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
-        case 8: launch_segsort<8>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
-        case 9: launch_segsort<9>(ctx, words, N, D, nb, layouts, all, d_passes, big, cnt, sumL); break;
+        case 2: launch_segsort<2>(ctx, words, N, D, nb, layouts, all_full, d_passes, big, cnt, sumL); break;
+        case 3: launch_segsort<3>(ctx, words, N, D, nb, layouts, all_full, d_passes, big, cnt, sumL); break;
+        case 4: launch_segsort<4>(ctx, words, N, D, nb, layouts, all_full, d_passes, big, cnt, sumL); break;
+        case 5: launch_segsort<5>(ctx, words, N, D, nb, layouts, all_full, d_passes, big, cnt, sumL); break;
+        case 6: launch_segsort<6>(ctx, words, N, D, nb, layouts, all_full, d_passes, big, cnt, sumL); break;
+        case 7: launch_segsort<7>(ctx, words, N, D, nb, layouts, all_full, d_passes, big, cnt, sumL); break;
+        case 8: launch_segsort<8>(ctx, words, N, D, nb, layouts, all_full, d_passes, big, cnt, sumL); break;
+        case 9: launch_segsort<9>(ctx, words, N, D, nb, layouts, all_full, d_passes, big, cnt, sumL); break;
         default: throw error(ZI_E_INVALID, "radix sort: unsupported record width");
     }
     uint32_t hc[4] = {0, 0, 0, 0};
@@ -724,7 +796,7 @@ static void finish_hybrid(zi_ctx* ctx, uint32_t** words, uint32_t** orig, int W,
         // current order give the reference permutation.  Later builds with these dims go one
         // byte deeper, or straight to LSD.
         learnt = nb + 1 > D - 3 ? -1 : nb + 1;
-        radix_sort_words(ctx, words, nw, N, all, nullptr, false);
+        radix_sort_words(ctx, words, nw, N, all, nullptr, false, nullptr, G);
         return;
     }
     std::vector<unsigned long long> h(2 * nbig);
@@ -736,7 +808,7 @@ static void finish_hybrid(zi_ctx* ctx, uint32_t** words, uint32_t** orig, int W,
     for (uint32_t q = 0; q < nbig; ++q) {
         uint32_t* sub[kMaxWords];
         for (int k = 0; k < nw; ++k) sub[k] = words[k] + h[2 * q];
-        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], all, nullptr, false);
+        radix_sort_words(ctx, sub, nw, h[2 * q + 1] - h[2 * q], all_full, nullptr, false);
     }
 }
 
@@ -769,8 +841,10 @@ static void verify_sorted(zi_ctx* ctx, uint32_t* const* words, int W, uint64_t N
 // Sort (key words, payload) records by (Morton key, payload); `layouts`: the payload's top 3
 // bits are a layout id that orders first.
 // result (optional, see radix_sort_words): the buffers holding the sorted records
+// G > 1 (layouts): the records are G equal layout groups, group-major -- every global pass sorts
+// the groups on their own, so no pass on the layout digit is needed
 static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts,
-                               uint32_t** result = nullptr) {
+                               uint32_t** result = nullptr, int G = 1) {
     const int nw = W + 1;
     uint32_t* cur[kMaxWords];
     auto done = [&] {  // hand the final buffers to the caller, or move them into `words`
@@ -781,9 +855,12 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
                 ZI_CUDA(cudaMemcpyAsync(words[k], cur[k], N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
         }
     };
-    std::vector<int2> all;
+    if (G > 1 && (!layouts || N % G != 0 || !groups_fit(D, G))) G = 1;
+    std::vector<int2> all, all_full;
     for (int p = 0; p < D; ++p) all.push_back(make_int2(p >> 2, (p & 3) * 8));
-    if (layouts) all.push_back(make_int2(W, 29));
+    all_full = all;
+    if (layouts) all_full.push_back(make_int2(W, 29));
+    if (G == 1) all = all_full;
     int& learnt = ctx->sort_depth[D][layouts ? 1 : 0];
     if (learnt > 0 && msd_bytes_forced() <= 0 && learnt <= D - 3) {
         // depth known from an earlier build: MSD passes with device-side digit bases, no
@@ -791,21 +868,23 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         const int nb = learnt;
         std::vector<int2> msd;
         for (int p = D - nb; p < D; ++p) msd.push_back(make_int2(p >> 2, (p & 3) * 8));
-        if (layouts) msd.push_back(make_int2(W, 29));
-        radix_sort_words(ctx, words, nw, N, msd, nullptr, true, cur);
-        finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, learnt);
+        if (layouts && G == 1) msd.push_back(make_int2(W, 29));
+        radix_sort_words(ctx, words, nw, N, msd, nullptr, true, cur, G);
+        finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, all_full, G, learnt);
         if (verify_on()) verify_sorted(ctx, cur, W, N, D, nb, layouts);
         done();
         return;
     }
-    const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all);
+    const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all, G);  // [pass][group][256]
     // MSD depth: the fewest top bytes whose (marginal) entropies predict segments of <= 16
     // records per layout; a clustered top (smooth images) pushes it up, and when the split
     // would leave little for the windows the plain LSD sort is used.
     auto entropy = [&](int q) {
         double e = 0.0;
         for (int b = 0; b < 256; ++b) {
-            const double pr = static_cast<double>(hist[static_cast<size_t>(q) * 256 + b]) / static_cast<double>(N);
+            uint64_t c = 0;
+            for (int g = 0; g < G; ++g) c += hist[(static_cast<size_t>(q) * G + g) * 256 + b];
+            const double pr = static_cast<double>(c) / static_cast<double>(N);
             if (pr > 0) e -= pr * std::log2(pr);
         }
         return e;
@@ -826,23 +905,24 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     static const bool debug = std::getenv("ZI_DEBUG_SORT") != nullptr;
     if (nb > D - 3) {  // little left for the windows: all-LSD with the histograms already taken
         if (debug) std::fprintf(stderr, "hybrid sort N=%llu: MSD depth %d of %d -> LSD\n", static_cast<unsigned long long>(N), nb, D);
-        radix_sort_words(ctx, words, nw, N, all, hist.data(), false, cur);
+        radix_sort_words(ctx, words, nw, N, all, hist.data(), false, cur, G);
         done();
         return;
     }
     std::vector<int2> msd;
     std::vector<uint32_t> msd_hist;
+    const size_t qw = static_cast<size_t>(G) * 256;  // histogram words per pass
     for (int p = D - nb; p < D; ++p) {
         msd.push_back(make_int2(p >> 2, (p & 3) * 8));
-        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(p) * 256, hist.begin() + static_cast<size_t>(p + 1) * 256);
+        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(p) * qw, hist.begin() + static_cast<size_t>(p + 1) * qw);
     }
-    if (layouts) {
+    if (layouts && G == 1) {
         msd.push_back(make_int2(W, 29));
-        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(D) * 256, hist.end());
+        msd_hist.insert(msd_hist.end(), hist.begin() + static_cast<size_t>(D) * qw, hist.end());
     }
-    radix_sort_words(ctx, words, nw, N, msd, msd_hist.data(), false, cur);
+    radix_sort_words(ctx, words, nw, N, msd, msd_hist.data(), false, cur, G);
     if (learnt == 0) learnt = nb;  // remembered: later builds skip the histogram round trip
-    finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, learnt);
+    finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, all_full, G, learnt);
     if (verify_on()) verify_sorted(ctx, cur, W, N, D, nb, layouts);
     done();
 }
@@ -865,6 +945,40 @@ void morton_sort_rows(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n
     for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * n;
     words[W] = d_val;
     morton_sort_hybrid(ctx, words, W, n, D, false);
+}
+
+void morton_sort_records(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int G, int D,
+                         bool group_in_payload, uint32_t** out, bool payload_ascending) {
+    const int W = (D + 3) / 4;
+    const uint64_t N = static_cast<uint64_t>(G) * n;
+    static const bool splitter = [] {
+        const char* e = std::getenv("ZI_SORT");
+        return e != nullptr && std::strcmp(e, "splitter") == 0;
+    }();
+    if (splitter && payload_ascending) {  // experimental: k_ssort.cu
+        uint32_t* words[kMaxWords];
+        for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * N;
+        words[W] = d_val;
+        sample_sort_groups(ctx, words, W + 1, n, G, D, group_in_payload, out);
+        return;
+    }
+    if (G > 1) {  // layout groups sorted on their own: no layout-digit pass
+        uint32_t* words[kMaxWords];
+        for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * N;
+        words[W] = d_val;
+        morton_sort_hybrid(ctx, words, W, N, D, group_in_payload, out, G);
+        return;
+    }
+    if (payload_ascending) {  // hybrid MSD + window sort, stable: payload order ties
+        uint32_t* words[kMaxWords];
+        for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * n;
+        words[W] = d_val;
+        morton_sort_hybrid(ctx, words, W, n, D, false, out);
+        return;
+    }
+    morton_sort(ctx, d_keyw, d_val, n, D, true);  // payload passes first: any input order
+    for (int k = 0; k < W; ++k) out[k] = d_keyw + static_cast<size_t>(k) * n;
+    out[W] = d_val;
 }
 
 void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D, uint32_t** out) {

@@ -384,10 +384,11 @@ void build_vector_index_device(zi_vector_index* vi) {
     uint32_t* keyw = vi->recs.p;
     uint32_t* val = vi->recs.p + static_cast<size_t>(W) * n;
     quantize_interleave(ctx, vi->Y.p, vi->minmax.p, n, n, 0, D, keyw, val);
-    morton_sort_rows(ctx, keyw, val, n, D);
+    uint32_t* sorted[10];
+    morton_sort_records(ctx, keyw, val, n, 1, D, false, sorted);
     vi->index.ctx = ctx;
     vi->index.layout_id = 0;
-    finalize_index(ctx, keyw, val, n, 0, n, D, nullptr, &vi->index);
+    finalize_index(ctx, sorted[0], sorted[W], n, 0, n, D, nullptr, &vi->index);
     vi->host_model = false;
 }
 

@@ -141,8 +141,9 @@ void index_from_host(zi_ctx* ctx, const uint8_t* coords, const uint32_t* keys, u
     uint32_t* keyw = recs.p;
     uint32_t* val = recs.p + static_cast<size_t>(W) * n;
     interleave_coords(ctx, dc.p, keys_in, n, D, keyw, val);
-    morton_sort(ctx, keyw, val, n, D, !ascending);
-    finalize_index(ctx, keyw, val, n, 0, n, D, nullptr, idx);
+    uint32_t* sorted[10];
+    morton_sort_records(ctx, keyw, val, n, 1, D, false, sorted, ascending);
+    finalize_index(ctx, sorted[0], sorted[W], n, 0, n, D, nullptr, idx);
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));  // dc / recs are freed (stream-ordered) on return
 }
 

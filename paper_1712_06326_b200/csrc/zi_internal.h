@@ -127,6 +127,7 @@ struct zi_ctx {
     int sort_depth[33][2] = {};
     int flush_toggle = 1;
     zi::dbuf<int2> gm_wtab;      // fused moments: gather word table
+    zi::dbuf<uint32_t> ss_buf;   // splitter sort: output records, samples, splitters, histograms
 };
 
 // One z-curve-sorted index, device resident.
@@ -275,6 +276,18 @@ void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_k
 // payload_first, 4 leading passes order by the payload (ties of the Morton key -> key order).
 // d_keyw: W*n words (SoA), d_val: n.  Result in place.
 void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first);
+constexpr int kSortMaxWords = 9;  // up to 8 Morton key words (D <= 32) + payload
+// Splitter sort (k_ssort.cu) of G groups of n records (group-major, SoA: nw-1 Morton words then
+// the payload) by (Morton key, payload) inside each group; group_in_payload: the group id is the
+// payload's top 3 bits (the 8-layout build).  out[k]: the buffers holding the sorted words (the
+// input, or ctx->ss_buf), valid until the next sort on this context.
+void sample_sort_groups(zi_ctx* ctx, uint32_t* const* words, int nw, uint64_t n, int G, int D, bool group_in_payload,
+                        uint32_t** out);
+// the build's sort: G groups (layouts) of n records, group-major; out[k] = word k of the sorted
+// records (stride G*n), payload at out[W].  Onesweep LSD / hybrid sorts (k_sort.cu); ZI_SORT=splitter
+// selects the experimental two-level splitter sort (k_ssort.cu) when the payload is ascending.
+void morton_sort_records(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int G, int D,
+                         bool group_in_payload, uint32_t** out, bool payload_ascending = true);
 // all 8 layouts at once: N = 8n records, Morton passes then one pass on the layout bits of the
 // payload ((layout << 29) | row) -- stable, so each layout segment ends in reference order
 // out (optional): the buffers holding the sorted words (out[k] = out[0] + k*N, the payload at
