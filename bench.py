@@ -13,8 +13,10 @@ fix-up), one hybrid Morton sort over the records of all layouts, 8 finalizes.  L
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config cfg2|cfg1|cfg4]
 
-N > 1 (torchrun): every rank builds the index of its own image (seed + rank) -- independent
-objects, no data-path collective, weak scaling; timing is the max over ranks.
+N > 1 (torchrun): ONE cfg image range-partitioned by Morton key over the ranks (the sharded build
+of SURVEY.md §8(e): moments SUM, lo/hi MIN/MAX, sample all-gather, two all-to-alls over NCCL),
+strong scaling, timing the max over ranks; --replicas runs one independent image per rank instead
+(weak scaling).  --sharded forces the sharded pipeline at N = 1 too (its single-rank overhead).
 """
 from __future__ import annotations
 
@@ -56,8 +58,10 @@ def parse():
     p.add_argument("--no-vector", action="store_true", help="skip the cfg5 vector-index build line")
     p.add_argument("--vec-n", type=int, default=1 << 24, help="cfg5 vector-index rows")
     p.add_argument("--sharded", action="store_true",
-                   help="range-partitioned build of ONE image over the N ranks (SURVEY.md §8(e); strong scaling) "
-                        "instead of one image per rank")
+                   help="range-partitioned build of ONE image over the N ranks (SURVEY.md §8(e); strong scaling); "
+                        "the default when N > 1")
+    p.add_argument("--replicas", action="store_true",
+                   help="N > 1: one independent image per rank (weak scaling) instead of the sharded build")
     return p.parse_args()
 
 
@@ -386,10 +390,12 @@ def candidate_scoring(zb, ctx, args, hbm_peak):
 
 
 def run_sharded(args, zb, world, rank, local, dist):
-    """One image (seed of rank 0) range-partitioned over the ranks: every step is the whole
-    sharded build from host memory (shard create + moments SUM + lo/hi MIN/MAX + sample sort +
-    rebalancing all-to-all + finalize), timed on the ctx stream; the step time is the max over
-    ranks and the value counts the image's dictionary once (strong scaling)."""
+    """One image (seed of rank 0) range-partitioned over the ranks: every step
+    is the whole sharded build from the device-resident image (dictionary, moments SUM over NCCL,
+    8 PCA models, lo/hi MIN/MAX, projection + quantiser, local sort, sample all-gather, two
+    all-to-alls, finalize), timed on the ctx stream; the step time is the max over ranks and the
+    value counts the image's dictionary once (strong scaling).  e2e: the same build from host
+    memory through a fresh shard (image + mask upload inside the timing)."""
     from paper_1712_06326_b200 import sharding
     img, known, p = workload(args.config, 0)
     ctx = zb.Context(local)
@@ -399,11 +405,12 @@ def run_sharded(args, zb, world, rank, local, dist):
         comm = sharding.TorchComm(device=torch.device("cuda", local))
     else:
         comm = sharding.LoopbackComm(1)
+    sh = sharding.DeviceShard(img, known, cfg, rank, world, ctx=ctx)
+    info = sharding.build_sharded([sh], comm)
 
     def build():
-        sh = sharding.DeviceShard(img, known, cfg, rank, world, ctx=ctx)
-        info = sharding.build_sharded([sh], comm)
-        return sh, info
+        sh.rebuild()
+        return sharding.build_sharded([sh], comm)
 
     for _ in range(max(args.warmup, 0)):
         build()
@@ -414,19 +421,28 @@ def run_sharded(args, zb, world, rank, local, dist):
         dist.barrier()
     clocks.begin()
     total_ms = 0.0
-    info = None
     for _ in range(args.steps):
+        ctx.flush_l2()
         ctx.timer_start()
-        sh, info = build()
+        info = build()
         total_ms += ctx.timer_stop()
     clocks.end()
     launches = ctx.kernel_launches - launches0
     n_total = sh.n_total
+    e2e_ms = 0.0
+    for _ in range(max(1, args.steps // 4)):
+        ctx.synchronize()
+        ctx.timer_start()
+        fresh = sharding.DeviceShard(img, known, cfg, rank, world, ctx=ctx)
+        sharding.build_sharded([fresh], comm)
+        e2e_ms += ctx.timer_stop()
+        del fresh
+    e2e_steps = max(1, args.steps // 4)
     if dist is not None:
         import torch
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms, e2e_ms = float(t[0].item()), float(t[1].item())
     value = n_total * args.steps / (total_ms * 1e-3)
     if rank == 0:
         h2d = img.nbytes + known.nbytes
@@ -436,9 +452,10 @@ def run_sharded(args, zb, world, rank, local, dist):
                 "config": {"workload": f"{args.config}: one image range-partitioned by Morton key over {world} rank(s), "
                                        f"n={n_total} dictionary patches, 8 layout indices",
                            "global_batch": n_total, "parallelism": f"range-partitioned x{world} (sample sort over NCCL)",
-                           "l2": "not flushed (every step re-uploads the image and rebuilds every buffer)"},
-                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 0,
-                        "api": "sharding.DeviceShard + build_sharded (zi_shard_*), host image in"},
+                           "l2": "flushed (256 MiB write) before every timed step"},
+                "e2e": {"value": n_total * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": 0, "ms_per_step": e2e_ms / e2e_steps,
+                        "api": "sharding.DeviceShard (host image + mask in) + build_sharded (zi_shard_*)"},
                 "exchange": info, "gpu_launches": launches, "clocks": clocks.result()}
         print(json.dumps(line), flush=True)
 
@@ -461,7 +478,7 @@ def main():
         dist = tdist
 
     import paper_1712_06326_b200 as zb
-    if args.sharded:
+    if args.sharded or (world > 1 and not args.replicas):
         run_sharded(args, zb, world, rank, local, dist)
         return
 

@@ -293,6 +293,12 @@ typedef struct zi_shard zi_shard;
 zi_status zi_shard_create(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h,
                           int32_t C, const zi_index_config* cfg, int32_t rank, int32_t world, zi_shard** out);
 zi_status zi_shard_destroy(zi_shard* sh);
+/* restart the stages for the next build over the same device-resident image and mask, every
+ * device buffer kept (bench: one sharded build per step) */
+zi_status zi_shard_rebuild(zi_shard* sh);
+/* world == 1, after quantize_sort: the locally sorted layouts are the index -- finalise them
+ * without the exchange stages (partition / receive / finish) */
+zi_status zi_shard_finish_local(zi_shard* sh);
 /* info[10]: n_total, row_begin, row_end, F, dims, words, rank, world, stage, records held */
 zi_status zi_shard_info(const zi_shard* sh, uint64_t* info);
 zi_status zi_shard_moments(zi_shard* sh, int64_t* moments_out);

@@ -123,6 +123,8 @@ SIGNATURES = {
     "zi_shard_create": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig), C.c_int32,
                                   C.c_int32, C.POINTER(vp)]),
     "zi_shard_destroy": (C.c_int, [vp]),
+    "zi_shard_rebuild": (C.c_int, [vp]),
+    "zi_shard_finish_local": (C.c_int, [vp]),
     "zi_shard_info": (C.c_int, [vp, u64p]),
     "zi_shard_moments": (C.c_int, [vp, i64p]),
     "zi_shard_fit_project": (C.c_int, [vp, i64p, i64p, i64p]),

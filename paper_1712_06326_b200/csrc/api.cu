@@ -967,6 +967,16 @@ zi_status zi_shard_create(zi_ctx* ctx, const uint8_t* image, const uint8_t* know
     });
 }
 
+zi_status zi_shard_rebuild(zi_shard* sh) {
+    if (!sh) return fail(ZI_E_INVALID, "null argument");
+    return guard(zi::shard_multi_index(sh)->ctx, [&] { zi::shard_rebuild(sh); });
+}
+
+zi_status zi_shard_finish_local(zi_shard* sh) {
+    if (!sh) return fail(ZI_E_INVALID, "null argument");
+    return guard(zi::shard_multi_index(sh)->ctx, [&] { zi::shard_finish_local(sh); });
+}
+
 zi_status zi_shard_destroy(zi_shard* sh) {
     if (!sh) return ZI_OK;
     zi_multi_index* mi = zi::shard_multi_index(sh);

@@ -70,28 +70,43 @@ double confidence_term(const mask& m, const std::vector<double>& conf, int cx, i
 
 // Per-pixel caches of the data term's inputs, kept current across pastes:
 //   inten[i] = channel_mean (int channel sum / C as double, proj/src/engine.cpp:24-28)
-//   gflag[i] = interior pixel whose 4 neighbours and itself are known (engine.cpp:110-121)
+//   sq[i]    = gx^2 + gy^2 of the central-difference gradient when the pixel is interior and it
+//              and its 4 neighbours are known (engine.cpp:110-121), else -2 (below any candidate:
+//              the window scan starts from -1 and keeps the first strict maximum)
+// A paste changes inten inside its window and the known flags there, so sq changes only within
+// one pixel of it (refresh); the argmax pixel's gx, gy are recomputed from inten, same formula.
 struct grad_cache {
-    std::vector<double> inten;
-    std::vector<uint8_t> gflag;
+    std::vector<double> inten, sq;
+    int w = 0;
     void init(const raster& img, const mask& m) {
+        w = m.w;
         inten.assign(static_cast<size_t>(m.w) * m.h, 0.0);
-        gflag.assign(static_cast<size_t>(m.w) * m.h, 0);
+        sq.assign(static_cast<size_t>(m.w) * m.h, -2.0);
         for (int y = 0; y < m.h; ++y)
             for (int x = 0; x < m.w; ++x) inten[m.idx(x, y)] = channel_mean(img.at(x, y), img.C);
         refresh(m, 0, 0, m.w - 1, m.h - 1);
     }
     void set_pixel(const raster& img, const mask& m, int x, int y) { inten[m.idx(x, y)] = channel_mean(img.at(x, y), img.C); }
+    double gx(size_t i) const { return (inten[i + 1] - inten[i - 1]) / 2.0; }
+    double gy(size_t i) const { return (inten[i + w] - inten[i - w]) / 2.0; }
     void refresh(const mask& m, int xa, int ya, int xb, int yb) {
         xa = std::max(xa, 0);
         ya = std::max(ya, 0);
         xb = std::min(xb, m.w - 1);
         yb = std::min(yb, m.h - 1);
         for (int y = ya; y <= yb; ++y)
-            for (int x = xa; x <= xb; ++x)
-                gflag[m.idx(x, y)] = x >= 1 && y >= 1 && x + 1 < m.w && y + 1 < m.h && m.is_known(x, y) &&
-                                     m.is_known(x - 1, y) && m.is_known(x + 1, y) && m.is_known(x, y - 1) &&
-                                     m.is_known(x, y + 1);
+            for (int x = xa; x <= xb; ++x) {
+                const size_t i = m.idx(x, y);
+                const bool g = x >= 1 && y >= 1 && x + 1 < m.w && y + 1 < m.h && m.is_known(x, y) &&
+                               m.is_known(x - 1, y) && m.is_known(x + 1, y) && m.is_known(x, y - 1) &&
+                               m.is_known(x, y + 1);
+                if (g) {
+                    const double a = gx(i), b = gy(i);
+                    sq[i] = a * a + b * b;
+                } else {
+                    sq[i] = -2.0;
+                }
+            }
     }
 };
 
@@ -101,21 +116,21 @@ double compute_priority(const raster& img, const mask& m, const std::vector<doub
     const int r = (K - 1) / 2;
     const double cterm = confidence_term(m, conf, cx, cy, K);
     double best_sq = -1.0, bgx = 0.0, bgy = 0.0;
+    size_t best_i = 0;
     const int y0 = std::max(cy - r, 0), y1 = std::min(cy + r, m.h - 1);
     const int x0 = std::max(cx - r, 0), x1 = std::min(cx + r, m.w - 1);
     for (int y = y0; y <= y1; ++y) {
         const size_t row = static_cast<size_t>(y) * m.w;
-        for (int x = x0; x <= x1; ++x) {
-            if (!gc.gflag[row + x]) continue;
-            const double gx = (gc.inten[row + x + 1] - gc.inten[row + x - 1]) / 2.0;
-            const double gy = (gc.inten[row + m.w + x] - gc.inten[row - m.w + x]) / 2.0;
-            const double sq = gx * gx + gy * gy;
-            if (sq > best_sq) {
-                best_sq = sq;
-                bgx = gx;
-                bgy = gy;
+        const double* sq = gc.sq.data() + row;
+        for (int x = x0; x <= x1; ++x)
+            if (sq[x] > best_sq) {  // the first strict maximum in scan order, as the reference
+                best_sq = sq[x];
+                best_i = row + x;
             }
-        }
+    }
+    if (best_sq > -1.0) {
+        bgx = gc.gx(best_i);
+        bgy = gc.gy(best_i);
     }
     (void)img;
     auto unknown_at = [&](int x, int y) {

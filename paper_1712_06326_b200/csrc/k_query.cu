@@ -915,6 +915,93 @@ __global__ void __launch_bounds__(256) k_brute(const uint8_t* __restrict__ img, 
     if (threadIdx.x == 0) atomicMin(best, s_best);
 }
 
+// The exhaustive scan for gray images (C == 1), four dictionary entries per thread: when the four
+// keys are consecutive columns of one row (the common case: the dictionary is every fully known
+// window in row-major order) one unaligned 4-byte load holds a known pixel of all four patches,
+// and the four costs are accumulated byte-wise (__vabsdiffu4, then __dp4a per byte lane).  Other
+// quads fall back to one patch at a time.  Same (cost, key) minimum as k_brute.
+__global__ void __launch_bounds__(256) k_brute4(const uint8_t* __restrict__ img, int w, int K,
+                                                const uint32_t* __restrict__ dict, uint64_t n,
+                                                const uint8_t* __restrict__ target, int norm,
+                                                unsigned long long* __restrict__ best) {
+    // shared: the known target values replicated x4, and their byte offsets from the patch origin
+    extern __shared__ uint32_t s_t4[];
+    __shared__ int s_nv;
+    __shared__ unsigned long long s_best;
+    const int KK = K * K;
+    int* s_off = reinterpret_cast<int*>(s_t4 + KK);
+    if (threadIdx.x < 32) {
+        int cnt = 0;
+        for (int base = 0; base < KK; base += 32) {
+            const int l = base + threadIdx.x;
+            const bool kn = l < KK && target[KK + l] != 0;
+            const unsigned m = __ballot_sync(0xffffffffu, kn);
+            if (kn) {
+                const int slot = cnt + __popc(m & ((1u << threadIdx.x) - 1u));
+                const int ly = l / K, lx = l - ly * K;
+                s_t4[slot] = static_cast<uint32_t>(target[l]) * 0x01010101u;
+                s_off[slot] = ly * w + lx;
+            }
+            cnt += __popc(m);
+        }
+        if (threadIdx.x == 0) {
+            s_nv = cnt;
+            s_best = kU64Max;
+        }
+    }
+    __syncthreads();
+    const int nv = s_nv;
+    unsigned long long mine = kU64Max;
+    const uint64_t nq = (n + 3) / 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t qd = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; qd < nq; qd += stride) {
+        const uint64_t i0 = 4 * qd;
+        uint32_t key[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) key[u] = i0 + u < n ? __ldg(dict + i0 + u) : 0xffffffffu;
+        if (i0 + 3 < n && key[3] == key[0] + 3u) {
+            const uint32_t a0 = (key[0] >> 16) * static_cast<uint32_t>(w) + (key[0] & 0xffffu);
+            uint32_t acc[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 4
+            for (int v = 0; v < nv; ++v) {
+                const uint32_t a = a0 + static_cast<uint32_t>(s_off[v]);
+                const uint32_t* wp = reinterpret_cast<const uint32_t*>(img + (a & ~3u));
+                const uint32_t s4 = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (a & 3u) * 8u);
+                const uint32_t d = __vabsdiffu4(s4, s_t4[v]);
+                if (norm == 0) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] = __dp4a(d & (0xffu << (8 * u)), d, acc[u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] = __dp4a(d & (0xffu << (8 * u)), 0x01010101u, acc[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned long long c = pack_candidate(acc[u], key[u]);
+                mine = c < mine ? c : mine;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (i0 + u >= n) continue;
+                const uint8_t* base = img + (static_cast<size_t>(key[u] >> 16) * w + (key[u] & 0xffffu));
+                uint32_t acc = 0;
+                for (int v = 0; v < nv; ++v) {
+                    const int dd = static_cast<int>(s_t4[v] & 0xffu) - static_cast<int>(__ldg(base + s_off[v]));
+                    acc += norm == 0 ? static_cast<uint32_t>(dd * dd) : static_cast<uint32_t>(dd < 0 ? -dd : dd);
+                }
+                const unsigned long long c = pack_candidate(acc, key[u]);
+                mine = c < mine ? c : mine;
+            }
+        }
+    }
+    mine = warp_min(mine);
+    if ((threadIdx.x & 31) == 0) atomicMin(&s_best, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMin(best, s_best);
+}
+
 // exhaustive path for k > kMaxScanK: pack every entry, radix-sort the u64 packed values
 __global__ void __launch_bounds__(256) k_pack_all(views8 V, const qws* ws, int norm, uint32_t* __restrict__ lo,
                                                   uint32_t* __restrict__ hi) {
@@ -1412,6 +1499,7 @@ struct qlat_params {
     uint32_t seq;
     int want_list;
     int tbytes;
+    unsigned long long* dbg;  // ZI_DEBUG_QUERY: per-CTA %globaltimer at start and before the ticket
     uint8_t target[kLatMaxTarget];
 };
 
@@ -1441,6 +1529,7 @@ __global__ void __launch_bounds__(kLatThreads, P <= 3 ? 2 : 1) k_query_lat(const
     const int norm = prm.norm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     ZI_TPHASE(0)
+    if (prm.dbg && tid == 0) prm.dbg[4 * blockIdx.x] = gtimer();
     for (int i = tid; i < prm.tbytes; i += kLatThreads) s_t[i] = prm.target[i];
     if (tid < 32) s_q[tid] = 0;
     if (tid == 0) {
@@ -1479,7 +1568,11 @@ __global__ void __launch_bounds__(kLatThreads, P <= 3 ? 2 : 1) k_query_lat(const
     }
     __syncthreads();
     const int lid = s_lid;
-    {  // make_query (builder.cpp:110-127): x - mean staged, then the canonical fp64 chain per dim
+    // make_query (builder.cpp:110-127): x - mean and the layout's components ([j][d], staged in
+    // the candidate buffer, unused until the seed) in shared memory, then the canonical fp64
+    // chain per dim
+    double* s_comp = reinterpret_cast<double*>(s_buf);
+    {
         const double* mean = mv.mean + static_cast<size_t>(lid) * mc;
         const int32_t* loc = mv.local + lid * mv.m;
         for (int j = tid; j < mc; j += kLatThreads) {
@@ -1488,20 +1581,24 @@ __global__ void __launch_bounds__(kLatThreads, P <= 3 ? 2 : 1) k_query_lat(const
             const double x = tk[l] ? static_cast<double>(tv[l * C + j % C]) : mj;
             s_xc[j] = __dsub_rn(x, mj);
         }
+        const double* comp = mv.comp + static_cast<size_t>(lid) * mc * D;
+        for (int i = tid; i < mc * D; i += kLatThreads) s_comp[i] = __ldg(comp + i);
     }
     __syncthreads();
     if (tid < D) {
-        const double* comp = mv.comp + static_cast<size_t>(lid) * mc * D + tid;
         double y = 0.0;
         int j = 0;
-        for (; j + 8 <= mc; j += 8) {  // eight component loads in flight ahead of the chain
-            double cc[8];
+        for (; j + 8 <= mc; j += 8) {
+            double cc[8], xx[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) cc[u] = __ldg(comp + static_cast<size_t>(j + u) * D);
+            for (int u = 0; u < 8; ++u) {
+                cc[u] = s_comp[(j + u) * D + tid];
+                xx[u] = s_xc[j + u];
+            }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) y = __fma_rn(cc[u], s_xc[j + u], y);
+            for (int u = 0; u < 8; ++u) y = __fma_rn(cc[u], xx[u], y);
         }
-        for (; j < mc; ++j) y = __fma_rn(__ldg(comp + static_cast<size_t>(j) * D), s_xc[j], y);
+        for (; j < mc; ++j) y = __fma_rn(s_comp[j * D + tid], s_xc[j], y);
         const unsigned long long* mm = mv.minmax + static_cast<size_t>(lid) * 2 * D;
         s_q[tid] = quantize_rn(ordered_to_double_hd(mm[tid]), ordered_to_double_hd(mm[D + tid]), y);
     }
@@ -1616,6 +1713,10 @@ __global__ void __launch_bounds__(kLatThreads, P <= 3 ? 2 : 1) k_query_lat(const
     }
     __syncthreads();
     ZI_TPHASE(3)
+    if (prm.dbg && tid == 0) {
+        prm.dbg[4 * blockIdx.x + 2] = static_cast<unsigned long long>(nsurv);
+        prm.dbg[4 * blockIdx.x + 3] = static_cast<unsigned long long>(s_cnt);
+    }
     {  // exact local top-k (unsorted), then the winners that can still make the global top-k
         const int m0 = s_cnt;
         uint32_t mx = 0;
@@ -1665,6 +1766,7 @@ __global__ void __launch_bounds__(kLatThreads, P <= 3 ? 2 : 1) k_query_lat(const
         }
     }
     ZI_TPHASE(4)
+    if (prm.dbg && tid == 0) prm.dbg[4 * blockIdx.x + 1] = gtimer();
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = atomicAdd(&ws->done, 1u) == gridDim.x - 1;
@@ -2424,6 +2526,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
     const uint64_t G2 = std::min<uint64_t>(std::max<uint64_t>(nblk, 1),
                                            lat_g > 0 ? static_cast<uint64_t>(lat_g) : lat_g_max);
     if (!use_one && !force_multi && k <= kLatMaxK && tbytes <= static_cast<size_t>(kLatMaxTarget) &&
+        static_cast<size_t>(mi->mc) * mi->dims <= static_cast<size_t>(kLatCap - kLatThreads * kLatBlkRegs) &&
         lat_smem <= 112 * 1024 && nblk <= G2 * kLatThreads * kLatBlkRegs) {
         if (!mi->qws_clean) {
             ZI_CUDA(cudaMemsetAsync(&s.ws->bound, 0xff, sizeof(unsigned long long), ctx->stream));
@@ -2444,6 +2547,8 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
         prm.seq = seq;
         prm.want_list = knn_out != nullptr ? 1 : 0;
         prm.tbytes = static_cast<int>(tbytes);
+        static dbuf<unsigned long long> dbg_buf;
+        prm.dbg = debug_query ? dbg_buf.ensure(4 * G2) : nullptr;
         std::memcpy(prm.target, h_tv, KK * mi->C);
         std::memcpy(prm.target + KK * mi->C, h_tk, KK);
         switch (mv.idx[0].P) {
@@ -2460,6 +2565,28 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
         if (debug_query || ctx->profiling) {
             ZI_CUDA(cudaMemcpyAsync(hq, s.ws, sizeof(qws), cudaMemcpyDeviceToHost, ctx->stream));
             ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (debug_query) {  // CTA start / finish spread relative to the first start
+                std::vector<unsigned long long> d(4 * G2);
+                ZI_CUDA(cudaMemcpy(d.data(), prm.dbg, d.size() * 8, cudaMemcpyDeviceToHost));
+                unsigned long long s0 = ~0ull, s1 = 0, f0 = ~0ull, f1 = 0, sv = 0, sc = 0, slast_v = 0, slast_c = 0;
+                for (uint64_t c = 0; c < G2; ++c) {
+                    s0 = std::min(s0, d[4 * c]);
+                    s1 = std::max(s1, d[4 * c]);
+                    f0 = std::min(f0, d[4 * c + 1]);
+                    if (d[4 * c + 1] > f1) {
+                        f1 = d[4 * c + 1];
+                        slast_v = d[4 * c + 2];
+                        slast_c = d[4 * c + 3];
+                    }
+                    sv = std::max(sv, d[4 * c + 2]);
+                    sc = std::max(sc, d[4 * c + 3]);
+                }
+                std::fprintf(stderr,
+                             "qlat ctas=%llu start_spread_us=%.1f finish_first_us=%.1f finish_last_us=%.1f "
+                             "max_surv=%llu max_cand=%llu last_surv=%llu last_cand=%llu\n",
+                             static_cast<unsigned long long>(G2), (s1 - s0) * 1e-3, (f0 - s0) * 1e-3, (f1 - s0) * 1e-3,
+                             sv, sc, slast_v, slast_c);
+            }
         } else {
             unsigned spins = 0;
             while (hr->seq != seq) {
@@ -2592,8 +2719,14 @@ uint64_t brute_force_scan(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K
     ZI_CUDA(cudaMemsetAsync(&s.ws->best, 0xff, sizeof(unsigned long long), ctx->stream));
     const size_t smem = ((KK * C + 3) & ~size_t(3)) + KK * C * sizeof(int) + 16;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
-    if (n > 0)
+    static const bool scalar = std::getenv("ZI_BRUTE_SCALAR") != nullptr;
+    if (n > 0 && C == 1 && !scalar) {
+        const unsigned g4 = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, static_cast<uint64_t>(ctx->num_sms) * 8));
+        ZI_LAUNCH(ctx, "brute_force", k_brute4, g4, 256, KK * 8 + 16, d_img, w, K, d_dict, n, s.target, norm,
+                  &s.ws->best);
+    } else if (n > 0) {
         ZI_LAUNCH(ctx, "brute_force", k_brute, grid, 256, smem, d_img, w, C, K, d_dict, n, s.target, norm, &s.ws->best);
+    }
     unsigned long long* hb = reinterpret_cast<unsigned long long*>(stage + res_off);
     ZI_CUDA(cudaMemcpyAsync(hb, &s.ws->best, 8, cudaMemcpyDeviceToHost, ctx->stream));
     ZI_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -32,21 +32,39 @@ struct sort_words {
 
 // Histograms of every pass in one read: hist[(q*G + g)*256 + digit] for records in groups of gn
 // (group g = records [g*gn, (g+1)*gn)).  Each CTA reads a contiguous chunk (at most a few group
-// changes, flushed as they come); per pass a warp's equal digits are merged with match_any, so a
-// hot digit (the clustered top Morton bytes) costs one shared atomic per warp, not 32.
+// changes, flushed as they come) with four records per thread in flight.
 __global__ void __launch_bounds__(256) k_sort_hist(sort_words io, int npass, const int2* __restrict__ passes,
                                                    uint64_t n, uint64_t gn, int G, uint32_t* __restrict__ hist) {
     extern __shared__ uint32_t s_hist[];  // npass*256
     __shared__ int2 s_pass[40];
     const int nb = npass * 256;
-    const int lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) s_hist[i] = 0;
     if (threadIdx.x < npass) s_pass[threadIdx.x] = passes[threadIdx.x];
     __syncthreads();
     const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
     const uint64_t c0 = static_cast<uint64_t>(blockIdx.x) * chunk;
     const uint64_t c1 = c0 + chunk < n ? c0 + chunk : n;
-    auto flush = [&](int g) {
+    uint64_t seg = c0;
+    while (seg < c1) {  // the part of the chunk inside one group
+        const int g = G > 1 ? static_cast<int>(seg / gn) : 0;
+        const uint64_t gend = G > 1 ? (static_cast<uint64_t>(g) + 1) * gn : n;
+        const uint64_t e = gend < c1 ? gend : c1;
+        constexpr int U = 4;
+        for (uint64_t b = seg + threadIdx.x; b < e; b += static_cast<uint64_t>(blockDim.x) * U) {
+            for (int q = 0; q < npass; ++q) {
+                const uint32_t* wq = io.in[s_pass[q].x];
+                const int sh = s_pass[q].y;
+                uint32_t v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint64_t i = b + static_cast<uint64_t>(u) * blockDim.x;
+                    v[u] = i < e ? __ldg(wq + i) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (b + static_cast<uint64_t>(u) * blockDim.x < e) atomicAdd(&s_hist[q * 256 + ((v[u] >> sh) & 0xffu)], 1u);
+            }
+        }
         __syncthreads();
         for (int i = threadIdx.x; i < nb; i += blockDim.x) {
             const uint32_t v = s_hist[i];
@@ -56,31 +74,6 @@ __global__ void __launch_bounds__(256) k_sort_hist(sort_words io, int npass, con
             }
         }
         __syncthreads();
-    };
-    uint64_t seg = c0;
-    while (seg < c1) {  // the part of the chunk inside one group
-        const int g = G > 1 ? static_cast<int>(seg / gn) : 0;
-        const uint64_t gend = G > 1 ? (static_cast<uint64_t>(g) + 1) * gn : n;
-        const uint64_t e = gend < c1 ? gend : c1;
-        constexpr int U = 4;  // records per thread per round (loads in flight)
-        for (uint64_t b = seg; b < e; b += static_cast<uint64_t>(blockDim.x) * U) {  // whole warps (match_any)
-            for (int q = 0; q < npass; ++q) {
-                const uint32_t* wq = io.in[s_pass[q].x];
-                const int sh = s_pass[q].y;
-                uint32_t v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const uint64_t i = b + static_cast<uint64_t>(u) * blockDim.x + threadIdx.x;
-                    v[u] = i < e ? (__ldg(wq + i) >> sh) & 0xffu : 256u;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const uint32_t peers = __match_any_sync(0xffffffffu, v[u]);
-                    if (v[u] < 256u && (__ffs(peers) - 1) == lane) atomicAdd(&s_hist[q * 256 + v[u]], __popc(peers));
-                }
-            }
-        }
-        flush(g);
         seg = e;
     }
 }

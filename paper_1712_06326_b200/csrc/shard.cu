@@ -51,6 +51,7 @@ struct zi_shard {
     uint64_t held = 0;              // records held after the first exchange
     bool tc = false;                // projection on the int8 tensor cores (k_proj_tc.cu)
     bool refined = false;           // refine_ranges ran after fit_project
+    uint32_t* sorted[10] = {};      // the locally sorted records (word k at sorted[k], stride 8n)
 };
 
 namespace zi {
@@ -169,22 +170,13 @@ void shard_ranges(uint64_t n, int world, int r, uint64_t* b, uint64_t* e) {
     *e = *b + base + (rr < extra ? 1 : 0);
 }
 
-zi_shard* shard_create(zi_multi_index* mi, int rank, int world) {
-    zi_ctx* ctx = mi->ctx;
-    auto* sh = new zi_shard();
-    sh->mi = mi;
-    sh->rank = rank;
-    sh->world = world;
-    mi->shard = true;
-    mi->n_total = collect_dictionary(ctx, mi->known.p, mi->w, mi->h, mi->K, mi->dict);
-    if (mi->n_total == 0) {
-        delete sh;
-        throw error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
-    }
-    if (mi->n_total >= (1ull << 29) - 1) {
-        delete sh;
-        throw error(ZI_E_INVALID, "dictionary above 2^29 patches");
-    }
+// (re)start the stage machine: the dictionary from the device-resident mask, this rank's rows
+static void shard_start(zi_shard* sh) {
+    zi_multi_index* mi = sh->mi;
+    const int rank = sh->rank, world = sh->world;
+    mi->n_total = collect_dictionary(mi->ctx, mi->known.p, mi->w, mi->h, mi->K, mi->dict);
+    if (mi->n_total == 0) throw error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
+    if (mi->n_total >= (1ull << 29) - 1) throw error(ZI_E_INVALID, "dictionary above 2^29 patches");
     sh->n_total = mi->n_total;
     shard_ranges(sh->n_total, world, rank, &sh->row_b, &sh->row_e);
     mi->row_begin = sh->row_b;
@@ -194,8 +186,28 @@ zi_shard* shard_create(zi_multi_index* mi, int rank, int world) {
     mi->F = mi->K * mi->K * mi->C;
     sh->D = mi->dims;
     sh->W = (sh->D + 3) / 4;
+    sh->stage = 0;
+    sh->held = 0;
+    sh->refined = false;
+}
+
+zi_shard* shard_create(zi_multi_index* mi, int rank, int world) {
+    auto* sh = new zi_shard();
+    sh->mi = mi;
+    sh->rank = rank;
+    sh->world = world;
+    mi->shard = true;
+    try {
+        shard_start(sh);
+    } catch (...) {
+        delete sh;
+        throw;
+    }
     return sh;
 }
+
+// the next build over the same device-resident image and mask, every buffer kept
+void shard_rebuild(zi_shard* sh) { shard_start(sh); }
 
 void shard_moments(zi_shard* sh, int64_t* out) {
     zi_multi_index* mi = sh->mi;
@@ -306,10 +318,21 @@ void shard_quantize_sort(zi_shard* sh, const int64_t* lo, const int64_t* hi, uin
             quantize_interleave(ctx, sh->Y.p + static_cast<size_t>(l) * D * n, mi->minmax.p + static_cast<size_t>(l) * 2 * D,
                                 n, N, static_cast<uint32_t>(l), D, keyw, val, static_cast<uint32_t>(sh->row_b));
     }
-    if (N) morton_sort_layouts(ctx, keyw, val, N, D);
+    // the 8 layouts are equal groups of n records: sorted each on its own (no layout-digit pass)
+    for (int k = 0; k <= W; ++k) sh->sorted[k] = keyw + static_cast<size_t>(k) * N;
+    if (N) morton_sort_records(ctx, keyw, val, n, 8, D, true, sh->sorted);
+    if (sh->world > 1 && sh->sorted[0] != keyw) {
+        // the sort left the records in the context scratch; another shard of this process (or
+        // the receive-side sort) reuses it before partition: keep them in the shard's buffer
+        for (int k = 0; k <= W; ++k) {
+            ZI_CUDA(cudaMemcpyAsync(keyw + static_cast<size_t>(k) * N, sh->sorted[k], N * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+            sh->sorted[k] = keyw + static_cast<size_t>(k) * N;
+        }
+    }
     if (S) {
         uint32_t* d = sh->small.ensure(static_cast<size_t>(8) * S * (W + 1));
-        ZI_LAUNCH(ctx, "shard_samples", k_shard_samples, (8 * S + 255) / 256, 256, 0, mi->recs.p, N, W, n,
+        ZI_LAUNCH(ctx, "shard_samples", k_shard_samples, (8 * S + 255) / 256, 256, 0, sh->sorted[0], N, W, n,
                   static_cast<int>(S), d);
         ZI_CUDA(cudaMemcpyAsync(samples_out, d, static_cast<size_t>(8) * S * (W + 1) * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, ctx->stream));
@@ -353,7 +376,7 @@ void shard_partition(zi_shard* sh, const uint32_t* splitters, uint64_t* counts_o
         ZI_CUDA(cudaMemcpyAsync(d, splitters, static_cast<size_t>(8) * P * (W + 1) * sizeof(uint32_t),
                                 cudaMemcpyHostToDevice, ctx->stream));
         unsigned long long* dp = reinterpret_cast<unsigned long long*>(sh->pos.ensure(static_cast<size_t>(8) * P));
-        ZI_LAUNCH(ctx, "shard_bounds", k_shard_bounds, (8 * P + 127) / 128, 128, 0, mi->recs.p, N, W, n, d, P, dp);
+        ZI_LAUNCH(ctx, "shard_bounds", k_shard_bounds, (8 * P + 127) / 128, 128, 0, sh->sorted[0], N, W, n, d, P, dp);
         std::vector<uint64_t> hp(static_cast<size_t>(8) * P);
         ZI_CUDA(cudaMemcpyAsync(hp.data(), dp, hp.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
         ZI_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -376,7 +399,7 @@ void shard_partition(zi_shard* sh, const uint32_t* splitters, uint64_t* counts_o
             dst += e - b;
         }
     sh->send.ensure(static_cast<size_t>(W + 1) * (N ? N : 1));
-    move_segments(sh, mi->recs.p, N, sh->send.p, 0, segs, N);
+    move_segments(sh, sh->sorted[0], N, sh->send.p, 0, segs, N);
     *d_send = sh->send.p;
     sh->stage = 4;
 }
@@ -474,6 +497,24 @@ void shard_finish(zi_shard* sh, const uint32_t* d_recv2, const uint64_t* all_cou
     sh->Y.release();
     sh->send.release();
     mi->host_lohi = false;
+    sh->stage = 6;
+}
+
+// one rank: the locally sorted layouts ARE the index -- finalise them, no exchange
+void shard_finish_local(zi_shard* sh) {
+    if (sh->stage != 3 || sh->world != 1) throw error(ZI_E_INVALID, "shard: finish_local needs world 1 after quantize");
+    zi_multi_index* mi = sh->mi;
+    zi_ctx* ctx = mi->ctx;
+    const int W = sh->W, D = sh->D;
+    const uint64_t n = mi->n, N = 8 * n;
+    for (int l = 0; l < 8; ++l) {
+        mi->L[l].index.ctx = ctx;
+        mi->L[l].index.layout_id = static_cast<uint32_t>(l);
+        finalize_index(ctx, sh->sorted[0], sh->sorted[W], N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p,
+                       &mi->L[l].index);
+    }
+    mi->host_lohi = false;
+    sh->held = N;
     sh->stage = 6;
 }
 

@@ -351,6 +351,8 @@ void knn_batch_device(zi_ctx* ctx, zi_index* idx, const uint8_t* d_queries, uint
 // ---- range-partitioned shard (shard.cu) ----
 void shard_ranges(uint64_t n, int world, int r, uint64_t* b, uint64_t* e);
 zi_shard* shard_create(zi_multi_index* mi, int rank, int world);
+void shard_rebuild(zi_shard* sh);
+void shard_finish_local(zi_shard* sh);
 void shard_moments(zi_shard* sh, int64_t* out);
 void shard_fit_project(zi_shard* sh, const int64_t* moments, int64_t* lo_out, int64_t* hi_out);
 void shard_refine_ranges(zi_shard* sh, const int64_t* lo, const int64_t* hi, int64_t* lo_out, int64_t* hi_out);

@@ -198,8 +198,14 @@ class TorchComm(Comm):
         (s,) = sends
         sc = [int(v) for v in send_counts[0]]
         rc = [int(v) for v in recv_counts[0]]
+        dev = s.device
+        if s.is_cuda and dist.get_backend(self.group) != "nccl":
+            torch.cuda.synchronize(dev)  # host staging for backends without device buffers (gloo)
+            s = s.cpu()
         recv = torch.empty((sum(rc), s.shape[1]), dtype=s.dtype, device=s.device)
         dist.all_to_all_single(recv, s, rc, sc, group=self.group)
+        if recv.device != dev:
+            recv = recv.to(dev)
         if recv.is_cuda:
             torch.cuda.synchronize(recv.device)
         return [recv]
@@ -289,6 +295,16 @@ class DeviceShard:
                                      ptr(ac, u64p), ptr(counts2, u64p), C.byref(d)))
         return counts2, self._as_tensor(d.value, int(counts2.sum()))
 
+    def rebuild(self):
+        """Restart the stages for another build (same device-resident image; buffers kept)."""
+        check(lib().zi_shard_rebuild(self.h))
+        self._info()
+
+    def finish_local(self):
+        """One rank: finalise the locally sorted layouts (no exchange)."""
+        check(lib().zi_shard_finish_local(self.h))
+        self._info()
+
     def finish(self, recv2, all_counts2):
         ac = np.ascontiguousarray(all_counts2, dtype=np.uint64)
         check(lib().zi_shard_finish(self.h, C.c_void_p(recv2.data_ptr()) if recv2.numel() else None, ptr(ac, u64p)))
@@ -296,9 +312,10 @@ class DeviceShard:
 
     def _as_tensor(self, p, n):
         torch, _ = _torch()
+        dev = torch.device("cuda", self.ctx.device)  # the shard ctx's GPU, not torch's current one
         if n == 0 or not p:
-            return torch.zeros((0, self.words + 1), dtype=torch.int32, device="cuda")
-        return torch.as_tensor(_DeviceRecords(p, n, self.words + 1), device="cuda")
+            return torch.zeros((0, self.words + 1), dtype=torch.int32, device=dev)
+        return torch.as_tensor(_DeviceRecords(p, n, self.words + 1), device=dev)
 
     # -- the built shard
     @property
@@ -363,6 +380,10 @@ def build_sharded(shards: list, comm: Comm, samples: int = 256) -> dict:
     hi = comm.allreduce([x[1] for x in lohi], "max")
     samp = [sh.quantize_sort(a, b, samples if world > 1 else 0) for sh, a, b in zip(shards, lo, hi)]
     words = shards[0].words
+    if world == 1 and all(hasattr(sh, "finish_local") for sh in shards):
+        for sh in shards:  # one rank: the sorted layouts are the index, no exchange
+            sh.finish_local()
+        return {"records_exchanged": 0, "records_rebalanced": 0, "words_per_record": words + 1}
     if world > 1:
         gathered = comm.allgather(samp)
         spl = [splitters_from_samples(g, words, world) for g in gathered]

@@ -931,3 +931,84 @@ def test_brute_force_scan_caller_dictionary(zb, golden, norm):
     for tv, tk in _query_cases(img, kn, 6):
         key, cost, _ = zb.brute_force_scan(img, sub, tv, tk, 9, norm)
         assert (cost << 32 | key) == oracle.brute_force_best(img, tv, tk, 9, sub, nrm)
+
+
+def _device_shard_worker(rank, world, port, q):
+    """One rank of a 2-process sharded build on the device (zi_shard_* stages), exchanging over
+    gloo with host staging -- both ranks share the one GPU, no kernel waits on the other rank."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1712_06326_b200 as zb
+    from paper_1712_06326_b200 import sharding
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        img, known = workloads.small_image(96, 120, 3, seed=23, hole_frac=0.07)
+        cfg = zb.index_config(patch_size=7, dims=8, knn=24)
+        sh = sharding.DeviceShard(img, known, cfg, rank, world)
+        info = sharding.build_sharded([sh], sharding.TorchComm(), samples=64)
+        first = {l: sh.multi_index.index_arrays(l) for l in range(8)}
+        sh.rebuild()  # the buffers are kept; the second build must give the same bytes
+        sharding.build_sharded([sh], sharding.TorchComm(), samples=64)
+        same = all(np.array_equal(first[l][0], sh.multi_index.index_arrays(l)[0]) and
+                   np.array_equal(first[l][1], sh.multi_index.index_arrays(l)[1]) for l in range(8))
+        mi = zb.MultiIndex(img, known, cfg)
+        b, e = sharding.shard_ranges(mi.n, world)[rank]
+        ok = same and (sh.row_begin, sh.row_end) == (b, e)
+        for l in range(8):
+            c, k = mi.index_arrays(l)
+            cs, ks = first[l]
+            ok = ok and np.array_equal(cs, c[b:e]) and np.array_equal(ks, k[b:e])
+        # the sharded query over gloo equals the single-GPU query
+        for (x, y) in fillfront(known)[:6]:
+            tv, tk = oracle.extract_patch_clamped(img, known, int(x), int(y), 7)
+            got = sharding.sharded_query([sh], sharding.TorchComm(), tv, tk, 24, 0)[0]
+            want = mi.query_best_patch(tv, tk)
+            ok = ok and (got[0], got[1], got[3], got[4]) == (want[0], want[1], want[3], want[4])
+        q.put((rank, bool(ok), info["records_exchanged"]))
+    except Exception as ex:  # noqa: BLE001
+        q.put((rank, repr(ex), 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_build_device_gloo_world2():
+    """Two processes run the device zi_shard_* stages end to end (NCCL stands in for gloo with
+    host staging: the pool has one GPU) and each holds exactly its slice of the single-GPU build."""
+    import multiprocessing as mp
+
+    from tests.test_cpu import _free_port
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_device_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(g[1] is True for g in got), got
+    assert got[0][2] > 0
+
+
+def test_sharded_world1_local_finish_and_rebuild(zb):
+    """World 1 skips the exchange (finish_local) and a rebuild keeps the buffers: both equal the
+    single-GPU build byte for byte."""
+    from paper_1712_06326_b200 import sharding
+    img, known = workloads.small_image(80, 100, 1, seed=29, hole_frac=0.08)
+    cfg = zb.index_config(patch_size=9, dims=8, knn=16)
+    mi = zb.MultiIndex(img, known, cfg)
+    sh = sharding.DeviceShard(img, known, cfg, 0, 1)
+    info = sharding.build_sharded([sh], sharding.LoopbackComm(1))
+    assert info["records_exchanged"] == 0
+    for rep in range(2):
+        for l in range(8):
+            a, b = sh.multi_index.index_arrays(l), mi.index_arrays(l)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (rep, l)
+        sh.rebuild()
+        sharding.build_sharded([sh], sharding.LoopbackComm(1))

@@ -49,3 +49,12 @@ labels = {1: "make_query", 2: "seed", 3: "scan", 4: "local_topk+cost", 5: "-", 6
 for j in range(9):
     col = a[:, 6 + j]
     print(f"  phase {j + 1} {labels[j + 1]:>16}: median {np.median(col):7.1f} us  p90 {np.percentile(col, 90):7.1f}")
+sp = re.compile(r"qlat ctas=(\d+) start_spread_us=([\d.]+) finish_first_us=([\d.]+) finish_last_us=([\d.]+) "
+                r"max_surv=(\d+) max_cand=(\d+) last_surv=(\d+) last_cand=(\d+)")
+rows = [tuple(float(x) for x in m.groups()) for m in (sp.match(l) for l in r.stderr.splitlines()) if m][:limit]
+if rows:
+    a = np.array(rows)
+    print(f"  CTAs {int(a[0, 0])}: start spread median {np.median(a[:, 1]):.1f} us, first finish {np.median(a[:, 2]):.1f}, "
+          f"last finish {np.median(a[:, 3]):.1f} (p90 {np.percentile(a[:, 3], 90):.1f})")
+    print(f"  survivors per CTA: max median {np.median(a[:, 4]):.0f}, candidates max median {np.median(a[:, 5]):.0f}; "
+          f"the last CTA: survivors {np.median(a[:, 6]):.0f}, candidates {np.median(a[:, 7]):.0f}")
