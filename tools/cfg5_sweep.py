@@ -99,7 +99,7 @@ def main():
         del X
         torch.cuda.empty_cache()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
-    json.dump({"config": "cfg5 (BASELINE.json configs[4]): dim 125, 0.9^k eigen-decay, 40% unknown query coords, k=%d" % k,
+    json.dump({"config": f"cfg5 (BASELINE.json configs[4]): dim 125, 0.9^k eigen-decay, 40 pct unknown query coords, k={k}",
                "queries": nq, "hbm_peak_gbs": hbm, "rows": rows}, open(args.out, "w"), indent=1)
 
 
