@@ -25,6 +25,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -39,7 +40,13 @@ constexpr int kPtMmaWarp = kPtGatherWarps + kPtEpiWarps;
 constexpr int kPtThreads = (kPtMmaWarp + 1) * 32;
 constexpr int kPtMaxFpad = 384;
 constexpr int kPtMaxN = 256;
-constexpr int kPtDigits = 5;                     // t = rint(c * 2^38) in five balanced base-256 digits
+// t = rint(c * 2^38) in five balanced base-256 digits.  (Four digits put all 8 layouts of a D = 8
+// build in one 256-column group, but their 256x larger E flags ~1.5 % of the cfg4 pairs for the
+// fp64 fix-up -- low-variance dims have ranges of only a few units -- which costs more than the
+// second group's gather saves.)
+constexpr int kPtDigits = 5;
+constexpr double kPtScale = 274877906944.0;      // 2^(8 * kPtDigits - 2)
+constexpr double kPtUnit = 1.0 / kPtScale;       // 2^-38
 
 struct pt_params {
     const uint8_t* img;
@@ -235,12 +242,12 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
                 const double M = s_M[li][d];
                 // z' = T * za + zb = 255 (T 2^-38 - M - lo) / R + 1/2 (its rounding, ~1e-11 even
                 // with cancellation, is inside Bz's 1e-9 slack)
-                const double za = degen ? 0.0 : 255.0 * 0x1p-38 / R;
+                const double za = degen ? 0.0 : 255.0 * kPtUnit / R;
                 const double zb = degen ? 0.0 : 0.5 - 255.0 * (M + lo) / R;
                 const double bz = degen ? 1.0 : 1.01 * 255.0 * 4.0 * P.E / R + 1e-9;
                 // lo / hi candidates: y' <= lo + 2E or y' >= hi - 2E, as T thresholds widened by
                 // a margin (a superset is harmless: candidates only cost a fix-up)
-                const double tl = (lo + 2.0 * P.E + M) * 0x1p38, th = (hi - 2.0 * P.E + M) * 0x1p38;
+                const double tl = (lo + 2.0 * P.E + M) * kPtScale, th = (hi - 2.0 * P.E + M) * kPtScale;
                 const long long tlo = degen ? LLONG_MAX : static_cast<long long>(ceil(tl + fabs(tl) * 0x1p-40)) + 16;
                 const long long thi = degen ? LLONG_MAX : static_cast<long long>(floor(th - fabs(th) * 0x1p-40)) - 16;
                 s_qc[li][d][0] = make_double2(za, zb);
@@ -366,6 +373,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
                     // fraction of the integer rate, so the min / max pass stays integer and the
                     // quantise pass converts once: y' = fl(T * 2^-38 - M) (T exact in a double)
                     const uint32_t* vd = v + kPtDigits * d;
+                    static_assert(kPtDigits == 5, "T assembly below is written for five digits");
                     const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
                                         (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
                                         (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
@@ -441,9 +449,9 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant
         if (li < nl && tmn0 <= tmx0) {  // the slot saw a valid row: y' of the extreme T (one rounding, as in the epilogue)
             const int l = P.l0 + li;
             const double M = s_M[li][d];
-            atomicMin(P.amm + static_cast<size_t>(l) * 2 * D + d, double_to_ordered(__dsub_rn(static_cast<double>(tmn0) * 0x1p-38, M)));
+            atomicMin(P.amm + static_cast<size_t>(l) * 2 * D + d, double_to_ordered(__dsub_rn(static_cast<double>(tmn0) * kPtUnit, M)));
             atomicMax(P.amm + static_cast<size_t>(l) * 2 * D + D + d,
-                      double_to_ordered(__dsub_rn(static_cast<double>(tmx0) * 0x1p-38, M)));
+                      double_to_ordered(__dsub_rn(static_cast<double>(tmx0) * kPtUnit, M)));
         }
     }
     tc_fence_before();
@@ -704,7 +712,7 @@ __global__ void k_pt_prep(const double* __restrict__ mean, const double* __restr
     if (tid < total) {
         const int l = tid / (mc * D), rem = tid - l * mc * D, j = rem / D, d = rem - j * D;
         const double c = comp[(static_cast<size_t>(l) * mc + j) * D + d];
-        long long t = llrint(c * 274877906944.0);  // exact scaling by 2^38, then round to nearest
+        long long t = llrint(c * kPtScale);  // exact scaling by 2^38, then round to nearest
         const int g = l / nlmax, li = l - g * nlmax;
         const int f = cols[l * mc + j];
         for (int k = 0; k < kPtDigits; ++k) {
@@ -883,7 +891,7 @@ static pt_plan pt_make_plan(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, u
     P.row_base = static_cast<uint32_t>(mi->row_begin);
     P.M = reinterpret_cast<const double*>(s + pl.o_M);
     P.amm = reinterpret_cast<unsigned long long*>(s + pl.o_amm);
-    P.E = 255.0 * mc * (0x1p-39 + 0x1p-44);
+    P.E = 255.0 * mc * (0.5 * kPtUnit + 0x1p-44);
     P.keyw = keyw;
     P.val = val;
     P.Nrec = Nrec;
@@ -994,8 +1002,25 @@ static void pt_phase_b(zi_multi_index* mi, pt_plan& pl) {
         uint32_t cnt = 0;
         ZI_CUDA(cudaMemcpyAsync(&cnt, pl.P.list_count, sizeof(cnt), cudaMemcpyDeviceToHost, mi->ctx->stream));
         ZI_CUDA(cudaStreamSynchronize(mi->ctx->stream));
-        std::fprintf(stderr, "project_tc: n=%llu D=%d groups=%d fix-up list %u (%.4f%% of patch x layout pairs)\n",
-                     static_cast<unsigned long long>(pl.P.n), pl.D, pl.ng, cnt, 100.0 * cnt / (8.0 * std::max<uint64_t>(pl.P.n, 1)));
+        std::vector<uint32_t> hl(cnt);
+        if (cnt) ZI_CUDA(cudaMemcpy(hl.data(), pl.P.list, cnt * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        uint64_t ncand = 0, per_l[8] = {};
+        for (uint32_t e : hl) {
+            ncand += (e >> 3) & 1u;
+            ++per_l[e & 7u];
+        }
+        std::vector<unsigned long long> amm(16 * pl.D);
+        ZI_CUDA(cudaMemcpy(amm.data(), pl.P.amm, amm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "project_tc: n=%llu D=%d groups=%d fix-up list %u (%.4f%% of patch x layout pairs), %llu lo/hi candidates; per layout",
+                     static_cast<unsigned long long>(pl.P.n), pl.D, pl.ng, cnt, 100.0 * cnt / (8.0 * std::max<uint64_t>(pl.P.n, 1)),
+                     static_cast<unsigned long long>(ncand));
+        for (int l = 0; l < 8; ++l) std::fprintf(stderr, " %llu", static_cast<unsigned long long>(per_l[l]));
+        std::fprintf(stderr, "\n  ranges(layout 0):");
+        for (int d = 0; d < pl.D; ++d) {
+            const double lo = ordered_to_double_hd(amm[d]), hi = ordered_to_double_hd(amm[pl.D + d]);
+            std::fprintf(stderr, " %.3g", hi - lo);
+        }
+        std::fprintf(stderr, "\n");
     }
     pt_launch_exact(mi->ctx, mi, pl, 0);
 }

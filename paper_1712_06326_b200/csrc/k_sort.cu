@@ -19,8 +19,6 @@
 namespace zi {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 constexpr int kMaxWords = 9;  // up to 8 Morton key words (D <= 32) + payload
@@ -97,58 +95,118 @@ __global__ void __launch_bounds__(256) k_sort_bases(const uint32_t* __restrict__
     bases[q * 256 + d] = wp + x - c;
 }
 
-// One stable digit pass.  Records come in groups of gn (group-major; G = 1: one group); a group
-// is tiled on its own (tpg tiles) and sorted on its own: digit_base holds the exclusive digit
-// prefix of each group ([g][256]), the decoupled look-back stops at the group's first tile.
-template <int NW>
-__global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort_words io, int dw, int ds,
-                                                           const uint32_t* __restrict__ digit_base,
-                                                           uint32_t* __restrict__ status,
-                                                           uint32_t* __restrict__ tile_ctr, uint64_t gn,
-                                                           uint32_t tpg) {
-    extern __shared__ uint32_t s_stage[];  // NW * kSortTile
+__device__ __forceinline__ uint32_t os_load(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void os_store(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Decoupled look-back for digit d (one thread per digit, status words tile-major: st[tile*256 + d]).
+// The statuses of kLbWin predecessors are loaded together (independent loads, one round trip),
+// then summed up to the first inclusive one; an unpublished predecessor is re-read from there.
+// A one-at-a-time walk pays one dependent L2 round trip per predecessor, and the number of
+// predecessors still holding only their aggregate grows with the tiles in flight.
+constexpr int kLbWin = 4;
+__device__ __forceinline__ uint32_t lookback(const uint32_t* st, uint32_t tile, uint32_t gfirst, int d) {
+    uint32_t prefix = 0;
+    int j = static_cast<int>(tile) - 1;
+    while (true) {
+        uint32_t v[kLbWin];
+#pragma unroll
+        for (int u = 0; u < kLbWin; ++u)
+            v[u] = j - u >= static_cast<int>(gfirst) ? os_load(st + static_cast<size_t>(j - u) * 256 + d) : kFlagInc;
+        int used = 0;
+        bool done = false;
+#pragma unroll
+        for (int u = 0; u < kLbWin; ++u) {
+            if (used == u && !done) {
+                const uint32_t flag = v[u] & ~kValMask;
+                if (flag != 0u) {
+                    prefix += v[u] & kValMask;
+                    ++used;
+                    done = flag == kFlagInc;
+                }
+            }
+        }
+        if (done) return prefix;
+        j -= used;
+    }
+}
+
+// One stable digit pass over a tile of TILE = 256 * IT records.  Records come in groups of gn
+// (group-major; G = 1: one group); a group is tiled on its own (tpg tiles) and sorted on its own.
+// Where the records of a digit go:
+//   MODE 1 (default): offs[tile][d] = global position of the tile's first record of digit d,
+//          precomputed by k_lsd_count + the chunk scans (reduce-then-scan: no inter-tile waits);
+//   MODE 0: digit_base[g][d] + decoupled look-back over the previous tiles of the group (status).
+// All record indices are 32-bit (N < 2^30); the word pointers are offset once per tile.  A
+// thread keeps IT records in registers plus one (digit << 16 | warp rank) word per record; the
+// records are staged in shared memory in tile-sorted order, then written as runs per digit.
+template <int NW, int IT, int MODE>
+__global__ void __launch_bounds__(kSortThreads, NW * IT <= 24 ? 4 : NW * IT <= 36 ? 3 : 2)
+    k_onesweep(sort_words io, int dw, int ds, const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
+               uint32_t* __restrict__ tile_ctr, const uint32_t* __restrict__ offs, uint32_t gn, uint32_t tpg) {
+    constexpr int TILE = kSortThreads * IT;
+    extern __shared__ uint32_t s_stage[];  // NW * TILE
     __shared__ uint32_t s_hist[kSortWarps][256];
     __shared__ uint32_t s_start[256];
-    __shared__ uint32_t s_gofs[256];
-    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_delta[256];  // global position of the digit's first record, minus its tile start
+    __shared__ uint32_t s_warp[kSortWarps];
     __shared__ uint32_t s_tile;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&s_hist[0][0])[i] = 0;
-    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    if (MODE == 0) {
+        if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+        __syncthreads();
+    }
+    const uint32_t tile = MODE == 0 ? s_tile : blockIdx.x;
     const uint32_t grp = tile / tpg, tig = tile - grp * tpg;  // group, tile inside the group
-    const uint64_t gbase = static_cast<uint64_t>(grp) * gn;
-    const uint64_t tbase = gbase + static_cast<uint64_t>(tig) * kSortTile;
-    const uint64_t n = gbase + gn;  // end of the group
-    const uint64_t wbase = tbase + warp * (kSortItems * 32);
+    const uint32_t t0 = tig * static_cast<uint32_t>(TILE);
+    const uint32_t cnt = gn - t0 < static_cast<uint32_t>(TILE) ? gn - t0 : static_cast<uint32_t>(TILE);
+    const uint32_t tb = grp * gn + t0;  // global index of the tile's first record
+    uint32_t goff = 0;
+    if (MODE == 1) goff = __ldg(offs + static_cast<size_t>(tile) * 256 + tid);  // in flight with the records
 
     // every word of the tile's records is loaded up front (maximum loads in flight)
-    uint32_t rec[kSortItems][NW];
-    uint32_t dig[kSortItems];
-    uint32_t rank[kSortItems];
+    uint32_t rec[IT][NW];
+    uint32_t dr[IT];
+    const uint32_t w0 = static_cast<uint32_t>(warp * (IT * 32) + lane);
+    {
+        const uint32_t* src[NW];
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        const uint64_t idx = wbase + i * 32 + lane;
-        const bool ok = idx < n;
+        for (int k = 0; k < NW; ++k) src[k] = io.in[k] + tb;
 #pragma unroll
-        for (int k = 0; k < NW; ++k) rec[i][k] = ok ? io.in[k][idx] : 0u;
-        // (a second, L1-hitting load of the digit word: selecting it from rec[] by the runtime
-        // dw makes the compiler spill rec[] to local memory)
-        dig[i] = ok ? (__ldg(io.in[dw] + idx) >> ds) & 0xffu : 0x100u;
+        for (int i = 0; i < IT; ++i) {
+            const uint32_t j = w0 + static_cast<uint32_t>(i * 32);
+            const bool ok = j < cnt;
+#pragma unroll
+            for (int k = 0; k < NW; ++k) rec[i][k] = ok ? __ldg(src[k] + j) : 0u;
+        }
     }
+    if (MODE == 1) __syncthreads();  // s_hist zeroed
     const uint32_t lt_mask = (1u << lane) - 1u;
+    // the digit word through masks (a select chain on rec[i][k] becomes an indexed local-memory
+    // load of rec[] after the compiler's select-to-index rewrite)
+    uint32_t wmask[NW];
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        const uint32_t d = dig[i];
+    for (int k = 0; k < NW; ++k) wmask[k] = dw == k ? 0xffffffffu : 0u;
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) x |= rec[i][k] & wmask[k];
+        const uint32_t d = w0 + static_cast<uint32_t>(i * 32) < cnt ? (x >> ds) & 0xffu : 0x100u;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t old = 0;
         if (d < 256u) old = s_hist[warp][d];
         __syncwarp();
         if (d < 256u && (peers >> lane) == 1u) s_hist[warp][d] = old + __popc(peers);
         __syncwarp();
-        rank[i] = old + __popc(peers & lt_mask);
+        dr[i] = (d << 16) | (old + __popc(peers & lt_mask));
     }
     __syncthreads();
 
@@ -162,11 +220,10 @@ __global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort
         run += t;
     }
     const uint32_t tile_cnt = run;
-    volatile uint32_t* vstatus = status;
-    if (tig == 0) vstatus[static_cast<size_t>(tile) * 256 + d] = kFlagInc | tile_cnt;
-    else vstatus[static_cast<size_t>(tile) * 256 + d] = kFlagAgg | tile_cnt;
+    if (MODE == 0) os_store(status + static_cast<size_t>(tile) * 256 + d, (tig == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
 
     // tile-local exclusive scan over digits
+    uint32_t start;
     {
         uint32_t x = tile_cnt;
 #pragma unroll
@@ -177,58 +234,197 @@ __global__ void __launch_bounds__(kSortThreads, NW <= 3 ? 3 : 2) k_onesweep(sort
         if (lane == 31) s_warp[warp] = x;
         __syncthreads();
         uint32_t wp = 0;
-        for (int w = 0; w < warp; ++w) wp += s_warp[w];
-        s_start[d] = wp + x - tile_cnt;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) wp += w < warp ? s_warp[w] : 0u;
+        start = wp + x - tile_cnt;
+        s_start[d] = start;
     }
-
-    // decoupled look-back for the prefix of digit d over the previous tiles
-    uint32_t prefix = 0;
-    if (tig > 0) {
-        int64_t j = static_cast<int64_t>(tile) - 1;
-        while (true) {
-            const uint32_t v = vstatus[static_cast<size_t>(j) * 256 + d];
-            const uint32_t flag = v & ~kValMask;
-            if (flag == 0) continue;  // predecessor not yet published
-            prefix += v & kValMask;
-            if (flag == kFlagInc) break;
-            --j;
+    if (MODE == 0) {
+        uint32_t prefix = 0;
+        if (tig > 0) {
+            prefix = lookback(status, tile, tile - tig, d);
+            os_store(status + static_cast<size_t>(tile) * 256 + d, kFlagInc | (prefix + tile_cnt));
         }
-        vstatus[static_cast<size_t>(tile) * 256 + d] = kFlagInc | (prefix + tile_cnt);
+        goff = grp * gn + digit_base[grp * 256 + d] + prefix;
     }
-    s_gofs[d] = static_cast<uint32_t>(gbase) + digit_base[grp * 256 + d] + prefix;
+    s_delta[d] = goff - start;
     __syncthreads();
 
     // stage records in tile-sorted order
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        if (dig[i] < 256u) {
-            const uint32_t pos = s_start[dig[i]] + s_hist[warp][dig[i]] + rank[i];
+    for (int i = 0; i < IT; ++i) {
+        const uint32_t dg = dr[i] >> 16;
+        if (dg < 256u) {
+            const uint32_t pos = s_start[dg] + s_hist[warp][dg] + (dr[i] & 0xffffu);
 #pragma unroll
-            for (int k = 0; k < NW; ++k) s_stage[k * kSortTile + pos] = rec[i][k];
+            for (int k = 0; k < NW; ++k) s_stage[k * TILE + pos] = rec[i][k];
         }
     }
     __syncthreads();
-    const uint32_t cnt = static_cast<uint32_t>(n - tbase < static_cast<uint64_t>(kSortTile) ? n - tbase : kSortTile);
-    for (uint32_t j = tid; j < cnt; j += kSortThreads) {
-        const uint32_t dd = (s_stage[dw * kSortTile + j] >> ds) & 0xffu;
-        const uint64_t o = static_cast<uint64_t>(s_gofs[dd]) + (j - s_start[dd]);
+    uint32_t* dst[NW];
 #pragma unroll
-        for (int k = 0; k < NW; ++k) io.out[k][o] = s_stage[k * kSortTile + j];
+    for (int k = 0; k < NW; ++k) dst[k] = io.out[k];
+    const uint32_t* sdig = s_stage + dw * TILE;
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const uint32_t j = static_cast<uint32_t>(tid + i * kSortThreads);
+        if (j < cnt) {
+            const uint32_t o = s_delta[(sdig[j] >> ds) & 0xffu] + j;
+#pragma unroll
+            for (int k = 0; k < NW; ++k) dst[k][o] = s_stage[k * TILE + j];
+        }
     }
 }
 
+// ---- reduce-then-scan offsets of one pass (MODE 1).  Tiles are grouped in chunks of kLsdChunk
+// consecutive tiles of one group: counts[tile][d] -> chunk sums -> per group an exclusive scan over
+// its chunks plus the group's digit bases -> per chunk a running sum over its tiles, in place:
+// counts[tile][d] becomes the global position of the tile's first record of digit d.
+constexpr int kLsdChunk = 32;
+
+template <int IT>
+__global__ void __launch_bounds__(kSortThreads) k_lsd_count(const uint32_t* __restrict__ word, int ds, uint32_t gn,
+                                                            uint32_t tpg, uint32_t* __restrict__ counts) {
+    constexpr int TILE = kSortThreads * IT;
+    __shared__ uint32_t s_h[kSortWarps][256];  // per-warp counts: contention only inside a warp
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t tile = blockIdx.x, grp = tile / tpg, tig = tile - grp * tpg;
+    const uint32_t t0 = tig * static_cast<uint32_t>(TILE);
+    const uint32_t cnt = gn - t0 < static_cast<uint32_t>(TILE) ? gn - t0 : static_cast<uint32_t>(TILE);
+    const uint32_t* src = word + grp * gn + t0;
+    for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&s_h[0][0])[i] = 0;
+    uint32_t x[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const uint32_t j = static_cast<uint32_t>(tid + i * kSortThreads);
+        x[i] = j < cnt ? __ldg(src + j) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const uint32_t j = static_cast<uint32_t>(tid + i * kSortThreads);
+        if (j < cnt) atomicAdd(&s_h[warp][(x[i] >> ds) & 0xffu], 1u);
+    }
+    __syncthreads();
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) c += s_h[w][tid];
+    counts[static_cast<size_t>(tile) * 256 + tid] = c;
+}
+
+__global__ void __launch_bounds__(256) k_lsd_chunk_sum(const uint32_t* __restrict__ counts, uint32_t tpg, uint32_t cpg,
+                                                       uint32_t* __restrict__ csum) {
+    const uint32_t c = blockIdx.x, g = c / cpg, k = c - g * cpg, d = threadIdx.x;
+    const uint32_t t0 = g * tpg + k * kLsdChunk, t1 = min(t0 + kLsdChunk, (g + 1) * tpg);
+    uint32_t s = 0;
+#pragma unroll 8
+    for (uint32_t t = t0; t < t1; ++t) s += __ldg(counts + static_cast<size_t>(t) * 256 + d);
+    csum[static_cast<size_t>(c) * 256 + d] = s;
+}
+
+__global__ void __launch_bounds__(256) k_lsd_chunk_scan(uint32_t* __restrict__ csum, uint32_t cpg, uint32_t gn) {
+    __shared__ uint32_t s_w[8];
+    const uint32_t g = blockIdx.x;
+    const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    uint32_t* cs = csum + static_cast<size_t>(g) * cpg * 256 + d;
+    uint32_t run = 0;
+    for (uint32_t k = 0; k < cpg; ++k) {
+        const uint32_t v = cs[static_cast<size_t>(k) * 256];
+        cs[static_cast<size_t>(k) * 256] = run;
+        run += v;
+    }
+    // the group's digit bases: exclusive scan of the totals over the digits
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t wp = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) wp += w < warp ? s_w[w] : 0u;
+    const uint32_t base = g * gn + wp + x - run;
+    for (uint32_t k = 0; k < cpg; ++k) cs[static_cast<size_t>(k) * 256] += base;
+}
+
+__global__ void __launch_bounds__(256) k_lsd_offsets(uint32_t* __restrict__ counts, const uint32_t* __restrict__ csum,
+                                                     uint32_t tpg, uint32_t cpg) {
+    const uint32_t c = blockIdx.x, g = c / cpg, k = c - g * cpg, d = threadIdx.x;
+    const uint32_t t0 = g * tpg + k * kLsdChunk, t1 = min(t0 + kLsdChunk, (g + 1) * tpg);
+    uint32_t run = csum[static_cast<size_t>(c) * 256 + d];
+    uint32_t v[kLsdChunk];  // the chunk's counts, all loads in flight before the running sum
+#pragma unroll
+    for (int u = 0; u < kLsdChunk; ++u) v[u] = t0 + u < t1 ? counts[static_cast<size_t>(t0 + u) * 256 + d] : 0u;
+#pragma unroll
+    for (int u = 0; u < kLsdChunk; ++u) {
+        if (t0 + u < t1) counts[static_cast<size_t>(t0 + u) * 256 + d] = run;
+        run += v[u];
+    }
+}
+
+// records per thread: the largest count whose registers fit without spills at the kernel's
+// occupancy (NW * IT <= 36: three CTAs per SM, else two)
 template <int NW>
-static void launch_onesweep(zi_ctx* ctx, const sort_words& io, int dw, int ds, const uint32_t* base, uint32_t* status,
-                            uint32_t* ctr, uint64_t gn, unsigned tpg, unsigned ntiles) {
-    const size_t smem = static_cast<size_t>(NW) * kSortTile * sizeof(uint32_t);
-    smem_attr(ctx->device, k_onesweep<NW>, kMaxWords * kSortTile * sizeof(uint32_t));
-    ZI_LAUNCH(ctx, "radix_onesweep", k_onesweep<NW>, ntiles, kSortThreads, smem, io, dw, ds, base, status, ctr, gn,
-              tpg);
+constexpr int os_items() {
+    return NW == 2 ? 12 : NW == 3 ? 12 : NW == 4 ? 16 : NW == 5 ? 12 : 8;
+}
+
+static int onesweep_items(int nw) {
+    switch (nw) {
+        case 2: return os_items<2>();
+        case 3: return os_items<3>();
+        case 4: return os_items<4>();
+        case 5: return os_items<5>();
+        case 6: return os_items<6>();
+        case 7: return os_items<7>();
+        case 8: return os_items<8>();
+        default: return os_items<9>();
+    }
+}
+
+static bool lookback_mode() {  // ZI_SORT_LOOKBACK=1: the decoupled look-back pass (A/B)
+    static const bool v = std::getenv("ZI_SORT_LOOKBACK") != nullptr;
+    return v;
+}
+
+struct pass_plan {
+    uint64_t gn;
+    unsigned tpg, ntiles, cpg;
+    const uint32_t* digit_base;  // MODE 0
+    uint32_t* status;            // MODE 0
+    uint32_t* ctr;               // MODE 0
+    uint32_t* counts;            // MODE 1: [ntiles][256]
+    uint32_t* csum;              // MODE 1: [G * cpg][256]
+};
+
+template <int NW>
+static void launch_pass(zi_ctx* ctx, const sort_words& io, int dw, int ds, const pass_plan& pp, int G) {
+    constexpr int IT = os_items<NW>();
+    const size_t smem = static_cast<size_t>(NW) * kSortThreads * IT * sizeof(uint32_t);
+    if (lookback_mode()) {
+        smem_attr(ctx->device, k_onesweep<NW, IT, 0>, smem);
+        ZI_LAUNCH(ctx, "radix_onesweep", (k_onesweep<NW, IT, 0>), pp.ntiles, kSortThreads, smem, io, dw, ds, pp.digit_base,
+                  pp.status, pp.ctr, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t>(pp.gn), pp.tpg);
+        return;
+    }
+    const uint32_t gn = static_cast<uint32_t>(pp.gn);
+    ZI_LAUNCH(ctx, "radix_count", k_lsd_count<IT>, pp.ntiles, kSortThreads, 0, io.in[dw], ds, gn, pp.tpg, pp.counts);
+    const unsigned nch = pp.cpg * static_cast<unsigned>(G);
+    ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_sum, nch, 256, 0, pp.counts, pp.tpg, pp.cpg, pp.csum);
+    ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_scan, static_cast<unsigned>(G), 256, 0, pp.csum, pp.cpg, gn);
+    ZI_LAUNCH(ctx, "radix_scan", k_lsd_offsets, nch, 256, 0, pp.counts, pp.csum, pp.tpg, pp.cpg);
+    smem_attr(ctx->device, k_onesweep<NW, IT, 1>, smem);
+    ZI_LAUNCH(ctx, "radix_onesweep", (k_onesweep<NW, IT, 1>), pp.ntiles, kSortThreads, smem, io, dw, ds,
+              static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+              static_cast<const uint32_t*>(pp.counts), gn, pp.tpg);
 }
 
 // Generic stable LSD sort of NW-word SoA records; passes are (word, shift) digits from the
-// least significant.  Trivial passes (every group's records share the digit) are skipped.
-// G groups of n/G records (group-major) are sorted each on its own (no pass on a group digit).
+// least significant.  Trivial passes (every group's records share the digit) are skipped when the
+// histograms are on the host.  G groups of n/G records (group-major) are sorted each on its own
+// (no pass on a group digit).
 // digit histograms of every pass (host copy, [pass][group][256]), one read of the records
 std::vector<uint32_t> pass_histograms(zi_ctx* ctx, uint32_t* const* words, int nw, uint64_t n,
                                       const std::vector<int2>& passes, int G) {
@@ -255,81 +451,100 @@ std::vector<uint32_t> pass_histograms(zi_ctx* ctx, uint32_t* const* words, int n
 static bool groups_fit(int npass, int G) { return npass <= 40 && G <= 8; }
 
 // result (optional): receives the buffers holding the sorted words -- the scratch copy after an
-// odd number of passes -- instead of copying them back into `words`
+// odd number of passes -- instead of copying them back into `words`.  device_bases: every pass
+// runs, nothing goes through the host (the histograms are only needed to skip trivial passes).
 void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
                       const uint32_t* hist_host, bool device_bases, uint32_t** result, int G) {
     if (result)
         for (int k = 0; k < nw; ++k) result[k] = words[k];
     if (n <= 1 || passes.empty()) return;
     if (n > kValMask) throw error(ZI_E_INVALID, "radix sort: more than 2^30 records");
-    if (nw > kMaxWords) throw error(ZI_E_INVALID, "radix sort: too many words");
+    if (nw < 2 || nw > kMaxWords) throw error(ZI_E_INVALID, "radix sort: unsupported record width");
     if (G < 1 || n % G != 0) throw error(ZI_E_INVALID, "radix sort: records do not split into equal groups");
     const int npass = static_cast<int>(passes.size());
-    const uint64_t gn = n / G;
-    const unsigned tpg = static_cast<unsigned>((gn + kSortTile - 1) / kSortTile);
-    const unsigned ntiles = tpg * static_cast<unsigned>(G);
-    // scratch layout: alt words (nw*n) | hist (npass*G*256) | bases (same) | status (npass*ntiles*256) | ctr
+    const bool lb = lookback_mode();
+    pass_plan pp{};
+    pp.gn = n / G;
+    const uint64_t tile = static_cast<uint64_t>(kSortThreads) * onesweep_items(nw);
+    pp.tpg = static_cast<unsigned>((pp.gn + tile - 1) / tile);
+    pp.ntiles = pp.tpg * static_cast<unsigned>(G);
+    pp.cpg = (pp.tpg + kLsdChunk - 1) / kLsdChunk;
+    // scratch: alt words (nw*n) | hist (npass*G*256) | bases (same) | MODE 1: counts (ntiles*256),
+    // chunk sums (G*cpg*256) / MODE 0: status (npass*ntiles*256), counters | pass table
     const size_t alt_words = static_cast<size_t>(nw) * n;
     const size_t hist_words = static_cast<size_t>(npass) * G * 256;
-    const size_t status_words = static_cast<size_t>(npass) * ntiles * 256;
+    const size_t work_words = lb ? static_cast<size_t>(npass) * pp.ntiles * 256 + npass + 8
+                                 : static_cast<size_t>(pp.ntiles) * 256 + static_cast<size_t>(G) * pp.cpg * 256;
     uint32_t* scr = reinterpret_cast<uint32_t*>(
-        ctx->scratch.ensure((alt_words + 2 * hist_words + status_words + 4 * npass + 64) * sizeof(uint32_t)));
+        ctx->scratch.ensure((alt_words + 2 * hist_words + work_words + 4 * npass + 64) * sizeof(uint32_t)));
     uint32_t* alt = scr;
     uint32_t* hist = alt + alt_words;
     uint32_t* bases = hist + hist_words;
-    uint32_t* status = bases + hist_words;
-    uint32_t* ctr = status + status_words;
-    int2* d_passes = reinterpret_cast<int2*>(ctr + npass + 8);  // tiny
+    uint32_t* work = bases + hist_words;
+    int2* d_passes = reinterpret_cast<int2*>(work + work_words + 8);  // tiny
     d_passes = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(d_passes) + 15) & ~uintptr_t(15));
+    if (lb) {
+        pp.status = work;
+        pp.ctr = work + static_cast<size_t>(npass) * pp.ntiles * 256;
+    } else {
+        pp.counts = work;
+        pp.csum = work + static_cast<size_t>(pp.ntiles) * 256;
+    }
 
-    ZI_CUDA(cudaMemsetAsync(hist, 0, hist_words * sizeof(uint32_t), ctx->stream));
-    ZI_CUDA(cudaMemcpyAsync(d_passes, passes.data(), passes.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
     sort_words io{};
     for (int k = 0; k < nw; ++k) {
         io.in[k] = words[k];
         io.out[k] = alt + static_cast<size_t>(k) * n;
     }
-    std::vector<uint32_t> h_hist(hist_words);
     std::vector<int> active;
-    std::vector<uint32_t> h_bases(hist_words, 0);
+    std::vector<uint32_t> h_hist(hist_words);
     auto run_hist = [&] {
+        ZI_CUDA(cudaMemsetAsync(hist, 0, hist_words * sizeof(uint32_t), ctx->stream));
+        ZI_CUDA(cudaMemcpyAsync(d_passes, passes.data(), passes.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 4));
         const size_t hsm = static_cast<size_t>(npass) * 256 * sizeof(uint32_t);
         smem_attr(ctx->device, k_sort_hist, hsm);
-        ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hsm, io, npass, d_passes, n, gn, G, hist);
+        ZI_LAUNCH(ctx, "radix_hist", k_sort_hist, grid, 256, hsm, io, npass, d_passes, n, pp.gn, G, hist);
     };
     if (device_bases) {  // no host round trip: every pass runs (trivial ones are a copy)
-        run_hist();
-        ZI_LAUNCH(ctx, "radix_bases", k_sort_bases, static_cast<unsigned>(npass * G), 256, 0, hist, bases);
-        for (int q = 0; q < npass; ++q) active.push_back(q);
-    } else if (hist_host) {
-        std::copy(hist_host, hist_host + hist_words, h_hist.begin());
-    } else {
-        run_hist();
-        ZI_CUDA(cudaMemcpyAsync(h_hist.data(), hist, hist_words * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-        ZI_CUDA(cudaStreamSynchronize(ctx->stream));
-    }
-    for (int q = 0; q < npass && !device_bases; ++q) {
-        bool trivial = true;
-        for (int g = 0; g < G; ++g) {
-            bool gt = false;
-            uint32_t run = 0;
-            for (int dgt = 0; dgt < 256; ++dgt) {
-                const size_t at = (static_cast<size_t>(q) * G + g) * 256 + dgt;
-                const uint32_t c = h_hist[at];
-                if (c == gn) gt = true;
-                h_bases[at] = run;
-                run += c;
-            }
-            trivial = trivial && gt;
+        if (lb) {  // the look-back pass needs the global digit bases up front
+            run_hist();
+            ZI_LAUNCH(ctx, "radix_bases", k_sort_bases, static_cast<unsigned>(npass * G), 256, 0, hist, bases);
         }
-        if (!trivial) active.push_back(q);
+        for (int q = 0; q < npass; ++q) active.push_back(q);
+    } else {
+        if (hist_host) {
+            std::copy(hist_host, hist_host + hist_words, h_hist.begin());
+        } else {
+            run_hist();
+            ZI_CUDA(cudaMemcpyAsync(h_hist.data(), hist, hist_words * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        std::vector<uint32_t> h_bases(hist_words, 0);
+        for (int q = 0; q < npass; ++q) {
+            bool trivial = true;
+            for (int g = 0; g < G; ++g) {
+                bool gt = false;
+                uint32_t r = 0;
+                for (int dgt = 0; dgt < 256; ++dgt) {
+                    const size_t at = (static_cast<size_t>(q) * G + g) * 256 + dgt;
+                    const uint32_t c = h_hist[at];
+                    if (c == pp.gn) gt = true;
+                    h_bases[at] = r;
+                    r += c;
+                }
+                trivial = trivial && gt;
+            }
+            if (!trivial) active.push_back(q);
+        }
+        if (!active.empty() && lb)
+            ZI_CUDA(cudaMemcpyAsync(bases, h_bases.data(), hist_words * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
     }
     if (active.empty()) return;
-    if (!device_bases)
-        ZI_CUDA(cudaMemcpyAsync(bases, h_bases.data(), hist_words * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
-    ZI_CUDA(cudaMemsetAsync(status, 0, status_words * sizeof(uint32_t), ctx->stream));
-    ZI_CUDA(cudaMemsetAsync(ctr, 0, npass * sizeof(uint32_t), ctx->stream));
+    if (lb) {
+        ZI_CUDA(cudaMemsetAsync(pp.status, 0, static_cast<size_t>(npass) * pp.ntiles * 256 * sizeof(uint32_t), ctx->stream));
+        ZI_CUDA(cudaMemsetAsync(pp.ctr, 0, npass * sizeof(uint32_t), ctx->stream));
+    }
     uint32_t* cur[kMaxWords];
     uint32_t* oth[kMaxWords];
     for (int k = 0; k < nw; ++k) {
@@ -342,19 +557,22 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
             io.in[k] = cur[k];
             io.out[k] = oth[k];
         }
-        uint32_t* st = status + static_cast<size_t>(q) * ntiles * 256;
-        const uint32_t* qb = bases + static_cast<size_t>(q) * G * 256;
+        pass_plan pq = pp;
+        if (lb) {
+            pq.status = pp.status + static_cast<size_t>(q) * pp.ntiles * 256;
+            pq.ctr = pp.ctr + q;
+            pq.digit_base = bases + static_cast<size_t>(q) * G * 256;
+        }
         const int dw = passes[q].x, ds = passes[q].y;
         switch (nw) {
-            case 2: launch_onesweep<2>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
-            case 3: launch_onesweep<3>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
-            case 4: launch_onesweep<4>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
-            case 5: launch_onesweep<5>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
-            case 6: launch_onesweep<6>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
-            case 7: launch_onesweep<7>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
-            case 8: launch_onesweep<8>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
-            case 9: launch_onesweep<9>(ctx, io, dw, ds, qb, st, ctr + q, gn, tpg, ntiles); break;
-            default: throw error(ZI_E_INVALID, "radix sort: unsupported record width");
+            case 2: launch_pass<2>(ctx, io, dw, ds, pq, G); break;
+            case 3: launch_pass<3>(ctx, io, dw, ds, pq, G); break;
+            case 4: launch_pass<4>(ctx, io, dw, ds, pq, G); break;
+            case 5: launch_pass<5>(ctx, io, dw, ds, pq, G); break;
+            case 6: launch_pass<6>(ctx, io, dw, ds, pq, G); break;
+            case 7: launch_pass<7>(ctx, io, dw, ds, pq, G); break;
+            case 8: launch_pass<8>(ctx, io, dw, ds, pq, G); break;
+            default: launch_pass<9>(ctx, io, dw, ds, pq, G); break;
         }
         for (int k = 0; k < nw; ++k) std::swap(cur[k], oth[k]);
     }
@@ -865,6 +1083,13 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         radix_sort_words(ctx, words, nw, N, msd, nullptr, true, cur, G);
         finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, all_full, G, learnt);
         if (verify_on()) verify_sorted(ctx, cur, W, N, D, nb, layouts);
+        done();
+        return;
+    }
+    if (learnt < 0 && msd_bytes_forced() <= 0) {
+        // an earlier build with these dims found the top bytes too clustered for the MSD split:
+        // the plain LSD sort, every pass on the device (no histogram round trip)
+        radix_sort_words(ctx, words, nw, N, all, nullptr, true, cur, G);
         done();
         return;
     }
