@@ -615,53 +615,68 @@ __global__ void __launch_bounds__(256) k_interleave(const uint8_t* __restrict__ 
 // ============================================================== K5: finalize
 // Sorted Morton words -> dim planes (4 dims per u32), keys, and per-256-entry bboxes.
 // Entries [off, off+n) of a record array with word stride N; when dict != nullptr the payload
-// is a dictionary row (low 29 bits) and the key is gathered from dict.
+// is a dictionary row (low 29 bits) and the key is gathered from dict (L2-resident).
+// One warp per 256-entry bbox block, 8 entries per lane (coalesced, all loads and the dictionary
+// gathers in flight together); the bbox is a warp reduction (no block barrier).
+constexpr int kFinWarps = 8;
 template <int D>
-__global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
-                                                  uint64_t N, uint64_t off, uint64_t n,
-                                                  const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
-                                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
-                                                  uint32_t* __restrict__ bmax, uint64_t nblk) {
-    constexpr int W = (D + 3) / 4, P = W;
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
-    const bool ok = i < n;
-    uint32_t kw[W];
+__global__ void __launch_bounds__(kFinWarps * 32) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
+                                                           uint64_t N, uint64_t off, uint64_t n,
+                                                           const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
+                                                           uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
+                                                           uint32_t* __restrict__ bmax, uint64_t nblk) {
+    constexpr int W = (D + 3) / 4, P = W, E = 8;
+    const int lane = threadIdx.x & 31;
+    const uint64_t blk = static_cast<uint64_t>(blockIdx.x) * kFinWarps + (threadIdx.x >> 5);
+    if (blk >= nblk) return;
+    const uint64_t b0 = blk * 256;
+    uint32_t kw[E][W], v[E];
 #pragma unroll
-    for (int k = 0; k < W; ++k) kw[k] = ok ? keyw[static_cast<size_t>(k) * N + off + i] : 0u;
-    if (ok) {
-        const uint32_t v = val[off + i];
-        keys[i] = dict ? dict[v & ((1u << 29) - 1u)] : v;
+    for (int e = 0; e < E; ++e) {
+        const uint64_t i = b0 + e * 32 + lane;
+        const bool ok = i < n;
+#pragma unroll
+        for (int k = 0; k < W; ++k) kw[e][k] = ok ? __ldg(keyw + static_cast<size_t>(k) * N + off + i) : 0u;
+        v[e] = ok ? __ldg(val + off + i) : 0u;
     }
-    __shared__ uint32_t s_mn[P][8], s_mx[P][8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t pw[P];
-    morton_deinterleave8<D>(kw, pw);
+    if (dict) {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            if (b0 + e * 32 + lane < n) v[e] = __ldg(dict + (v[e] & ((1u << 29) - 1u)));
+    }
+    uint32_t mn[P], mx[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-        const uint32_t word = pw[p];
-        if (ok) planes[static_cast<size_t>(p) * n + i] = word;
-        uint32_t mn = ok ? word : 0xffffffffu, mx = ok ? word : 0u;
+        mn[p] = 0xffffffffu;
+        mx[p] = 0u;
+    }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mn = __vminu4(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = __vmaxu4(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        }
-        if (lane == 0) {
-            s_mn[p][warp] = mn;
-            s_mx[p][warp] = mx;
+    for (int e = 0; e < E; ++e) {
+        const uint64_t i = b0 + e * 32 + lane;
+        if (i < n) {
+            uint32_t pw[P];
+            morton_deinterleave8<D>(kw[e], pw);
+            keys[i] = v[e];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                planes[static_cast<size_t>(p) * n + i] = pw[p];
+                mn[p] = __vminu4(mn[p], pw[p]);
+                mx[p] = __vmaxu4(mx[p], pw[p]);
+            }
         }
     }
-    __syncthreads();
-    if (threadIdx.x < P) {
-        const int p = threadIdx.x;
-        uint32_t mn = 0xffffffffu, mx = 0;
-        for (int k = 0; k < 8; ++k) {
-            mn = __vminu4(mn, s_mn[p][k]);
-            mx = __vmaxu4(mx, s_mx[p][k]);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[p] = __vminu4(mn[p], __shfl_xor_sync(0xffffffffu, mn[p], o));
+            mx[p] = __vmaxu4(mx[p], __shfl_xor_sync(0xffffffffu, mx[p], o));
         }
         // padding bytes (dims >= D) are zero in both coords and queries
-        bmin[static_cast<size_t>(p) * nblk + blockIdx.x] = mn;
-        bmax[static_cast<size_t>(p) * nblk + blockIdx.x] = mx;
+        if (lane == p) {
+            bmin[static_cast<size_t>(p) * nblk + blk] = mn[p];
+            bmax[static_cast<size_t>(p) * nblk + blk] = mx[p];
+        }
     }
 }
 
@@ -713,7 +728,8 @@ static void launch_quantize_t(zi_ctx* ctx, const double* Y, const unsigned long 
 template <int D>
 static void launch_finalize_t(zi_ctx* ctx, const uint32_t* keyw, const uint32_t* val, uint64_t N, uint64_t off,
                               uint64_t n, const uint32_t* dict, zi_index* idx) {
-    ZI_LAUNCH(ctx, "finalize_index", k_finalize<D>, static_cast<unsigned>(idx->nblk), 256, 0, keyw, val, N, off, n,
+    ZI_LAUNCH(ctx, "finalize_index", k_finalize<D>, static_cast<unsigned>((idx->nblk + kFinWarps - 1) / kFinWarps),
+              kFinWarps * 32, 0, keyw, val, N, off, n,
               dict, idx->planes.p, idx->keys.p, idx->bbox_min.p, idx->bbox_max.p, idx->nblk);
 }
 
