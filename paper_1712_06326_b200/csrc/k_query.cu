@@ -1002,6 +1002,136 @@ __global__ void __launch_bounds__(256) k_brute4(const uint8_t* __restrict__ img,
     if (threadIdx.x == 0) atomicMin(best, s_best);
 }
 
+// The exhaustive scan for gray images, eight dictionary entries per thread.  When the eight keys
+// are consecutive columns of one row, three aligned word loads + two funnel shifts per known value
+// give that pixel for all eight patches; the byte differences (__vabsdiffu4) of four values are
+// transposed with byte permutes so that one __dp4a adds four values of one patch (8 PRMT + 8 DP4A
+// per 4 values x 8 patches, instead of a mask + __dp4a per patch and value).  The known values and
+// their offsets are read as 16-byte vectors; a tail of nv % 4 values and non-consecutive octets
+// take the per-lane path.  Same (cost, key) minimum as k_brute.
+__device__ __forceinline__ void transpose4x4_bytes(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3, uint32_t (&t)[4]) {
+    const uint32_t a = __byte_perm(d0, d1, 0x5140), b = __byte_perm(d0, d1, 0x7362);
+    const uint32_t c = __byte_perm(d2, d3, 0x5140), e = __byte_perm(d2, d3, 0x7362);
+    t[0] = __byte_perm(a, c, 0x5410);
+    t[1] = __byte_perm(a, c, 0x7632);
+    t[2] = __byte_perm(b, e, 0x5410);
+    t[3] = __byte_perm(b, e, 0x7632);
+}
+
+__global__ void __launch_bounds__(256) k_brute8(const uint8_t* __restrict__ img, int w, int K,
+                                                const uint32_t* __restrict__ dict, uint64_t n,
+                                                const uint8_t* __restrict__ target, int norm,
+                                                unsigned long long* __restrict__ best) {
+    // shared: the known target values replicated x4 and their byte offsets from the patch origin,
+    // padded to a multiple of 4 entries (16-byte aligned arrays)
+    extern __shared__ __align__(16) uint32_t s_t4[];
+    __shared__ int s_nv;
+    __shared__ unsigned long long s_best;
+    const int KK = K * K, KP = (KK + 3) & ~3;
+    int* s_off = reinterpret_cast<int*>(s_t4 + KP);
+    if (threadIdx.x < 32) {
+        int cnt = 0;
+        for (int base = 0; base < KK; base += 32) {
+            const int l = base + threadIdx.x;
+            const bool kn = l < KK && target[KK + l] != 0;
+            const unsigned m = __ballot_sync(0xffffffffu, kn);
+            if (kn) {
+                const int slot = cnt + __popc(m & ((1u << threadIdx.x) - 1u));
+                const int ly = l / K, lx = l - ly * K;
+                s_t4[slot] = static_cast<uint32_t>(target[l]) * 0x01010101u;
+                s_off[slot] = ly * w + lx;
+            }
+            cnt += __popc(m);
+        }
+        if (threadIdx.x == 0) {
+            s_nv = cnt;
+            s_best = kU64Max;
+        }
+    }
+    __syncthreads();
+    const int nv = s_nv, nv4 = nv & ~3;
+    const bool l2 = norm == 0;
+    unsigned long long mine = kU64Max;
+    const uint64_t no = (n + 7) / 8;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t oc = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; oc < no; oc += stride) {
+        const uint64_t i0 = 8 * oc;
+        uint32_t key[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) key[u] = i0 + u < n ? __ldg(dict + i0 + u) : 0xffffffffu;
+        uint32_t acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = 0u;
+        if (i0 + 7 < n && key[7] == key[0] + 7u) {
+            const uint32_t a0 = (key[0] >> 16) * static_cast<uint32_t>(w) + (key[0] & 0xffffu);
+            auto pix8 = [&](int off, uint32_t& lo, uint32_t& hi) {
+                const uint32_t a = a0 + static_cast<uint32_t>(off);
+                const uint32_t* wp = reinterpret_cast<const uint32_t*>(img + (a & ~3u));
+                const uint32_t x0 = __ldg(wp), x1 = __ldg(wp + 1), x2 = __ldg(wp + 2), sh = (a & 3u) * 8u;
+                lo = __funnelshift_r(x0, x1, sh);
+                hi = __funnelshift_r(x1, x2, sh);
+            };
+            for (int v = 0; v < nv4; v += 4) {
+                const uint4 t4 = *reinterpret_cast<const uint4*>(s_t4 + v);
+                const int4 o4 = *reinterpret_cast<const int4*>(s_off + v);
+                uint32_t lo[4], hi[4];
+                pix8(o4.x, lo[0], hi[0]);
+                pix8(o4.y, lo[1], hi[1]);
+                pix8(o4.z, lo[2], hi[2]);
+                pix8(o4.w, lo[3], hi[3]);
+                const uint32_t tv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    lo[u] = __vabsdiffu4(lo[u], tv[u]);
+                    hi[u] = __vabsdiffu4(hi[u], tv[u]);
+                }
+                uint32_t tl[4], th[4];
+                transpose4x4_bytes(lo[0], lo[1], lo[2], lo[3], tl);
+                transpose4x4_bytes(hi[0], hi[1], hi[2], hi[3], th);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc[u] = __dp4a(tl[u], l2 ? tl[u] : 0x01010101u, acc[u]);
+                    acc[4 + u] = __dp4a(th[u], l2 ? th[u] : 0x01010101u, acc[4 + u]);
+                }
+            }
+            for (int v = nv4; v < nv; ++v) {
+                uint32_t lo, hi;
+                pix8(s_off[v], lo, hi);
+                const uint32_t dl = __vabsdiffu4(lo, s_t4[v]), dh = __vabsdiffu4(hi, s_t4[v]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t ml = dl & (0xffu << (8 * u)), mh = dh & (0xffu << (8 * u));
+                    acc[u] = __dp4a(ml, l2 ? dl : 0x01010101u, acc[u]);
+                    acc[4 + u] = __dp4a(mh, l2 ? dh : 0x01010101u, acc[4 + u]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (i0 + u >= n) continue;
+                const uint8_t* base = img + (static_cast<size_t>(key[u] >> 16) * w + (key[u] & 0xffffu));
+                uint32_t a = 0;
+                for (int v = 0; v < nv; ++v) {
+                    const int dd = static_cast<int>(s_t4[v] & 0xffu) - static_cast<int>(__ldg(base + s_off[v]));
+                    a += l2 ? static_cast<uint32_t>(dd * dd) : static_cast<uint32_t>(dd < 0 ? -dd : dd);
+                }
+                acc[u] = a;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (i0 + u < n) {
+                const unsigned long long c = pack_candidate(acc[u], key[u]);
+                mine = c < mine ? c : mine;
+            }
+        }
+    }
+    mine = warp_min(mine);
+    if ((threadIdx.x & 31) == 0) atomicMin(&s_best, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMin(best, s_best);
+}
+
 // exhaustive path for k > kMaxScanK: pack every entry, radix-sort the u64 packed values
 __global__ void __launch_bounds__(256) k_pack_all(views8 V, const qws* ws, int norm, uint32_t* __restrict__ lo,
                                                   uint32_t* __restrict__ hi) {
@@ -2720,7 +2850,12 @@ uint64_t brute_force_scan(zi_ctx* ctx, const uint8_t* d_img, int w, int C, int K
     const size_t smem = ((KK * C + 3) & ~size_t(3)) + KK * C * sizeof(int) + 16;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->num_sms) * 8));
     static const bool scalar = std::getenv("ZI_BRUTE_SCALAR") != nullptr;
-    if (n > 0 && C == 1 && !scalar) {
+    static const bool quad = std::getenv("ZI_BRUTE_QUAD") != nullptr;  // A/B: the 4-entry kernel
+    if (n > 0 && C == 1 && !scalar && !quad) {
+        const unsigned g8 = static_cast<unsigned>(std::min<uint64_t>((n + 2047) / 2048, static_cast<uint64_t>(ctx->num_sms) * 8));
+        ZI_LAUNCH(ctx, "brute_force", k_brute8, g8, 256, ((KK + 3) & ~size_t(3)) * 8 + 16, d_img, w, K, d_dict, n, s.target,
+                  norm, &s.ws->best);
+    } else if (n > 0 && C == 1 && !scalar) {
         const unsigned g4 = static_cast<unsigned>(std::min<uint64_t>((n + 1023) / 1024, static_cast<uint64_t>(ctx->num_sms) * 8));
         ZI_LAUNCH(ctx, "brute_force", k_brute4, g4, 256, KK * 8 + 16, d_img, w, K, d_dict, n, s.target, norm,
                   &s.ws->best);
