@@ -87,9 +87,9 @@ __device__ inline void cp_async16_v(void* dst, const void* src) {
 // Blocked variant: warp w owns a 4x4 block of 8x8 tiles (block (bi, bj), bi <= bj, of the upper
 // triangle), so a k-step loads 4 A and 4 B fragments for 16 MMAs (the per-tile variant loads 2
 // per MMA and is shared-memory bound).  Tiles below the diagonal of a diagonal block are computed
-// but not stored.  One warp per block, up to 16 blocks per CTA.
-constexpr int kGramMaxWarps = 16;
-__global__ void __launch_bounds__(kGramMaxWarps * 32, 1) k_vec_gram_blk(const float* __restrict__ X, uint64_t n, int dim,
+// but not stored.  One warp per block, up to 10 blocks per CTA (two CTAs per SM: the 512 stripes of n = 2^24 then run in under two waves with twice the warps per SM).
+constexpr int kGramMaxWarps = 10;  // 10 = the 4x4-tile blocks of the upper triangle at dim <= 128
+__global__ void __launch_bounds__(kGramMaxWarps * 32, 2) k_vec_gram_blk(const float* __restrict__ X, uint64_t n, int dim,
                                                                         int Pd, const double* __restrict__ mean,
                                                                         int nblocks, double* __restrict__ part) {
     extern __shared__ __align__(16) double s_x[];  // kGramRows x (Pd + 4) fp64, then 2 raw fp32 rounds
