@@ -1002,12 +1002,13 @@ static void finish_hybrid(zi_ctx* ctx, uint32_t** words, uint32_t** orig, int W,
         }
     }
     if (nbig > kMaxBig || static_cast<uint64_t>(hc[1]) * 8 > N) {
-        // top bytes too clustered for the split (smooth images): finish with the full LSD sort.
-        // Equal keys are already in payload order everywhere, so the stable passes from the
-        // current order give the reference permutation.  Later builds with these dims go one
-        // byte deeper, or straight to LSD.
-        learnt = nb + 1 > D - 3 ? -1 : nb + 1;
-        radix_sort_words(ctx, words, nw, N, all, nullptr, false, nullptr, G);
+        // top bytes too clustered for the split (smooth images, or few high-variance PCA dims):
+        // finish with the full LSD sort.  Equal keys are already in payload order everywhere, so
+        // the stable passes from the current order give the reference permutation.  Later builds
+        // with these dims go straight to LSD (one byte deeper rarely splits a clustered top: cfg4
+        // still leaves 10 % / 6 % of the records in oversized segments at 4 / 5 MSD bytes).
+        learnt = -1;
+        radix_sort_words(ctx, words, nw, N, all, nullptr, true, nullptr, G);
         return;
     }
     std::vector<unsigned long long> h(2 * nbig);

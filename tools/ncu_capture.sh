@@ -6,7 +6,7 @@ TAG=${1:-r02}; CFG=${2:-cfg4}
 OUT=gpurun_out
 REP=/tmp/${TAG}_full_${CFG}
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_onesweep|k_proj_tc|k_sort_hist|k_finalize|k_query_lat|k_brute4|k_gram_fused" -c 14 \
+    -k regex:"k_onesweep|k_lsd_count|k_proj_tc|k_finalize|k_query_lat|k_brute8|k_gram_fused" -c 24 \
     -o $REP -f python tools/ncu_driver.py $CFG > $OUT/${TAG}_ncu_full_${CFG}.log 2>&1
 python tools/tools_ncu_summary.py $REP.ncu-rep > $OUT/${TAG}_ncu_full_${CFG}.txt 2>&1
 python tools/ncu_traffic.py $REP.ncu-rep $CFG --out $OUT/${TAG}_traffic_${CFG}.json > /dev/null 2>&1

@@ -12,7 +12,9 @@ import os
 import subprocess
 import sys
 
-NAMES = {"k_onesweep": "radix_onesweep", "k_sort_hist": "radix_hist", "k_proj_tc": None, "k_finalize": "finalize_index",
+NAMES = {"k_onesweep": "radix_onesweep", "k_sort_hist": "radix_hist", "k_lsd_count": "radix_count",
+         "k_lsd_chunk_sum": "radix_scan", "k_lsd_chunk_scan": "radix_scan", "k_lsd_offsets": "radix_scan",
+         "k_brute8": "brute_force", "k_proj_tc": None, "k_finalize": "finalize_index",
          "k_query_lat": "query_one", "k_brute4": "brute_force", "k_brute": "brute_force", "k_segsort": "segment_sort",
          "k_gram_fused": "patch_moments_fused", "k_vec_gram_blk": "vec_gram", "k_vec_project": "vec_project",
          "k_knn_batch": "knn_batch"}
