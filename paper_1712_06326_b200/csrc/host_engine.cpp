@@ -110,11 +110,16 @@ struct grad_cache {
     }
 };
 
-// proj/src/engine.cpp:96-146
+// proj/src/engine.cpp:96-146: priority = confidence term x data term
+double data_term(const mask& m, const grad_cache& gc, int cx, int cy, int K);
 double compute_priority(const raster& img, const mask& m, const std::vector<double>& conf, const grad_cache& gc,
                         int cx, int cy, int K) {
+    (void)img;
+    return confidence_term(m, conf, cx, cy, K) * data_term(m, gc, cx, cy, K);
+}
+
+double data_term(const mask& m, const grad_cache& gc, int cx, int cy, int K) {
     const int r = (K - 1) / 2;
-    const double cterm = confidence_term(m, conf, cx, cy, K);
     double best_sq = -1.0, bgx = 0.0, bgy = 0.0;
     size_t best_i = 0;
     const int y0 = std::max(cy - r, 0), y1 = std::min(cy + r, m.h - 1);
@@ -132,7 +137,6 @@ double compute_priority(const raster& img, const mask& m, const std::vector<doub
         bgx = gc.gx(best_i);
         bgy = gc.gy(best_i);
     }
-    (void)img;
     auto unknown_at = [&](int x, int y) {
         x = std::clamp(x, 0, m.w - 1);
         y = std::clamp(y, 0, m.h - 1);
@@ -146,7 +150,7 @@ double compute_priority(const raster& img, const mask& m, const std::vector<doub
         const double iso_x = -bgy, iso_y = bgx;
         data = std::abs(iso_x * nx / nlen + iso_y * ny / nlen) / 255.0 + kPriorityEpsilon;
     }
-    return cterm * data;
+    return data;
 }
 
 struct by_priority {
@@ -169,33 +173,42 @@ public:
             for (int x = 0; x < m.w; ++x)
                 if (is_fillfront_pixel(m_, x, y)) add(x, y);
     }
-    bool empty() const { return queue_.empty(); }
-    void next_target(int& x, int& y) const {
-        const uint32_t pos = queue_.begin()->second;
+    bool empty() {
+        prune();
+        return heap_.empty();
+    }
+    void next_target(int& x, int& y) {
+        prune();
+        const uint32_t pos = heap_.front().second;
         x = static_cast<int>(pos % m_.w);
         y = static_cast<int>(pos / m_.w);
     }
-    // paste (engine.cpp:238-257) + membership / priority refresh (engine.cpp:307-330)
-    int apply_paste(int cx, int cy, uint32_t src, double* center_conf) {
+    // paste (engine.cpp:238-257) + membership / priority refresh (engine.cpp:307-330), in two
+    // halves so that the first can run while the device answers the query:
+    //  prepare_paste: everything that does not depend on the source patch -- the center's
+    //    pre-paste confidence, the filled pixels' known flags and confidences, the new fill-front
+    //    membership of the zone, and the confidence terms of the zone's front pixels;
+    //  finish_paste: the pasted values, the gradient cache, the data terms, the queue updates.
+    // Priorities only read the post-paste state, and the queue's final content does not depend
+    // on the order of its updates, so the result equals the one-step paste.
+    void prepare_paste(int cx, int cy) {
         const int r = (K_ - 1) / 2;
-        const double cc = confidence_term(m_, conf_, cx, cy, K_);
-        const int sx = static_cast<int>(src & 0xffffu), sy = static_cast<int>(src >> 16);
-        int filled = 0;
+        pcx_ = cx;
+        pcy_ = cy;
+        pcc_ = confidence_term(m_, conf_, cx, cy, K_);
+        filled_.clear();
         for (int dy = 0; dy < K_; ++dy) {
             const int y = cy - r + dy;
             for (int dx = 0; dx < K_; ++dx) {
                 const int x = cx - r + dx;
                 if (!m_.in_bounds(x, y) || m_.is_known(x, y)) continue;
-                const uint8_t* s = img_.at(sx + dx, sy + dy);
-                uint8_t* d = img_.at(x, y);
-                for (int c = 0; c < img_.C; ++c) d[c] = s[c];
+                filled_.push_back(static_cast<uint32_t>(dy * K_ + dx));
                 m_.known[m_.idx(x, y)] = 1;
-                conf_[m_.idx(x, y)] = cc;
-                gc_.set_pixel(img_, m_, x, y);
-                ++filled;
+                conf_[m_.idx(x, y)] = pcc_;
             }
         }
-        if (filled) gc_.refresh(m_, cx - r - 1, cy - r - 1, cx + r + 1, cy + r + 1);
+        acts_.clear();
+        if (filled_.empty()) return;
         const int refresh = K_ - 1;
         for (int y = cy - refresh; y <= cy + refresh; ++y) {
             if (y < 0 || y >= m_.h) continue;
@@ -204,13 +217,43 @@ public:
                 const size_t i = m_.idx(x, y);
                 const bool zone = std::abs(x - cx) <= r + 1 && std::abs(y - cy) <= r + 1;
                 const bool now = zone ? is_fillfront_pixel(m_, x, y) : in_front_[i] != 0;
-                if (in_front_[i] && !now) remove(x, y);
-                else if (!in_front_[i] && now) add(x, y);
-                else if (in_front_[i] && now) refresh_one(x, y);
+                if (in_front_[i] && !now) acts_.push_back({static_cast<uint32_t>(i), 0, 0.0});
+                else if (now) acts_.push_back({static_cast<uint32_t>(i), in_front_[i] ? 2 : 1, confidence_term(m_, conf_, x, y, K_)});
             }
         }
-        *center_conf = cc;
-        return filled;
+    }
+    int finish_paste(uint32_t src, double* center_conf) {
+        const int r = (K_ - 1) / 2, cx = pcx_, cy = pcy_;
+        const int sx = static_cast<int>(src & 0xffffu), sy = static_cast<int>(src >> 16);
+        for (const uint32_t l : filled_) {
+            const int dy = static_cast<int>(l) / K_, dx = static_cast<int>(l) % K_;
+            const int x = cx - r + dx, y = cy - r + dy;
+            const uint8_t* sp = img_.at(sx + dx, sy + dy);
+            uint8_t* d = img_.at(x, y);
+            for (int c = 0; c < img_.C; ++c) d[c] = sp[c];
+            gc_.set_pixel(img_, m_, x, y);
+        }
+        *center_conf = pcc_;
+        if (filled_.empty()) return 0;
+        gc_.refresh(m_, cx - r - 1, cy - r - 1, cx + r + 1, cy + r + 1);
+        for (const act& a : acts_) {
+            const int x = static_cast<int>(a.i % static_cast<uint32_t>(m_.w)), y = static_cast<int>(a.i / static_cast<uint32_t>(m_.w));
+            if (a.kind == 0) {
+                remove(x, y);
+                continue;
+            }
+            const double fresh = a.cterm * data_term(m_, gc_, x, y, K_);
+            if (a.kind == 1) {
+                cached_[a.i] = fresh;
+                in_front_[a.i] = 1;
+                ++live_;
+                push(fresh, a.i);
+            } else if (fresh != cached_[a.i]) {
+                cached_[a.i] = fresh;
+                push(fresh, a.i);
+            }
+        }
+        return static_cast<int>(filled_.size());
     }
 
 private:
@@ -218,20 +261,20 @@ private:
         const size_t i = m_.idx(x, y);
         cached_[i] = compute_priority(img_, m_, conf_, gc_, x, y, K_);
         in_front_[i] = 1;
-        queue_.emplace(cached_[i], static_cast<uint32_t>(i));
+        ++live_;
+        push(cached_[i], static_cast<uint32_t>(i));
     }
     void remove(int x, int y) {
         const size_t i = m_.idx(x, y);
-        queue_.erase({cached_[i], static_cast<uint32_t>(i)});
-        in_front_[i] = 0;
+        in_front_[i] = 0;  // its heap entries go stale
+        --live_;
     }
     void refresh_one(int x, int y) {
         const size_t i = m_.idx(x, y);
         const double fresh = compute_priority(img_, m_, conf_, gc_, x, y, K_);
         if (fresh != cached_[i]) {
-            queue_.erase({cached_[i], static_cast<uint32_t>(i)});
             cached_[i] = fresh;
-            queue_.emplace(fresh, static_cast<uint32_t>(i));
+            push(fresh, static_cast<uint32_t>(i));
         }
     }
     raster& img_;
@@ -239,8 +282,49 @@ private:
     int K_;
     std::vector<double> conf_, cached_;
     std::vector<uint8_t> in_front_;
-    std::set<std::pair<double, uint32_t>, by_priority> queue_;
+    // The fill front ordered as the reference's std::set<(priority, pixel)> with by_priority
+    // (priority desc, pixel index asc; engine.cpp:283-306): a binary heap under the same strict
+    // order with lazy deletion -- an entry is live iff its pixel is on the front with exactly
+    // that cached priority.  The set's begin() is then the heap's first live entry (keys are
+    // unique: one pixel, one cached priority), without a node allocation per update.
+    std::vector<std::pair<double, uint32_t>> heap_;
+    size_t live_ = 0;
+    static bool heap_less(const std::pair<double, uint32_t>& a, const std::pair<double, uint32_t>& b) {
+        return by_priority{}(b, a);  // std heaps keep the largest under `less` first
+    }
+    bool live(const std::pair<double, uint32_t>& e) const { return in_front_[e.second] && cached_[e.second] == e.first; }
+    void push(double p, uint32_t i) {
+        heap_.emplace_back(p, i);
+        std::push_heap(heap_.begin(), heap_.end(), heap_less);
+        if (heap_.size() > 64 && heap_.size() > 8 * front_size()) compact();
+    }
+    size_t front_size() const { return live_; }
+    void prune() {
+        while (!heap_.empty() && !live(heap_.front())) {
+            std::pop_heap(heap_.begin(), heap_.end(), heap_less);
+            heap_.pop_back();
+        }
+    }
+    void compact() {  // drop stale entries (and duplicates of a live key) and re-heapify
+        std::vector<std::pair<double, uint32_t>> keep;
+        keep.reserve(live_ + 16);
+        for (const auto& e : heap_)
+            if (live(e)) keep.push_back(e);
+        std::sort(keep.begin(), keep.end());
+        keep.erase(std::unique(keep.begin(), keep.end()), keep.end());
+        heap_.swap(keep);
+        std::make_heap(heap_.begin(), heap_.end(), heap_less);
+    }
     grad_cache gc_;
+    struct act {
+        uint32_t i;
+        int kind;      // 0 leaves the front, 1 joins it, 2 stays (priority refreshed)
+        double cterm;  // post-paste confidence term (kinds 1, 2)
+    };
+    int pcx_ = 0, pcy_ = 0;
+    double pcc_ = 0.0;
+    std::vector<uint32_t> filled_;
+    std::vector<act> acts_;
 };
 
 // extract_patch_clamped (proj/src/image.cpp:7-47)
@@ -303,6 +387,11 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
         int tx, ty;
         drv.next_target(tx, ty);
         extract_clamped(img, m, tx, ty, K, tv, tk);
+        bool prepared = false;
+        const std::function<void()> prepare = [&] {
+            drv.prepare_paste(tx, ty);
+            prepared = true;
+        };
         zi_iteration_record rec{};
         rec.iteration = it;
         rec.target_x = tx;
@@ -314,7 +403,7 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
             rec.layout_id = 0;
             rec.candidates = mi->n;
         } else {
-            const query_result q = query_best_patch(mi, tv.data(), tk.data(), k, cfg.norm, nullptr);
+            const query_result q = query_best_patch(mi, tv.data(), tk.data(), k, cfg.norm, nullptr, &prepare);
             best = q.best;
             rec.layout_id = q.lid;
             rec.candidates = q.count;
@@ -343,7 +432,8 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
         const auto tp0 = std::chrono::steady_clock::now();
         t_query += std::chrono::duration<double>(tp0 - tq0).count();
         double cc;
-        unknown_left -= static_cast<uint64_t>(drv.apply_paste(tx, ty, rec.source_key, &cc));
+        if (!prepared) prepare();  // brute-force runs (and the oracle scan) take no callback
+        unknown_left -= static_cast<uint64_t>(drv.finish_paste(rec.source_key, &cc));
         t_paste += std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count();
         stats->confidence_low = std::min(stats->confidence_low, cc);
         stats->confidence_high = std::max(stats->confidence_high, cc);

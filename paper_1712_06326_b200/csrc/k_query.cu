@@ -2608,8 +2608,19 @@ static bool fused_query(zi_multi_index* mi, const query_scratch& s, const mi_vie
 }
 
 query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, uint32_t k, int norm,
-                              uint64_t* knn_out) {
+                              uint64_t* knn_out, const std::function<void()>* while_waiting) {
     zi_ctx* ctx = mi->ctx;
+    bool waited = false;  // while_waiting runs exactly once, during the device work when possible
+    auto run_waiting = [&] {
+        if (while_waiting && !waited) {
+            waited = true;
+            (*while_waiting)();
+        }
+    };
+    struct waiting_guard {  // every other path: run it before returning
+        std::function<void()> f;
+        ~waiting_guard() { f(); }
+    } wg{[&] { run_waiting(); }};
     k = std::max<uint32_t>(k, 1);
     ensure_smem_attr(ctx);
     const size_t KK = static_cast<size_t>(mi->K) * mi->K;
@@ -2718,6 +2729,7 @@ query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uin
                              sv, sc, slast_v, slast_c);
             }
         } else {
+            run_waiting();
             unsigned spins = 0;
             while (hr->seq != seq) {
                 if ((++spins & 1023u) == 0) {

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "zinpaint_b200.h"
@@ -323,8 +324,10 @@ struct query_result {
 };
 // full query_best_patch on the device for the target staged at d_target (K*K*C values then K*K
 // flags); knn list optionally copied out.
+// while_waiting (optional): host work run once while the device answers (the fill loop's
+// result-independent part of the paste)
 query_result query_best_patch(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk,
-                              uint32_t k, int norm, uint64_t* knn_out);
+                              uint32_t k, int norm, uint64_t* knn_out, const std::function<void()>* while_waiting = nullptr);
 uint64_t brute_force_best(zi_multi_index* mi, const uint8_t* h_tv, const uint8_t* h_tk, int norm);
 // the exhaustive scan over any device image + dictionary (brute_force_best with the reference's
 // (image, target, dictionary, norm) arguments, engine.hpp:98-99)
