@@ -175,6 +175,14 @@ zi_status zi_dictionary_collect(zi_ctx* ctx, const uint8_t* known, int32_t width
 zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t* known,
                                int32_t width, int32_t height, int32_t channels,
                                const zi_index_config* cfg, zi_multi_index** out);
+/* multi_index::build with the dictionary returned in the same call: keys_out (keys_cap entries,
+ * pinned host memory for the copy to overlap) receives the n dictionary keys while the indices
+ * are built -- the image upload and the dictionary download run on the copy engines alongside
+ * the build's kernels.  Synchronous: keys_out is filled and the indices are ready on return. */
+zi_status zi_multi_index_build_to(zi_ctx* ctx, const uint8_t* image, const uint8_t* known,
+                                  int32_t width, int32_t height, int32_t channels,
+                                  const zi_index_config* cfg, uint32_t* keys_out, uint64_t keys_cap,
+                                  uint64_t* n_out, zi_multi_index** out);
 /* rebuild from the device-resident image/mask (bench: inputs already in HBM) */
 zi_status zi_multi_index_rebuild(zi_multi_index* mi);
 zi_status zi_multi_index_destroy(zi_multi_index* mi);

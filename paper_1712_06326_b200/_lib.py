@@ -100,6 +100,8 @@ SIGNATURES = {
     "zi_dictionary_collect": (C.c_int, [vp, u8p, C.c_int32, C.c_int32, C.c_int32, u32p, C.c_uint64, u64p]),
     "zi_multi_index_build": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig),
                                        C.POINTER(vp)]),
+    "zi_multi_index_build_to": (C.c_int, [vp, u8p, u8p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(IndexConfig),
+                                          u32p, C.c_uint64, u64p, C.POINTER(vp)]),
     "zi_multi_index_rebuild": (C.c_int, [vp]),
     "zi_vector_index_build": (C.c_int, [vp, f32p, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(vp)]),
     "zi_vector_index_build_device": (C.c_int, [vp, vp, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(vp)]),

@@ -148,16 +148,32 @@ static void upload_layouts(zi_multi_index* mi) {
     ZI_CUDA(cudaMemcpyAsync(mi->layout_local.p, loc.data(), loc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, mi->ctx->stream));
 }
 
+static void ensure_copy_stream(zi_ctx* ctx) {
+    if (ctx->copy_stream) return;
+    ZI_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ctx->ev_alloc, &ctx->ev_img, &ctx->ev_dict, &ctx->ev_copy})
+        ZI_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
 static void upload_image(zi_multi_index* mi, const uint8_t* image, const uint8_t* known) {
     const size_t npx = static_cast<size_t>(mi->w) * mi->h;
+    zi_ctx* ctx = mi->ctx;
     mi->image.ensure(npx * mi->C + 16);  // +16: aligned word loads past the last byte (k_proj_tc gather)
     mi->known.ensure(npx);
-    ZI_CUDA(cudaMemcpyAsync(mi->image.p, image, npx * mi->C, cudaMemcpyHostToDevice, mi->ctx->stream));
-    ZI_CUDA(cudaMemcpyAsync(mi->known.p, known, npx, cudaMemcpyHostToDevice, mi->ctx->stream));
+    ZI_CUDA(cudaMemcpyAsync(mi->known.p, known, npx, cudaMemcpyHostToDevice, ctx->stream));
+    if (mi->image_on_copy) {  // the mask is all the dictionary needs: the image follows on the copy engine
+        ensure_copy_stream(ctx);
+        ZI_CUDA(cudaEventRecord(ctx->ev_alloc, ctx->stream));  // after the (stream-ordered) allocation
+        ZI_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_alloc, 0));
+        ZI_CUDA(cudaMemcpyAsync(mi->image.p, image, npx * mi->C, cudaMemcpyHostToDevice, ctx->copy_stream));
+        ZI_CUDA(cudaEventRecord(ctx->ev_img, ctx->copy_stream));
+    } else {
+        ZI_CUDA(cudaMemcpyAsync(mi->image.p, image, npx * mi->C, cudaMemcpyHostToDevice, ctx->stream));
+    }
 }
 
 static zi_multi_index* new_multi_index(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h,
-                                       int32_t C, const zi_index_config* cfg) {
+                                       int32_t C, const zi_index_config* cfg, bool image_on_copy = false) {
     require(ctx && image && known && cfg, "null argument");
     require(w > 0 && h > 0 && (C == 1 || C == 3), "raster_image: bad dimensions");
     require(w <= 65535 && h <= 65535, "image side above the 16-bit patch_key range");
@@ -170,6 +186,7 @@ static zi_multi_index* new_multi_index(zi_ctx* ctx, const uint8_t* image, const 
     mi->h = h;
     mi->C = C;
     mi->K = cfg->patch_size;
+    mi->image_on_copy = image_on_copy;
     try {
         upload_layouts(mi);
         upload_image(mi, image, known);
@@ -221,6 +238,11 @@ zi_status zi_ctx_destroy(zi_ctx* ctx) {
             }
         cudaEventDestroy(ctx->t0);
         cudaEventDestroy(ctx->t1);
+        if (ctx->copy_stream) {
+            cudaStreamSynchronize(ctx->copy_stream);
+            for (cudaEvent_t e : {ctx->ev_alloc, ctx->ev_img, ctx->ev_dict, ctx->ev_copy}) cudaEventDestroy(e);
+            cudaStreamDestroy(ctx->copy_stream);
+        }
         ctx->scratch.release();  // stream-ordered frees before the stream goes away
         ctx->ss_buf.release();
         ctx->counter.release();
@@ -527,6 +549,29 @@ zi_status zi_multi_index_build(zi_ctx* ctx, const uint8_t* image, const uint8_t*
             delete mi;
             throw;
         }
+        *out = mi;
+    });
+}
+
+zi_status zi_multi_index_build_to(zi_ctx* ctx, const uint8_t* image, const uint8_t* known, int32_t w, int32_t h,
+                                  int32_t C, const zi_index_config* cfg, uint32_t* keys_out, uint64_t keys_cap,
+                                  uint64_t* n_out, zi_multi_index** out) {
+    return guard(ctx, [&] {
+        require(out != nullptr && keys_out != nullptr && n_out != nullptr, "null argument");
+        zi_multi_index* mi = new_multi_index(ctx, image, known, w, h, C, cfg, true);
+        try {
+            mi->dict_out = keys_out;
+            mi->dict_cap = keys_cap;
+            zi::build_multi_index(mi);
+            ZI_CUDA(cudaStreamSynchronize(ctx->stream));  // the kernels and (ev_copy) the dictionary copy
+            mi->dict_out = nullptr;
+            mi->image_on_copy = false;
+        } catch (...) {
+            cudaStreamSynchronize(ctx->copy_stream);  // no copy may still target the caller's buffers
+            delete mi;
+            throw;
+        }
+        *n_out = mi->n;
         *out = mi;
     });
 }

@@ -165,6 +165,14 @@ void build_multi_index(zi_multi_index* mi) {
     mi->n = collect_dictionary(ctx, mi->known.p, w, h, K, mi->dict);
     if (mi->n == 0) throw error(ZI_E_EMPTY_DICT, "no fully known patch window; inpainting impossible");
     const uint64_t n = mi->n;
+    if (mi->dict_out) {  // zi_multi_index_build_to: the dictionary goes home while the build runs
+        if (n > mi->dict_cap) throw error(ZI_E_INVALID, "build_to: dictionary larger than the output buffer");
+        ZI_CUDA(cudaEventRecord(ctx->ev_dict, ctx->stream));
+        ZI_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_dict, 0));
+        ZI_CUDA(cudaMemcpyAsync(mi->dict_out, mi->dict.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->copy_stream));
+        ZI_CUDA(cudaEventRecord(ctx->ev_copy, ctx->copy_stream));
+    }
+    if (mi->image_on_copy) ZI_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_img, 0));  // the moments read it
     mi->dims = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(mi->cfg.dims),
                                                    std::min<uint64_t>(static_cast<uint64_t>(mi->mc), n)));
     const int D = mi->dims, mc = mi->mc, m = mi->m;
@@ -205,6 +213,7 @@ void build_multi_index(zi_multi_index* mi) {
         mi->L[l].index.layout_id = static_cast<uint32_t>(l);
         finalize_index(ctx, sorted[0], sorted[W], N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p, &mi->L[l].index);
     }
+    if (mi->dict_out) ZI_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
     ZI_CUDA(cudaEventRecord(mi->ev1, ctx->stream));
     mi->build_ms_pending = true;
     mi->host_lohi = false;

@@ -129,6 +129,10 @@ struct zi_ctx {
     int flush_toggle = 1;
     zi::dbuf<int2> gm_wtab;      // fused moments: gather word table
     zi::dbuf<uint32_t> ss_buf;   // splitter sort: output records, samples, splitters, histograms
+    // copy stream of zi_multi_index_build_to: the image upload and the dictionary download run
+    // on the copy engines while the build's kernels run (created on first use)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_alloc = nullptr, ev_img = nullptr, ev_dict = nullptr, ev_copy = nullptr;
 };
 
 // One z-curve-sorted index, device resident.
@@ -195,6 +199,11 @@ struct zi_multi_index {
     // dictionary rows in dict (every rank keeps the whole dictionary: payload rows are global)
     bool shard = false;
     uint64_t row_begin = 0, n_total = 0;
+    // zi_multi_index_build_to: the image arrives on ctx->copy_stream (ev_img), and the dictionary
+    // goes to dict_out on it as soon as it is collected (ev_copy)
+    bool image_on_copy = false;
+    uint32_t* dict_out = nullptr;
+    uint64_t dict_cap = 0;
     zi_layout_state L[8];
 };
 

@@ -159,6 +159,43 @@ def test_dictionary_collect(zb, golden):
             assert np.array_equal(mi.dictionary, mi_dict), (tag, K)
 
 
+def test_build_to_overlapped_copies_equal_build(zb, golden):
+    """zi_multi_index_build_to (image upload and dictionary download on the copy stream beside the
+    build) returns the dictionary and builds the same 8 indices as zi_multi_index_build."""
+    import ctypes as C
+    from paper_1712_06326_b200 import _lib
+    L = _lib.lib()
+    for tag, img, kn in _images(golden)[:3]:
+        cfg = zb.index_config(patch_size=9, dims=6)
+        ref = zb.MultiIndex(img, kn, cfg)
+        h_, w_ = kn.shape
+        ch = 1 if img.ndim == 2 else img.shape[2]
+        cap = (w_ - 8) * (h_ - 8)
+        keys = np.zeros(cap, np.uint32)
+        n = C.c_uint64(0)
+        hmi = C.c_void_p()
+        _lib.check(L.zi_multi_index_build_to(ref.ctx.h, _lib.ptr(np.ascontiguousarray(img), _lib.u8p),
+                                             _lib.ptr(np.ascontiguousarray(kn), _lib.u8p), w_, h_, ch, C.byref(cfg),
+                                             _lib.ptr(keys, _lib.u32p), cap, C.byref(n), C.byref(hmi)))
+        try:
+            assert n.value == ref.n, tag
+            assert np.array_equal(keys[:n.value], ref.dictionary), tag
+            for l in range(8):
+                c = np.zeros((ref.n, ref.dims), np.uint8)
+                k = np.zeros(ref.n, np.uint32)
+                _lib.check(L.zi_multi_index_layout_index(hmi, l, _lib.ptr(c, _lib.u8p), _lib.ptr(k, _lib.u32p)))
+                rc, rk = ref.index_arrays(l)
+                assert np.array_equal(c, rc) and np.array_equal(k, rk), (tag, l)
+        finally:
+            _lib.check(L.zi_multi_index_destroy(hmi))
+        small = np.zeros(max(1, ref.n - 1), np.uint32)
+        with pytest.raises(ValueError):  # ZI_E_INVALID: the dictionary does not fit
+            _lib.check(L.zi_multi_index_build_to(ref.ctx.h, _lib.ptr(np.ascontiguousarray(img), _lib.u8p),
+                                                 _lib.ptr(np.ascontiguousarray(kn), _lib.u8p), w_, h_, ch,
+                                                 C.byref(cfg), _lib.ptr(small, _lib.u32p), small.size, C.byref(n),
+                                                 C.byref(hmi)))
+
+
 def test_empty_dictionary_raises(zb):
     img = np.zeros((20, 20), np.uint8)
     with pytest.raises(zb.EmptyDictionaryError):
