@@ -34,10 +34,16 @@ namespace zi {
 
 constexpr int kPtRows = 128;
 constexpr int kPtGatherWarps = 4;                // warps 0-3: one thread per patch row
-constexpr int kPtEpiWarps = 12;                  // warps 4-15: TMEM lane quarter (w & 3), layouts li = (w >> 2) mod 3
-constexpr int kPtEpiSets = kPtEpiWarps / 4;
-constexpr int kPtMmaWarp = kPtGatherWarps + kPtEpiWarps;
-constexpr int kPtThreads = (kPtMmaWarp + 1) * 32;
+// epilogue warps 4 .. 4 + 4S - 1: TMEM lane quarter (w & 3), layouts li = (w >> 2) mod S.  S = 4 sets
+// for D <= 10 (a group's layouts spread one per set); S = 3 above, where the larger per-layout
+// register state would spill at the 80 registers a 21-warp CTA leaves per thread
+template <int D>
+struct pt_shape {
+    static constexpr int kEpiSets = D <= 10 ? 4 : 3;
+    static constexpr int kEpiWarps = 4 * kEpiSets;
+    static constexpr int kMmaWarp = kPtGatherWarps + kEpiWarps;
+    static constexpr int kThreads = (kMmaWarp + 1) * 32;
+};
 constexpr int kPtMaxFpad = 384;
 constexpr int kPtMaxN = 256;
 // t = rint(c * 2^38) in five balanced base-256 digits.  (Four digits put all 8 layouts of a D = 8
@@ -192,7 +198,9 @@ __device__ __forceinline__ void pt_gather_static(const uint8_t* __restrict__ img
 }
 
 template <int D, int MODE, int KT>
-__global__ void __launch_bounds__(kPtThreads, 1) k_proj_tc(const __grid_constant__ pt_params P) {
+__global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __grid_constant__ pt_params P) {
+    constexpr int kPtEpiSets = pt_shape<D>::kEpiSets, kPtEpiWarps = pt_shape<D>::kEpiWarps;
+    constexpr int kPtMmaWarp = pt_shape<D>::kMmaWarp, kPtThreads = pt_shape<D>::kThreads;
     constexpr int W = (D + 3) / 4;
     extern __shared__ uint8_t pt_raw[];
     uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(pt_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -824,8 +832,8 @@ static void launch_pt_kt(zi_ctx* ctx, const pt_params& P, int mode, size_t smem)
     if (mode == 0) smem_attr(ctx->device, k_proj_tc<D, 0, KT>, 200 * 1024);
     else smem_attr(ctx->device, k_proj_tc<D, 1, KT>, 200 * 1024);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(P.ntiles, static_cast<uint64_t>(ctx->num_sms)));
-    if (mode == 0) ZI_LAUNCH(ctx, "project_tc_minmax", (k_proj_tc<D, 0, KT>), grid, kPtThreads, smem, P);
-    else ZI_LAUNCH(ctx, "project_tc_quantize", (k_proj_tc<D, 1, KT>), grid, kPtThreads, smem, P);
+    if (mode == 0) ZI_LAUNCH(ctx, "project_tc_minmax", (k_proj_tc<D, 0, KT>), grid, pt_shape<D>::kThreads, smem, P);
+    else ZI_LAUNCH(ctx, "project_tc_quantize", (k_proj_tc<D, 1, KT>), grid, pt_shape<D>::kThreads, smem, P);
 }
 
 // patch shapes with a static gather: (9, 1) -> 1 (cfg1, cfg4), (11, 3) -> 2 (cfg2); for the dims
@@ -861,8 +869,11 @@ static pt_plan pt_make_plan(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, u
     const uint64_t n = mi->n, ntot = mi->shard ? mi->n_total : mi->n;
     if (off_env || D < 1 || D > 16 || Fpad > kPtMaxFpad || mc > 232 || ntot == 0 || ntot >= (1ull << 27)) return pl;
     pl.D = D;
+    // as few 256-column groups as fit, with the layouts spread evenly over them (D = 8: 4 + 4, not
+    // 6 + 2 -- the small group's launch costs as much gather as the big one's)
     pl.nlmax = std::min(8, kPtMaxN / (kPtDigits * D));
     pl.ng = (8 + pl.nlmax - 1) / pl.nlmax;
+    pl.nlmax = (8 + pl.ng - 1) / pl.ng;
     for (int g = 0; g < pl.ng; ++g) {
         const int nl = std::min(pl.nlmax, 8 - g * pl.nlmax);
         pl.gnpad[g] = (nl * kPtDigits * D + 15) / 16 * 16;
