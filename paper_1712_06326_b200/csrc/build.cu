@@ -196,7 +196,13 @@ void build_multi_index(zi_multi_index* mi) {
     recs.ensure(static_cast<size_t>(W + 1) * N);
     uint32_t* keyw = recs.p;
     uint32_t* val = recs.p + static_cast<size_t>(W) * N;
+    // a sort that goes straight to LSD passes writes the indices in its last pass; its records
+    // then carry the patch key as payload (same tie order as the row: the dictionary is ascending)
+    static const bool no_fuse = std::getenv("ZI_SORT_NO_FUSE") != nullptr;  // A/B: separate finalize
+    bool fuse = !no_fuse && layouts_sort_fuses(ctx, D);
+    mi->payload_key = fuse;
     if (!project_quantize_tc(mi, keyw, val, N)) {
+        mi->payload_key = fuse = false;  // the fp64 fallback writes (layout << 29) | row
         for (int l = 0; l < 8; ++l) {
             unsigned long long* mm = mi->minmax.p + static_cast<size_t>(l) * 2 * D;
             mi->proj.ensure(static_cast<size_t>(D) * n);
@@ -207,11 +213,27 @@ void build_multi_index(zi_multi_index* mi) {
         }
     }
     uint32_t* sorted[10];  // the sorted records, possibly in the sort's scratch (no copy back)
-    morton_sort_records(ctx, keyw, val, n, 8, D, true, sorted);
+    // when the sort ends in an LSD pass, that pass writes the indices' planes and keys itself
+    final_sink sink{};
     for (int l = 0; l < 8; ++l) {
-        mi->L[l].index.ctx = ctx;
-        mi->L[l].index.layout_id = static_cast<uint32_t>(l);
-        finalize_index(ctx, sorted[0], sorted[W], N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p, &mi->L[l].index);
+        zi_index* idx = &mi->L[l].index;
+        idx->ctx = ctx;
+        idx->layout_id = static_cast<uint32_t>(l);
+        prepare_index(idx, n, D);
+        sink.planes[l] = idx->planes.p;
+        sink.keys[l] = idx->keys.p;
+    }
+    sink.dict = nullptr;  // the payload is the key
+    const bool fused = morton_sort_records(ctx, keyw, val, n, 8, D, true, sorted, true, fuse ? &sink : nullptr);
+    if (fuse != fused) throw error(ZI_E_RUNTIME, "build: the layout sort did not take its fused path");
+    mi->payload_key = false;
+    if (fused) {
+        zi_index* idx[8];
+        for (int l = 0; l < 8; ++l) idx[l] = &mi->L[l].index;
+        finalize_index_bboxes(ctx, idx, 8);
+    } else {
+        for (int l = 0; l < 8; ++l)
+            finalize_index(ctx, sorted[0], sorted[W], N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p, &mi->L[l].index);
     }
     if (mi->dict_out) ZI_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
     ZI_CUDA(cudaEventRecord(mi->ev1, ctx->stream));

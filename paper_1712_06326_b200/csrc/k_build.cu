@@ -493,47 +493,6 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const uint8_t* __restr
     }
 }
 
-// Morton de-interleave by 8x8 bit-matrix transposes, no tables (a lookup per key byte and plane
-// word was 12% slower in finalize; the quantiser keeps its spread table, which measured faster).  Key bit L*D + D-1-d
-// is bit L of dim d (proj/include/zinpaint/morton.hpp:14-29); dims go in chunks of 8: chunk c
-// holds dims 8c..8c+7, and its level-L byte (bit 7-r = bit L of dim 8c+r) sits at key bit
-// L*D + D-8-8c (a negative offset drops the bits of dims >= D, which are zero).
-__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {  // byte i bit j <-> byte j bit i
-    x = (x & 0xAA55AA55AA55AA55ull) | ((x & 0x00AA00AA00AA00AAull) << 7) | ((x >> 7) & 0x00AA00AA00AA00AAull);
-    x = (x & 0xCCCC3333CCCC3333ull) | ((x & 0x0000CCCC0000CCCCull) << 14) | ((x >> 14) & 0x0000CCCC0000CCCCull);
-    x = (x & 0xF0F0F0F00F0F0F0Full) | ((x & 0x00000000F0F0F0F0ull) << 28) | ((x >> 28) & 0x00000000F0F0F0F0ull);
-    return x;
-}
-
-template <int D>
-__device__ __forceinline__ void morton_deinterleave8(const uint32_t (&kw)[(D + 3) / 4], uint32_t (&pw)[(D + 3) / 4]) {
-    constexpr int W = (D + 3) / 4;
-#pragma unroll
-    for (int k = 0; k < W; ++k) pw[k] = 0;
-#pragma unroll
-    for (int c = 0; c < (D + 7) / 8; ++c) {
-        uint64_t m = 0;
-#pragma unroll
-        for (int L = 0; L < 8; ++L) {
-            const int sh = D - 8 - 8 * c;
-            const int pos = L * D + (sh >= 0 ? sh : 0);
-            const int nb = sh >= 0 ? 8 : 8 + sh;  // bits of this level byte present in the key
-            const int wd = pos >> 5, off = pos & 31;
-            uint32_t v = kw[wd] >> off;
-            if (off + nb > 32 && wd + 1 < W) v |= kw[wd + 1] << (32 - off);
-            v &= (1u << nb) - 1u;
-            if (sh < 0) v <<= -sh;
-            m |= static_cast<uint64_t>(v) << (8 * L);
-        }
-        m = transpose8x8(m);
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int d = 8 * c + r;
-            if (d < D) pw[d >> 2] |= (static_cast<uint32_t>(m >> (8 * (7 - r))) & 0xffu) << (8 * (d & 3));
-        }
-    }
-}
-
 // quantise (proj/src/builder.cpp:55-61) and interleave to the 8*D-bit Morton key
 // (proj/include/zinpaint/morton.hpp:14-29): bit L of dim d -> key bit L*D + D-1-d.
 // Records of all 8 layouts share one array of N = 8n entries (layout-major); word k of entry
@@ -757,8 +716,7 @@ void interleave_coords(zi_ctx* ctx, const uint8_t* d_coords, const uint32_t* d_k
     ZI_LAUNCH(ctx, "interleave_coords", k_interleave, grid, 256, 0, d_coords, d_keys_in, n, D, d_keyw, d_val);
 }
 
-void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t off, uint64_t n,
-                    int D, const uint32_t* d_dict, zi_index* idx) {
+void prepare_index(zi_index* idx, uint64_t n, int D) {
     idx->n = n;
     idx->dims = static_cast<uint32_t>(D);
     idx->planes_n = static_cast<uint32_t>((D + 3) / 4);
@@ -767,6 +725,11 @@ void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, 
     idx->keys.ensure(n ? n : 1);
     idx->bbox_min.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
     idx->bbox_max.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
+}
+
+void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t off, uint64_t n,
+                    int D, const uint32_t* d_dict, zi_index* idx) {
+    prepare_index(idx, n, D);
     if (n == 0) return;
     ZI_DIMS_SWITCH(D, launch_finalize_t, ctx, d_keyw, d_val, N, off, n, d_dict, idx);
 }

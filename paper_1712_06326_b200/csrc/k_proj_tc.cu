@@ -60,6 +60,7 @@ struct pt_params {
     const uint32_t* keys;
     uint64_t n;
     uint32_t row_base;
+    int payload_key;   // records carry the patch key as payload (the fused final sort pass), not (l << 29) | row
     const uint8_t* B;  // this group's digit matrix, pre-swizzled (Npad x Fpad)
     int Npad, l0, nl;
     const double* M;          // [8][D]
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __gr
                         const uint64_t e = static_cast<uint64_t>(l) * P.n + row;
 #pragma unroll
                         for (int k = 0; k < W; ++k) P.keyw[static_cast<size_t>(k) * P.Nrec + e] = kw[k];
-                        P.val[e] = (l << 29) | (P.row_base + static_cast<uint32_t>(row));
+                        P.val[e] = P.payload_key ? __ldg(P.keys + row) : (l << 29) | (P.row_base + static_cast<uint32_t>(row));
                     }
                     flag = flag || cand;
                     const uint32_t m = __ballot_sync(0xffffffffu, valid && flag);
@@ -754,7 +755,7 @@ __global__ void __launch_bounds__(kPtxWarps * 32) k_pt_exact(const uint8_t* __re
                                                              const uint32_t* __restrict__ list_count,
                                                              unsigned long long* __restrict__ minmax,
                                                              uint32_t* __restrict__ keyw, uint32_t* __restrict__ val,
-                                                             uint64_t Nrec) {
+                                                             uint64_t Nrec, int payload_key) {
     constexpr int W = (D + 3) / 4;
     __shared__ double s_xc[kPtxWarps][232];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -807,7 +808,7 @@ __global__ void __launch_bounds__(kPtxWarps * 32) k_pt_exact(const uint8_t* __re
                 const uint32_t word = __reduce_or_sync(0xffffffffu, part);
                 if (lane == 0) keyw[static_cast<size_t>(k) * Nrec + er] = word;
             }
-            if (lane == 0) val[er] = (l << 29) | (row_base + row);
+            if (lane == 0) val[er] = payload_key ? key : (l << 29) | (row_base + row);
         }
     }
 }
@@ -820,11 +821,11 @@ static void launch_pt_exact(zi_ctx* ctx, zi_multi_index* mi, const pt_params& P,
     if (mode == 0)
         ZI_LAUNCH(ctx, "project_tc_exact_minmax", (k_pt_exact<D, 0>), grid, kPtxWarps * 32, 0, mi->image.p, mi->w, mi->C, keys, mi->n,
                   rb, mi->layout_off.p, mi->m, mi->pca_mean.p, mi->pca_comp.p, P.list, P.list_count, mi->minmax.p, P.keyw,
-                  P.val, P.Nrec);
+                  P.val, P.Nrec, P.payload_key);
     else
         ZI_LAUNCH(ctx, "project_tc_fixup", (k_pt_exact<D, 1>), grid, kPtxWarps * 32, 0, mi->image.p, mi->w, mi->C, keys, mi->n, rb,
                   mi->layout_off.p, mi->m, mi->pca_mean.p, mi->pca_comp.p, P.list, P.list_count, mi->minmax.p, P.keyw,
-                  P.val, P.Nrec);
+                  P.val, P.Nrec, P.payload_key);
 }
 
 template <int D, int KT>
@@ -900,6 +901,7 @@ static pt_plan pt_make_plan(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, u
     P.keys = mi->dict.p + mi->row_begin;
     P.n = n;
     P.row_base = static_cast<uint32_t>(mi->row_begin);
+    P.payload_key = mi->payload_key ? 1 : 0;
     P.M = reinterpret_cast<const double*>(s + pl.o_M);
     P.amm = reinterpret_cast<unsigned long long*>(s + pl.o_amm);
     P.E = 255.0 * mc * (0.5 * kPtUnit + 0x1p-44);

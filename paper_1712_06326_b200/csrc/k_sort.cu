@@ -145,10 +145,14 @@ __device__ __forceinline__ uint32_t lookback(const uint32_t* st, uint32_t tile, 
 // All record indices are 32-bit (N < 2^30); the word pointers are offset once per tile.  A
 // thread keeps IT records in registers plus one (digit << 16 | warp rank) word per record; the
 // records are staged in shared memory in tile-sorted order, then written as runs per digit.
-template <int NW, int IT, int MODE>
+// MODE 1 with DF > 0 (the sort's last pass over the 8-layout records, D = DF): the records are not
+// written back but straight into the layout indices -- dim planes (de-interleaved Morton key) and
+// the dictionary key of the payload row -- at their final positions (finalize without its read).
+template <int NW, int IT, int MODE, int DF = 0>
 __global__ void __launch_bounds__(kSortThreads, NW * IT <= 24 ? 4 : NW * IT <= 36 ? 3 : 2)
     k_onesweep(sort_words io, int dw, int ds, const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
-               uint32_t* __restrict__ tile_ctr, const uint32_t* __restrict__ offs, uint32_t gn, uint32_t tpg) {
+               uint32_t* __restrict__ tile_ctr, const uint32_t* __restrict__ offs, uint32_t gn, uint32_t tpg,
+               const __grid_constant__ final_sink sink) {
     constexpr int TILE = kSortThreads * IT;
     extern __shared__ uint32_t s_stage[];  // NW * TILE
     __shared__ uint32_t s_hist[kSortWarps][256];
@@ -261,17 +265,84 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 24 ? 4 : NW * IT <= 3
         }
     }
     __syncthreads();
-    uint32_t* dst[NW];
-#pragma unroll
-    for (int k = 0; k < NW; ++k) dst[k] = io.out[k];
     const uint32_t* sdig = s_stage + dw * TILE;
+    if constexpr (DF > 0) {
+        constexpr int W = NW - 1;
+        static_assert((DF + 3) / 4 == W, "final pass: record width and dims disagree");
+        uint32_t* pl = sink.planes[grp];
+        uint32_t* ky = sink.keys[grp];
+        const uint32_t g0 = grp * gn;
+#pragma unroll 4
+        for (int i = 0; i < IT; ++i) {
+            const uint32_t j = static_cast<uint32_t>(tid + i * kSortThreads);
+            if (j < cnt) {
+                const uint32_t loc = s_delta[(sdig[j] >> ds) & 0xffu] + j - g0;
+                uint32_t kw[W], pw[W];
 #pragma unroll
-    for (int i = 0; i < IT; ++i) {
-        const uint32_t j = static_cast<uint32_t>(tid + i * kSortThreads);
-        if (j < cnt) {
-            const uint32_t o = s_delta[(sdig[j] >> ds) & 0xffu] + j;
+                for (int k = 0; k < W; ++k) kw[k] = s_stage[k * TILE + j];
+                morton_deinterleave8<DF>(kw, pw);
 #pragma unroll
-            for (int k = 0; k < NW; ++k) dst[k][o] = s_stage[k * TILE + j];
+                for (int p = 0; p < W; ++p) pl[static_cast<size_t>(p) * gn + loc] = pw[p];
+                const uint32_t pay = s_stage[W * TILE + j];
+                ky[loc] = sink.dict ? __ldg(sink.dict + (pay & ((1u << 29) - 1u))) : pay;  // null dict: payload = key
+            }
+        }
+    } else {
+        uint32_t* dst[NW];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) dst[k] = io.out[k];
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {
+            const uint32_t j = static_cast<uint32_t>(tid + i * kSortThreads);
+            if (j < cnt) {
+                const uint32_t o = s_delta[(sdig[j] >> ds) & 0xffu] + j;
+#pragma unroll
+                for (int k = 0; k < NW; ++k) dst[k][o] = s_stage[k * TILE + j];
+            }
+        }
+    }
+}
+
+// per-256-entry bounding boxes of the layout indices' dim planes (the fused last pass leaves them
+// out): one warp per (layout, block), every plane's eight loads per lane in flight together
+struct bbox_job {
+    const uint32_t* planes[8];
+    uint32_t* bmin[8];
+    uint32_t* bmax[8];
+};
+template <int P>
+__global__ void __launch_bounds__(256) k_index_bbox(const __grid_constant__ bbox_job J, uint64_t n, uint64_t nblk,
+                                                    int nidx) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (wid >= nblk * static_cast<uint64_t>(nidx)) return;
+    const int l = static_cast<int>(wid / nblk);
+    const uint64_t blk = wid - static_cast<uint64_t>(l) * nblk;
+    uint32_t v[P][8];
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint64_t i = blk * 256 + e * 32 + lane;
+            v[p][e] = i < n ? __ldg(J.planes[l] + static_cast<size_t>(p) * n + i) : 0u;
+        }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (blk * 256 + e * 32 + lane < n) {
+                mn = __vminu4(mn, v[p][e]);
+                mx = __vmaxu4(mx, v[p][e]);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = __vminu4(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = __vmaxu4(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            J.bmin[l][static_cast<size_t>(p) * nblk + blk] = mn;
+            J.bmax[l][static_cast<size_t>(p) * nblk + blk] = mx;
         }
     }
 }
@@ -400,13 +471,15 @@ struct pass_plan {
 };
 
 template <int NW>
-static void launch_pass(zi_ctx* ctx, const sort_words& io, int dw, int ds, const pass_plan& pp, int G) {
+static void launch_pass(zi_ctx* ctx, const sort_words& io, int dw, int ds, const pass_plan& pp, int G,
+                        const final_sink* sink = nullptr) {
     constexpr int IT = os_items<NW>();
     const size_t smem = static_cast<size_t>(NW) * kSortThreads * IT * sizeof(uint32_t);
     if (lookback_mode()) {
         smem_attr(ctx->device, k_onesweep<NW, IT, 0>, smem);
         ZI_LAUNCH(ctx, "radix_onesweep", (k_onesweep<NW, IT, 0>), pp.ntiles, kSortThreads, smem, io, dw, ds, pp.digit_base,
-                  pp.status, pp.ctr, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t>(pp.gn), pp.tpg);
+                  pp.status, pp.ctr, static_cast<const uint32_t*>(nullptr), static_cast<uint32_t>(pp.gn), pp.tpg,
+                  final_sink{});
         return;
     }
     const uint32_t gn = static_cast<uint32_t>(pp.gn);
@@ -415,10 +488,20 @@ static void launch_pass(zi_ctx* ctx, const sort_words& io, int dw, int ds, const
     ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_sum, nch, 256, 0, pp.counts, pp.tpg, pp.cpg, pp.csum);
     ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_scan, static_cast<unsigned>(G), 256, 0, pp.csum, pp.cpg, gn);
     ZI_LAUNCH(ctx, "radix_scan", k_lsd_offsets, nch, 256, 0, pp.counts, pp.csum, pp.tpg, pp.cpg);
+    if (sink) {  // the last pass of the 8-layout sort: straight into the indices
+        constexpr int DF = NW == 2 ? 4 : NW == 3 ? 8 : NW == 4 ? 12 : 16;
+        if constexpr (NW >= 2 && NW <= 5) {
+            smem_attr(ctx->device, k_onesweep<NW, IT, 1, DF>, smem);
+            ZI_LAUNCH(ctx, "radix_onesweep", (k_onesweep<NW, IT, 1, DF>), pp.ntiles, kSortThreads, smem, io, dw, ds,
+                      static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                      static_cast<uint32_t*>(nullptr), static_cast<const uint32_t*>(pp.counts), gn, pp.tpg, *sink);
+            return;
+        }
+    }
     smem_attr(ctx->device, k_onesweep<NW, IT, 1>, smem);
     ZI_LAUNCH(ctx, "radix_onesweep", (k_onesweep<NW, IT, 1>), pp.ntiles, kSortThreads, smem, io, dw, ds,
               static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-              static_cast<const uint32_t*>(pp.counts), gn, pp.tpg);
+              static_cast<const uint32_t*>(pp.counts), gn, pp.tpg, final_sink{});
 }
 
 // Generic stable LSD sort of NW-word SoA records; passes are (word, shift) digits from the
@@ -454,7 +537,8 @@ static bool groups_fit(int npass, int G) { return npass <= 40 && G <= 8; }
 // odd number of passes -- instead of copying them back into `words`.  device_bases: every pass
 // runs, nothing goes through the host (the histograms are only needed to skip trivial passes).
 void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const std::vector<int2>& passes,
-                      const uint32_t* hist_host, bool device_bases, uint32_t** result, int G) {
+                      const uint32_t* hist_host, bool device_bases, uint32_t** result, int G,
+                      const final_sink* sink = nullptr) {
     if (result)
         for (int k = 0; k < nw; ++k) result[k] = words[k];
     if (n <= 1 || passes.empty()) return;
@@ -564,11 +648,12 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
             pq.digit_base = bases + static_cast<size_t>(q) * G * 256;
         }
         const int dw = passes[q].x, ds = passes[q].y;
+        const final_sink* sk = a + 1 == active.size() ? sink : nullptr;  // (the look-back mode takes no sink)
         switch (nw) {
-            case 2: launch_pass<2>(ctx, io, dw, ds, pq, G); break;
-            case 3: launch_pass<3>(ctx, io, dw, ds, pq, G); break;
-            case 4: launch_pass<4>(ctx, io, dw, ds, pq, G); break;
-            case 5: launch_pass<5>(ctx, io, dw, ds, pq, G); break;
+            case 2: launch_pass<2>(ctx, io, dw, ds, pq, G, sk); break;
+            case 3: launch_pass<3>(ctx, io, dw, ds, pq, G, sk); break;
+            case 4: launch_pass<4>(ctx, io, dw, ds, pq, G, sk); break;
+            case 5: launch_pass<5>(ctx, io, dw, ds, pq, G, sk); break;
             case 6: launch_pass<6>(ctx, io, dw, ds, pq, G); break;
             case 7: launch_pass<7>(ctx, io, dw, ds, pq, G); break;
             case 8: launch_pass<8>(ctx, io, dw, ds, pq, G); break;
@@ -1055,8 +1140,16 @@ static void verify_sorted(zi_ctx* ctx, uint32_t* const* words, int W, uint64_t N
 // result (optional, see radix_sort_words): the buffers holding the sorted records
 // G > 1 (layouts): the records are G equal layout groups, group-major -- every global pass sorts
 // the groups on their own, so no pass on the layout digit is needed
-static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts,
-                               uint32_t** result = nullptr, int G = 1) {
+static bool fusable_dims(int D) { return D % 4 == 0 && D <= 16 && !lookback_mode(); }
+
+// true when the 8-layout build sort of these dims goes straight to device LSD passes (an earlier
+// build found its top bytes too clustered for the MSD split): its last pass can take a sink
+bool layouts_sort_fuses(zi_ctx* ctx, int D) {
+    return ctx->sort_depth[D][1] < 0 && msd_bytes_forced() <= 0 && fusable_dims(D);
+}
+
+static bool morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N, int D, bool layouts,
+                               uint32_t** result = nullptr, int G = 1, const final_sink* sink = nullptr) {
     const int nw = W + 1;
     uint32_t* cur[kMaxWords];
     auto done = [&] {  // hand the final buffers to the caller, or move them into `words`
@@ -1085,14 +1178,17 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, all_full, G, learnt);
         if (verify_on()) verify_sorted(ctx, cur, W, N, D, nb, layouts);
         done();
-        return;
+        return false;
     }
     if (learnt < 0 && msd_bytes_forced() <= 0) {
         // an earlier build with these dims found the top bytes too clustered for the MSD split:
-        // the plain LSD sort, every pass on the device (no histogram round trip)
-        radix_sort_words(ctx, words, nw, N, all, nullptr, true, cur, G);
+        // the plain LSD sort, every pass on the device (no histogram round trip); with a sink the
+        // last pass writes the layout indices themselves
+        const bool fused = sink && G == 8 && fusable_dims(D);
+        radix_sort_words(ctx, words, nw, N, all, nullptr, true, cur, G, fused ? sink : nullptr);
+        if (fused) return true;
         done();
-        return;
+        return false;
     }
     const std::vector<uint32_t> hist = pass_histograms(ctx, words, nw, N, all, G);  // [pass][group][256]
     // MSD depth: the fewest top bytes whose (marginal) entropies predict segments of <= 16
@@ -1126,7 +1222,7 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
         if (debug) std::fprintf(stderr, "hybrid sort N=%llu: MSD depth %d of %d -> LSD\n", static_cast<unsigned long long>(N), nb, D);
         radix_sort_words(ctx, words, nw, N, all, hist.data(), false, cur, G);
         done();
-        return;
+        return false;
     }
     std::vector<int2> msd;
     std::vector<uint32_t> msd_hist;
@@ -1144,6 +1240,7 @@ static void morton_sort_hybrid(zi_ctx* ctx, uint32_t** words, int W, uint64_t N,
     finish_hybrid(ctx, cur, words, W, N, D, nb, layouts, all, all_full, G, learnt);
     if (verify_on()) verify_sorted(ctx, cur, W, N, D, nb, layouts);
     done();
+    return false;
 }
 
 void morton_sort(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int D, bool payload_first) {
@@ -1166,8 +1263,8 @@ void morton_sort_rows(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n
     morton_sort_hybrid(ctx, words, W, n, D, false);
 }
 
-void morton_sort_records(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int G, int D,
-                         bool group_in_payload, uint32_t** out, bool payload_ascending) {
+bool morton_sort_records(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int G, int D,
+                         bool group_in_payload, uint32_t** out, bool payload_ascending, const final_sink* sink) {
     const int W = (D + 3) / 4;
     const uint64_t N = static_cast<uint64_t>(G) * n;
     static const bool splitter = [] {
@@ -1179,25 +1276,46 @@ void morton_sort_records(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_
         for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * N;
         words[W] = d_val;
         sample_sort_groups(ctx, words, W + 1, n, G, D, group_in_payload, out);
-        return;
+        return false;
     }
     if (G > 1) {  // layout groups sorted on their own: no layout-digit pass
         uint32_t* words[kMaxWords];
         for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * N;
         words[W] = d_val;
-        morton_sort_hybrid(ctx, words, W, N, D, group_in_payload, out, G);
-        return;
+        return morton_sort_hybrid(ctx, words, W, N, D, group_in_payload, out, G, sink);
     }
     if (payload_ascending) {  // hybrid MSD + window sort, stable: payload order ties
         uint32_t* words[kMaxWords];
         for (int k = 0; k < W; ++k) words[k] = d_keyw + static_cast<size_t>(k) * n;
         words[W] = d_val;
         morton_sort_hybrid(ctx, words, W, n, D, false, out);
-        return;
+        return false;
     }
     morton_sort(ctx, d_keyw, d_val, n, D, true);  // payload passes first: any input order
     for (int k = 0; k < W; ++k) out[k] = d_keyw + static_cast<size_t>(k) * n;
     out[W] = d_val;
+    return false;
+}
+
+void finalize_index_bboxes(zi_ctx* ctx, zi_index* const* idx, int nidx) {
+    if (nidx <= 0 || idx[0]->n == 0) return;
+    bbox_job J{};
+    for (int l = 0; l < nidx; ++l) {
+        J.planes[l] = idx[l]->planes.p;
+        J.bmin[l] = idx[l]->bbox_min.p;
+        J.bmax[l] = idx[l]->bbox_max.p;
+    }
+    const uint64_t nblk = idx[0]->nblk;
+    const unsigned grid = static_cast<unsigned>((nblk * nidx + 7) / 8);
+    switch (idx[0]->planes_n) {
+#define ZI_BBOX_CASE(PP)                                                                                        \
+    case PP:                                                                                                    \
+        ZI_LAUNCH(ctx, "finalize_index", k_index_bbox<PP>, grid, 256, 0, J, idx[0]->n, nblk, nidx);             \
+        break;
+        ZI_BBOX_CASE(1) ZI_BBOX_CASE(2) ZI_BBOX_CASE(3) ZI_BBOX_CASE(4)
+#undef ZI_BBOX_CASE
+        default: throw error(ZI_E_INVALID, "index bboxes: more than 16 dims");
+    }
 }
 
 void morton_sort_layouts(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t N, int D, uint32_t** out) {

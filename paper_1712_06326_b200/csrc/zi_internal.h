@@ -204,6 +204,9 @@ struct zi_multi_index {
     bool image_on_copy = false;
     uint32_t* dict_out = nullptr;
     uint64_t dict_cap = 0;
+    // build records carry the patch key as payload (instead of (layout << 29) | row): set when the
+    // sort's fused last pass writes the indices (no dictionary gather there)
+    bool payload_key = false;
     zi_layout_state L[8];
 };
 
@@ -296,8 +299,22 @@ void sample_sort_groups(zi_ctx* ctx, uint32_t* const* words, int nw, uint64_t n,
 // the build's sort: G groups (layouts) of n records, group-major; out[k] = word k of the sorted
 // records (stride G*n), payload at out[W].  Onesweep LSD / hybrid sorts (k_sort.cu); ZI_SORT=splitter
 // selects the experimental two-level splitter sort (k_ssort.cu) when the payload is ascending.
-void morton_sort_records(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int G, int D,
-                         bool group_in_payload, uint32_t** out, bool payload_ascending = true);
+// sink (optional, G = 8 layout groups, D a multiple of 4 up to 16): when the sort ends in an LSD
+// pass, that pass writes the layout indices' dim planes and keys instead of records; the return
+// value tells whether it did (the caller then only adds the bboxes, finalize_index_bboxes)
+struct final_sink {
+    uint32_t* planes[8];   // per group (layout): [P][n] plane words
+    uint32_t* keys[8];     // per group: [n] patch keys
+    const uint32_t* dict;  // payload row -> patch key
+};
+bool morton_sort_records(zi_ctx* ctx, uint32_t* d_keyw, uint32_t* d_val, uint64_t n, int G, int D,
+                         bool group_in_payload, uint32_t** out, bool payload_ascending = true,
+                         const final_sink* sink = nullptr);
+bool layouts_sort_fuses(zi_ctx* ctx, int D);  // the 8-layout sort will write the indices itself
+// the index buffers finalize_index fills (the fused sort's last pass writes planes and keys)
+void prepare_index(zi_index* idx, uint64_t n, int D);
+// the per-256-entry bboxes of nidx (<= 8) equally sized indices whose planes are written
+void finalize_index_bboxes(zi_ctx* ctx, zi_index* const* idx, int nidx);
 // all 8 layouts at once: N = 8n records, Morton passes then one pass on the layout bits of the
 // payload ((layout << 29) | row) -- stable, so each layout segment ends in reference order
 // out (optional): the buffers holding the sorted words (out[k] = out[0] + k*N, the payload at
