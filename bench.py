@@ -243,8 +243,11 @@ class ClockSampler:
 # ---------------------------------------------------------------------------- roofline model
 def pt_groups(D: int):
     """Layout groups of the int8 tensor-core projection (k_proj_tc.cu): five digit columns per
-    (layout, dim), at most 256 MMA columns per group, padded to a multiple of 16."""
+    (layout, dim), at most 256 MMA columns per group (padded to a multiple of 16), the layouts
+    spread evenly over the fewest groups."""
     nlmax = min(8, 256 // (5 * D))
+    ng = (8 + nlmax - 1) // nlmax
+    nlmax = (8 + ng - 1) // ng
     out, l0 = [], 0
     while l0 < 8:
         nl = min(nlmax, 8 - l0)
@@ -268,6 +271,8 @@ def algorithmic_bytes(kernel: str, n: int, D: int, mc: int, F: int = 0) -> float
         "ssort_scatter": 2 * 4 * (W + 1) * N,           # records read + written to their buckets
         "ssort_local": 2 * 4 * (W + 1) * N,             # every bucket read + written back in order
         "radix_hist": 4 * (W + 1) * N,
+        "radix_count": 4 * N,                           # the digit word of every record (tile counts: ~0.3 %)
+        "index_bbox": 4 * W * N,                        # fused final pass: the 8 indices' dim planes read once
         "proj_minmax": 8 * D * n,
         "quantize_interleave": (8 * D + 4 + 4 * (W + 1)) * n,
         "finalize_index": (4 * (W + 1) + 4 * (W + 1)) * n,

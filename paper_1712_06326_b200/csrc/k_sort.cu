@@ -1310,7 +1310,7 @@ void finalize_index_bboxes(zi_ctx* ctx, zi_index* const* idx, int nidx) {
     switch (idx[0]->planes_n) {
 #define ZI_BBOX_CASE(PP)                                                                                        \
     case PP:                                                                                                    \
-        ZI_LAUNCH(ctx, "finalize_index", k_index_bbox<PP>, grid, 256, 0, J, idx[0]->n, nblk, nidx);             \
+        ZI_LAUNCH(ctx, "index_bbox", k_index_bbox<PP>, grid, 256, 0, J, idx[0]->n, nblk, nidx);                 \
         break;
         ZI_BBOX_CASE(1) ZI_BBOX_CASE(2) ZI_BBOX_CASE(3) ZI_BBOX_CASE(4)
 #undef ZI_BBOX_CASE
