@@ -37,6 +37,13 @@ constexpr int kPtGatherWarps = 4;                // warps 0-3: one thread per pa
 // epilogue warps 4 .. 4 + 4S - 1: TMEM lane quarter (w & 3), layouts li = (w >> 2) mod S.  S = 4 sets
 // for D <= 10 (a group's layouts spread one per set); S = 3 above, where the larger per-layout
 // register state would spill at the 80 registers a 21-warp CTA leaves per thread
+// the min / max pass keeps running per-thread extremes when every epilogue warp set has exactly one
+// layout of the group (the host's plan for D = 7..10: two groups of four layouts, four sets)
+template <int D>
+__host__ __device__ constexpr bool pt_running() {
+    return D >= 7 && D <= 10;
+}
+
 template <int D>
 struct pt_shape {
     static constexpr int kEpiSets = D <= 10 ? 4 : 3;
@@ -338,6 +345,86 @@ __global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __gr
             __syncwarp();
             if (lane == 0) tc_mbar_arrive(tc_smem(&s_afull[buf]));
         }
+    } else if (MODE == 0 && pt_running<D>()) {
+        // min / max pass, one layout per warp set: every thread keeps running int64 minima and
+        // maxima of T for its layout over all its rows, so a tile costs two compares per dim
+        // instead of four warp reductions; TMEM is read in two halves of the dims (registers)
+        const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;
+        constexpr int DH = (D + 1) / 2;
+        long long rmn[D], rmx[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            rmn[d] = LLONG_MAX;
+            rmx[d] = LLONG_MIN;
+        }
+        for (uint64_t j = 0; j < nloc; ++j) {
+            const int buf = static_cast<int>(j & 1);
+            tc_mbar_wait(tc_smem(&s_accfull[buf]), static_cast<uint32_t>(j >> 1) & 1);
+            tc_fence_after();
+            const uint64_t tile = blockIdx.x + j * gridDim.x;
+            const bool valid = tile * kPtRows + q4 * 32 + lane < P.n;
+            const uint32_t ta = tmem + static_cast<uint32_t>(buf * 256) + (static_cast<uint32_t>(q4 * 32) << 16) +
+                                static_cast<uint32_t>(lpar * kPtDigits * D);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                constexpr int NH = kPtDigits * DH;
+                const int d0 = h * DH, nd = h ? D - DH : DH;
+                uint32_t v[NH];
+                if (lpar < nl) {
+#pragma unroll
+                    for (int c = 0; c + 4 <= NH; c += 4) {
+                        uint32_t t4[4];
+                        tc_ld_x4(ta + static_cast<uint32_t>(kPtDigits * d0 + c), t4);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) v[c + u] = t4[u];
+                    }
+#pragma unroll
+                    for (int c = NH & ~3; c < NH; ++c) tc_ld_x1(ta + static_cast<uint32_t>(kPtDigits * d0 + c), v[c]);
+                    tc_ld_wait();
+                }
+                if (h == 1) {  // this buffer is read: release it to the MMA warp
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
+                }
+                if (lpar < nl && valid) {
+#pragma unroll
+                    for (int dd = 0; dd < DH; ++dd) {
+                        if (dd < nd) {
+                            const uint32_t* vd = v + kPtDigits * dd;
+                            const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
+                                                (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
+                                                (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
+                                                (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
+                                                static_cast<long long>(static_cast<int>(vd[0]));
+                            rmn[d0 + dd] = T < rmn[d0 + dd] ? T : rmn[d0 + dd];
+                            rmx[d0 + dd] = T > rmx[d0 + dd] ? T : rmx[d0 + dd];
+                        }
+                    }
+                }
+            }
+        }
+        if (lpar < nl) {  // warp reductions, then one ordered atomic per (layout, dim) and warp
+            const int l = P.l0 + lpar;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int mh = __reduce_min_sync(0xffffffffu, static_cast<int>(rmn[d] >> 32));
+                const uint32_t ml = __reduce_min_sync(0xffffffffu, static_cast<int>(rmn[d] >> 32) == mh
+                                                                       ? static_cast<uint32_t>(rmn[d]) : 0xffffffffu);
+                const int xh = __reduce_max_sync(0xffffffffu, static_cast<int>(rmx[d] >> 32));
+                const uint32_t xl = __reduce_max_sync(0xffffffffu, static_cast<int>(rmx[d] >> 32) == xh
+                                                                       ? static_cast<uint32_t>(rmx[d]) : 0u);
+                const long long wmn = (static_cast<long long>(mh) << 32) | ml;
+                const long long wmx = (static_cast<long long>(xh) << 32) | xl;
+                if (lane == 0 && wmn <= wmx) {  // the warp saw a valid row
+                    const double M = s_M[lpar][d];
+                    atomicMin(P.amm + static_cast<size_t>(l) * 2 * D + d,
+                              double_to_ordered(__dsub_rn(static_cast<double>(wmn) * kPtUnit, M)));
+                    atomicMax(P.amm + static_cast<size_t>(l) * 2 * D + D + d,
+                              double_to_ordered(__dsub_rn(static_cast<double>(wmx) * kPtUnit, M)));
+                }
+            }
+        }
     } else {  // epilogue: TMEM lane quarter ew & 3, layouts of parity ew >> 2, one patch row per thread
         const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;  // lpar in [0, kPtEpiSets)
         for (uint64_t j = 0; j < nloc; ++j) {
@@ -452,7 +539,7 @@ __global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __gr
             }
         }
     }
-    if (MODE == 0 && warp >= kPtGatherWarps && warp < kPtMmaWarp) {
+    if (MODE == 0 && !pt_running<D>() && warp >= kPtGatherWarps && warp < kPtMmaWarp) {
         const int lpar = (warp - kPtGatherWarps) >> 2;
         const int li = kPtEpiSets * (lane / D) + lpar, d = lane % D;
         if (li < nl && tmn0 <= tmx0) {  // the slot saw a valid row: y' of the extreme T (one rounding, as in the epilogue)
