@@ -220,6 +220,8 @@ __global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __gr
     __shared__ double s_M[8][D];
     // quantise constants per (layout, dim): {za, zb} {bz, tlo} {thi, -} as two-word vectors (16 B loads)
     __shared__ __align__(16) double2 s_qc[8][D][3];
+    // fp32 pre-filter of the quantise pass per (layout, dim): {za * 2^20, zb, bz + eps, 1 - bz - eps}
+    __shared__ __align__(16) float4 s_qf[8][D];
     // Morton spread table, four copies 8 banks apart (lane group g = lane >> 3 reads copy g)
     constexpr int kSpStride = 256 * W + 8;
     __shared__ uint32_t s_spread[4 * kSpStride];
@@ -269,6 +271,15 @@ __global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __gr
                 s_qc[li][d][0] = make_double2(za, zb);
                 s_qc[li][d][1] = make_double2(bz, __longlong_as_double(tlo));
                 s_qc[li][d][2] = make_double2(__longlong_as_double(thi), 0.0);
+                // z32 = fmaf(float(T >> 20), za * 2^20, zb) is within eps of z': the dropped low 20
+                // bits of T (2^20 za), and five fp32 roundings of terms below |T za| + |zb| + 256,
+                // where |T za| = 255 |y' + M| / R is bounded through the approximate range (a row
+                // outside it is a lo / hi candidate, which the exact path also sees); doubled
+                const double tza = degen ? 0.0 : 255.0 * fmax(fabs(lo + M), fabs(hi + M)) / R;
+                const double eps = 2.0 * (0x1p20 * za + 0x1p-22 * (2.0 * tza + fabs(zb) + 256.0)) + 1e-9;
+                s_qf[li][d] = degen ? make_float4(0.f, 0.f, 2.f, -1.f)  // never decided in fp32
+                                    : make_float4(static_cast<float>(za * 0x1p20), static_cast<float>(zb),
+                                                  static_cast<float>(bz + eps), static_cast<float>(1.0 - bz - eps));
             }
         }
         if (MODE == 1 && tid < 256) {
@@ -493,19 +504,31 @@ __global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __gr
                     } else {
                         // degenerate ranges (amax - amin <= 4E) carry bz = 1 and tlo = LLONG_MAX:
                         // every row is flagged and a lo / hi candidate, with no branch here
-                        const double2 c0 = s_qc[li][d][0], c1 = s_qc[li][d][1];
+                        const double2 c1 = s_qc[li][d][1];
                         const double thi = s_qc[li][d][2].x;
-                        const double zf = __fma_rn(__ll2double_rn(T), c0.x, c0.y);
-                        // floor(zf) through the 2^52 rounding trick (no conversion): the nearest
-                        // integer to zf - 1/2; a tie only happens at an integer zf, which the
-                        // boundary test below flags anyway
-                        const double tq = __dadd_rn(zf, 4503599627370495.5);  // zf - 0.5 + 2^52
-                        const double qf = __dsub_rn(tq, 4503599627370496.0);
-                        const double fr = zf - qf;
-                        const double bz = c1.x;
-                        flag = flag || (fr < bz) || (fr > 1.0 - bz);
                         cand = cand || (T <= __double_as_longlong(c1.y)) || (T >= __double_as_longlong(thi));
-                        const int qi = static_cast<int>(static_cast<uint32_t>(__double_as_longlong(tq)));
+                        // fp32 first: when z32's fraction keeps eps + bz off both integers, floor(z32)
+                        // is floor(z') and the fp64 test below could not flag (|z32 - z'| <= eps)
+                        const float4 qf32 = s_qf[li][d];
+                        const float z32 = __fmaf_rn(static_cast<float>(static_cast<int>(T >> 20)), qf32.x, qf32.y);
+                        const float fl32 = floorf(z32);
+                        const float fr32 = z32 - fl32;
+                        int qi;
+                        if (fr32 >= qf32.z && fr32 <= qf32.w) {
+                            qi = static_cast<int>(fl32);
+                        } else {
+                            const double2 c0 = s_qc[li][d][0];
+                            const double zf = __fma_rn(__ll2double_rn(T), c0.x, c0.y);
+                            // floor(zf) through the 2^52 rounding trick (no conversion): the nearest
+                            // integer to zf - 1/2; a tie only happens at an integer zf, which the
+                            // boundary test below flags anyway
+                            const double tq = __dadd_rn(zf, 4503599627370495.5);  // zf - 0.5 + 2^52
+                            const double qf = __dsub_rn(tq, 4503599627370496.0);
+                            const double fr = zf - qf;
+                            const double bz = c1.x;
+                            flag = flag || (fr < bz) || (fr > 1.0 - bz);
+                            qi = static_cast<int>(static_cast<uint32_t>(__double_as_longlong(tq)));
+                        }
                         const uint32_t q = static_cast<uint32_t>(min(max(qi, 0), 255));
                         const int sh = D - 1 - d;
                         uint32_t prev = 0;
