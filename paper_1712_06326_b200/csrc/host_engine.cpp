@@ -17,6 +17,7 @@
 #include <limits>
 #include <set>
 #include <utility>
+#include <thread>
 #include <vector>
 
 #include "zi_internal.h"
@@ -25,6 +26,23 @@ namespace zi {
 namespace {
 
 constexpr double kPriorityEpsilon = 1e-3;
+
+// rows [0, h) split over the host's cores (the fill loop's one-time setup: pure per-pixel work,
+// so the results do not depend on the split)
+template <typename F>
+void parallel_rows(int h, F&& f) {
+    const int nt = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    if (nt == 1 || h < 256) {
+        f(0, h);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+        const int y0 = static_cast<int>(static_cast<int64_t>(h) * t / nt), y1 = static_cast<int>(static_cast<int64_t>(h) * (t + 1) / nt);
+        th.emplace_back([&f, y0, y1] { f(y0, y1); });
+    }
+    for (auto& t : th) t.join();
+}
 
 struct raster {
     int w, h, C;
@@ -82,9 +100,11 @@ struct grad_cache {
         w = m.w;
         inten.assign(static_cast<size_t>(m.w) * m.h, 0.0);
         sq.assign(static_cast<size_t>(m.w) * m.h, -2.0);
-        for (int y = 0; y < m.h; ++y)
-            for (int x = 0; x < m.w; ++x) inten[m.idx(x, y)] = channel_mean(img.at(x, y), img.C);
-        refresh(m, 0, 0, m.w - 1, m.h - 1);
+        parallel_rows(m.h, [&](int y0, int y1) {
+            for (int y = y0; y < y1; ++y)
+                for (int x = 0; x < m.w; ++x) inten[m.idx(x, y)] = channel_mean(img.at(x, y), img.C);
+        });
+        parallel_rows(m.h, [&](int y0, int y1) { refresh(m, 0, y0, m.w - 1, y1 - 1); });
     }
     void set_pixel(const raster& img, const mask& m, int x, int y) { inten[m.idx(x, y)] = channel_mean(img.at(x, y), img.C); }
     double gx(size_t i) const { return (inten[i + 1] - inten[i - 1]) / 2.0; }
@@ -169,9 +189,21 @@ public:
           cached_(static_cast<size_t>(m.w) * m.h, 0.0), in_front_(static_cast<size_t>(m.w) * m.h, 0) {
         for (size_t i = 0; i < conf_.size(); ++i) conf_[i] = m.known[i] ? 1.0 : 0.0;
         gc_.init(img_, m_);
-        for (int y = 0; y < m.h; ++y)
-            for (int x = 0; x < m.w; ++x)
-                if (is_fillfront_pixel(m_, x, y)) add(x, y);
+        // the initial front's priorities in parallel, then the queue in pixel order
+        parallel_rows(m.h, [&](int y0, int y1) {
+            for (int y = y0; y < y1; ++y)
+                for (int x = 0; x < m.w; ++x)
+                    if (is_fillfront_pixel(m_, x, y)) {
+                        const size_t i = m_.idx(x, y);
+                        cached_[i] = compute_priority(img_, m_, conf_, gc_, x, y, K_);
+                        in_front_[i] = 1;
+                    }
+        });
+        for (size_t i = 0; i < in_front_.size(); ++i)
+            if (in_front_[i]) {
+                ++live_;
+                push(cached_[i], static_cast<uint32_t>(i));
+            }
     }
     bool empty() {
         prune();
@@ -380,13 +412,14 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
     fill_driver drv(img, m, K);
     std::vector<uint8_t> tv(static_cast<size_t>(K) * K * mi->C), tk(static_cast<size_t>(K) * K);
     const uint32_t k = static_cast<uint32_t>(std::max(cfg.knn, 1));
-    double t_query = 0.0, t_paste = 0.0;
+    double t_query = 0.0, t_paste = 0.0, t_select = 0.0;
     while (unknown_left > 0) {
-        if (drv.empty()) throw error(ZI_E_RUNTIME, "inpaint: unknown pixels unreachable from the fillfront");
         const auto t_it = std::chrono::steady_clock::now();
+        if (drv.empty()) throw error(ZI_E_RUNTIME, "inpaint: unknown pixels unreachable from the fillfront");
         int tx, ty;
         drv.next_target(tx, ty);
         extract_clamped(img, m, tx, ty, K, tv, tk);
+        t_select += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_it).count();
         bool prepared = false;
         const std::function<void()> prepare = [&] {
             drv.prepare_paste(tx, ty);
@@ -447,8 +480,9 @@ void run_inpaint(zi_multi_index* mi, const uint8_t* image, const uint8_t* known,
     stats->inpaint_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (ae_contrib > 0) stats->mean_ae = ae_sum / static_cast<double>(ae_contrib);
     if (std::getenv("ZI_DEBUG_QUERY") || std::getenv("ZI_DEBUG_FILL"))
-        std::fprintf(stderr, "fill loop: %llu iterations, query %.1f us/it, paste+priorities %.1f us/it\n",
-                     static_cast<unsigned long long>(it), 1e6 * t_query / it, 1e6 * t_paste / it);
+        std::fprintf(stderr, "fill loop: %llu iterations, select+extract %.1f us/it, query %.1f us/it, paste+priorities %.1f us/it, total %.1f us/it\n",
+                     static_cast<unsigned long long>(it), 1e6 * t_select / it, 1e6 * t_query / it, 1e6 * t_paste / it,
+                     1e6 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / it);
     stats->ae_excluded = ae_excl;
 }
 
