@@ -727,13 +727,15 @@ __global__ void __launch_bounds__(kGmThreads, 1) k_gram_fused(const __grid_const
 }
 
 // sum of the per-CTA partial Grams in int64 into the moments (every output has one owner: no atomics)
+struct gm_pairs {
+    int pti[kGmPairs], ptj[kGmPairs];
+};
 __global__ void __launch_bounds__(256) k_gram_reduce(const uint32_t* __restrict__ part, int nblocks, int npair,
-                                                     const int* __restrict__ pti, const int* __restrict__ ptj, int F,
-                                                     unsigned long long* __restrict__ out) {
+                                                     const gm_pairs pairs, int F, unsigned long long* __restrict__ out) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= npair * 128 * 128) return;
     const int p = idx >> 14, r = (idx >> 7) & 127, c = idx & 127;
-    const int fi = pti[p] * kPtRows + r, fj = ptj[p] * kPtRows + c;
+    const int fi = pairs.pti[p] * kPtRows + r, fj = pairs.ptj[p] * kPtRows + c;
     if (fi >= F || fj > F) return;
     unsigned long long acc = 0;
     const size_t stride = static_cast<size_t>(npair) * 128 * 128;
@@ -751,17 +753,15 @@ static void launch_gram(zi_ctx* ctx, const gm_params& G, size_t smem) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(G.P.ntiles, want));
     gm_params g = G;
     g.part = reinterpret_cast<uint32_t*>(ctx->scratch.ensure(static_cast<size_t>(grid) * G.npair * 128 * 128 * 4 + 256));
-    int* pp = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(g.part) + static_cast<size_t>(grid) * G.npair * 128 * 128 * 4);
     ZI_LAUNCH(ctx, "patch_moments_fused", k_gram_fused<KT>, grid, kGmThreads, smem, g);
-    int hp[2 * kGmPairs];
+    gm_pairs pairs{};  // by value: no upload of the tile pairs
     for (int i = 0; i < kGmPairs; ++i) {
-        hp[i] = G.pti[i];
-        hp[kGmPairs + i] = G.ptj[i];
+        pairs.pti[i] = G.pti[i];
+        pairs.ptj[i] = G.ptj[i];
     }
-    ZI_CUDA(cudaMemcpyAsync(pp, hp, sizeof(hp), cudaMemcpyHostToDevice, ctx->stream));
     const int outs = G.npair * 128 * 128;
     ZI_LAUNCH(ctx, "patch_moments_reduce", k_gram_reduce, (outs + 255) / 256, 256, 0, g.part, static_cast<int>(grid), G.npair,
-              pp, pp + kGmPairs, G.P.F, G.out);
+              pairs, G.P.F, G.out);
 }
 
 // exact moments of the n patches at d_keys (row-major key order) straight from the image;
