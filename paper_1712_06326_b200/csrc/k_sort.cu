@@ -149,7 +149,7 @@ __device__ __forceinline__ uint32_t lookback(const uint32_t* st, uint32_t tile, 
 // written back but straight into the layout indices -- dim planes (de-interleaved Morton key) and
 // the dictionary key of the payload row -- at their final positions (finalize without its read).
 template <int NW, int IT, int MODE, int DF = 0>
-__global__ void __launch_bounds__(kSortThreads, NW * IT <= 24 ? 4 : NW * IT <= 36 ? 3 : 2)
+__global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? 4 : 2)
     k_onesweep(sort_words io, int dw, int ds, const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                uint32_t* __restrict__ tile_ctr, const uint32_t* __restrict__ offs, uint32_t gn, uint32_t tpg,
                const __grid_constant__ final_sink sink) {
