@@ -33,7 +33,6 @@
 namespace zi {
 
 constexpr int kPtRows = 128;
-constexpr int kPtGatherWarps = 4;                // warps 0-3: one thread per patch row
 // epilogue warps 4 .. 4 + 4S - 1: TMEM lane quarter (w & 3), layouts li = (w >> 2) mod S.  S = 4 sets
 // for D <= 10 (a group's layouts spread one per set); S = 3 above, where the larger per-layout
 // register state would spill at the 80 registers a 21-warp CTA leaves per thread
@@ -44,11 +43,15 @@ __host__ __device__ constexpr bool pt_running() {
     return D >= 7 && D <= 10;
 }
 
-template <int D>
+template <int D, int MODE>
 struct pt_shape {
+    // gather warps 0 .. G-1: G = 8 (two threads per patch row, the halves of its features) for the
+    // min / max pass at D <= 8, whose light epilogue leaves the gather as the limit; G = 4 (one
+    // thread per row) otherwise (the quantise pass measured slower with 8: 2.49 -> 2.61 ms at cfg4)
+    static constexpr int kGatherWarps = (D <= 8 && MODE == 0) ? 8 : 4;
     static constexpr int kEpiSets = D <= 10 ? 4 : 3;
     static constexpr int kEpiWarps = 4 * kEpiSets;
-    static constexpr int kMmaWarp = kPtGatherWarps + kEpiWarps;
+    static constexpr int kMmaWarp = kGatherWarps + kEpiWarps;
     static constexpr int kThreads = (kMmaWarp + 1) * 32;
 };
 constexpr int kPtMaxFpad = 384;
@@ -206,9 +209,10 @@ __device__ __forceinline__ void pt_gather_static(const uint8_t* __restrict__ img
 }
 
 template <int D, int MODE, int KT>
-__global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __grid_constant__ pt_params P) {
-    constexpr int kPtEpiSets = pt_shape<D>::kEpiSets, kPtEpiWarps = pt_shape<D>::kEpiWarps;
-    constexpr int kPtMmaWarp = pt_shape<D>::kMmaWarp, kPtThreads = pt_shape<D>::kThreads;
+__global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(const __grid_constant__ pt_params P) {
+    constexpr int kPtEpiSets = pt_shape<D, MODE>::kEpiSets, kPtEpiWarps = pt_shape<D, MODE>::kEpiWarps;
+    constexpr int kPtGatherWarps = pt_shape<D, MODE>::kGatherWarps;
+    constexpr int kPtMmaWarp = pt_shape<D, MODE>::kMmaWarp, kPtThreads = pt_shape<D, MODE>::kThreads;
     constexpr int W = (D + 3) / 4;
     extern __shared__ uint8_t pt_raw[];
     uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(pt_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -325,15 +329,17 @@ __global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __gr
                 tc_commit(tc_smem(&s_accfull[buf]));
             }
         }
-    } else if (warp < kPtGatherWarps) {  // gather: one thread per patch row
-        const int nchunk = P.Fpad >> 4;
+    } else if (warp < kPtGatherWarps) {  // gather: two threads per patch row (the halves of its features)
+        const int nchunk = P.Fpad >> 4, hc = (nchunk + 1) >> 1, gh = tid >> 7;
+        constexpr bool kTwo = kPtGatherWarps == 8;  // else one thread does both halves
         for (uint64_t i = 0; i < nloc; ++i) {
             const int buf = static_cast<int>(i & 1);
             const uint32_t use = static_cast<uint32_t>(i >> 1);
             if (i >= 2) tc_mbar_wait(tc_smem(&s_aempty[buf]), (use - 1) & 1);
             const uint64_t tile = blockIdx.x + i * gridDim.x;
             if (KT == 0) {
-                pt_gather(P, s_wtab, tile, tc_smem(sA + buf * abytes), tid, 0, nchunk);
+                if (kTwo) pt_gather(P, s_wtab, tile, tc_smem(sA + buf * abytes), tid & 127, gh ? hc : 0, gh ? nchunk : hc);
+                else pt_gather(P, s_wtab, tile, tc_smem(sA + buf * abytes), tid, 0, nchunk);
             } else {
                 const int r = tid & 127;
                 const uint64_t pr = tile * kPtRows + r;
@@ -345,11 +351,11 @@ __global__ void __launch_bounds__(pt_shape<D>::kThreads, 1) k_proj_tc(const __gr
                 }
                 const uint32_t wC = static_cast<uint32_t>(P.w * P.C), sa = tc_smem(sA + buf * abytes);
                 if (KT == 1) {
-                    pt_gather_static<9, 1, 0>(P.img, base, wC, valid, sa, r);
-                    pt_gather_static<9, 1, 1>(P.img, base, wC, valid, sa, r);
+                    if (!kTwo || !gh) pt_gather_static<9, 1, 0>(P.img, base, wC, valid, sa, r);
+                    if (!kTwo || gh) pt_gather_static<9, 1, 1>(P.img, base, wC, valid, sa, r);
                 } else {
-                    pt_gather_static<11, 3, 0>(P.img, base, wC, valid, sa, r);
-                    pt_gather_static<11, 3, 1>(P.img, base, wC, valid, sa, r);
+                    if (!kTwo || !gh) pt_gather_static<11, 3, 0>(P.img, base, wC, valid, sa, r);
+                    if (!kTwo || gh) pt_gather_static<11, 3, 1>(P.img, base, wC, valid, sa, r);
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -943,8 +949,8 @@ static void launch_pt_kt(zi_ctx* ctx, const pt_params& P, int mode, size_t smem)
     if (mode == 0) smem_attr(ctx->device, k_proj_tc<D, 0, KT>, 200 * 1024);
     else smem_attr(ctx->device, k_proj_tc<D, 1, KT>, 200 * 1024);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(P.ntiles, static_cast<uint64_t>(ctx->num_sms)));
-    if (mode == 0) ZI_LAUNCH(ctx, "project_tc_minmax", (k_proj_tc<D, 0, KT>), grid, pt_shape<D>::kThreads, smem, P);
-    else ZI_LAUNCH(ctx, "project_tc_quantize", (k_proj_tc<D, 1, KT>), grid, pt_shape<D>::kThreads, smem, P);
+    if (mode == 0) ZI_LAUNCH(ctx, "project_tc_minmax", (k_proj_tc<D, 0, KT>), grid, (pt_shape<D, 0>::kThreads), smem, P);
+    else ZI_LAUNCH(ctx, "project_tc_quantize", (k_proj_tc<D, 1, KT>), grid, (pt_shape<D, 1>::kThreads), smem, P);
 }
 
 // patch shapes with a static gather: (9, 1) -> 1 (cfg1, cfg4), (11, 3) -> 2 (cfg2); for the dims
