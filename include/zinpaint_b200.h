@@ -123,6 +123,11 @@ zi_status zi_ctx_flush_l2(zi_ctx* ctx);
 uint64_t zi_ctx_kernel_launches(const zi_ctx* ctx);
 /* per-kernel device time accumulated while profiling is on (name-indexed, see api.cu) */
 zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on);
+/* Morton sort policy of this ctx's 8-layout builds with `dims` quantised dims: 0 = learn (the
+ * first build picks MSD + window sort from the byte histograms and falls back to LSD when the top
+ * bytes are too clustered; later builds remember), -1 = LSD digit passes, whose last pass writes
+ * the indices (fused finalize), k > 0 = k MSD bytes + window sort.  Results are identical. */
+zi_status zi_ctx_set_sort_policy(zi_ctx* ctx, int32_t dims, int32_t policy);
 /* time only these kernels (comma-separated launch names; NULL or "": every kernel) */
 zi_status zi_ctx_set_profile_filter(zi_ctx* ctx, const char* names);
 zi_status zi_ctx_profile(const zi_ctx* ctx, int slot, double* ms, uint64_t* launches,

@@ -110,6 +110,10 @@ class Context:
     def set_profiling(self, on: bool):
         check(lib().zi_ctx_set_profiling(self.h, int(on)))
 
+    def set_sort_policy(self, dims: int, policy: int):
+        """8-layout build sort for `dims`: 0 learn, -1 LSD passes (fused finalize), k > 0 MSD bytes."""
+        check(lib().zi_ctx_set_sort_policy(self.h, int(dims), int(policy)))
+
     def set_profile_filter(self, names=None):
         """Time only these kernels while profiling (None: every kernel)."""
         check(lib().zi_ctx_set_profile_filter(self.h, ",".join(names).encode() if names else None))

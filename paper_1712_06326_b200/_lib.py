@@ -73,6 +73,7 @@ SIGNATURES = {
     "zi_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
     "zi_ctx_profile": (C.c_int, [vp, C.c_int, f64p, u64p, C.POINTER(C.c_char_p)]),
     "zi_ctx_set_profile_filter": (C.c_int, [vp, C.c_char_p]),
+    "zi_ctx_set_sort_policy": (C.c_int, [vp, C.c_int32, C.c_int32]),
     "zi_less_most_significant_bit": (C.c_int, [C.c_int, C.c_int]),
     "zi_morton_less": (C.c_int, [u8p, u8p, C.c_uint32]),
     "zi_subset_pixel_count": (C.c_int, [C.c_int, C.c_double]),

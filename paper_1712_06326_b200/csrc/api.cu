@@ -294,6 +294,15 @@ zi_status zi_ctx_set_profiling(zi_ctx* ctx, int on) {
     });
 }
 
+zi_status zi_ctx_set_sort_policy(zi_ctx* ctx, int32_t dims, int32_t policy) {
+    return guard(ctx, [&] {
+        require(ctx != nullptr, "null argument");
+        require(dims >= 1 && dims <= 32, "sort policy: dims must be in [1, 32]");
+        require(policy >= -1 && policy <= dims - 3, "sort policy: -1, 0 or an MSD depth in [1, dims - 3]");
+        ctx->sort_depth[dims][1] = policy;
+    });
+}
+
 zi_status zi_ctx_set_profile_filter(zi_ctx* ctx, const char* names) {
     return guard(ctx, [&] {
         require(ctx != nullptr, "null argument");

@@ -196,6 +196,41 @@ def test_build_to_overlapped_copies_equal_build(zb, golden):
                                                  C.byref(hmi)))
 
 
+@pytest.mark.parametrize("K,ch,D", [(9, 1, 8), (9, 1, 4), (11, 3, 12), (9, 1, 16)])
+def test_fused_lsd_build_equals_oracle(zb, K, ch, D):
+    """The LSD sort policy: the sort's last pass writes the 8 indices (dim planes, keys carried as
+    the record payload) and one kernel adds the bboxes -- byte-equal to the oracle's build_index."""
+    from tests.helpers import pca_of
+    img, kn = workloads.small_image(120, 104, ch, seed=40 + D, hole_frac=0.1)
+    ctx = zb.Context.default()
+    ctx.set_sort_policy(D, -1)
+    try:
+        ctx.set_profiling(True)
+        mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=K, dims=D), ctx=ctx)
+        prof = ctx.profile()
+        ctx.set_profiling(False)
+        assert mi.dims == D
+        assert prof.get("index_bbox", (0.0, 0))[1] == 1, "the fused final pass did not run"
+        assert prof.get("finalize_index", (0.0, 0))[1] == 0
+        pm, pc = pca_of(mi)
+        om = oracle.MultiIndex(img, kn, K, 0.6, D, pca_mean=pm, pca_comp=pc)
+        for l in range(8):
+            c, k = mi.index_arrays(l)
+            ref = om.index(l)
+            assert np.array_equal(c, ref.coords) and np.array_equal(k, ref.keys), (D, l)
+            lay = mi.layout(l)
+            assert np.array_equal(lay["lo"], ref.lo) and np.array_equal(lay["hi"], ref.hi), (D, l)
+        # the bboxes the queries prune with: a query equals the oracle's
+        ys, xs = np.nonzero(kn == 0)
+        tv, tk = oracle.extract_patch_clamped(img, kn, int(xs[0]), int(ys[0]) - 1, K)
+        got = mi.query_best_patch(tv, tk)
+        best, lid, ncand, _ = om.query_best_patch(img, tv, tk, 80)
+        assert (got[1] << 32 | got[0]) == best and got[3] == lid and got[4] == ncand, D
+    finally:
+        ctx.set_profiling(False)
+        ctx.set_sort_policy(D, 0)
+
+
 def test_empty_dictionary_raises(zb):
     img = np.zeros((20, 20), np.uint8)
     with pytest.raises(zb.EmptyDictionaryError):

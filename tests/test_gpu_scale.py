@@ -142,6 +142,19 @@ def test_cfg4_all_layouts_bitexact(cfg4_pair):
     _check_layouts(mi, om, range(8))
 
 
+def test_cfg4_rebuild_fused_sort_bitexact(cfg4_pair):
+    """The first cfg4 build finds the top Morton bytes too clustered for the MSD split and falls
+    back to LSD; later builds go straight to LSD passes whose last pass writes the indices (the
+    bench's steady state).  That rebuild is byte-equal to the oracle too."""
+    img, kn, p, mi, om = cfg4_pair
+    mi.ctx.set_profiling(True)
+    mi.rebuild()
+    prof = mi.ctx.profile()
+    mi.ctx.set_profiling(False)
+    assert prof.get("index_bbox", (0.0, 0))[1] == 1 and prof.get("finalize_index", (0.0, 0))[1] == 0
+    _check_layouts(mi, om, range(8))
+
+
 def test_cfg4_sort_equals_compiled_reference(cfg4_pair):
     img, kn, p, mi, om = cfg4_pair
     d = mi.dictionary
