@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libzinpaint_b200.so")
+LIB_PATH = os.environ.get("ZI_LIB_PATH") or os.path.join(HERE, "libzinpaint_b200.so")  # ZI_LIB_PATH: dev A/B of a variant build
 
 u8p = C.POINTER(C.c_uint8)
 f32p = C.POINTER(C.c_float)

@@ -148,21 +148,72 @@ __device__ __forceinline__ uint32_t lookback(const uint32_t* st, uint32_t tile, 
 // MODE 1 with DF > 0 (the sort's last pass over the 8-layout records, D = DF): the records are not
 // written back but straight into the layout indices -- dim planes (de-interleaved Morton key) and
 // the dictionary key of the payload row -- at their final positions (finalize without its read).
+#ifndef ZI_OS_MATCH
+#define ZI_OS_MATCH 0
+#endif
+// lanes of the warp holding the same 9-bit value (bit 8 = "no record"): MATCH.ANY is throttled
+// in the MIO pipe when the warp holds many distinct values (a random digit: ~30 per warp), eight
+// ballots and their mask updates issue on the ALU side
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
+#if ZI_OS_MATCH == 0
+    return __match_any_sync(0xffffffffu, d);
+#else
+    uint32_t peers = __ballot_sync(0xffffffffu, d < 256u);
+    if (d >= 256u) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
+    }
+    return peers;
+#endif
+}
+
+#ifndef ZI_OS_IT3
+#define ZI_OS_IT3 12
+#endif
+#ifndef ZI_OS_KC
+#define ZI_OS_KC 2
+#endif
+#ifndef ZI_OS_HT
+#define ZI_OS_HT uint32_t
+#endif
+#ifndef ZI_OS_CTAS
+#define ZI_OS_CTAS 4
+#endif
+#ifndef ZI_OS_RANK
+#define ZI_OS_RANK 2
+#endif
 template <int NW, int IT, int MODE, int DF = 0>
-__global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? 4 : 2)
+__global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? ZI_OS_CTAS : 2)
     k_onesweep(sort_words io, int dw, int ds, const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                uint32_t* __restrict__ tile_ctr, const uint32_t* __restrict__ offs, uint32_t gn, uint32_t tpg,
                const __grid_constant__ final_sink sink) {
     constexpr int TILE = kSortThreads * IT;
     extern __shared__ uint32_t s_stage[];  // NW * TILE
+#if ZI_OS_RANK == 2
+    // KC independent ranking chains: record slot i of a warp counts into histogram i / (IT / KC)
+    constexpr int KC = IT % ZI_OS_KC == 0 ? ZI_OS_KC : 1;
+    constexpr int SPC = IT / KC;  // slots per chain
+    typedef ZI_OS_HT hist_t;
+    __shared__ hist_t s_hist[kSortWarps][KC][256];
+#else
+    constexpr int KC = 1;
     __shared__ uint32_t s_hist[kSortWarps][256];
+#endif
     __shared__ uint32_t s_start[256];
     __shared__ uint32_t s_delta[256];  // global position of the digit's first record, minus its tile start
     __shared__ uint32_t s_warp[kSortWarps];
     __shared__ uint32_t s_tile;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if ZI_OS_RANK == 2
+    for (int i = tid; i < kSortWarps * KC * 256 * static_cast<int>(sizeof(hist_t)) / 4; i += kSortThreads)
+        reinterpret_cast<uint32_t*>(&s_hist[0][0][0])[i] = 0;
+#else
     for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&s_hist[0][0])[i] = 0;
+#endif
     if (MODE == 0) {
         if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
         __syncthreads();
@@ -198,13 +249,66 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? 4 : 2)
     uint32_t wmask[NW];
 #pragma unroll
     for (int k = 0; k < NW; ++k) wmask[k] = dw == k ? 0xffffffffu : 0u;
+#if ZI_OS_RANK == 2
+    // Ranking: per record slot the lanes read their digit's running count in the warp's
+    // histogram and the highest lane of each digit group adds the group's size.  That read ->
+    // write -> next read chain costs a shared-memory round trip per slot; the slots are split over
+    // KC histograms (slot i -> chain i / SPC, which keeps the record order: warp, chain, slot)
+    // and one step advances all KC chains, so the round trips of KC slots overlap.
+#pragma unroll
+    for (int s = 0; s < SPC; ++s) {
+        uint32_t dd[KC], pp[KC], oo[KC];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+            const int i = c * SPC + s;
+            uint32_t x = 0;
+#pragma unroll
+            for (int k = 0; k < NW; ++k) x |= rec[i][k] & wmask[k];
+            dd[c] = w0 + static_cast<uint32_t>(i * 32) < cnt ? (x >> ds) & 0xffu : 0x100u;
+            pp[c] = digit_peers(dd[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < KC; ++c) oo[c] = dd[c] < 256u ? s_hist[warp][c][dd[c]] : 0u;
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < KC; ++c)
+            if (dd[c] < 256u && (pp[c] >> lane) == 1u) s_hist[warp][c][dd[c]] = static_cast<hist_t>(oo[c] + __popc(pp[c]));
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < KC; ++c) dr[c * SPC + s] = (dd[c] << 16) | (oo[c] + __popc(pp[c] & lt_mask));
+    }
+#elif ZI_OS_RANK == 1
+    // Ranking without a dependent shared-memory round trip per record: the highest peer lane of
+    // each digit group adds the group's size to the warp's histogram with one shared atomic per
+    // record slot -- issued back to back (nothing waits on the result; a warp's shared-memory
+    // instructions are performed in issue order, so slot i's groups precede slot i + 1's) -- and
+    // the returned bases are handed to the peers by shuffles at the end.
+    uint32_t old[IT];
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
         uint32_t x = 0;
 #pragma unroll
         for (int k = 0; k < NW; ++k) x |= rec[i][k] & wmask[k];
         const uint32_t d = w0 + static_cast<uint32_t>(i * 32) < cnt ? (x >> ds) & 0xffu : 0x100u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t peers = digit_peers(d);
+        old[i] = 0;
+        if (d < 256u && (peers >> lane) == 1u) old[i] = atomicAdd(&s_hist[warp][d], static_cast<uint32_t>(__popc(peers)));
+        // digit | leader lane | rank among the peers
+        dr[i] = (d << 16) | (static_cast<uint32_t>(31 - __clz(peers)) << 8) | static_cast<uint32_t>(__popc(peers & lt_mask));
+    }
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const uint32_t base = __shfl_sync(0xffffffffu, old[i], (dr[i] >> 8) & 31u);
+        dr[i] = (dr[i] & 0xffff0000u) | (base + (dr[i] & 0xffu));
+    }
+#else
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) x |= rec[i][k] & wmask[k];
+        const uint32_t d = w0 + static_cast<uint32_t>(i * 32) < cnt ? (x >> ds) & 0xffu : 0x100u;
+        const uint32_t peers = digit_peers(d);
         uint32_t old = 0;
         if (d < 256u) old = s_hist[warp][d];
         __syncwarp();
@@ -212,17 +316,29 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? 4 : 2)
         __syncwarp();
         dr[i] = (d << 16) | (old + __popc(peers & lt_mask));
     }
+#endif
     __syncthreads();
 
     // per-digit: warp exclusive offsets + tile count
     const int d = tid;
     uint32_t run = 0;
+#if ZI_OS_RANK == 2
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w)
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+            const uint32_t t = s_hist[w][c][d];
+            s_hist[w][c][d] = static_cast<hist_t>(run);
+            run += t;
+        }
+#else
 #pragma unroll
     for (int w = 0; w < kSortWarps; ++w) {
         const uint32_t t = s_hist[w][d];
         s_hist[w][d] = run;
         run += t;
     }
+#endif
     const uint32_t tile_cnt = run;
     if (MODE == 0) os_store(status + static_cast<size_t>(tile) * 256 + d, (tig == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
 
@@ -259,7 +375,11 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? 4 : 2)
     for (int i = 0; i < IT; ++i) {
         const uint32_t dg = dr[i] >> 16;
         if (dg < 256u) {
+#if ZI_OS_RANK == 2
+            const uint32_t pos = s_start[dg] + s_hist[warp][i / SPC][dg] + (dr[i] & 0xffffu);
+#else
             const uint32_t pos = s_start[dg] + s_hist[warp][dg] + (dr[i] & 0xffffu);
+#endif
 #pragma unroll
             for (int k = 0; k < NW; ++k) s_stage[k * TILE + pos] = rec[i][k];
         }
@@ -439,7 +559,7 @@ __global__ void __launch_bounds__(256) k_lsd_offsets(uint32_t* __restrict__ coun
 // occupancy (NW * IT <= 36: three CTAs per SM, else two)
 template <int NW>
 constexpr int os_items() {
-    return NW == 2 ? 12 : NW == 3 ? 12 : NW == 4 ? 16 : NW == 5 ? 12 : 8;
+    return NW == 2 ? 12 : NW == 3 ? ZI_OS_IT3 : NW == 4 ? 16 : NW == 5 ? 12 : 8;
 }
 
 static int onesweep_items(int nw) {
