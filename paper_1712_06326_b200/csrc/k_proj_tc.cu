@@ -536,15 +536,31 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                             qi = static_cast<int>(static_cast<uint32_t>(__double_as_longlong(tq)));
                         }
                         const uint32_t q = static_cast<uint32_t>(min(max(qi, 0), 255));
-                        const int sh = D - 1 - d;
-                        uint32_t prev = 0;
+                        if constexpr (D == 8) {
+                            // the bytes of the 8 dims (dim 0 on top); the key is their 8x8 bit transpose
+                            kw[d < 4 ? 1 : 0] |= q << (8 * (3 - (d & 3)));
+                        } else {
+                            const int sh = D - 1 - d;
+                            uint32_t prev = 0;
 #pragma unroll
-                        for (int k = 0; k < W; ++k) {
-                            const uint32_t cur = s_spread[(lane >> 3) * kSpStride + q * W + k];
-                            kw[k] |= sh ? __funnelshift_l(prev, cur, sh) : cur;
-                            prev = cur;
+                            for (int k = 0; k < W; ++k) {
+                                const uint32_t cur = s_spread[(lane >> 3) * kSpStride + q * W + k];
+                                kw[k] |= sh ? __funnelshift_l(prev, cur, sh) : cur;
+                                prev = cur;
+                            }
                         }
                     }
+                }
+                if constexpr (MODE == 1 && D == 8) {
+                    // Morton key of 8 dims x 8 bits = the bit transpose of the 8x8 matrix whose row d
+                    // is dim d's byte: two delta swaps inside each word, one nibble exchange across
+                    uint32_t hi = kw[1], lo = kw[0], t;
+                    t = (hi ^ (hi >> 7)) & 0x00AA00AAu, hi = hi ^ t ^ (t << 7);
+                    t = (lo ^ (lo >> 7)) & 0x00AA00AAu, lo = lo ^ t ^ (t << 7);
+                    t = (hi ^ (hi >> 14)) & 0x0000CCCCu, hi = hi ^ t ^ (t << 14);
+                    t = (lo ^ (lo >> 14)) & 0x0000CCCCu, lo = lo ^ t ^ (t << 14);
+                    kw[0] = (lo & 0x0F0F0F0Fu) | ((hi & 0x0F0F0F0Fu) << 4);
+                    kw[1] = (hi & 0xF0F0F0F0u) | ((lo >> 4) & 0x0F0F0F0Fu);
                 }
                 if (MODE == 1) {
                     const uint32_t l = static_cast<uint32_t>(P.l0 + li);
