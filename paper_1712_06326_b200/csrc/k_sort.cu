@@ -18,7 +18,10 @@
 
 namespace zi {
 
-constexpr int kSortThreads = 256;
+#ifndef ZI_OS_THREADS
+#define ZI_OS_THREADS 256
+#endif
+constexpr int kSortThreads = ZI_OS_THREADS;  // the first 256 threads double as the digits' threads
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 constexpr int kMaxWords = 9;  // up to 8 Morton key words (D <= 32) + payload
@@ -186,7 +189,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
 #define ZI_OS_RANK 2
 #endif
 template <int NW, int IT, int MODE, int DF = 0>
-__global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? ZI_OS_CTAS : 2)
+__global__ void __launch_bounds__(kSortThreads, (NW * IT <= 36 ? ZI_OS_CTAS : 2) * 256 / kSortThreads)
     k_onesweep(sort_words io, int dw, int ds, const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
                uint32_t* __restrict__ tile_ctr, const uint32_t* __restrict__ offs, uint32_t gn, uint32_t tpg,
                const __grid_constant__ final_sink sink) {
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? ZI_OS_CTAS : 2)
 #endif
     __shared__ uint32_t s_start[256];
     __shared__ uint32_t s_delta[256];  // global position of the digit's first record, minus its tile start
-    __shared__ uint32_t s_warp[kSortWarps];
+    __shared__ uint32_t s_warp[8];
     __shared__ uint32_t s_tile;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? ZI_OS_CTAS : 2)
     const uint32_t cnt = gn - t0 < static_cast<uint32_t>(TILE) ? gn - t0 : static_cast<uint32_t>(TILE);
     const uint32_t tb = grp * gn + t0;  // global index of the tile's first record
     uint32_t goff = 0;
-    if (MODE == 1) goff = __ldg(offs + static_cast<size_t>(tile) * 256 + tid);  // in flight with the records
+    if (MODE == 1 && tid < 256) goff = __ldg(offs + static_cast<size_t>(tile) * 256 + tid);  // in flight with the records
 
     // every word of the tile's records is loaded up front (maximum loads in flight)
     uint32_t rec[IT][NW];
@@ -320,27 +323,30 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? ZI_OS_CTAS : 2)
     __syncthreads();
 
     // per-digit: warp exclusive offsets + tile count
-    const int d = tid;
+    const int d = tid & 255;
+    const bool dthr = tid < 256;  // digit thread
     uint32_t run = 0;
+    if (dthr) {
 #if ZI_OS_RANK == 2
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w)
+        for (int w = 0; w < kSortWarps; ++w)
 #pragma unroll
-        for (int c = 0; c < KC; ++c) {
-            const uint32_t t = s_hist[w][c][d];
-            s_hist[w][c][d] = static_cast<hist_t>(run);
-            run += t;
-        }
+            for (int c = 0; c < KC; ++c) {
+                const uint32_t t = s_hist[w][c][d];
+                s_hist[w][c][d] = static_cast<hist_t>(run);
+                run += t;
+            }
 #else
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) {
-        const uint32_t t = s_hist[w][d];
-        s_hist[w][d] = run;
-        run += t;
-    }
+        for (int w = 0; w < kSortWarps; ++w) {
+            const uint32_t t = s_hist[w][d];
+            s_hist[w][d] = run;
+            run += t;
+        }
 #endif
+    }
     const uint32_t tile_cnt = run;
-    if (MODE == 0) os_store(status + static_cast<size_t>(tile) * 256 + d, (tig == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
+    if (MODE == 0 && dthr) os_store(status + static_cast<size_t>(tile) * 256 + d, (tig == 0 ? kFlagInc : kFlagAgg) | tile_cnt);
 
     // tile-local exclusive scan over digits
     uint32_t start;
@@ -351,15 +357,15 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? ZI_OS_CTAS : 2)
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
-        if (lane == 31) s_warp[warp] = x;
+        if (lane == 31 && dthr) s_warp[warp] = x;
         __syncthreads();
         uint32_t wp = 0;
 #pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) wp += w < warp ? s_warp[w] : 0u;
+        for (int w = 0; w < 8; ++w) wp += w < warp ? s_warp[w] : 0u;
         start = wp + x - tile_cnt;
-        s_start[d] = start;
+        if (dthr) s_start[d] = start;
     }
-    if (MODE == 0) {
+    if (MODE == 0 && dthr) {
         uint32_t prefix = 0;
         if (tig > 0) {
             prefix = lookback(status, tile, tile - tig, d);
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(kSortThreads, NW * IT <= 36 ? ZI_OS_CTAS : 2)
         }
         goff = grp * gn + digit_base[grp * 256 + d] + prefix;
     }
-    s_delta[d] = goff - start;
+    if (dthr) s_delta[d] = goff - start;
     __syncthreads();
 
     // stage records in tile-sorted order
@@ -497,10 +503,12 @@ __global__ void __launch_bounds__(kSortThreads) k_lsd_count(const uint32_t* __re
         if (j < cnt) atomicAdd(&s_h[warp][(x[i] >> ds) & 0xffu], 1u);
     }
     __syncthreads();
-    uint32_t c = 0;
+    if (tid < 256) {
+        uint32_t c = 0;
 #pragma unroll
-    for (int w = 0; w < kSortWarps; ++w) c += s_h[w][tid];
-    counts[static_cast<size_t>(tile) * 256 + tid] = c;
+        for (int w = 0; w < kSortWarps; ++w) c += s_h[w][tid];
+        counts[static_cast<size_t>(tile) * 256 + tid] = c;
+    }
 }
 
 __global__ void __launch_bounds__(256) k_lsd_chunk_sum(const uint32_t* __restrict__ counts, uint32_t tpg, uint32_t cpg,
@@ -513,18 +521,25 @@ __global__ void __launch_bounds__(256) k_lsd_chunk_sum(const uint32_t* __restric
     csum[static_cast<size_t>(c) * 256 + d] = s;
 }
 
-__global__ void __launch_bounds__(256) k_lsd_chunk_scan(uint32_t* __restrict__ csum, uint32_t cpg, uint32_t gn) {
+__global__ void __launch_bounds__(256) k_lsd_chunk_scan(uint32_t* __restrict__ csum, uint32_t cpg, uint32_t gn,
+                                                        uint32_t* __restrict__ gbase) {
     __shared__ uint32_t s_w[8];
     const uint32_t g = blockIdx.x;
     const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
     uint32_t* cs = csum + static_cast<size_t>(g) * cpg * 256 + d;
     uint32_t run = 0;
-    for (uint32_t k = 0; k < cpg; ++k) {
-        const uint32_t v = cs[static_cast<size_t>(k) * 256];
-        cs[static_cast<size_t>(k) * 256] = run;
-        run += v;
+    constexpr uint32_t U = 8;  // chunk sums loaded together (the running sum waits once per batch)
+    for (uint32_t k0 = 0; k0 < cpg; k0 += U) {
+        uint32_t v[U];
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) v[u] = k0 + u < cpg ? cs[static_cast<size_t>(k0 + u) * 256] : 0u;
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+            if (k0 + u < cpg) cs[static_cast<size_t>(k0 + u) * 256] = run;
+            run += v[u];
+        }
     }
-    // the group's digit bases: exclusive scan of the totals over the digits
+    // the group's digit bases: exclusive scan of the totals over the digits (added by k_lsd_offsets)
     uint32_t x = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -536,15 +551,14 @@ __global__ void __launch_bounds__(256) k_lsd_chunk_scan(uint32_t* __restrict__ c
     uint32_t wp = 0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) wp += w < warp ? s_w[w] : 0u;
-    const uint32_t base = g * gn + wp + x - run;
-    for (uint32_t k = 0; k < cpg; ++k) cs[static_cast<size_t>(k) * 256] += base;
+    gbase[g * 256 + d] = g * gn + wp + x - run;
 }
 
 __global__ void __launch_bounds__(256) k_lsd_offsets(uint32_t* __restrict__ counts, const uint32_t* __restrict__ csum,
-                                                     uint32_t tpg, uint32_t cpg) {
+                                                     const uint32_t* __restrict__ gbase, uint32_t tpg, uint32_t cpg) {
     const uint32_t c = blockIdx.x, g = c / cpg, k = c - g * cpg, d = threadIdx.x;
     const uint32_t t0 = g * tpg + k * kLsdChunk, t1 = min(t0 + kLsdChunk, (g + 1) * tpg);
-    uint32_t run = csum[static_cast<size_t>(c) * 256 + d];
+    uint32_t run = csum[static_cast<size_t>(c) * 256 + d] + gbase[g * 256 + d];
     uint32_t v[kLsdChunk];  // the chunk's counts, all loads in flight before the running sum
 #pragma unroll
     for (int u = 0; u < kLsdChunk; ++u) v[u] = t0 + u < t1 ? counts[static_cast<size_t>(t0 + u) * 256 + d] : 0u;
@@ -588,6 +602,7 @@ struct pass_plan {
     uint32_t* ctr;               // MODE 0
     uint32_t* counts;            // MODE 1: [ntiles][256]
     uint32_t* csum;              // MODE 1: [G * cpg][256]
+    uint32_t* gbase;             // MODE 1: [G][256] first position of every (group, digit)
 };
 
 template <int NW>
@@ -606,8 +621,8 @@ static void launch_pass(zi_ctx* ctx, const sort_words& io, int dw, int ds, const
     ZI_LAUNCH(ctx, "radix_count", k_lsd_count<IT>, pp.ntiles, kSortThreads, 0, io.in[dw], ds, gn, pp.tpg, pp.counts);
     const unsigned nch = pp.cpg * static_cast<unsigned>(G);
     ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_sum, nch, 256, 0, pp.counts, pp.tpg, pp.cpg, pp.csum);
-    ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_scan, static_cast<unsigned>(G), 256, 0, pp.csum, pp.cpg, gn);
-    ZI_LAUNCH(ctx, "radix_scan", k_lsd_offsets, nch, 256, 0, pp.counts, pp.csum, pp.tpg, pp.cpg);
+    ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_scan, static_cast<unsigned>(G), 256, 0, pp.csum, pp.cpg, gn, pp.gbase);
+    ZI_LAUNCH(ctx, "radix_scan", k_lsd_offsets, nch, 256, 0, pp.counts, pp.csum, pp.gbase, pp.tpg, pp.cpg);
     if (sink) {  // the last pass of the 8-layout sort: straight into the indices
         constexpr int DF = NW == 2 ? 4 : NW == 3 ? 8 : NW == 4 ? 12 : 16;
         if constexpr (NW >= 2 && NW <= 5) {
@@ -678,7 +693,7 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
     const size_t alt_words = static_cast<size_t>(nw) * n;
     const size_t hist_words = static_cast<size_t>(npass) * G * 256;
     const size_t work_words = lb ? static_cast<size_t>(npass) * pp.ntiles * 256 + npass + 8
-                                 : static_cast<size_t>(pp.ntiles) * 256 + static_cast<size_t>(G) * pp.cpg * 256;
+                                 : static_cast<size_t>(pp.ntiles) * 256 + static_cast<size_t>(G) * (pp.cpg + 1) * 256;
     uint32_t* scr = reinterpret_cast<uint32_t*>(
         ctx->scratch.ensure((alt_words + 2 * hist_words + work_words + 4 * npass + 64) * sizeof(uint32_t)));
     uint32_t* alt = scr;
@@ -693,6 +708,7 @@ void radix_sort_words(zi_ctx* ctx, uint32_t** words, int nw, uint64_t n, const s
     } else {
         pp.counts = work;
         pp.csum = work + static_cast<size_t>(pp.ntiles) * 256;
+        pp.gbase = pp.csum + static_cast<size_t>(G) * pp.cpg * 256;
     }
 
     sort_words io{};
