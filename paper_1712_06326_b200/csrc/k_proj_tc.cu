@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
     __shared__ __align__(16) double2 s_qc[8][D][3];
     // fp32 pre-filter of the quantise pass per (layout, dim): {za * 2^20, zb, bz + eps, 1 - bz - eps}
     __shared__ __align__(16) float4 s_qf[8][D];
+    // lo / hi candidate thresholds on T >> 20 (floors of tlo, thi: a superset of the exact test)
+    __shared__ __align__(8) int2 s_qt[8][D];
     // Morton spread table, four copies 8 banks apart (lane group g = lane >> 3 reads copy g)
     constexpr int kSpStride = 256 * W + 8;
     __shared__ uint32_t s_spread[4 * kSpStride];
@@ -275,6 +277,9 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                 s_qc[li][d][0] = make_double2(za, zb);
                 s_qc[li][d][1] = make_double2(bz, __longlong_as_double(tlo));
                 s_qc[li][d][2] = make_double2(__longlong_as_double(thi), 0.0);
+                s_qt[li][d] = degen ? make_int2(INT_MAX, INT_MAX)
+                                    : make_int2(static_cast<int>(max(min(tlo >> 20, static_cast<long long>(INT_MAX)), static_cast<long long>(INT_MIN))),
+                                                static_cast<int>(max(min(thi >> 20, static_cast<long long>(INT_MAX)), static_cast<long long>(INT_MIN))));
                 // z32 = fmaf(float(T >> 20), za * 2^20, zb) is within eps of z': the dropped low 20
                 // bits of T (2^20 za), and five fp32 roundings of terms below |T za| + |zb| + 256,
                 // where |T za| = 255 |y' + M| / R is bounded through the approximate range (a row
@@ -487,12 +492,12 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                     // quantise pass converts once: y' = fl(T * 2^-38 - M) (T exact in a double)
                     const uint32_t* vd = v + kPtDigits * d;
                     static_assert(kPtDigits == 5, "T assembly below is written for five digits");
-                    const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
-                                        (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
-                                        (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
-                                        (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
-                                        static_cast<long long>(static_cast<int>(vd[0]));
                     if (MODE == 0) {
+                        const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
+                                            (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
+                                            (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
+                                            (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
+                                            static_cast<long long>(static_cast<int>(vd[0]));
                         // y' is monotone in T: min / max on T
                         const int th = static_cast<int>(T >> 32);
                         const uint32_t tl = static_cast<uint32_t>(T);
@@ -508,21 +513,32 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                             tmx0 = wmx > tmx0 ? wmx : tmx0;
                         }
                     } else {
-                        // degenerate ranges (amax - amin <= 4E) carry bz = 1 and tlo = LLONG_MAX:
+                        // floor(T / 2^20) in 32-bit arithmetic (|T| < 2^51; nested floors of the low
+                        // digits, wrap-around sums): the fast path never assembles the 64-bit T
+                        const int s0 = static_cast<int>(vd[0]) >> 8;
+                        const int s1 = (static_cast<int>(vd[1]) + s0) >> 8;
+                        const int s2 = (static_cast<int>(vd[2]) + s1) >> 4;
+                        const int t20 = static_cast<int>(vd[4] * 4096u + vd[3] * 16u + static_cast<uint32_t>(s2));
+                        // degenerate ranges (amax - amin <= 4E) carry bz = 1 and thresholds INT_MAX:
                         // every row is flagged and a lo / hi candidate, with no branch here
-                        const double2 c1 = s_qc[li][d][1];
-                        const double thi = s_qc[li][d][2].x;
-                        cand = cand || (T <= __double_as_longlong(c1.y)) || (T >= __double_as_longlong(thi));
+                        const int2 qt = s_qt[li][d];
+                        cand = cand || (t20 <= qt.x) || (t20 >= qt.y);
                         // fp32 first: when z32's fraction keeps eps + bz off both integers, floor(z32)
                         // is floor(z') and the fp64 test below could not flag (|z32 - z'| <= eps)
                         const float4 qf32 = s_qf[li][d];
-                        const float z32 = __fmaf_rn(static_cast<float>(static_cast<int>(T >> 20)), qf32.x, qf32.y);
+                        const float z32 = __fmaf_rn(static_cast<float>(t20), qf32.x, qf32.y);
                         const float fl32 = floorf(z32);
                         const float fr32 = z32 - fl32;
                         int qi;
                         if (fr32 >= qf32.z && fr32 <= qf32.w) {
                             qi = static_cast<int>(fl32);
                         } else {
+                            // T = sum_k S_k 2^(8k) in int64 (exact); y' = fl(T * 2^-38 - M)
+                            const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
+                                                (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
+                                                (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
+                                                (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
+                                                static_cast<long long>(static_cast<int>(vd[0]));
                             const double2 c0 = s_qc[li][d][0];
                             const double zf = __fma_rn(__ll2double_rn(T), c0.x, c0.y);
                             // floor(zf) through the 2^52 rounding trick (no conversion): the nearest
@@ -531,7 +547,7 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                             const double tq = __dadd_rn(zf, 4503599627370495.5);  // zf - 0.5 + 2^52
                             const double qf = __dsub_rn(tq, 4503599627370496.0);
                             const double fr = zf - qf;
-                            const double bz = c1.x;
+                            const double bz = s_qc[li][d][1].x;
                             flag = flag || (fr < bz) || (fr > 1.0 - bz);
                             qi = static_cast<int>(static_cast<uint32_t>(__double_as_longlong(tq)));
                         }

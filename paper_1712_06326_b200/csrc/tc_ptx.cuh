@@ -15,13 +15,19 @@ __device__ __forceinline__ void tc_mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void tc_mbar_expect(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// the suspend-time hint lets a waiting thread sleep in hardware until the phase completes (or the
+// limit passes) instead of re-issuing try_wait: a polling MMA lane or gather warp otherwise takes
+// issue slots from the epilogue warps (15 % of the min / max pass's executed instructions)
+#ifndef ZI_MBAR_HINT_NS
+#define ZI_MBAR_HINT_NS 20000u
+#endif
 __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "TC_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra TC_WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(ZI_MBAR_HINT_NS)
         : "memory");
 }
 __device__ __forceinline__ void tc_tma_load_2d(uint32_t dst, const CUtensorMap* tm, int x, int y, uint32_t bar) {
