@@ -373,13 +373,29 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
         // instead of four warp reductions; TMEM is read in two halves of the dims (registers)
         const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;
         constexpr int DH = (D + 1) / 2;
+        // |T| < 2^51: the start values sit outside every T and their 2^20-floors are INT_MAX / INT_MIN
         long long rmn[D], rmx[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-            rmn[d] = LLONG_MAX;
-            rmx[d] = LLONG_MIN;
+            rmn[d] = (1ll << 51) - (1ll << 20);
+            rmx[d] = -(1ll << 51);
         }
         for (uint64_t j = 0; j < nloc; ++j) {
+            if ((j & 63) == 63 && lpar < nl) {
+                // hand the warp's extremes to every lane: the 32-bit test below then passes only
+                // for rows near the extremes of all the warp's rows so far
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    const int mh = __reduce_min_sync(0xffffffffu, static_cast<int>(rmn[d] >> 32));
+                    const uint32_t ml = __reduce_min_sync(0xffffffffu, static_cast<int>(rmn[d] >> 32) == mh
+                                                                           ? static_cast<uint32_t>(rmn[d]) : 0xffffffffu);
+                    const int xh = __reduce_max_sync(0xffffffffu, static_cast<int>(rmx[d] >> 32));
+                    const uint32_t xl = __reduce_max_sync(0xffffffffu, static_cast<int>(rmx[d] >> 32) == xh
+                                                                           ? static_cast<uint32_t>(rmx[d]) : 0u);
+                    rmn[d] = (static_cast<long long>(mh) << 32) | ml;
+                    rmx[d] = (static_cast<long long>(xh) << 32) | xl;
+                }
+            }
             const int buf = static_cast<int>(j & 1);
             tc_mbar_wait(tc_smem(&s_accfull[buf]), static_cast<uint32_t>(j >> 1) & 1);
             tc_fence_after();
@@ -413,14 +429,23 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
 #pragma unroll
                     for (int dd = 0; dd < DH; ++dd) {
                         if (dd < nd) {
+                            // floor(T / 2^20) in 32-bit arithmetic; T can only replace an extreme when
+                            // its floor reaches the extreme's floor, so the 64-bit T is assembled and
+                            // compared for those rows only (few once the extremes have settled)
                             const uint32_t* vd = v + kPtDigits * dd;
-                            const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
-                                                (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
-                                                (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
-                                                (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
-                                                static_cast<long long>(static_cast<int>(vd[0]));
-                            rmn[d0 + dd] = T < rmn[d0 + dd] ? T : rmn[d0 + dd];
-                            rmx[d0 + dd] = T > rmx[d0 + dd] ? T : rmx[d0 + dd];
+                            const int s0 = static_cast<int>(vd[0]) >> 8;
+                            const int s1 = (static_cast<int>(vd[1]) + s0) >> 8;
+                            const int s2 = (static_cast<int>(vd[2]) + s1) >> 4;
+                            const int t20 = static_cast<int>(vd[4] * 4096u + vd[3] * 16u + static_cast<uint32_t>(s2));
+                            if (t20 <= static_cast<int>(rmn[d0 + dd] >> 20) || t20 >= static_cast<int>(rmx[d0 + dd] >> 20)) {
+                                const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
+                                                    (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
+                                                    (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
+                                                    (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
+                                                    static_cast<long long>(static_cast<int>(vd[0]));
+                                rmn[d0 + dd] = T < rmn[d0 + dd] ? T : rmn[d0 + dd];
+                                rmx[d0 + dd] = T > rmx[d0 + dd] ? T : rmx[d0 + dd];
+                            }
                         }
                     }
                 }
