@@ -139,18 +139,15 @@ __device__ __forceinline__ uint32_t lookback(const uint32_t* st, uint32_t tile, 
     }
 }
 
-// One stable digit pass over a tile of TILE = 256 * IT records.  Records come in groups of gn
-// (group-major; G = 1: one group); a group is tiled on its own (tpg tiles) and sorted on its own.
-// Where the records of a digit go:
-//   MODE 1 (default): offs[tile][d] = global position of the tile's first record of digit d,
-//          precomputed by k_lsd_count + the chunk scans (reduce-then-scan: no inter-tile waits);
-//   MODE 0: digit_base[g][d] + decoupled look-back over the previous tiles of the group (status).
-// All record indices are 32-bit (N < 2^30); the word pointers are offset once per tile.  A
-// thread keeps IT records in registers plus one (digit << 16 | warp rank) word per record; the
-// records are staged in shared memory in tile-sorted order, then written as runs per digit.
-// MODE 1 with DF > 0 (the sort's last pass over the 8-layout records, D = DF): the records are not
-// written back but straight into the layout indices -- dim planes (de-interleaved Morton key) and
-// the dictionary key of the payload row -- at their final positions (finalize without its read).
+// Build-time knobs of the pass (defaults = the measured best at cfg4, n = 8 x 14.9 M records of
+// 3 words; the alternatives are kept for A/B):
+//   ZI_OS_RANK  2: KC per-warp histogram chains advanced together (default); 1: one shared atomic
+//               per digit group (MIO-bound when the digit is random); 0: one chain, a shared-memory
+//               round trip per record slot
+//   ZI_OS_KC    chains of ZI_OS_RANK 2 (2; 3 and 4 need more shared memory than four CTAs per SM leave)
+//   ZI_OS_MATCH 0: __match_any_sync (default); 1: eight ballots (slower with two chains)
+//   ZI_OS_CTAS  CTAs per SM for records of <= 36 words per thread (4); ZI_OS_IT3: records per thread
+//               of 3-word records (12); ZI_OS_THREADS: CTA size (256; 512 measured 7 % slower)
 #ifndef ZI_OS_MATCH
 #define ZI_OS_MATCH 0
 #endif
@@ -188,6 +185,18 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
 #ifndef ZI_OS_RANK
 #define ZI_OS_RANK 2
 #endif
+// One stable digit pass over a tile of TILE = kSortThreads * IT records.  Records come in groups of gn
+// (group-major; G = 1: one group); a group is tiled on its own (tpg tiles) and sorted on its own.
+// Where the records of a digit go:
+//   MODE 1 (default): offs[tile][d] = global position of the tile's first record of digit d,
+//          precomputed by k_lsd_count + the chunk scans (reduce-then-scan: no inter-tile waits);
+//   MODE 0: digit_base[g][d] + decoupled look-back over the previous tiles of the group (status).
+// All record indices are 32-bit (N < 2^30); the word pointers are offset once per tile.  A
+// thread keeps IT records in registers plus one (digit << 16 | warp rank) word per record; the
+// records are staged in shared memory in tile-sorted order, then written as runs per digit.
+// MODE 1 with DF > 0 (the sort's last pass over the 8-layout records, D = DF): the records are not
+// written back but straight into the layout indices -- dim planes (de-interleaved Morton key) and
+// the dictionary key of the payload row -- at their final positions (finalize without its read).
 template <int NW, int IT, int MODE, int DF = 0>
 __global__ void __launch_bounds__(kSortThreads, (NW * IT <= 36 ? ZI_OS_CTAS : 2) * 256 / kSortThreads)
     k_onesweep(sort_words io, int dw, int ds, const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ status,
