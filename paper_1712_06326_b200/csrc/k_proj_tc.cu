@@ -73,6 +73,7 @@ struct pt_params {
     int payload_key;   // records carry the patch key as payload (the fused final sort pass), not (l << 29) | row
     const uint8_t* B;  // this group's digit matrix, pre-swizzled (Npad x Fpad)
     int Npad, l0, nl;
+    int nhalf;  // layout groups in this launch (1, or 2: both groups' accumulators from one gathered A tile)
     const double* M;          // [8][D]
     unsigned long long* amm;  // approx min / max of y', ordered u64 [8][2][D]
     double E;
@@ -252,10 +253,10 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
     {  // the digit matrix (already in the swizzled layout) and the per-(layout, dim) constants
         const uint4* src = reinterpret_cast<const uint4*>(P.B);
         uint4* dst = reinterpret_cast<uint4*>(sB);
-        const int nv = P.Npad * P.Fpad / 16;
+        const int nv = P.nhalf * P.Npad * P.Fpad / 16;
         for (int i = tid; i < nv; i += kPtThreads) dst[i] = __ldg(src + i);
         for (int i = tid; i < P.Fpad / 4; i += kPtThreads) s_wtab[i] = P.wtab[i];
-        for (int i = tid; i < nl * D; i += kPtThreads) {
+        for (int i = tid; i < P.nhalf * nl * D; i += kPtThreads) {
             const int li = i / D, d = i - li * D, l = P.l0 + li;
             s_M[li][d] = P.M[l * D + d];
             if (MODE == 1) {
@@ -316,22 +317,29 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
         if (lane == 0) {  // MMA issuer
             const uint32_t idesc = pt_idesc(P.Npad);
             const int KB = P.Fpad >> 7;
+            const int NH = P.nhalf;
+            const uint32_t bbytes = static_cast<uint32_t>(P.Npad * P.Fpad);
             for (uint64_t i = 0; i < nloc; ++i) {
-                const int buf = static_cast<int>(i & 1);
-                const uint32_t use = static_cast<uint32_t>(i >> 1);
-                tc_mbar_wait(tc_smem(&s_afull[buf]), use & 1);
-                if (i >= 2) tc_mbar_wait(tc_smem(&s_accempty[buf]), (use - 1) & 1);
-                tc_fence_after();
-                const uint32_t acc = tmem + static_cast<uint32_t>(buf * 256);
-                const uint32_t a0 = tc_smem(sA + buf * abytes), b0 = tc_smem(sB);
-                for (int kb = 0; kb < KB; ++kb) {
-                    const uint64_t da = tc_desc_k128(a0 + kb * kPtRows * 128);
-                    const uint64_t db = tc_desc_k128(b0 + kb * P.Npad * 128);
+                const int abuf = static_cast<int>(i & 1);
+                tc_mbar_wait(tc_smem(&s_afull[abuf]), static_cast<uint32_t>(i >> 1) & 1);
+                const uint32_t a0 = tc_smem(sA + abuf * abytes);
+                for (int h = 0; h < NH; ++h) {  // unit u = NH i + h: accumulator buffer u & 1
+                    const uint64_t u = i * NH + h;
+                    const int buf = static_cast<int>(u & 1);
+                    const uint32_t use = static_cast<uint32_t>(u >> 1);
+                    if (u >= 2) tc_mbar_wait(tc_smem(&s_accempty[buf]), (use - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t acc = tmem + static_cast<uint32_t>(buf * 256);
+                    const uint32_t b0 = tc_smem(sB) + static_cast<uint32_t>(h) * bbytes;
+                    for (int kb = 0; kb < KB; ++kb) {
+                        const uint64_t da = tc_desc_k128(a0 + kb * kPtRows * 128);
+                        const uint64_t db = tc_desc_k128(b0 + kb * P.Npad * 128);
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks) pt_mma(acc, da + 2 * ks, db + 2 * ks, idesc, (kb | ks) != 0 ? 1u : 0u);
+                        for (int ks = 0; ks < 4; ++ks) pt_mma(acc, da + 2 * ks, db + 2 * ks, idesc, (kb | ks) != 0 ? 1u : 0u);
+                    }
+                    if (h == NH - 1) tc_commit(tc_smem(&s_aempty[abuf]));
+                    tc_commit(tc_smem(&s_accfull[buf]));
                 }
-                tc_commit(tc_smem(&s_aempty[buf]));
-                tc_commit(tc_smem(&s_accfull[buf]));
             }
         }
     } else if (warp < kPtGatherWarps) {  // gather: two threads per patch row (the halves of its features)
@@ -368,115 +376,124 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
             if (lane == 0) tc_mbar_arrive(tc_smem(&s_afull[buf]));
         }
     } else if (MODE == 0 && pt_running<D>()) {
-        // min / max pass, one layout per warp set: every thread keeps running int64 minima and
-        // maxima of T for its layout over all its rows, so a tile costs two compares per dim
-        // instead of four warp reductions; TMEM is read in two halves of the dims (registers)
+        // min / max pass, one layout per warp set and half.  The exact int64 extremes of T live
+        // in lane slots (lane h D + d of the warp holds those of its half-h layout's dim d); every
+        // thread keeps only their floors by 2^20 as 32-bit filters.  A row can replace an extreme
+        // only if floor(T / 2^20) -- nested 32-bit shifts of the digits -- reaches the filter; then
+        // the warp assembles the 64-bit T of that dim, reduces it, the slot lane and every lane's
+        // filter take the result (floor is monotone, so the filters stay the extremes' floors and
+        // equal across the warp).  TMEM is read in two halves of the dims (registers).
         const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;
         constexpr int DH = (D + 1) / 2;
-        // |T| < 2^51: the start values sit outside every T and their 2^20-floors are INT_MAX / INT_MIN
-        long long rmn[D], rmx[D];
+        static_assert(2 * D <= 32, "lane slots: two halves of D dims");
+        int fmn[2][D], fmx[2][D];
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-            rmn[d] = (1ll << 51) - (1ll << 20);
-            rmx[d] = -(1ll << 51);
-        }
-        for (uint64_t j = 0; j < nloc; ++j) {
-            if ((j & 63) == 63 && lpar < nl) {
-                // hand the warp's extremes to every lane: the 32-bit test below then passes only
-                // for rows near the extremes of all the warp's rows so far
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int d = 0; d < D; ++d) {
-                    const int mh = __reduce_min_sync(0xffffffffu, static_cast<int>(rmn[d] >> 32));
-                    const uint32_t ml = __reduce_min_sync(0xffffffffu, static_cast<int>(rmn[d] >> 32) == mh
-                                                                           ? static_cast<uint32_t>(rmn[d]) : 0xffffffffu);
-                    const int xh = __reduce_max_sync(0xffffffffu, static_cast<int>(rmx[d] >> 32));
-                    const uint32_t xl = __reduce_max_sync(0xffffffffu, static_cast<int>(rmx[d] >> 32) == xh
-                                                                           ? static_cast<uint32_t>(rmx[d]) : 0u);
-                    rmn[d] = (static_cast<long long>(mh) << 32) | ml;
-                    rmx[d] = (static_cast<long long>(xh) << 32) | xl;
-                }
+            for (int d = 0; d < D; ++d) {
+                fmn[h][d] = INT_MAX;  // everything passes until the first reduction
+                fmx[h][d] = INT_MIN;
             }
-            const int buf = static_cast<int>(j & 1);
-            tc_mbar_wait(tc_smem(&s_accfull[buf]), static_cast<uint32_t>(j >> 1) & 1);
-            tc_fence_after();
+        // |T| < 2^51: start values outside every T
+        long long emn = 1ll << 51, emx = -(1ll << 51);
+        const int NH = P.nhalf;
+        for (uint64_t j = 0; j < nloc; ++j) {
             const uint64_t tile = blockIdx.x + j * gridDim.x;
             const bool valid = tile * kPtRows + q4 * 32 + lane < P.n;
-            const uint32_t ta = tmem + static_cast<uint32_t>(buf * 256) + (static_cast<uint32_t>(q4 * 32) << 16) +
-                                static_cast<uint32_t>(lpar * kPtDigits * D);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                constexpr int NH = kPtDigits * DH;
-                const int d0 = h * DH, nd = h ? D - DH : DH;
-                uint32_t v[NH];
-                if (lpar < nl) {
+                if (h < NH) {
+                    const uint64_t u = j * NH + h;
+                    const int buf = static_cast<int>(u & 1);
+                    tc_mbar_wait(tc_smem(&s_accfull[buf]), static_cast<uint32_t>(u >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t ta = tmem + static_cast<uint32_t>(buf * 256) + (static_cast<uint32_t>(q4 * 32) << 16) +
+                                        static_cast<uint32_t>(lpar * kPtDigits * D);
 #pragma unroll
-                    for (int c = 0; c + 4 <= NH; c += 4) {
-                        uint32_t t4[4];
-                        tc_ld_x4(ta + static_cast<uint32_t>(kPtDigits * d0 + c), t4);
+                    for (int hd = 0; hd < 2; ++hd) {
+                        constexpr int NV = kPtDigits * DH;
+                        const int d0 = hd * DH, nd = hd ? D - DH : DH;
+                        uint32_t v[NV];
+                        if (lpar < nl) {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) v[c + u] = t4[u];
-                    }
+                            for (int c = 0; c + 4 <= NV; c += 4) {
+                                uint32_t t4[4];
+                                tc_ld_x4(ta + static_cast<uint32_t>(kPtDigits * d0 + c), t4);
 #pragma unroll
-                    for (int c = NH & ~3; c < NH; ++c) tc_ld_x1(ta + static_cast<uint32_t>(kPtDigits * d0 + c), v[c]);
-                    tc_ld_wait();
-                }
-                if (h == 1) {  // this buffer is read: release it to the MMA warp
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
-                }
-                if (lpar < nl && valid) {
+                                for (int q = 0; q < 4; ++q) v[c + q] = t4[q];
+                            }
 #pragma unroll
-                    for (int dd = 0; dd < DH; ++dd) {
-                        if (dd < nd) {
-                            // floor(T / 2^20) in 32-bit arithmetic; T can only replace an extreme when
-                            // its floor reaches the extreme's floor, so the 64-bit T is assembled and
-                            // compared for those rows only (few once the extremes have settled)
-                            const uint32_t* vd = v + kPtDigits * dd;
-                            const int s0 = static_cast<int>(vd[0]) >> 8;
-                            const int s1 = (static_cast<int>(vd[1]) + s0) >> 8;
-                            const int s2 = (static_cast<int>(vd[2]) + s1) >> 4;
-                            const int t20 = static_cast<int>(vd[4] * 4096u + vd[3] * 16u + static_cast<uint32_t>(s2));
-                            if (t20 <= static_cast<int>(rmn[d0 + dd] >> 20) || t20 >= static_cast<int>(rmx[d0 + dd] >> 20)) {
-                                const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
-                                                    (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
-                                                    (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
-                                                    (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
-                                                    static_cast<long long>(static_cast<int>(vd[0]));
-                                rmn[d0 + dd] = T < rmn[d0 + dd] ? T : rmn[d0 + dd];
-                                rmx[d0 + dd] = T > rmx[d0 + dd] ? T : rmx[d0 + dd];
+                            for (int c = NV & ~3; c < NV; ++c) tc_ld_x1(ta + static_cast<uint32_t>(kPtDigits * d0 + c), v[c]);
+                            tc_ld_wait();
+                        }
+                        if (hd == 1) {  // this buffer is read: release it to the MMA warp
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
+                        }
+                        if (lpar < nl) {
+                            uint32_t cm = 0;  // dims of this half whose filter the row reaches
+#pragma unroll
+                            for (int dd = 0; dd < DH; ++dd) {
+                                if (dd < nd) {
+                                    const uint32_t* vd = v + kPtDigits * dd;
+                                    const int s0 = static_cast<int>(vd[0]) >> 8;
+                                    const int s1 = (static_cast<int>(vd[1]) + s0) >> 8;
+                                    const int s2 = (static_cast<int>(vd[2]) + s1) >> 4;
+                                    const int t20 = static_cast<int>(vd[4] * 4096u + vd[3] * 16u + static_cast<uint32_t>(s2));
+                                    if (t20 <= fmn[h][d0 + dd] || t20 >= fmx[h][d0 + dd]) cm |= 1u << dd;
+                                }
+                            }
+                            const uint32_t any = __reduce_or_sync(0xffffffffu, valid ? cm : 0u);
+                            if (any) {
+#pragma unroll
+                                for (int dd = 0; dd < DH; ++dd) {
+                                    if (dd < nd && ((any >> dd) & 1u)) {
+                                        const uint32_t* vd = v + kPtDigits * dd;
+                                        const long long T = (static_cast<long long>(static_cast<int>(vd[4])) << 32) +
+                                                            (static_cast<long long>(static_cast<int>(vd[3])) << 24) +
+                                                            (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
+                                                            (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
+                                                            static_cast<long long>(static_cast<int>(vd[0]));
+                                        const int th = static_cast<int>(T >> 32);
+                                        const uint32_t tl = static_cast<uint32_t>(T);
+                                        const int mh = __reduce_min_sync(0xffffffffu, valid ? th : 0x7fffffff);
+                                        const uint32_t ml = __reduce_min_sync(0xffffffffu, (valid && th == mh) ? tl : 0xffffffffu);
+                                        const int xh = __reduce_max_sync(0xffffffffu, valid ? th : static_cast<int>(0x80000000));
+                                        const uint32_t xl = __reduce_max_sync(0xffffffffu, (valid && th == xh) ? tl : 0u);
+                                        const long long wmn = (static_cast<long long>(mh) << 32) | ml;
+                                        const long long wmx = (static_cast<long long>(xh) << 32) | xl;
+                                        if (lane == h * D + d0 + dd) {
+                                            emn = wmn < emn ? wmn : emn;
+                                            emx = wmx > emx ? wmx : emx;
+                                        }
+                                        const int fn = static_cast<int>(wmn >> 20), fx = static_cast<int>(wmx >> 20);
+                                        fmn[h][d0 + dd] = fn < fmn[h][d0 + dd] ? fn : fmn[h][d0 + dd];
+                                        fmx[h][d0 + dd] = fx > fmx[h][d0 + dd] ? fx : fmx[h][d0 + dd];
+                                    }
+                                }
                             }
                         }
                     }
                 }
             }
         }
-        if (lpar < nl) {  // warp reductions, then one ordered atomic per (layout, dim) and warp
-            const int l = P.l0 + lpar;
-#pragma unroll
-            for (int d = 0; d < D; ++d) {
-                const int mh = __reduce_min_sync(0xffffffffu, static_cast<int>(rmn[d] >> 32));
-                const uint32_t ml = __reduce_min_sync(0xffffffffu, static_cast<int>(rmn[d] >> 32) == mh
-                                                                       ? static_cast<uint32_t>(rmn[d]) : 0xffffffffu);
-                const int xh = __reduce_max_sync(0xffffffffu, static_cast<int>(rmx[d] >> 32));
-                const uint32_t xl = __reduce_max_sync(0xffffffffu, static_cast<int>(rmx[d] >> 32) == xh
-                                                                       ? static_cast<uint32_t>(rmx[d]) : 0u);
-                const long long wmn = (static_cast<long long>(mh) << 32) | ml;
-                const long long wmx = (static_cast<long long>(xh) << 32) | xl;
-                if (lane == 0 && wmn <= wmx) {  // the warp saw a valid row
-                    const double M = s_M[lpar][d];
-                    atomicMin(P.amm + static_cast<size_t>(l) * 2 * D + d,
-                              double_to_ordered(__dsub_rn(static_cast<double>(wmn) * kPtUnit, M)));
-                    atomicMax(P.amm + static_cast<size_t>(l) * 2 * D + D + d,
-                              double_to_ordered(__dsub_rn(static_cast<double>(wmx) * kPtUnit, M)));
-                }
-            }
+        if (lpar < nl && lane < NH * D && emn <= emx) {  // the slot saw a valid row: one ordered atomic each
+            const int h = lane / D, d = lane - h * D;
+            const int li = h * nl + lpar, l = P.l0 + li;
+            const double M = s_M[li][d];
+            atomicMin(P.amm + static_cast<size_t>(l) * 2 * D + d, double_to_ordered(__dsub_rn(static_cast<double>(emn) * kPtUnit, M)));
+            atomicMax(P.amm + static_cast<size_t>(l) * 2 * D + D + d,
+                      double_to_ordered(__dsub_rn(static_cast<double>(emx) * kPtUnit, M)));
         }
     } else {  // epilogue: TMEM lane quarter ew & 3, layouts of parity ew >> 2, one patch row per thread
         const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;  // lpar in [0, kPtEpiSets)
-        for (uint64_t j = 0; j < nloc; ++j) {
-            const int buf = static_cast<int>(j & 1);
-            tc_mbar_wait(tc_smem(&s_accfull[buf]), static_cast<uint32_t>(j >> 1) & 1);
+        const uint64_t NH = static_cast<uint64_t>(P.nhalf);
+        for (uint64_t u = 0; u < nloc * NH; ++u) {  // unit u = NH j + h: tile j, layout half h
+            const uint64_t j = NH == 2 ? u >> 1 : u;
+            const int h = NH == 2 ? static_cast<int>(u & 1) : 0, cb = h * nl;  // cb: first constant slot of the half
+            const int buf = static_cast<int>(u & 1);
+            tc_mbar_wait(tc_smem(&s_accfull[buf]), static_cast<uint32_t>(u >> 1) & 1);
             tc_fence_after();
             const uint64_t tile = blockIdx.x + j * gridDim.x;
             const uint64_t row = tile * kPtRows + q4 * 32 + lane;
@@ -546,11 +563,11 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                         const int t20 = static_cast<int>(vd[4] * 4096u + vd[3] * 16u + static_cast<uint32_t>(s2));
                         // degenerate ranges (amax - amin <= 4E) carry bz = 1 and thresholds INT_MAX:
                         // every row is flagged and a lo / hi candidate, with no branch here
-                        const int2 qt = s_qt[li][d];
+                        const int2 qt = s_qt[cb + li][d];
                         cand = cand || (t20 <= qt.x) || (t20 >= qt.y);
                         // fp32 first: when z32's fraction keeps eps + bz off both integers, floor(z32)
                         // is floor(z') and the fp64 test below could not flag (|z32 - z'| <= eps)
-                        const float4 qf32 = s_qf[li][d];
+                        const float4 qf32 = s_qf[cb + li][d];
                         const float z32 = __fmaf_rn(static_cast<float>(t20), qf32.x, qf32.y);
                         const float fl32 = floorf(z32);
                         const float fr32 = z32 - fl32;
@@ -564,7 +581,7 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                                                 (static_cast<long long>(static_cast<int>(vd[2])) << 16) +
                                                 (static_cast<long long>(static_cast<int>(vd[1])) << 8) +
                                                 static_cast<long long>(static_cast<int>(vd[0]));
-                            const double2 c0 = s_qc[li][d][0];
+                            const double2 c0 = s_qc[cb + li][d][0];
                             const double zf = __fma_rn(__ll2double_rn(T), c0.x, c0.y);
                             // floor(zf) through the 2^52 rounding trick (no conversion): the nearest
                             // integer to zf - 1/2; a tie only happens at an integer zf, which the
@@ -572,7 +589,7 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                             const double tq = __dadd_rn(zf, 4503599627370495.5);  // zf - 0.5 + 2^52
                             const double qf = __dsub_rn(tq, 4503599627370496.0);
                             const double fr = zf - qf;
-                            const double bz = s_qc[li][d][1].x;
+                            const double bz = s_qc[cb + li][d][1].x;
                             flag = flag || (fr < bz) || (fr > 1.0 - bz);
                             qi = static_cast<int>(static_cast<uint32_t>(__double_as_longlong(tq)));
                         }
@@ -604,7 +621,7 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                     kw[1] = (hi & 0xF0F0F0F0u) | ((lo >> 4) & 0x0F0F0F0Fu);
                 }
                 if (MODE == 1) {
-                    const uint32_t l = static_cast<uint32_t>(P.l0 + li);
+                    const uint32_t l = static_cast<uint32_t>(P.l0 + cb + li);
                     if (valid) {
                         const uint64_t e = static_cast<uint64_t>(l) * P.n + row;
 #pragma unroll
@@ -1029,6 +1046,7 @@ struct pt_plan {
     bool ok = false;
     uint8_t* s = nullptr;  // the scratch the offsets below point into
     int D = 0, ng = 0, nlmax = 0, goff[8] = {}, gnpad[8] = {};
+    bool fuse = false;  // both layout groups in one launch (two accumulator halves per gathered tile)
     size_t smem = 0, btot = 0, o_B = 0, o_M = 0, o_amm = 0, o_cnt = 0, o_list = 0;
     pt_params P{};
 };
@@ -1056,6 +1074,15 @@ static pt_plan pt_make_plan(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, u
     }
     pl.smem = 2 * static_cast<size_t>(kPtRows) * Fpad + static_cast<size_t>(kPtMaxN) * Fpad + 1024;
     if (pl.smem > 200 * 1024) return pl;
+    {
+        // two equal groups of four layouts whose min / max pass keeps lane-slot extremes: one launch
+        // gathers every A tile once and fills both groups' accumulators from it
+        static const bool nofuse_env = std::getenv("ZI_PROJ_NOFUSE") != nullptr;
+        const size_t fsmem = 2 * static_cast<size_t>(kPtRows) * Fpad + 2 * static_cast<size_t>(pl.gnpad[0]) * Fpad + 1024;
+        pl.fuse = !nofuse_env && pl.ng == 2 && pl.nlmax == 4 && pl.gnpad[0] == pl.gnpad[1] && D >= 7 && D <= 10 &&
+                  fsmem <= 200 * 1024;
+        if (pl.fuse) pl.smem = std::max(pl.smem, fsmem);
+    }
     // scratch: [goff/gnpad ints][B bytes][M doubles][amm][count][list]
     pl.o_B = 256;
     pl.o_M = (pl.o_B + pl.btot + 255) & ~size_t(255);
@@ -1097,6 +1124,7 @@ static void pt_launch_pass(zi_ctx* ctx, pt_plan& pl, int mode) {
         P.Npad = pl.gnpad[g];
         P.l0 = g * pl.nlmax;
         P.nl = std::min(pl.nlmax, 8 - g * pl.nlmax);
+        P.nhalf = pl.fuse ? 2 : 1;
         switch (pl.D) {
 #define ZI_PT_CASE(DD) \
     case DD: launch_pt<DD>(ctx, P, mode, pl.smem); break;
@@ -1106,6 +1134,7 @@ static void pt_launch_pass(zi_ctx* ctx, pt_plan& pl, int mode) {
 #undef ZI_PT_CASE
             default: throw error(ZI_E_INVALID, "projection: dims above 16");
         }
+        if (pl.fuse) break;  // the launch covered both groups
     }
 }
 

@@ -826,6 +826,26 @@ np.savez(sys.argv[3], **out)
 """
 
 
+@pytest.mark.parametrize("D", [7, 8, 9, 10])
+def test_projection_two_half_launch_vs_oracle(zb, D):
+    """D = 7..10: both groups of four layouts in one projection launch (every A tile gathered once,
+    two accumulator halves; the min / max pass keeps lane-slot extremes behind 32-bit filters) --
+    all 8 indices and quantiser ranges byte-equal to the oracle fed the build's PCA model, on an
+    image whose last tile is partial and whose rows break at holes."""
+    from tests.helpers import pca_of
+    img, kn = workloads.small_image(150, 131, 1, seed=70 + D, hole_frac=0.08)
+    mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=9, dims=D))
+    assert mi.dims == D and mi.n % 128 != 0
+    pm, pc = pca_of(mi)
+    om = oracle.MultiIndex(img, kn, 9, 0.6, D, pca_mean=pm, pca_comp=pc)
+    for l in range(8):
+        c, k = mi.index_arrays(l)
+        ref = om.index(l)
+        lay = mi.layout(l)
+        assert np.array_equal(lay["lo"], ref.lo) and np.array_equal(lay["hi"], ref.hi), (D, l)
+        assert np.array_equal(c, ref.coords) and np.array_equal(k, ref.keys), (D, l)
+
+
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
 def test_projection_tc_equals_fp64_path(zb, cfg, tmp_path):
     """The int8 tensor-core filter + fix-up writes the same index bytes and quantiser ranges as the
