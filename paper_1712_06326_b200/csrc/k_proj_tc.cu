@@ -32,6 +32,12 @@
 
 namespace zi {
 
+#ifndef ZI_PT_G8
+#define ZI_PT_G8 0
+#endif
+#ifndef ZI_PT_ONE_READ
+#define ZI_PT_ONE_READ 0
+#endif
 constexpr int kPtRows = 128;
 // epilogue warps 4 .. 4 + 4S - 1: TMEM lane quarter (w & 3), layouts li = (w >> 2) mod S.  S = 4 sets
 // for D <= 10 (a group's layouts spread one per set); S = 3 above, where the larger per-layout
@@ -45,10 +51,11 @@ __host__ __device__ constexpr bool pt_running() {
 
 template <int D, int MODE>
 struct pt_shape {
-    // gather warps 0 .. G-1: G = 8 (two threads per patch row, the halves of its features) for the
-    // min / max pass at D <= 8, whose light epilogue leaves the gather as the limit; G = 4 (one
-    // thread per row) otherwise (the quantise pass measured slower with 8: 2.49 -> 2.61 ms at cfg4)
-    static constexpr int kGatherWarps = (D <= 8 && MODE == 0) ? 8 : 4;
+    // gather warps 0 .. G-1: one thread per patch row (G = 4).  ZI_PT_G8 = 1 (A/B): two threads per
+    // row for the min / max pass at D <= 8 -- the better shape while that pass ran once per layout
+    // group and was bound by its gather (1.80 -> 1.55 ms at cfg4); with both groups fed from one
+    // gathered tile the epilogue is the limit and the four extra warps cost registers (1.13 vs 1.02 ms)
+    static constexpr int kGatherWarps = (D <= 8 && MODE == 0 && ZI_PT_G8) ? 8 : 4;
     static constexpr int kEpiSets = D <= 10 ? 4 : 3;
     static constexpr int kEpiWarps = 4 * kEpiSets;
     static constexpr int kMmaWarp = kGatherWarps + kEpiWarps;
@@ -384,7 +391,7 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
         // filter take the result (floor is monotone, so the filters stay the extremes' floors and
         // equal across the warp).  TMEM is read in two halves of the dims (registers).
         const int ew = warp - kPtGatherWarps, q4 = ew & 3, lpar = ew >> 2;
-        constexpr int DH = (D + 1) / 2;
+        constexpr int DH = ZI_PT_ONE_READ ? D : (D + 1) / 2, NHD = ZI_PT_ONE_READ ? 1 : 2;
         static_assert(2 * D <= 32, "lane slots: two halves of D dims");
         int fmn[2][D], fmx[2][D];
 #pragma unroll
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                     const uint32_t ta = tmem + static_cast<uint32_t>(buf * 256) + (static_cast<uint32_t>(q4 * 32) << 16) +
                                         static_cast<uint32_t>(lpar * kPtDigits * D);
 #pragma unroll
-                    for (int hd = 0; hd < 2; ++hd) {
+                    for (int hd = 0; hd < NHD; ++hd) {
                         constexpr int NV = kPtDigits * DH;
                         const int d0 = hd * DH, nd = hd ? D - DH : DH;
                         uint32_t v[NV];
@@ -426,7 +433,7 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                             for (int c = NV & ~3; c < NV; ++c) tc_ld_x1(ta + static_cast<uint32_t>(kPtDigits * d0 + c), v[c]);
                             tc_ld_wait();
                         }
-                        if (hd == 1) {  // this buffer is read: release it to the MMA warp
+                        if (hd == NHD - 1) {  // this buffer is read: release it to the MMA warp
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
