@@ -450,34 +450,74 @@ __global__ void __launch_bounds__(256) k_index_bbox(const __grid_constant__ bbox
                                                     int nidx) {
     const int lane = threadIdx.x & 31;
     const uint64_t wid = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (wid >= nblk * static_cast<uint64_t>(nidx)) return;
-    const int l = static_cast<int>(wid / nblk);
-    const uint64_t blk = wid - static_cast<uint64_t>(l) * nblk;
-    uint32_t v[P][8];
+    // a warp takes kBB consecutive blocks of one layout; full blocks of 16-byte-aligned planes are
+    // read as two 16-byte vectors per lane and plane, all of the warp's loads in flight together
+    constexpr int kBB = P <= 2 ? 4 : 2;
+    const uint64_t wpl = (nblk + kBB - 1) / kBB;  // warps per layout
+    if (wid >= wpl * static_cast<uint64_t>(nidx)) return;
+    const int l = static_cast<int>(wid / wpl);
+    const uint64_t blk0 = (wid - static_cast<uint64_t>(l) * wpl) * kBB;
+    const uint32_t* pl = J.planes[l];
+    const bool vec = (n & 3u) == 0 && (reinterpret_cast<uintptr_t>(pl) & 15u) == 0 && (blk0 + kBB) * 256 <= n;
+    if (vec) {
+        uint4 v[kBB][P][2];
 #pragma unroll
-    for (int p = 0; p < P; ++p)
+        for (int b = 0; b < kBB; ++b)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const uint64_t i = blk * 256 + e * 32 + lane;
-            v[p][e] = i < n ? __ldg(J.planes[l] + static_cast<size_t>(p) * n + i) : 0u;
-        }
+            for (int p = 0; p < P; ++p)
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-        uint32_t mn = 0xffffffffu, mx = 0u;
+                for (int e = 0; e < 2; ++e)
+                    v[b][p][e] = __ldg(reinterpret_cast<const uint4*>(pl + static_cast<size_t>(p) * n + (blk0 + b) * 256 + e * 128) + lane);
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if (blk * 256 + e * 32 + lane < n) {
-                mn = __vminu4(mn, v[p][e]);
-                mx = __vmaxu4(mx, v[p][e]);
+        for (int b = 0; b < kBB; ++b)
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const uint4 x = v[b][p][e];
+                    mn = __vminu4(__vminu4(mn, __vminu4(x.x, x.y)), __vminu4(x.z, x.w));
+                    mx = __vmaxu4(__vmaxu4(mx, __vmaxu4(x.x, x.y)), __vmaxu4(x.z, x.w));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mn = __vminu4(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    mx = __vmaxu4(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
+                if (lane == 0) {
+                    J.bmin[l][static_cast<size_t>(p) * nblk + blk0 + b] = mn;
+                    J.bmax[l][static_cast<size_t>(p) * nblk + blk0 + b] = mx;
+                }
+            }
+        return;
+    }
+    for (uint64_t blk = blk0; blk < blk0 + kBB && blk < nblk; ++blk) {
+        uint32_t v[P][8];
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint64_t i = blk * 256 + e * 32 + lane;
+                v[p][e] = i < n ? __ldg(pl + static_cast<size_t>(p) * n + i) : 0u;
             }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mn = __vminu4(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = __vmaxu4(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        }
-        if (lane == 0) {
-            J.bmin[l][static_cast<size_t>(p) * nblk + blk] = mn;
-            J.bmax[l][static_cast<size_t>(p) * nblk + blk] = mx;
+        for (int p = 0; p < P; ++p) {
+            uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (blk * 256 + e * 32 + lane < n) {
+                    mn = __vminu4(mn, v[p][e]);
+                    mx = __vmaxu4(mx, v[p][e]);
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mn = __vminu4(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = __vmaxu4(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            if (lane == 0) {
+                J.bmin[l][static_cast<size_t>(p) * nblk + blk] = mn;
+                J.bmax[l][static_cast<size_t>(p) * nblk + blk] = mx;
+            }
         }
     }
 }
@@ -1451,7 +1491,8 @@ void finalize_index_bboxes(zi_ctx* ctx, zi_index* const* idx, int nidx) {
         J.bmax[l] = idx[l]->bbox_max.p;
     }
     const uint64_t nblk = idx[0]->nblk;
-    const unsigned grid = static_cast<unsigned>((nblk * nidx + 7) / 8);
+    const uint64_t kbb = idx[0]->planes_n <= 2 ? 4 : 2;  // blocks per warp (k_index_bbox)
+    const unsigned grid = static_cast<unsigned>((((nblk + kbb - 1) / kbb) * nidx + 7) / 8);
     switch (idx[0]->planes_n) {
 #define ZI_BBOX_CASE(PP)                                                                                        \
     case PP:                                                                                                    \
