@@ -698,7 +698,10 @@ __device__ __forceinline__ uint64_t tc_desc_mn128(uint32_t saddr) {  // MN-major
     return d;
 }
 
-constexpr int kGmGroups = 2;                         // gather groups (tiles i, i + 1 in flight together)
+#ifndef ZI_GM_GROUPS
+#define ZI_GM_GROUPS 2
+#endif
+constexpr int kGmGroups = ZI_GM_GROUPS;                         // gather groups (tiles i, i + 1 in flight together)
 constexpr int kGmThreads = (8 * kGmGroups + 1) * 32;  // 8 gather warps per group + the MMA warp
 
 template <int KT>
