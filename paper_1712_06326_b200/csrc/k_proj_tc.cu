@@ -35,6 +35,9 @@ namespace zi {
 #ifndef ZI_PT_G8
 #define ZI_PT_G8 0
 #endif
+#ifndef ZI_PT_SPLIT_LD
+#define ZI_PT_SPLIT_LD 1
+#endif
 #ifndef ZI_PT_ONE_READ
 #define ZI_PT_ONE_READ 0
 #endif
@@ -515,17 +518,34 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                 constexpr int NC = kPtDigits * D;
                 uint32_t v[NC];
                 const uint32_t ta = tbase + static_cast<uint32_t>(li * NC);
+                // MODE 1 reads the columns in two parts: the second part's loads are in flight while
+                // the dims of the first are quantised (DB = the first dim that needs the second part)
+                constexpr int C1 = (MODE == 1 && ZI_PT_SPLIT_LD && D >= 4) ? ((NC / 2) & ~3) : NC;
+                constexpr int DB = C1 / kPtDigits;
 #pragma unroll
-                for (int c = 0; c + 4 <= NC; c += 4) {
+                for (int c = 0; c + 4 <= C1; c += 4) {
                     uint32_t t4[4];
                     tc_ld_x4(ta + c, t4);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) v[c + u] = t4[u];
                 }
+                if constexpr (C1 == NC) {
 #pragma unroll
-                for (int c = NC & ~3; c < NC; ++c) tc_ld_x1(ta + c, v[c]);
+                    for (int c = NC & ~3; c < NC; ++c) tc_ld_x1(ta + c, v[c]);
+                }
                 tc_ld_wait();
-                if (li + kPtEpiSets >= nl) {  // TMEM of this buffer fully read: release it to the MMA warp early
+                if constexpr (C1 < NC) {
+#pragma unroll
+                    for (int c = C1; c + 4 <= NC; c += 4) {
+                        uint32_t t4[4];
+                        tc_ld_x4(ta + c, t4);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) v[c + u] = t4[u];
+                    }
+#pragma unroll
+                    for (int c = C1 + ((NC - C1) & ~3); c < NC; ++c) tc_ld_x1(ta + c, v[c]);
+                }
+                if (C1 == NC && li + kPtEpiSets >= nl) {  // TMEM of this buffer fully read: release it to the MMA warp early
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
@@ -536,6 +556,18 @@ __global__ void __launch_bounds__(pt_shape<D, MODE>::kThreads, 1) k_proj_tc(cons
                 bool flag = false, cand = false;
 #pragma unroll
                 for (int d = 0; d < D; ++d) {
+                    if constexpr (C1 < NC) {
+                        if (d == DB) {  // the second part has landed; its registers are read only after this point
+                            tc_ld_wait();
+#pragma unroll
+                            for (int c = C1; c < NC; ++c) asm volatile("" : "+r"(v[c]));
+                            if (li + kPtEpiSets >= nl) {  // TMEM of this buffer fully read: release it to the MMA warp
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) tc_mbar_arrive(tc_smem(&s_accempty[buf]));
+                            }
+                        }
+                    }
                     // T = sum_k S_k 2^(8k) in int64 (exact, |T| < 2^51); the fp64 conversions run at a
                     // fraction of the integer rate, so the min / max pass stays integer and the
                     // quantise pass converts once: y' = fl(T * 2^-38 - M) (T exact in a double)
