@@ -256,14 +256,24 @@ def pt_groups(D: int):
     return out
 
 
+def pt_launches(D: int) -> int:
+    """Projection launches per pass: one per layout group, or a single launch when the two groups
+    of four layouts of D = 7..10 are fed from one gathered tile (k_proj_tc.cu, pt_plan::fuse)."""
+    gs = pt_groups(D)
+    if len(gs) == 2 and gs[0] == gs[1] and gs[0][0] == 4 and 7 <= D <= 10 and not os.environ.get("ZI_PROJ_NOFUSE"):
+        return 1
+    return len(gs)
+
+
 def algorithmic_bytes(kernel: str, n: int, D: int, mc: int, F: int = 0) -> float | None:
     """Algorithmic HBM bytes per launch; gathered pixels are L1/L2 served.
     The radix passes and the window sort run once over the records of all 8 layouts (N = 8n);
-    the tensor-core projection launches once per (pass, layout group): keys in, and in the
-    quantise pass the Morton records of its layouts out (averaged over the groups)."""
+    the tensor-core projection launches once per (pass, layout group) -- once per pass when the
+    groups share a gathered tile (pt_launches): keys in, and in the quantise pass the Morton
+    records of its layouts out (averaged over the launches)."""
     W = (D + 3) // 4
     N = 8 * n
-    g = len(pt_groups(D)) if D <= 16 else 1
+    g = pt_launches(D) if D <= 16 else 1
     return {
         "radix_onesweep": 2 * 4 * (W + 1) * N,          # legacy LSD sort: read + write of (W key words + payload)
         "segment_sort": 2 * 4 * (W + 1) * N,            # one read + one in-place write per record
@@ -284,13 +294,13 @@ def algorithmic_bytes(kernel: str, n: int, D: int, mc: int, F: int = 0) -> float
 def algorithmic_ops(kernel: str, n: int, D: int, mc: int, F: int = 0) -> float | None:
     """Tensor-core ops per launch: the fp64 projection (2 per FMA over the layout's m*C columns),
     or the int8 digit GEMM of the tensor-core projection (2 * n * Fpad * columns, averaged over
-    its layout groups)."""
+    its launches)."""
     if kernel == "project":
         return 2.0 * n * mc * D
     if kernel in ("project_tc_minmax", "project_tc_quantize") and D <= 16:
         Fpad = (F + 127) // 128 * 128
         gs = pt_groups(D)
-        return 2.0 * n * Fpad * sum(npad for _, npad in gs) / len(gs)
+        return 2.0 * n * Fpad * sum(npad for _, npad in gs) / pt_launches(D)
     return None
 
 
