@@ -35,6 +35,57 @@ __global__ void k_validflag(const uint8_t* __restrict__ colflag, int w, int K, i
     valid[static_cast<size_t>(y) * wo + x] = any ? 0 : 1;
 }
 
+// Both window flags in one pass for word-aligned rows (w % 4 == 0, K <= KMAX): a thread makes the
+// valid flags x .. x+3 of R consecutive rows from the (R + K - 1) x (K + 3) mask bytes above them,
+// read once as aligned words: f = byte-wise (known == 0); the column flags of an output row are
+// the OR of its K rows of f, the valid flag of byte j the OR of the column bytes j .. j+K-1 (funnel
+// shifts of the flag words).  No colflag array, word loads, every mask word loaded once per thread.
+template <int KMAX, int R>
+__global__ void __launch_bounds__(256) k_validfused(const uint8_t* __restrict__ known, int w, int K, int wo, int ho,
+                                                    uint8_t* __restrict__ valid) {
+    constexpr int NW = (KMAX + 6) / 4;  // words covering K + 3 bytes
+    constexpr int NR = R + KMAX - 1;
+    const int x = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    const int y0 = blockIdx.y * R;
+    if (x >= wo) return;
+    const int nw = (K + 6) >> 2;
+    uint32_t f[NR][NW];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        const bool rok = r < R + K - 1 && y0 + r < ho + K - 1;
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(known + static_cast<size_t>(y0 + r) * w + x);
+#pragma unroll
+        for (int i = 0; i < NW; ++i) f[r][i] = (rok && i < nw && x + 4 * i < w) ? __vcmpeq4(__ldg(row + i), 0u) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        if (y0 + j >= ho) break;
+        uint32_t c[NW + 1];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            uint32_t v = 0u;
+#pragma unroll
+            for (int r = 0; r < KMAX; ++r)
+                if (r < K) v |= f[j + r][i];
+            c[i] = v;
+        }
+        c[NW] = 0u;
+        uint32_t any = 0u;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (k < K) any |= (k & 3) ? __funnelshift_r(c[k >> 2], c[(k >> 2) + 1], 8 * (k & 3)) : c[k >> 2];
+        const uint32_t ok = ~any & 0x01010101u;  // __vcmpeq4 gives 0xff per equal byte
+        const size_t o = static_cast<size_t>(y0 + j) * wo + x;
+        if (x + 3 < wo && (o & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(valid + o) = ok;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (x + q < wo) valid[o + q] = static_cast<uint8_t>((ok >> (8 * q)) & 1u);
+        }
+    }
+}
+
 constexpr int kCompactThreads = 256;
 constexpr int kCompactPer = 16;
 constexpr int kCompactTile = kCompactThreads * kCompactPer;  // 4096 flags per block
@@ -129,8 +180,16 @@ uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, i
     uint8_t* colflag = base;
     uint8_t* valid = base + sz_col;
     uint32_t* counts = reinterpret_cast<uint32_t*>(base + ((sz_col + sz_valid + 15) & ~size_t(15)));
-    ZI_LAUNCH(ctx, "collect_colflag", k_colflag, dim3((w + 255) / 256, ho), 256, 0, d_known, w, h, K, colflag);
-    ZI_LAUNCH(ctx, "collect_validflag", k_validflag, dim3((wo + 255) / 256, ho), 256, 0, colflag, w, K, wo, valid);
+    if ((w & 3) == 0 && K <= 17 && (reinterpret_cast<uintptr_t>(d_known) & 3) == 0 && (reinterpret_cast<uintptr_t>(valid) & 3) == 0) {
+        const unsigned gx = static_cast<unsigned>(((wo + 3) / 4 + 255) / 256);
+        if (K <= 9)
+            ZI_LAUNCH(ctx, "collect_validflag", (k_validfused<9, 8>), dim3(gx, (ho + 7) / 8), 256, 0, d_known, w, K, wo, ho, valid);
+        else
+            ZI_LAUNCH(ctx, "collect_validflag", (k_validfused<17, 2>), dim3(gx, (ho + 1) / 2), 256, 0, d_known, w, K, wo, ho, valid);
+    } else {
+        ZI_LAUNCH(ctx, "collect_colflag", k_colflag, dim3((w + 255) / 256, ho), 256, 0, d_known, w, h, K, colflag);
+        ZI_LAUNCH(ctx, "collect_validflag", k_validflag, dim3((wo + 255) / 256, ho), 256, 0, colflag, w, K, wo, valid);
+    }
     ZI_LAUNCH(ctx, "collect_count", k_count_flags, dim3(static_cast<unsigned>(nb)), kCompactThreads, 0, valid,
               n_orig, counts);
     ZI_LAUNCH(ctx, "collect_scan", k_scan_counts, 1, 1024, 0, counts, nb);
