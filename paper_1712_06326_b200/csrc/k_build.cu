@@ -153,19 +153,40 @@ __global__ void __launch_bounds__(kCompactThreads) k_write_keys(const uint8_t* _
                                                                 uint32_t* __restrict__ keys) {
     __shared__ uint32_t s_warp[32];
     const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kCompactTile + threadIdx.x * kCompactPer;
+    static_assert(kCompactPer == 16, "one 16-byte vector of flags per thread");
     uint8_t f[kCompactPer];
     uint32_t c = 0;
-    for (int i = 0; i < kCompactPer; ++i) {
-        f[i] = (base + i < n) ? flags[base + i] : 0;
-        c += f[i];
-    }
-    uint32_t pos = offsets[blockIdx.x] + block_exclusive_scan(c, s_warp, nullptr);
-    for (int i = 0; i < kCompactPer; ++i)
-        if (f[i]) {
-            const uint64_t o = base + i;
-            const uint32_t y = static_cast<uint32_t>(o / wo), x = static_cast<uint32_t>(o % wo);
-            keys[pos++] = (y << 16) | x;
+    if (base + kCompactPer <= n && (reinterpret_cast<uintptr_t>(flags + base) & 15) == 0) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(flags + base));
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < kCompactPer; ++i) {
+            f[i] = static_cast<uint8_t>((wv[i >> 2] >> (8 * (i & 3))) & 0xffu);
+            c += f[i];
         }
+    } else {
+        for (int i = 0; i < kCompactPer; ++i) {
+            f[i] = (base + i < n) ? flags[base + i] : 0;
+            c += f[i];
+        }
+    }
+    // the block's keys are collected in shared memory and written as one contiguous run
+    __shared__ uint32_t s_keys[kCompactTile];
+    uint32_t total;
+    uint32_t pos = block_exclusive_scan(c, s_warp, &total);
+    // (row, column) of the thread's first flag by one division, then stepped
+    uint32_t y = static_cast<uint32_t>(base / wo), x = static_cast<uint32_t>(base - static_cast<uint64_t>(y) * wo);
+#pragma unroll
+    for (int i = 0; i < kCompactPer; ++i) {
+        if (f[i]) s_keys[pos++] = (y << 16) | x;
+        if (++x == static_cast<uint32_t>(wo)) {
+            x = 0;
+            ++y;
+        }
+    }
+    __syncthreads();
+    uint32_t* dst = keys + offsets[blockIdx.x];
+    for (uint32_t i = threadIdx.x; i < total; i += kCompactThreads) dst[i] = s_keys[i];
 }
 
 uint64_t collect_dictionary(zi_ctx* ctx, const uint8_t* d_known, int w, int h, int K,
