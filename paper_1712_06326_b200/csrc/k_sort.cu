@@ -570,37 +570,62 @@ __global__ void __launch_bounds__(256) k_lsd_chunk_sum(const uint32_t* __restric
     csum[static_cast<size_t>(c) * 256 + d] = s;
 }
 
-__global__ void __launch_bounds__(256) k_lsd_chunk_scan(uint32_t* __restrict__ csum, uint32_t cpg, uint32_t gn,
-                                                        uint32_t* __restrict__ gbase) {
+// one block per group, kScanParts x 256 threads: thread (part q, digit d) owns a contiguous part of
+// the group's chunks (the walk over the chunks is a chain of L2 round trips; the parts run side by
+// side): part totals -> exclusive prefix over the parts -> the running sums, in place
+constexpr int kScanParts = 4;
+__global__ void __launch_bounds__(256 * kScanParts) k_lsd_chunk_scan(uint32_t* __restrict__ csum, uint32_t cpg, uint32_t gn,
+                                                                     uint32_t* __restrict__ gbase) {
     __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_part[kScanParts][256];
     const uint32_t g = blockIdx.x;
-    const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    const int d = threadIdx.x & 255, q = threadIdx.x >> 8, lane = d & 31, warp = d >> 5;
     uint32_t* cs = csum + static_cast<size_t>(g) * cpg * 256 + d;
-    uint32_t run = 0;
-    constexpr uint32_t U = 8;  // chunk sums loaded together (the running sum waits once per batch)
-    for (uint32_t k0 = 0; k0 < cpg; k0 += U) {
+    const uint32_t plen = (cpg + kScanParts - 1) / kScanParts;
+    const uint32_t k0 = min(cpg, static_cast<uint32_t>(q) * plen), k1 = min(cpg, k0 + plen);
+    constexpr uint32_t U = 8;  // chunk sums loaded together
+    uint32_t tot = 0;
+    for (uint32_t k = k0; k < k1; k += U) {
         uint32_t v[U];
 #pragma unroll
-        for (uint32_t u = 0; u < U; ++u) v[u] = k0 + u < cpg ? cs[static_cast<size_t>(k0 + u) * 256] : 0u;
+        for (uint32_t u = 0; u < U; ++u) v[u] = k + u < k1 ? cs[static_cast<size_t>(k + u) * 256] : 0u;
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) tot += v[u];
+    }
+    s_part[q][d] = tot;
+    __syncthreads();
+    uint32_t run = 0, all = 0;
+#pragma unroll
+    for (int p = 0; p < kScanParts; ++p) {
+        const uint32_t t = s_part[p][d];
+        run += p < q ? t : 0u;
+        all += t;
+    }
+    for (uint32_t k = k0; k < k1; k += U) {
+        uint32_t v[U];
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) v[u] = k + u < k1 ? cs[static_cast<size_t>(k + u) * 256] : 0u;
 #pragma unroll
         for (uint32_t u = 0; u < U; ++u) {
-            if (k0 + u < cpg) cs[static_cast<size_t>(k0 + u) * 256] = run;
+            if (k + u < k1) cs[static_cast<size_t>(k + u) * 256] = run;
             run += v[u];
         }
     }
     // the group's digit bases: exclusive scan of the totals over the digits (added by k_lsd_offsets)
-    uint32_t x = run;
+    uint32_t x = all;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) s_w[warp] = x;
+    if (q == 0 && lane == 31) s_w[warp] = x;
     __syncthreads();
-    uint32_t wp = 0;
+    if (q == 0) {
+        uint32_t wp = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) wp += w < warp ? s_w[w] : 0u;
-    gbase[g * 256 + d] = g * gn + wp + x - run;
+        for (int w = 0; w < 8; ++w) wp += w < warp ? s_w[w] : 0u;
+        gbase[g * 256 + d] = g * gn + wp + x - all;
+    }
 }
 
 __global__ void __launch_bounds__(256) k_lsd_offsets(uint32_t* __restrict__ counts, const uint32_t* __restrict__ csum,
@@ -670,7 +695,7 @@ static void launch_pass(zi_ctx* ctx, const sort_words& io, int dw, int ds, const
     ZI_LAUNCH(ctx, "radix_count", k_lsd_count<IT>, pp.ntiles, kSortThreads, 0, io.in[dw], ds, gn, pp.tpg, pp.counts);
     const unsigned nch = pp.cpg * static_cast<unsigned>(G);
     ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_sum, nch, 256, 0, pp.counts, pp.tpg, pp.cpg, pp.csum);
-    ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_scan, static_cast<unsigned>(G), 256, 0, pp.csum, pp.cpg, gn, pp.gbase);
+    ZI_LAUNCH(ctx, "radix_scan", k_lsd_chunk_scan, static_cast<unsigned>(G), 256 * kScanParts, 0, pp.csum, pp.cpg, gn, pp.gbase);
     ZI_LAUNCH(ctx, "radix_scan", k_lsd_offsets, nch, 256, 0, pp.counts, pp.csum, pp.gbase, pp.tpg, pp.cpg);
     if (sink) {  // the last pass of the 8-layout sort: straight into the indices
         constexpr int DF = NW == 2 ? 4 : NW == 3 ? 8 : NW == 4 ? 12 : 16;
