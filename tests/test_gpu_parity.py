@@ -159,6 +159,26 @@ def test_dictionary_collect(zb, golden):
             assert np.array_equal(mi.dictionary, mi_dict), (tag, K)
 
 
+@pytest.mark.parametrize("h,w", [(45, 64), (37, 132), (64, 68), (23, 24), (41, 63), (50, 130)])
+def test_dictionary_collect_window_flag_shapes(zb, h, w):
+    """The fused window-flag kernel (word-aligned rows: 4 columns x 8 rows per thread, K <= 9, or
+    4 x 2 for K <= 17) and the two-kernel fallback (w % 4 != 0, larger K): heights that are not a
+    multiple of the rows per thread, widths whose last word is partial, holes on the borders --
+    the dictionary equals the oracle's."""
+    img, kn = workloads.small_image(h, w, 1, seed=h * 131 + w, hole_frac=0.1)
+    kn[0, :3] = 0
+    kn[-1, -2:] = 0
+    kn[h // 2, 0] = 0
+    for K in (3, 5, 7, 9, 11, 13, 17, 19):
+        if K > min(h, w):
+            continue
+        ref = oracle.collect_dictionary(kn, K)
+        if ref.size == 0:
+            continue
+        mi = zb.MultiIndex(img, kn, zb.index_config(patch_size=K, dims=2))
+        assert np.array_equal(mi.dictionary, ref), (h, w, K)
+
+
 def test_build_to_overlapped_copies_equal_build(zb, golden):
     """zi_multi_index_build_to (image upload and dictionary download on the copy stream beside the
     build) returns the dictionary and builds the same 8 indices as zi_multi_index_build."""
