@@ -232,8 +232,9 @@ void build_multi_index(zi_multi_index* mi) {
         for (int l = 0; l < 8; ++l) idx[l] = &mi->L[l].index;
         finalize_index_bboxes(ctx, idx, 8);
     } else {
-        for (int l = 0; l < 8; ++l)
-            finalize_index(ctx, sorted[0], sorted[W], N, static_cast<uint64_t>(l) * n, n, D, mi->dict.p, &mi->L[l].index);
+        zi_index* idx[8];
+        for (int l = 0; l < 8; ++l) idx[l] = &mi->L[l].index;
+        finalize_layout_indexes(ctx, sorted[0], sorted[W], N, n, D, mi->dict.p, idx, 8);
     }
     if (mi->dict_out) ZI_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
     ZI_CUDA(cudaEventRecord(mi->ev1, ctx->stream));

@@ -659,11 +659,11 @@ __global__ void __launch_bounds__(256) k_interleave(const uint8_t* __restrict__ 
 // gathers in flight together); the bbox is a warp reduction (no block barrier).
 constexpr int kFinWarps = 8;
 template <int D>
-__global__ void __launch_bounds__(kFinWarps * 32) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
-                                                           uint64_t N, uint64_t off, uint64_t n,
-                                                           const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
-                                                           uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
-                                                           uint32_t* __restrict__ bmax, uint64_t nblk) {
+__device__ __forceinline__ void finalize_block(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
+                                               uint64_t N, uint64_t off, uint64_t n,
+                                               const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
+                                               uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
+                                               uint32_t* __restrict__ bmax, uint64_t nblk) {
     constexpr int W = (D + 3) / 4, P = W, E = 8;
     const int lane = threadIdx.x & 31;
     const uint64_t blk = static_cast<uint64_t>(blockIdx.x) * kFinWarps + (threadIdx.x >> 5);
@@ -717,6 +717,31 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_finalize(const uint32_t* __r
             bmax[static_cast<size_t>(p) * nblk + blk] = mx[p];
         }
     }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFinWarps * 32) k_finalize(const uint32_t* __restrict__ keyw, const uint32_t* __restrict__ val,
+                                                           uint64_t N, uint64_t off, uint64_t n,
+                                                           const uint32_t* __restrict__ dict, uint32_t* __restrict__ planes,
+                                                           uint32_t* __restrict__ keys, uint32_t* __restrict__ bmin,
+                                                           uint32_t* __restrict__ bmax, uint64_t nblk) {
+    finalize_block<D>(keyw, val, N, off, n, dict, planes, keys, bmin, bmax, nblk);
+}
+
+// the 8 layout indices of a build in one launch (blockIdx.y = layout; layout l's records start at l n)
+struct fin_job {
+    uint32_t* planes[8];
+    uint32_t* keys[8];
+    uint32_t* bmin[8];
+    uint32_t* bmax[8];
+};
+template <int D>
+__global__ void __launch_bounds__(kFinWarps * 32) k_finalize_layouts(const uint32_t* __restrict__ keyw,
+                                                                   const uint32_t* __restrict__ val, uint64_t N, uint64_t n,
+                                                                   const uint32_t* __restrict__ dict,
+                                                                   const __grid_constant__ fin_job J, uint64_t nblk) {
+    const int l = blockIdx.y;
+    finalize_block<D>(keyw, val, N, static_cast<uint64_t>(l) * n, n, dict, J.planes[l], J.keys[l], J.bmin[l], J.bmax[l], nblk);
 }
 
 // ============================================================== host launchers
@@ -805,6 +830,29 @@ void prepare_index(zi_index* idx, uint64_t n, int D) {
     idx->keys.ensure(n ? n : 1);
     idx->bbox_min.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
     idx->bbox_max.ensure(static_cast<size_t>(idx->planes_n) * (idx->nblk ? idx->nblk : 1));
+}
+
+template <int D>
+static void launch_finalize_layouts_t(zi_ctx* ctx, const uint32_t* keyw, const uint32_t* val, uint64_t N, uint64_t n,
+                                      const uint32_t* dict, const fin_job& J, uint64_t nblk, int nidx) {
+    ZI_LAUNCH(ctx, "finalize_index", k_finalize_layouts<D>,
+              dim3(static_cast<unsigned>((nblk + kFinWarps - 1) / kFinWarps), static_cast<unsigned>(nidx)), kFinWarps * 32, 0,
+              keyw, val, N, n, dict, J, nblk);
+}
+
+// finalize of the nidx <= 8 layout indices whose sorted records sit layout-major (n each) in one launch
+void finalize_layout_indexes(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t n, int D,
+                             const uint32_t* d_dict, zi_index* const* idx, int nidx) {
+    fin_job J{};
+    for (int l = 0; l < nidx; ++l) {
+        prepare_index(idx[l], n, D);
+        J.planes[l] = idx[l]->planes.p;
+        J.keys[l] = idx[l]->keys.p;
+        J.bmin[l] = idx[l]->bbox_min.p;
+        J.bmax[l] = idx[l]->bbox_max.p;
+    }
+    if (n == 0 || nidx <= 0) return;
+    ZI_DIMS_SWITCH(D, launch_finalize_layouts_t, ctx, d_keyw, d_val, N, n, d_dict, J, idx[0]->nblk, nidx);
 }
 
 void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t off, uint64_t n,

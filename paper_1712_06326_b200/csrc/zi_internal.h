@@ -336,6 +336,8 @@ void shard_tc_quantize(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64
 void shard_tc_fixup(zi_multi_index* mi, uint32_t* keyw, uint32_t* val, uint64_t Nrec);
 
 // sorted key words + payload -> index planes, keys, bbox
+void finalize_layout_indexes(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t n, int D,
+                             const uint32_t* d_dict, zi_index* const* idx, int nidx);
 void finalize_index(zi_ctx* ctx, const uint32_t* d_keyw, const uint32_t* d_val, uint64_t N, uint64_t off,
                     uint64_t n, int D, const uint32_t* d_dict, zi_index* idx);
 
