@@ -871,7 +871,10 @@ static void launch_gram(zi_ctx* ctx, const gm_params& G, size_t smem) {
     smem_attr(ctx->device, k_gram_fused<KT>, smem);
     // one CTA per SM, more when an SM would sum more than kGmChunk tiles (65536 patches: the
     // u32 view of the s32 accumulators stays exact)
-    const uint64_t want = std::max<uint64_t>(static_cast<uint64_t>(ctx->num_sms), (G.P.ntiles + kGmChunk - 1) / kGmChunk);
+    // -- rounded up to whole waves (the 512-column TMEM allocation keeps one CTA per SM, so a grid
+    // of 1.5 waves would leave a third of the SMs idle for the second half)
+    const uint64_t sms = static_cast<uint64_t>(ctx->num_sms);
+    const uint64_t want = (std::max<uint64_t>(sms, (G.P.ntiles + kGmChunk - 1) / kGmChunk) + sms - 1) / sms * sms;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(G.P.ntiles, want));
     gm_params g = G;
     g.part = reinterpret_cast<uint32_t*>(ctx->scratch.ensure(static_cast<size_t>(grid) * G.npair * 128 * 128 * 4 + 256));
